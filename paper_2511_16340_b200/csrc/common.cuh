@@ -1,0 +1,162 @@
+// common.cuh -- shared internals of libwarmgp_b200.so (not part of the ABI).
+//
+// Device data layout:
+//   X    : row-major [cap][dpad]   fp64 (always) and fp32 (fp32 precisions), dpad = dim
+//          rounded up to 8 (one tf32 K-atom = 32 bytes), zero padded.
+//   sq   : [cap] squared row norms (fp64 and fp32), used by the norm-form distance
+//          |x|^2 + |y|^2 - 2 x.y of kernel.cpp:39-46/48-72.
+//   RHS  : row-major [n][s] in the compute type ("RHS-interleaved"): one row of X
+//          meets all s right-hand sides in one contiguous 4*s / 8*s byte span.
+//   L/M  : preconditioner factors row-major [n][kpad] fp64 (+ fp32 copy of M).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/warmgp_capi.h"
+
+namespace wgp {
+
+constexpr int kChunkRows = 512;  // fixed reduction chunk: sums are world-size independent
+
+struct Error : std::runtime_error {
+  wgp_status code;
+  int col = -1;
+  int iterations = 0;
+  Error(wgp_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_error(wgp_status code, const char* fmt, ...);
+
+#define WGP_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      ::wgp::throw_error(e_ == cudaErrorMemoryAllocation ? WGP_OOM : WGP_CUDA_ERROR,     \
+                         "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define WGP_REQUIRE(cond, ...)                                  \
+  do {                                                          \
+    if (!(cond)) ::wgp::throw_error(WGP_INVALID_ARGUMENT, __VA_ARGS__); \
+  } while (0)
+
+// Owning device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count) WGP_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void ensure(size_t count) { if (count > n) alloc(count); }
+  void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+};
+
+// Kernel-map parameters (kernel.cpp:17-21 Matern-3/2; RBF extension).
+struct KParams {
+  int kind;        // WGP_MATERN32 / WGP_RBF
+  double c1;       // Matern: sqrt(3)/l   RBF: 1/(2 l^2)
+  double s2;       // signal^2
+  double noise2;   // sigma_n^2 (diagonal of H only)
+};
+
+struct Comm;  // NCCL plumbing (dist.cpp)
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  Comm* comm = nullptr;
+};
+
+struct Op {
+  Ctx* ctx = nullptr;
+  int kind = WGP_MATERN32;
+  double lengthscale = 1, signal_scale = 1, noise_scale = 1e-3;
+  int precision = WGP_F64;
+  int dim = 0, dpad = 0;
+  int64_t n = 0, cap = 0;
+  DBuf<double> X64, sq64;
+  DBuf<float> X32, sq32;
+  DBuf<unsigned char> scratch[3];  // host-boundary staging, reused across calls
+  KParams kp() const {
+    KParams p;
+    p.kind = kind;
+    p.c1 = kind == WGP_MATERN32 ? 1.7320508075688772935 / lengthscale
+                                : 0.5 / (lengthscale * lengthscale);
+    p.s2 = signal_scale * signal_scale;
+    p.noise2 = noise_scale * noise_scale;
+    return p;
+  }
+  bool f64() const { return precision == WGP_F64; }
+  size_t esize() const { return f64() ? sizeof(double) : sizeof(float); }
+  void local_rows(int64_t* r0, int64_t* r1) const {
+    wgp_shard_range(n, ctx->world, ctx->rank, r0, r1);
+  }
+};
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ------------------------------------------------------------------ launchers
+// kmatvec.cu: Y[r, :] = sum_j k(xr_r, xc_j) V[j, :] (+ noise2 V[j,:] when the global row
+// index row0 + r == j in gram mode), or Y = B - (...) in residual mode.
+template <typename T>
+void launch_kmatvec(const Op& op, const T* Xr, const T* sqr, int64_t nrows, int64_t row0,
+                    const T* Xc, const T* sqc, int64_t ncols, const T* V, int s, const T* B,
+                    T* Y, bool gram, cudaStream_t st);
+
+// vecops.cu
+void launch_colmajor_to_rows(const double* src, int64_t ld, int64_t n, int s, void* dst,
+                             bool f64, cudaStream_t st);
+void launch_rows_to_colmajor(const void* src, int64_t n, int s, double* dst, int64_t ld, bool f64,
+                             cudaStream_t st);
+template <typename T>
+void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t n, int s,
+                    double* part, cudaStream_t st);  // part: [nchunks][nq][s]
+template <typename T>
+void launch_axpy_cols(T* Y, const T* X, const double* alpha, int64_t n, int s, cudaStream_t st);
+template <typename T>
+void launch_xpby_cols(T* P, const T* Z, const double* beta, const int* active, int64_t n, int s,
+                      cudaStream_t st);
+template <typename T>
+void launch_fill(T* p, T v, size_t count, cudaStream_t st);
+
+// precond.cu
+struct PrecondDev {
+  int64_t n = 0, k = 0, kpad = 0;
+  double shift = 1.0;
+  DBuf<double> L;    // [n][kpad] row-major (pivoted Cholesky factor)
+  DBuf<double> M64;  // [n][kpad]  M = L C^{-T}, C = chol(shift I + L^T L): M M^T = L cap^{-1} L^T
+  DBuf<float> M32;
+};
+void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStream_t st);
+void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd, cudaStream_t st);
+template <typename T>
+void precond_apply(const PrecondDev& pd, const T* R, T* Z, int s, double* work_t, double* work_part,
+                   cudaStream_t st);
+
+// rff.cu
+template <typename T>
+void launch_rff_eval(const T* X, int dpad, int dim, int64_t m, const double* Om, const double* ph,
+                     const double* amp, int F, int S, double coeff, T* out, cudaStream_t st);
+
+}  // namespace wgp

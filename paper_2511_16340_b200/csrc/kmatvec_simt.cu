@@ -1,0 +1,197 @@
+// kmatvec_simt.cu -- CUDA-core fused kernel-matvec (fp64 path and fp32 validation path).
+//
+// Replaces gram_matrix (kernel.cpp:48-72) + the dense GEMV H*p (solvers.cpp:162) and
+// b - H*v (solvers.cpp:150,171,...) with one tiled pass that never materialises K:
+//   Y[r, c] = sum_j k(x_r, x_j) V[j, c]  (+ sigma_n^2 V[r, c] on the gram diagonal)
+// Per 64x64 (row, col) tile: phase 1 evaluates the 4096 kernel entries into shared
+// memory (the diagonal is set exactly to s^2 + sigma_n^2 like kernel.cpp:70), phase 2
+// multiplies the tile into register accumulators for up to 64 RHS.
+//
+// Distances here use explicit differences sum_k (x_rk - x_jk)^2, which equals the
+// reference's norm form to rounding and has no cancellation; the tensor-core path
+// (kmatvec_tc.cu) uses the norm form as a contraction.
+#include "common.cuh"
+
+namespace wgp {
+namespace {
+
+constexpr int BM = 64, BN = 64, NT = 256;
+
+template <typename T>
+__device__ __forceinline__ T kmap(T d2, const KParams& p);
+
+template <>
+__device__ __forceinline__ double kmap<double>(double d2, const KParams& p) {
+  d2 = d2 > 0.0 ? d2 : 0.0;
+  if (p.kind == WGP_RBF) return p.s2 * exp(-p.c1 * d2);
+  const double z = p.c1 * sqrt(d2);
+  return p.s2 * (1.0 + z) * exp(-z);
+}
+
+template <>
+__device__ __forceinline__ float kmap<float>(float d2, const KParams& p) {
+  d2 = fmaxf(d2, 0.0f);
+  const float s2 = (float)p.s2, c1 = (float)p.c1;
+  if (p.kind == WGP_RBF) return s2 * exp2f(-c1 * 1.4426950408889634f * d2);
+  const float z = c1 * sqrtf(d2);
+  return s2 * (1.0f + z) * exp2f(-1.4426950408889634f * z);
+}
+
+// BS: RHS columns per block.  Phase-2 thread layout: 16 row groups x (BS/CN) column
+// groups x JG interleaved j-groups, 4 rows x CN columns per thread.
+template <typename T, int BS>
+__global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
+    const T* __restrict__ Xr, int64_t nrows, int64_t row0, const T* __restrict__ Xc,
+    int64_t ncols, int dpad, int dim, const T* __restrict__ V, int s, const T* __restrict__ B,
+    T* __restrict__ Y, KParams p, int gram) {
+  constexpr int CN = BS >= 64 ? 4 : (BS == 32 ? 2 : 1);
+  constexpr int TXN = BS / CN;
+  constexpr int JG = NT / (16 * TXN);
+  static_assert(JG >= 1 && 16 * TXN * JG == NT, "bad layout");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sXr = reinterpret_cast<T*>(smem_raw);          // BM x (dim+1)
+  T* sXc = sXr + BM * (dim + 1);                     // BN x (dim+1)
+  T* sK = sXc + BN * (dim + 1);                      // BM x (BN+1)
+  T* sV = sK + BM * (BN + 1);                        // BN x BS
+
+  const int tid = threadIdx.x;
+  const int64_t rbase = (int64_t)blockIdx.x * BM;
+  const int c0 = blockIdx.y * BS;
+  const int ds = dim + 1;
+
+  for (int e = tid; e < BM * dim; e += NT) {
+    const int r = e / dim, k = e % dim;
+    const int64_t gr = rbase + r;
+    sXr[r * ds + k] = gr < nrows ? Xr[gr * dpad + k] : T(0);
+  }
+
+  const int tx = tid % TXN;
+  const int ty = (tid / TXN) % 16;
+  const int jg = tid / (TXN * 16);
+  T acc[4][CN];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < CN; ++b) acc[a][b] = T(0);
+
+  const T kdiag = T(p.s2 + p.noise2);
+  for (int64_t jb = 0; jb < ncols; jb += BN) {
+    __syncthreads();
+    for (int e = tid; e < BN * dim; e += NT) {
+      const int j = e / dim, k = e % dim;
+      const int64_t gj = jb + j;
+      sXc[j * ds + k] = gj < ncols ? Xc[gj * dpad + k] : T(0);
+    }
+    for (int e = tid; e < BN * BS; e += NT) {
+      const int j = e / BS, c = e % BS;
+      const int64_t gj = jb + j;
+      sV[j * BS + c] = (gj < ncols && c0 + c < s) ? V[gj * s + c0 + c] : T(0);
+    }
+    __syncthreads();
+    // phase 1: kernel tile
+    {
+      const int j = tid % BN;
+      const int64_t gj = jb + j;
+#pragma unroll 4
+      for (int q = 0; q < BM * BN / NT; ++q) {
+        const int r = tid / BN + q * (NT / BN);
+        T d2 = T(0);
+        for (int k = 0; k < dim; ++k) {
+          const T df = sXr[r * ds + k] - sXc[j * ds + k];
+          d2 = fma(df, df, d2);
+        }
+        T kv = kmap<T>(d2, p);
+        if (gram && row0 + rbase + r == gj) kv = kdiag;
+        if (gj >= ncols) kv = T(0);
+        sK[r * (BN + 1) + j] = kv;
+      }
+    }
+    __syncthreads();
+    // phase 2: accumulate K_tile * V_tile
+#pragma unroll 4
+    for (int jj = jg; jj < BN; jj += JG) {
+      T kv[4], vv[CN];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) kv[a] = sK[(ty * 4 + a) * (BN + 1) + jj];
+#pragma unroll
+      for (int b = 0; b < CN; ++b) vv[b] = sV[jj * BS + tx + b * TXN];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < CN; ++b) acc[a][b] = fma(kv[a], vv[b], acc[a][b]);
+    }
+  }
+
+  if constexpr (JG > 1) {
+    __syncthreads();
+    T* red = sK;  // JG x BM x BS  (<= 1024 elements, fits in sK)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < CN; ++b) red[(jg * BM + ty * 4 + a) * BS + tx + b * TXN] = acc[a][b];
+    __syncthreads();
+    if (jg == 0) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < CN; ++b) {
+          T sacc = T(0);
+          for (int g = 0; g < JG; ++g) sacc += red[(g * BM + ty * 4 + a) * BS + tx + b * TXN];
+          acc[a][b] = sacc;
+        }
+    }
+    if (jg != 0) return;
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int64_t gr = rbase + ty * 4 + a;
+    if (gr >= nrows) continue;
+#pragma unroll
+    for (int b = 0; b < CN; ++b) {
+      const int c = c0 + tx + b * TXN;
+      if (c >= s) continue;
+      const T y = acc[a][b];
+      Y[gr * s + c] = B ? B[gr * s + c] - y : y;
+    }
+  }
+}
+
+template <typename T, int BS>
+void launch_bs(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc, int64_t ncols,
+               const T* V, int s, const T* B, T* Y, bool gram, cudaStream_t st) {
+  const int dim = op.dim;
+  const size_t smem = sizeof(T) * ((size_t)(BM + BN) * (dim + 1) + BM * (BN + 1) + BN * BS);
+  auto kern = kmatvec_simt_kernel<T, BS>;
+  if (smem > 48 * 1024)
+    WGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(ceil_div(nrows, BM), ceil_div(s, BS));
+  kern<<<grid, NT, smem, st>>>(Xr, nrows, row0, Xc, ncols, op.dpad, dim, V, s, B, Y, op.kp(),
+                               gram ? 1 : 0);
+  WGP_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+template <typename T>
+void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
+                         int64_t ncols, const T* V, int s, const T* B, T* Y, bool gram,
+                         cudaStream_t st) {
+  if (nrows <= 0 || s <= 0) return;
+  if (s <= 1) return launch_bs<T, 1>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
+  if (s <= 2) return launch_bs<T, 2>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
+  if (s <= 4) return launch_bs<T, 4>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
+  if (s <= 8) return launch_bs<T, 8>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
+  if (s <= 16) return launch_bs<T, 16>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
+  if (s <= 32) return launch_bs<T, 32>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
+  return launch_bs<T, 64>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
+}
+
+template void launch_kmatvec_simt<double>(const Op&, const double*, int64_t, int64_t,
+                                          const double*, int64_t, const double*, int,
+                                          const double*, double*, bool, cudaStream_t);
+template void launch_kmatvec_simt<float>(const Op&, const float*, int64_t, int64_t, const float*,
+                                         int64_t, const float*, int, const float*, float*, bool,
+                                         cudaStream_t);
+
+}  // namespace wgp

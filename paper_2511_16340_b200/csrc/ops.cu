@@ -1,0 +1,117 @@
+// ops.cu -- device-resident operator state: row append (K8) and kernel-matvec dispatch.
+//
+// append_rows restates the growth half of extend_system (kernel.cpp:108-130) and
+// bo_round (thompson.cpp:403-422) for a matrix-free operator: new rows of X are
+// appended to the device copy (capacity doubling, old rows never re-uploaded) with their
+// squared norms, so the next system is ready without recomputing or storing H11.
+#include "solvers.h"
+
+namespace wgp {
+namespace {
+
+__global__ void append_rows_kernel(const double* __restrict__ src, int64_t ld, int col_major,
+                                   int64_t n_new, int dim, int dpad, int64_t row_off,
+                                   double* __restrict__ X64, double* __restrict__ sq64,
+                                   float* __restrict__ X32, float* __restrict__ sq32) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_new;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    float acc32 = 0.0f;
+    const int64_t g = row_off + i;
+    for (int k = 0; k < dpad; ++k) {
+      double x = 0.0;
+      if (k < dim) x = col_major ? src[(int64_t)k * ld + i] : src[i * ld + k];
+      X64[g * dpad + k] = x;
+      acc += x * x;  // sum in k order, as Eigen's rowwise().squaredNorm() / rankUpdate diagonal
+      if (X32) {
+        const float xf = (float)x;
+        X32[g * dpad + k] = xf;
+        acc32 = fmaf(xf, xf, acc32);
+      }
+    }
+    sq64[g] = acc;
+    if (sq32) sq32[g] = acc32;
+  }
+}
+
+}  // namespace
+
+void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major) {
+  if (n_new <= 0) return;
+  cudaStream_t st = op.ctx->stream;
+  const int64_t need = op.n + n_new;
+  if (need > op.cap) {
+    int64_t cap = op.cap > 0 ? op.cap : 1024;
+    while (cap < need) cap *= 2;
+    DBuf<double> X64((size_t)cap * op.dpad), sq64(cap);
+    DBuf<float> X32, sq32;
+    if (!op.f64()) {
+      X32.alloc((size_t)cap * op.dpad);
+      sq32.alloc(cap);
+    }
+    if (op.n > 0) {
+      WGP_CUDA(cudaMemcpyAsync(X64.p, op.X64.p, sizeof(double) * op.n * op.dpad,
+                               cudaMemcpyDeviceToDevice, st));
+      WGP_CUDA(cudaMemcpyAsync(sq64.p, op.sq64.p, sizeof(double) * op.n, cudaMemcpyDeviceToDevice,
+                               st));
+      if (!op.f64()) {
+        WGP_CUDA(cudaMemcpyAsync(X32.p, op.X32.p, sizeof(float) * op.n * op.dpad,
+                                 cudaMemcpyDeviceToDevice, st));
+        WGP_CUDA(cudaMemcpyAsync(sq32.p, op.sq32.p, sizeof(float) * op.n,
+                                 cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    WGP_CUDA(cudaStreamSynchronize(st));
+    op.X64 = std::move(X64);
+    op.sq64 = std::move(sq64);
+    op.X32 = std::move(X32);
+    op.sq32 = std::move(sq32);
+    op.cap = cap;
+  }
+  // stage the host rows (column-major n_new x dim with ld, or row-major with stride ld)
+  const size_t elems = col_major ? (size_t)ld * (op.dim - 1) + n_new : (size_t)ld * (n_new - 1) + op.dim;
+  DBuf<double> stage(elems);
+  WGP_CUDA(cudaMemcpyAsync(stage.p, host_rows, sizeof(double) * elems, cudaMemcpyHostToDevice, st));
+  int grid = ceil_div(n_new, 256);
+  if (grid > 148 * 8) grid = 148 * 8;
+  append_rows_kernel<<<grid, 256, 0, st>>>(stage.p, ld, col_major, n_new, op.dim, op.dpad, op.n,
+                                           op.X64.p, op.sq64.p, op.f64() ? nullptr : op.X32.p,
+                                           op.f64() ? nullptr : op.sq32.p);
+  WGP_CUDA(cudaGetLastError());
+  WGP_CUDA(cudaStreamSynchronize(st));
+  op.n = need;
+}
+
+template <typename T>
+static const T* xrows(const Op& op);
+template <>
+const double* xrows<double>(const Op& op) { return op.X64.p; }
+template <>
+const float* xrows<float>(const Op& op) { return op.X32.p; }
+
+// Y (this rank's rows) = H V, V full n x s.
+template <typename T>
+void launch_kmatvec_full(const Op& op, const T* V, T* Y, int s, cudaStream_t st) {
+  int64_t r0, r1;
+  op.local_rows(&r0, &r1);
+  const T* X = xrows<T>(op);
+  launch_kmatvec_simt<T>(op, X + r0 * op.dpad, r1 - r0, r0, X, op.n, V, s, nullptr, Y, true, st);
+}
+
+// Y = B - H V  (B and Y: this rank's rows; V full)
+template <typename T>
+void launch_residual(const Op& op, const T* B, const T* V, T* Y, int s, cudaStream_t st) {
+  int64_t r0, r1;
+  op.local_rows(&r0, &r1);
+  const T* X = xrows<T>(op);
+  launch_kmatvec_simt<T>(op, X + r0 * op.dpad, r1 - r0, r0, X, op.n, V, s, B, Y, true, st);
+}
+
+template void launch_kmatvec_full<double>(const Op&, const double*, double*, int, cudaStream_t);
+template void launch_kmatvec_full<float>(const Op&, const float*, float*, int, cudaStream_t);
+template void launch_residual<double>(const Op&, const double*, const double*, double*, int,
+                                      cudaStream_t);
+template void launch_residual<float>(const Op&, const float*, const float*, float*, int,
+                                     cudaStream_t);
+
+}  // namespace wgp

@@ -1,0 +1,49 @@
+// solvers.h -- internal solver interfaces (device work buffers, operator applications).
+#pragma once
+
+#include "common.cuh"
+
+namespace wgp {
+
+// Per-solve device buffers, all row-major [n][s] in the compute type.
+template <typename T>
+struct SolverWork {
+  int64_t n = 0;
+  int s = 0;
+  int nch = 0;
+  DBuf<T> V, R, Z, P, HP, B;
+  DBuf<double> part;   // [nch][2][s] chunk partials
+  DBuf<double> scal;   // rz, alpha, beta, bnorm, rel, spare (6 x s)
+  DBuf<int> act;       // active[s] + failure column
+  DBuf<double> pwork;  // preconditioner chunk partials
+  DBuf<double> tvec;   // M^T r  (k x s)
+  void alloc(int64_t n, int s);
+};
+
+struct SolveOutputs {
+  std::vector<std::vector<double>> history;
+  std::vector<int> iterations, converged, status, diverged_at;
+  explicit SolveOutputs(int s) : history(s), iterations(s, 0), converged(s, 0), status(s, 0),
+                                 diverged_at(s, 0) {}
+};
+
+// Operator applications on the full row set (world = 1) or this rank's rows.
+template <typename T>
+void launch_kmatvec_full(const Op& op, const T* V, T* Y, int s, cudaStream_t st);
+template <typename T>
+void launch_residual(const Op& op, const T* B, const T* V, T* Y, int s, cudaStream_t st);
+template <typename T>
+void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
+                         int64_t ncols, const T* V, int s, const T* B, T* Y, bool gram,
+                         cudaStream_t st);
+
+template <typename T>
+void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb, const double* U1,
+                    int64_t ldu, int64_t n1, cudaStream_t st);
+template <typename T>
+void download_solution(SolverWork<T>& w, double* V, int64_t ldv, cudaStream_t st);
+template <typename T>
+void cg_solve_batched(const Op& op, const wgp_solver_config& cfg, const PrecondDev& pd,
+                      SolverWork<T>& w, SolveOutputs& out, cudaStream_t st);
+
+}  // namespace wgp

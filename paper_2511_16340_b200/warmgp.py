@@ -1,0 +1,433 @@
+"""Python mirror of the reference's warmgp API over the C-ABI of libwarmgp_b200.so.
+
+The reference (/root/reference/proj) is a C++ library whose boundary is the
+free-function API of warmgp::{kernel,solvers,sampling}.hpp; its C++ mirror over
+this ABI is include/warmgp/gpu.hpp.  This module offers the same names to Python
+callers (tests, bench.py) -- a thin ctypes layer, no compute of its own:
+
+    reference (dense H)                           here (matrix-free device operator)
+    gram_matrix(X, hyp)          kernel.cpp:48    KernelOperator(hyp, X)
+    extend_system(prev, X2, ..)  kernel.cpp:108   op.append_rows(X2)
+    H * V                        solvers.cpp:162  op.kmatvec(V)
+    solve_many(H, rhs, inits, cfg) solvers.cpp:321 solve_many(op, rhs, inits, cfg)
+    cg_solve / sgd_solve / ap_solve / solve       same names
+    pivoted_cholesky(H, rank)    solvers.cpp:72   pivoted_cholesky(op, rank)
+
+Errors map like the reference's exceptions (types.hpp:15-32): NotSpdError,
+DivergenceError(iterations), ValueError for std::invalid_argument.  There is no
+CPU fallback: a missing library or GPU raises ExtensionUnavailable.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwarmgp_b200.so")
+
+MATERN32, RBF = 0, 1
+F64, F32_3XTF32, TF32, F32_SIMT = 0, 1, 2, 3
+CG, SGD, AP = 0, 1, 2
+SGD_UNBIASED, SGD_BLOCK = 0, 1
+AP_GREEDY, AP_CYCLIC = 0, 1
+SHIFT_CALIBRATED, SHIFT_NOISE_ONLY = 0, 1
+OK, INVALID_ARGUMENT, NOT_SPD, DIVERGED, CUDA_ERROR, NCCL_ERROR, OOM = range(7)
+
+# Every symbol include/warmgp_capi.h declares (checked by tests/test_capi_abi.py).
+EXPORTS = (
+    "wgp_abi_version", "wgp_last_error", "wgp_solver_config_default", "wgp_shard_range",
+    "wgp_ctx_create", "wgp_nccl_unique_id", "wgp_ctx_create_sharded", "wgp_ctx_destroy",
+    "wgp_ctx_stream", "wgp_op_create", "wgp_op_destroy", "wgp_op_append_rows", "wgp_op_size",
+    "wgp_op_dim", "wgp_op_precision", "wgp_kmatvec", "wgp_kmatvec_dev", "wgp_residual_dev",
+    "wgp_cross_matvec", "wgp_solve_many", "wgp_pivoted_cholesky", "wgp_precond_info",
+    "wgp_rff_eval",
+)
+
+
+class ExtensionUnavailable(RuntimeError):
+    """The CUDA library is missing or cannot run (no silent fallback exists)."""
+
+
+class NotSpdError(RuntimeError):
+    """warmgp::NotSpdError (types.hpp:15-18)."""
+
+
+class DivergenceError(RuntimeError):
+    """warmgp::DivergenceError (types.hpp:21-26)."""
+
+    def __init__(self, what: str, iterations: int):
+        super().__init__(what)
+        self.iterations = iterations
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class SolverConfig(C.Structure):
+    """warmgp::SolverConfig (solvers.hpp:27-48), defaults from wgp_solver_config_default."""
+    _fields_ = [("method", C.c_int32), ("tolerance", C.c_double), ("max_iters", C.c_int32),
+                ("learning_rate", C.c_double), ("momentum", C.c_double),
+                ("batch_size", C.c_int64), ("sgd_scaling", C.c_int32),
+                ("block_size", C.c_int64), ("ap_ordering", C.c_int32),
+                ("precond_rank", C.c_int64), ("precond_shift", C.c_double),
+                ("precond_shift_mode", C.c_int32), ("seed", C.c_uint64)]
+
+    def __init__(self, **kw):
+        super().__init__()
+        lib().wgp_solver_config_default(C.byref(self))
+        for k, v in kw.items():
+            setattr(self, k, v)
+
+    def copy(self, **kw) -> "SolverConfig":
+        c = SolverConfig()
+        C.memmove(C.byref(c), C.byref(self), C.sizeof(SolverConfig))
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+
+
+P = C.c_void_p
+I64 = C.c_int64
+D = C.c_double
+_lib = None
+
+
+def _declare(L):
+    sig = {
+        "wgp_abi_version": (C.c_int, []),
+        "wgp_last_error": (C.c_char_p, []),
+        "wgp_solver_config_default": (None, [P]),
+        "wgp_shard_range": (None, [I64, C.c_int, C.c_int, P, P]),
+        "wgp_ctx_create": (C.c_int, [C.c_int, P]),
+        "wgp_nccl_unique_id": (C.c_int, [P]),
+        "wgp_ctx_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, P, P]),
+        "wgp_ctx_destroy": (None, [P]),
+        "wgp_ctx_stream": (P, [P]),
+        "wgp_op_create": (C.c_int, [P, C.c_int, D, D, D, C.c_int, C.c_int, P]),
+        "wgp_op_destroy": (None, [P]),
+        "wgp_op_append_rows": (C.c_int, [P, P, I64, I64, C.c_int]),
+        "wgp_op_size": (I64, [P]),
+        "wgp_op_dim": (C.c_int, [P]),
+        "wgp_op_precision": (C.c_int, [P]),
+        "wgp_kmatvec": (C.c_int, [P, P, I64, C.c_int, P, I64]),
+        "wgp_kmatvec_dev": (C.c_int, [P, P, P, C.c_int, P]),
+        "wgp_residual_dev": (C.c_int, [P, P, P, P, C.c_int, P]),
+        "wgp_cross_matvec": (C.c_int, [P, P, I64, I64, P, I64, C.c_int, P, I64]),
+        "wgp_solve_many": (C.c_int, [P, P, P, I64, C.c_int, P, I64, I64, P, I64, P, P, I64, P, P,
+                                     P, P]),
+        "wgp_pivoted_cholesky": (C.c_int, [P, I64, P, I64, P]),
+        "wgp_precond_info": (C.c_int, [P, I64, D, C.c_int, P, P]),
+        "wgp_rff_eval": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, I64, P, I64]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+
+
+def lib():
+    """Load libwarmgp_b200.so (fails loudly when it is missing: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ExtensionUnavailable(
+                f"{LIB_PATH} is missing; build it with `python -m paper_2511_16340_b200.build`")
+        _lib = C.CDLL(LIB_PATH)
+        _declare(_lib)
+    return _lib
+
+
+def _check(st: int, iterations: int = 0):
+    if st == OK:
+        return
+    msg = lib().wgp_last_error().decode(errors="replace")
+    if st == INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if st == NOT_SPD:
+        raise NotSpdError(msg)
+    if st == DIVERGED:
+        raise DivergenceError(msg, iterations)
+    if st == OOM:
+        raise MemoryError(msg)
+    if st == CUDA_ERROR:
+        raise CudaError(msg)
+    raise RuntimeError(f"wgp status {st}: {msg}")
+
+
+def _f64(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    a, b = C.c_int64(), C.c_int64()
+    lib().wgp_shard_range(n, world, rank, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+@dataclass
+class KernelHyperparams:
+    """warmgp::KernelHyperparams (kernel.hpp:8-14) + ``kind`` (RBF extension)."""
+    lengthscale: float = 1.0
+    signal_scale: float = 1.0
+    noise_scale: float = 1e-3
+    kind: int = MATERN32
+
+
+class DeviceContext:
+    """One CUDA device (one process per GPU); optionally a NCCL row-sharded group."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
+        self._h = C.c_void_p()
+        if world == 1:
+            _check(lib().wgp_ctx_create(device, C.byref(self._h)))
+        else:
+            buf = C.create_string_buffer(bytes(unique_id), 128)
+            _check(lib().wgp_ctx_create_sharded(device, rank, world, buf, C.byref(self._h)))
+        self.device, self.rank, self.world = device, rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().wgp_nccl_unique_id(buf))
+        return buf.raw
+
+    @property
+    def stream(self) -> int:
+        return lib().wgp_ctx_stream(self._h) or 0
+
+    def close(self):
+        if self._h:
+            lib().wgp_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: DeviceContext | None = None
+
+
+def default_context() -> DeviceContext:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = DeviceContext(0)
+    return _default_ctx
+
+
+class KernelOperator:
+    """Matrix-free H = K(X, X) + sigma_n^2 I resident on the device.
+
+    Replaces CovarianceMatrix / gram_matrix (kernel.hpp:25-38): X lives on the
+    GPU, H is never materialised.  ``append_rows`` is extend_system's growth step.
+    """
+
+    def __init__(self, hyp: KernelHyperparams, X=None, dim: int | None = None,
+                 precision: int = F64, ctx: DeviceContext | None = None):
+        self.ctx = ctx or default_context()
+        self.hyp = hyp
+        if X is not None:
+            X = _f64(X)
+            if X.ndim != 2:
+                raise ValueError("X must be 2-d (n x dim)")
+            dim = X.shape[1]
+        self._h = C.c_void_p()
+        _check(lib().wgp_op_create(self.ctx._h, hyp.kind, hyp.lengthscale, hyp.signal_scale,
+                                   hyp.noise_scale, precision, int(dim), C.byref(self._h)))
+        self.dim = int(dim)
+        self.precision = precision
+        if X is not None and X.shape[0] > 0:
+            self.append_rows(X)
+
+    def append_rows(self, X2):
+        X2 = _f64(X2)
+        if X2.ndim != 2 or (X2.shape[0] > 0 and X2.shape[1] != self.dim):
+            raise ValueError("extend_system: feature dimension mismatch")
+        _check(lib().wgp_op_append_rows(self._h, _ptr(X2), X2.shape[0], max(X2.shape[0], 1), 1))
+
+    @property
+    def n(self) -> int:
+        return int(lib().wgp_op_size(self._h))
+
+    def size(self) -> int:
+        return self.n
+
+    def kmatvec(self, V, out=None) -> np.ndarray:
+        """(K(X,X) + sigma_n^2 I) V for host V (n or n x s); ``out``: optional
+        Fortran-ordered n x s float64 destination (e.g. a pinned buffer)."""
+        V = _f64(V)
+        squeeze = V.ndim == 1
+        if squeeze:
+            V = V.reshape(-1, 1, order="F")
+        n = self.n
+        if V.shape[0] != n:
+            raise ValueError("kmatvec: V rows != operator size")
+        if out is None:
+            Y = np.zeros((n, V.shape[1]), order="F")
+        else:
+            Y = out
+            if Y.shape != V.shape or Y.dtype != np.float64 or not Y.flags.f_contiguous:
+                raise ValueError("kmatvec: out must be a Fortran-ordered float64 n x s array")
+        _check(lib().wgp_kmatvec(self._h, _ptr(V), n, V.shape[1], _ptr(Y), n))
+        return Y[:, 0] if squeeze else Y
+
+    def kmatvec_dev(self, dV_ptr: int, dY_ptr: int, s: int, stream: int = 0):
+        _check(lib().wgp_kmatvec_dev(self._h, C.c_void_p(dV_ptr), C.c_void_p(dY_ptr), s,
+                                     C.c_void_p(stream) if stream else None))
+
+    def residual_dev(self, dB_ptr: int, dV_ptr: int, dY_ptr: int, s: int, stream: int = 0):
+        _check(lib().wgp_residual_dev(self._h, C.c_void_p(dB_ptr), C.c_void_p(dV_ptr),
+                                      C.c_void_p(dY_ptr), s, C.c_void_p(stream) if stream else None))
+
+    def cross_matvec(self, Xs, W) -> np.ndarray:
+        """K(X*, X) W without the noise term (cross_kernel kernel.cpp:74-89 times weights)."""
+        Xs = _f64(Xs)
+        W = _f64(W)
+        squeeze = W.ndim == 1
+        if squeeze:
+            W = W.reshape(-1, 1, order="F")
+        if Xs.shape[1] != self.dim:
+            raise ValueError("cross_kernel: dimension mismatch")
+        m = Xs.shape[0]
+        Y = np.zeros((m, W.shape[1]), order="F")
+        _check(lib().wgp_cross_matvec(self._h, _ptr(Xs), m, max(m, 1), _ptr(W), self.n, W.shape[1],
+                                      _ptr(Y), max(m, 1)))
+        return Y[:, 0] if squeeze else Y
+
+    def close(self):
+        if self._h:
+            lib().wgp_op_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gram_operator(X, hyp: KernelHyperparams, precision: int = F64, ctx=None) -> KernelOperator:
+    """Device counterpart of gram_matrix (kernel.cpp:48-72)."""
+    X = _f64(X)
+    if X.shape[0] < 1:
+        raise ValueError("gram_matrix: need at least one row")
+    return KernelOperator(hyp, X, precision=precision, ctx=ctx)
+
+
+@dataclass
+class Initialization:
+    """warmgp::Initialization (solvers.hpp:52-63)."""
+    warm_start: bool = False
+    u1: np.ndarray | None = None
+
+    @staticmethod
+    def cold() -> "Initialization":
+        return Initialization()
+
+    @staticmethod
+    def warm(u1) -> "Initialization":
+        return Initialization(True, np.asarray(u1, dtype=np.float64).copy())
+
+
+@dataclass
+class SolveResult:
+    """warmgp::SolveResult (solvers.hpp:102-109)."""
+    v: np.ndarray
+    iterations: int
+    residual_history: list = field(default_factory=list)
+    converged: bool = False
+
+    def final_residual(self) -> float:
+        return self.residual_history[-1]
+
+
+def solve_many(op: KernelOperator, rhs, inits: list, cfg: SolverConfig, return_status: bool = False):
+    """solve_many (solvers.cpp:321-354) on the device: all columns in one batched solve.
+
+    Raises at the lowest failing column like the reference.  With
+    ``return_status=True`` no exception is raised; returns (results, status, diverged_at)
+    so callers can implement solve_best_effort (thompson.cpp:299-317)."""
+    B = _f64(rhs)
+    if B.ndim == 1:
+        B = B.reshape(-1, 1, order="F")
+    n, s = B.shape
+    if len(inits) != s:
+        raise ValueError("solve_many: one initialization per right-hand side required")
+    if n != op.n:
+        raise ValueError("solve_many: rhs rows != operator size")
+    warm = [i.warm_start for i in inits]
+    U1 = None
+    n1 = 0
+    if any(warm):
+        n1s = {i.u1.size for i in inits if i.warm_start}
+        if len(n1s) != 1:
+            raise ValueError("solve_many: warm starts must share one length")
+        n1 = n1s.pop()
+        U1 = np.zeros((n1, s), order="F")
+        for c, i in enumerate(inits):
+            if i.warm_start:
+                U1[:, c] = i.u1
+    V = np.zeros((n, s), order="F")
+    hs = cfg.max_iters + 1
+    hist = np.zeros((s, hs))
+    its = np.zeros(s, dtype=np.int32)
+    hl = np.zeros(s, dtype=np.int32)
+    cv = np.zeros(s, dtype=np.int32)
+    cst = np.zeros(s, dtype=np.int32)
+    dv = np.zeros(s, dtype=np.int32)
+    st = lib().wgp_solve_many(op._h, C.byref(cfg), _ptr(B), n, s, _ptr(U1), max(n1, 1), n1, _ptr(V), n,
+                              _ptr(its), _ptr(hist), hs, _ptr(hl), _ptr(cv), _ptr(cst), _ptr(dv))
+    results = [SolveResult(V[:, c].copy(), int(its[c]), hist[c, : hl[c]].tolist(), bool(cv[c]))
+               for c in range(s)]
+    if return_status:
+        if st not in (OK, NOT_SPD, DIVERGED):
+            _check(st)
+        return results, cst, dv
+    if st != OK:
+        bad = [c for c in range(s) if cst[c] != OK]
+        _check(st, int(dv[bad[0]]) if bad else 0)
+    return results
+
+
+def solve(op: KernelOperator, b, init: Initialization, cfg: SolverConfig) -> SolveResult:
+    """solve (solvers.cpp:311-319): one RHS."""
+    return solve_many(op, np.asarray(b, dtype=np.float64).reshape(-1, 1), [init], cfg)[0]
+
+
+def cg_solve(op, b, init, cfg) -> SolveResult:
+    return solve(op, b, init, cfg.copy(method=CG))
+
+
+def sgd_solve(op, b, init, cfg) -> SolveResult:
+    return solve(op, b, init, cfg.copy(method=SGD))
+
+
+def ap_solve(op, b, init, cfg) -> SolveResult:
+    return solve(op, b, init, cfg.copy(method=AP))
+
+
+def pivoted_cholesky(op: KernelOperator, rank: int) -> np.ndarray:
+    """pivoted_cholesky (solvers.cpp:72-107) on the device; returns n x achieved (column-major)."""
+    n = op.n
+    L = np.zeros((n, max(rank, 0)), order="F")
+    ach = C.c_int64()
+    _check(lib().wgp_pivoted_cholesky(op._h, rank, _ptr(L) if rank > 0 else None, max(n, 1), C.byref(ach)))
+    return np.asfortranarray(L[:, : ach.value])
+
+
+def precond_info(op: KernelOperator, rank: int, shift: float, mode: int = SHIFT_CALIBRATED):
+    """(achieved rank, calibrated shift) of CgPreconditioner::from_matrix (solvers.cpp:123-133)."""
+    ach = C.c_int64()
+    sh = C.c_double()
+    _check(lib().wgp_precond_info(op._h, rank, shift, mode, C.byref(ach), C.byref(sh)))
+    return ach.value, sh.value

@@ -1,0 +1,102 @@
+"""GPU CG parity against the oracle: iteration counts within +-2%, histories and final
+residuals within tolerance, and the reference's per-column semantics (solvers.cpp:142-183,
+321-354)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def iters_close(a, b):
+    return abs(a - b) <= max(1, round(0.02 * max(a, b)))
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_cg_c1_reduced_golden(W, precision):
+    g = np.load(os.path.join(HERE, "golden", "cg_c1_reduced.npz"))
+    kind, ls, sf, sn = g["hyp"]
+    op = W.KernelOperator(W.KernelHyperparams(ls, sf, sn, int(kind)), g["X"], precision=precision)
+    cfg = W.SolverConfig(tolerance=1e-6, precond_rank=100, precond_shift=0.01)
+    cold = W.solve(op, g["y"], W.Initialization.cold(), cfg)
+    warm = W.solve(op, g["y"], W.Initialization.warm(g["u1"]), cfg)
+    for res, key in ((cold, "cold"), (warm, "warm")):
+        hist = g[f"{key}_hist"]
+        assert iters_close(res.iterations, len(hist) - 1), (key, res.iterations, len(hist) - 1)
+        assert res.converged
+        if precision == 0:
+            n = min(len(hist), len(res.residual_history))
+            np.testing.assert_allclose(res.residual_history[:n], hist[:n], rtol=1e-6)
+            np.testing.assert_allclose(res.v, g[f"{key}_v"], rtol=0, atol=1e-6 * np.abs(g[f"{key}_v"]).max())
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_cg_multi_rhs_vs_oracle(W, O, precision):
+    h = O.KernelHyperparams(0.5, 1.0, 0.5, O.MATERN32)
+    X = O.uniform_inputs(36, 600, 3)
+    B = np.asfortranarray(np.stack([O.gaussian_vector(100 + k, 600) for k in range(9)], 1))
+    B[:, 4] = 0.0  # zero right-hand side column -> zero_rhs_result
+    cfg = O.SolverConfig(tolerance=1e-6, precond_rank=20, precond_shift=0.25, max_iters=500)
+    H = O.gram_matrix(X, h)
+    ref = O.solve_many(H, B, [O.Initialization.cold()] * 9, cfg)
+    op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.5, 0), X, precision=precision)
+    wcfg = W.SolverConfig(tolerance=1e-6, precond_rank=20, precond_shift=0.25, max_iters=500)
+    got = W.solve_many(op, B, [W.Initialization.cold()] * 9, wcfg)
+    for r, g in zip(ref, got):
+        assert iters_close(r.iterations, g.iterations), (r.iterations, g.iterations)
+        assert g.converged == r.converged
+        assert len(g.residual_history) == g.iterations + 1
+    assert got[4].iterations == 0 and got[4].residual_history == [0.0] and not got[4].v.any()
+
+
+def test_cg_budget_binds_and_history_contract(W, O):
+    X = O.uniform_inputs(30, 300, 3)
+    B = np.random.default_rng(2).standard_normal((300, 5))
+    op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.5, 0), X)
+    cfg = W.SolverConfig(tolerance=0.0, max_iters=5, precond_rank=10, precond_shift=0.25)
+    res = W.solve_many(op, B, [W.Initialization.cold()] * 5, cfg)
+    for r in res:
+        assert r.iterations == 5 and len(r.residual_history) == 6 and not r.converged
+        assert r.residual_history[0] == pytest.approx(1.0, abs=1e-15)
+    cfg0 = W.SolverConfig(tolerance=1e-6, max_iters=0)
+    r0 = W.solve(op, B[:, 0], W.Initialization.cold(), cfg0)
+    assert r0.iterations == 0 and len(r0.residual_history) == 1
+
+
+def test_cg_identical_columns_identical_results(W, O):
+    X = O.uniform_inputs(36, 500, 3)
+    b = O.gaussian_vector(7, 500)
+    op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.5, 0), X)
+    cfg = W.SolverConfig(tolerance=1e-6, precond_rank=10, precond_shift=0.25)
+    res = W.solve_many(op, np.stack([b, b, b], 1), [W.Initialization.cold()] * 3, cfg)
+    assert np.array_equal(res[0].v, res[1].v) and np.array_equal(res[1].v, res[2].v)
+    single = W.solve(op, b, W.Initialization.cold(), cfg)
+    assert np.array_equal(single.v, res[0].v)
+
+
+def test_warm_start_layout(W, O):
+    """Initialization::warm -> [u1; 0]; zero-iteration budget keeps the init verbatim."""
+    X = O.uniform_inputs(3, 120, 2)
+    op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.3, 0), X)
+    u1 = np.arange(100, dtype=float) / 100
+    cfg = W.SolverConfig(tolerance=0.0, max_iters=0)
+    r = W.solve(op, np.ones(120), W.Initialization.warm(u1), cfg)
+    assert np.array_equal(r.v[:100], u1) and not r.v[100:].any()
+    with pytest.raises(ValueError):
+        W.solve(op, np.ones(120), W.Initialization.warm(np.ones(121)), cfg)
+
+
+def test_pivoted_cholesky_matches_oracle(W, O):
+    h = O.KernelHyperparams(0.4, 1.0, 0.3, O.MATERN32)
+    X = O.uniform_inputs(9, 400, 3)
+    H = O.gram_matrix(X, h)
+    Lref = O.pivoted_cholesky(H, 40)
+    op = W.KernelOperator(W.KernelHyperparams(0.4, 1.0, 0.3, 0), X)
+    L = W.pivoted_cholesky(op, 40)
+    assert L.shape == Lref.shape
+    np.testing.assert_allclose(L, Lref, atol=1e-10)
+    ach, shift = W.precond_info(op, 40, 0.09)
+    pre = O.CgPreconditioner.from_matrix(H, 40, 0.09)
+    assert ach == pre.rank and shift == pytest.approx(pre.shift, rel=1e-12)

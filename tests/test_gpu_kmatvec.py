@@ -1,0 +1,92 @@
+"""GPU parity of the fused kernel-matvec (K1) against the CPU oracle, through the C-ABI.
+
+Bars (BASELINE.json north_star): relative error <= 1e-10 on the fp64 path and
+<= 1e-4 on the fp32/tf32 path, measured per RHS column as |Y - Y_ref| / |Y_ref|.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+TOL = {0: 1e-10, 1: 1e-4, 3: 1e-4}  # F64, F32_3XTF32, F32_SIMT
+
+
+def colrel(Y, Yref):
+    return float(np.max(np.linalg.norm(Y - Yref, axis=0) / np.linalg.norm(Yref, axis=0)))
+
+
+def hyp_of(W, arr):
+    kind, ls, sf, sn = arr
+    return W.KernelHyperparams(float(ls), float(sf), float(sn), int(kind))
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(HERE, "golden", "kmatvec_*.npz"))),
+                         ids=lambda p: os.path.basename(p)[8:-4])
+@pytest.mark.parametrize("precision", [0, 1, 3])
+def test_kmatvec_golden(W, path, precision):
+    g = np.load(path)
+    op = W.KernelOperator(hyp_of(W, g["hyp"]), g["X"], precision=precision)
+    Y = op.kmatvec(g["V"])
+    assert colrel(Y, g["Y"]) <= TOL[precision]
+
+
+@pytest.mark.parametrize("n,d,s", [(1, 3, 1), (2, 1, 2), (63, 5, 3), (65, 16, 17), (200, 8, 129), (1000, 2, 64)])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_kmatvec_shapes_vs_oracle(W, O, n, d, s, kind):
+    h = O.KernelHyperparams(0.6, 1.3, 0.2, kind)
+    X = O.uniform_inputs(n * 7 + d, n, d)
+    V = np.random.default_rng(n + s).standard_normal((n, s))
+    Yref = O.kmatvec(X, h, V)
+    for prec in (0, 1, 3):
+        op = W.KernelOperator(W.KernelHyperparams(0.6, 1.3, 0.2, kind), X, precision=prec)
+        assert colrel(op.kmatvec(V), Yref) <= TOL[prec], prec
+
+
+def test_append_rows_equals_concat(W, O):
+    h = O.KernelHyperparams(0.5, 1.0, 0.1, O.MATERN32)
+    X1 = O.uniform_inputs(51, 300, 3)
+    X2 = O.uniform_inputs(52, 700, 3)
+    X = np.vstack([X1, X2])
+    V = np.random.default_rng(0).standard_normal((1000, 4))
+    op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.1, 0), X1)
+    op.append_rows(X2[:100])
+    op.append_rows(X2[100:])  # crosses the initial capacity (1024 rows) growth path
+    assert op.n == 1000
+    assert colrel(op.kmatvec(V), O.kmatvec(X, h, V)) <= 1e-12
+
+
+def test_cross_matvec_vs_oracle(W, O):
+    h = O.KernelHyperparams(0.3, 1.1, 1e-3, O.MATERN32)
+    X = O.uniform_inputs(61, 400, 4)
+    Xs = O.uniform_inputs(62, 333, 4)
+    Wt = np.random.default_rng(1).standard_normal((400, 5))
+    ref = O.cross_kernel(Xs, X, h) @ Wt
+    for prec in (0, 1):
+        op = W.KernelOperator(W.KernelHyperparams(0.3, 1.1, 1e-3, 0), X, precision=prec)
+        assert colrel(op.cross_matvec(Xs, Wt), ref) <= TOL[prec]
+
+
+def test_kmatvec_linearity_large(W):
+    """Size-independent property at a BASELINE-scale N: H(aU + bV) = aHU + bHV."""
+    rng = np.random.default_rng(5)
+    n, d = 20000, 8
+    X = rng.random((n, d))
+    U = rng.standard_normal((n, 4))
+    V = rng.standard_normal((n, 4))
+    op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.1, 1), X, precision=1)
+    lhs = op.kmatvec(2.0 * U - 3.0 * V)
+    rhs = 2.0 * op.kmatvec(U) - 3.0 * op.kmatvec(V)
+    assert colrel(lhs, rhs) <= 1e-4
+
+
+def test_invalid_arguments(W):
+    with pytest.raises(ValueError):
+        W.KernelOperator(W.KernelHyperparams(-1.0, 1.0, 0.1), np.zeros((3, 2)))
+    op = W.KernelOperator(W.KernelHyperparams(1.0, 1.0, 0.1), np.zeros((3, 2)))
+    with pytest.raises(ValueError):
+        op.append_rows(np.zeros((2, 3)))
+    with pytest.raises(ValueError):
+        op.kmatvec(np.zeros((4, 1)))
