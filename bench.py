@@ -195,7 +195,8 @@ def run_ours(args):
     V = torch.randn(n, S, device="cuda", dtype=dt, generator=gen)
     Y = torch.empty(r1 - r0, S, device="cuda", dtype=dt)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real (non-legacy) stream: our launches and the events share it
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
     def step():

@@ -163,6 +163,22 @@ wgp_status wgp_rff_eval(wgp_op* op, const double* Omega, const double* phases, c
                         int F, int S, double signal_scale, const double* Xstar, int64_t m,
                         int64_t ldx, double* out, int64_t ldo);
 
+/* ---- host-side randomness (rng.hpp:11-61, bit-identical streams) ----
+ * Draws that the reference makes on the host stay on the host: RFF frequencies,
+ * observation noise, SGD batch indices.  `state` is warmgp::Rng's 64-bit state. */
+uint64_t wgp_derive_seed(uint64_t seed, uint64_t stream);
+uint64_t wgp_rng_next_u64(uint64_t* state);
+double wgp_rng_uniform(uint64_t* state);
+double wgp_rng_normal(uint64_t* state);
+double wgp_rng_chi_square3(uint64_t* state);
+uint64_t wgp_rng_uniform_index(uint64_t* state, uint64_t n);
+/* out[i] = scale * Rng(seed).normal(), i = 0..n-1 (build_sample_rhs noise, sampling.cpp:58-62) */
+void wgp_normal_fill(uint64_t seed, int64_t n, double scale, double* out);
+/* sample_prior (sampling.cpp:14-35): Omega F x dim column-major, phases F, amps F.
+ * Matern-3/2 rows are Student-t(3)/l (reference); RBF rows N(0, l^-2 I) (extension). */
+wgp_status wgp_sample_prior(int kernel, double lengthscale, int64_t dim, int64_t F, uint64_t seed,
+                            double* Omega, double* phases, double* amps);
+
 #ifdef __cplusplus
 }
 #endif

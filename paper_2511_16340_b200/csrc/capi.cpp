@@ -23,6 +23,9 @@ void throw_error(wgp_status code, const char* fmt, ...) {
 }
 
 void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major);
+void launch_rff_eval64(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
+                       const double* ph, const double* amp, int F, int S, double coeff,
+                       double* out, int64_t ldo, cudaStream_t st);
 void dist_init(Ctx& ctx, const void* uid);
 void dist_destroy(Ctx& ctx);
 
@@ -395,7 +398,37 @@ wgp_status wgp_rff_eval(wgp_op* op, const double* Omega, const double* phases, c
                         int F, int S, double signal_scale, const double* Xs, int64_t m, int64_t ldx,
                         double* out, int64_t ldo) {
   return guard([&] {
-    throw_error(WGP_INVALID_ARGUMENT, "wgp_rff_eval: not available in this build");
+    WGP_REQUIRE(op && Omega && phases && amps && out, "wgp_rff_eval: null argument");
+    WGP_REQUIRE(F >= 1 && S >= 0, "sample_prior: dim and num_features must be positive");
+    if (S == 0) return;
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    const int dim = op->dim;
+    Op tmp;
+    const double* Xd = op->X64.p;
+    if (Xs) {  // evaluation points given on the host (candidates); else the operator's rows
+      WGP_REQUIRE(m >= 0 && ldx >= m, "wgp_rff_eval: bad X* shape");
+      tmp.ctx = op->ctx;
+      tmp.precision = WGP_F64;
+      tmp.dim = dim;
+      tmp.dpad = op->dpad;
+      op_append_rows(tmp, Xs, m, ldx, 1);
+      Xd = tmp.X64.p;
+    } else {
+      m = op->n;
+    }
+    WGP_REQUIRE(ldo >= m, "wgp_rff_eval: ldo < m");
+    if (m == 0) return;
+    const size_t nom = (size_t)S * F * dim, nf = (size_t)S * F;
+    DBuf<double> dOm(nom), dPh(nf), dAm(nf), dOut((size_t)m * S);
+    WGP_CUDA(cudaMemcpyAsync(dOm.p, Omega, sizeof(double) * nom, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpyAsync(dPh.p, phases, sizeof(double) * nf, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpyAsync(dAm.p, amps, sizeof(double) * nf, cudaMemcpyHostToDevice, st));
+    const double coeff = signal_scale * std::sqrt(2.0 / (double)F);  // sampling.cpp:40-41
+    launch_rff_eval64(Xd, op->dpad, dim, m, dOm.p, dPh.p, dAm.p, F, S, coeff, dOut.p, m, st);
+    WGP_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * ldo, dOut.p, sizeof(double) * m,
+                               sizeof(double) * m, S, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
   });
 }
 

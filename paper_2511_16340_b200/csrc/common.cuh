@@ -154,9 +154,5 @@ template <typename T>
 void precond_apply(const PrecondDev& pd, const T* R, T* Z, int s, double* work_t, double* work_part,
                    cudaStream_t st);
 
-// rff.cu
-template <typename T>
-void launch_rff_eval(const T* X, int dpad, int dim, int64_t m, const double* Om, const double* ph,
-                     const double* amp, int F, int S, double coeff, T* out, cudaStream_t st);
 
 }  // namespace wgp

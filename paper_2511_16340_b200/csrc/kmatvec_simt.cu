@@ -38,7 +38,9 @@ __device__ __forceinline__ float kmap<float>(float d2, const KParams& p) {
 }
 
 // BS: RHS columns per block.  Phase-2 thread layout: 16 row groups x (BS/CN) column
-// groups x JG interleaved j-groups, 4 rows x CN columns per thread.
+// groups, 4 rows x CN columns per thread, j accumulated strictly in order -- every output
+// column sees the same summation order whatever s is, so batched and single-RHS solves
+// agree bitwise (test_solvers.cpp:397-413).  Threads beyond 16*BS/CN idle in phase 2.
 template <typename T, int BS>
 __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
     const T* __restrict__ Xr, int64_t nrows, int64_t row0, const T* __restrict__ Xc,
@@ -46,8 +48,7 @@ __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
     T* __restrict__ Y, KParams p, int gram) {
   constexpr int CN = BS >= 64 ? 4 : (BS == 32 ? 2 : 1);
   constexpr int TXN = BS / CN;
-  constexpr int JG = NT / (16 * TXN);
-  static_assert(JG >= 1 && 16 * TXN * JG == NT, "bad layout");
+  static_assert(16 * TXN <= NT, "bad layout");
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sXr = reinterpret_cast<T*>(smem_raw);          // BM x (dim+1)
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
 
   const int tx = tid % TXN;
   const int ty = (tid / TXN) % 16;
-  const int jg = tid / (TXN * 16);
+  const bool p2 = tid < 16 * TXN;
   T acc[4][CN];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -109,8 +110,9 @@ __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
     }
     __syncthreads();
     // phase 2: accumulate K_tile * V_tile
+    if (!p2) continue;
 #pragma unroll 4
-    for (int jj = jg; jj < BN; jj += JG) {
+    for (int jj = 0; jj < BN; ++jj) {
       T kv[4], vv[CN];
 #pragma unroll
       for (int a = 0; a < 4; ++a) kv[a] = sK[(ty * 4 + a) * (BN + 1) + jj];
@@ -123,26 +125,7 @@ __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
     }
   }
 
-  if constexpr (JG > 1) {
-    __syncthreads();
-    T* red = sK;  // JG x BM x BS  (<= 1024 elements, fits in sK)
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < CN; ++b) red[(jg * BM + ty * 4 + a) * BS + tx + b * TXN] = acc[a][b];
-    __syncthreads();
-    if (jg == 0) {
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < CN; ++b) {
-          T sacc = T(0);
-          for (int g = 0; g < JG; ++g) sacc += red[(g * BM + ty * 4 + a) * BS + tx + b * TXN];
-          acc[a][b] = sacc;
-        }
-    }
-    if (jg != 0) return;
-  }
+  if (!p2) return;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int64_t gr = rbase + ty * 4 + a;

@@ -49,52 +49,43 @@ __global__ void rows_to_colmajor_kernel(const T* __restrict__ src, int64_t n, in
   }
 }
 
-// One block per chunk.  Lanes map to (row-sub, column) with SP = pow2 >= min(s,32)
-// columns per warp step; the 8 warps stride rows; fixed-order combine at the end.
+// One block per chunk.  Per column the chunk is cut into 32 fixed 16-row slabs summed
+// sequentially, then the 32 slab sums are added in slab order: the order of every column's
+// sum depends only on the row index, never on s or on the other columns (solve_many must
+// equal single-RHS solves bitwise, test_solvers.cpp:397-413).
+constexpr int kSlabRows = kChunkRows / 32;
+
 template <typename T, int NQ>
 __global__ void __launch_bounds__(256) coldots_kernel(const T* __restrict__ A0,
                                                       const T* __restrict__ B0,
                                                       const T* __restrict__ A1,
                                                       const T* __restrict__ B1, int64_t n, int s,
-                                                      int SP, double* __restrict__ part) {
-  __shared__ double red[8][NQ][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                                      double* __restrict__ part) {
+  extern __shared__ double red[];  // [NQ][32][s]
   const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
-  const int64_t r1 = min(n, r0 + (int64_t)kChunkRows);
-  const int RS = 32 / SP;  // rows per warp step
-  const int rsub = lane / SP, cl = lane % SP;
-  for (int cb = 0; cb < s; cb += SP) {
-    const int c = cb + cl;
+  for (int f = threadIdx.x; f < 32 * s; f += blockDim.x) {
+    const int q = f / s, c = f % s;
+    const int64_t i0 = r0 + (int64_t)q * kSlabRows;
+    const int64_t i1 = min(n, i0 + kSlabRows);
     double a0 = 0.0, a1 = 0.0;
-    if (c < s) {
-      for (int64_t i = r0 + warp * RS + rsub; i < r1; i += 8 * RS) {
-        const int64_t e = i * s + c;
-        a0 = fma((double)A0[e], (double)B0[e], a0);
-        if (NQ > 1) a1 = fma((double)A1[e], (double)B1[e], a1);
-      }
+    for (int64_t i = i0; i < i1; ++i) {
+      const int64_t e = i * s + c;
+      a0 = fma((double)A0[e], (double)B0[e], a0);
+      if (NQ > 1) a1 = fma((double)A1[e], (double)B1[e], a1);
     }
-    // combine row-subs inside the warp (lanes with equal cl), fixed butterfly order
-    for (int off = SP; off < 32; off <<= 1) {
-      a0 += __shfl_xor_sync(0xffffffffu, a0, off);
-      if (NQ > 1) a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+    red[q * s + c] = a0;
+    if (NQ > 1) red[(32 + q) * s + c] = a1;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < s; c += blockDim.x) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int q = 0; q < 32; ++q) {
+      t0 += red[q * s + c];
+      if (NQ > 1) t1 += red[(32 + q) * s + c];
     }
-    if (rsub == 0) {
-      red[warp][0][cl] = a0;
-      if (NQ > 1) red[warp][NQ - 1][cl] = a1;
-    }
-    __syncthreads();
-    if (threadIdx.x < SP && cb + (int)threadIdx.x < s) {
-      const int cc = threadIdx.x;
-      double t0 = 0.0, t1 = 0.0;
-      for (int w = 0; w < 8; ++w) {
-        t0 += red[w][0][cc];
-        if (NQ > 1) t1 += red[w][NQ - 1][cc];
-      }
-      double* out = part + (int64_t)blockIdx.x * NQ * s;
-      out[cb + cc] = t0;
-      if (NQ > 1) out[s + cb + cc] = t1;
-    }
-    __syncthreads();
+    double* out = part + (int64_t)blockIdx.x * NQ * s;
+    out[c] = t0;
+    if (NQ > 1) out[s + c] = t1;
   }
 }
 
@@ -162,12 +153,18 @@ void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t 
   if (s <= 0) return;
   const int nch = ceil_div(n, kChunkRows);
   if (nch <= 0) return;
-  int SP = 1;
-  while (SP < s && SP < 32) SP <<= 1;
-  if (A1)
-    coldots_kernel<T, 2><<<nch, 256, 0, st>>>(A0, B0, A1, B1, n, s, SP, part);
-  else
-    coldots_kernel<T, 1><<<nch, 256, 0, st>>>(A0, B0, A0, B0, n, s, SP, part);
+  const size_t smem = sizeof(double) * 32 * s * (A1 ? 2 : 1);
+  if (A1) {
+    if (smem > 48 * 1024)
+      WGP_CUDA(cudaFuncSetAttribute(coldots_kernel<T, 2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    coldots_kernel<T, 2><<<nch, 256, smem, st>>>(A0, B0, A1, B1, n, s, part);
+  } else {
+    if (smem > 48 * 1024)
+      WGP_CUDA(cudaFuncSetAttribute(coldots_kernel<T, 1>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    coldots_kernel<T, 1><<<nch, 256, smem, st>>>(A0, B0, A0, B0, n, s, part);
+  }
   WGP_CUDA(cudaGetLastError());
 }
 

@@ -43,7 +43,8 @@ EXPORTS = (
     "wgp_ctx_stream", "wgp_op_create", "wgp_op_destroy", "wgp_op_append_rows", "wgp_op_size",
     "wgp_op_dim", "wgp_op_precision", "wgp_kmatvec", "wgp_kmatvec_dev", "wgp_residual_dev",
     "wgp_cross_matvec", "wgp_solve_many", "wgp_pivoted_cholesky", "wgp_precond_info",
-    "wgp_rff_eval",
+    "wgp_rff_eval", "wgp_derive_seed", "wgp_rng_next_u64", "wgp_rng_uniform", "wgp_rng_normal",
+    "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
 )
 
 
@@ -122,6 +123,14 @@ def _declare(L):
         "wgp_pivoted_cholesky": (C.c_int, [P, I64, P, I64, P]),
         "wgp_precond_info": (C.c_int, [P, I64, D, C.c_int, P, P]),
         "wgp_rff_eval": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, I64, P, I64]),
+        "wgp_derive_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+        "wgp_rng_next_u64": (C.c_uint64, [P]),
+        "wgp_rng_uniform": (D, [P]),
+        "wgp_rng_normal": (D, [P]),
+        "wgp_rng_chi_square3": (D, [P]),
+        "wgp_rng_uniform_index": (C.c_uint64, [P, C.c_uint64]),
+        "wgp_normal_fill": (None, [C.c_uint64, I64, D, P]),
+        "wgp_sample_prior": (C.c_int, [C.c_int, D, I64, I64, C.c_uint64, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -431,3 +440,110 @@ def precond_info(op: KernelOperator, rank: int, shift: float, mode: int = SHIFT_
     sh = C.c_double()
     _check(lib().wgp_precond_info(op._h, rank, shift, mode, C.byref(ach), C.byref(sh)))
     return ach.value, sh.value
+
+
+# ----------------------------------------------------------------- host randomness
+_M64 = 2**64 - 1
+
+
+def derive_seed(seed: int, stream: int) -> int:
+    """derive_seed (rng.hpp:11-16)."""
+    return int(lib().wgp_derive_seed(seed & _M64, stream & _M64))
+
+
+class Rng:
+    """warmgp::Rng (rng.hpp:21-61), bit-identical streams."""
+
+    def __init__(self, seed: int):
+        self._s = C.c_uint64(seed & _M64)
+
+    def next_u64(self) -> int:
+        return int(lib().wgp_rng_next_u64(C.byref(self._s)))
+
+    def uniform(self, lo: float | None = None, hi: float | None = None) -> float:
+        u = lib().wgp_rng_uniform(C.byref(self._s))
+        return u if lo is None else lo + (hi - lo) * u
+
+    def normal(self) -> float:
+        return lib().wgp_rng_normal(C.byref(self._s))
+
+    def chi_square3(self) -> float:
+        return lib().wgp_rng_chi_square3(C.byref(self._s))
+
+    def uniform_index(self, n: int) -> int:
+        return int(lib().wgp_rng_uniform_index(C.byref(self._s), n))
+
+    def derive(self, stream: int) -> "Rng":
+        return Rng(derive_seed(self._s.value, stream))
+
+
+def normal_fill(seed: int, n: int, scale: float = 1.0) -> np.ndarray:
+    out = np.zeros(n)
+    lib().wgp_normal_fill(seed & _M64, n, scale, _ptr(out))
+    return out
+
+
+@dataclass
+class RffPrior:
+    """warmgp::RffPrior (sampling.hpp:14-22)."""
+    frequencies: np.ndarray  # F x D
+    phases: np.ndarray
+    amplitudes: np.ndarray
+    signal_scale: float = 1.0
+
+    @property
+    def num_features(self) -> int:
+        return self.frequencies.shape[0]
+
+    @property
+    def dim(self) -> int:
+        return self.frequencies.shape[1]
+
+
+def sample_prior(hyp: KernelHyperparams, dim: int, num_features: int, seed: int) -> RffPrior:
+    """sample_prior (sampling.cpp:14-35) with the reference's RNG consumption order."""
+    if not (hyp.lengthscale > 0 and hyp.signal_scale > 0 and hyp.noise_scale > 0):
+        raise ValueError("kernel hyperparameters must be strictly positive")
+    if dim < 1 or num_features < 1:
+        raise ValueError("sample_prior: dim and num_features must be positive")
+    Om = np.zeros((num_features, dim), order="F")
+    ph = np.zeros(num_features)
+    am = np.zeros(num_features)
+    _check(lib().wgp_sample_prior(hyp.kind, hyp.lengthscale, dim, num_features, seed & _M64,
+                                  _ptr(Om), _ptr(ph), _ptr(am)))
+    return RffPrior(Om, ph, am, hyp.signal_scale)
+
+
+def rff_eval(op: KernelOperator, priors: list, Xs=None) -> np.ndarray:
+    """eval_prior (sampling.cpp:37-46) for several priors sharing F and signal scale, fused on
+    the device; evaluated at the operator's rows (Xs=None) or at host points Xs (m x d)."""
+    if not priors:
+        return np.zeros((op.n if Xs is None else np.asarray(Xs).shape[0], 0), order="F")
+    F = priors[0].num_features
+    sf = priors[0].signal_scale
+    for p in priors:
+        if p.num_features != F or p.signal_scale != sf or p.dim != op.dim:
+            raise ValueError("rff_eval: priors must share F, signal scale and the operator's dim")
+    S = len(priors)
+    Om = np.ascontiguousarray(np.stack([np.asfortranarray(p.frequencies).ravel(order="F") for p in priors]))
+    ph = np.ascontiguousarray(np.stack([p.phases for p in priors]))
+    am = np.ascontiguousarray(np.stack([p.amplitudes for p in priors]))
+    if Xs is not None:
+        Xs = _f64(Xs)
+        if Xs.shape[1] != op.dim:
+            raise ValueError("eval_prior: dimension mismatch")
+        m = Xs.shape[0]
+    else:
+        m = op.n
+    out = np.zeros((m, S), order="F")
+    _check(lib().wgp_rff_eval(op._h, _ptr(Om), _ptr(ph), _ptr(am), F, S, sf, _ptr(Xs), m, max(m, 1),
+                              _ptr(out), max(m, 1)))
+    return out
+
+
+def build_sample_rhs(op: KernelOperator, prior: RffPrior, noise_scale: float, seed: int) -> np.ndarray:
+    """build_sample_rhs (sampling.cpp:56-64): prior at the operator's rows + host-drawn noise."""
+    rhs = rff_eval(op, [prior])[:, 0].copy()
+    if noise_scale > 0.0:
+        rhs += normal_fill(seed, rhs.size, noise_scale)
+    return rhs

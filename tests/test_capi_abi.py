@@ -1,0 +1,57 @@
+"""CPU-side checks of the product boundary: libwarmgp_b200.so loads (no GPU needed to
+load), exports every symbol include/warmgp_capi.h declares, and its host-only entry
+points (shard partition, defaults, RNG) behave like the reference."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "warmgp_capi.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(wgp_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_all_exported(W):
+    L = W.lib()
+    names = declared_symbols()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    assert set(names) == set(W.EXPORTS)
+
+
+def test_abi_version_and_defaults(W):
+    assert W.lib().wgp_abi_version() == 1
+    c = W.SolverConfig()  # solvers.hpp:27-48
+    assert (c.method, c.tolerance, c.max_iters, c.learning_rate, c.momentum) == (W.CG, 1e-2, 1000, 0.3, 0.9)
+    assert (c.batch_size, c.block_size, c.precond_rank, c.precond_shift, c.seed) == (100, 100, 100, 1e-6, 0)
+    assert (c.sgd_scaling, c.ap_ordering, c.precond_shift_mode) == (W.SGD_UNBIASED, W.AP_GREEDY, W.SHIFT_CALIBRATED)
+
+
+@pytest.mark.parametrize("n", [0, 1, 511, 512, 513, 100_000, 101_000, 500_000])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_shard_range_partition(W, n, world):
+    ranges = [W.shard_range(n, world, r) for r in range(world)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == n
+    for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
+        assert a1 == b0
+    for a, b in ranges:
+        assert a <= b and a % 512 == 0  # chunk-aligned: reductions independent of world size
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= 512 + (n % 512)
+
+
+def test_sample_prior_matches_oracle(W, O):
+    for kind in (0, 1):
+        hw = W.KernelHyperparams(0.7, 1.3, 1e-3, kind)
+        ho = O.KernelHyperparams(0.7, 1.3, 1e-3, kind)
+        a = W.sample_prior(hw, 5, 300, 42)
+        b = O.sample_prior(ho, 5, 300, 42)
+        assert np.array_equal(a.frequencies, b.frequencies)
+        assert np.array_equal(a.phases, b.phases) and np.array_equal(a.amplitudes, b.amplitudes)
+    assert np.array_equal(W.normal_fill(9, 50, 0.1), 0.1 * O.gaussian_vector(9, 50))
