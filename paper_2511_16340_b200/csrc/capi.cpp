@@ -48,14 +48,13 @@ static wgp_status guard(F&& f) {
 
 static void set_device(const Ctx& ctx) { WGP_CUDA(cudaSetDevice(ctx.device)); }
 
-template <typename T>
 static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int64_t ldb, int s,
                       const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
                       SolveOutputs& out) {
   cudaStream_t st = op.ctx->stream;
-  SolverWork<T> w;
+  SolverWork<double> w;
   w.alloc(op.n, s);
-  upload_problem<T>(op, w, B, ldb, U1, ldu, n1, st);
+  upload_problem<double>(op, w, B, ldb, U1, ldu, n1, st);
   switch (cfg.method) {
     case WGP_CG: {
       PrecondDev pd;
@@ -66,14 +65,14 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
       } else {
         pd.n = op.n;
       }
-      cg_solve_batched<T>(op, cfg, pd, w, out, st);
+      cg_solve_batched<double>(op, cfg, pd, w, out, st);
       break;
     }
     default:
       throw_error(WGP_INVALID_ARGUMENT, "solve_many: method %d not available in this build",
                   cfg.method);
   }
-  download_solution<T>(w, V, ldv, st);
+  download_solution<double>(w, V, ldv, st);
 }
 
 }  // namespace wgp
@@ -213,10 +212,7 @@ wgp_status wgp_kmatvec_dev(wgp_op* op, const void* dV, void* dY, int s, void* st
     WGP_REQUIRE(op && dV && dY && s >= 1, "wgp_kmatvec_dev: bad argument");
     WGP_REQUIRE(op->n >= 1, "wgp_kmatvec_dev: empty operator");
     cudaStream_t st = stream ? (cudaStream_t)stream : op->ctx->stream;
-    if (op->f64())
-      launch_kmatvec_full<double>(*op, (const double*)dV, (double*)dY, s, st);
-    else
-      launch_kmatvec_full<float>(*op, (const float*)dV, (float*)dY, s, st);
+    launch_kmatvec_full(*op, (const double*)dV, (double*)dY, s, st);
   });
 }
 
@@ -224,11 +220,9 @@ wgp_status wgp_residual_dev(wgp_op* op, const void* dB, const void* dV, void* dY
                             void* stream) {
   return guard([&] {
     WGP_REQUIRE(op && dB && dV && dY && s >= 1, "wgp_residual_dev: bad argument");
+    WGP_REQUIRE(op->n >= 1, "wgp_residual_dev: empty operator");
     cudaStream_t st = stream ? (cudaStream_t)stream : op->ctx->stream;
-    if (op->f64())
-      launch_residual<double>(*op, (const double*)dB, (const double*)dV, (double*)dY, s, st);
-    else
-      launch_residual<float>(*op, (const float*)dB, (const float*)dV, (float*)dY, s, st);
+    launch_residual(*op, (const double*)dB, (const double*)dV, (double*)dY, s, st);
   });
 }
 
@@ -241,22 +235,19 @@ wgp_status wgp_kmatvec(wgp_op* op, const double* V, int64_t ldv, int s, double* 
     WGP_REQUIRE(op->ctx->world == 1, "wgp_kmatvec: host form needs an unsharded context");
     set_device(*op->ctx);
     cudaStream_t st = op->ctx->stream;
-    const size_t es = op->esize();
-    op->scratch[0].ensure((size_t)n * s * sizeof(double));
-    op->scratch[1].ensure((size_t)n * s * es);
-    op->scratch[2].ensure((size_t)n * s * es);
-    double* stage_p = (double*)op->scratch[0].p;
-    struct { double* p; } stage{stage_p};
-    struct { unsigned char* p; } dV{op->scratch[1].p}, dY{op->scratch[2].p};
-    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, V, sizeof(double) * ldv,
+    const size_t bytes = (size_t)n * s * sizeof(double);
+    op->scratch[0].ensure(bytes);
+    op->scratch[1].ensure(bytes);
+    op->scratch[2].ensure(bytes);
+    double* stage = (double*)op->scratch[0].p;
+    double* dV = (double*)op->scratch[1].p;
+    double* dY = (double*)op->scratch[2].p;
+    WGP_CUDA(cudaMemcpy2DAsync(stage, sizeof(double) * n, V, sizeof(double) * ldv,
                                sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
-    launch_colmajor_to_rows(stage.p, n, n, s, dV.p, op->f64(), st);
-    if (op->f64())
-      launch_kmatvec_full<double>(*op, (const double*)dV.p, (double*)dY.p, s, st);
-    else
-      launch_kmatvec_full<float>(*op, (const float*)dV.p, (float*)dY.p, s, st);
-    launch_rows_to_colmajor(dY.p, n, s, stage.p, n, op->f64(), st);
-    WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage.p, sizeof(double) * n,
+    launch_colmajor_to_rows(stage, n, n, s, dV, true, st);
+    launch_kmatvec_full(*op, dV, dY, s, st);
+    launch_rows_to_colmajor(dY, n, s, stage, n, true, st);
+    WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage, sizeof(double) * n,
                                sizeof(double) * n, s, cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
   });
@@ -278,23 +269,26 @@ wgp_status wgp_cross_matvec(wgp_op* op, const double* Xs, int64_t m, int64_t ldx
     tmp.lengthscale = op->lengthscale;
     tmp.signal_scale = op->signal_scale;
     tmp.noise_scale = op->noise_scale;
-    tmp.precision = op->precision;
+    tmp.precision = op->precision == WGP_F64 ? WGP_F64 : WGP_F32_SIMT;
     tmp.dim = op->dim;
     tmp.dpad = op->dpad;
     op_append_rows(tmp, Xs, m, ldx, 1);
-    const size_t es = op->esize();
     DBuf<double> stage((size_t)std::max(n, m) * s);
-    DBuf<unsigned char> dW((size_t)n * s * es), dY((size_t)m * s * es);
+    DBuf<double> dW((size_t)n * s), dY((size_t)m * s);
     WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, W, sizeof(double) * ldw,
                                sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
-    launch_colmajor_to_rows(stage.p, n, n, s, dW.p, op->f64(), st);
-    if (op->f64())
-      launch_kmatvec_simt<double>(*op, tmp.X64.p, m, 0, op->X64.p, n, (const double*)dW.p, s,
-                                  nullptr, (double*)dY.p, false, st);
-    else
-      launch_kmatvec_simt<float>(*op, tmp.X32.p, m, 0, op->X32.p, n, (const float*)dW.p, s,
-                                 nullptr, (float*)dY.p, false, st);
-    launch_rows_to_colmajor(dY.p, m, s, stage.p, m, op->f64(), st);
+    launch_colmajor_to_rows(stage.p, n, n, s, dW.p, true, st);
+    if (op->f64()) {
+      launch_kmatvec_simt<double>(*op, tmp.X64.p, m, 0, op->X64.p, n, dW.p, s, nullptr, dY.p,
+                                  false, st);
+    } else {
+      if (!op->X32.p) {  // tensor-core operators keep no fp32 row copy; cross mode uses SIMT
+        throw_error(WGP_INVALID_ARGUMENT, "cross_matvec: unsupported for this precision");
+      }
+      launch_kmatvec_simt<float>(*op, tmp.X32.p, m, 0, op->X32.p, n, dW.p, s, nullptr, dY.p,
+                                 false, st);
+    }
+    launch_rows_to_colmajor(dY.p, m, s, stage.p, m, true, st);
     WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage.p, sizeof(double) * m,
                                sizeof(double) * m, s, cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
@@ -326,10 +320,7 @@ wgp_status wgp_solve_many(wgp_op* op, const wgp_solver_config* cfg, const double
     set_device(*op->ctx);
     SolveOutputs out(s);
     try {
-      if (op->f64())
-        run_solve<double>(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out);
-      else
-        run_solve<float>(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out);
+      run_solve(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out);
     } catch (Error& e) {
       fail_col = e.col;
       fail_iters = e.iterations;

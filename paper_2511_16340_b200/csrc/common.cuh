@@ -98,6 +98,12 @@ struct Op {
   DBuf<double> X64, sq64;
   DBuf<float> X32, sq32;
   DBuf<unsigned char> scratch[3];  // host-boundary staging, reused across calls
+  // tensor-core path: tiled 3xTF32 operand rows (rebuilt lazily after appends), the
+  // translation applied before forming them, and per-call V staging.
+  DBuf<float> XA, XB, vt;
+  DBuf<double> center, vchunk, ychunk;
+  std::vector<double> h_center;
+  bool tc_dirty = true;
   KParams kp() const {
     KParams p;
     p.kind = kind;
@@ -108,7 +114,7 @@ struct Op {
     return p;
   }
   bool f64() const { return precision == WGP_F64; }
-  size_t esize() const { return f64() ? sizeof(double) : sizeof(float); }
+  bool tensor() const { return precision == WGP_F32_3XTF32 || precision == WGP_TF32; }
   void local_rows(int64_t* r0, int64_t* r1) const {
     wgp_shard_range(n, ctx->world, ctx->rank, r0, r1);
   }
@@ -117,13 +123,6 @@ struct Op {
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // ------------------------------------------------------------------ launchers
-// kmatvec.cu: Y[r, :] = sum_j k(xr_r, xc_j) V[j, :] (+ noise2 V[j,:] when the global row
-// index row0 + r == j in gram mode), or Y = B - (...) in residual mode.
-template <typename T>
-void launch_kmatvec(const Op& op, const T* Xr, const T* sqr, int64_t nrows, int64_t row0,
-                    const T* Xc, const T* sqc, int64_t ncols, const T* V, int s, const T* B,
-                    T* Y, bool gram, cudaStream_t st);
-
 // vecops.cu
 void launch_colmajor_to_rows(const double* src, int64_t ld, int64_t n, int s, void* dst,
                              bool f64, cudaStream_t st);
@@ -146,7 +145,6 @@ struct PrecondDev {
   double shift = 1.0;
   DBuf<double> L;    // [n][kpad] row-major (pivoted Cholesky factor)
   DBuf<double> M64;  // [n][kpad]  M = L C^{-T}, C = chol(shift I + L^T L): M M^T = L cap^{-1} L^T
-  DBuf<float> M32;
 };
 void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStream_t st);
 void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd, cudaStream_t st);

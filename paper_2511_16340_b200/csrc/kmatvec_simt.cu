@@ -44,8 +44,8 @@ __device__ __forceinline__ float kmap<float>(float d2, const KParams& p) {
 template <typename T, int BS>
 __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
     const T* __restrict__ Xr, int64_t nrows, int64_t row0, const T* __restrict__ Xc,
-    int64_t ncols, int dpad, int dim, const T* __restrict__ V, int s, const T* __restrict__ B,
-    T* __restrict__ Y, KParams p, int gram) {
+    int64_t ncols, int dpad, int dim, const double* __restrict__ V, int s,
+    const double* __restrict__ B, double* __restrict__ Y, KParams p, int gram) {
   constexpr int CN = BS >= 64 ? 4 : (BS == 32 ? 2 : 1);
   constexpr int TXN = BS / CN;
   static_assert(16 * TXN <= NT, "bad layout");
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
     for (int e = tid; e < BN * BS; e += NT) {
       const int j = e / BS, c = e % BS;
       const int64_t gj = jb + j;
-      sV[j * BS + c] = (gj < ncols && c0 + c < s) ? V[gj * s + c0 + c] : T(0);
+      sV[j * BS + c] = (gj < ncols && c0 + c < s) ? (T)V[gj * s + c0 + c] : T(0);
     }
     __syncthreads();
     // phase 1: kernel tile
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
     for (int b = 0; b < CN; ++b) {
       const int c = c0 + tx + b * TXN;
       if (c >= s) continue;
-      const T y = acc[a][b];
+      const double y = (double)acc[a][b];
       Y[gr * s + c] = B ? B[gr * s + c] - y : y;
     }
   }
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(NT) kmatvec_simt_kernel(
 
 template <typename T, int BS>
 void launch_bs(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc, int64_t ncols,
-               const T* V, int s, const T* B, T* Y, bool gram, cudaStream_t st) {
+               const double* V, int s, const double* B, double* Y, bool gram, cudaStream_t st) {
   const int dim = op.dim;
   const size_t smem = sizeof(T) * ((size_t)(BM + BN) * (dim + 1) + BM * (BN + 1) + BN * BS);
   auto kern = kmatvec_simt_kernel<T, BS>;
@@ -158,8 +158,8 @@ void launch_bs(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* 
 
 template <typename T>
 void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
-                         int64_t ncols, const T* V, int s, const T* B, T* Y, bool gram,
-                         cudaStream_t st) {
+                         int64_t ncols, const double* V, int s, const double* B, double* Y,
+                         bool gram, cudaStream_t st) {
   if (nrows <= 0 || s <= 0) return;
   if (s <= 1) return launch_bs<T, 1>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
   if (s <= 2) return launch_bs<T, 2>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
@@ -174,7 +174,7 @@ template void launch_kmatvec_simt<double>(const Op&, const double*, int64_t, int
                                           const double*, int64_t, const double*, int,
                                           const double*, double*, bool, cudaStream_t);
 template void launch_kmatvec_simt<float>(const Op&, const float*, int64_t, int64_t, const float*,
-                                         int64_t, const float*, int, const float*, float*, bool,
+                                         int64_t, const double*, int, const double*, double*, bool,
                                          cudaStream_t);
 
 }  // namespace wgp

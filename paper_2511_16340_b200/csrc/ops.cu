@@ -78,40 +78,55 @@ void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, 
                                            op.X64.p, op.sq64.p, op.f64() ? nullptr : op.X32.p,
                                            op.f64() ? nullptr : op.sq32.p);
   WGP_CUDA(cudaGetLastError());
+  if (op.h_center.empty()) {
+    // Translation for the tensor-core operands: the mean of the first batch.  Distances
+    // are translation invariant; centering shrinks |x|^2 and with it the cancellation in
+    // |x|^2 + |y|^2 - 2 x.y.  Fixed afterwards so appended rows reuse it.
+    op.h_center.assign(op.dim, 0.0);
+    for (int64_t i = 0; i < n_new; ++i)
+      for (int k = 0; k < op.dim; ++k)
+        op.h_center[k] += col_major ? host_rows[(int64_t)k * ld + i] : host_rows[i * ld + k];
+    for (int k = 0; k < op.dim; ++k) op.h_center[k] /= (double)n_new;
+    op.center.alloc(op.dim);
+    WGP_CUDA(cudaMemcpyAsync(op.center.p, op.h_center.data(), sizeof(double) * op.dim,
+                             cudaMemcpyHostToDevice, st));
+  }
   WGP_CUDA(cudaStreamSynchronize(st));
   op.n = need;
+  op.tc_dirty = true;
 }
 
-template <typename T>
-static const T* xrows(const Op& op);
-template <>
-const double* xrows<double>(const Op& op) { return op.X64.p; }
-template <>
-const float* xrows<float>(const Op& op) { return op.X32.p; }
+static void ensure_tc_operands(Op& op, cudaStream_t st) {
+  if (!op.tc_dirty) return;
+  tc_build_operands(op, op.XA, op.XB, op.center.p, st);
+  op.tc_dirty = false;
+}
 
-// Y (this rank's rows) = H V, V full n x s.
-template <typename T>
-void launch_kmatvec_full(const Op& op, const T* V, T* Y, int s, cudaStream_t st) {
+static void dispatch(Op& op, const double* B, const double* V, double* Y, int s, cudaStream_t st) {
   int64_t r0, r1;
   op.local_rows(&r0, &r1);
-  const T* X = xrows<T>(op);
-  launch_kmatvec_simt<T>(op, X + r0 * op.dpad, r1 - r0, r0, X, op.n, V, s, nullptr, Y, true, st);
+  if (op.tensor()) {
+    ensure_tc_operands(op, st);
+    const int K1 = tc_k1(op.dim);
+    launch_kmatvec_tc(op, op.XA.p + r0 * K1, op.XB.p, r1 - r0, r0, op.n, V, s, B, Y, true, op.vt,
+                      op.vchunk, op.ychunk, st);
+  } else if (op.f64()) {
+    launch_kmatvec_simt<double>(op, op.X64.p + r0 * op.dpad, r1 - r0, r0, op.X64.p, op.n, V, s, B,
+                                Y, true, st);
+  } else {
+    launch_kmatvec_simt<float>(op, op.X32.p + r0 * op.dpad, r1 - r0, r0, op.X32.p, op.n, V, s, B,
+                               Y, true, st);
+  }
+}
+
+// Y (this rank's rows) = H V, V full n x s (fp64 row-major).
+void launch_kmatvec_full(Op& op, const double* V, double* Y, int s, cudaStream_t st) {
+  dispatch(op, nullptr, V, Y, s, st);
 }
 
 // Y = B - H V  (B and Y: this rank's rows; V full)
-template <typename T>
-void launch_residual(const Op& op, const T* B, const T* V, T* Y, int s, cudaStream_t st) {
-  int64_t r0, r1;
-  op.local_rows(&r0, &r1);
-  const T* X = xrows<T>(op);
-  launch_kmatvec_simt<T>(op, X + r0 * op.dpad, r1 - r0, r0, X, op.n, V, s, B, Y, true, st);
+void launch_residual(Op& op, const double* B, const double* V, double* Y, int s, cudaStream_t st) {
+  dispatch(op, B, V, Y, s, st);
 }
-
-template void launch_kmatvec_full<double>(const Op&, const double*, double*, int, cudaStream_t);
-template void launch_kmatvec_full<float>(const Op&, const float*, float*, int, cudaStream_t);
-template void launch_residual<double>(const Op&, const double*, const double*, double*, int,
-                                      cudaStream_t);
-template void launch_residual<float>(const Op&, const float*, const float*, float*, int,
-                                     cudaStream_t);
 
 }  // namespace wgp

@@ -335,13 +335,12 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   DBuf<double> dW((size_t)k * k);
   WGP_CUDA(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
   pd.M64.alloc((size_t)n * pd.kpad);
-  if (!op.f64()) pd.M32.alloc((size_t)n * pd.kpad);
   const size_t smem = sizeof(double) * k * k;
   if (smem > 48 * 1024)
     WGP_CUDA(cudaFuncSetAttribute(apply_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   apply_upper_kernel<<<grid_rows(n * pd.kpad), 256, smem, st>>>(
-      pd.L.p, dW.p, n, k, (int)pd.kpad, pd.M64.p, op.f64() ? nullptr : pd.M32.p);
+      pd.L.p, dW.p, n, k, (int)pd.kpad, pd.M64.p, nullptr);
   WGP_CUDA(cudaGetLastError());
   WGP_CUDA(cudaStreamSynchronize(st));  // dW / part / G are freed on return
 }
@@ -356,7 +355,7 @@ void precond_apply(const PrecondDev& pd, const T* R, T* Z, int s, double* work_t
     return;
   }
   WGP_REQUIRE((int64_t)k * s <= 256 * 64, "preconditioner: rank*s too large (%d*%d)", k, s);
-  const T* M = std::is_same<T, double>::value ? (const T*)pd.M64.p : (const T*)pd.M32.p;
+  const T* M = (const T*)pd.M64.p;  // solver vectors are fp64 for every precision
   const int nch = ceil_div(n, kChunkRows);
   const size_t smem1 = sizeof(T) * 32 * (pd.kpad + s);
   mtr_partial_kernel<T><<<nch, 256, smem1, st>>>(M, R, n, k, (int)pd.kpad, s, work_part);
@@ -372,7 +371,5 @@ void precond_apply(const PrecondDev& pd, const T* R, T* Z, int s, double* work_t
 
 template void precond_apply<double>(const PrecondDev&, const double*, double*, int, double*,
                                     double*, cudaStream_t);
-template void precond_apply<float>(const PrecondDev&, const float*, float*, int, double*, double*,
-                                   cudaStream_t);
 
 }  // namespace wgp

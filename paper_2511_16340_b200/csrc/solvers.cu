@@ -100,17 +100,16 @@ void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb
                     int64_t ldu, int64_t n1, cudaStream_t st) {
   const int64_t n = w.n;
   const int s = w.s;
-  const bool f64 = std::is_same<T, double>::value;
   // B: host column-major -> device staging (fp64 col-major) -> row-major T
   DBuf<double> stage((size_t)std::max<int64_t>(n, 1) * s);
   WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, B, sizeof(double) * ldb,
                              sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
-  launch_colmajor_to_rows(stage.p, n, n, s, w.B.p, f64, st);
+  launch_colmajor_to_rows(stage.p, n, n, s, w.B.p, true, st);
   WGP_CUDA(cudaMemsetAsync(w.V.p, 0, sizeof(T) * n * s, st));
   if (U1 && n1 > 0) {  // expand_init: [u1; 0] (solvers.cpp:43-48)
     WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n1, U1, sizeof(double) * ldu,
                                sizeof(double) * n1, s, cudaMemcpyHostToDevice, st));
-    launch_colmajor_to_rows(stage.p, n1, n1, s, w.V.p, f64, st);
+    launch_colmajor_to_rows(stage.p, n1, n1, s, w.V.p, true, st);
   }
   WGP_CUDA(cudaStreamSynchronize(st));
 }
@@ -120,14 +119,14 @@ void download_solution(SolverWork<T>& w, double* V, int64_t ldv, cudaStream_t st
   const int64_t n = w.n;
   const int s = w.s;
   DBuf<double> stage((size_t)std::max<int64_t>(n, 1) * s);
-  launch_rows_to_colmajor(w.V.p, n, s, stage.p, n, std::is_same<T, double>::value, st);
+  launch_rows_to_colmajor(w.V.p, n, s, stage.p, n, true, st);
   WGP_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * ldv, stage.p, sizeof(double) * n,
                              sizeof(double) * n, s, cudaMemcpyDeviceToHost, st));
   WGP_CUDA(cudaStreamSynchronize(st));
 }
 
 template <typename T>
-void cg_solve_batched(const Op& op, const wgp_solver_config& cfg, const PrecondDev& pd,
+void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd,
                       SolverWork<T>& w, SolveOutputs& out, cudaStream_t st) {
   const int64_t n = w.n;
   const int s = w.s;
@@ -146,7 +145,7 @@ void cg_solve_batched(const Op& op, const wgp_solver_config& cfg, const PrecondD
   launch_coldots<T>(w.B.p, w.B.p, nullptr, nullptr, n, s, w.part.p, st);
   init_bnorm_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, bnorm, active);
   // r0 = b - H v0 (solvers.cpp:150)
-  launch_residual<T>(op, w.B.p, w.V.p, w.R.p, s, st);
+  launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
   launch_coldots<T>(w.R.p, w.R.p, nullptr, nullptr, n, s, w.part.p, st);
   resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance, rel,
                                               active);
@@ -174,11 +173,11 @@ void cg_solve_batched(const Op& op, const wgp_solver_config& cfg, const PrecondD
   WGP_CUDA(cudaMemcpyAsync(fail, &int_max, sizeof(int), cudaMemcpyHostToDevice, st));
 
   for (int k = 1; k <= cfg.max_iters; ++k) {
-    launch_kmatvec_full<T>(op, w.P.p, w.HP.p, s, st);  // Hp = H p (:162)
+    launch_kmatvec_full(op, w.P.p, w.HP.p, s, st);  // Hp = H p (:162)
     launch_coldots<T>(w.P.p, w.HP.p, nullptr, nullptr, n, s, w.part.p, st);
     cg_alpha_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, alpha, fail);
     launch_axpy_cols<T>(w.V.p, w.P.p, alpha, n, s, st);  // v += alpha p (:168)
-    launch_residual<T>(op, w.B.p, w.V.p, w.R.p, s, st);  // r = b - H v (:171)
+    launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // r = b - H v (:171)
     launch_coldots<T>(w.R.p, w.R.p, nullptr, nullptr, n, s, w.part.p, st);
     resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance, rel,
                                                 active);
@@ -210,14 +209,11 @@ void cg_solve_batched(const Op& op, const wgp_solver_config& cfg, const PrecondD
   WGP_CUDA(cudaGetLastError());
 }
 
-#define WGP_INST(T)                                                                          \
-  template struct SolverWork<T>;                                                             \
-  template void upload_problem<T>(const Op&, SolverWork<T>&, const double*, int64_t,         \
-                                  const double*, int64_t, int64_t, cudaStream_t);            \
-  template void download_solution<T>(SolverWork<T>&, double*, int64_t, cudaStream_t);        \
-  template void cg_solve_batched<T>(const Op&, const wgp_solver_config&, const PrecondDev&,  \
-                                    SolverWork<T>&, SolveOutputs&, cudaStream_t);
-WGP_INST(double)
-WGP_INST(float)
+template struct SolverWork<double>;
+template void upload_problem<double>(const Op&, SolverWork<double>&, const double*, int64_t,
+                                     const double*, int64_t, int64_t, cudaStream_t);
+template void download_solution<double>(SolverWork<double>&, double*, int64_t, cudaStream_t);
+template void cg_solve_batched<double>(Op&, const wgp_solver_config&, const PrecondDev&,
+                                       SolverWork<double>&, SolveOutputs&, cudaStream_t);
 
 }  // namespace wgp

@@ -27,15 +27,22 @@ struct SolveOutputs {
                                  diverged_at(s, 0) {}
 };
 
-// Operator applications on the full row set (world = 1) or this rank's rows.
-template <typename T>
-void launch_kmatvec_full(const Op& op, const T* V, T* Y, int s, cudaStream_t st);
-template <typename T>
-void launch_residual(const Op& op, const T* B, const T* V, T* Y, int s, cudaStream_t st);
+// Operator applications on this rank's rows (all rows when world = 1).  Solver vectors are
+// fp64 for every precision; the precision selects the kernel (SIMT fp64 / SIMT fp32 /
+// tcgen05 3xTF32), which converts on the fly.
+void launch_kmatvec_full(Op& op, const double* V, double* Y, int s, cudaStream_t st);
+void launch_residual(Op& op, const double* B, const double* V, double* Y, int s, cudaStream_t st);
 template <typename T>
 void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
-                         int64_t ncols, const T* V, int s, const T* B, T* Y, bool gram,
-                         cudaStream_t st);
+                         int64_t ncols, const double* V, int s, const double* B, double* Y,
+                         bool gram, cudaStream_t st);
+void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int64_t nrows,
+                       int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
+                       double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
+                       DBuf<double>& ychunk, cudaStream_t st);
+void tc_build_operands(const Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
+                       cudaStream_t st);
+int tc_k1(int dim);
 
 template <typename T>
 void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb, const double* U1,
@@ -43,7 +50,7 @@ void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb
 template <typename T>
 void download_solution(SolverWork<T>& w, double* V, int64_t ldv, cudaStream_t st);
 template <typename T>
-void cg_solve_batched(const Op& op, const wgp_solver_config& cfg, const PrecondDev& pd,
+void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd,
                       SolverWork<T>& w, SolveOutputs& out, cudaStream_t st);
 
 }  // namespace wgp
