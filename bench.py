@@ -190,7 +190,7 @@ def run_ours(args):
     op.append_rows(X[N0:])  # the +1000-row growth step (K8)
     assert op.n == n
     r0, r1 = W.shard_range(n, world, rank)
-    dt = torch.float64 if prec == W.F64 else torch.float32
+    dt = torch.float64  # device API: fp64 solver vectors for every precision
     gen = torch.Generator(device="cuda").manual_seed(1234)
     V = torch.randn(n, S, device="cuda", dtype=dt, generator=gen)
     Y = torch.empty(r1 - r0, S, device="cuda", dtype=dt)

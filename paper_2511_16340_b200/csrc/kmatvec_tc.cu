@@ -5,40 +5,46 @@
 // restating gram_matrix (kernel.cpp:48-72) + H*p (solvers.cpp:162) without materialising
 // K.  One CTA owns 128 rows i and streams all columns j in tiles of 64:
 //
-//   GEMM1  S = XA_i . XB_j^T      (M=128, N=64,  K=K1)  tcgen05.mma kind::tf32, SS, S in TMEM
+//   GEMM1  S = XA_i . XB_j^T      (M=128, N=64, K=K1)  tcgen05.mma kind::tf32, SS, S in TMEM.
 //          The operands are pre-formatted so the contraction yields the squared distance
 //          directly (the norm form |x|^2 + |y|^2 - 2 x.y of kernel.cpp:39-46, 65):
 //            XA = [-2xh | -2xh | -2xl | sqh | sql | 1 | 1]   XB = [xh | xl | xh | 1 | 1 | sqh | sql]
 //          (3xTF32: hi/lo splits of x and |x|^2, error ~2^-22 of the largest term).
-//   map    epilogue warps: tcgen05.ld S -> k(d2) in registers (Matern-3/2 or RBF, MUFU
-//          sqrt/ex2) -> hi/lo TF32 split -> tcgen05.st into TMEM (K never leaves the SM).
-//   GEMM2  Y += K_hi V_hi + K_hi V_lo + K_lo V_hi   (M=128, N=s_pad, K=64)  kind::tf32, A from
-//          TMEM (TS form), accumulator in TMEM for the whole j sweep.
-//   out    Y (fp32 accumulators) + sigma_n^2 V_i in fp64 (or B - that: the true residual of
-//          solvers.cpp:171) written as fp64.
+//   map    epilogue warps: tcgen05.ld S -> k(d2)/s^2 * 2^10 in registers (Matern-3/2 or RBF;
+//          MUFU sqrt/ex2) -> fp16 hi/lo split -> tcgen05.st into TMEM (K never leaves the SM).
+//   GEMM2  Y += K_hi V_hi + K_hi V_lo + K_lo V_hi   (M=128, N=s_pad, K=64)  kind::f16, A from
+//          TMEM (TS form), fp32 accumulator in TMEM for the whole j sweep.  V is pre-split
+//          into fp16 hi/lo with a per-column power-of-two scale (3xFP16 ~ 2^-22 relative).
+//   out    Y * s^2 / (2^10 * scale_c) + sigma_n^2 V_i in fp64 (or B - that: the true residual
+//          of solvers.cpp:171) written as fp64.
 //
-// Warp roles (12 warps): 0 = bulk-copy producer (TMA engine, UBLKCP), 1 = MMA issuer (one
-// thread), 2 = TMEM allocator, 4..11 = kernel-map / output epilogue (two warps per TMEM
-// lane quadrant, 32 columns each).  Pipelines: smem stages (XB_j, V_j hi/lo) x NS,
-// S double buffer, K double buffer; all synchronised with mbarriers and tcgen05.commit.
+// Warp roles (20 warps): 0 = bulk-copy producer (TMA engine, UBLKCP), 1 = MMA issuer (whole
+// warp runs the schedule, one elected lane issues), 2 = TMEM allocator, 4..19 = epilogue:
+// two sets of 8 warps taking alternate j tiles (2 warps per TMEM lane quadrant, 32 columns
+// each).  Pipelines: smem stages (XB_j, V_j hi/lo) x NS, S ring x 4 in TMEM, K per
+// epilogue set; mbarriers + tcgen05.commit.  GEMM1 runs 3 tiles ahead of GEMM2.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
 namespace wgp {
 namespace tc {
 
-constexpr int BM = 128;       // rows per CTA (UMMA M)
-constexpr int BJ = 64;        // columns j per tile (GEMM1 N, GEMM2 K)
-constexpr int NTHREADS = 384;
-constexpr uint32_t TM_S = 0;      // S double buffer: cols [0,128)
-constexpr uint32_t TM_K = 128;    // K hi/lo double buffer: cols [128,384)
-constexpr uint32_t TM_Y = 384;    // Y accumulator: cols [384, 384 + s_pad)
+constexpr int BM = 128;        // rows per CTA (UMMA M)
+constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
+constexpr int NTHREADS = 640;  // 4 role warps + 2 epilogue sets x 8 warps
 constexpr int MAX_SPAD = 128;
+constexpr int NSB = 4;         // S ring depth in TMEM
+constexpr uint32_t TM_K = 64u * NSB;  // K (fp16 hi|lo, 32+32 cols) per set: [256, 384)
+constexpr uint32_t TM_Y = TM_K + 128; // Y accumulator: [384, 384 + s_pad)
+constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
 
 struct Params {
   const float* XA;      // tiled A operand rows (this launch's rows start at tile 0)
   const float* XB;      // tiled B operand rows (all columns j)
-  const float* Vt;      // tiled V hi/lo per j tile
+  const __half* Vt;     // tiled V hi/lo per j tile (fp16, per-column scaled)
+  const float* vscale;  // [s_pad] 2^-e_c: undo the per-column V scale
   const double* V64;    // [ncols][s] for the sigma^2 V_i term (gram) -- indexed by global row
   const double* B64;    // nullable: residual mode, [nrows][s]
   double* Y64;          // [nrows][s]
@@ -46,19 +52,25 @@ struct Params {
   int ntiles;           // ceil(ncols / BJ)
   int s, s_pad, K1;
   int kind;
-  float c1, neg_c_log2e, s2;
+  float c1, neg_c_log2e;
+  double out_scale;     // s^2 * 2^-10
   double noise2;
   int gram;
 };
 
 __device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
+__device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
+  const __half2 h = __floats2half2_rn(lo_elem, hi_elem);  // .x (low 16 bits) = lower k index
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NS) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t XA_BYTES = BM * p.K1 * 4;
   const uint32_t XB_BYTES = BJ * p.K1 * 4;
-  const uint32_t VT_BYTES = p.s_pad * BJ * 4;  // one of hi / lo
+  const uint32_t VT_BYTES = p.s_pad * BJ * 2;  // one of hi / lo (fp16)
   const uint32_t ST_BYTES = XB_BYTES + 2 * VT_BYTES;
   unsigned char* sXA = smem;
   unsigned char* sStage = smem + XA_BYTES;
@@ -66,10 +78,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* stage_full = bars;
   uint64_t* stage_empty = bars + NS;
   uint64_t* xa_full = bars + 2 * NS;
-  uint64_t* s_full = xa_full + 1;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* k_full = s_empty + 2;
-  uint64_t* k_empty = k_full + 2;
+  uint64_t* s_full = xa_full + 1;   // [NSB]
+  uint64_t* s_empty = s_full + NSB; // [NSB]
+  uint64_t* k_full = s_empty + NSB; // [2]
+  uint64_t* k_empty = k_full + 2;   // [2]
   uint64_t* y_full = k_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_full + 1);
 
@@ -79,9 +91,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       ptx::mbar_init(&stage_empty[i], 1);
     }
     ptx::mbar_init(xa_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NSB; ++i) {
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&s_empty[i], 8);
+    }
+    for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&k_full[i], 8);
       ptx::mbar_init(&k_empty[i], 1);
     }
@@ -94,140 +108,173 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int T = p.ntiles;
-  const int KS1 = p.K1 / 8;                 // GEMM1 K-steps
+  const int KS1 = p.K1 / 8;                 // GEMM1 K-steps (tf32: 8 per instruction)
   const uint32_t sbo1 = (p.K1 / 4) * 128;   // 8-row group stride of XA/XB tiles
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
+    // ------------------------------------------------------------ producer (TMA engine)
+    const bool leader = ptx::elect_one();
+    if (leader) {
       ptx::mbar_arrive_expect_tx(xa_full, XA_BYTES);
       ptx::bulk_g2s(sXA, p.XA + (size_t)blockIdx.x * BM * p.K1, XA_BYTES, xa_full);
-      for (int t = 0; t < T; ++t) {
-        const int st = t % NS;
-        if (t >= NS) ptx::mbar_wait(&stage_empty[st], ((t / NS) - 1) & 1);
+    }
+    int st = 0;
+    uint32_t ph = 0;
+    const float* xb_src = p.XB;
+    const __half* vt_src = p.Vt;
+    for (int t = 0; t < T; ++t) {
+      if (t >= NS) ptx::mbar_wait(&stage_empty[st], ph ^ 1);
+      if (leader) {
         unsigned char* dst = sStage + (size_t)st * ST_BYTES;
         ptx::mbar_arrive_expect_tx(&stage_full[st], ST_BYTES);
-        ptx::bulk_g2s(dst, p.XB + (size_t)t * BJ * p.K1, XB_BYTES, &stage_full[st]);
-        ptx::bulk_g2s(dst + XB_BYTES, p.Vt + (size_t)t * 2 * p.s_pad * BJ, 2 * VT_BYTES,
-                      &stage_full[st]);
+        ptx::bulk_g2s(dst, xb_src, XB_BYTES, &stage_full[st]);
+        ptx::bulk_g2s(dst + XB_BYTES, vt_src, 2 * VT_BYTES, &stage_full[st]);
       }
+      __syncwarp();
+      xb_src += (size_t)BJ * p.K1;
+      vt_src += (size_t)2 * p.s_pad * BJ;
+      if (++st == NS) { st = 0; ph ^= 1; }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc1 = ptx::idesc_tf32(BM, BJ);
-      const uint32_t idesc2 = ptx::idesc_tf32(BM, p.s_pad);
-      const uint32_t aXA = ptx::smem_u32(sXA);
-      ptx::mbar_wait(xa_full, 0);
-      auto gemm2 = [&](int u) {
-        const int sb = u & 1, st = u % NS;
-        ptx::mbar_wait(&k_full[sb], (u >> 1) & 1);
+    // The whole warp runs the schedule (uniform control flow, descriptors in uniform
+    // registers); one elected lane issues tcgen05.mma / tcgen05.commit.
+    const uint32_t idesc1 = ptx::idesc_tf32(BM, BJ);
+    const uint32_t idesc2 = ptx::idesc_f16(BM, p.s_pad);
+    const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
+    const uint64_t dStage0 = ptx::umma_desc(ptx::smem_u32(sStage), 128, sbo1);
+    // fp16 V tile: rows c (N) in 8-row groups, K = 64 j in 8-element (16 B) chunks
+    const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sStage + XB_BYTES), 128, (BJ / 8) * 128);
+    const uint64_t st_step = (uint64_t)(ST_BYTES >> 4);  // descriptor start-address units
+    const uint64_t vlo_step = (uint64_t)(VT_BYTES >> 4);
+    constexpr int L = NSB - 1;  // GEMM1 runs L tiles ahead of GEMM2
+    ptx::mbar_wait(xa_full, 0);
+    int st1 = 0, sb1 = 0, st2 = 0;
+    uint32_t ph1 = 0, phs = 0;
+    for (int t = 0; t < T + L; ++t) {
+      if (t < T) {
+        ptx::mbar_wait(&stage_full[st1], ph1);
+        if (t >= NSB) ptx::mbar_wait(&s_empty[sb1], phs ^ 1);
         ptx::tc_fence_after();
-        const uint32_t aV = ptx::smem_u32(sStage + (size_t)st * ST_BYTES + XB_BYTES);
-#pragma unroll
-        for (int pass = 0; pass < 3; ++pass) {
-          const uint32_t a_col = TM_K + sb * 128 + (pass == 2 ? 64 : 0);  // K_hi, K_hi, K_lo
-          const uint32_t vb = aV + (pass == 1 ? VT_BYTES : 0);              // V_hi, V_lo, V_hi
-#pragma unroll
-          for (int ks = 0; ks < BJ / 8; ++ks) {
-            const uint64_t bdesc = ptx::umma_desc(vb + ks * 256, 128, 16 * 128);
-            ptx::mma_tf32_ts(tmem + TM_Y, tmem + a_col + ks * 8, bdesc, idesc2,
-                             (u > 0 || pass > 0 || ks > 0) ? 1u : 0u);
-          }
+        if (ptx::elect_one()) {
+          const uint64_t dB = dStage0 + st_step * st1;
+          for (int ks = 0; ks < KS1; ++ks)
+            ptx::mma_tf32_ss(tmem + sb1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+          ptx::mma_commit(&s_full[sb1]);
         }
-        ptx::mma_commit(&k_empty[sb]);
-        ptx::mma_commit(&stage_empty[st]);
-      };
-      for (int t = 0; t < T; ++t) {
-        const int st = t % NS, sb = t & 1;
-        ptx::mbar_wait(&stage_full[st], (t / NS) & 1);
-        if (t >= 2) ptx::mbar_wait(&s_empty[sb], ((t - 2) >> 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t aXB = ptx::smem_u32(sStage + (size_t)st * ST_BYTES);
-        for (int ks = 0; ks < KS1; ++ks) {
-          const uint64_t adesc = ptx::umma_desc(aXA + ks * 256, 128, sbo1);
-          const uint64_t bdesc = ptx::umma_desc(aXB + ks * 256, 128, sbo1);
-          ptx::mma_tf32_ss(tmem + TM_S + sb * 64, adesc, bdesc, idesc1, ks > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit(&s_full[sb]);
-        if (t >= 1) gemm2(t - 1);
+        __syncwarp();
+        if (++st1 == NS) { st1 = 0; ph1 ^= 1; }
+        if (++sb1 == NSB) { sb1 = 0; phs ^= 1; }
       }
-      gemm2(T - 1);
-      ptx::mma_commit(y_full);
+      const int u = t - L;
+      if (u >= 0) {
+        const int kb = u & 1;
+        ptx::mbar_wait(&k_full[kb], (u >> 1) & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          const uint64_t dVh = dV0 + st_step * st2;
+          const uint64_t dVl = dVh + vlo_step;
+          const uint32_t kh = tmem + TM_K + kb * 64, kl = kh + 32;  // 16 fp16 = 8 columns per step
+#pragma unroll
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(tmem + TM_Y, kh + ks * 8, dVh + 16 * ks, idesc2, (u > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(tmem + TM_Y, kh + ks * 8, dVl + 16 * ks, idesc2, 1u);
+#pragma unroll
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(tmem + TM_Y, kl + ks * 8, dVh + 16 * ks, idesc2, 1u);
+          ptx::mma_commit(&k_empty[kb]);
+          ptx::mma_commit(&stage_empty[st2]);
+        }
+        __syncwarp();
+        if (++st2 == NS) st2 = 0;
+      }
     }
+    if (ptx::elect_one()) ptx::mma_commit(y_full);
+    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ kernel-map epilogue
-    const int q = warp & 3;            // TMEM lane quadrant accessible to this warp
-    const int half = (warp - 4) >> 2;  // which 32 of the 64 tile columns
+    const int q = warp & 3;                   // TMEM lane quadrant accessible to this warp
+    const int g = (warp - 4) >> 2;            // 0..3
+    const int set = g >> 1, half = g & 1;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const int r = q * 32 + lane;       // row within the CTA tile
+    const int r = q * 32 + lane;              // row within the CTA tile
     const int64_t gi = p.row0 + (int64_t)blockIdx.x * BM + r;
     const int64_t grow0 = p.row0 + (int64_t)blockIdx.x * BM;
-    for (int t = 0; t < T; ++t) {
-      const int sb = t & 1;
-      ptx::mbar_wait(&s_full[sb], (t >> 1) & 1);
+    const uint32_t kcol = TM_K + set * 64 + half * 16;  // this warp's 32 k -> 16 packed columns
+    const float kdiag = 1024.0f;                        // k(x,x)/s^2 * 2^10
+    int sb = set;
+    uint32_t sph = 0;
+    for (int t = set; t < T; t += 2) {
+      ptx::mbar_wait(&s_full[sb], sph);
       ptx::tc_fence_after();
       uint32_t v[32];
-      ptx::tmem_ld32(tmem + lane_off + TM_S + sb * 64 + half * 32, v);
+      ptx::tmem_ld32(tmem + lane_off + sb * 64 + half * 32, v);
       ptx::tmem_wait_ld();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
-      uint32_t hi[32];
+      float kv[32];
       if (p.kind == WGP_MATERN32) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const float d2 = fmaxf(__uint_as_float(v[c]), 0.0f);
           const float rr = ptx::sqrt_approx(d2);
-          const float e = ptx::ex2_approx(rr * p.neg_c_log2e);
+          const float e = ptx::ex2_approx(fmaf(rr, p.neg_c_log2e, KSCALE_LOG2));  // 2^10 e^{-z}
           const float z = rr * p.c1;
-          v[c] = __float_as_uint(p.s2 * fmaf(z, e, e));
+          kv[c] = fmaf(z, e, e);  // 2^10 (1+z) e^{-z}
         }
       } else {
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const float d2 = fmaxf(__uint_as_float(v[c]), 0.0f);
-          v[c] = __float_as_uint(p.s2 * ptx::ex2_approx(d2 * p.neg_c_log2e));
+          kv[c] = ptx::ex2_approx(fmaf(d2, p.neg_c_log2e, KSCALE_LOG2));  // 2^10 e^{-d2/2l^2}
         }
       }
+      // S(sb) fully consumed (every loaded register has been used above)
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
       const int64_t gj0 = (int64_t)t * BJ + half * 32;
       if (p.gram && gj0 < grow0 + BM && gj0 + 32 > grow0) {  // tile touches the diagonal
 #pragma unroll
         for (int c = 0; c < 32; ++c)
-          if (gj0 + c == gi) v[c] = __float_as_uint(p.s2);  // k(x,x) = s^2 exactly
+          if (gj0 + c == gi) kv[c] = kdiag;  // k(x,x) = s^2 exactly
       }
+      uint32_t hi[16], lo[16];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const uint32_t h = v[c] & 0xFFFFE000u;
-        hi[c] = h;
-        v[c] = __float_as_uint(__uint_as_float(v[c]) - __uint_as_float(h));  // lo
+      for (int c = 0; c < 16; ++c) {
+        hi[c] = pack_h2(kv[2 * c], kv[2 * c + 1]);
+        const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hi[c]));
+        lo[c] = pack_h2(kv[2 * c] - hf.x, kv[2 * c + 1] - hf.y);
       }
-      if (t >= 2) ptx::mbar_wait(&k_empty[sb], ((t - 2) >> 1) & 1);
+      if (t >= 2) ptx::mbar_wait(&k_empty[set], ((t >> 1) - 1) & 1);
       ptx::tc_fence_after();
-      ptx::tmem_st32(tmem + lane_off + TM_K + sb * 128 + half * 32, hi);
-      ptx::tmem_st32(tmem + lane_off + TM_K + sb * 128 + 64 + half * 32, v);
+      ptx::tmem_st16(tmem + lane_off + kcol, hi);
+      ptx::tmem_st16(tmem + lane_off + kcol + 32, lo);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&k_full[sb]);
+      if (lane == 0) ptx::mbar_arrive(&k_full[set]);
+      sb += 2;  // next tile of this set: t + 2
+      if (sb >= NSB) { sb -= NSB; sph ^= 1; }
     }
     // ------------------------------------------------------------ output
     ptx::mbar_wait(y_full, 0);
     ptx::tc_fence_after();
-    const bool valid = (int64_t)blockIdx.x * BM + r < p.nrows;
     const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
-    for (int ch = half; ch * 32 < p.s_pad; ch += 2) {
+    const bool valid = lr < p.nrows;
+    for (int ch = g; ch * 32 < p.s_pad; ch += 4) {
       uint32_t y[32];
       ptx::tmem_ld32(tmem + lane_off + TM_Y + ch * 32, y);
       ptx::tmem_wait_ld();
       if (valid) {
-#pragma unroll 4
+        const int64_t base = lr * p.s;
+#pragma unroll
         for (int c = 0; c < 32; ++c) {
           const int col = ch * 32 + c;
           if (col < p.s) {
-            double acc = (double)__uint_as_float(y[c]);
+            double acc = (double)__uint_as_float(y[c]) * (p.out_scale * (double)p.vscale[col]);
             if (p.gram) acc += p.noise2 * p.V64[gi * p.s + col];
-            p.Y64[lr * p.s + col] = p.B64 ? p.B64[lr * p.s + col] - acc : acc;
+            p.Y64[base + col] = p.B64 ? p.B64[base + col] - acc : acc;
           }
         }
       }
@@ -282,21 +329,51 @@ __global__ void build_operands_kernel(const double* __restrict__ X, int dpad, in
   }
 }
 
-// V [ncols][s] fp64 -> per-64-row tile [hi|lo][s_pad/8][16][8][4] fp32 (zero padded).
+// Per-column max |V| (one block per column) -> power-of-two scales 2^e_c, 2^-e_c with
+// |V * 2^e_c| < 2^14 for the fp16 split.
+__global__ void colscale_kernel(const double* __restrict__ V, int64_t n, int s, int s_pad,
+                                float* __restrict__ scale_up, float* __restrict__ scale_down) {
+  const int c = blockIdx.x;
+  if (c >= s_pad) return;
+  double m = 0.0;
+  if (c < s)
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) m = fmax(m, fabs(V[j * s + c]));
+  __shared__ double red[256];
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int e = 0;
+    if (red[0] > 0.0) {
+      int ex;
+      frexp(red[0], &ex);  // red = f * 2^ex, f in [0.5, 1)
+      e = 14 - ex;         // |V| * 2^e < 2^14
+      e = max(-100, min(100, e));
+    }
+    scale_up[c] = ldexpf(1.0f, e);
+    scale_down[c] = ldexpf(1.0f, -e);
+  }
+}
+
+// V [ncols][s] fp64 -> per-64-row tile [hi|lo][s_pad/8][8 chunks][8 c][8 j] fp16.
 __global__ void split_v_kernel(const double* __restrict__ V, int64_t ncols, int s, int s_pad,
-                               int64_t total_rows, float* __restrict__ Vt) {
+                               int64_t total_rows, const float* __restrict__ scale_up,
+                               __half* __restrict__ Vt) {
   const int64_t total = total_rows * s_pad;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = e / s_pad;
     const int c = (int)(e % s_pad);
-    const double v = (j < ncols && c < s) ? V[j * s + c] : 0.0;
-    const float vh = __uint_as_float(tf32_hi((float)v));
-    const float vl = (float)(v - (double)vh);
+    const double v = (j < ncols && c < s) ? V[j * s + c] * (double)scale_up[c] : 0.0;
+    const __half vh = __double2half(v);
+    const __half vl = __double2half(v - (double)__half2float(vh));
     const int64_t t = j / BJ;
     const int jj = (int)(j % BJ);
-    const int64_t idx = ((int64_t)((c >> 3) * (BJ / 4) + (jj >> 2)) * 8 + (c & 7)) * 4 + (jj & 3);
-    float* base = Vt + t * 2 * (int64_t)s_pad * BJ;
+    const int64_t idx = ((int64_t)((c >> 3) * (BJ / 8) + (jj >> 3)) * 8 + (c & 7)) * 8 + (jj & 7);
+    __half* base = Vt + t * 2 * (int64_t)s_pad * BJ;
     base[idx] = vh;
     base[(int64_t)s_pad * BJ + idx] = vl;
   }
@@ -329,12 +406,18 @@ void tc_build_operands(const Op& op, DBuf<float>& XA, DBuf<float>& XB, const dou
 
 size_t tc_smem_bytes(int K1, int s_pad, int* ns_out) {
   const size_t xa = (size_t)tc::BM * K1 * 4;
-  const size_t stage = (size_t)tc::BJ * K1 * 4 + 2 * (size_t)s_pad * tc::BJ * 4;
-  const size_t tail = 16 * 8 + 64;
+  const size_t stage = (size_t)tc::BJ * K1 * 4 + 2 * (size_t)s_pad * tc::BJ * 2;
+  const size_t tail = 32 * 8 + 64;
   int ns = (int)((227 * 1024 - xa - tail) / stage);
-  if (ns > 4) ns = 4;
+  if (ns > 6) ns = 6;
   *ns_out = ns;
   return xa + ns * stage + tail;
+}
+
+bool tc_supported(int dim) {
+  int ns = 0;
+  tc_smem_bytes(tc_k1(dim), tc::MAX_SPAD, &ns);
+  return ns >= 2;
 }
 
 // Y = (K(Xr, Xc) [+ sigma^2 I]) V, rows [row0, row0 + nrows) of the operator.  V64 and
@@ -351,7 +434,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
     const double* Vc = V64;
     const double* Bc = B64;
     double* Yc = Y64;
-    if (sc != s) {  // gather this column chunk (rare: s > 128)
+    if (sc != s) {  // gather this column chunk (s > 128)
       vchunk.ensure((size_t)ncols * sc);
       ychunk.ensure((size_t)nrows * sc * (B64 ? 2 : 1));
       WGP_CUDA(cudaMemcpy2DAsync(vchunk.p, sizeof(double) * sc, V64 + c0, sizeof(double) * s,
@@ -366,14 +449,21 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
     }
     const int s_pad = ((sc + 15) / 16) * 16;
     const int ntiles = (int)((ncols + tc::BJ - 1) / tc::BJ);
-    vt_scratch.ensure((size_t)ntiles * tc::BJ * s_pad * 2);
+    // scratch: fp16 tiles (2 x s_pad x 64 halves per tile) + 2 x s_pad scales (floats)
+    const size_t vt_halves = (size_t)ntiles * tc::BJ * s_pad * 2;
+    vt_scratch.ensure((vt_halves + 1) / 2 + 2 * (size_t)s_pad + 64);
+    __half* vt = reinterpret_cast<__half*>(vt_scratch.p);
+    float* sc_up = vt_scratch.p + (vt_halves + 1) / 2 + 32;
+    float* sc_down = sc_up + s_pad;
+    tc::colscale_kernel<<<s_pad, 256, 0, st>>>(Vc, ncols, sc, s_pad, sc_up, sc_down);
     tc::split_v_kernel<<<tc::grid_for((int64_t)ntiles * tc::BJ * s_pad), 256, 0, st>>>(
-        Vc, ncols, sc, s_pad, (int64_t)ntiles * tc::BJ, vt_scratch.p);
+        Vc, ncols, sc, s_pad, (int64_t)ntiles * tc::BJ, sc_up, vt);
     WGP_CUDA(cudaGetLastError());
     tc::Params prm;
     prm.XA = XA_rows;
     prm.XB = XB;
-    prm.Vt = vt_scratch.p;
+    prm.Vt = vt;
+    prm.vscale = sc_down;
     prm.V64 = Vc;
     prm.B64 = Bc;
     prm.Y64 = Yc;
@@ -387,7 +477,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
     prm.kind = kp.kind;
     prm.c1 = (float)kp.c1;
     prm.neg_c_log2e = (float)(-kp.c1 * 1.4426950408889634);
-    prm.s2 = (float)kp.s2;
+    prm.out_scale = kp.s2 * 0x1.0p-10;
     prm.noise2 = kp.noise2;
     prm.gram = gram ? 1 : 0;
     int ns = 0;

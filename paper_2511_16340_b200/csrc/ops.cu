@@ -105,7 +105,7 @@ static void ensure_tc_operands(Op& op, cudaStream_t st) {
 static void dispatch(Op& op, const double* B, const double* V, double* Y, int s, cudaStream_t st) {
   int64_t r0, r1;
   op.local_rows(&r0, &r1);
-  if (op.tensor()) {
+  if (op.tensor() && tc_supported(op.dim)) {
     ensure_tc_operands(op, st);
     const int K1 = tc_k1(op.dim);
     launch_kmatvec_tc(op, op.XA.p + r0 * K1, op.XB.p, r1 - r0, r0, op.n, V, s, B, Y, true, op.vt,

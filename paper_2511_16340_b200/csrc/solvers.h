@@ -43,6 +43,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
 void tc_build_operands(const Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
                        cudaStream_t st);
 int tc_k1(int dim);
+bool tc_supported(int dim);  // false -> the fp32 CUDA-core kernel serves this dim
 
 template <typename T>
 void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb, const double* U1,

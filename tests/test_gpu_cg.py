@@ -36,19 +36,36 @@ def test_cg_c1_reduced_golden(W):
         assert np.linalg.norm(res.v - ref_v) <= 1e-3 * np.linalg.norm(ref_v)
 
 
-def test_cg_f32_path_vs_oracle(W, O):
-    """fp32 path at the fp32 configs' tolerance (1e-4): iteration counts within +-2%."""
+def test_cg_f32_path_vs_oracle_ensemble(W, O):
+    """fp32/3xTF32 path on the ill-conditioned config-1 system at tol 1e-4: the iteration
+    count must lie in the band the oracle itself spans when its matvec carries 1e-6
+    relative noise (a 1e-9 perturbation already moves it by one here)."""
+    from cg_ensemble import iteration_band
     g = np.load(os.path.join(HERE, "golden", "cg_c1_reduced.npz"))
     h = O.KernelHyperparams(0.5, 1.0, 0.1, O.RBF)
     H = O.gram_matrix(g["X"], h)
-    ocfg = O.SolverConfig(tolerance=1e-4, precond_rank=100, precond_shift=0.01)
+    pre = O.CgPreconditioner.from_matrix(H, 100, 0.01)
     op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.1, W.RBF), g["X"], precision=W.F32_3XTF32)
     cfg = W.SolverConfig(tolerance=1e-4, precond_rank=100, precond_shift=0.01)
-    for init_o, init_w in ((O.Initialization.cold(), W.Initialization.cold()),
-                           (O.Initialization.warm(g["u1"]), W.Initialization.warm(g["u1"]))):
-        ref = O.cg_solve(H, g["y"], init_o, ocfg)
-        got = W.solve(op, g["y"], init_w, cfg)
-        assert got.converged and iters_close(got.iterations, ref.iterations), (got.iterations, ref.iterations)
+    w0 = np.concatenate([g["u1"], np.zeros(20)])
+    for v0, init in ((np.zeros(400), W.Initialization.cold()), (w0, W.Initialization.warm(g["u1"]))):
+        lo, hi = iteration_band(H, pre, g["y"], v0, 1e-4)
+        got = W.solve(op, g["y"], init, cfg)
+        assert got.converged and lo - 1 <= got.iterations <= hi + 1, (got.iterations, lo, hi)
+
+
+@pytest.mark.parametrize("kind,ls,sn,rank", [(0, 1.0, 0.5, 100), (1, 0.7, 0.3, 50)])
+def test_cg_f32_path_well_conditioned(W, O, kind, ls, sn, rank):
+    """Where the oracle's count is stable under 1e-6 matvec noise (checked in cg_ensemble),
+    the fp32 path matches it within +-2%."""
+    h = O.KernelHyperparams(ls, 1.0, sn, kind)
+    X = O.uniform_inputs(41, 3000, 4)
+    b = O.gaussian_vector(42, 3000)
+    H = O.gram_matrix(X, h)
+    ref = O.cg_solve(H, b, O.Initialization.cold(), O.SolverConfig(tolerance=1e-4, precond_rank=rank, precond_shift=sn * sn))
+    op = W.KernelOperator(W.KernelHyperparams(ls, 1.0, sn, kind), X, precision=W.F32_3XTF32)
+    got = W.solve(op, b, W.Initialization.cold(), W.SolverConfig(tolerance=1e-4, precond_rank=rank, precond_shift=sn * sn))
+    assert got.converged and iters_close(got.iterations, ref.iterations), (got.iterations, ref.iterations)
 
 
 @pytest.mark.parametrize("precision", [0, 1])
@@ -64,8 +81,15 @@ def test_cg_multi_rhs_vs_oracle(W, O, precision):
     op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.5, 0), X, precision=precision)
     wcfg = W.SolverConfig(tolerance=tol, precond_rank=20, precond_shift=0.25, max_iters=500)
     got = W.solve_many(op, B, [W.Initialization.cold()] * 9, wcfg)
-    for r, g in zip(ref, got):
-        assert iters_close(r.iterations, g.iterations), (r.iterations, g.iterations)
+    if precision != 0:
+        from cg_ensemble import iteration_band
+        pre = O.CgPreconditioner.from_matrix(H, 20, 0.25)
+    for c, (r, g) in enumerate(zip(ref, got)):
+        if precision == 0 or c == 4:
+            assert iters_close(r.iterations, g.iterations), (r.iterations, g.iterations)
+        else:  # fp32 matvec: within the oracle's own 1e-6-noise band (cg_ensemble.py)
+            lo, hi = iteration_band(H, pre, B[:, c], np.zeros(600), tol, trials=6)
+            assert lo - 1 <= g.iterations <= hi + 1, (c, g.iterations, lo, hi)
         assert g.converged == r.converged
         assert len(g.residual_history) == g.iterations + 1
     assert got[4].iterations == 0 and got[4].residual_history == [0.0] and not got[4].v.any()
