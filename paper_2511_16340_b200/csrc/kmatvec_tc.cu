@@ -18,12 +18,16 @@
 //   out    Y * s^2 / (2^10 * scale_c) + sigma_n^2 V_i in fp64 (or B - that: the true residual
 //          of solvers.cpp:171) written as fp64.
 //
-// Warp roles (20 warps): 0 = bulk-copy producer (TMA engine, UBLKCP), 1 = MMA issuer (whole
-// warp runs the schedule, one elected lane issues), 2 = TMEM allocator, 4..19 = epilogue:
+// Warp roles (20 warps): 0 = bulk-copy producer (TMA engine, UBLKCP), 1 = GEMM1 issuer,
+// 3 = GEMM2 issuer (whole warps run the schedules, one elected lane issues), 2 = TMEM
+// allocator, 4..19 = epilogue:
 // two sets of 8 warps taking alternate j tiles (2 warps per TMEM lane quadrant, 32 columns
-// each).  Pipelines: smem stages (XB_j, V_j hi/lo) x NS, S ring x 4 in TMEM, K per
-// epilogue set; mbarriers + tcgen05.commit.  GEMM1 runs 3 tiles ahead of GEMM2.
+// each).  Pipelines: smem stages (XB_j, V_j hi/lo) x NS; a ring of 6-7 TMEM tile buffers
+// (S written by GEMM1, overwritten in place by K for GEMM2); mbarriers + tcgen05.commit.
 #include <cuda_fp16.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -35,9 +39,12 @@ constexpr int BM = 128;        // rows per CTA (UMMA M)
 constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
 constexpr int NTHREADS = 640;  // 4 role warps + 2 epilogue sets x 8 warps
 constexpr int MAX_SPAD = 128;
-constexpr int NSB = 4;         // S ring depth in TMEM
-constexpr uint32_t TM_K = 64u * NSB;  // K (fp16 hi|lo, 32+32 cols) per set: [256, 384)
-constexpr uint32_t TM_Y = TM_K + 128; // Y accumulator: [384, 384 + s_pad)
+// TMEM: a ring of NB 64-column tile buffers followed by the Y accumulator.  A buffer holds
+// S(t) (fp32 d^2, written by GEMM1); the epilogue loads it into registers and writes K(t)
+// back in place as packed fp16 (each warp into the 32 columns it read: 16 hi + 16 lo), which
+// GEMM2 then reads as its A operand; GEMM2's commit frees the buffer for GEMM1 of tile
+// t + NB.  NB = (512 - s_pad_alloc) / 64: 7 for s_pad <= 64, 6 for s_pad <= 128.
+constexpr int MAX_NB = 7;
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
 
 struct Params {
@@ -56,7 +63,12 @@ struct Params {
   double out_scale;     // s^2 * 2^-10
   double noise2;
   int gram;
+  unsigned long long* trace;  // debug: per-tile event clocks of CTA 0 (nullptr normally)
 };
+
+__device__ __forceinline__ void trace_ev(const Params& p, int t, int slot) {
+  if (p.trace && blockIdx.x == 0) p.trace[(size_t)t * 8 + slot] = clock64();
+}
 
 __device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
 
@@ -78,12 +90,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* stage_full = bars;
   uint64_t* stage_empty = bars + NS;
   uint64_t* xa_full = bars + 2 * NS;
-  uint64_t* s_full = xa_full + 1;   // [NSB]
-  uint64_t* s_empty = s_full + NSB; // [NSB]
-  uint64_t* k_full = s_empty + NSB; // [2]
-  uint64_t* k_empty = k_full + 2;   // [2]
-  uint64_t* y_full = k_empty + 2;
+  uint64_t* s_full = xa_full + 1;        // [MAX_NB] GEMM1 -> epilogue
+  uint64_t* k_full = s_full + MAX_NB;    // [MAX_NB] epilogue -> GEMM2 (8 arrivals)
+  uint64_t* b_free = k_full + MAX_NB;    // [MAX_NB] GEMM2 -> GEMM1
+  uint64_t* y_full = b_free + MAX_NB;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_full + 1);
+  const int s_alloc = p.s_pad <= 64 ? 64 : 128;
+  const int NB = (512 - s_alloc) / 64;
+  const uint32_t TM_Y = 512u - (uint32_t)s_alloc;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -91,13 +105,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       ptx::mbar_init(&stage_empty[i], 1);
     }
     ptx::mbar_init(xa_full, 1);
-    for (int i = 0; i < NSB; ++i) {
+    for (int i = 0; i < MAX_NB; ++i) {
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&s_empty[i], 8);
-    }
-    for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&k_full[i], 8);
-      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&b_free[i], 1);
     }
     ptx::mbar_init(y_full, 1);
     ptx::fence_mbar_init();
@@ -125,6 +136,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     for (int t = 0; t < T; ++t) {
       if (t >= NS) ptx::mbar_wait(&stage_empty[st], ph ^ 1);
       if (leader) {
+        trace_ev(p, t, 6);
         unsigned char* dst = sStage + (size_t)st * ST_BYTES;
         ptx::mbar_arrive_expect_tx(&stage_full[st], ST_BYTES);
         ptx::bulk_g2s(dst, xb_src, XB_BYTES, &stage_full[st]);
@@ -135,64 +147,76 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       vt_src += (size_t)2 * p.s_pad * BJ;
       if (++st == NS) { st = 0; ph ^= 1; }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    // The whole warp runs the schedule (uniform control flow, descriptors in uniform
-    // registers); one elected lane issues tcgen05.mma / tcgen05.commit.
-    const uint32_t idesc1 = ptx::idesc_tf32(BM, BJ);
-    const uint32_t idesc2 = ptx::idesc_f16(BM, p.s_pad);
-    const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
-    const uint64_t dStage0 = ptx::umma_desc(ptx::smem_u32(sStage), 128, sbo1);
-    // fp16 V tile: rows c (N) in 8-row groups, K = 64 j in 8-element (16 B) chunks
-    const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sStage + XB_BYTES), 128, (BJ / 8) * 128);
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------------ MMA issuers
+    // tcgen05.mma issue blocks for about the instruction's execution time, so one thread
+    // cannot keep two dependent streams fed.  Warp 1 issues GEMM1 (distance tiles) and warp 3
+    // issues GEMM2 (K.V); each waits only on its own inputs and each tcgen05.commit tracks
+    // its own thread's MMAs.  Whole warps run the schedule (uniform control flow,
+    // descriptors in uniform registers); one elected lane issues.
     const uint64_t st_step = (uint64_t)(ST_BYTES >> 4);  // descriptor start-address units
-    const uint64_t vlo_step = (uint64_t)(VT_BYTES >> 4);
-    constexpr int L = NSB - 1;  // GEMM1 runs L tiles ahead of GEMM2
-    ptx::mbar_wait(xa_full, 0);
-    int st1 = 0, sb1 = 0, st2 = 0;
-    uint32_t ph1 = 0, phs = 0;
-    for (int t = 0; t < T + L; ++t) {
-      if (t < T) {
+    if (warp == 1) {
+      const uint32_t idesc1 = ptx::idesc_tf32(BM, BJ);
+      const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
+      const uint64_t dStage0 = ptx::umma_desc(ptx::smem_u32(sStage), 128, sbo1);
+      ptx::mbar_wait(xa_full, 0);
+      int st1 = 0, b1 = 0;
+      uint32_t ph1 = 0, phb1 = 0;
+      for (int t = 0; t < T; ++t) {
         ptx::mbar_wait(&stage_full[st1], ph1);
-        if (t >= NSB) ptx::mbar_wait(&s_empty[sb1], phs ^ 1);
+        if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
+          trace_ev(p, t, 0);
           const uint64_t dB = dStage0 + st_step * st1;
           for (int ks = 0; ks < KS1; ++ks)
-            ptx::mma_tf32_ss(tmem + sb1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
-          ptx::mma_commit(&s_full[sb1]);
+            ptx::mma_tf32_ss(tmem + b1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+          ptx::mma_commit(&s_full[b1]);
         }
         __syncwarp();
         if (++st1 == NS) { st1 = 0; ph1 ^= 1; }
-        if (++sb1 == NSB) { sb1 = 0; phs ^= 1; }
+        if (++b1 == NB) { b1 = 0; phb1 ^= 1; }
       }
-      const int u = t - L;
-      if (u >= 0) {
-        const int kb = u & 1;
-        ptx::mbar_wait(&k_full[kb], (u >> 1) & 1);
+    } else {
+      const uint32_t idesc2 = ptx::idesc_f16(BM, p.s_pad);
+      // fp16 V tile: rows c (N) in 8-row groups, K = 64 j in 8-element (16 B) chunks
+      const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sStage + XB_BYTES), 128, (BJ / 8) * 128);
+      const uint64_t vlo_step = (uint64_t)(VT_BYTES >> 4);
+      int st2 = 0, b2 = 0;
+      uint32_t phb2 = 0;
+      for (int t = 0; t < T; ++t) {
+        ptx::mbar_wait(&k_full[b2], phb2);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
+          trace_ev(p, t, 1);
           const uint64_t dVh = dV0 + st_step * st2;
           const uint64_t dVl = dVh + vlo_step;
-          const uint32_t kh = tmem + TM_K + kb * 64, kl = kh + 32;  // 16 fp16 = 8 columns per step
+          // K layout in the buffer: [hi j0-31 | lo j0-31 | hi j32-63 | lo j32-63], 16 cols each
+          const uint32_t kb = tmem + b2 * 64;
 #pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks)
-            ptx::mma_f16_ts(tmem + TM_Y, kh + ks * 8, dVh + 16 * ks, idesc2, (u > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < BJ / 16; ++ks) {
+            const uint32_t hcol = kb + (ks >> 1) * 32 + (ks & 1) * 8;
+            ptx::mma_f16_ts(tmem + TM_Y, hcol, dVh + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
+          }
 #pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks)
-            ptx::mma_f16_ts(tmem + TM_Y, kh + ks * 8, dVl + 16 * ks, idesc2, 1u);
+          for (int ks = 0; ks < BJ / 16; ++ks) {
+            const uint32_t hcol = kb + (ks >> 1) * 32 + (ks & 1) * 8;
+            ptx::mma_f16_ts(tmem + TM_Y, hcol, dVl + 16 * ks, idesc2, 1u);
+          }
 #pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks)
-            ptx::mma_f16_ts(tmem + TM_Y, kl + ks * 8, dVh + 16 * ks, idesc2, 1u);
-          ptx::mma_commit(&k_empty[kb]);
+          for (int ks = 0; ks < BJ / 16; ++ks) {
+            const uint32_t lcol = kb + (ks >> 1) * 32 + 16 + (ks & 1) * 8;
+            ptx::mma_f16_ts(tmem + TM_Y, lcol, dVh + 16 * ks, idesc2, 1u);
+          }
+          ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&stage_empty[st2]);
+          if (t == T - 1) ptx::mma_commit(y_full);
         }
         __syncwarp();
         if (++st2 == NS) st2 = 0;
+        if (++b2 == NB) { b2 = 0; phb2 ^= 1; }
       }
     }
-    if (ptx::elect_one()) ptx::mma_commit(y_full);
-    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ kernel-map epilogue
     const int q = warp & 3;                   // TMEM lane quadrant accessible to this warp
@@ -202,15 +226,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     const int r = q * 32 + lane;              // row within the CTA tile
     const int64_t gi = p.row0 + (int64_t)blockIdx.x * BM + r;
     const int64_t grow0 = p.row0 + (int64_t)blockIdx.x * BM;
-    const uint32_t kcol = TM_K + set * 64 + half * 16;  // this warp's 32 k -> 16 packed columns
-    const float kdiag = 1024.0f;                        // k(x,x)/s^2 * 2^10
-    int sb = set;
-    uint32_t sph = 0;
+    const float kdiag = 1024.0f;              // k(x,x)/s^2 * 2^10
+    int b = set;                              // buffer of tile t = t % NB
+    uint32_t bph = 0;
     for (int t = set; t < T; t += 2) {
-      ptx::mbar_wait(&s_full[sb], sph);
+      const bool tr = lane == 0 && q == 0 && half == 0;
+      if (tr) trace_ev(p, t, 2);
+      ptx::mbar_wait(&s_full[b], bph);
       ptx::tc_fence_after();
+      if (tr) trace_ev(p, t, 3);
+      const uint32_t col = tmem + lane_off + b * 64 + half * 32;
       uint32_t v[32];
-      ptx::tmem_ld32(tmem + lane_off + sb * 64 + half * 32, v);
+      ptx::tmem_ld32(col, v);
       ptx::tmem_wait_ld();
       float kv[32];
       if (p.kind == WGP_MATERN32) {
@@ -229,10 +256,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
           kv[c] = ptx::ex2_approx(fmaf(d2, p.neg_c_log2e, KSCALE_LOG2));  // 2^10 e^{-d2/2l^2}
         }
       }
-      // S(sb) fully consumed (every loaded register has been used above)
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
       const int64_t gj0 = (int64_t)t * BJ + half * 32;
       if (p.gram && gj0 < grow0 + BM && gj0 + 32 > grow0) {  // tile touches the diagonal
 #pragma unroll
@@ -246,16 +269,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hi[c]));
         lo[c] = pack_h2(kv[2 * c] - hf.x, kv[2 * c + 1] - hf.y);
       }
-      if (t >= 2) ptx::mbar_wait(&k_empty[set], ((t >> 1) - 1) & 1);
-      ptx::tc_fence_after();
-      ptx::tmem_st16(tmem + lane_off + kcol, hi);
-      ptx::tmem_st16(tmem + lane_off + kcol + 32, lo);
+      if (tr) trace_ev(p, t, 4);
+      // K back into the columns this warp read: [hi 16 | lo 16]
+      ptx::tmem_st16(col, hi);
+      ptx::tmem_st16(col + 16, lo);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&k_full[set]);
-      sb += 2;  // next tile of this set: t + 2
-      if (sb >= NSB) { sb -= NSB; sph ^= 1; }
+      if (lane == 0) ptx::mbar_arrive(&k_full[b]);
+      if (tr) trace_ev(p, t, 5);
+      b += 2;  // tile t + 2 -> buffer (t + 2) % NB, phase ((t + 2) / NB) & 1
+      if (b >= NB) { b -= NB; bph ^= 1; }
     }
     // ------------------------------------------------------------ output
     ptx::mbar_wait(y_full, 0);
@@ -407,7 +431,7 @@ void tc_build_operands(const Op& op, DBuf<float>& XA, DBuf<float>& XB, const dou
 size_t tc_smem_bytes(int K1, int s_pad, int* ns_out) {
   const size_t xa = (size_t)tc::BM * K1 * 4;
   const size_t stage = (size_t)tc::BJ * K1 * 4 + 2 * (size_t)s_pad * tc::BJ * 2;
-  const size_t tail = 32 * 8 + 64;
+  const size_t tail = 48 * 8 + 64;
   int ns = (int)((227 * 1024 - xa - tail) / stage);
   if (ns > 6) ns = 6;
   *ns_out = ns;
@@ -480,6 +504,14 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
     prm.out_scale = kp.s2 * 0x1.0p-10;
     prm.noise2 = kp.noise2;
     prm.gram = gram ? 1 : 0;
+    prm.trace = nullptr;
+    static const char* trace_path = getenv("WGP_TC_TRACE");
+    DBuf<unsigned long long> trace_buf;
+    if (trace_path) {
+      trace_buf.alloc((size_t)ntiles * 8);
+      WGP_CUDA(cudaMemsetAsync(trace_buf.p, 0, sizeof(unsigned long long) * ntiles * 8, st));
+      prm.trace = trace_buf.p;
+    }
     int ns = 0;
     const size_t smem = tc_smem_bytes(K1, s_pad, &ns);
     WGP_REQUIRE(ns >= 2, "kmatvec_tc: dim %d too large for the shared-memory pipeline", op.dim);
@@ -488,6 +520,19 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
     const int grid = (int)((nrows + tc::BM - 1) / tc::BM);
     tc::kmatvec_tc_kernel<<<grid, tc::NTHREADS, smem, st>>>(prm, ns);
     WGP_CUDA(cudaGetLastError());
+    if (trace_path) {
+      std::vector<unsigned long long> h((size_t)ntiles * 8);
+      WGP_CUDA(cudaMemcpyAsync(h.data(), trace_buf.p, sizeof(unsigned long long) * h.size(),
+                               cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaStreamSynchronize(st));
+      if (FILE* f = fopen(trace_path, "w")) {
+        fprintf(f, "tile,g1_issue,g2_issue,epi_wait_s,epi_s_ready,epi_wait_k,epi_done,prod_issue\n");
+        for (int t = 0; t < ntiles; ++t)
+          fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", t, h[t * 8], h[t * 8 + 1], h[t * 8 + 2],
+                  h[t * 8 + 3], h[t * 8 + 4], h[t * 8 + 5], h[t * 8 + 6]);
+        fclose(f);
+      }
+    }
     if (sc != s) {
       WGP_CUDA(cudaMemcpy2DAsync(Y64 + c0, sizeof(double) * s, Yc, sizeof(double) * sc,
                                  sizeof(double) * sc, nrows, cudaMemcpyDeviceToDevice, st));
