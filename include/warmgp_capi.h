@@ -146,6 +146,14 @@ wgp_status wgp_solve_many(wgp_op* op, const wgp_solver_config* cfg, const double
                           int32_t* history_len, int32_t* converged, int32_t* col_status,
                           int32_t* diverged_at);
 
+/* Single right-hand side with the semantics of solve (solvers.cpp:311-319) /
+ * cg_solve / sgd_solve / ap_solve: SGD draws from Rng(cfg->seed) itself (solve_many uses
+ * derive_seed(cfg->seed, column)).  b: n; u1: nullable warm start of length n1; v: n;
+ * history: max_iters+1 doubles.  Errors as wgp_solve_many (diverged_at: nullable). */
+wgp_status wgp_solve(wgp_op* op, const wgp_solver_config* cfg, const double* b, const double* u1,
+                     int64_t n1, double* v, int32_t* iterations, double* history,
+                     int32_t* history_len, int32_t* converged, int32_t* diverged_at);
+
 /* ---- preconditioner (pivoted_cholesky solvers.cpp:72-107, from_matrix :123-133) ----
  * Builds the rank-limited factor on the device and returns it: L (n x rank,
  * column-major, ldl), achieved rank, and the (calibrated) shift. */

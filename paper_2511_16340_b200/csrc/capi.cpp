@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 
+#include "rng.h"
 #include "solvers.h"
 
 namespace wgp {
@@ -50,7 +51,7 @@ static void set_device(const Ctx& ctx) { WGP_CUDA(cudaSetDevice(ctx.device)); }
 
 static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int64_t ldb, int s,
                       const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
-                      SolveOutputs& out) {
+                      SolveOutputs& out, bool derive_seeds) {
   cudaStream_t st = op.ctx->stream;
   SolverWork<double> w;
   w.alloc(op.n, s);
@@ -68,9 +69,19 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
       cg_solve_batched<double>(op, cfg, pd, w, out, st);
       break;
     }
+    case WGP_SGD: {
+      // solve_many derives one stream per RHS (solvers.cpp:343-345); sgd_solve uses cfg.seed
+      std::vector<uint64_t> seeds(s);
+      for (int c = 0; c < s; ++c) seeds[c] = derive_seeds ? derive_seed(cfg.seed, (uint64_t)c) : cfg.seed;
+      WGP_REQUIRE(op.dim <= 32, "sgd_solve: dim > 32 not supported on the device path");
+      sgd_solve_batched(op, cfg, seeds, w, out, st);
+      break;
+    }
+    case WGP_AP:
+      ap_solve_batched(op, cfg, w, out, st);
+      break;
     default:
-      throw_error(WGP_INVALID_ARGUMENT, "solve_many: method %d not available in this build",
-                  cfg.method);
+      throw_error(WGP_INVALID_ARGUMENT, "solve: unknown method");
   }
   download_solution<double>(w, V, ldv, st);
 }
@@ -295,11 +306,13 @@ wgp_status wgp_cross_matvec(wgp_op* op, const double* Xs, int64_t m, int64_t ldx
   });
 }
 
-wgp_status wgp_solve_many(wgp_op* op, const wgp_solver_config* cfg, const double* B, int64_t ldb,
-                          int s, const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
-                          int32_t* iterations, double* history, int64_t hist_stride,
-                          int32_t* history_len, int32_t* converged, int32_t* col_status,
-                          int32_t* diverged_at) {
+}  // extern "C"
+
+static wgp_status solve_impl(wgp_op* op, const wgp_solver_config* cfg, const double* B, int64_t ldb,
+                             int s, const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
+                             int32_t* iterations, double* history, int64_t hist_stride,
+                             int32_t* history_len, int32_t* converged, int32_t* col_status,
+                             int32_t* diverged_at, bool derive_seeds) {
   int fail_col = -1;
   int fail_iters = 0;
   wgp_status st = guard([&] {
@@ -320,7 +333,7 @@ wgp_status wgp_solve_many(wgp_op* op, const wgp_solver_config* cfg, const double
     set_device(*op->ctx);
     SolveOutputs out(s);
     try {
-      run_solve(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out);
+      run_solve(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out, derive_seeds);
     } catch (Error& e) {
       fail_col = e.col;
       fail_iters = e.iterations;
@@ -340,10 +353,40 @@ wgp_status wgp_solve_many(wgp_op* op, const wgp_solver_config* cfg, const double
       if (zero)
         for (int64_t i = 0; i < n; ++i) V[(int64_t)c * ldv + i] = 0.0;
     }
+    // the reference throws from the lowest failing column (DivergenceError, solvers.cpp:235)
+    for (int c = 0; c < s; ++c)
+      if (out.status[c] != WGP_OK) {
+        fail_col = c;
+        fail_iters = out.diverged_at[c];
+        Error e((wgp_status)out.status[c], "sgd_solve: diverged (relative residual above 1e3)");
+        e.col = c;
+        e.iterations = out.diverged_at[c];
+        throw e;
+      }
   });
   if (st != WGP_OK && col_status && fail_col >= 0 && fail_col < s) col_status[fail_col] = st;
   if (st != WGP_OK && diverged_at && fail_col >= 0 && fail_col < s) diverged_at[fail_col] = fail_iters;
   return st;
+}
+
+extern "C" {
+
+wgp_status wgp_solve_many(wgp_op* op, const wgp_solver_config* cfg, const double* B, int64_t ldb,
+                          int s, const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
+                          int32_t* iterations, double* history, int64_t hist_stride,
+                          int32_t* history_len, int32_t* converged, int32_t* col_status,
+                          int32_t* diverged_at) {
+  return solve_impl(op, cfg, B, ldb, s, U1, ldu, n1, V, ldv, iterations, history, hist_stride,
+                    history_len, converged, col_status, diverged_at, true);
+}
+
+wgp_status wgp_solve(wgp_op* op, const wgp_solver_config* cfg, const double* b, const double* u1,
+                     int64_t n1, double* v, int32_t* iterations, double* history,
+                     int32_t* history_len, int32_t* converged, int32_t* diverged_at) {
+  const int64_t n = op ? op->n : 0;
+  return solve_impl(op, cfg, b, n, 1, u1, n1 > 0 ? n1 : 1, n1, v, n, iterations, history,
+                    cfg ? (int64_t)cfg->max_iters + 1 : 1, history_len, converged, nullptr,
+                    diverged_at, false);
 }
 
 wgp_status wgp_pivoted_cholesky(wgp_op* op, int64_t rank, double* L, int64_t ldl, int64_t* achieved) {

@@ -6,43 +6,14 @@
 #include <cstdint>
 
 #include "../../include/warmgp_capi.h"
+#include "rng.h"
 
-namespace {
-
-struct Rng {  // warmgp::Rng, rng.hpp:21-61
-  uint64_t state;
-  uint64_t next_u64() {
-    uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-    return z ^ (z >> 31);
-  }
-  double uniform() { return (double)(next_u64() >> 11) * 0x1.0p-53; }
-  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
-  double normal() {
-    double u1 = uniform();
-    while (u1 <= 0.0) u1 = uniform();
-    const double u2 = uniform();
-    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925287 * u2);
-  }
-  double chi_square3() {
-    const double a = normal(), b = normal(), c = normal();
-    return a * a + b * b + c * c;
-  }
-  uint64_t uniform_index(uint64_t n) {
-    return (uint64_t)(((unsigned __int128)next_u64() * n) >> 64);
-  }
-};
-
-}  // namespace
+using wgp::Rng;
 
 extern "C" {
 
 uint64_t wgp_derive_seed(uint64_t seed, uint64_t stream) {  // rng.hpp:11-16
-  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (stream + 1);
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-  return z ^ (z >> 31);
+  return wgp::derive_seed(seed, stream);
 }
 
 uint64_t wgp_rng_next_u64(uint64_t* state) { Rng r{*state}; uint64_t v = r.next_u64(); *state = r.state; return v; }

@@ -1,0 +1,377 @@
+// sgd_ap.cu -- device kernels for the SGD and alternating-projection solvers.
+//
+//   krows   g[c][i] = H[row_ci, :] . v_c - b_c[row_ci]   (SGD minibatch rows, solvers.cpp:225-228)
+//   kcols   r_c -= H[:, B_c] delta_c                      (AP block column update, solvers.cpp:292)
+//   block_chol  H_BB = L L^T per contiguous block + L^-1  (AP factorisation, solvers.cpp:255-264)
+//   ap_block_solve  delta_c = L^-T L^-1 r_c[B_c]; v_c[B_c] += delta_c   (solvers.cpp:290-291)
+//   block_norms / greedy argmax (solvers.cpp:277-286, ties -> lowest block index)
+//
+// Kernel entries are evaluated on the fly from X with the same per-pair formula as the
+// kernel-matvec (explicit differences; H(i,i) = s^2 + sigma_n^2 exactly), in the operator's
+// compute type (fp64, or fp32 for the fp32 precisions).  Per-column work of different
+// columns is independent, so batching columns never changes a column's result.
+#include "common.cuh"
+
+namespace wgp {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T kentry(const T* __restrict__ xi, const T* __restrict__ xj, int dim,
+                                    const KParams& p) {
+  T d2 = T(0);
+  for (int k = 0; k < dim; ++k) {
+    const T df = xi[k] - xj[k];
+    d2 = fma(df, df, d2);
+  }
+  if (p.kind == WGP_RBF) return T(p.s2) * exp(-T(p.c1) * d2);
+  const T z = T(p.c1) * sqrt(d2);
+  return T(p.s2) * (T(1) + z) * exp(-z);
+}
+
+// One block = 64 gathered rows of one column.  4 threads per row split the j range.
+template <typename T>
+__global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int dpad, int dim,
+                                                    int64_t n, const int* __restrict__ rows,
+                                                    int nb, const double* __restrict__ V,
+                                                    const double* __restrict__ Bm, int s,
+                                                    const int* __restrict__ active, KParams p,
+                                                    double* __restrict__ g) {
+  const int c = blockIdx.y;
+  if (!active[c]) return;
+  __shared__ T sX[64][33];
+  __shared__ double sV[64];
+  __shared__ double red[256];
+  const int tid = threadIdx.x;
+  const int lr = tid >> 2, sub = tid & 3;
+  const int bi = blockIdx.x * 64 + lr;
+  const bool valid = bi < nb;
+  const int64_t row = valid ? rows[(int64_t)c * nb + bi] : 0;
+  T xr[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) xr[k] = (valid && k < dim) ? X[row * dpad + k] : T(0);
+  double acc = 0.0;
+  for (int64_t j0 = 0; j0 < n; j0 += 64) {
+    __syncthreads();
+    for (int e = tid; e < 64 * dim; e += 256) {
+      const int j = e / dim, k = e % dim;
+      sX[j][k] = j0 + j < n ? X[(j0 + j) * dpad + k] : T(0);
+    }
+    if (tid < 64) sV[tid] = j0 + tid < n ? V[(j0 + tid) * s + c] : 0.0;
+    __syncthreads();
+    if (valid) {
+      for (int jj = sub; jj < 64 && j0 + jj < n; jj += 4) {
+        T d2 = T(0);
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < dim) {
+            const T df = xr[k] - sX[jj][k];
+            d2 = fma(df, df, d2);
+          }
+        T kv;
+        if (j0 + jj == row) {
+          kv = T(p.s2 + p.noise2);
+        } else if (p.kind == WGP_RBF) {
+          kv = T(p.s2) * exp(-T(p.c1) * d2);
+        } else {
+          const T z = T(p.c1) * sqrt(d2);
+          kv = T(p.s2) * (T(1) + z) * exp(-z);
+        }
+        acc = fma((double)kv, sV[jj], acc);
+      }
+    }
+  }
+  red[tid] = acc;
+  __syncthreads();
+  if (valid && sub == 0) {
+    const double tot = ((red[tid] + red[tid + 1]) + red[tid + 2]) + red[tid + 3];
+    g[(int64_t)c * nb + bi] = tot - Bm[row * s + c];
+  }
+}
+
+// r[i, c] -= sum_{j in block_c} H[i, j] delta[j - start_c, c]    (thread per row i)
+template <typename T>
+__global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int dpad, int dim,
+                                                    int64_t n, const int* __restrict__ blk,
+                                                    int bs, const double* __restrict__ delta,
+                                                    int s, const int* __restrict__ active,
+                                                    KParams p, double* __restrict__ R) {
+  const int c = blockIdx.y;
+  if (!active[c]) return;
+  __shared__ T sX[64][33];
+  __shared__ double sD[64];
+  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const bool valid = i < n;
+  const int64_t start = (int64_t)blk[c] * bs;
+  const int len = (int)min((int64_t)bs, n - start);
+  T xr[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) xr[k] = (valid && k < dim) ? X[i * dpad + k] : T(0);
+  double acc = 0.0;
+  for (int j0 = 0; j0 < len; j0 += 64) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * dim; e += 128) {
+      const int j = e / dim, k = e % dim;
+      sX[j][k] = j0 + j < len ? X[(start + j0 + j) * dpad + k] : T(0);
+    }
+    if (threadIdx.x < 64) sD[threadIdx.x] = j0 + threadIdx.x < len ? delta[(int64_t)(j0 + threadIdx.x) * s + c] : 0.0;
+    __syncthreads();
+    if (valid) {
+      const int m = min(64, len - j0);
+      for (int jj = 0; jj < m; ++jj) {
+        T d2 = T(0);
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < dim) {
+            const T df = xr[k] - sX[jj][k];
+            d2 = fma(df, df, d2);
+          }
+        T kv;
+        if (start + j0 + jj == i) {
+          kv = T(p.s2 + p.noise2);
+        } else if (p.kind == WGP_RBF) {
+          kv = T(p.s2) * exp(-T(p.c1) * d2);
+        } else {
+          const T z = T(p.c1) * sqrt(d2);
+          kv = T(p.s2) * (T(1) + z) * exp(-z);
+        }
+        acc = fma((double)kv, sD[jj], acc);
+      }
+    }
+  }
+  if (valid) R[i * s + c] -= acc;
+}
+
+// One CTA per block: A = H_BB (fp64, from X64), in-place lower Cholesky, then L^-1.
+// fac: [n_blocks][bs][bs] row-major (lower L); inv: same shape (lower L^-1).
+__global__ void __launch_bounds__(512) block_chol_kernel(const double* __restrict__ X, int dpad,
+                                                         int dim, int64_t n, int bs, KParams p,
+                                                         double* __restrict__ fac,
+                                                         double* __restrict__ inv,
+                                                         int* __restrict__ fail) {
+  const int blkid = blockIdx.x;
+  const int64_t start = (int64_t)blkid * bs;
+  const int len = (int)min((int64_t)bs, n - start);
+  double* A = fac + (int64_t)blkid * bs * bs;
+  double* Li = inv + (int64_t)blkid * bs * bs;
+  // H_BB with the reference's exactly-set diagonal (kernel.cpp:70)
+  for (int e = threadIdx.x; e < len * len; e += blockDim.x) {
+    const int a = e / len, b = e % len;
+    double v;
+    if (a == b) {
+      v = p.s2 + p.noise2;
+    } else {
+      v = kentry<double>(X + (start + a) * dpad, X + (start + b) * dpad, dim, p);
+    }
+    A[a * bs + b] = v;
+  }
+  __syncthreads();
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  // right-looking Cholesky (Eigen::LLT semantics: pivot must be > 0)
+  for (int j = 0; j < len; ++j) {
+    __shared__ double ljj;
+    if (threadIdx.x == 0) {
+      const double x = A[j * bs + j];
+      if (!(x > 0.0)) bad = 1;
+      ljj = sqrt(x > 0.0 ? x : 1.0);
+      A[j * bs + j] = ljj;
+    }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < len; i += blockDim.x) A[i * bs + j] /= ljj;
+    __syncthreads();
+    const int m = len - j - 1;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int a = j + 1 + e / m, b = j + 1 + e % m;
+      if (b <= a) A[a * bs + b] -= A[a * bs + j] * A[b * bs + j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && bad) atomicExch(fail, 1);
+  // L^-1 column by column (thread per column): Li[i][col] = (delta_i,col - sum_k L_ik Li_k,col)/L_ii
+  for (int col = threadIdx.x; col < len; col += blockDim.x) {
+    for (int i = 0; i < len; ++i) {
+      double v = (i == col) ? 1.0 : 0.0;
+      if (i < col) {
+        Li[i * bs + col] = 0.0;
+        continue;
+      }
+      for (int k = col; k < i; ++k) v -= A[i * bs + k] * Li[k * bs + col];
+      Li[i * bs + col] = v / A[i * bs + i];
+    }
+  }
+}
+
+// delta_c = L^-T (L^-1 r_c[B]) for the column's chosen block; v_c[B] += delta_c.
+__global__ void __launch_bounds__(1024) ap_block_solve_kernel(
+    const double* __restrict__ inv, int bs, int64_t n, const int* __restrict__ blk,
+    const int* __restrict__ active, const double* __restrict__ R, int s, double* __restrict__ V,
+    double* __restrict__ delta) {
+  const int c = blockIdx.x;
+  if (!active[c]) return;
+  extern __shared__ double sh[];
+  double* rb = sh;        // bs
+  double* y = sh + bs;    // bs
+  const int64_t start = (int64_t)blk[c] * bs;
+  const int len = (int)min((int64_t)bs, n - start);
+  const double* Li = inv + (int64_t)blk[c] * bs * bs;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) rb[i] = R[(start + i) * s + c];
+  __syncthreads();
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {  // y = L^-1 r  (lower)
+    double a = 0.0;
+    for (int k = 0; k <= i; ++k) a = fma(Li[i * bs + k], rb[k], a);
+    y[i] = a;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < len; j += blockDim.x) {  // delta = L^-T y
+    double a = 0.0;
+    for (int i = j; i < len; ++i) a = fma(Li[i * bs + j], y[i], a);
+    delta[(int64_t)j * s + c] = a;
+    V[(start + j) * s + c] += a;
+  }
+}
+
+// Per column: squared norms of each block of r, then greedy argmax (strict >, first wins)
+// -- one block per column, n_blocks small (<= a few hundred).
+__global__ void greedy_block_kernel(const double* __restrict__ R, int64_t n, int bs, int nblk,
+                                    int s, const int* __restrict__ active, int* __restrict__ blk) {
+  const int c = blockIdx.x;
+  if (!active[c]) return;
+  extern __shared__ double nrm[];
+  for (int b = threadIdx.y; b < nblk; b += blockDim.y) {
+    const int64_t s0 = (int64_t)b * bs;
+    const int64_t s1 = min(n, s0 + bs);
+    double a = 0.0;
+    for (int64_t i = s0 + threadIdx.x; i < s1; i += 32) a = fma(R[i * s + c], R[i * s + c], a);
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (threadIdx.x == 0) nrm[b] = sqrt(a);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    double best = -1.0;
+    int arg = 0;
+    for (int b = 0; b < nblk; ++b)
+      if (nrm[b] > best) {
+        best = nrm[b];
+        arg = b;
+      }
+    blk[c] = arg;
+  }
+}
+
+__global__ void set_cyclic_kernel(int* blk, int s, int value) {
+  for (int c = threadIdx.x; c < s; c += blockDim.x) blk[c] = value;
+}
+
+// velocity *= momentum; velocity[rows] += scale * g; v -= lr * velocity   (active columns)
+__global__ void sgd_momentum_kernel(double* __restrict__ vel, int64_t n, int s,
+                                    const int* __restrict__ active, double momentum) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * s;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (active[e % s]) vel[e] *= momentum;
+}
+__global__ void sgd_scatter_kernel(double* __restrict__ vel, const int* __restrict__ rows,
+                                   const double* __restrict__ g, int nb, int s,
+                                   const int* __restrict__ active, double scale) {
+  const int c = blockIdx.y;
+  if (!active[c]) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const int64_t row = rows[(int64_t)c * nb + i];
+    vel[row * s + c] += scale * g[(int64_t)c * nb + i];
+  }
+}
+__global__ void sgd_step_kernel(double* __restrict__ V, const double* __restrict__ vel, int64_t n,
+                                int s, const int* __restrict__ active, double lr) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * s;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (active[e % s]) V[e] -= lr * vel[e];
+}
+
+// Copy columns flagged in mask from src to dst (AP convergence confirmation).
+__global__ void copy_masked_cols_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                        int64_t n, int s, const int* __restrict__ mask) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * s;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (mask[e % s]) dst[e] = src[e];
+}
+
+inline int grid_for(int64_t total) {
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+void launch_krows(const Op& op, const int* rows, int nb, const double* V, const double* B, int s,
+                  const int* active, double* g, cudaStream_t st) {
+  dim3 grid(ceil_div(nb, 64), s);
+  if (op.f64())
+    krows_kernel<double><<<grid, 256, 0, st>>>(op.X64.p, op.dpad, op.dim, op.n, rows, nb, V, B, s,
+                                               active, op.kp(), g);
+  else
+    krows_kernel<float><<<grid, 256, 0, st>>>(op.X32.p, op.dpad, op.dim, op.n, rows, nb, V, B, s,
+                                              active, op.kp(), g);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_kcols(const Op& op, const int* blk, int bs, const double* delta, int s,
+                  const int* active, double* R, cudaStream_t st) {
+  dim3 grid(ceil_div(op.n, 128), s);
+  if (op.f64())
+    kcols_kernel<double><<<grid, 128, 0, st>>>(op.X64.p, op.dpad, op.dim, op.n, blk, bs, delta, s,
+                                               active, op.kp(), R);
+  else
+    kcols_kernel<float><<<grid, 128, 0, st>>>(op.X32.p, op.dpad, op.dim, op.n, blk, bs, delta, s,
+                                              active, op.kp(), R);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_block_chol(const Op& op, int bs, int nblk, double* fac, double* inv, int* fail,
+                       cudaStream_t st) {
+  block_chol_kernel<<<nblk, 512, 0, st>>>(op.X64.p, op.dpad, op.dim, op.n, bs, op.kp(), fac, inv,
+                                          fail);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_ap_block_solve(const double* inv, int bs, int64_t n, const int* blk, const int* active,
+                           const double* R, int s, double* V, double* delta, cudaStream_t st) {
+  const size_t smem = sizeof(double) * 2 * bs;
+  if (smem > 48 * 1024)
+    WGP_CUDA(cudaFuncSetAttribute(ap_block_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  ap_block_solve_kernel<<<s, 1024, smem, st>>>(inv, bs, n, blk, active, R, s, V, delta);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_greedy_block(const double* R, int64_t n, int bs, int nblk, int s, const int* active,
+                         int* blk, cudaStream_t st) {
+  const size_t smem = sizeof(double) * nblk;
+  if (smem > 48 * 1024)
+    WGP_CUDA(cudaFuncSetAttribute(greedy_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  greedy_block_kernel<<<s, dim3(32, 16), smem, st>>>(R, n, bs, nblk, s, active, blk);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_set_cyclic(int* blk, int s, int value, cudaStream_t st) {
+  set_cyclic_kernel<<<1, 256, 0, st>>>(blk, s, value);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_sgd_update(double* V, double* vel, const int* rows, const double* g, int nb, int64_t n,
+                       int s, const int* active, double momentum, double scale, double lr,
+                       cudaStream_t st) {
+  sgd_momentum_kernel<<<grid_for(n * s), 256, 0, st>>>(vel, n, s, active, momentum);
+  sgd_scatter_kernel<<<dim3(ceil_div(nb, 256), s), 256, 0, st>>>(vel, rows, g, nb, s, active, scale);
+  sgd_step_kernel<<<grid_for(n * s), 256, 0, st>>>(V, vel, n, s, active, lr);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_copy_masked_cols(double* dst, const double* src, int64_t n, int s, const int* mask,
+                             cudaStream_t st) {
+  copy_masked_cols_kernel<<<grid_for(n * s), 256, 0, st>>>(dst, src, n, s, mask);
+  WGP_CUDA(cudaGetLastError());
+}
+
+}  // namespace wgp

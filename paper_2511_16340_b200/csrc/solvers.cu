@@ -12,6 +12,7 @@
 #include <climits>
 #include <cmath>
 
+#include "rng.h"
 #include "solvers.h"
 
 namespace wgp {
@@ -92,7 +93,7 @@ void SolverWork<T>::alloc(int64_t n_, int s_) {
   B.alloc(ns);
   part.alloc((size_t)(nch > 0 ? nch : 1) * 2 * s);
   scal.alloc((size_t)6 * s);
-  act.alloc((size_t)s + 1);
+  act.alloc((size_t)2 * s + 2);
 }
 
 template <typename T>
@@ -207,6 +208,192 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
     launch_xpby_cols<T>(w.P.p, w.Z.p, beta, active, n, s, st);  // p = z + beta p (:180)
   }
   WGP_CUDA(cudaGetLastError());
+}
+
+
+// ---------------------------------------------------------------------------------------
+// shared per-iteration helpers (host side)
+
+// |b| per column; zero right-hand sides are inactive from the start.
+static void bnorms(SolverWork<double>& w, double* bnorm, int* active, cudaStream_t st) {
+  launch_coldots<double>(w.B.p, w.B.p, nullptr, nullptr, w.n, w.s, w.part.p, st);
+  init_bnorm_kernel<<<sgrid(w.s), 256, 0, st>>>(w.part.p, w.nch, w.s, bnorm, active);
+  WGP_CUDA(cudaGetLastError());
+}
+
+// rel = |R| / |b| per column (device), copied to the host.  Does not touch the flags.
+static void residual_norms(SolverWork<double>& w, const double* R, const double* bnorm,
+                           double* rel_dev, std::vector<double>& hrel, cudaStream_t st) {
+  launch_coldots<double>(R, R, nullptr, nullptr, w.n, w.s, w.part.p, st);
+  resid_step_kernel<<<sgrid(w.s), 256, 0, st>>>(w.part.p, w.nch, 1, w.s, bnorm, -1.0, rel_dev,
+                                                w.act.p + w.s + 1);  // scratch flags
+  WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel_dev, sizeof(double) * w.s, cudaMemcpyDeviceToHost, st));
+  WGP_CUDA(cudaStreamSynchronize(st));
+}
+
+// ---------------------------------------------------------------------------------------
+// SGD (sgd_solve, solvers.cpp:193-243), batched over columns.  Minibatch rows come from
+// each column's own Rng stream with the reference's persistent partial Fisher-Yates index
+// array (:211-222); the rows are drawn on the host and uploaded (B int32 per column).
+void sgd_solve_batched(Op& op, const wgp_solver_config& cfg, const std::vector<uint64_t>& seeds,
+                       SolverWork<double>& w, SolveOutputs& out, cudaStream_t st) {
+  const int64_t n = w.n;
+  const int s = w.s;
+  const int64_t batch = std::min<int64_t>(cfg.batch_size, n);
+  WGP_REQUIRE(batch > 0, "sgd_solve: batch size must be positive");
+  WGP_REQUIRE(batch <= INT32_MAX, "sgd_solve: batch too large");
+  double* bnorm = w.scal.p + 3 * s;
+  double* rel = w.scal.p + 4 * s;
+  int* active = w.act.p;
+  bnorms(w, bnorm, active, st);
+  launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
+  std::vector<double> hrel(s);
+  std::vector<int> hact(s);
+  WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
+  residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+  int n_active = 0;
+  for (int c = 0; c < s; ++c) {
+    out.history[c].assign(1, hact[c] ? hrel[c] : 0.0);
+    out.iterations[c] = 0;
+    if (hact[c] && hrel[c] <= cfg.tolerance) hact[c] = 0;  // converged at the start
+    out.converged[c] = !hact[c];
+    n_active += hact[c];
+  }
+  if (n_active == 0) return;
+  const double scale = cfg.sgd_scaling == WGP_SGD_UNBIASED ? (double)n / (double)batch : 1.0;
+  std::vector<Rng> rngs;
+  for (int c = 0; c < s; ++c) rngs.push_back(Rng{seeds[c]});
+  std::vector<std::vector<int64_t>> idx(s);
+  for (int c = 0; c < s; ++c) {
+    idx[c].resize(n);
+    for (int64_t i = 0; i < n; ++i) idx[c][i] = i;
+  }
+  std::vector<int> hrows((size_t)s * batch, 0);
+  DBuf<int> drows((size_t)s * batch);
+  DBuf<double> g((size_t)s * batch), vel((size_t)n * s);
+  WGP_CUDA(cudaMemsetAsync(vel.p, 0, sizeof(double) * n * s, st));
+  WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
+  for (int k = 1; k <= cfg.max_iters && n_active > 0; ++k) {
+    for (int c = 0; c < s; ++c) {
+      if (!hact[c]) continue;
+      std::vector<int64_t>& ix = idx[c];
+      for (int64_t i = 0; i < batch; ++i) {  // partial Fisher-Yates (:219-222)
+        const int64_t j = i + (int64_t)rngs[c].uniform_index((uint64_t)(n - i));
+        std::swap(ix[i], ix[j]);
+        hrows[(size_t)c * batch + i] = (int)ix[i];
+      }
+    }
+    WGP_CUDA(cudaMemcpyAsync(drows.p, hrows.data(), sizeof(int) * hrows.size(), cudaMemcpyHostToDevice, st));
+    launch_krows(op, drows.p, (int)batch, w.V.p, w.B.p, s, active, g.p, st);  // H[row].v - b[row]
+    launch_sgd_update(w.V.p, vel.p, drows.p, g.p, (int)batch, n, s, active, cfg.momentum, scale,
+                      cfg.learning_rate, st);
+    launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // full true residual (:231)
+    residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+    bool changed = false;
+    for (int c = 0; c < s; ++c) {
+      if (!hact[c]) continue;
+      const double r = hrel[c];
+      out.history[c].push_back(r);
+      out.iterations[c] = k;
+      if (r > 1e3 || !std::isfinite(r)) {  // DivergenceError(k), solvers.cpp:234-236
+        out.status[c] = WGP_DIVERGED;
+        out.diverged_at[c] = k;
+        hact[c] = 0;
+        changed = true;
+      } else if (r <= cfg.tolerance) {
+        out.converged[c] = 1;
+        hact[c] = 0;
+        changed = true;
+      }
+    }
+    if (changed) {
+      n_active = 0;
+      for (int c = 0; c < s; ++c) n_active += hact[c];
+      WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Alternating projections (ap_solve, solvers.cpp:245-309), batched over columns: each
+// column picks its own block (Greedy: argmax block residual norm; Cyclic: (k-1) mod
+// n_blocks); factors of every diagonal block are built once on the device.
+void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& w,
+                      SolveOutputs& out, cudaStream_t st) {
+  const int64_t n = w.n;
+  const int s = w.s;
+  const int64_t bs64 = std::min<int64_t>(cfg.block_size, n);
+  WGP_REQUIRE(bs64 > 0, "ap_solve: block size must be positive");
+  WGP_REQUIRE(bs64 <= 1024, "ap_solve: block size > 1024 not supported on the device path");
+  WGP_REQUIRE(op.dim <= 32, "ap_solve: dim > 32 not supported on the device path");
+  const int bs = (int)bs64;
+  const int nblk = (int)((n + bs - 1) / bs);
+  DBuf<double> fac((size_t)nblk * bs * bs), inv((size_t)nblk * bs * bs);
+  DBuf<int> fail(1);
+  WGP_CUDA(cudaMemsetAsync(fail.p, 0, sizeof(int), st));
+  launch_block_chol(op, bs, nblk, fac.p, inv.p, fail.p, st);
+  int hfail = 0;
+  WGP_CUDA(cudaMemcpyAsync(&hfail, fail.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  WGP_CUDA(cudaStreamSynchronize(st));
+  if (hfail) throw_error(WGP_NOT_SPD, "ap_solve: diagonal block factorization failed");
+  double* bnorm = w.scal.p + 3 * s;
+  double* rel = w.scal.p + 4 * s;
+  int* active = w.act.p;
+  bnorms(w, bnorm, active, st);
+  launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
+  std::vector<double> hrel(s);
+  std::vector<int> hact(s), confirm(s);
+  WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
+  residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+  int n_active = 0;
+  for (int c = 0; c < s; ++c) {
+    out.history[c].assign(1, hact[c] ? hrel[c] : 0.0);
+    out.iterations[c] = 0;
+    if (hact[c] && hrel[c] <= cfg.tolerance) hact[c] = 0;
+    out.converged[c] = !hact[c];
+    n_active += hact[c];
+  }
+  if (n_active == 0) return;
+  DBuf<int> blk(s), dconf(s);
+  DBuf<double> delta((size_t)bs * s);
+  WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
+  for (int k = 1; k <= cfg.max_iters && n_active > 0; ++k) {
+    if (cfg.ap_ordering == WGP_AP_GREEDY)
+      launch_greedy_block(w.R.p, n, bs, nblk, s, active, blk.p, st);
+    else
+      launch_set_cyclic(blk.p, s, (k - 1) % nblk, st);
+    launch_ap_block_solve(inv.p, bs, n, blk.p, active, w.R.p, s, w.V.p, delta.p, st);
+    launch_kcols(op, blk.p, bs, delta.p, s, active, w.R.p, st);  // r -= H[:, B] delta
+    if (k % nblk == 0) launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // drift refresh
+    residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+    int nconf = 0;
+    for (int c = 0; c < s; ++c) {
+      confirm[c] = hact[c] && hrel[c] <= cfg.tolerance;
+      nconf += confirm[c];
+    }
+    if (nconf) {  // confirm with the true residual (:296-300)
+      launch_residual(op, w.B.p, w.V.p, w.Z.p, s, st);
+      WGP_CUDA(cudaMemcpyAsync(dconf.p, confirm.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
+      launch_copy_masked_cols(w.R.p, w.Z.p, n, s, dconf.p, st);
+      residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+    }
+    bool changed = false;
+    for (int c = 0; c < s; ++c) {
+      if (!hact[c]) continue;
+      out.history[c].push_back(hrel[c]);
+      out.iterations[c] = k;
+      if (hrel[c] <= cfg.tolerance) {
+        out.converged[c] = 1;
+        hact[c] = 0;
+        changed = true;
+      }
+    }
+    if (changed) {
+      n_active = 0;
+      for (int c = 0; c < s; ++c) n_active += hact[c];
+      WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
+    }
+  }
 }
 
 template struct SolverWork<double>;

@@ -54,4 +54,27 @@ template <typename T>
 void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd,
                       SolverWork<T>& w, SolveOutputs& out, cudaStream_t st);
 
+void sgd_solve_batched(Op& op, const wgp_solver_config& cfg, const std::vector<uint64_t>& seeds,
+                       SolverWork<double>& w, SolveOutputs& out, cudaStream_t st);
+void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& w,
+                      SolveOutputs& out, cudaStream_t st);
+
+// sgd_ap.cu
+void launch_krows(const Op& op, const int* rows, int nb, const double* V, const double* B, int s,
+                  const int* active, double* g, cudaStream_t st);
+void launch_kcols(const Op& op, const int* blk, int bs, const double* delta, int s,
+                  const int* active, double* R, cudaStream_t st);
+void launch_block_chol(const Op& op, int bs, int nblk, double* fac, double* inv, int* fail,
+                       cudaStream_t st);
+void launch_ap_block_solve(const double* inv, int bs, int64_t n, const int* blk, const int* active,
+                           const double* R, int s, double* V, double* delta, cudaStream_t st);
+void launch_greedy_block(const double* R, int64_t n, int bs, int nblk, int s, const int* active,
+                         int* blk, cudaStream_t st);
+void launch_set_cyclic(int* blk, int s, int value, cudaStream_t st);
+void launch_sgd_update(double* V, double* vel, const int* rows, const double* g, int nb, int64_t n,
+                       int s, const int* active, double momentum, double scale, double lr,
+                       cudaStream_t st);
+void launch_copy_masked_cols(double* dst, const double* src, int64_t n, int s, const int* mask,
+                             cudaStream_t st);
+
 }  // namespace wgp

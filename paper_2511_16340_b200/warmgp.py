@@ -42,7 +42,7 @@ EXPORTS = (
     "wgp_ctx_create", "wgp_nccl_unique_id", "wgp_ctx_create_sharded", "wgp_ctx_destroy",
     "wgp_ctx_stream", "wgp_op_create", "wgp_op_destroy", "wgp_op_append_rows", "wgp_op_size",
     "wgp_op_dim", "wgp_op_precision", "wgp_kmatvec", "wgp_kmatvec_dev", "wgp_residual_dev",
-    "wgp_cross_matvec", "wgp_solve_many", "wgp_pivoted_cholesky", "wgp_precond_info",
+    "wgp_cross_matvec", "wgp_solve_many", "wgp_solve", "wgp_pivoted_cholesky", "wgp_precond_info",
     "wgp_rff_eval", "wgp_derive_seed", "wgp_rng_next_u64", "wgp_rng_uniform", "wgp_rng_normal",
     "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
 )
@@ -120,6 +120,7 @@ def _declare(L):
         "wgp_cross_matvec": (C.c_int, [P, P, I64, I64, P, I64, C.c_int, P, I64]),
         "wgp_solve_many": (C.c_int, [P, P, P, I64, C.c_int, P, I64, I64, P, I64, P, P, I64, P, P,
                                      P, P]),
+        "wgp_solve": (C.c_int, [P, P, P, P, I64, P, P, P, P, P, P]),
         "wgp_pivoted_cholesky": (C.c_int, [P, I64, P, I64, P]),
         "wgp_precond_info": (C.c_int, [P, I64, D, C.c_int, P, P]),
         "wgp_rff_eval": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, I64, P, I64]),
@@ -409,8 +410,20 @@ def solve_many(op: KernelOperator, rhs, inits: list, cfg: SolverConfig, return_s
 
 
 def solve(op: KernelOperator, b, init: Initialization, cfg: SolverConfig) -> SolveResult:
-    """solve (solvers.cpp:311-319): one RHS."""
-    return solve_many(op, np.asarray(b, dtype=np.float64).reshape(-1, 1), [init], cfg)[0]
+    """solve (solvers.cpp:311-319): one RHS; SGD uses cfg.seed itself (not derive_seed)."""
+    b = np.ascontiguousarray(b, dtype=np.float64).ravel()
+    n = op.n
+    if b.size != n:
+        raise ValueError("solve: rhs length != operator size")
+    u1 = None if not init.warm_start else np.ascontiguousarray(init.u1, dtype=np.float64)
+    n1 = 0 if u1 is None else u1.size
+    v = np.zeros(n)
+    hist = np.zeros(cfg.max_iters + 1)
+    its, hl, cv, dv = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    st = lib().wgp_solve(op._h, C.byref(cfg), _ptr(b), _ptr(u1), n1, _ptr(v), C.byref(its), _ptr(hist),
+                         C.byref(hl), C.byref(cv), C.byref(dv))
+    _check(st, dv.value)
+    return SolveResult(v, its.value, hist[: hl.value].tolist(), bool(cv.value))
 
 
 def cg_solve(op, b, init, cfg) -> SolveResult:

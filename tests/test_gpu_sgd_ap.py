@@ -1,0 +1,99 @@
+"""GPU parity of the SGD and alternating-projection solvers against the oracle
+(solvers.cpp:193-309, solve_many :321-354) through the C-ABI."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def system(O, seed, n, dim=3, ls=0.5, noise=0.5, kind=0):
+    h = O.KernelHyperparams(ls, 1.0, noise, kind)
+    X = O.uniform_inputs(seed, n, dim)
+    return h, X, O.gram_matrix(X, h), O.gaussian_vector(O.derive_seed(seed, 0xB), n)
+
+
+def wop(W, X, h, precision=0):
+    return W.KernelOperator(W.KernelHyperparams(h.lengthscale, h.signal_scale, h.noise_scale, h.kind), X,
+                            precision=precision)
+
+
+def test_sgd_same_stream_same_trajectory(W, O):
+    h, X, H, b = system(O, 19, 400)
+    kw = dict(method=O.SGD, learning_rate=0.02, batch_size=25, max_iters=300, tolerance=1e-8, seed=1234)
+    ref = O.sgd_solve(H, b, O.Initialization.cold(), O.SolverConfig(**kw))
+    got = W.sgd_solve(wop(W, X, h), b, W.Initialization.cold(), W.SolverConfig(**kw))
+    assert got.iterations == ref.iterations
+    np.testing.assert_allclose(got.residual_history, ref.residual_history, rtol=1e-8)
+    np.testing.assert_allclose(got.v, ref.v, rtol=1e-8, atol=1e-10)
+
+
+def test_sgd_solve_many_per_column_seeds(W, O):
+    h, X, H, b = system(O, 36, 300)
+    B = np.stack([b, b, 2 * b], 1)
+    kw = dict(method=O.SGD, learning_rate=0.02, batch_size=10, max_iters=100, tolerance=1e-10, seed=9)
+    ref = O.solve_many(H, B, [O.Initialization.cold()] * 3, O.SolverConfig(**kw))
+    got = W.solve_many(wop(W, X, h), B, [W.Initialization.cold()] * 3, W.SolverConfig(**kw))
+    for r, g in zip(ref, got):
+        np.testing.assert_allclose(g.residual_history, r.residual_history, rtol=1e-8)
+    assert not np.array_equal(got[0].v, got[1].v)  # distinct streams per column
+
+
+def test_sgd_divergence_guard(W, O):
+    h, X, H, b = system(O, 20, 200, noise=0.3)
+    kw = dict(method=O.SGD, learning_rate=5.0, momentum=0.9, batch_size=50, max_iters=10000, seed=3)
+    with pytest.raises(O.DivergenceError) as eo:
+        O.sgd_solve(H, b, O.Initialization.cold(), O.SolverConfig(**kw))
+    with pytest.raises(W.DivergenceError) as ew:
+        W.sgd_solve(wop(W, X, h), b, W.Initialization.cold(), W.SolverConfig(**kw))
+    assert ew.value.iterations == eo.value.iterations
+    # batched: statuses per column, lowest failing column raised
+    res, status, dv = W.solve_many(wop(W, X, h), np.stack([b, b], 1), [W.Initialization.cold()] * 2,
+                                   W.SolverConfig(**kw), return_status=True)
+    assert list(status) == [W.DIVERGED, W.DIVERGED] and dv[0] >= 1
+
+
+@pytest.mark.parametrize("ordering", [0, 1])
+@pytest.mark.parametrize("bs", [25, 64, 100])
+def test_ap_matches_oracle(W, O, ordering, bs):
+    h, X, H, b = system(O, 26, 300, ls=0.4, noise=0.4)
+    kw = dict(method=O.AP, block_size=bs, tolerance=1e-6, max_iters=3000, ap_ordering=ordering)
+    ref = O.ap_solve(H, b, O.Initialization.cold(), O.SolverConfig(**kw))
+    got = W.ap_solve(wop(W, X, h), b, W.Initialization.cold(), W.SolverConfig(**kw))
+    assert got.converged == ref.converged
+    assert abs(got.iterations - ref.iterations) <= max(1, round(0.02 * ref.iterations)), (got.iterations, ref.iterations)
+    k = min(20, len(ref.residual_history))
+    np.testing.assert_allclose(got.residual_history[:k], ref.residual_history[:k], rtol=1e-7)
+
+
+def test_ap_single_block_is_exact(W, O):
+    h, X, H, b = system(O, 22, 25)
+    got = W.ap_solve(wop(W, X, h), b, W.Initialization.cold(), W.SolverConfig(method=W.AP, block_size=25, tolerance=1e-8))
+    assert got.converged and got.iterations == 1
+
+
+def test_warm_not_worse_than_cold_plus_one(W, O):
+    for seed in (31, 32):
+        h = O.KernelHyperparams(0.4, 1.0, 0.5)
+        X1 = O.uniform_inputs(seed, 80, 3)
+        X2 = O.uniform_inputs(O.derive_seed(seed, 1), 12, 3)
+        X = np.vstack([X1, X2])
+        b = np.concatenate([O.gaussian_vector(O.derive_seed(seed, 2), 80), O.gaussian_vector(O.derive_seed(seed, 3), 12)])
+        u1 = O.exact_solve(O.gram_matrix(X1, h), b[:80])
+        op = wop(W, X, h)
+        for m in (W.CG, W.SGD, W.AP):
+            cfg = W.SolverConfig(method=m, tolerance=0.01, max_iters=20000, learning_rate=0.02, batch_size=30,
+                                 block_size=12, precond_rank=20, precond_shift=0.25)
+            cold = W.solve(op, b, W.Initialization.cold(), cfg)
+            warm = W.solve(op, b, W.Initialization.warm(u1), cfg)
+            assert cold.converged and warm.converged
+            assert warm.iterations <= cold.iterations + 1
+
+
+@pytest.mark.parametrize("method", [1, 2])
+def test_f32_path_sgd_ap(W, O, method):
+    h, X, H, b = system(O, 44, 1500, dim=4, ls=0.5, noise=0.5)
+    kw = dict(method=method, tolerance=1e-4, max_iters=5000, learning_rate=0.01, batch_size=100, block_size=100)
+    ref = O.solve(H, b, O.Initialization.cold(), O.SolverConfig(**kw))
+    got = W.solve(wop(W, X, h, precision=W.F32_3XTF32), b, W.Initialization.cold(), W.SolverConfig(**kw))
+    assert got.converged
+    assert abs(got.iterations - ref.iterations) <= max(2, round(0.05 * ref.iterations)), (got.iterations, ref.iterations)
