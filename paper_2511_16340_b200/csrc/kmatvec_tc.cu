@@ -38,13 +38,18 @@ namespace tc {
 constexpr int BM = 128;        // rows per CTA (UMMA M)
 constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
 constexpr int NTHREADS = 640;  // 4 role warps + 2 epilogue sets x 8 warps
-constexpr int MAX_SPAD = 128;
+constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
+constexpr int CH = 16;         // j tiles per TMEM accumulation chunk (fp64 drain after each)
 // TMEM: a ring of NB 64-column tile buffers followed by the Y accumulator.  A buffer holds
 // S(t) (fp32 d^2, written by GEMM1); the epilogue loads it into registers and writes K(t)
 // back in place as packed fp16 (each warp into the 32 columns it read: 16 hi + 16 lo), which
 // GEMM2 then reads as its A operand; GEMM2's commit frees the buffer for GEMM1 of tile
-// t + NB.  NB = (512 - s_pad_alloc) / 64: 7 for s_pad <= 64, 6 for s_pad <= 128.
-constexpr int MAX_NB = 7;
+// t + NB.  Two 64-column Y accumulators alternate per chunk of CH tiles: the tensor core's
+// fp32 accumulation error grows with the number of accumulated K-steps (measured 3.5e-4 at
+// N = 101k in one accumulator), so every CH tiles the epilogue warps drain the finished
+// accumulator into fp64 partial sums in shared memory (~4e-6 per chunk, summed in fp64).
+// TMEM: NB = 6 buffers [0,384), Y0 [384,448), Y1 [448,512).
+constexpr int MAX_NB = 6;
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
 
 struct Params {
@@ -93,11 +98,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* s_full = xa_full + 1;        // [MAX_NB] GEMM1 -> epilogue
   uint64_t* k_full = s_full + MAX_NB;    // [MAX_NB] epilogue -> GEMM2 (8 arrivals)
   uint64_t* b_free = k_full + MAX_NB;    // [MAX_NB] GEMM2 -> GEMM1
-  uint64_t* y_full = b_free + MAX_NB;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_full + 1);
-  const int s_alloc = p.s_pad <= 64 ? 64 : 128;
-  const int NB = (512 - s_alloc) / 64;
-  const uint32_t TM_Y = 512u - (uint32_t)s_alloc;
+  uint64_t* y_full = b_free + MAX_NB;    // [2] chunk accumulator done (GEMM2 commit)
+  uint64_t* y_free = y_full + 2;         // [2] chunk accumulator drained (16 warp arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_free + 2);
+  double* ypart = reinterpret_cast<double*>(smem + (size_t)(XA_BYTES + NS * ST_BYTES + 512));
+  constexpr int NB = MAX_NB;
+  constexpr uint32_t TM_Y = 384;         // Y accumulator a at TM_Y + 64 a
+  const int NCH = (p.ntiles + CH - 1) / CH;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -110,10 +117,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       ptx::mbar_init(&k_full[i], 8);
       ptx::mbar_init(&b_free[i], 1);
     }
-    ptx::mbar_init(y_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&y_full[i], 1);
+      ptx::mbar_init(&y_free[i], 16);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  for (int e = threadIdx.x; e < BM * p.s_pad; e += NTHREADS) ypart[e] = 0.0;
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -185,32 +196,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       int st2 = 0, b2 = 0;
       uint32_t phb2 = 0;
       for (int t = 0; t < T; ++t) {
+        const int c = t / CH, ya = c & 1;
+        const bool first = t == c * CH, last = t == T - 1 || t == c * CH + CH - 1;
+        if (first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
         ptx::mbar_wait(&k_full[b2], phb2);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 1);
           const uint64_t dVh = dV0 + st_step * st2;
           const uint64_t dVl = dVh + vlo_step;
+          const uint32_t yacc = tmem + TM_Y + ya * 64;
           // K layout in the buffer: [hi j0-31 | lo j0-31 | hi j32-63 | lo j32-63], 16 cols each
           const uint32_t kb = tmem + b2 * 64;
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks) {
             const uint32_t hcol = kb + (ks >> 1) * 32 + (ks & 1) * 8;
-            ptx::mma_f16_ts(tmem + TM_Y, hcol, dVh + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
+            ptx::mma_f16_ts(yacc, hcol, dVh + 16 * ks, idesc2, (!first || ks > 0) ? 1u : 0u);
           }
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks) {
             const uint32_t hcol = kb + (ks >> 1) * 32 + (ks & 1) * 8;
-            ptx::mma_f16_ts(tmem + TM_Y, hcol, dVl + 16 * ks, idesc2, 1u);
+            ptx::mma_f16_ts(yacc, hcol, dVl + 16 * ks, idesc2, 1u);
           }
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks) {
             const uint32_t lcol = kb + (ks >> 1) * 32 + 16 + (ks & 1) * 8;
-            ptx::mma_f16_ts(tmem + TM_Y, lcol, dVh + 16 * ks, idesc2, 1u);
+            ptx::mma_f16_ts(yacc, lcol, dVh + 16 * ks, idesc2, 1u);
           }
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&stage_empty[st2]);
-          if (t == T - 1) ptx::mma_commit(y_full);
+          if (last) ptx::mma_commit(&y_full[ya]);
         }
         __syncwarp();
         if (++st2 == NS) st2 = 0;
@@ -227,9 +242,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     const int64_t gi = p.row0 + (int64_t)blockIdx.x * BM + r;
     const int64_t grow0 = p.row0 + (int64_t)blockIdx.x * BM;
     const float kdiag = 1024.0f;              // k(x,x)/s^2 * 2^10
+    // drain share of this warp: its quadrant's 32 rows x 16 accumulator columns
+    const int dc0 = g * 16;
+    int drained = 0;
+    auto drain = [&](int c) {
+      const int ya = c & 1;
+      ptx::mbar_wait(&y_full[ya], (c >> 1) & 1);
+      ptx::tc_fence_after();
+      if (dc0 < p.s_pad) {
+        uint32_t y[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15}, [%16];"
+            : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3]), "=r"(y[4]), "=r"(y[5]), "=r"(y[6]),
+              "=r"(y[7]), "=r"(y[8]), "=r"(y[9]), "=r"(y[10]), "=r"(y[11]), "=r"(y[12]),
+              "=r"(y[13]), "=r"(y[14]), "=r"(y[15])
+            : "r"(tmem + lane_off + TM_Y + ya * 64 + dc0));
+        ptx::tmem_wait_ld();
+        // column-major partials: lanes (rows) hit consecutive 8-byte words (no bank conflicts)
+        double* colp = ypart + (size_t)dc0 * BM + r;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) colp[(size_t)k * BM] += (double)__uint_as_float(y[k]);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&y_free[ya]);
+    };
     int b = set;                              // buffer of tile t = t % NB
     uint32_t bph = 0;
     for (int t = set; t < T; t += 2) {
+      // drain a finished chunk once this warp is well past its last tile
+      while (drained < NCH - 1 && t >= (drained + 1) * CH + CH / 2) drain(drained++);
       const bool tr = lane == 0 && q == 0 && half == 0;
       if (tr) trace_ev(p, t, 2);
       ptx::mbar_wait(&s_full[b], bph);
@@ -282,25 +325,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       if (b >= NB) { b -= NB; bph ^= 1; }
     }
     // ------------------------------------------------------------ output
-    ptx::mbar_wait(y_full, 0);
-    ptx::tc_fence_after();
+    while (drained < NCH) drain(drained++);
     const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
-    const bool valid = lr < p.nrows;
-    for (int ch = g; ch * 32 < p.s_pad; ch += 4) {
-      uint32_t y[32];
-      ptx::tmem_ld32(tmem + lane_off + TM_Y + ch * 32, y);
-      ptx::tmem_wait_ld();
-      if (valid) {
-        const int64_t base = lr * p.s;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int col = ch * 32 + c;
-          if (col < p.s) {
-            double acc = (double)__uint_as_float(y[c]) * (p.out_scale * (double)p.vscale[col]);
-            if (p.gram) acc += p.noise2 * p.V64[gi * p.s + col];
-            p.Y64[base + col] = p.B64 ? p.B64[base + col] - acc : acc;
-          }
-        }
+    if (lr < p.nrows && dc0 < p.s) {
+      const int64_t base = lr * p.s;
+      for (int col = dc0; col < dc0 + 16 && col < p.s; ++col) {
+        double acc = ypart[(size_t)col * BM + r] * (p.out_scale * (double)p.vscale[col]);
+        if (p.gram) acc += p.noise2 * p.V64[gi * p.s + col];
+        p.Y64[base + col] = p.B64 ? p.B64[base + col] - acc : acc;
       }
     }
   }
@@ -431,7 +463,7 @@ void tc_build_operands(const Op& op, DBuf<float>& XA, DBuf<float>& XB, const dou
 size_t tc_smem_bytes(int K1, int s_pad, int* ns_out) {
   const size_t xa = (size_t)tc::BM * K1 * 4;
   const size_t stage = (size_t)tc::BJ * K1 * 4 + 2 * (size_t)s_pad * tc::BJ * 2;
-  const size_t tail = 48 * 8 + 64;
+  const size_t tail = 512 + (size_t)tc::BM * s_pad * 8;  // barriers + fp64 partial Y
   int ns = (int)((227 * 1024 - xa - tail) / stage);
   if (ns > 6) ns = 6;
   *ns_out = ns;

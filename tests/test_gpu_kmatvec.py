@@ -90,3 +90,18 @@ def test_invalid_arguments(W):
         op.append_rows(np.zeros((2, 3)))
     with pytest.raises(ValueError):
         op.kmatvec(np.zeros((4, 1)))
+
+
+@pytest.mark.parametrize("n", [20000, 101000])
+def test_tc_accuracy_scales_with_n(W, n):
+    """Size-independent cross-check at BASELINE scale: the tensor-core path against the fp64
+    CUDA-core path (itself pinned to the oracle at <=1e-10 above), relative error <= 1e-4."""
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, 16))
+    V = rng.standard_normal((n, 4))
+    hyp = W.KernelHyperparams(0.8, 1.0, 1e-3 ** 0.5, 0)
+    Y64 = W.KernelOperator(hyp, X, precision=W.F64).kmatvec(V)
+    Ytc = W.KernelOperator(hyp, X, precision=W.F32_3XTF32).kmatvec(V)
+    err = colrel(Ytc, Y64)
+    print(f"n={n} tc rel err {err:.3e}")
+    assert err <= 1e-4
