@@ -19,7 +19,7 @@ def wop(W, X, h, precision=0):
 
 def test_sgd_same_stream_same_trajectory(W, O):
     h, X, H, b = system(O, 19, 400)
-    kw = dict(method=O.SGD, learning_rate=0.02, batch_size=25, max_iters=300, tolerance=1e-8, seed=1234)
+    kw = dict(method=O.SGD, learning_rate=0.005, batch_size=100, max_iters=300, tolerance=1e-8, seed=1234)
     ref = O.sgd_solve(H, b, O.Initialization.cold(), O.SolverConfig(**kw))
     got = W.sgd_solve(wop(W, X, h), b, W.Initialization.cold(), W.SolverConfig(**kw))
     assert got.iterations == ref.iterations
@@ -30,7 +30,7 @@ def test_sgd_same_stream_same_trajectory(W, O):
 def test_sgd_solve_many_per_column_seeds(W, O):
     h, X, H, b = system(O, 36, 300)
     B = np.stack([b, b, 2 * b], 1)
-    kw = dict(method=O.SGD, learning_rate=0.02, batch_size=10, max_iters=100, tolerance=1e-10, seed=9)
+    kw = dict(method=O.SGD, learning_rate=0.002, batch_size=10, max_iters=100, tolerance=1e-10, seed=9)
     ref = O.solve_many(H, B, [O.Initialization.cold()] * 3, O.SolverConfig(**kw))
     got = W.solve_many(wop(W, X, h), B, [W.Initialization.cold()] * 3, W.SolverConfig(**kw))
     for r, g in zip(ref, got):
@@ -92,7 +92,7 @@ def test_warm_not_worse_than_cold_plus_one(W, O):
 @pytest.mark.parametrize("method", [1, 2])
 def test_f32_path_sgd_ap(W, O, method):
     h, X, H, b = system(O, 44, 1500, dim=4, ls=0.5, noise=0.5)
-    kw = dict(method=method, tolerance=1e-4, max_iters=5000, learning_rate=0.01, batch_size=100, block_size=100)
+    kw = dict(method=method, tolerance=1e-4, max_iters=5000, learning_rate=0.005, batch_size=100, block_size=100)
     ref = O.solve(H, b, O.Initialization.cold(), O.SolverConfig(**kw))
     got = W.solve(wop(W, X, h, precision=W.F32_3XTF32), b, W.Initialization.cold(), W.SolverConfig(**kw))
     assert got.converged
