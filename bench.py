@@ -162,6 +162,44 @@ def run_reference(args):
     return 0
 
 
+# --------------------------------------------------------------------------- CG warm/cold
+def cg_time_to_tolerance(W, ctx, X, prec, hyp, tol=1e-4, seed=0):
+    """BASELINE configs[2]: solve the N=100k system, append 1000 rows, then warm-started
+    ([u; 0], Initialization::warm) vs cold CG to tol on N=101k.  RHS = y + 63 pathwise
+    prior samples: 64 Matern RFF priors (F=2048, sample_prior's Student-t spectral draws)
+    evaluated on the device plus sigma_n N(0,1) noise (build_sample_rhs).  Times are the
+    public solve_many call (host buffers in/out, preconditioner build included)."""
+    import numpy as np
+
+    n = X.shape[0]
+    priors = [W.sample_prior(hyp, DIM, 2048, W.derive_seed(seed, 100 + c)) for c in range(S)]
+    op = W.KernelOperator(hyp, X[:N0], precision=prec, ctx=ctx)
+    full = W.KernelOperator(hyp, X, precision=W.F64, ctx=ctx)  # RFF evaluation host (rows only)
+    B = W.rff_eval(full, priors)
+    del full
+    B += hyp.noise_scale * W.normal_fill(W.derive_seed(seed, 3), n * S).reshape(n, S, order="F")
+    B = np.asfortranarray(B)
+    cfg = W.SolverConfig(tolerance=tol, max_iters=1000, precond_rank=100, precond_shift=hyp.noise_scale ** 2)
+
+    def run(o, rhs, inits):
+        t0 = time.perf_counter()
+        res = W.solve_many(o, rhs, inits, cfg)
+        dt = time.perf_counter() - t0
+        its = [r.iterations for r in res]
+        return res, {"seconds": dt, "iters_max": max(its), "iters_mean": float(np.mean(its)),
+                     "converged": int(sum(r.converged for r in res)),
+                     "final_rel_residual_max": float(max(r.residual_history[-1] for r in res))}
+
+    prev, prev_stats = run(op, np.asfortranarray(B[:N0]), [W.Initialization.cold()] * S)
+    op.append_rows(X[N0:])  # device-resident growth (K8)
+    warm_res, warm = run(op, B, [W.Initialization.warm(r.v) for r in prev])
+    cold_res, cold = run(op, B, [W.Initialization.cold()] * S)
+    return {"n_prev": N0, "n": n, "s": S, "tol": tol, "precond_rank": 100,
+            "prev_solve_n100k": prev_stats, "warm": warm, "cold": cold,
+            "warm_over_cold_time": warm["seconds"] / cold["seconds"],
+            "warm_over_cold_iters": warm["iters_mean"] / max(cold["iters_mean"], 1e-9)}
+
+
 # --------------------------------------------------------------------------- GPU arm
 def run_ours(args):
     import torch
@@ -256,6 +294,10 @@ def run_ours(args):
             "peak_source": f"{peak_kind} bf16_tflops/2 (TF32 dense) from MEASURED_PEAKS.json",
             "kernel": "kmatvec", "algorithmic_flops_per_launch": total_flops / world}
 
+    cg = None
+    if world == 1 and not args.no_cg:
+        cg = cg_time_to_tolerance(W, ctx, X, prec, hyp)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         nthreads = os.cpu_count() or 1
@@ -275,6 +317,7 @@ def run_ours(args):
                        "kernel": "matern32", "lengthscale": LS, "noise_var": NOISE_VAR,
                        "rows_per_rank": r1 - r0, "l2": "flushed (256 MiB memset) before each step"},
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": args.steps,
+            "cg_warm_vs_cold": cg,
             "clocks": clk.summary(), "wall_s": t_wall,
             "step_ms_min": float(np.min(ms)), "step_ms_max": float(np.max(ms)),
         }
@@ -294,6 +337,7 @@ def main():
     ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32", "f32simt", "f64"])
     ap.add_argument("--ref-rows", type=int, default=1000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cg", action="store_true", help="skip the warm/cold CG time-to-tolerance leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
