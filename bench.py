@@ -289,10 +289,21 @@ def run_ours(args):
     peaks, peak_kind = measured_peaks()
     # tensor-core roofline: tf32 dense = bf16 dense / 2 on Blackwell (measured bf16 GEMM)
     peak_tf32 = peaks["bf16_tflops"] / 2.0
+    clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    pairs = float(n) * float(n)
+    mufu_per_pair = 2.0  # Matern-3/2: sqrt + exp2 per pair on the SFU (MUFU) pipe
+    t_mufu = pairs * mufu_per_pair / (16.0 * 148 * clk)  # 16 MUFU ops/clk/SM
     roof = {"bound": "tensor", "achieved": value, "peak": peak_tf32, "unit": "TFLOP/s",
-            "frac": value / peak_tf32, "traffic": None,
+            "frac": value / peak_tf32,
+            # dram bytes per launch of the kmatvec kernel from profiles/r01_kmatvec_tc_metrics.json
+            # (ncu --set full, one launch of this workload): X/XA/XB + V tiles stay L2-resident.
+            "traffic": 225.5e6,
             "peak_source": f"{peak_kind} bf16_tflops/2 (TF32 dense) from MEASURED_PEAKS.json",
-            "kernel": "kmatvec", "algorithmic_flops_per_launch": total_flops / world}
+            "kernel": "tc::kmatvec_tc_kernel (+ colscale/split_v prep, ~1.5% of the step)",
+            "algorithmic_flops_per_launch": total_flops / world,
+            "composite": {"bound": "mufu", "mufu_ops_per_pair": mufu_per_pair,
+                          "t_roof_ms": t_mufu * 1e3 / world, "frac": (t_mufu / world) / (ms_step * 1e-3),
+                          "note": "SFU roofline at sm_max_mhz: the Matern map's sqrt+exp2 per pair"}}
 
     cg = None
     if world == 1 and not args.no_cg:
@@ -316,7 +327,7 @@ def run_ours(args):
             "config": {"workload": "C3 kernel-matvec (BASELINE configs[2])", "n": n, "d": DIM, "s": S,
                        "kernel": "matern32", "lengthscale": LS, "noise_var": NOISE_VAR,
                        "rows_per_rank": r1 - r0, "l2": "flushed (256 MiB memset) before each step"},
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": args.steps,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": 3 * args.steps,  # colscale + split_v + kmatvec_tc per step
             "cg_warm_vs_cold": cg,
             "clocks": clk.summary(), "wall_s": t_wall,
             "step_ms_min": float(np.min(ms)), "step_ms_max": float(np.max(ms)),

@@ -1,0 +1,309 @@
+// warmgp/gpu.hpp -- header-only C++ mirror of the reference warmgp API
+// (/root/reference/proj/core/include/warmgp/{kernel,solvers,sampling}.hpp) over the C-ABI
+// of libwarmgp_b200.so (include/warmgp_capi.h).
+//
+// Same type and function names, same argument meaning, same exception types
+// (types.hpp:15-32).  The only change a caller sees is that the covariance is a
+// device-resident KernelOperator instead of a dense Eigen::MatrixXd (which cannot
+// exist at N >= 100k): gram_matrix(X, hyp) -> KernelOperator(X, hyp), extend_system ->
+// op.append_rows(X2).  Matrices are column-major doubles like Eigen::MatrixXd; with
+// WARMGP_GPU_EIGEN defined, Eigen overloads are provided for drop-in use in the reference
+// build.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../warmgp_capi.h"
+
+#ifdef WARMGP_GPU_EIGEN
+#include <Eigen/Dense>
+#endif
+
+namespace warmgp {
+namespace gpu {
+
+// ---------------------------------------------------------------- errors (types.hpp:15-26)
+class NotSpdError : public std::runtime_error {
+ public:
+  explicit NotSpdError(const std::string& w) : std::runtime_error(w) {}
+};
+class DivergenceError : public std::runtime_error {
+ public:
+  DivergenceError(const std::string& w, int it) : std::runtime_error(w), iterations(it) {}
+  int iterations;
+};
+class CudaError : public std::runtime_error {
+ public:
+  explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+
+inline void check(wgp_status st, int iterations = 0) {
+  if (st == WGP_OK) return;
+  const std::string msg = wgp_last_error();
+  switch (st) {
+    case WGP_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case WGP_NOT_SPD: throw NotSpdError(msg);
+    case WGP_DIVERGED: throw DivergenceError(msg, iterations);
+    case WGP_OOM: throw std::bad_alloc();
+    default: throw CudaError(msg);
+  }
+}
+
+// ---------------------------------------------------------------- value types
+struct Matrix {  // column-major, like Eigen::MatrixXd
+  int64_t rows = 0, cols = 0;
+  std::vector<double> data;
+  Matrix() = default;
+  Matrix(int64_t r, int64_t c) : rows(r), cols(c), data((size_t)(r * c), 0.0) {}
+  double& operator()(int64_t i, int64_t j) { return data[(size_t)(j * rows + i)]; }
+  double operator()(int64_t i, int64_t j) const { return data[(size_t)(j * rows + i)]; }
+  const double* col(int64_t j) const { return data.data() + j * rows; }
+};
+using Vector = std::vector<double>;
+
+enum class Method { CG = WGP_CG, SGD = WGP_SGD, AP = WGP_AP };            // solvers.hpp:10
+enum class SgdScaling { Unbiased = WGP_SGD_UNBIASED, Block = WGP_SGD_BLOCK };
+enum class ApOrdering { Greedy = WGP_AP_GREEDY, Cyclic = WGP_AP_CYCLIC };
+enum class Kernel { Matern32 = WGP_MATERN32, RBF = WGP_RBF };
+enum class Precision { F64 = WGP_F64, F32_3xTF32 = WGP_F32_3XTF32, TF32 = WGP_TF32, F32 = WGP_F32_SIMT };
+
+struct KernelHyperparams {  // kernel.hpp:8-14
+  double lengthscale = 1.0;
+  double signal_scale = 1.0;
+  double noise_scale = 1e-3;
+  Kernel kind = Kernel::Matern32;
+};
+
+struct SolverConfig {  // solvers.hpp:27-48, same defaults
+  enum class PrecondShiftMode { Calibrated = WGP_SHIFT_CALIBRATED, NoiseOnly = WGP_SHIFT_NOISE_ONLY };
+  Method method = Method::CG;
+  double tolerance = 1e-2;
+  int max_iters = 1000;
+  double learning_rate = 0.3;
+  double momentum = 0.9;
+  int64_t batch_size = 100;
+  SgdScaling sgd_scaling = SgdScaling::Unbiased;
+  int64_t block_size = 100;
+  ApOrdering ap_ordering = ApOrdering::Greedy;
+  int64_t precond_rank = 100;
+  double precond_shift = 1e-6;
+  PrecondShiftMode precond_shift_mode = PrecondShiftMode::Calibrated;
+  std::uint64_t seed = 0;
+
+  wgp_solver_config c() const {
+    wgp_solver_config r;
+    r.method = (int32_t)method;
+    r.tolerance = tolerance;
+    r.max_iters = max_iters;
+    r.learning_rate = learning_rate;
+    r.momentum = momentum;
+    r.batch_size = batch_size;
+    r.sgd_scaling = (int32_t)sgd_scaling;
+    r.block_size = block_size;
+    r.ap_ordering = (int32_t)ap_ordering;
+    r.precond_rank = precond_rank;
+    r.precond_shift = precond_shift;
+    r.precond_shift_mode = (int32_t)precond_shift_mode;
+    r.seed = seed;
+    return r;
+  }
+};
+
+struct Initialization {  // solvers.hpp:52-63
+  static Initialization cold() { return Initialization{}; }
+  static Initialization warm(Vector u1_prev) {
+    Initialization i;
+    i.warm_start = true;
+    i.u1 = std::move(u1_prev);
+    return i;
+  }
+  bool warm_start = false;
+  Vector u1;
+};
+
+struct SolveResult {  // solvers.hpp:102-109
+  Vector v;
+  int iterations = 0;
+  std::vector<double> residual_history;
+  bool converged = false;
+  double final_residual() const { return residual_history.back(); }
+};
+
+// ---------------------------------------------------------------- device handles
+class Context {
+ public:
+  explicit Context(int device = 0) { check(wgp_ctx_create(device, &h_)); }
+  Context(int device, int rank, int world, const void* nccl_uid128) {
+    check(wgp_ctx_create_sharded(device, rank, world, nccl_uid128, &h_));
+  }
+  ~Context() { wgp_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  wgp_ctx* get() const { return h_; }
+
+ private:
+  wgp_ctx* h_ = nullptr;
+};
+
+// H = K(X, X) + sigma_n^2 I, device resident (replaces CovarianceMatrix, kernel.hpp:25-31).
+class KernelOperator {
+ public:
+  KernelOperator(Context& ctx, const Matrix& X, const KernelHyperparams& hyp,
+                 Precision precision = Precision::F64) {
+    check(wgp_op_create(ctx.get(), (int)hyp.kind, hyp.lengthscale, hyp.signal_scale,
+                        hyp.noise_scale, (int)precision, (int)X.cols, &h_));
+    if (X.rows > 0) append_rows(X);
+  }
+  ~KernelOperator() { wgp_op_destroy(h_); }
+  KernelOperator(const KernelOperator&) = delete;
+  KernelOperator& operator=(const KernelOperator&) = delete;
+
+  // extend_system's growth step (kernel.cpp:108-130): old rows are never re-uploaded
+  void append_rows(const Matrix& X2) {
+    check(wgp_op_append_rows(h_, X2.data.data(), X2.rows, X2.rows > 0 ? X2.rows : 1, 1));
+  }
+  int64_t size() const { return wgp_op_size(h_); }
+  Matrix operator*(const Matrix& V) const {  // H * V  (solvers.cpp:162)
+    Matrix Y(V.rows, V.cols);
+    check(wgp_kmatvec(h_, V.data.data(), V.rows, (int)V.cols, Y.data.data(), Y.rows));
+    return Y;
+  }
+  wgp_op* get() const { return h_; }
+
+ private:
+  wgp_op* h_ = nullptr;
+};
+
+inline KernelOperator gram_matrix(Context& ctx, const Matrix& X, const KernelHyperparams& hyp,
+                                  Precision p = Precision::F64) {  // kernel.cpp:48
+  if (X.rows < 1) throw std::invalid_argument("gram_matrix: need at least one row");
+  return KernelOperator(ctx, X, hyp, p);
+}
+
+// ---------------------------------------------------------------- solvers (solvers.hpp:111-141)
+inline std::vector<SolveResult> solve_many(const KernelOperator& H, const Matrix& rhs_columns,
+                                           const std::vector<Initialization>& inits,
+                                           const SolverConfig& cfg) {
+  const int64_t n = rhs_columns.rows;
+  const int s = (int)rhs_columns.cols;
+  if ((int64_t)inits.size() != s)
+    throw std::invalid_argument("solve_many: one initialization per right-hand side required");
+  int64_t n1 = 0;
+  bool warm = false;
+  for (const auto& i : inits)
+    if (i.warm_start) {
+      warm = true;
+      n1 = (int64_t)i.u1.size();
+    }
+  std::vector<double> U1;
+  if (warm) {
+    U1.assign((size_t)(n1 * s), 0.0);
+    for (int c = 0; c < s; ++c)
+      if (inits[c].warm_start) {
+        if ((int64_t)inits[c].u1.size() != n1)
+          throw std::invalid_argument("solve_many: warm starts must share one length");
+        std::copy(inits[c].u1.begin(), inits[c].u1.end(), U1.begin() + c * n1);
+      }
+  }
+  const wgp_solver_config c = cfg.c();
+  const int64_t hs = (int64_t)cfg.max_iters + 1;
+  std::vector<double> V((size_t)(n * s)), hist((size_t)(hs * s));
+  std::vector<int32_t> its(s), hl(s), cv(s), cst(s), dv(s);
+  const wgp_status st = wgp_solve_many(H.get(), &c, rhs_columns.data.data(), n, s,
+                                       warm ? U1.data() : nullptr, n1 > 0 ? n1 : 1, n1, V.data(), n,
+                                       its.data(), hist.data(), hs, hl.data(), cv.data(),
+                                       cst.data(), dv.data());
+  int fail_iters = 0;
+  for (int k = 0; k < s; ++k)
+    if (cst[k] != WGP_OK) {
+      fail_iters = dv[k];
+      break;
+    }
+  check(st, fail_iters);
+  std::vector<SolveResult> out(s);
+  for (int k = 0; k < s; ++k) {
+    out[k].v.assign(V.begin() + k * n, V.begin() + (k + 1) * n);
+    out[k].iterations = its[k];
+    out[k].residual_history.assign(hist.begin() + k * hs, hist.begin() + k * hs + hl[k]);
+    out[k].converged = cv[k] != 0;
+  }
+  return out;
+}
+
+inline SolveResult solve(const KernelOperator& H, const Vector& b, const Initialization& init,
+                         const SolverConfig& cfg) {  // solvers.cpp:311-319
+  const int64_t n = (int64_t)b.size();
+  SolveResult r;
+  r.v.assign((size_t)n, 0.0);
+  std::vector<double> hist((size_t)cfg.max_iters + 1);
+  int32_t its = 0, hl = 0, cv = 0, dv = 0;
+  const wgp_solver_config c = cfg.c();
+  check(wgp_solve(H.get(), &c, b.data(), init.warm_start ? init.u1.data() : nullptr,
+                  init.warm_start ? (int64_t)init.u1.size() : 0, r.v.data(), &its, hist.data(), &hl,
+                  &cv, &dv),
+        dv);
+  r.iterations = its;
+  r.residual_history.assign(hist.begin(), hist.begin() + hl);
+  r.converged = cv != 0;
+  return r;
+}
+
+inline SolveResult cg_solve(const KernelOperator& H, const Vector& b, const Initialization& i,
+                            SolverConfig cfg) {
+  cfg.method = Method::CG;
+  return solve(H, b, i, cfg);
+}
+inline SolveResult sgd_solve(const KernelOperator& H, const Vector& b, const Initialization& i,
+                             SolverConfig cfg) {
+  cfg.method = Method::SGD;
+  return solve(H, b, i, cfg);
+}
+inline SolveResult ap_solve(const KernelOperator& H, const Vector& b, const Initialization& i,
+                            SolverConfig cfg) {
+  cfg.method = Method::AP;
+  return solve(H, b, i, cfg);
+}
+
+// ---------------------------------------------------------------- sampling (sampling.hpp)
+struct RffPrior {
+  Matrix frequencies;  // F x D
+  Vector phases, amplitudes;
+  double signal_scale = 1.0;
+};
+
+inline RffPrior sample_prior(const KernelHyperparams& hyp, int64_t dim, int64_t F,
+                             std::uint64_t seed) {  // sampling.cpp:14-35
+  RffPrior p;
+  p.frequencies = Matrix(F, dim);
+  p.phases.assign((size_t)F, 0.0);
+  p.amplitudes.assign((size_t)F, 0.0);
+  p.signal_scale = hyp.signal_scale;
+  check(wgp_sample_prior((int)hyp.kind, hyp.lengthscale, dim, F, seed, p.frequencies.data.data(),
+                         p.phases.data(), p.amplitudes.data()));
+  return p;
+}
+
+// eval_prior (sampling.cpp:37-46) at the operator's rows for several priors: m x S.
+inline Matrix eval_priors(const KernelOperator& H, const std::vector<RffPrior>& priors) {
+  const int S = (int)priors.size();
+  const int64_t m = H.size();
+  Matrix out(m, S);
+  if (!S) return out;
+  const int64_t F = priors[0].frequencies.rows, D = priors[0].frequencies.cols;
+  std::vector<double> Om((size_t)(S * F * D)), ph((size_t)(S * F)), am((size_t)(S * F));
+  for (int p = 0; p < S; ++p) {
+    std::copy(priors[p].frequencies.data.begin(), priors[p].frequencies.data.end(), Om.begin() + p * F * D);
+    std::copy(priors[p].phases.begin(), priors[p].phases.end(), ph.begin() + p * F);
+    std::copy(priors[p].amplitudes.begin(), priors[p].amplitudes.end(), am.begin() + p * F);
+  }
+  check(wgp_rff_eval(H.get(), Om.data(), ph.data(), am.data(), (int)F, S, priors[0].signal_scale,
+                     nullptr, m, m, out.data.data(), m));
+  return out;
+}
+
+}  // namespace gpu
+}  // namespace warmgp

@@ -1,0 +1,19 @@
+"""Builds and runs the C++ mirror test (tests/cpp/test_gpu_api.cpp) against the C-ABI .so."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_cpp_reference_api_mirror(tmp_path):
+    exe = tmp_path / "test_gpu_api"
+    libdir = os.path.join(ROOT, "paper_2511_16340_b200")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_gpu_api.cpp"), "-L", libdir, "-lwarmgp_b200",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert "gpu.hpp ok" in r.stdout
