@@ -289,10 +289,10 @@ def run_ours(args):
     peaks, peak_kind = measured_peaks()
     # tensor-core roofline: tf32 dense = bf16 dense / 2 on Blackwell (measured bf16 GEMM)
     peak_tf32 = peaks["bf16_tflops"] / 2.0
-    clk = peaks.get("sm_max_mhz", 1965.0) * 1e6
+    sm_hz = peaks.get("sm_max_mhz", 1965.0) * 1e6
     pairs = float(n) * float(n)
     mufu_per_pair = 2.0  # Matern-3/2: sqrt + exp2 per pair on the SFU (MUFU) pipe
-    t_mufu = pairs * mufu_per_pair / (16.0 * 148 * clk)  # 16 MUFU ops/clk/SM
+    t_mufu = pairs * mufu_per_pair / (16.0 * 148 * sm_hz)  # 16 MUFU ops/clk/SM
     roof = {"bound": "tensor", "achieved": value, "peak": peak_tf32, "unit": "TFLOP/s",
             "frac": value / peak_tf32,
             # dram bytes per launch of the kmatvec kernel from profiles/r01_kmatvec_tc_metrics.json

@@ -101,7 +101,7 @@ struct Op {
   // tensor-core path: tiled 3xTF32 operand rows (rebuilt lazily after appends), the
   // translation applied before forming them, and per-call V staging.
   DBuf<float> XA, XB, vt;
-  DBuf<double> center, vchunk, ychunk;
+  DBuf<double> center, vchunk, ychunk, ysplit;
   std::vector<double> h_center;
   bool tc_dirty = true;
   KParams kp() const {

@@ -26,6 +26,7 @@
 // (S written by GEMM1, overwritten in place by K for GEMM2); mbarriers + tcgen05.commit.
 #include <cuda_fp16.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
@@ -62,6 +63,8 @@ struct Params {
   double* Y64;          // [nrows][s]
   int64_t nrows, row0, ncols;
   int ntiles;           // ceil(ncols / BJ)
+  int tiles_per_split;  // j tiles per CTA along grid.y (2-D decomposition)
+  double* Ysplit;       // nullptr: full output; else fp64 partials [gridDim.y][nrows][s]
   int s, s_pad, K1;
   int kind;
   float c1, neg_c_log2e;
@@ -72,7 +75,7 @@ struct Params {
 };
 
 __device__ __forceinline__ void trace_ev(const Params& p, int t, int slot) {
-  if (p.trace && blockIdx.x == 0) p.trace[(size_t)t * 8 + slot] = clock64();
+  if (p.trace && blockIdx.x == 0 && blockIdx.y == 0) p.trace[(size_t)t * 8 + slot] = clock64();
 }
 
 __device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
@@ -104,7 +107,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   double* ypart = reinterpret_cast<double*>(smem + (size_t)(XA_BYTES + NS * ST_BYTES + 512));
   constexpr int NB = MAX_NB;
   constexpr uint32_t TM_Y = 384;         // Y accumulator a at TM_Y + 64 a
-  const int NCH = (p.ntiles + CH - 1) / CH;
+  // this CTA's j range: tiles [jt0, jt0 + T) of the column sweep
+  const int jt0 = blockIdx.y * p.tiles_per_split;
+  const int T = min(p.ntiles - jt0, p.tiles_per_split);
+  const int NCH = (T + CH - 1) / CH;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -129,7 +135,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int T = p.ntiles;
   const int KS1 = p.K1 / 8;                 // GEMM1 K-steps (tf32: 8 per instruction)
   const uint32_t sbo1 = (p.K1 / 4) * 128;   // 8-row group stride of XA/XB tiles
 
@@ -142,8 +147,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     }
     int st = 0;
     uint32_t ph = 0;
-    const float* xb_src = p.XB;
-    const __half* vt_src = p.Vt;
+    const float* xb_src = p.XB + (size_t)jt0 * BJ * p.K1;
+    const __half* vt_src = p.Vt + (size_t)jt0 * 2 * p.s_pad * BJ;
     for (int t = 0; t < T; ++t) {
       if (t >= NS) ptx::mbar_wait(&stage_empty[st], ph ^ 1);
       if (leader) {
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
           kv[c] = ptx::ex2_approx(fmaf(d2, p.neg_c_log2e, KSCALE_LOG2));  // 2^10 e^{-d2/2l^2}
         }
       }
-      const int64_t gj0 = (int64_t)t * BJ + half * 32;
+      const int64_t gj0 = (int64_t)(jt0 + t) * BJ + half * 32;
       if (p.gram && gj0 < grow0 + BM && gj0 + 32 > grow0) {  // tile touches the diagonal
 #pragma unroll
         for (int c = 0; c < 32; ++c)
@@ -329,10 +334,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
     if (lr < p.nrows && dc0 < p.s) {
       const int64_t base = lr * p.s;
-      for (int col = dc0; col < dc0 + 16 && col < p.s; ++col) {
-        double acc = ypart[(size_t)col * BM + r] * (p.out_scale * (double)p.vscale[col]);
-        if (p.gram) acc += p.noise2 * p.V64[gi * p.s + col];
-        p.Y64[base + col] = p.B64 ? p.B64[base + col] - acc : acc;
+      if (p.Ysplit) {  // partial over this CTA's j range; reduce_splits adds the rest
+        double* dst = p.Ysplit + (size_t)blockIdx.y * p.nrows * p.s + base;
+        for (int col = dc0; col < dc0 + 16 && col < p.s; ++col)
+          dst[col] = ypart[(size_t)col * BM + r] * (p.out_scale * (double)p.vscale[col]);
+      } else {
+        for (int col = dc0; col < dc0 + 16 && col < p.s; ++col) {
+          double acc = ypart[(size_t)col * BM + r] * (p.out_scale * (double)p.vscale[col]);
+          if (p.gram) acc += p.noise2 * p.V64[gi * p.s + col];
+          p.Y64[base + col] = p.B64 ? p.B64[base + col] - acc : acc;
+        }
       }
     }
   }
@@ -435,10 +446,42 @@ __global__ void split_v_kernel(const double* __restrict__ V, int64_t ncols, int 
   }
 }
 
+// Y = sum over j-splits (fixed order) + sigma^2 V_i (gram), or B - that.
+__global__ void reduce_splits_kernel(const double* __restrict__ Ysplit, int nsplit, int64_t nrows,
+                                     int64_t row0, int s, const double* __restrict__ V64,
+                                     const double* __restrict__ B64, double noise2, int gram,
+                                     double* __restrict__ Y64) {
+  const int64_t total = nrows * s;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < nsplit; ++q) acc += Ysplit[(size_t)q * total + e];
+    if (gram) acc += noise2 * V64[row0 * s + e];
+    Y64[e] = B64 ? B64[e] - acc : acc;
+  }
+}
+
 inline int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
   return (int)(g < 1 ? 1 : g);
+}
+
+// Number of j splits: pad the grid to a near-integral number of waves of 148 SMs
+// (one CTA per SM), keeping >= 32 tiles per split.
+inline int choose_splits(int row_ctas, int ntiles) {
+  int best = 1;
+  double best_cost = 1e30;
+  for (int k = 1; k <= 16; ++k) {
+    if (k > 1 && ntiles / k < 32) break;
+    const double w = (double)row_ctas * k / 148.0;
+    const double cost = std::ceil(w) / w * (1.0 + 0.01 * (k - 1));
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = k;
+    }
+  }
+  return best;
 }
 
 }  // namespace tc
@@ -481,7 +524,7 @@ bool tc_supported(int dim) {
 void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int64_t nrows,
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
-                       DBuf<double>& ychunk, cudaStream_t st) {
+                       DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st) {
   if (nrows <= 0 || s <= 0) return;
   const int K1 = tc_k1(op.dim);
   const KParams kp = op.kp();
@@ -527,6 +570,16 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
     prm.row0 = row0;
     prm.ncols = ncols;
     prm.ntiles = ntiles;
+    const int row_ctas = (int)((nrows + tc::BM - 1) / tc::BM);
+    static const int forced_splits = getenv("WGP_TC_SPLITS") ? atoi(getenv("WGP_TC_SPLITS")) : 0;
+    const int nsplit = forced_splits > 0 ? forced_splits : tc::choose_splits(row_ctas, ntiles);
+    prm.tiles_per_split = (ntiles + nsplit - 1) / nsplit;
+    const int gy = (ntiles + prm.tiles_per_split - 1) / prm.tiles_per_split;
+    prm.Ysplit = nullptr;
+    if (gy > 1) {
+      ysplit.ensure((size_t)gy * nrows * sc);
+      prm.Ysplit = ysplit.p;
+    }
     prm.s = sc;
     prm.s_pad = s_pad;
     prm.K1 = K1;
@@ -549,9 +602,13 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
     WGP_REQUIRE(ns >= 2, "kmatvec_tc: dim %d too large for the shared-memory pipeline", op.dim);
     WGP_CUDA(cudaFuncSetAttribute(tc::kmatvec_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-    const int grid = (int)((nrows + tc::BM - 1) / tc::BM);
-    tc::kmatvec_tc_kernel<<<grid, tc::NTHREADS, smem, st>>>(prm, ns);
+    tc::kmatvec_tc_kernel<<<dim3(row_ctas, gy), tc::NTHREADS, smem, st>>>(prm, ns);
     WGP_CUDA(cudaGetLastError());
+    if (gy > 1) {
+      tc::reduce_splits_kernel<<<tc::grid_for(nrows * sc), 256, 0, st>>>(
+          ysplit.p, gy, nrows, row0, sc, Vc, Bc, kp.noise2, gram ? 1 : 0, Yc);
+      WGP_CUDA(cudaGetLastError());
+    }
     if (trace_path) {
       std::vector<unsigned long long> h((size_t)ntiles * 8);
       WGP_CUDA(cudaMemcpyAsync(h.data(), trace_buf.p, sizeof(unsigned long long) * h.size(),

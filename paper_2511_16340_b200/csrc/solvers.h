@@ -39,7 +39,7 @@ void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0,
 void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int64_t nrows,
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
-                       DBuf<double>& ychunk, cudaStream_t st);
+                       DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st);
 void tc_build_operands(const Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
                        cudaStream_t st);
 int tc_k1(int dim);
