@@ -238,6 +238,8 @@ def run_ours(args):
     sp = stream.cuda_stream
 
     def step():
+        if world > 1:  # the exchange step of a sharded matvec: all-gather the V row slices
+            ctx.allgather_rows_dev(V.data_ptr(), n, S, sp)
         op.kmatvec_dev(V.data_ptr(), Y.data_ptr(), S, sp)
 
     for _ in range(args.warmup):

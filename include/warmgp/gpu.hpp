@@ -192,6 +192,7 @@ inline std::vector<SolveResult> solve_many(const KernelOperator& H, const Matrix
   const int s = (int)rhs_columns.cols;
   if ((int64_t)inits.size() != s)
     throw std::invalid_argument("solve_many: one initialization per right-hand side required");
+  if (n != H.size()) throw std::invalid_argument("solve_many: rhs rows != operator size");
   int64_t n1 = 0;
   bool warm = false;
   for (const auto& i : inits)
@@ -237,6 +238,7 @@ inline std::vector<SolveResult> solve_many(const KernelOperator& H, const Matrix
 inline SolveResult solve(const KernelOperator& H, const Vector& b, const Initialization& init,
                          const SolverConfig& cfg) {  // solvers.cpp:311-319
   const int64_t n = (int64_t)b.size();
+  if (n != H.size()) throw std::invalid_argument("solve: rhs length != operator size");
   SolveResult r;
   r.v.assign((size_t)n, 0.0);
   std::vector<double> hist((size_t)cfg.max_iters + 1);

@@ -13,8 +13,8 @@
  * types.hpp:9-11): host matrices are column-major fp64 with an explicit
  * leading dimension; right-hand sides are N x s with one RHS per column.
  * Device-resident buffers (the *_dev entry points) are row-major N x s
- * ("RHS-interleaved") in the operator's compute type (double for WGP_F64,
- * float otherwise).
+ * ("RHS-interleaved") fp64 for every precision; the precision selects the
+ * arithmetic inside the kernel-matvec.
  *
  * Threading: calls on one handle are serialised by the caller (one stream per
  * device context); distinct contexts may be used concurrently.  Every call
@@ -99,6 +99,10 @@ wgp_status wgp_nccl_unique_id(void* out128);
 wgp_status wgp_ctx_create_sharded(int device, int rank, int world, const void* unique_id128,
                                   wgp_ctx** out);
 void wgp_ctx_destroy(wgp_ctx* ctx);
+/* In-place all-gather of row slices: dV is a full n x s row-major fp64 buffer on every
+ * rank, rank r holding valid rows wgp_shard_range(n, world, r); afterwards all rows are
+ * valid everywhere (NCCL over NVLink; the exchange step of a sharded matvec). */
+wgp_status wgp_allgather_rows_dev(wgp_ctx* ctx, void* dV, int64_t n, int s, void* stream);
 /* cudaStream_t the context launches on (for device-pointer callers). */
 void* wgp_ctx_stream(wgp_ctx* ctx);
 

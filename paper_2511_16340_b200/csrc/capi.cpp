@@ -54,7 +54,9 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
                       SolveOutputs& out, bool derive_seeds) {
   cudaStream_t st = op.ctx->stream;
   SolverWork<double> w;
-  w.alloc(op.n, s);
+  w.alloc(op, s);
+  WGP_REQUIRE(op.ctx->world == 1 || cfg.method == WGP_CG,
+              "sharded contexts support CG solves (SGD/AP: one GPU per operator)");
   upload_problem<double>(op, w, B, ldb, U1, ldu, n1, st);
   switch (cfg.method) {
     case WGP_CG: {
@@ -64,7 +66,11 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
         build_pivoted_cholesky(op, rank, pd, st);
         finish_preconditioner(op, cfg.precond_shift, cfg.precond_shift_mode, pd, st);
       } else {
+        int64_t a, b;
+        op.local_rows(&a, &b);
         pd.n = op.n;
+        pd.r0 = a;
+        pd.n_local = b - a;
       }
       cg_solve_batched<double>(op, cfg, pd, w, out, st);
       break;
@@ -328,7 +334,6 @@ static wgp_status solve_impl(wgp_op* op, const wgp_solver_config* cfg, const dou
       WGP_REQUIRE(n1 <= n, "initialization longer than the system");  // solvers.cpp:46
       WGP_REQUIRE(n1 >= 0 && (n1 == 0 || ldu >= n1), "solve_many: bad warm-start shape");
     }
-    WGP_REQUIRE(op->ctx->world == 1, "wgp_solve_many: sharded solves go through wgp_solve_many_dist");
     if (s == 0) return;
     set_device(*op->ctx);
     SolveOutputs out(s);

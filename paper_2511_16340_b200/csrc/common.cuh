@@ -122,6 +122,16 @@ struct Op {
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// ------------------------------------------------------------------ collectives (dist.cpp)
+// All are no-ops (or local copies) when ctx.world == 1.
+void dist_allgather_rows(const Ctx& ctx, void* full, int64_t n, int64_t row_elems, size_t esize,
+                         cudaStream_t st);
+void dist_allgather_chunks(const Ctx& ctx, double* part, int64_t n, int64_t per_chunk,
+                           cudaStream_t st);
+void dist_broadcast(const Ctx& ctx, void* buf, size_t bytes, int root, cudaStream_t st);
+void dist_allgather(const Ctx& ctx, const double* in, double* out, size_t count, cudaStream_t st);
+int owner_rank(const Ctx& ctx, int64_t n, int64_t row);
+
 // ------------------------------------------------------------------ launchers
 // vecops.cu
 void launch_colmajor_to_rows(const double* src, int64_t ld, int64_t n, int s, void* dst,
@@ -142,6 +152,7 @@ void launch_fill(T* p, T v, size_t count, cudaStream_t st);
 // precond.cu
 struct PrecondDev {
   int64_t n = 0, k = 0, kpad = 0;
+  int64_t r0 = 0, n_local = 0;  // this rank's rows of L / M
   double shift = 1.0;
   DBuf<double> L;    // [n][kpad] row-major (pivoted Cholesky factor)
   DBuf<double> M64;  // [n][kpad]  M = L C^{-T}, C = chol(shift I + L^T L): M M^T = L cap^{-1} L^T
@@ -149,8 +160,8 @@ struct PrecondDev {
 void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStream_t st);
 void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd, cudaStream_t st);
 template <typename T>
-void precond_apply(const PrecondDev& pd, const T* R, T* Z, int s, double* work_t, double* work_part,
-                   cudaStream_t st);
+void precond_apply(const Op& op, const PrecondDev& pd, const T* R, T* Z, int s, double* work_t,
+                   double* work_part, cudaStream_t st);
 
 
 }  // namespace wgp

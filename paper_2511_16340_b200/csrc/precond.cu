@@ -37,12 +37,12 @@ __device__ __forceinline__ ArgBest better(ArgBest a, ArgBest b) {
 }
 
 __global__ void argmax_partial_kernel(const double* __restrict__ d, const int* __restrict__ used,
-                                      int64_t n, double floor_, double* __restrict__ pv,
+                                      int64_t n, int64_t r0, double floor_, double* __restrict__ pv,
                                       int64_t* __restrict__ pi) {
   ArgBest b{0.0, -1};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (!used[i] && d[i] > floor_) b = better(b, ArgBest{d[i], i});
+    if (!used[i] && d[i] > floor_) b = better(b, ArgBest{d[i], r0 + i});
   }
   __shared__ double sv[256];
   __shared__ int64_t si[256];
@@ -64,10 +64,9 @@ __global__ void argmax_partial_kernel(const double* __restrict__ d, const int* _
   }
 }
 
-// Single block: final argmax; writes the pivot index and root = sqrt(d[piv]).
+// Single block: this rank's best (value, global index) as two doubles (index -1: none).
 __global__ void argmax_final_kernel(const double* __restrict__ pv, const int64_t* __restrict__ pi,
-                                    int nb, const double* __restrict__ d,
-                                    int64_t* __restrict__ piv_out, double* __restrict__ root_out) {
+                                    int nb, double* __restrict__ best2) {
   __shared__ double sv[256];
   __shared__ int64_t si[256];
   ArgBest b{0.0, -1};
@@ -85,24 +84,30 @@ __global__ void argmax_final_kernel(const double* __restrict__ pv, const int64_t
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    *piv_out = si[0];
-    *root_out = si[0] >= 0 ? sqrt(d[si[0]]) : 0.0;
+    best2[0] = sv[0];
+    best2[1] = (double)si[0];
   }
 }
 
-// One pivoted-Cholesky step for every row i (solvers.cpp:93-103).
+// Owner of the pivot row: lpiv[0..k) = L[piv, :k], lpiv[k] = sqrt(d[piv]).
+__global__ void fill_pivot_kernel(const double* __restrict__ L, const double* __restrict__ d,
+                                  int64_t li, int k, int kpad, double* __restrict__ lpiv) {
+  for (int t = threadIdx.x; t < k; t += blockDim.x) lpiv[t] = L[li * kpad + t];
+  if (threadIdx.x == 0) lpiv[k] = sqrt(d[li]);
+}
+
+// One pivoted-Cholesky step for every local row (solvers.cpp:93-103); the pivot row of L
+// and root = sqrt(d[piv]) arrive in lpiv (broadcast from the owning rank).
 __global__ void pchol_step_kernel(const double* __restrict__ X, const double* __restrict__ sq,
-                                  int64_t n, int dpad, int dim, KParams p, int k, int kpad,
-                                  const int64_t* __restrict__ piv_p,
-                                  const double* __restrict__ root_p, double* __restrict__ L,
-                                  double* __restrict__ d, int* __restrict__ used) {
-  const int64_t piv = *piv_p;
-  if (piv < 0) return;
-  const double root = *root_p;
+                                  int64_t n_local, int64_t r0, int dpad, int dim, KParams p, int k,
+                                  int kpad, int64_t piv, const double* __restrict__ lpiv,
+                                  double* __restrict__ L, double* __restrict__ d,
+                                  int* __restrict__ used) {
+  const double root = lpiv[k];
   const double* xp = X + piv * dpad;
-  const double* Lp = L + piv * kpad;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < n_local;
+       li += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = r0 + li;
     double h;
     if (i == piv) {
       h = p.s2 + p.noise2;
@@ -112,26 +117,26 @@ __global__ void pchol_step_kernel(const double* __restrict__ X, const double* __
       for (int t = 0; t < dim; ++t) g += xi[t] * xp[t];
       h = kmap64(sq[i] + sq[piv] - 2.0 * g, p);
     }
-    double* Li = L + i * kpad;
+    double* Li = L + li * kpad;
     double col = h;
-    for (int t = 0; t < k; ++t) col -= Li[t] * Lp[t];
+    for (int t = 0; t < k; ++t) col -= Li[t] * lpiv[t];
     const double lik = (i == piv) ? root : col / root;
     Li[k] = lik;
     if (i == piv) {
-      used[i] = 1;
-      d[i] = 0.0;
-    } else if (!used[i]) {
-      d[i] -= lik * lik;
+      used[li] = 1;
+      d[li] = 0.0;
+    } else if (!used[li]) {
+      d[li] -= lik * lik;
     }
   }
 }
 
-// Per-block partial of G = A^T A over a contiguous slab of rows (fixed assignment).
-__global__ void gram_partial_kernel(const double* __restrict__ A, int64_t n, int k, int kpad,
-                                    double* __restrict__ part) {
-  const int nb = gridDim.x;
-  const int64_t per = (n + nb - 1) / nb;
-  const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+// Per-chunk partial of G = A^T A (A local rows [n_local][kpad]); chunk q of the local rows
+// is global chunk c0 + q, so the fixed-order sum over chunks is world-size independent.
+__global__ void gram_chunk_kernel(const double* __restrict__ A, int64_t n_local, int k, int kpad,
+                                  double* __restrict__ part) {
+  const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
+  const int64_t r1 = min(n_local, r0 + (int64_t)kChunkRows);
   double* out = part + (int64_t)blockIdx.x * k * k;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
     const int a = e / k, b = e % k;
@@ -251,32 +256,55 @@ inline int grid_rows(int64_t n) {
 void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStream_t st) {
   const int64_t n = op.n;
   WGP_REQUIRE(rank >= 0 && rank <= n, "pivoted_cholesky: rank out of range");
+  int64_t r0, r1;
+  op.local_rows(&r0, &r1);
+  const int64_t nl = r1 - r0;
+  const Ctx& ctx = *op.ctx;
   pd.n = n;
+  pd.r0 = r0;
+  pd.n_local = nl;
   pd.k = 0;
   pd.kpad = rank > 0 ? ((rank + 3) / 4) * 4 : 0;
   if (rank == 0) return;
-  pd.L.alloc((size_t)n * pd.kpad);
-  WGP_CUDA(cudaMemsetAsync(pd.L.p, 0, sizeof(double) * n * pd.kpad, st));
+  pd.L.alloc((size_t)std::max<int64_t>(nl, 1) * pd.kpad);
+  WGP_CUDA(cudaMemsetAsync(pd.L.p, 0, sizeof(double) * std::max<int64_t>(nl, 1) * pd.kpad, st));
   const KParams p = op.kp();
   const double dval = p.s2 + p.noise2;  // stationary kernels: every diagonal entry is equal
-  DBuf<double> d(n);
-  DBuf<int> used(n);
-  launch_fill<double>(d.p, dval, n, st);
-  WGP_CUDA(cudaMemsetAsync(used.p, 0, sizeof(int) * n, st));
+  DBuf<double> d(std::max<int64_t>(nl, 1));
+  DBuf<int> used(std::max<int64_t>(nl, 1));
+  launch_fill<double>(d.p, dval, nl, st);
+  WGP_CUDA(cudaMemsetAsync(used.p, 0, sizeof(int) * std::max<int64_t>(nl, 1), st));
   const double floor_ = 1e-12 * (dval > 0.0 ? dval : 0.0);  // solvers.cpp:77
   const int nb = 148 * 2;
-  DBuf<double> pv(nb), root(1);
-  DBuf<int64_t> pi(nb), piv(1);
-  int64_t hpiv = -1;
+  DBuf<double> pv(nb), best2(2), all2((size_t)2 * ctx.world), lpiv(pd.kpad + 1);
+  DBuf<int64_t> pi(nb);
+  std::vector<double> h_all((size_t)2 * ctx.world);
   for (int64_t k = 0; k < rank; ++k) {
-    argmax_partial_kernel<<<nb, 256, 0, st>>>(d.p, used.p, n, floor_, pv.p, pi.p);
-    argmax_final_kernel<<<1, 256, 0, st>>>(pv.p, pi.p, nb, d.p, piv.p, root.p);
-    WGP_CUDA(cudaMemcpyAsync(&hpiv, piv.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    argmax_partial_kernel<<<nb, 256, 0, st>>>(d.p, used.p, nl, r0, floor_, pv.p, pi.p);
+    argmax_final_kernel<<<1, 256, 0, st>>>(pv.p, pi.p, nb, best2.p);
+    dist_allgather(ctx, best2.p, all2.p, 2, st);
+    WGP_CUDA(cudaMemcpyAsync(h_all.data(), all2.p, sizeof(double) * h_all.size(),
+                             cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
-    if (hpiv < 0) break;  // no positive pivot beyond the floor (solvers.cpp:91)
-    pchol_step_kernel<<<grid_rows(n), 256, 0, st>>>(op.X64.p, op.sq64.p, n, op.dpad, op.dim, p,
-                                                    (int)k, (int)pd.kpad, piv.p, root.p, pd.L.p,
-                                                    d.p, used.p);
+    // global argmax: strict '>' scan order == larger value, then lower index
+    int64_t piv = -1;
+    double bv = 0.0;
+    for (int r = 0; r < ctx.world; ++r) {
+      const int64_t idx = (int64_t)h_all[2 * r + 1];
+      if (idx < 0) continue;
+      const double v = h_all[2 * r];
+      if (piv < 0 || v > bv || (v == bv && idx < piv)) {
+        piv = idx;
+        bv = v;
+      }
+    }
+    if (piv < 0) break;  // no positive pivot beyond the floor (solvers.cpp:91)
+    const int owner = owner_rank(ctx, n, piv);
+    if (owner == ctx.rank) fill_pivot_kernel<<<1, 128, 0, st>>>(pd.L.p, d.p, piv - r0, (int)k, (int)pd.kpad, lpiv.p);
+    dist_broadcast(ctx, lpiv.p, sizeof(double) * (pd.kpad + 1), owner, st);
+    pchol_step_kernel<<<grid_rows(std::max<int64_t>(nl, 1)), 256, 0, st>>>(
+        op.X64.p, op.sq64.p, nl, r0, op.dpad, op.dim, p, (int)k, (int)pd.kpad, piv, lpiv.p, pd.L.p,
+        d.p, used.p);
     WGP_CUDA(cudaGetLastError());
     pd.k = k + 1;
   }
@@ -287,10 +315,14 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   const int k = (int)pd.k;
   if (k == 0) return;
   const KParams p = op.kp();
-  const int nb = 148;
-  DBuf<double> part((size_t)nb * k * k), G((size_t)k * k);
-  gram_partial_kernel<<<nb, 256, 0, st>>>(pd.L.p, n, k, (int)pd.kpad, part.p);
-  sum_partials_kernel<<<ceil_div((int64_t)k * k, 256), 256, 0, st>>>(part.p, nb, k * k, G.p);
+  const int nch = ceil_div(n, kChunkRows);
+  const int c0 = (int)(pd.r0 / kChunkRows);
+  DBuf<double> part((size_t)nch * k * k), G((size_t)k * k);
+  if (pd.n_local > 0)
+    gram_chunk_kernel<<<ceil_div(pd.n_local, kChunkRows), 256, 0, st>>>(pd.L.p, pd.n_local, k, (int)pd.kpad,
+                                                                        part.p + (int64_t)c0 * k * k);
+  dist_allgather_chunks(*op.ctx, part.p, n, (int64_t)k * k, st);
+  sum_partials_kernel<<<ceil_div((int64_t)k * k, 256), 256, 0, st>>>(part.p, nch, k * k, G.p);
   WGP_CUDA(cudaGetLastError());
   std::vector<double> cap((size_t)k * k);
   WGP_CUDA(cudaMemcpyAsync(cap.data(), G.p, sizeof(double) * k * k, cudaMemcpyDeviceToHost, st));
@@ -334,42 +366,48 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   }
   DBuf<double> dW((size_t)k * k);
   WGP_CUDA(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
-  pd.M64.alloc((size_t)n * pd.kpad);
+  const int64_t nl = std::max<int64_t>(pd.n_local, 1);
+  pd.M64.alloc((size_t)nl * pd.kpad);
   const size_t smem = sizeof(double) * k * k;
   if (smem > 48 * 1024)
     WGP_CUDA(cudaFuncSetAttribute(apply_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-  apply_upper_kernel<<<grid_rows(n * pd.kpad), 256, smem, st>>>(
-      pd.L.p, dW.p, n, k, (int)pd.kpad, pd.M64.p, nullptr);
+  apply_upper_kernel<<<grid_rows(nl * pd.kpad), 256, smem, st>>>(
+      pd.L.p, dW.p, pd.n_local, k, (int)pd.kpad, pd.M64.p, nullptr);
   WGP_CUDA(cudaGetLastError());
   WGP_CUDA(cudaStreamSynchronize(st));  // dW / part / G are freed on return
 }
 
 template <typename T>
-void precond_apply(const PrecondDev& pd, const T* R, T* Z, int s, double* work_t,
+void precond_apply(const Op& op, const PrecondDev& pd, const T* R, T* Z, int s, double* work_t,
                    double* work_part, cudaStream_t st) {
-  const int64_t n = pd.n;
+  const int64_t nl = pd.n_local;
   const int k = (int)pd.k;
   if (k == 0) {
-    WGP_CUDA(cudaMemcpyAsync(Z, R, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
+    if (nl > 0) WGP_CUDA(cudaMemcpyAsync(Z, R, sizeof(T) * nl * s, cudaMemcpyDeviceToDevice, st));
     return;
   }
   WGP_REQUIRE((int64_t)k * s <= 256 * 64, "preconditioner: rank*s too large (%d*%d)", k, s);
   const T* M = (const T*)pd.M64.p;  // solver vectors are fp64 for every precision
-  const int nch = ceil_div(n, kChunkRows);
+  const int nch = ceil_div(pd.n, kChunkRows);
+  const int c0 = (int)(pd.r0 / kChunkRows);
   const size_t smem1 = sizeof(T) * 32 * (pd.kpad + s);
-  mtr_partial_kernel<T><<<nch, 256, smem1, st>>>(M, R, n, k, (int)pd.kpad, s, work_part);
+  if (nl > 0)
+    mtr_partial_kernel<T><<<ceil_div(nl, kChunkRows), 256, smem1, st>>>(
+        M, R, nl, k, (int)pd.kpad, s, work_part + (int64_t)c0 * k * s);
+  dist_allgather_chunks(*op.ctx, work_part, pd.n, (int64_t)k * s, st);
   sum_partials_kernel<<<ceil_div((int64_t)k * s, 256), 256, 0, st>>>(work_part, nch, k * s, work_t);
   const size_t smem2 = sizeof(T) * k * s;
   if (smem2 > 48 * 1024)
     WGP_CUDA(cudaFuncSetAttribute(woodbury_out_kernel<T>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  woodbury_out_kernel<T><<<grid_rows(n * s), 256, smem2, st>>>(M, R, work_t, n, k, (int)pd.kpad,
-                                                               s, 1.0 / pd.shift, Z);
+  if (nl > 0)
+    woodbury_out_kernel<T><<<grid_rows(nl * s), 256, smem2, st>>>(M, R, work_t, nl, k, (int)pd.kpad,
+                                                                  s, 1.0 / pd.shift, Z);
   WGP_CUDA(cudaGetLastError());
 }
 
-template void precond_apply<double>(const PrecondDev&, const double*, double*, int, double*,
-                                    double*, cudaStream_t);
+template void precond_apply<double>(const Op&, const PrecondDev&, const double*, double*, int,
+                                    double*, double*, cudaStream_t);
 
 }  // namespace wgp

@@ -80,15 +80,20 @@ inline int sgrid(int s) { return (s + 255) / 256; }
 }  // namespace
 
 template <typename T>
-void SolverWork<T>::alloc(int64_t n_, int s_) {
-  n = n_;
+void SolverWork<T>::alloc(const Op& op, int s_) {
+  int64_t a, b;
+  op.local_rows(&a, &b);
+  N = op.n;
+  r0 = a;
+  n = b - a;
   s = s_;
-  nch = ceil_div(n, kChunkRows);
-  const size_t ns = (size_t)n * s;
-  V.alloc(ns);
+  nch = ceil_div(N, kChunkRows);
+  c0 = (int)(r0 / kChunkRows);
+  const size_t ns = (size_t)std::max<int64_t>(n, 1) * s, Ns = (size_t)N * s;
+  V.alloc(Ns);
+  P.alloc(Ns);
   R.alloc(ns);
   Z.alloc(ns);
-  P.alloc(ns);
   HP.alloc(ns);
   B.alloc(ns);
   part.alloc((size_t)(nch > 0 ? nch : 1) * 2 * s);
@@ -101,13 +106,15 @@ void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb
                     int64_t ldu, int64_t n1, cudaStream_t st) {
   const int64_t n = w.n;
   const int s = w.s;
-  // B: host column-major -> device staging (fp64 col-major) -> row-major T
-  DBuf<double> stage((size_t)std::max<int64_t>(n, 1) * s);
-  WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, B, sizeof(double) * ldb,
-                             sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
-  launch_colmajor_to_rows(stage.p, n, n, s, w.B.p, true, st);
-  WGP_CUDA(cudaMemsetAsync(w.V.p, 0, sizeof(T) * n * s, st));
-  if (U1 && n1 > 0) {  // expand_init: [u1; 0] (solvers.cpp:43-48)
+  // B: this rank's rows of the host column-major matrix -> row-major on the device
+  DBuf<double> stage((size_t)std::max<int64_t>(std::max(n, n1), 1) * s);
+  if (n > 0) {
+    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, B + w.r0, sizeof(double) * ldb,
+                               sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+    launch_colmajor_to_rows(stage.p, n, n, s, w.B.p, true, st);
+  }
+  WGP_CUDA(cudaMemsetAsync(w.V.p, 0, sizeof(T) * w.N * s, st));
+  if (U1 && n1 > 0) {  // expand_init: [u1; 0] (solvers.cpp:43-48), full rows on every rank
     WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n1, U1, sizeof(double) * ldu,
                                sizeof(double) * n1, s, cudaMemcpyHostToDevice, st));
     launch_colmajor_to_rows(stage.p, n1, n1, s, w.V.p, true, st);
@@ -117,19 +124,27 @@ void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb
 
 template <typename T>
 void download_solution(SolverWork<T>& w, double* V, int64_t ldv, cudaStream_t st) {
-  const int64_t n = w.n;
+  const int64_t N = w.N;
   const int s = w.s;
-  DBuf<double> stage((size_t)std::max<int64_t>(n, 1) * s);
-  launch_rows_to_colmajor(w.V.p, n, s, stage.p, n, true, st);
-  WGP_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * ldv, stage.p, sizeof(double) * n,
-                             sizeof(double) * n, s, cudaMemcpyDeviceToHost, st));
+  DBuf<double> stage((size_t)std::max<int64_t>(N, 1) * s);
+  launch_rows_to_colmajor(w.V.p, N, s, stage.p, N, true, st);
+  WGP_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * ldv, stage.p, sizeof(double) * N,
+                             sizeof(double) * N, s, cudaMemcpyDeviceToHost, st));
   WGP_CUDA(cudaStreamSynchronize(st));
+}
+
+// Column dot products over this rank's rows -> global chunk partials on every rank.
+template <typename T>
+static void dots(const Op& op, SolverWork<T>& w, const T* A, const T* Bv, cudaStream_t st) {
+  if (w.n > 0)
+    launch_coldots<T>(A, Bv, nullptr, nullptr, w.n, w.s, w.part.p + (int64_t)w.c0 * w.s, st);
+  dist_allgather_chunks(*op.ctx, w.part.p, w.N, w.s, st);
 }
 
 template <typename T>
 void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd,
                       SolverWork<T>& w, SolveOutputs& out, cudaStream_t st) {
-  const int64_t n = w.n;
+  const int64_t n = w.n, N = w.N;
   const int s = w.s;
   double* rz = w.scal.p;
   double* alpha = rz + s;
@@ -139,15 +154,16 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
   int* active = w.act.p;
   int* fail = w.act.p + s;
   const int nch = w.nch;
+  const Ctx& ctx = *op.ctx;
   w.pwork.ensure((size_t)(nch > 0 ? nch : 1) * (pd.k + 1) * s);
   w.tvec.ensure((size_t)(pd.k + 1) * s);
 
   // |b| per column
-  launch_coldots<T>(w.B.p, w.B.p, nullptr, nullptr, n, s, w.part.p, st);
+  dots(op, w, w.B.p, w.B.p, st);
   init_bnorm_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, bnorm, active);
-  // r0 = b - H v0 (solvers.cpp:150)
+  // r0 = b - H v0 (solvers.cpp:150); V is full on every rank
   launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
-  launch_coldots<T>(w.R.p, w.R.p, nullptr, nullptr, n, s, w.part.p, st);
+  dots(op, w, w.R.p, w.R.p, st);
   resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance, rel,
                                               active);
   std::vector<double> hrel(s);
@@ -166,20 +182,22 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
   if (n_active == 0) return;
 
   // z = P r; p = z; rz = r.z (solvers.cpp:157-159)
-  precond_apply<T>(pd, w.R.p, w.Z.p, s, w.tvec.p, w.pwork.p, st);
-  WGP_CUDA(cudaMemcpyAsync(w.P.p, w.Z.p, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
-  launch_coldots<T>(w.R.p, w.Z.p, nullptr, nullptr, n, s, w.part.p, st);
+  precond_apply<T>(op, pd, w.R.p, w.Z.p, s, w.tvec.p, w.pwork.p, st);
+  if (n > 0) WGP_CUDA(cudaMemcpyAsync(w.Pl(), w.Z.p, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
+  dots(op, w, w.R.p, w.Z.p, st);
   cg_beta_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta, 1);
   const int int_max = INT_MAX;
   WGP_CUDA(cudaMemcpyAsync(fail, &int_max, sizeof(int), cudaMemcpyHostToDevice, st));
 
   for (int k = 1; k <= cfg.max_iters; ++k) {
-    launch_kmatvec_full(op, w.P.p, w.HP.p, s, st);  // Hp = H p (:162)
-    launch_coldots<T>(w.P.p, w.HP.p, nullptr, nullptr, n, s, w.part.p, st);
+    dist_allgather_rows(ctx, w.P.p, N, s, sizeof(T), st);  // exchange: full p for the matvec
+    launch_kmatvec_full(op, w.P.p, w.HP.p, s, st);          // Hp = H p (:162), local rows
+    dots(op, w, w.Pl(), w.HP.p, st);
     cg_alpha_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, alpha, fail);
-    launch_axpy_cols<T>(w.V.p, w.P.p, alpha, n, s, st);  // v += alpha p (:168)
-    launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // r = b - H v (:171)
-    launch_coldots<T>(w.R.p, w.R.p, nullptr, nullptr, n, s, w.part.p, st);
+    if (n > 0) launch_axpy_cols<T>(w.Vl(), w.Pl(), alpha, n, s, st);  // v += alpha p (:168)
+    dist_allgather_rows(ctx, w.V.p, N, s, sizeof(T), st);
+    launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);         // r = b - H v (:171)
+    dots(op, w, w.R.p, w.R.p, st);
     resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance, rel,
                                                 active);
     WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
@@ -202,14 +220,13 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
       n_active += hact[c];
     }
     if (n_active == 0) break;
-    precond_apply<T>(pd, w.R.p, w.Z.p, s, w.tvec.p, w.pwork.p, st);  // z = P r (:178)
-    launch_coldots<T>(w.R.p, w.Z.p, nullptr, nullptr, n, s, w.part.p, st);
+    precond_apply<T>(op, pd, w.R.p, w.Z.p, s, w.tvec.p, w.pwork.p, st);  // z = P r (:178)
+    dots(op, w, w.R.p, w.Z.p, st);
     cg_beta_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta, 0);
-    launch_xpby_cols<T>(w.P.p, w.Z.p, beta, active, n, s, st);  // p = z + beta p (:180)
+    if (n > 0) launch_xpby_cols<T>(w.Pl(), w.Z.p, beta, active, n, s, st);  // p = z + beta p (:180)
   }
   WGP_CUDA(cudaGetLastError());
 }
-
 
 // ---------------------------------------------------------------------------------------
 // shared per-iteration helpers (host side)

@@ -5,19 +5,26 @@
 
 namespace wgp {
 
-// Per-solve device buffers, all row-major [n][s] in the compute type.
+// Per-solve device buffers, row-major [rows][s] fp64.  Sharded (world > 1): this rank owns
+// rows [r0, r0 + n) of N; V and P are full N-row buffers (the matvec reads every row,
+// all-gathered after each update), R, Z, HP, B hold the local rows only.  Chunk partials
+// `part` are indexed by global chunk (c0 = r0 / kChunkRows).
 template <typename T>
 struct SolverWork {
-  int64_t n = 0;
+  int64_t n = 0;        // local rows
+  int64_t N = 0, r0 = 0;
   int s = 0;
-  int nch = 0;
+  int nch = 0;          // global chunk count
+  int c0 = 0;
   DBuf<T> V, R, Z, P, HP, B;
+  T* Vl() const { return V.p + r0 * s; }
+  T* Pl() const { return P.p + r0 * s; }
   DBuf<double> part;   // [nch][2][s] chunk partials
   DBuf<double> scal;   // rz, alpha, beta, bnorm, rel, spare (6 x s)
   DBuf<int> act;       // active[s] + failure column
   DBuf<double> pwork;  // preconditioner chunk partials
   DBuf<double> tvec;   // M^T r  (k x s)
-  void alloc(int64_t n, int s);
+  void alloc(const Op& op, int s);
 };
 
 struct SolveOutputs {

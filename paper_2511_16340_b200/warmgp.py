@@ -40,6 +40,7 @@ OK, INVALID_ARGUMENT, NOT_SPD, DIVERGED, CUDA_ERROR, NCCL_ERROR, OOM = range(7)
 EXPORTS = (
     "wgp_abi_version", "wgp_last_error", "wgp_solver_config_default", "wgp_shard_range",
     "wgp_ctx_create", "wgp_nccl_unique_id", "wgp_ctx_create_sharded", "wgp_ctx_destroy",
+    "wgp_allgather_rows_dev",
     "wgp_ctx_stream", "wgp_op_create", "wgp_op_destroy", "wgp_op_append_rows", "wgp_op_size",
     "wgp_op_dim", "wgp_op_precision", "wgp_kmatvec", "wgp_kmatvec_dev", "wgp_residual_dev",
     "wgp_cross_matvec", "wgp_solve_many", "wgp_solve", "wgp_pivoted_cholesky", "wgp_precond_info",
@@ -107,6 +108,7 @@ def _declare(L):
         "wgp_nccl_unique_id": (C.c_int, [P]),
         "wgp_ctx_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, P, P]),
         "wgp_ctx_destroy": (None, [P]),
+        "wgp_allgather_rows_dev": (C.c_int, [P, P, I64, C.c_int, P]),
         "wgp_ctx_stream": (P, [P]),
         "wgp_op_create": (C.c_int, [P, C.c_int, D, D, D, C.c_int, C.c_int, P]),
         "wgp_op_destroy": (None, [P]),
@@ -208,6 +210,11 @@ class DeviceContext:
         buf = C.create_string_buffer(128)
         _check(lib().wgp_nccl_unique_id(buf))
         return buf.raw
+
+    def allgather_rows_dev(self, dV_ptr: int, n: int, s: int, stream: int = 0):
+        """In-place all-gather of this group's row slices of a full n x s fp64 buffer."""
+        _check(lib().wgp_allgather_rows_dev(self._h, C.c_void_p(dV_ptr), n, s,
+                                            C.c_void_p(stream) if stream else None))
 
     @property
     def stream(self) -> int:
