@@ -184,6 +184,8 @@ double wgp_rng_uniform(uint64_t* state);
 double wgp_rng_normal(uint64_t* state);
 double wgp_rng_chi_square3(uint64_t* state);
 uint64_t wgp_rng_uniform_index(uint64_t* state, uint64_t n);
+/* n consecutive scale * normal() draws from (and advancing) the generator at *state. */
+void wgp_rng_normal_fill(uint64_t* state, int64_t n, double scale, double* out);
 /* out[i] = scale * Rng(seed).normal(), i = 0..n-1 (build_sample_rhs noise, sampling.cpp:58-62) */
 void wgp_normal_fill(uint64_t seed, int64_t n, double scale, double* out);
 /* sample_prior (sampling.cpp:14-35): Omega F x dim column-major, phases F, amps F.

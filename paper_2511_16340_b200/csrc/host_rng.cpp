@@ -27,6 +27,12 @@ uint64_t wgp_rng_uniform_index(uint64_t* state, uint64_t n) {
   return v;
 }
 
+void wgp_rng_normal_fill(uint64_t* state, int64_t n, double scale, double* out) {
+  Rng r{*state};
+  for (int64_t i = 0; i < n; ++i) out[i] = scale * r.normal();
+  *state = r.state;
+}
+
 void wgp_normal_fill(uint64_t seed, int64_t n, double scale, double* out) {
   Rng r{seed};  // build_sample_rhs noise order, sampling.cpp:58-62
   for (int64_t i = 0; i < n; ++i) out[i] = scale * r.normal();

@@ -46,6 +46,7 @@ EXPORTS = (
     "wgp_cross_matvec", "wgp_solve_many", "wgp_solve", "wgp_pivoted_cholesky", "wgp_precond_info",
     "wgp_rff_eval", "wgp_derive_seed", "wgp_rng_next_u64", "wgp_rng_uniform", "wgp_rng_normal",
     "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
+    "wgp_rng_normal_fill",
 )
 
 
@@ -133,6 +134,7 @@ def _declare(L):
         "wgp_rng_chi_square3": (D, [P]),
         "wgp_rng_uniform_index": (C.c_uint64, [P, C.c_uint64]),
         "wgp_normal_fill": (None, [C.c_uint64, I64, D, P]),
+        "wgp_rng_normal_fill": (None, [P, I64, D, P]),
         "wgp_sample_prior": (C.c_int, [C.c_int, D, I64, I64, C.c_uint64, P, P, P]),
     }
     for name, (res, args) in sig.items():
@@ -368,6 +370,18 @@ class SolveResult:
         return self.residual_history[-1]
 
 
+def init_weights(init: Initialization, n1: int, n2: int) -> np.ndarray:
+    """init_weights (solvers.cpp:27-38): cold -> zeros(n1+n2); warm -> [u1; 0]."""
+    if n1 < 0 or n2 < 0:
+        raise ValueError("init_weights: negative block size")
+    v = np.zeros(n1 + n2)
+    if init.warm_start:
+        if init.u1.size != n1:
+            raise ValueError("init_weights: warm-start vector length does not match n1")
+        v[:n1] = init.u1
+    return v
+
+
 def solve_many(op: KernelOperator, rhs, inits: list, cfg: SolverConfig, return_status: bool = False):
     """solve_many (solvers.cpp:321-354) on the device: all columns in one batched solve.
 
@@ -495,6 +509,12 @@ class Rng:
 
     def derive(self, stream: int) -> "Rng":
         return Rng(derive_seed(self._s.value, stream))
+
+    def normal_fill(self, n: int, scale: float = 1.0) -> np.ndarray:
+        """n consecutive scale * normal() draws (advances this generator)."""
+        out = np.zeros(n)
+        lib().wgp_rng_normal_fill(C.byref(self._s), n, scale, _ptr(out))
+        return out
 
 
 def normal_fill(seed: int, n: int, scale: float = 1.0) -> np.ndarray:
