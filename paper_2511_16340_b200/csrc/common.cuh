@@ -104,6 +104,9 @@ struct Op {
   DBuf<double> center, vchunk, ychunk, ysplit;
   std::vector<double> h_center;
   bool tc_dirty = true;
+  // GEMM1 operand format chosen at operand build: fp16 splits of x / l (kind::f16, half the
+  // bytes and MMA time of tf32) when the scaled coordinates fit fp16, else tf32 splits of x.
+  bool tc_f16 = false;
   KParams kp() const {
     KParams p;
     p.kind = kind;

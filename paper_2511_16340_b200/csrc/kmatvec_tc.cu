@@ -8,8 +8,12 @@
 //   GEMM1  S = XA_i . XB_j^T      (M=128, N=64, K=K1)  tcgen05.mma kind::tf32, SS, S in TMEM.
 //          The operands are pre-formatted so the contraction yields the squared distance
 //          directly (the norm form |x|^2 + |y|^2 - 2 x.y of kernel.cpp:39-46, 65):
-//            XA = [-2xh | -2xh | -2xl | sqh | sql | 1 | 1]   XB = [xh | xl | xh | 1 | 1 | sqh | sql]
-//          (3xTF32: hi/lo splits of x and |x|^2, error ~2^-22 of the largest term).
+//            F32_3XTF32: XA = [-2xh | -2xh | -2xl | sqh | sql | 1 | 1]
+//                        XB = [ xh  |  xl  |  xh  |  1  |  1  | sqh | sql]
+//            (round-to-nearest tf32 hi/lo splits: x.y to ~2^-22 |x||y|; a fourth xl.yl
+//            product gains nothing measurable -- the fp32 accumulation below dominates --
+//            and costs 7% at C3 through K1 = 4d+4)
+//            TF32:       XA = [-2xh | sqh | 1]   XB = [xh | 1 | sqh]   (single pass, ~2^-11)
 //   map    epilogue warps: tcgen05.ld S -> k(d2)/s^2 * 2^10 in registers (Matern-3/2 or RBF;
 //          MUFU sqrt/ex2) -> fp16 hi/lo split -> tcgen05.st into TMEM (K never leaves the SM).
 //   GEMM2  Y += K_hi V_hi + K_hi V_lo + K_lo V_hi   (M=128, N=s_pad, K=64)  kind::f16, A from
@@ -26,9 +30,12 @@
 // (S written by GEMM1, overwritten in place by K for GEMM2); mbarriers + tcgen05.commit.
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -38,84 +45,213 @@ namespace tc {
 
 constexpr int BM = 128;        // rows per CTA (UMMA M)
 constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
-constexpr int NTHREADS = 640;  // 4 role warps + 2 epilogue sets x 8 warps
+constexpr int NSET = 3;         // epilogue sets (8 warps each) taking tiles round-robin
+constexpr int NPROD = 1;        // producer warps per ring (XB ring, V ring); 3 measured slower
+constexpr int NROLE = 4;        // role warps: 2 MMA issuers + 2 x NPROD producers (+ alloc)
+constexpr int NTHREADS = 32 * NROLE + NSET * 256;  // role warps + NSET x 8 epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
-constexpr int CH = 16;         // j tiles per TMEM accumulation chunk (fp64 drain after each)
+constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (fp64 drain after each)
 // TMEM: a ring of NB 64-column tile buffers followed by the Y accumulator.  A buffer holds
 // S(t) (fp32 d^2, written by GEMM1); the epilogue loads it into registers and writes K(t)
 // back in place as packed fp16 (each warp into the 32 columns it read: 16 hi + 16 lo), which
 // GEMM2 then reads as its A operand; GEMM2's commit frees the buffer for GEMM1 of tile
-// t + NB.  Two 64-column Y accumulators alternate per chunk of CH tiles: the tensor core's
-// fp32 accumulation error grows with the number of accumulated K-steps (measured 3.5e-4 at
-// N = 101k in one accumulator), so every CH tiles the epilogue warps drain the finished
-// accumulator into fp64 partial sums in shared memory (~4e-6 per chunk, summed in fp64).
+// t + NB.  Two 64-column Y accumulators alternate per chunk of CH tiles: each tcgen05.mma
+// truncates its fp32 sum (a relative bias of about -2^-25 per instruction against the running
+// accumulator: -7.5e-6 for positive V at CH = 16, i.e. 192 instructions per chunk, and
+// 3.5e-4 at N = 101k in a single chain), so every CH tiles the epilogue warps drain the
+// finished accumulator into fp64 partial sums in shared memory.  Measured at N = 10k RBF
+// (tests/gpu_probe_ch.py): CH = 16 -> 3.3e-6 relative, 4 -> 1.1e-6, 1 -> 4.9e-7, at 1.0 /
+// 1.08 / 2.2x the C3 time (the fp64 shared-memory traffic of the drains); WGP_TC_CH overrides.
 // TMEM: NB = 6 buffers [0,384), Y0 [384,448), Y1 [448,512).
-constexpr int MAX_NB = 6;
+constexpr int MAX_NB = 5;
+constexpr int TRW = 12;  // trace slots per tile
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
+// Software-exponential share (quarters) of the kernel map: Matern spends 2 SFU ops per pair
+// (sqrt, ex2), RBF 1.
+constexpr int SWQ_MATERN = 2;
+constexpr int SWQ_RBF = 1;
 
 struct Params {
-  const float* XA;      // tiled A operand rows (this launch's rows start at tile 0)
-  const float* XB;      // tiled B operand rows (all columns j)
+  const void* XA;       // tiled A operand rows (this launch's rows start at tile 0)
+  const void* XB;       // tiled B operand rows (all columns j)
+  int g1f16;            // GEMM1 operands fp16 (kind::f16, K = 16) instead of tf32 (K = 8)
   const __half* Vt;     // tiled V hi/lo per j tile (fp16, per-column scaled)
   const float* vscale;  // [s_pad] 2^-e_c: undo the per-column V scale
-  const double* V64;    // [ncols][s] for the sigma^2 V_i term (gram) -- indexed by global row
-  const double* B64;    // nullable: residual mode, [nrows][s]
-  double* Y64;          // [nrows][s]
   int64_t nrows, row0, ncols;
   int ntiles;           // ceil(ncols / BJ)
   int tiles_per_split;  // j tiles per CTA along grid.y (2-D decomposition)
-  double* Ysplit;       // nullptr: full output; else fp64 partials [gridDim.y][nrows][s]
+  int ch;               // j tiles per accumulation chunk
+  double* Ypart;        // fp64 partial sums [gridDim.y][nrows][s] (unscaled; reduce_splits)
   int s, s_pad, K1;
   int kind;
   float c1, neg_c_log2e;
   double out_scale;     // s^2 * 2^-10
   double noise2;
   int gram;
+  int sleep_ns;  // epilogue wait backoff (WGP_TC_SLEEP)
+  int dbg;  // timing experiments only (WGP_TC_DEBUG): 1 GEMM2 hi.hi only, 2 GEMM1 one K-step, 4 no map
   unsigned long long* trace;  // debug: per-tile event clocks of CTA 0 (nullptr normally)
+  unsigned long long* cta_trace;  // debug: per-CTA [start, loop end, end] globaltimer + smid
 };
 
-__device__ __forceinline__ void trace_ev(const Params& p, int t, int slot) {
-  if (p.trace && blockIdx.x == 0 && blockIdx.y == 0) p.trace[(size_t)t * 8 + slot] = clock64();
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cta_ev(const Params& p, int slot) {
+  if (p.cta_trace) {
+    const size_t c = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    p.cta_trace[c * 4 + slot] = gtimer();
+    if (slot == 0) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+      p.cta_trace[c * 4 + 3] = sm;
+    }
+  }
 }
 
-__device__ __forceinline__ uint32_t tf32_hi(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
+__device__ __forceinline__ void trace_ev(const Params& p, int t, int slot) {
+  if (p.trace && blockIdx.x == 0 && blockIdx.y == 0) p.trace[(size_t)t * TRW + slot] = clock64();
+}
+
+// round to the nearest tf32 (10 explicit mantissa bits; the tensor core ignores the low 13)
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+  return __uint_as_float(u);
+}
+
+// Exact fp32 -> fp64 with integer ops on the ALU pipe (F2F.F64.F32 issues to the XU pipe,
+// which the kernel map keeps ~80% busy with MUFU work).  fp32 denormals flush to zero;
+// TMEM accumulators never hold inf/nan for finite inputs.
+__device__ __forceinline__ double f32_to_f64_alu(uint32_t u) {
+  const uint32_t mag = u & 0x7FFFFFFFu;
+  const uint32_t hi = mag < 0x00800000u ? (u & 0x80000000u)
+                                        : (u & 0x80000000u) | ((mag >> 3) + 0x38000000u);
+  const uint32_t lo = mag < 0x00800000u ? 0u : (u << 29);
+  return __hiloint2double((int)hi, (int)lo);
+}
 
 __device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
   const __half2 h = __floats2half2_rn(lo_elem, hi_elem);  // .x (low 16 bits) = lower k index
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NS) {
+// 2^a for a pair on the FMA pipe (FFMA2/FADD2 + integer exponent insert): a is clamped to
+// >= -125, rounded to j = rn(a) with the 1.5*2^23 shifter, and 2^(a-j) in [2^-1/2, 2^1/2]
+// comes from a degree-5 near-minimax polynomial (max relative error 2.3e-7 evaluated in
+// fp32, vs ~1.2e-7 for MUFU.EX2).  Used for a fraction of the map's exponentials so the SFU
+// (16/clk/SM) and the FP32 pipe (128/clk/SM, two lanes per FFMA2) finish together.
+__device__ __forceinline__ float2 sw_ex2x2(float2 a) {
+  a.x = fmaxf(a.x, -125.0f);
+  a.y = fmaxf(a.y, -125.0f);
+  const float2 t = __fadd2_rn(a, make_float2(12582912.0f, 12582912.0f));
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.0f, -1.0f), a);
+  float2 q = __ffma2_rn(make_float2(1.32764655e-3f, 1.32764655e-3f), f,
+                        make_float2(9.67554096e-3f, 9.67554096e-3f));
+  q = __ffma2_rn(q, f, make_float2(5.55071346e-2f, 5.55071346e-2f));
+  q = __ffma2_rn(q, f, make_float2(2.40221202e-1f, 2.40221202e-1f));
+  q = __ffma2_rn(q, f, make_float2(6.93146944e-1f, 6.93146944e-1f));
+  q = __ffma2_rn(q, f, make_float2(1.00000012f, 1.00000012f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
+// Kernel map of one 32-column row slice: v = fp32 d^2 from TMEM, kv = k/s^2 * 2^10.
+// Pairs of columns go through the packed FP32 pipe; SWQ of every 4 pairs take the software
+// exponential, the rest MUFU.EX2.  sqrt(|d2|): a tiny negative d2 from the norm-form
+// cancellation maps to ~0 like the reference's max(.,0) clamp (kernel.cpp:44).
+template <int SWQ, int NCOL>
+__device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* kv, float c1,
+                                           float nclog2e) {
+  const float2 NC = make_float2(nclog2e, nclog2e);
+  const float2 OFF = make_float2(KSCALE_LOG2, KSCALE_LOG2);
+  if (kind == WGP_MATERN32) {
+    const float2 C1 = make_float2(c1, c1);
+#pragma unroll
+    for (int q = 0; q < NCOL / 2; ++q) {
+      float2 r;
+      r.x = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q])));
+      r.y = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q + 1])));
+      const float2 a = __ffma2_rn(r, NC, OFF);  // log2(2^10 e^{-z})
+      float2 e;
+      if ((q & 3) < SWQ) {
+        e = sw_ex2x2(a);
+      } else {
+        e.x = ptx::ex2_approx(a.x);
+        e.y = ptx::ex2_approx(a.y);
+      }
+      const float2 z = __fmul2_rn(r, C1);
+      const float2 k = __ffma2_rn(z, e, e);  // 2^10 (1+z) e^{-z}
+      kv[2 * q] = k.x;
+      kv[2 * q + 1] = k.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NCOL / 2; ++q) {
+      const float2 d2 = make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+      const float2 a = __ffma2_rn(d2, NC, OFF);  // log2(2^10 e^{-d2/2l^2})
+      float2 e;
+      if ((q & 3) < SWQ) {
+        e = sw_ex2x2(a);
+      } else {
+        e.x = ptx::ex2_approx(a.x);
+        e.y = ptx::ex2_approx(a.y);
+      }
+      kv[2 * q] = e.x;
+      kv[2 * q + 1] = e.y;
+    }
+  }
+}
+
+template <int SWQ>
+__global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NSX, int NSV) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t XA_BYTES = BM * p.K1 * 4;
-  const uint32_t XB_BYTES = BJ * p.K1 * 4;
+  const uint32_t ESZ = p.g1f16 ? 2 : 4;     // GEMM1 operand element bytes
+  const uint32_t XA_BYTES = BM * p.K1 * ESZ;
+  const uint32_t XB_BYTES = BJ * p.K1 * ESZ;
   const uint32_t VT_BYTES = p.s_pad * BJ * 2;  // one of hi / lo (fp16)
-  const uint32_t ST_BYTES = XB_BYTES + 2 * VT_BYTES;
   unsigned char* sXA = smem;
-  unsigned char* sStage = smem + XA_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStage + (size_t)NS * ST_BYTES);
-  uint64_t* stage_full = bars;
-  uint64_t* stage_empty = bars + NS;
-  uint64_t* xa_full = bars + 2 * NS;
-  uint64_t* s_full = xa_full + 1;        // [MAX_NB] GEMM1 -> epilogue
-  uint64_t* k_full = s_full + MAX_NB;    // [MAX_NB] epilogue -> GEMM2 (8 arrivals)
-  uint64_t* b_free = k_full + MAX_NB;    // [MAX_NB] GEMM2 -> GEMM1
-  uint64_t* y_full = b_free + MAX_NB;    // [2] chunk accumulator done (GEMM2 commit)
-  uint64_t* y_free = y_full + 2;         // [2] chunk accumulator drained (16 warp arrivals)
+  unsigned char* sXB = smem + XA_BYTES;                        // NSX stages of XB_j
+  unsigned char* sV = sXB + (size_t)NSX * XB_BYTES;            // NSV stages of V_j hi | lo
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + (size_t)NSV * 2 * VT_BYTES);
+  uint64_t* xb_full = bars;               // [NSX] bulk copy -> GEMM1
+  uint64_t* xb_empty = xb_full + NSX;     // [NSX] GEMM1 -> XB producer
+  uint64_t* v_full = xb_empty + NSX;      // [NSV] bulk copy -> GEMM2
+  uint64_t* v_empty = v_full + NSV;       // [NSV] GEMM2 -> V producer
+  uint64_t* xa_full = v_empty + NSV;
+  uint64_t* s_full = xa_full + 1;         // [MAX_NB] GEMM1 -> epilogue
+  uint64_t* k_full = s_full + MAX_NB;     // [MAX_NB] epilogue -> GEMM2 (8 arrivals)
+  uint64_t* b_free = k_full + MAX_NB;     // [MAX_NB] GEMM2 -> GEMM1
+  uint64_t* y_full = b_free + MAX_NB;     // [2] chunk accumulator done (GEMM2 commit)
+  uint64_t* y_free = y_full + 2;          // [2] chunk accumulator drained (16 warp arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_free + 2);
-  double* ypart = reinterpret_cast<double*>(smem + (size_t)(XA_BYTES + NS * ST_BYTES + 512));
   constexpr int NB = MAX_NB;
-  constexpr uint32_t TM_Y = 384;         // Y accumulator a at TM_Y + 64 a
+  // TMEM: ring of NB 64-column S/K buffers [0, 320), the two chunk accumulators of the
+  // leading product Kh.Vh at TM_Y + 64 a, and one sweep-long accumulator of the correction
+  // products Kh.Vl + Kl.Vh at TM_C (2^-11 of the leading term, so its own truncation bias is
+  // negligible; keeping it out of the chunk accumulators divides their per-instruction
+  // truncation bias by three).
+  constexpr uint32_t TM_Y = 320;
+  constexpr uint32_t TM_C = 448;
   // this CTA's j range: tiles [jt0, jt0 + T) of the column sweep
   const int jt0 = blockIdx.y * p.tiles_per_split;
   const int T = min(p.ntiles - jt0, p.tiles_per_split);
+  const int CH = p.ch;
   const int NCH = (T + CH - 1) / CH;
+  if (threadIdx.x == 0) cta_ev(p, 0);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NS; ++i) {
-      ptx::mbar_init(&stage_full[i], 1);
-      ptx::mbar_init(&stage_empty[i], 1);
+    for (int i = 0; i < NSX; ++i) {
+      ptx::mbar_init(&xb_full[i], 1);
+      ptx::mbar_init(&xb_empty[i], 1);
+    }
+    for (int i = 0; i < NSV; ++i) {
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
     }
     ptx::mbar_init(xa_full, 1);
     for (int i = 0; i < MAX_NB; ++i) {
@@ -125,43 +261,61 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&y_full[i], 1);
-      ptx::mbar_init(&y_free[i], 16);
+      ptx::mbar_init(&y_free[i], 4 * (p.s_pad / 16));  // drainer warps with columns
     }
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
-  for (int e = threadIdx.x; e < BM * p.s_pad; e += NTHREADS) ypart[e] = 0.0;
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int KS1 = p.K1 / 8;                 // GEMM1 K-steps (tf32: 8 per instruction)
-  const uint32_t sbo1 = (p.K1 / 4) * 128;   // 8-row group stride of XA/XB tiles
+  const int KS1 = p.K1 * ESZ / 32;          // GEMM1 K-steps (32 bytes of K per instruction)
+  const uint32_t sbo1 = (p.K1 * ESZ / 16) * 128;  // 8-row group stride of XA/XB tiles
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer (TMA engine)
+  if (warp != 1 && warp != 3 && warp < NROLE) {
+    // ------------------------------------------------------------ producers (TMA engine)
+    // Two independent rings: XB_j is consumed by GEMM1 right away, V_j only by GEMM2 after
+    // the kernel map, so V stays resident ~4x longer; separate rings let each be as deep as
+    // its own lifetime needs.  Bulk copies issued by one warp are processed one at a time
+    // (~400-900 cycles each, nearly size-independent; tools/bulk_microbench2.cu), so each
+    // ring can be fed by NPROD warps taking its tiles round-robin (NPROD = 3 measured 9%
+    // slower at C3 than 1: the copies are not the binding stage).
+    // warps 0 (, 4, 6) -> XB ring; 2 (, 5, 7) -> V ring
+    static_assert(NROLE == 2 + 2 * NPROD && NPROD <= 3, "role warp layout");
+    const bool is_xb = warp == 0 || warp == 4 || warp == 6;
+    const int pk = warp == 0 || warp == 2 ? 0 : (warp == 4 || warp == 5 ? 1 : 2);
     const bool leader = ptx::elect_one();
-    if (leader) {
+    if (warp == 0 && leader) {
       ptx::mbar_arrive_expect_tx(xa_full, XA_BYTES);
-      ptx::bulk_g2s(sXA, p.XA + (size_t)blockIdx.x * BM * p.K1, XA_BYTES, xa_full);
+      ptx::bulk_g2s(sXA, static_cast<const char*>(p.XA) + (size_t)blockIdx.x * XA_BYTES, XA_BYTES,
+                    xa_full);
     }
-    int st = 0;
-    uint32_t ph = 0;
-    const float* xb_src = p.XB + (size_t)jt0 * BJ * p.K1;
-    const __half* vt_src = p.Vt + (size_t)jt0 * 2 * p.s_pad * BJ;
-    for (int t = 0; t < T; ++t) {
-      if (t >= NS) ptx::mbar_wait(&stage_empty[st], ph ^ 1);
-      if (leader) {
-        trace_ev(p, t, 6);
-        unsigned char* dst = sStage + (size_t)st * ST_BYTES;
-        ptx::mbar_arrive_expect_tx(&stage_full[st], ST_BYTES);
-        ptx::bulk_g2s(dst, xb_src, XB_BYTES, &stage_full[st]);
-        ptx::bulk_g2s(dst + XB_BYTES, vt_src, 2 * VT_BYTES, &stage_full[st]);
+    if (is_xb) {
+      for (int t = pk; t < T; t += NPROD) {
+        const int st = t % NSX;
+        if (t >= NSX) ptx::mbar_wait(&xb_empty[st], ((t / NSX) & 1) ^ 1);
+        if (leader) {
+          trace_ev(p, t, 6);
+          ptx::mbar_arrive_expect_tx(&xb_full[st], XB_BYTES);
+          ptx::bulk_g2s(sXB + (size_t)st * XB_BYTES,
+                        static_cast<const char*>(p.XB) + (size_t)(jt0 + t) * XB_BYTES, XB_BYTES,
+                        &xb_full[st]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      xb_src += (size_t)BJ * p.K1;
-      vt_src += (size_t)2 * p.s_pad * BJ;
-      if (++st == NS) { st = 0; ph ^= 1; }
+    } else {
+      for (int t = pk; t < T; t += NPROD) {
+        const int st = t % NSV;
+        if (t >= NSV) ptx::mbar_wait(&v_empty[st], ((t / NSV) & 1) ^ 1);
+        if (leader) {
+          trace_ev(p, t, 8);
+          ptx::mbar_arrive_expect_tx(&v_full[st], 2 * VT_BYTES);
+          ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES, p.Vt + (size_t)(jt0 + t) * 2 * p.s_pad * BJ,
+                        2 * VT_BYTES, &v_full[st]);
+        }
+        __syncwarp();
+      }
     }
   } else if (warp == 1 || warp == 3) {
     // ------------------------------------------------------------ MMA issuers
@@ -170,229 +324,342 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // issues GEMM2 (K.V); each waits only on its own inputs and each tcgen05.commit tracks
     // its own thread's MMAs.  Whole warps run the schedule (uniform control flow,
     // descriptors in uniform registers); one elected lane issues.
-    const uint64_t st_step = (uint64_t)(ST_BYTES >> 4);  // descriptor start-address units
     if (warp == 1) {
-      const uint32_t idesc1 = ptx::idesc_tf32(BM, BJ);
+      const uint32_t idesc1 = p.g1f16 ? ptx::idesc_f16(BM, BJ) : ptx::idesc_tf32(BM, BJ);
       const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
-      const uint64_t dStage0 = ptx::umma_desc(ptx::smem_u32(sStage), 128, sbo1);
+      const uint64_t dXB0 = ptx::umma_desc(ptx::smem_u32(sXB), 128, sbo1);
+      const uint64_t xb_step = (uint64_t)(XB_BYTES >> 4);  // descriptor start-address units
       ptx::mbar_wait(xa_full, 0);
       int st1 = 0, b1 = 0;
       uint32_t ph1 = 0, phb1 = 0;
       for (int t = 0; t < T; ++t) {
-        ptx::mbar_wait(&stage_full[st1], ph1);
+        ptx::mbar_wait(&xb_full[st1], ph1);
         if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 0);
-          const uint64_t dB = dStage0 + st_step * st1;
-          for (int ks = 0; ks < KS1; ++ks)
-            ptx::mma_tf32_ss(tmem + b1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+          const uint64_t dB = dXB0 + xb_step * st1;
+          const int nks = (p.dbg & 2) ? 1 : KS1;
+          if (p.g1f16) {
+            for (int ks = 0; ks < nks; ++ks)
+              ptx::mma_f16_ss(tmem + b1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+          } else {
+            for (int ks = 0; ks < nks; ++ks)
+              ptx::mma_tf32_ss(tmem + b1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+          }
           ptx::mma_commit(&s_full[b1]);
+          ptx::mma_commit(&xb_empty[st1]);
         }
         __syncwarp();
-        if (++st1 == NS) { st1 = 0; ph1 ^= 1; }
+        if (++st1 == NSX) { st1 = 0; ph1 ^= 1; }
         if (++b1 == NB) { b1 = 0; phb1 ^= 1; }
       }
     } else {
       const uint32_t idesc2 = ptx::idesc_f16(BM, p.s_pad);
       // fp16 V tile: rows c (N) in 8-row groups, K = 64 j in 8-element (16 B) chunks
-      const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sStage + XB_BYTES), 128, (BJ / 8) * 128);
+      const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sV), 128, (BJ / 8) * 128);
+      const uint64_t v_step = (uint64_t)((2 * VT_BYTES) >> 4);
       const uint64_t vlo_step = (uint64_t)(VT_BYTES >> 4);
       int st2 = 0, b2 = 0;
-      uint32_t phb2 = 0;
+      uint32_t ph2 = 0, phb2 = 0;
       for (int t = 0; t < T; ++t) {
         const int c = t / CH, ya = c & 1;
         const bool first = t == c * CH, last = t == T - 1 || t == c * CH + CH - 1;
         if (first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
+        ptx::mbar_wait(&v_full[st2], ph2);
+        if (lane == 0) trace_ev(p, t, 9);
         ptx::mbar_wait(&k_full[b2], phb2);
+        if ((p.dbg & 16) && t > 0) {  // experiment: issue only into a drained tensor queue
+          const int bp = (t - 1) % NB;
+          ptx::mbar_wait(&b_free[bp], ((t - 1) / NB) & 1);
+        }
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 1);
-          const uint64_t dVh = dV0 + st_step * st2;
+          const uint64_t dVh = dV0 + v_step * st2;
           const uint64_t dVl = dVh + vlo_step;
           const uint32_t yacc = tmem + TM_Y + ya * 64;
-          // K layout in the buffer: [hi j0-31 | lo j0-31 | hi j32-63 | lo j32-63], 16 cols each
+          const uint32_t ycor = tmem + TM_C;
+          // K layout in the buffer: per 16 j, [hi (8 packed cols) | lo (8 packed cols)]
           const uint32_t kb = tmem + b2 * 64;
 #pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks) {
-            const uint32_t hcol = kb + (ks >> 1) * 32 + (ks & 1) * 8;
-            ptx::mma_f16_ts(yacc, hcol, dVh + 16 * ks, idesc2, (!first || ks > 0) ? 1u : 0u);
-          }
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(yacc, kb + ks * 16, dVh + 16 * ks, idesc2, (!first || ks > 0) ? 1u : 0u);
+          if (!(p.dbg & 1)) {
 #pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks) {
-            const uint32_t hcol = kb + (ks >> 1) * 32 + (ks & 1) * 8;
-            ptx::mma_f16_ts(yacc, hcol, dVl + 16 * ks, idesc2, 1u);
-          }
+            for (int ks = 0; ks < BJ / 16; ++ks)
+              ptx::mma_f16_ts(ycor, kb + ks * 16, dVl + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
 #pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks) {
-            const uint32_t lcol = kb + (ks >> 1) * 32 + 16 + (ks & 1) * 8;
-            ptx::mma_f16_ts(yacc, lcol, dVh + 16 * ks, idesc2, 1u);
+            for (int ks = 0; ks < BJ / 16; ++ks)
+              ptx::mma_f16_ts(ycor, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);
           }
           ptx::mma_commit(&b_free[b2]);
-          ptx::mma_commit(&stage_empty[st2]);
+          ptx::mma_commit(&v_empty[st2]);
           if (last) ptx::mma_commit(&y_full[ya]);
         }
         __syncwarp();
-        if (++st2 == NS) st2 = 0;
+        if (++st2 == NSV) { st2 = 0; ph2 ^= 1; }
         if (++b2 == NB) { b2 = 0; phb2 ^= 1; }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= NROLE) {
     // ------------------------------------------------------------ kernel-map epilogue
+    // NSET sets of 8 warps take tiles round-robin (set = t mod NSET); within a set, warp
+    // (quadrant q, half) maps rows 32q.. and columns 32 half.. of the tile, 16 at a time.
     const int q = warp & 3;                   // TMEM lane quadrant accessible to this warp
-    const int g = (warp - 4) >> 2;            // 0..3
+    const int g = (warp - NROLE) >> 2;        // 0 .. 2 NSET - 1
     const int set = g >> 1, half = g & 1;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int r = q * 32 + lane;              // row within the CTA tile
     const int64_t gi = p.row0 + (int64_t)blockIdx.x * BM + r;
     const int64_t grow0 = p.row0 + (int64_t)blockIdx.x * BM;
+    const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
     const float kdiag = 1024.0f;              // k(x,x)/s^2 * 2^10
-    // drain share of this warp: its quadrant's 32 rows x 16 accumulator columns
-    const int dc0 = g * 16;
+    // drain share of this warp (sets 0 and 1 only): its quadrant's 32 rows x 16 accumulator
+    // columns, summed in fp64 into this CTA's slice of the column-major partials buffer
+    // [gy][s][nrows] (lanes = consecutive rows: coalesced; L2-resident); reduce_splits scales
+    // and transposes.
+    const bool drainer = set < 2;
+    const int dc0 = (g & 3) * 16;
+    const bool row_ok = lr < p.nrows;
+    const int ncol = max(0, min(16, p.s - dc0));
+    double* __restrict__ ypart = p.Ypart + ((size_t)blockIdx.y * p.s + dc0) * p.nrows + lr;
     int drained = 0;
-    auto drain = [&](int c) {
+    // Incremental drain: a finished chunk accumulator is moved out DSTEP columns per visit
+    // (one visit after each of this warp's tiles), so the fp64 store traffic trickles instead
+    // of arriving as one 64-KB burst per chunk (which stalled every warp's TMEM/LSU traffic
+    // for ~2000 cycles).  Chunk d may start once the epilogue is 4 tiles into chunk d+1 (its
+    // GEMM2 long done) and must finish before GEMM2 starts chunk d+2.
+    constexpr int DSTEP = 4;
+    int dk = 0;  // columns of chunk `drained` already moved
+    auto drain_step = [&](int c) {
       const int ya = c & 1;
-      ptx::mbar_wait(&y_full[ya], (c >> 1) & 1);
-      ptx::tc_fence_after();
-      if (dc0 < p.s_pad) {
-        uint32_t y[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-            "%14,%15}, [%16];"
-            : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3]), "=r"(y[4]), "=r"(y[5]), "=r"(y[6]),
-              "=r"(y[7]), "=r"(y[8]), "=r"(y[9]), "=r"(y[10]), "=r"(y[11]), "=r"(y[12]),
-              "=r"(y[13]), "=r"(y[14]), "=r"(y[15])
-            : "r"(tmem + lane_off + TM_Y + ya * 64 + dc0));
-        ptx::tmem_wait_ld();
-        // column-major partials: lanes (rows) hit consecutive 8-byte words (no bank conflicts)
-        double* colp = ypart + (size_t)dc0 * BM + r;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) colp[(size_t)k * BM] += (double)__uint_as_float(y[k]);
+      if (dk == 0) {
+        ptx::mbar_wait(&y_full[ya], (c >> 1) & 1);
+        ptx::tc_fence_after();
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&y_free[ya]);
+      uint32_t y[DSTEP];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3])
+                   : "r"(tmem + lane_off + TM_Y + ya * 64 + dc0 + dk));
+      ptx::tmem_wait_ld();
+      if (row_ok && !(p.dbg & 8)) {
+        // first chunk stores, later chunks add with fire-and-forget reductions performed at
+        // L2.  Each address is only ever touched by this thread, and same-address operations
+        // of one thread stay in program order, so the fp64 summation order (chunk 0, 1, 2,
+        // ...) is deterministic.
+#pragma unroll
+        for (int k = 0; k < DSTEP; ++k) {
+          if (dk + k >= ncol) break;
+          double* dst = ypart + (size_t)(dk + k) * p.nrows;
+          if (c == 0)
+            *dst = f32_to_f64_alu(y[k]);
+          else
+            asm volatile("red.global.add.f64 [%0], %1;" ::"l"(dst), "d"(f32_to_f64_alu(y[k]))
+                         : "memory");
+        }
+      }
+      dk += DSTEP;
+      if (dk >= 16) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&y_free[ya]);
+        dk = 0;
+        ++drained;
+      }
     };
-    int b = set;                              // buffer of tile t = t % NB
-    uint32_t bph = 0;
-    for (int t = set; t < T; t += 2) {
-      // drain a finished chunk once this warp is well past its last tile
-      while (drained < NCH - 1 && t >= (drained + 1) * CH + CH / 2) drain(drained++);
-      const bool tr = lane == 0 && q == 0 && half == 0;
+    auto drain_all = [&](int c) {  // the last chunk, after the sweep
+      while (drained == c) drain_step(c);
+    };
+    // after the sweep: the correction accumulator, added last (the final y_full commit
+    // covers it)
+    auto drain_corr = [&]() {
+      if (p.dbg & 1) return;
+      uint32_t y[16];
+      ptx::tmem_ld16(tmem + lane_off + TM_C + dc0, y);
+      ptx::tmem_wait_ld();
+      if (row_ok && !(p.dbg & 8)) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k < ncol)
+            asm volatile("red.global.add.f64 [%0], %1;" ::"l"(ypart + (size_t)k * p.nrows),
+                         "d"(f32_to_f64_alu(y[k]))
+                         : "memory");
+      }
+    };
+    for (int t = set; t < T; t += NSET) {
+      const int b = t % NB;                   // buffer and phase of tile t
+      const uint32_t bph = (t / NB) & 1;
+      // S(t) needs GEMM1(t) <- GEMM2(t - NB) <- (if that tile opens chunk >= drained + 2) this
+      // warp's share of chunk `drained`: finish it before blocking, so the pipeline can never
+      // wait on a drain that is itself waiting (deadlock-free for any CH).
+      if (drainer && dc0 < p.s_pad)
+        while (drained < NCH - 1 && t - NB >= (drained + 2) * CH) drain_all(drained);
+      const bool tr = lane == 0 && q == 0 && half == 0 && set == 0;
       if (tr) trace_ev(p, t, 2);
-      ptx::mbar_wait(&s_full[b], bph);
+      if (p.sleep_ns > 0)
+        ptx::mbar_wait_sleep(&s_full[b], bph, p.sleep_ns);
+      else
+        ptx::mbar_wait(&s_full[b], bph);
       ptx::tc_fence_after();
       if (tr) trace_ev(p, t, 3);
-      const uint32_t col = tmem + lane_off + b * 64 + half * 32;
-      uint32_t v[32];
-      ptx::tmem_ld32(col, v);
-      ptx::tmem_wait_ld();
-      float kv[32];
-      if (p.kind == WGP_MATERN32) {
+      const int64_t gj_base = (int64_t)(jt0 + t) * BJ + half * 32;
+      const bool diag = p.gram && gj_base < grow0 + BM && gj_base + 32 > grow0;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float d2 = fmaxf(__uint_as_float(v[c]), 0.0f);
-          const float rr = ptx::sqrt_approx(d2);
-          const float e = ptx::ex2_approx(fmaf(rr, p.neg_c_log2e, KSCALE_LOG2));  // 2^10 e^{-z}
-          const float z = rr * p.c1;
-          kv[c] = fmaf(z, e, e);  // 2^10 (1+z) e^{-z}
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const uint32_t col = tmem + lane_off + b * 64 + half * 32 + h2 * 16;
+        uint32_t v[16];
+        ptx::tmem_ld16(col, v);
+        ptx::tmem_wait_ld();
+        if (tr && h2 == 0) trace_ev(p, t, 7);
+        float kv[16];
+        if (p.dbg & 4) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) kv[c] = __uint_as_float(v[c]);
+        } else {
+          kernel_map<SWQ, 16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
         }
-      } else {
+        if (diag) {  // tile touches the diagonal: k(x,x) = s^2 exactly
+          const int64_t gj0 = gj_base + h2 * 16;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float d2 = fmaxf(__uint_as_float(v[c]), 0.0f);
-          kv[c] = ptx::ex2_approx(fmaf(d2, p.neg_c_log2e, KSCALE_LOG2));  // 2^10 e^{-d2/2l^2}
+          for (int c = 0; c < 16; ++c)
+            if (gj0 + c == gi) kv[c] = kdiag;
         }
-      }
-      const int64_t gj0 = (int64_t)(jt0 + t) * BJ + half * 32;
-      if (p.gram && gj0 < grow0 + BM && gj0 + 32 > grow0) {  // tile touches the diagonal
+        uint32_t hi[8], lo[8];
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (gj0 + c == gi) kv[c] = kdiag;  // k(x,x) = s^2 exactly
-      }
-      uint32_t hi[16], lo[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        hi[c] = pack_h2(kv[2 * c], kv[2 * c + 1]);
-        const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hi[c]));
-        lo[c] = pack_h2(kv[2 * c] - hf.x, kv[2 * c + 1] - hf.y);
+        for (int c = 0; c < 8; ++c) {
+          // hi = kv cut to fp16's 10 mantissa bits (exact in fp16 over its normal range; an
+          // integer LOP on the ALU pipe), lo = kv - hi (FADD2, exact) rounded to fp16
+          const float2 hf = make_float2(__uint_as_float(__float_as_uint(kv[2 * c]) & 0xFFFFE000u),
+                                        __uint_as_float(__float_as_uint(kv[2 * c + 1]) & 0xFFFFE000u));
+          const float2 rem =
+              __fadd2_rn(make_float2(kv[2 * c], kv[2 * c + 1]), make_float2(-hf.x, -hf.y));
+          hi[c] = pack_h2(hf.x, hf.y);
+          lo[c] = pack_h2(rem.x, rem.y);
+        }
+        // K back into the 16 columns just read: [hi 8 | lo 8]
+        ptx::tmem_st8(col, hi);
+        ptx::tmem_st8(col + 8, lo);
       }
       if (tr) trace_ev(p, t, 4);
-      // K back into the columns this warp read: [hi 16 | lo 16]
-      ptx::tmem_st16(col, hi);
-      ptx::tmem_st16(col + 16, lo);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&k_full[b]);
       if (tr) trace_ev(p, t, 5);
-      b += 2;  // tile t + 2 -> buffer (t + 2) % NB, phase ((t + 2) / NB) & 1
-      if (b >= NB) { b -= NB; bph ^= 1; }
+      if (lane == 0 && half == 0 && set == 0 && (q == 1 || q == 3)) trace_ev(p, t, q == 1 ? 10 : 11);
+      if (drainer && dc0 < p.s_pad && drained < NCH - 1 && t >= (drained + 1) * CH + 4)
+        drain_step(drained);
     }
-    // ------------------------------------------------------------ output
-    while (drained < NCH) drain(drained++);
-    const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
-    if (lr < p.nrows && dc0 < p.s) {
-      const int64_t base = lr * p.s;
-      if (p.Ysplit) {  // partial over this CTA's j range; reduce_splits adds the rest
-        double* dst = p.Ysplit + (size_t)blockIdx.y * p.nrows * p.s + base;
-        for (int col = dc0; col < dc0 + 16 && col < p.s; ++col)
-          dst[col] = ypart[(size_t)col * BM + r] * (p.out_scale * (double)p.vscale[col]);
-      } else {
-        for (int col = dc0; col < dc0 + 16 && col < p.s; ++col) {
-          double acc = ypart[(size_t)col * BM + r] * (p.out_scale * (double)p.vscale[col]);
-          if (p.gram) acc += p.noise2 * p.V64[gi * p.s + col];
-          p.Y64[base + col] = p.B64 ? p.B64[base + col] - acc : acc;
-        }
-      }
+    if (warp == NROLE && lane == 0) cta_ev(p, 1);
+    if (drainer && dc0 < p.s_pad) {
+      while (drained < NCH) drain_all(drained);
+      drain_corr();
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) cta_ev(p, 2);
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }
 }
 
-// XA / XB operand rows in the tiled K-major "interleave" layout
-// [row/8][k/4][row%8][k%4], from the centered fp64 rows.
+// XA / XB operand rows in the tiled K-major "interleave" layout of 8-row x 16-byte core
+// matrices: [row/8][k/CK][row%8][k%CK], CK = 16 / element size, from the centered fp64 rows
+// scaled by `inv_l` (1 for tf32 operands; 1/l for fp16 so coordinates are O(1)).
+template <typename E>
+__device__ __forceinline__ E to_op(double v);
+template <>
+__device__ __forceinline__ float to_op<float>(double v) { return tf32_rn((float)v); }
+template <>
+__device__ __forceinline__ __half to_op<__half>(double v) { return __double2half(v); }
+__device__ __forceinline__ double op_val(float v) { return (double)v; }
+__device__ __forceinline__ double op_val(__half v) { return (double)__half2float(v); }
+
+template <typename E>
 __global__ void build_operands_kernel(const double* __restrict__ X, int dpad, int dim,
-                                      const double* __restrict__ center, int64_t n, int K1,
-                                      float* __restrict__ XA, float* __restrict__ XB) {
+                                      const double* __restrict__ center, double inv_l, int64_t n,
+                                      int K1, int split, E* __restrict__ XA, E* __restrict__ XB) {
+  constexpr int CK = 16 / sizeof(E);
+  const E one = to_op<E>(1.0);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t g = i >> 3, ri = i & 7;
-    auto at = [&](int k) -> int64_t { return ((g * (K1 / 4) + k / 4) * 8 + ri) * 4 + (k & 3); };
+    auto at = [&](int k) -> int64_t { return ((g * (K1 / CK) + k / CK) * 8 + ri) * CK + (k % CK); };
     double sq = 0.0;
     for (int k = 0; k < dim; ++k) {
-      const double x = X[i * dpad + k] - center[k];
+      const double x = (X[i * dpad + k] - center[k]) * inv_l;
       sq += x * x;
-      const float xf = (float)x;
-      const float xh = __uint_as_float(tf32_hi(xf));
-      const float xl = (float)(x - (double)xh);
-      XA[at(k)] = -2.0f * xh;
-      XA[at(dim + k)] = -2.0f * xh;
-      XA[at(2 * dim + k)] = -2.0f * xl;
+      const E xh = to_op<E>(x);
+      const E m2xh = to_op<E>(-2.0 * op_val(xh));
+      XA[at(k)] = m2xh;
       XB[at(k)] = xh;
-      XB[at(dim + k)] = xl;
-      XB[at(2 * dim + k)] = xh;
+      if (split) {
+        const E xl = to_op<E>(x - op_val(xh));
+        XA[at(dim + k)] = m2xh;
+        XA[at(2 * dim + k)] = to_op<E>(-2.0 * op_val(xl));
+        XB[at(dim + k)] = xl;
+        XB[at(2 * dim + k)] = xh;
+      }
     }
-    const float sqh = __uint_as_float(tf32_hi((float)sq));
-    const float sql = (float)(sq - (double)sqh);
-    const int b = 3 * dim;
-    XA[at(b)] = sqh;
-    XA[at(b + 1)] = sql;
-    XA[at(b + 2)] = 1.0f;
-    XA[at(b + 3)] = 1.0f;
-    XB[at(b)] = 1.0f;
-    XB[at(b + 1)] = 1.0f;
-    XB[at(b + 2)] = sqh;
-    XB[at(b + 3)] = sql;
-    for (int k = b + 4; k < K1; ++k) {
-      XA[at(k)] = 0.0f;
-      XB[at(k)] = 0.0f;
+    const E sqh = to_op<E>(sq);
+    int b = dim;
+    if (split) {
+      const E sql = to_op<E>(sq - op_val(sqh));
+      b = 3 * dim;
+      XA[at(b)] = sqh;
+      XA[at(b + 1)] = sql;
+      XA[at(b + 2)] = one;
+      XA[at(b + 3)] = one;
+      XB[at(b)] = one;
+      XB[at(b + 1)] = one;
+      XB[at(b + 2)] = sqh;
+      XB[at(b + 3)] = sql;
+      b += 4;
+    } else {
+      XA[at(b)] = sqh;
+      XA[at(b + 1)] = one;
+      XB[at(b)] = one;
+      XB[at(b + 1)] = sqh;
+      b += 2;
     }
+    for (int k = b; k < K1; ++k) {
+      XA[at(k)] = to_op<E>(0.0);
+      XB[at(k)] = to_op<E>(0.0);
+    }
+  }
+}
+
+// max over rows of |x - c|_inf / l and |x - c|^2 / l^2 (one block; operand rebuilds only)
+__global__ void scaled_extent_kernel(const double* __restrict__ X, int dpad, int dim,
+                                     const double* __restrict__ center, double inv_l, int64_t n,
+                                     double* __restrict__ out) {
+  __shared__ double red[2][1024];
+  double mx = 0.0, msq = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    double sq = 0.0;
+    for (int k = 0; k < dim; ++k) {
+      const double x = (X[i * dpad + k] - center[k]) * inv_l;
+      sq += x * x;
+      mx = fmax(mx, fabs(x));
+    }
+    msq = fmax(msq, sq);
+  }
+  red[0][threadIdx.x] = mx;
+  red[1][threadIdx.x] = msq;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red[0][threadIdx.x] = fmax(red[0][threadIdx.x], red[0][threadIdx.x + o]);
+      red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = red[0][0];
+    out[1] = red[1][0];
   }
 }
 
@@ -446,18 +713,38 @@ __global__ void split_v_kernel(const double* __restrict__ V, int64_t ncols, int 
   }
 }
 
-// Y = sum over j-splits (fixed order) + sigma^2 V_i (gram), or B - that.
-__global__ void reduce_splits_kernel(const double* __restrict__ Ysplit, int nsplit, int64_t nrows,
-                                     int64_t row0, int s, const double* __restrict__ V64,
+// Y = (sum over j-splits, fixed order) * s^2 2^-10 / scale_c + sigma^2 V_i (gram), or B - that.
+// Partials are column-major [nsplit][s][nrows]; 32 x 32 (row, column) tiles are transposed
+// through shared memory so both the partial reads and the row-major writes coalesce.
+__global__ void reduce_splits_kernel(const double* __restrict__ Ypart, int nsplit, int64_t nrows,
+                                     int64_t row0, int s, const float* __restrict__ vscale,
+                                     double out_scale, const double* __restrict__ V64,
                                      const double* __restrict__ B64, double noise2, int gram,
                                      double* __restrict__ Y64) {
-  const int64_t total = nrows * s;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  __shared__ double tile[32][33];
+  const int64_t rb = (int64_t)blockIdx.x * 32;
+  const int cb = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  for (int k = ty; k < 32; k += 8) {
+    const int c = cb + k;
+    const int64_t r = rb + tx;
     double acc = 0.0;
-    for (int q = 0; q < nsplit; ++q) acc += Ysplit[(size_t)q * total + e];
-    if (gram) acc += noise2 * V64[row0 * s + e];
-    Y64[e] = B64 ? B64[e] - acc : acc;
+    if (c < s && r < nrows) {
+      for (int q = 0; q < nsplit; ++q) acc += Ypart[((size_t)q * s + c) * nrows + r];
+      acc *= out_scale * (double)vscale[c];
+    }
+    tile[k][tx] = acc;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t r = rb + k;
+    const int c = cb + tx;
+    if (c < s && r < nrows) {
+      const int64_t e = r * s + c;
+      double acc = tile[tx][k];
+      if (gram) acc += noise2 * V64[row0 * s + e];
+      Y64[e] = B64 ? B64[e] - acc : acc;
+    }
   }
 }
 
@@ -486,47 +773,87 @@ inline int choose_splits(int row_ctas, int ntiles) {
 
 }  // namespace tc
 
-int tc_k1(int dim) { return ((3 * dim + 4 + 7) / 8) * 8; }
+int tc_k1(int dim, int precision, bool f16) {
+  const int k = precision == WGP_TF32 ? dim + 2 : 3 * dim + 4;
+  const int q = f16 ? 16 : 8;  // one MMA K-step
+  return ((k + q - 1) / q) * q;
+}
 
 // Rebuild the tiled operand rows of an operator (after append).  XA/XB hold
-// round_up(n, 128) rows so every CTA tile and every 64-row j tile is in bounds.
-void tc_build_operands(const Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
+// round_up(n, 128) rows so every CTA tile and every 64-row j tile is in bounds.  fp16
+// operands (3xF16 split of x / l) are used when the scaled coordinates stay well inside the
+// fp16 range (|x|/l <= 64, |x|^2/l^2 <= 8192); tf32 (x itself) otherwise.
+void tc_build_operands(Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
                        cudaStream_t st) {
-  const int K1 = tc_k1(op.dim);
+  const double inv_l = 1.0 / op.lengthscale;
+  bool f16 = false;
+  static const int force_tf32 = getenv("WGP_TC_TF32_GEMM1") ? atoi(getenv("WGP_TC_TF32_GEMM1")) : 0;
+  if (op.precision == WGP_F32_3XTF32 && !force_tf32) {
+    DBuf<double> ext(2);
+    tc::scaled_extent_kernel<<<1, 1024, 0, st>>>(op.X64.p, op.dpad, op.dim, center, inv_l, op.n,
+                                                ext.p);
+    WGP_CUDA(cudaGetLastError());
+    double h[2];
+    WGP_CUDA(cudaMemcpyAsync(h, ext.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    f16 = h[0] <= 64.0 && h[1] <= 8192.0;
+  }
+  op.tc_f16 = f16;
+  const int K1 = tc_k1(op.dim, op.precision, f16);
   const int64_t npad = ((op.n + tc::BM - 1) / tc::BM) * tc::BM;
-  XA.ensure((size_t)npad * K1);
-  XB.ensure((size_t)npad * K1);
-  WGP_CUDA(cudaMemsetAsync(XA.p, 0, sizeof(float) * npad * K1, st));
-  WGP_CUDA(cudaMemsetAsync(XB.p, 0, sizeof(float) * npad * K1, st));
-  tc::build_operands_kernel<<<tc::grid_for(op.n), 256, 0, st>>>(op.X64.p, op.dpad, op.dim, center,
-                                                                op.n, K1, XA.p, XB.p);
+  const size_t bytes = (size_t)npad * K1 * (f16 ? 2 : 4);
+  XA.ensure(bytes / 4);
+  XB.ensure(bytes / 4);
+  WGP_CUDA(cudaMemsetAsync(XA.p, 0, bytes, st));
+  WGP_CUDA(cudaMemsetAsync(XB.p, 0, bytes, st));
+  const int split = op.precision == WGP_TF32 ? 0 : 1;
+  if (f16)
+    tc::build_operands_kernel<__half><<<tc::grid_for(op.n), 256, 0, st>>>(
+        op.X64.p, op.dpad, op.dim, center, inv_l, op.n, K1, split,
+        reinterpret_cast<__half*>(XA.p), reinterpret_cast<__half*>(XB.p));
+  else
+    tc::build_operands_kernel<float><<<tc::grid_for(op.n), 256, 0, st>>>(
+        op.X64.p, op.dpad, op.dim, center, 1.0, op.n, K1, split, XA.p, XB.p);
   WGP_CUDA(cudaGetLastError());
 }
 
-size_t tc_smem_bytes(int K1, int s_pad, int* ns_out) {
-  const size_t xa = (size_t)tc::BM * K1 * 4;
-  const size_t stage = (size_t)tc::BJ * K1 * 4 + 2 * (size_t)s_pad * tc::BJ * 2;
-  const size_t tail = 512 + (size_t)tc::BM * s_pad * 8;  // barriers + fp64 partial Y
-  int ns = (int)((227 * 1024 - xa - tail) / stage);
-  if (ns > 6) ns = 6;
-  *ns_out = ns;
-  return xa + ns * stage + tail;
+// Shared memory: XA rows + NSX XB stages + NSV V stages + 1 KB of barriers.  XB lives from
+// its copy to GEMM1 (~1 tile period), V until GEMM2 after the map (~4 periods), so the V
+// ring gets the space first: NSX = 3 (2 if tight), NSV up to 8.
+size_t tc_smem_bytes(int K1, int esz, int s_pad, int* nsx_out, int* nsv_out) {
+  const size_t xa = (size_t)tc::BM * K1 * esz;
+  const size_t xb = (size_t)tc::BJ * K1 * esz;
+  const size_t vb = 2 * (size_t)s_pad * tc::BJ * 2;
+  const size_t avail = 227 * 1024 - 1024 - xa;
+  static const int want_x = getenv("WGP_TC_NSX") ? atoi(getenv("WGP_TC_NSX")) : 5;
+  int nsx = want_x, nsv = 0;
+  for (; nsx >= 2; --nsx) {
+    if (avail < nsx * xb) continue;
+    nsv = (int)std::min<size_t>(8, (avail - nsx * xb) / vb);
+    if (nsv >= 5 || nsx == 2) break;
+  }
+  *nsx_out = nsx;
+  *nsv_out = nsv;
+  return xa + nsx * xb + nsv * vb + 1024;
 }
 
-bool tc_supported(int dim) {
-  int ns = 0;
-  tc_smem_bytes(tc_k1(dim), tc::MAX_SPAD, &ns);
-  return ns >= 2;
+bool tc_supported(int dim, int precision) {
+  int nsx = 0, nsv = 0;
+  tc_smem_bytes(tc_k1(dim, precision, false), 4, tc::MAX_SPAD, &nsx, &nsv);
+  return nsx >= 2 && nsv >= 2;
 }
 
 // Y = (K(Xr, Xc) [+ sigma^2 I]) V, rows [row0, row0 + nrows) of the operator.  V64 and
 // Y64/B64 are fp64 row-major; RHS chunks of <= 128 columns per launch.
-void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int64_t nrows,
+void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64_t nrows,
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
                        DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st) {
   if (nrows <= 0 || s <= 0) return;
-  const int K1 = tc_k1(op.dim);
+  const bool f16 = op.tc_f16;
+  const int esz = f16 ? 2 : 4;
+  const int K1 = tc_k1(op.dim, op.precision, f16);
+  const void* XA_rows = reinterpret_cast<const char*>(XA_all) + (size_t)row0 * K1 * esz;
   const KParams kp = op.kp();
   for (int c0 = 0; c0 < s; c0 += tc::MAX_SPAD) {
     const int sc = std::min(tc::MAX_SPAD, s - c0);
@@ -560,65 +887,91 @@ void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int6
     WGP_CUDA(cudaGetLastError());
     tc::Params prm;
     prm.XA = XA_rows;
+    prm.g1f16 = f16 ? 1 : 0;
     prm.XB = XB;
     prm.Vt = vt;
     prm.vscale = sc_down;
-    prm.V64 = Vc;
-    prm.B64 = Bc;
-    prm.Y64 = Yc;
     prm.nrows = nrows;
     prm.row0 = row0;
     prm.ncols = ncols;
     prm.ntiles = ntiles;
+    static const int forced_ch = getenv("WGP_TC_CH") ? atoi(getenv("WGP_TC_CH")) : 0;
+    prm.ch = forced_ch > 0 ? forced_ch : tc::CH_DEFAULT;
     const int row_ctas = (int)((nrows + tc::BM - 1) / tc::BM);
     static const int forced_splits = getenv("WGP_TC_SPLITS") ? atoi(getenv("WGP_TC_SPLITS")) : 0;
     const int nsplit = forced_splits > 0 ? forced_splits : tc::choose_splits(row_ctas, ntiles);
     prm.tiles_per_split = (ntiles + nsplit - 1) / nsplit;
     const int gy = (ntiles + prm.tiles_per_split - 1) / prm.tiles_per_split;
-    prm.Ysplit = nullptr;
-    if (gy > 1) {
-      ysplit.ensure((size_t)gy * nrows * sc);
-      prm.Ysplit = ysplit.p;
-    }
+    ysplit.ensure((size_t)gy * nrows * sc);
+    prm.Ypart = ysplit.p;
     prm.s = sc;
     prm.s_pad = s_pad;
     prm.K1 = K1;
     prm.kind = kp.kind;
-    prm.c1 = (float)kp.c1;
-    prm.neg_c_log2e = (float)(-kp.c1 * 1.4426950408889634);
+    // fp16 operands are in units of l: z = sqrt(3) r' (Matern), r'^2 / 2 (RBF)
+    const double c1 = f16 ? (kp.kind == WGP_MATERN32 ? kp.c1 * op.lengthscale
+                                                     : kp.c1 * op.lengthscale * op.lengthscale)
+                          : kp.c1;
+    prm.c1 = (float)c1;
+    prm.neg_c_log2e = (float)(-c1 * 1.4426950408889634);
     prm.out_scale = kp.s2 * 0x1.0p-10;
     prm.noise2 = kp.noise2;
     prm.gram = gram ? 1 : 0;
+    static const int dbg = getenv("WGP_TC_DEBUG") ? atoi(getenv("WGP_TC_DEBUG")) : 0;
+    prm.dbg = dbg;
+    static const int sleep_ns = getenv("WGP_TC_SLEEP") ? atoi(getenv("WGP_TC_SLEEP")) : 0;
+    prm.sleep_ns = sleep_ns;
     prm.trace = nullptr;
     static const char* trace_path = getenv("WGP_TC_TRACE");
+    prm.cta_trace = nullptr;
     DBuf<unsigned long long> trace_buf;
+    const size_t nctas = (size_t)row_ctas * gy;
     if (trace_path) {
-      trace_buf.alloc((size_t)ntiles * 8);
-      WGP_CUDA(cudaMemsetAsync(trace_buf.p, 0, sizeof(unsigned long long) * ntiles * 8, st));
+      trace_buf.alloc((size_t)ntiles * tc::TRW + nctas * 4);
+      WGP_CUDA(cudaMemsetAsync(trace_buf.p, 0, sizeof(unsigned long long) * (ntiles * tc::TRW + nctas * 4), st));
       prm.trace = trace_buf.p;
+      prm.cta_trace = trace_buf.p + (size_t)ntiles * tc::TRW;
     }
-    int ns = 0;
-    const size_t smem = tc_smem_bytes(K1, s_pad, &ns);
-    WGP_REQUIRE(ns >= 2, "kmatvec_tc: dim %d too large for the shared-memory pipeline", op.dim);
-    WGP_CUDA(cudaFuncSetAttribute(tc::kmatvec_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    tc::kmatvec_tc_kernel<<<dim3(row_ctas, gy), tc::NTHREADS, smem, st>>>(prm, ns);
+    int nsx = 0, nsv = 0;
+    const size_t smem = tc_smem_bytes(K1, esz, s_pad, &nsx, &nsv);
+    WGP_REQUIRE(nsx >= 2 && nsv >= 2, "kmatvec_tc: dim %d too large for the shared-memory pipeline",
+                op.dim);
+    static const int forced_swq = getenv("WGP_TC_SWQ") ? atoi(getenv("WGP_TC_SWQ")) : -1;
+    const int swq = forced_swq >= 0 ? std::min(forced_swq, 4)
+                                    : (kp.kind == WGP_MATERN32 ? tc::SWQ_MATERN : tc::SWQ_RBF);
+    auto kern = swq == 0 ? tc::kmatvec_tc_kernel<0>
+              : swq == 1 ? tc::kmatvec_tc_kernel<1>
+              : swq == 2 ? tc::kmatvec_tc_kernel<2>
+              : swq == 3 ? tc::kmatvec_tc_kernel<3> : tc::kmatvec_tc_kernel<4>;
+    WGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<dim3(row_ctas, gy), tc::NTHREADS, smem, st>>>(prm, nsx, nsv);
     WGP_CUDA(cudaGetLastError());
-    if (gy > 1) {
-      tc::reduce_splits_kernel<<<tc::grid_for(nrows * sc), 256, 0, st>>>(
-          ysplit.p, gy, nrows, row0, sc, Vc, Bc, kp.noise2, gram ? 1 : 0, Yc);
+    {
+      tc::reduce_splits_kernel<<<dim3((unsigned)((nrows + 31) / 32), (sc + 31) / 32), 256, 0, st>>>(
+          ysplit.p, gy, nrows, row0, sc, sc_down, prm.out_scale, Vc, Bc, kp.noise2, gram ? 1 : 0, Yc);
       WGP_CUDA(cudaGetLastError());
     }
     if (trace_path) {
-      std::vector<unsigned long long> h((size_t)ntiles * 8);
+      std::vector<unsigned long long> h((size_t)ntiles * tc::TRW + nctas * 4);
       WGP_CUDA(cudaMemcpyAsync(h.data(), trace_buf.p, sizeof(unsigned long long) * h.size(),
                                cudaMemcpyDeviceToHost, st));
       WGP_CUDA(cudaStreamSynchronize(st));
       if (FILE* f = fopen(trace_path, "w")) {
-        fprintf(f, "tile,g1_issue,g2_issue,epi_wait_s,epi_s_ready,epi_wait_k,epi_done,prod_issue\n");
+        fprintf(f, "tile,g1_issue,g2_issue,epi_wait_s,epi_s_ready,epi_wait_k,epi_done,prod_issue,epi_ld_done,v_issue,g2_vready,done_q1,done_q3\n");
         for (int t = 0; t < ntiles; ++t)
-          fprintf(f, "%d,%llu,%llu,%llu,%llu,%llu,%llu,%llu\n", t, h[t * 8], h[t * 8 + 1], h[t * 8 + 2],
-                  h[t * 8 + 3], h[t * 8 + 4], h[t * 8 + 5], h[t * 8 + 6]);
+        {
+          fprintf(f, "%d", t);
+          for (int k = 0; k < tc::TRW; ++k) fprintf(f, ",%llu", h[(size_t)t * tc::TRW + k]);
+          fprintf(f, "\n");
+        }
+        fclose(f);
+      }
+      if (FILE* f = fopen((std::string(trace_path) + ".ctas").c_str(), "w")) {
+        fprintf(f, "cta_x,cta_y,start_ns,loop_end_ns,end_ns,smid\n");
+        const unsigned long long* c = h.data() + (size_t)ntiles * tc::TRW;
+        for (size_t i = 0; i < nctas; ++i)
+          fprintf(f, "%zu,%zu,%llu,%llu,%llu,%llu\n", i % row_ctas, i / row_ctas, c[i * 4], c[i * 4 + 1],
+                  c[i * 4 + 2], c[i * 4 + 3]);
         fclose(f);
       }
     }

@@ -105,10 +105,9 @@ static void ensure_tc_operands(Op& op, cudaStream_t st) {
 static void dispatch(Op& op, const double* B, const double* V, double* Y, int s, cudaStream_t st) {
   int64_t r0, r1;
   op.local_rows(&r0, &r1);
-  if (op.tensor() && tc_supported(op.dim)) {
+  if (op.tensor() && tc_supported(op.dim, op.precision)) {
     ensure_tc_operands(op, st);
-    const int K1 = tc_k1(op.dim);
-    launch_kmatvec_tc(op, op.XA.p + r0 * K1, op.XB.p, r1 - r0, r0, op.n, V, s, B, Y, true, op.vt,
+    launch_kmatvec_tc(op, op.XA.p, op.XB.p, r1 - r0, r0, op.n, V, s, B, Y, true, op.vt,
                       op.vchunk, op.ychunk, op.ysplit, st);
   } else if (op.f64()) {
     launch_kmatvec_simt<double>(op, op.X64.p + r0 * op.dpad, r1 - r0, r0, op.X64.p, op.n, V, s, B,

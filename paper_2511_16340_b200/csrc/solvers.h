@@ -43,14 +43,14 @@ template <typename T>
 void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
                          int64_t ncols, const double* V, int s, const double* B, double* Y,
                          bool gram, cudaStream_t st);
-void launch_kmatvec_tc(const Op& op, const float* XA_rows, const float* XB, int64_t nrows,
+void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64_t nrows,
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
                        DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st);
-void tc_build_operands(const Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
+void tc_build_operands(Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
                        cudaStream_t st);
-int tc_k1(int dim);
-bool tc_supported(int dim);  // false -> the fp32 CUDA-core kernel serves this dim
+int tc_k1(int dim, int precision, bool f16);
+bool tc_supported(int dim, int precision);  // false -> the fp32 CUDA-core kernel serves this dim
 
 template <typename T>
 void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb, const double* U1,
