@@ -89,6 +89,7 @@ struct Params {
   double noise2;
   int gram;
   int sleep_ns;  // epilogue wait backoff (WGP_TC_SLEEP)
+  int role_sleep_ns;  // MMA-issuer wait backoff (WGP_TC_RSLEEP)
   int dbg;  // timing experiments only (WGP_TC_DEBUG): 1 GEMM2 hi.hi only, 2 GEMM1 one K-step, 4 no map
   unsigned long long* trace;  // debug: per-tile event clocks of CTA 0 (nullptr normally)
   unsigned long long* cta_trace;  // debug: per-CTA [start, loop end, end] globaltimer + smid
@@ -324,7 +325,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // issues GEMM2 (K.V); each waits only on its own inputs and each tcgen05.commit tracks
     // its own thread's MMAs.  Whole warps run the schedule (uniform control flow,
     // descriptors in uniform registers); one elected lane issues.
-    if (warp == 1) {
+    if (warp == ((p.dbg & 32) ? 3 : 1)) {  // dbg 32: GEMM1 on warp 3, GEMM2 on warp 1
       const uint32_t idesc1 = p.g1f16 ? ptx::idesc_f16(BM, BJ) : ptx::idesc_tf32(BM, BJ);
       const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
       const uint64_t dXB0 = ptx::umma_desc(ptx::smem_u32(sXB), 128, sbo1);
@@ -333,8 +334,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       int st1 = 0, b1 = 0;
       uint32_t ph1 = 0, phb1 = 0;
       for (int t = 0; t < T; ++t) {
-        ptx::mbar_wait(&xb_full[st1], ph1);
-        if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
+        if (p.role_sleep_ns > 0) {
+          ptx::mbar_wait_sleep(&xb_full[st1], ph1, p.role_sleep_ns);
+          if (t >= NB) ptx::mbar_wait_sleep(&b_free[b1], phb1 ^ 1, p.role_sleep_ns);
+        } else {
+          ptx::mbar_wait(&xb_full[st1], ph1);
+          if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
+        }
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 0);
@@ -366,9 +372,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         const int c = t / CH, ya = c & 1;
         const bool first = t == c * CH, last = t == T - 1 || t == c * CH + CH - 1;
         if (first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
-        ptx::mbar_wait(&v_full[st2], ph2);
-        if (lane == 0) trace_ev(p, t, 9);
-        ptx::mbar_wait(&k_full[b2], phb2);
+        if (p.role_sleep_ns > 0) {
+          ptx::mbar_wait_sleep(&v_full[st2], ph2, p.role_sleep_ns);
+          if (lane == 0) trace_ev(p, t, 9);
+          ptx::mbar_wait_sleep(&k_full[b2], phb2, p.role_sleep_ns);
+        } else {
+          ptx::mbar_wait(&v_full[st2], ph2);
+          if (lane == 0) trace_ev(p, t, 9);
+          ptx::mbar_wait(&k_full[b2], phb2);
+        }
         if ((p.dbg & 16) && t > 0) {  // experiment: issue only into a drained tensor queue
           const int bp = (t - 1) % NB;
           ptx::mbar_wait(&b_free[bp], ((t - 1) / NB) & 1);
@@ -921,6 +933,8 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     prm.dbg = dbg;
     static const int sleep_ns = getenv("WGP_TC_SLEEP") ? atoi(getenv("WGP_TC_SLEEP")) : 0;
     prm.sleep_ns = sleep_ns;
+    static const int rsleep_ns = getenv("WGP_TC_RSLEEP") ? atoi(getenv("WGP_TC_RSLEEP")) : 0;
+    prm.role_sleep_ns = rsleep_ns;
     prm.trace = nullptr;
     static const char* trace_path = getenv("WGP_TC_TRACE");
     prm.cta_trace = nullptr;
