@@ -186,6 +186,13 @@ double wgp_rng_chi_square3(uint64_t* state);
 uint64_t wgp_rng_uniform_index(uint64_t* state, uint64_t n);
 /* n consecutive scale * normal() draws from (and advancing) the generator at *state. */
 void wgp_rng_normal_fill(uint64_t* state, int64_t n, double scale, double* out);
+
+/* ---- measurement: CUDA-event timing of the tensor-core kernel-matvec launches only (the
+ *      prep kernels around it excluded), for roofline reporting.  enable != 0 starts
+ *      recording (and clears); read synchronizes the recorded events and returns the summed
+ *      kernel time and launch count since the last enable. ---- */
+void wgp_kernel_timer_enable(int enable);
+wgp_status wgp_kernel_timer_read(double* total_ms, int64_t* launches);
 /* out[i] = scale * Rng(seed).normal(), i = 0..n-1 (build_sample_rhs noise, sampling.cpp:58-62) */
 void wgp_normal_fill(uint64_t seed, int64_t n, double scale, double* out);
 /* sample_prior (sampling.cpp:14-35): Omega F x dim column-major, phases F, amps F.

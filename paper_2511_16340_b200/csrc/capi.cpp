@@ -103,6 +103,28 @@ extern "C" {
 
 int wgp_abi_version(void) { return WGP_ABI_VERSION; }
 
+void wgp_kernel_timer_enable(int enable) {
+  wgp::KernelTimer& kt = wgp::kernel_timer();
+  kt.clear();
+  kt.on = enable != 0;
+}
+
+wgp_status wgp_kernel_timer_read(double* total_ms, int64_t* launches) {
+  return guard([&] {
+    WGP_REQUIRE(total_ms && launches, "wgp_kernel_timer_read: null argument");
+    wgp::KernelTimer& kt = wgp::kernel_timer();
+    double tot = 0.0;
+    for (auto& e : kt.ev) {
+      WGP_CUDA(cudaEventSynchronize(e.second));
+      float ms = 0.f;
+      WGP_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+      tot += ms;
+    }
+    *total_ms = tot;
+    *launches = (int64_t)kt.ev.size();
+  });
+}
+
 const char* wgp_last_error(void) { return g_last_error.c_str(); }
 
 void wgp_solver_config_default(wgp_solver_config* c) {  // solvers.hpp:27-48

@@ -39,8 +39,14 @@
 
 #include "common.cuh"
 #include "ptx.cuh"
+#include "solvers.h"
 
 namespace wgp {
+KernelTimer& kernel_timer() {
+  static KernelTimer t;
+  return t;
+}
+
 namespace tc {
 
 constexpr int BM = 128;        // rows per CTA (UMMA M)
@@ -958,7 +964,18 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
               : swq == 2 ? tc::kmatvec_tc_kernel<2>
               : swq == 3 ? tc::kmatvec_tc_kernel<3> : tc::kmatvec_tc_kernel<4>;
     WGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    KernelTimer& kt = kernel_timer();
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (kt.on) {
+      WGP_CUDA(cudaEventCreate(&ev0));
+      WGP_CUDA(cudaEventCreate(&ev1));
+      WGP_CUDA(cudaEventRecord(ev0, st));
+    }
     kern<<<dim3(row_ctas, gy), tc::NTHREADS, smem, st>>>(prm, nsx, nsv);
+    if (kt.on) {
+      WGP_CUDA(cudaEventRecord(ev1, st));
+      kt.ev.emplace_back(ev0, ev1);
+    }
     WGP_CUDA(cudaGetLastError());
     {
       tc::reduce_splits_kernel<<<dim3((unsigned)((nrows + 31) / 32), (sc + 31) / 32), 256, 0, st>>>(

@@ -50,6 +50,19 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
 void tc_build_operands(Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
                        cudaStream_t st);
 int tc_k1(int dim, int precision, bool f16);
+// launch timing of the main TC kernel (wgp_kernel_timer_*): event pairs on the launch stream
+struct KernelTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  void clear() {
+    for (auto& e : ev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    ev.clear();
+  }
+};
+KernelTimer& kernel_timer();
 bool tc_supported(int dim, int precision);  // false -> the fp32 CUDA-core kernel serves this dim
 
 template <typename T>

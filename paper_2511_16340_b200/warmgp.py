@@ -46,7 +46,7 @@ EXPORTS = (
     "wgp_cross_matvec", "wgp_solve_many", "wgp_solve", "wgp_pivoted_cholesky", "wgp_precond_info",
     "wgp_rff_eval", "wgp_derive_seed", "wgp_rng_next_u64", "wgp_rng_uniform", "wgp_rng_normal",
     "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
-    "wgp_rng_normal_fill",
+    "wgp_rng_normal_fill", "wgp_kernel_timer_enable", "wgp_kernel_timer_read",
 )
 
 
@@ -135,6 +135,8 @@ def _declare(L):
         "wgp_rng_uniform_index": (C.c_uint64, [P, C.c_uint64]),
         "wgp_normal_fill": (None, [C.c_uint64, I64, D, P]),
         "wgp_rng_normal_fill": (None, [P, I64, D, P]),
+        "wgp_kernel_timer_enable": (None, [C.c_int]),
+        "wgp_kernel_timer_read": (C.c_int, [P, P]),
         "wgp_sample_prior": (C.c_int, [C.c_int, D, I64, I64, C.c_uint64, P, P, P]),
     }
     for name, (res, args) in sig.items():
@@ -587,3 +589,16 @@ def build_sample_rhs(op: KernelOperator, prior: RffPrior, noise_scale: float, se
     if noise_scale > 0.0:
         rhs += normal_fill(seed, rhs.size, noise_scale)
     return rhs
+
+
+def kernel_timer_enable(on: bool = True) -> None:
+    """Start (and clear) / stop CUDA-event timing of the tensor-core kmatvec kernel launches."""
+    lib().wgp_kernel_timer_enable(1 if on else 0)
+
+
+def kernel_timer_read() -> tuple[float, int]:
+    """(summed kernel milliseconds, launches) since the last kernel_timer_enable(True)."""
+    ms = C.c_double(0.0)
+    n = C.c_int64(0)
+    _check(lib().wgp_kernel_timer_read(C.byref(ms), C.byref(n)))
+    return ms.value, n.value
