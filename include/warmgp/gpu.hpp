@@ -7,10 +7,13 @@
 // device-resident KernelOperator instead of a dense Eigen::MatrixXd (which cannot
 // exist at N >= 100k): gram_matrix(X, hyp) -> KernelOperator(X, hyp), extend_system ->
 // op.append_rows(X2).  Matrices are column-major doubles like Eigen::MatrixXd; with
-// WARMGP_GPU_EIGEN defined, Eigen overloads are provided for drop-in use in the reference
-// build.
+// WARMGP_GPU_EIGEN defined, Eigen overloads (to_gpu/to_eigen, gram_matrix, append_rows,
+// warm, solve, solve_many, H * V) are provided for drop-in use in the reference build
+// (exercised by tests/cpp/test_eigen_overloads.cpp against a shim, since
+// Eigen3 is not installed in this image).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -306,6 +309,46 @@ inline Matrix eval_priors(const KernelOperator& H, const std::vector<RffPrior>& 
                      nullptr, m, m, out.data.data(), m));
   return out;
 }
+
+#ifdef WARMGP_GPU_EIGEN
+// ---------------------------------------------------------------- Eigen overloads
+// For the reference build (Eigen::MatrixXd is column-major fp64, like Matrix): the call
+// sites of INTEGRATION.md keep their Eigen values and gain the device operator.
+inline Matrix to_gpu(const Eigen::MatrixXd& A) {
+  Matrix M(A.rows(), A.cols());
+  std::copy(A.data(), A.data() + A.size(), M.data.begin());
+  return M;
+}
+inline Vector to_gpu(const Eigen::VectorXd& v) { return Vector(v.data(), v.data() + v.size()); }
+inline Eigen::MatrixXd to_eigen(const Matrix& M) {
+  Eigen::MatrixXd A(M.rows, M.cols);
+  std::copy(M.data.begin(), M.data.end(), A.data());
+  return A;
+}
+inline Eigen::VectorXd to_eigen(const Vector& v) {
+  Eigen::VectorXd e((Eigen::Index)v.size());
+  std::copy(v.begin(), v.end(), e.data());
+  return e;
+}
+inline KernelOperator gram_matrix(Context& ctx, const Eigen::MatrixXd& X, const KernelHyperparams& hyp,
+                                  Precision p = Precision::F64) {
+  return gram_matrix(ctx, to_gpu(X), hyp, p);
+}
+inline void append_rows(KernelOperator& H, const Eigen::MatrixXd& X2) { H.append_rows(to_gpu(X2)); }
+inline Initialization warm(const Eigen::VectorXd& u1) { return Initialization::warm(to_gpu(u1)); }
+inline std::vector<SolveResult> solve_many(const KernelOperator& H, const Eigen::MatrixXd& rhs,
+                                           const std::vector<Initialization>& inits,
+                                           const SolverConfig& cfg) {
+  return solve_many(H, to_gpu(rhs), inits, cfg);
+}
+inline SolveResult solve(const KernelOperator& H, const Eigen::VectorXd& b, const Initialization& init,
+                         const SolverConfig& cfg) {
+  return solve(H, to_gpu(b), init, cfg);
+}
+inline Eigen::MatrixXd operator*(const KernelOperator& H, const Eigen::MatrixXd& V) {
+  return to_eigen(H * to_gpu(V));
+}
+#endif  // WARMGP_GPU_EIGEN
 
 }  // namespace gpu
 }  // namespace warmgp

@@ -1,0 +1,50 @@
+// Exercises include/warmgp/gpu.hpp's WARMGP_GPU_EIGEN overloads (compiled against the
+// test shim tests/cpp/eigen_shim, since Eigen3 is absent): Eigen values in, the same
+// results as the plain-Matrix API out.
+#define WARMGP_GPU_EIGEN 1
+#include <warmgp/gpu.hpp>
+
+#include <cmath>
+#include <cstdio>
+
+namespace g = warmgp::gpu;
+
+int main() {
+  const int n = 200, d = 3;
+  Eigen::MatrixXd X(n, d);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < d; ++k) X(i, k) = std::sin(0.37 * i + 1.3 * k);
+  g::KernelHyperparams hyp;
+  hyp.lengthscale = 0.7;
+  hyp.noise_scale = 0.3;
+  g::Context ctx(0);
+  g::KernelOperator H = g::gram_matrix(ctx, X, hyp);
+  Eigen::VectorXd b(n);
+  for (int i = 0; i < n; ++i) b(i) = std::cos(0.11 * i);
+  g::SolverConfig cfg;
+  cfg.tolerance = 1e-8;
+  cfg.max_iters = 500;
+  const g::SolveResult r = g::solve(H, b, g::Initialization::cold(), cfg);
+  const g::SolveResult r2 = g::solve(H, g::to_gpu(b), g::Initialization::cold(), cfg);
+  if (!r.converged || r.iterations != r2.iterations) { std::printf("solve mismatch\n"); return 1; }
+  Eigen::MatrixXd V(n, 1);
+  for (int i = 0; i < n; ++i) V(i, 0) = r.v[(size_t)i];
+  const Eigen::MatrixXd HV = H * V;
+  double err = 0, nb = 0;
+  for (int i = 0; i < n; ++i) {
+    err += (HV(i, 0) - b(i)) * (HV(i, 0) - b(i));
+    nb += b(i) * b(i);
+  }
+  if (std::sqrt(err / nb) > 1e-7) { std::printf("residual %g\n", std::sqrt(err / nb)); return 1; }
+  Eigen::MatrixXd X2(20, d);
+  for (int i = 0; i < 20; ++i)
+    for (int k = 0; k < d; ++k) X2(i, k) = std::sin(0.37 * (n + i) + 1.3 * k);
+  g::append_rows(H, X2);
+  Eigen::MatrixXd B(n + 20, 2);
+  for (int i = 0; i < n + 20; ++i) { B(i, 0) = std::cos(0.11 * i); B(i, 1) = std::sin(0.05 * i); }
+  std::vector<g::Initialization> inits = {g::warm(g::to_eigen(r.v)), g::Initialization::warm(r.v)};
+  const auto rs = g::solve_many(H, B, inits, cfg);
+  if (rs.size() != 2 || !rs[0].converged || !rs[1].converged) { std::printf("solve_many failed\n"); return 1; }
+  std::printf("eigen overloads ok: %d iters, warm %d/%d\n", r.iterations, rs[0].iterations, rs[1].iterations);
+  return 0;
+}

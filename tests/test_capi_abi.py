@@ -55,3 +55,17 @@ def test_sample_prior_matches_oracle(W, O):
         assert np.array_equal(a.frequencies, b.frequencies)
         assert np.array_equal(a.phases, b.phases) and np.array_equal(a.amplitudes, b.amplitudes)
     assert np.array_equal(W.normal_fill(9, 50, 0.1), 0.1 * O.gaussian_vector(9, 50))
+
+
+def test_cpp_headers_compile_without_gpu():
+    """Both C++ test programs (reference-API mirror, Eigen overloads) compile and link here."""
+    import subprocess
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2511_16340_b200")
+    with tempfile.TemporaryDirectory() as td:
+        for src, extra in (("test_gpu_api.cpp", []), ("test_eigen_overloads.cpp",
+                                                      ["-I", os.path.join(root, "tests", "cpp", "eigen_shim")])):
+            subprocess.run(["g++", "-O1", "-std=c++17", "-I", os.path.join(root, "include"), *extra,
+                            os.path.join(root, "tests", "cpp", src), "-L", libdir, "-lwarmgp_b200",
+                            f"-Wl,-rpath,{libdir}", "-o", os.path.join(td, src + ".bin")], check=True)

@@ -17,3 +17,16 @@ def test_cpp_reference_api_mirror(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     assert "gpu.hpp ok" in r.stdout
+
+
+def test_cpp_eigen_overloads(tmp_path):
+    """gpu.hpp's WARMGP_GPU_EIGEN overloads, compiled against the test Eigen shim."""
+    exe = tmp_path / "test_eigen_overloads"
+    libdir = os.path.join(ROOT, "paper_2511_16340_b200")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-I", os.path.join(ROOT, "include"),
+                    "-I", os.path.join(ROOT, "tests", "cpp", "eigen_shim"),
+                    os.path.join(ROOT, "tests", "cpp", "test_eigen_overloads.cpp"), "-L", libdir,
+                    "-lwarmgp_b200", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert "eigen overloads ok" in r.stdout
