@@ -310,6 +310,35 @@ inline Matrix eval_priors(const KernelOperator& H, const std::vector<RffPrior>& 
   return out;
 }
 
+// eval_posterior (sampling.cpp:66-75) for S samples at m points at once:
+// out(:, s) = prior_s(X*) + K(X*, X) weights(:, s), weights n x S (pathwise samples).
+// Reference form: one PosteriorSample per call; here the training rows are the operator's.
+inline Matrix eval_posterior(const KernelOperator& H, const std::vector<RffPrior>& priors,
+                             const Matrix& weights, const Matrix& Xstar) {
+  const int S = (int)priors.size();
+  const int64_t m = Xstar.rows;
+  if (weights.rows != H.size() || weights.cols != S)
+    throw std::invalid_argument("eval_posterior: weights length != training rows");
+  Matrix out(m, S);
+  if (!S || !m) return out;
+  const int64_t F = priors[0].frequencies.rows, D = priors[0].frequencies.cols;
+  std::vector<double> Om((size_t)(S * F * D)), ph((size_t)(S * F)), am((size_t)(S * F));
+  for (int p = 0; p < S; ++p) {
+    std::copy(priors[p].frequencies.data.begin(), priors[p].frequencies.data.end(), Om.begin() + p * F * D);
+    std::copy(priors[p].phases.begin(), priors[p].phases.end(), ph.begin() + p * F);
+    std::copy(priors[p].amplitudes.begin(), priors[p].amplitudes.end(), am.begin() + p * F);
+  }
+  check(wgp_rff_eval(H.get(), Om.data(), ph.data(), am.data(), (int)F, S, priors[0].signal_scale,
+                     Xstar.data.data(), m, m, out.data.data(), m));
+  if (H.size() > 0) {
+    Matrix kw(m, S);
+    check(wgp_cross_matvec(H.get(), Xstar.data.data(), m, m, weights.data.data(), weights.rows, S,
+                           kw.data.data(), m));
+    for (size_t i = 0; i < out.data.size(); ++i) out.data[i] += kw.data[i];
+  }
+  return out;
+}
+
 #ifdef WARMGP_GPU_EIGEN
 // ---------------------------------------------------------------- Eigen overloads
 // For the reference build (Eigen::MatrixXd is column-major fp64, like Matrix): the call

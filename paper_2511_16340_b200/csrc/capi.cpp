@@ -320,10 +320,13 @@ wgp_status wgp_cross_matvec(wgp_op* op, const double* Xs, int64_t m, int64_t ldx
     if (op->f64()) {
       launch_kmatvec_simt<double>(*op, tmp.X64.p, m, 0, op->X64.p, n, dW.p, s, nullptr, dY.p,
                                   false, st);
+    } else if (op->tensor()) {
+      // tensor-core cross mode (no sigma^2 term); points outside the fp16 operand range of
+      // this operator fall back to the fp64 CUDA-core kernel
+      if (!op_cross_tc(*op, tmp.X64.p, m, tmp.dpad, dW.p, s, dY.p, st))
+        launch_kmatvec_simt<double>(*op, tmp.X64.p, m, 0, op->X64.p, n, dW.p, s, nullptr, dY.p,
+                                    false, st);
     } else {
-      if (!op->X32.p) {  // tensor-core operators keep no fp32 row copy; cross mode uses SIMT
-        throw_error(WGP_INVALID_ARGUMENT, "cross_matvec: unsupported for this precision");
-      }
       launch_kmatvec_simt<float>(*op, tmp.X32.p, m, 0, op->X32.p, n, dW.p, s, nullptr, dY.p,
                                  false, st);
     }

@@ -53,7 +53,14 @@ constexpr int BM = 128;        // rows per CTA (UMMA M)
 constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
 constexpr int NSET = 3;         // epilogue sets (8 warps each) taking tiles round-robin
 constexpr int NPROD = 1;        // producer warps per ring (XB ring, V ring); 3 measured slower
-constexpr int NROLE = 4;        // role warps: 2 MMA issuers + 2 x NPROD producers (+ alloc)
+#ifndef WGP_TC_NG2
+#define WGP_TC_NG2 3
+#endif
+// GEMM2 issuer warps taking tiles round-robin (on SMSPs 3, 0, 2): the warp issuing a tile's 12
+// MMAs costs its SM sub-partition issue slots, and K(t) needs all four TMEM quadrants
+// (one per sub-partition), so a single GEMM2 warp made its quadrant the late one every tile.
+constexpr int NG2 = WGP_TC_NG2;
+constexpr int NROLE = NG2 == 1 ? 4 : 8;  // role warps: producers, GEMM1, GEMM2 issuers
 constexpr int NTHREADS = 32 * NROLE + NSET * 256;  // role warps + NSET x 8 epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
 constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (fp64 drain after each)
@@ -235,7 +242,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* b_free = k_full + MAX_NB;     // [MAX_NB] GEMM2 -> GEMM1
   uint64_t* y_full = b_free + MAX_NB;     // [2] chunk accumulator done (GEMM2 commit)
   uint64_t* y_free = y_full + 2;          // [2] chunk accumulator drained (16 warp arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_free + 2);
+  uint64_t* g2_tok = y_free + 2;          // [NG2] GEMM2 issue-order tokens
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g2_tok + NG2);
   constexpr int NB = MAX_NB;
   // TMEM: ring of NB 64-column S/K buffers [0, 320), the two chunk accumulators of the
   // leading product Kh.Vh at TM_Y + 64 a, and one sweep-long accumulator of the correction
@@ -266,6 +274,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       ptx::mbar_init(&k_full[i], 8);
       ptx::mbar_init(&b_free[i], 1);
     }
+    for (int i = 0; i < NG2; ++i) ptx::mbar_init(&g2_tok[i], 1);
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&y_full[i], 1);
       ptx::mbar_init(&y_free[i], 4 * (p.s_pad / 16));  // drainer warps with columns
@@ -280,7 +289,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   const int KS1 = p.K1 * ESZ / 32;          // GEMM1 K-steps (32 bytes of K per instruction)
   const uint32_t sbo1 = (p.K1 * ESZ / 16) * 128;  // 8-row group stride of XA/XB tiles
 
-  if (warp != 1 && warp != 3 && warp < NROLE) {
+  const int g2k = warp == 3 ? 0 : (NG2 > 1 && warp == 4 ? 1 : (NG2 > 2 && warp == 6 ? 2 : -1));
+  if ((warp == 0 || warp == 2) || (NPROD > 1 && warp < NROLE && warp != 1 && g2k < 0)) {
     // ------------------------------------------------------------ producers (TMA engine)
     // Two independent rings: XB_j is consumed by GEMM1 right away, V_j only by GEMM2 after
     // the kernel map, so V stays resident ~4x longer; separate rings let each be as deep as
@@ -289,7 +299,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // ring can be fed by NPROD warps taking its tiles round-robin (NPROD = 3 measured 9%
     // slower at C3 than 1: the copies are not the binding stage).
     // warps 0 (, 4, 6) -> XB ring; 2 (, 5, 7) -> V ring
-    static_assert(NROLE == 2 + 2 * NPROD && NPROD <= 3, "role warp layout");
+    static_assert(NPROD == 1 || (NROLE == 2 + 2 * NPROD && NPROD <= 3 && NG2 == 1), "role warp layout");
     const bool is_xb = warp == 0 || warp == 4 || warp == 6;
     const int pk = warp == 0 || warp == 2 ? 0 : (warp == 4 || warp == 5 ? 1 : 2);
     const bool leader = ptx::elect_one();
@@ -324,14 +334,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         __syncwarp();
       }
     }
-  } else if (warp == 1 || warp == 3) {
+  } else if (warp == 1 || g2k >= 0) {
     // ------------------------------------------------------------ MMA issuers
     // tcgen05.mma issue blocks for about the instruction's execution time, so one thread
     // cannot keep two dependent streams fed.  Warp 1 issues GEMM1 (distance tiles) and warp 3
     // issues GEMM2 (K.V); each waits only on its own inputs and each tcgen05.commit tracks
     // its own thread's MMAs.  Whole warps run the schedule (uniform control flow,
     // descriptors in uniform registers); one elected lane issues.
-    if (warp == ((p.dbg & 32) ? 3 : 1)) {  // dbg 32: GEMM1 on warp 3, GEMM2 on warp 1
+    if (warp == 1) {
       const uint32_t idesc1 = p.g1f16 ? ptx::idesc_f16(BM, BJ) : ptx::idesc_tf32(BM, BJ);
       const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
       const uint64_t dXB0 = ptx::umma_desc(ptx::smem_u32(sXB), 128, sbo1);
@@ -372,25 +382,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sV), 128, (BJ / 8) * 128);
       const uint64_t v_step = (uint64_t)((2 * VT_BYTES) >> 4);
       const uint64_t vlo_step = (uint64_t)(VT_BYTES >> 4);
-      int st2 = 0, b2 = 0;
-      uint32_t ph2 = 0, phb2 = 0;
-      for (int t = 0; t < T; ++t) {
+      for (int t = g2k; t < T; t += NG2) {
+        const int st2 = t % NSV, b2 = t % NB;
+        const uint32_t ph2 = (t / NSV) & 1, phb2 = (t / NB) & 1;
         const int c = t / CH, ya = c & 1;
         const bool first = t == c * CH, last = t == T - 1 || t == c * CH + CH - 1;
         if (first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
-        if (p.role_sleep_ns > 0) {
-          ptx::mbar_wait_sleep(&v_full[st2], ph2, p.role_sleep_ns);
-          if (lane == 0) trace_ev(p, t, 9);
-          ptx::mbar_wait_sleep(&k_full[b2], phb2, p.role_sleep_ns);
-        } else {
-          ptx::mbar_wait(&v_full[st2], ph2);
-          if (lane == 0) trace_ev(p, t, 9);
-          ptx::mbar_wait(&k_full[b2], phb2);
-        }
-        if ((p.dbg & 16) && t > 0) {  // experiment: issue only into a drained tensor queue
-          const int bp = (t - 1) % NB;
-          ptx::mbar_wait(&b_free[bp], ((t - 1) / NB) & 1);
-        }
+        ptx::mbar_wait(&v_full[st2], ph2);
+        if (lane == 0) trace_ev(p, t, 9);
+        ptx::mbar_wait(&k_full[b2], phb2);
+        // accumulation order: tile t's MMAs enter the tensor pipe after tile t-1's (issued by
+        // the previous issuer, which arrives on g2_tok once its MMAs are dispatched)
+        if (NG2 > 1 && t > 0) ptx::mbar_wait(&g2_tok[t % NG2], (t / NG2 - (t % NG2 == 0 ? 1 : 0)) & 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 1);
@@ -414,10 +417,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
           if (last) ptx::mma_commit(&y_full[ya]);
+          if (NG2 > 1) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&g2_tok[(t + 1) % NG2]);
+          }
         }
         __syncwarp();
-        if (++st2 == NSV) { st2 = 0; ph2 ^= 1; }
-        if (++b2 == NB) { b2 = 0; phb2 ^= 1; }
       }
     }
   } else if (warp >= NROLE) {
@@ -613,13 +618,13 @@ __global__ void build_operands_kernel(const double* __restrict__ X, int dpad, in
       const E xh = to_op<E>(x);
       const E m2xh = to_op<E>(-2.0 * op_val(xh));
       XA[at(k)] = m2xh;
-      XB[at(k)] = xh;
+      if (XB) XB[at(k)] = xh;
       if (split) {
         const E xl = to_op<E>(x - op_val(xh));
         XA[at(dim + k)] = m2xh;
         XA[at(2 * dim + k)] = to_op<E>(-2.0 * op_val(xl));
-        XB[at(dim + k)] = xl;
-        XB[at(2 * dim + k)] = xh;
+        if (XB) XB[at(dim + k)] = xl;
+        if (XB) XB[at(2 * dim + k)] = xh;
       }
     }
     const E sqh = to_op<E>(sq);
@@ -631,21 +636,21 @@ __global__ void build_operands_kernel(const double* __restrict__ X, int dpad, in
       XA[at(b + 1)] = sql;
       XA[at(b + 2)] = one;
       XA[at(b + 3)] = one;
-      XB[at(b)] = one;
-      XB[at(b + 1)] = one;
-      XB[at(b + 2)] = sqh;
-      XB[at(b + 3)] = sql;
+      if (XB) XB[at(b)] = one;
+      if (XB) XB[at(b + 1)] = one;
+      if (XB) XB[at(b + 2)] = sqh;
+      if (XB) XB[at(b + 3)] = sql;
       b += 4;
     } else {
       XA[at(b)] = sqh;
       XA[at(b + 1)] = one;
-      XB[at(b)] = one;
-      XB[at(b + 1)] = sqh;
+      if (XB) XB[at(b)] = one;
+      if (XB) XB[at(b + 1)] = sqh;
       b += 2;
     }
     for (int k = b; k < K1; ++k) {
       XA[at(k)] = to_op<E>(0.0);
-      XB[at(k)] = to_op<E>(0.0);
+      if (XB) XB[at(k)] = to_op<E>(0.0);
     }
   }
 }
@@ -833,6 +838,38 @@ void tc_build_operands(Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* c
     tc::build_operands_kernel<float><<<tc::grid_for(op.n), 256, 0, st>>>(
         op.X64.p, op.dpad, op.dim, center, 1.0, op.n, K1, split, XA.p, XB.p);
   WGP_CUDA(cudaGetLastError());
+}
+
+// XA operand rows for arbitrary points (cross mode K(X*, X)): the operator's centring,
+// scale and element format.  Returns false when the points leave the fp16 range of an
+// fp16-operand operator (the caller then uses the fp64 CUDA-core path).
+bool tc_build_cross_rows(const Op& op, const double* Xs, int64_t m, int dpad, DBuf<float>& XAc,
+                         cudaStream_t st) {
+  const bool f16 = op.tc_f16;
+  const double inv_l = 1.0 / op.lengthscale;
+  if (f16) {
+    DBuf<double> ext(2);
+    tc::scaled_extent_kernel<<<1, 1024, 0, st>>>(Xs, dpad, op.dim, op.center.p, inv_l, m, ext.p);
+    WGP_CUDA(cudaGetLastError());
+    double h[2];
+    WGP_CUDA(cudaMemcpyAsync(h, ext.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    if (!(h[0] <= 64.0 && h[1] <= 8192.0)) return false;
+  }
+  const int K1 = tc_k1(op.dim, op.precision, f16);
+  const int64_t mpad = ((m + tc::BM - 1) / tc::BM) * tc::BM;
+  const size_t bytes = (size_t)mpad * K1 * (f16 ? 2 : 4);
+  XAc.ensure(bytes / 4);
+  WGP_CUDA(cudaMemsetAsync(XAc.p, 0, bytes, st));
+  const int split = op.precision == WGP_TF32 ? 0 : 1;
+  if (f16)
+    tc::build_operands_kernel<__half><<<tc::grid_for(m), 256, 0, st>>>(
+        Xs, dpad, op.dim, op.center.p, inv_l, m, K1, split, reinterpret_cast<__half*>(XAc.p), nullptr);
+  else
+    tc::build_operands_kernel<float><<<tc::grid_for(m), 256, 0, st>>>(
+        Xs, dpad, op.dim, op.center.p, 1.0, m, K1, split, XAc.p, nullptr);
+  WGP_CUDA(cudaGetLastError());
+  return true;
 }
 
 // Shared memory: XA rows + NSX XB stages + NSV V stages + 1 KB of barriers.  XB lives from

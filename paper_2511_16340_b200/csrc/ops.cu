@@ -102,6 +102,19 @@ static void ensure_tc_operands(Op& op, cudaStream_t st) {
   op.tc_dirty = false;
 }
 
+// Cross mode on the tensor cores: Y (m x s) = K(X*, X) W for device rows X* (row-major,
+// stride dpad).  Returns false if this operator / these points need the fp64 path.
+bool op_cross_tc(Op& op, const double* Xs, int64_t m, int dpad, const double* W, int s, double* Y,
+                 cudaStream_t st) {
+  if (!op.tensor() || !tc_supported(op.dim, op.precision)) return false;
+  ensure_tc_operands(op, st);
+  DBuf<float> XAc;
+  if (!tc_build_cross_rows(op, Xs, m, dpad, XAc, st)) return false;
+  launch_kmatvec_tc(op, XAc.p, op.XB.p, m, 0, op.n, W, s, nullptr, Y, false, op.vt, op.vchunk,
+                    op.ychunk, op.ysplit, st);
+  return true;
+}
+
 static void dispatch(Op& op, const double* B, const double* V, double* Y, int s, cudaStream_t st) {
   int64_t r0, r1;
   op.local_rows(&r0, &r1);

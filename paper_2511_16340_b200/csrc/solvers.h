@@ -50,6 +50,10 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
 void tc_build_operands(Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
                        cudaStream_t st);
 int tc_k1(int dim, int precision, bool f16);
+bool op_cross_tc(Op& op, const double* Xs, int64_t m, int dpad, const double* W, int s, double* Y,
+                 cudaStream_t st);
+bool tc_build_cross_rows(const Op& op, const double* Xs, int64_t m, int dpad, DBuf<float>& XAc,
+                         cudaStream_t st);
 // launch timing of the main TC kernel (wgp_kernel_timer_*): event pairs on the launch stream
 struct KernelTimer {
   bool on = false;

@@ -602,3 +602,17 @@ def kernel_timer_read() -> tuple[float, int]:
     n = C.c_int64(0)
     _check(lib().wgp_kernel_timer_read(C.byref(ms), C.byref(n)))
     return ms.value, n.value
+
+
+def eval_posterior(op: KernelOperator, priors: list, weights, Xs) -> np.ndarray:
+    """eval_posterior (sampling.cpp:66-75) for S pathwise samples at once: prior_s(X*) +
+    K(X*, X) weights[:, s], with the operator's rows as the training inputs -> m x S."""
+    weights = np.asarray(weights, dtype=np.float64)
+    if weights.ndim == 1:
+        weights = weights[:, None]
+    if weights.shape != (op.n, len(priors)):
+        raise ValueError("eval_posterior: weights length != training rows")
+    out = rff_eval(op, priors, Xs)
+    if op.n > 0:
+        out = out + op.cross_matvec(Xs, weights)
+    return out

@@ -143,3 +143,20 @@ def test_bo_loop_smoke(W):
     out = Cfg.bo_loop(dim=2, n_init=300, batch=8, rounds=3, n_samples=16, candidates=2000)
     assert [r["n"] for r in out["rounds"]] == [300, 308, 316]
     assert out["rounds"][1]["warm"] and all(np.isfinite(r["best_value"]) for r in out["rounds"])
+
+
+def test_eval_posterior_mirror_matches_oracle(W, O):
+    """warmgp.eval_posterior (the sampling.hpp:48 mirror, all samples at once) against the
+    oracle's per-sample eval_posterior, fp64 and tensor-core operators."""
+    seed = 6
+    X = O.uniform_inputs(O.derive_seed(seed, 1), 300, 3)
+    Xs = O.uniform_inputs(O.derive_seed(seed, 2), 777, 3)
+    wts = np.random.default_rng(seed).standard_normal((300, 4))
+    ohyp = O.KernelHyperparams(0.4, 1.2, 0.05, O.MATERN32)
+    whyp = W.KernelHyperparams(0.4, 1.2, 0.05, W.MATERN32)
+    priors = [W.sample_prior(whyp, 3, 256, W.derive_seed(seed, 100 + s)) for s in range(4)]
+    ref = np.column_stack([O.eval_posterior(ohyp, O.sample_prior(ohyp, 3, 256, W.derive_seed(seed, 100 + s)),
+                                            X, wts[:, s], Xs) for s in range(4)])
+    for prec, tol in ((W.F64, 1e-10), (W.F32_3XTF32, 1e-5)):
+        got = W.eval_posterior(W.KernelOperator(whyp, X, precision=prec), priors, wts, Xs)
+        assert np.abs(got - ref).max() <= tol * np.abs(ref).max()

@@ -69,6 +69,25 @@ def test_cross_matvec_vs_oracle(W, O):
         assert colrel(op.cross_matvec(Xs, Wt), ref) <= TOL[prec]
 
 
+def test_cross_matvec_tensor_core_path(W):
+    """Cross mode K(X*, X) W on the tensor cores (posterior evaluation at candidates, SURVEY
+    8f.1): wide RHS (two column chunks), ragged sizes, against the fp64 operator; points far
+    outside the fp16 operand range take the fp64 fallback and stay exact."""
+    rng = np.random.default_rng(7)
+    X = rng.random((3001, 5))
+    Xs = rng.random((4999, 5))
+    Wt = rng.standard_normal((3001, 70))
+    for kind, ls in ((0, 0.3), (1, 0.5)):
+        h = W.KernelHyperparams(ls, 1.3, 0.1, kind)
+        ref = W.KernelOperator(h, X, precision=W.F64).cross_matvec(Xs, Wt)
+        got = W.KernelOperator(h, X, precision=W.F32_3XTF32).cross_matvec(Xs, Wt)
+        assert colrel(got, ref) <= 1e-5
+        far = Xs[:50] + 1e3  # |x - c| / l >> 64: no fp16 operands for these rows
+        ref_far = W.KernelOperator(h, X, precision=W.F64).cross_matvec(far, Wt)
+        got_far = W.KernelOperator(h, X, precision=W.F32_3XTF32).cross_matvec(far, Wt)
+        assert np.array_equal(got_far, ref_far)
+
+
 def test_kmatvec_linearity_large(W):
     """Size-independent property at a BASELINE-scale N: H(aU + bV) = aHU + bHV."""
     rng = np.random.default_rng(5)
@@ -105,3 +124,21 @@ def test_tc_accuracy_scales_with_n(W, n):
     err = colrel(Ytc, Y64)
     print(f"n={n} tc rel err {err:.3e}")
     assert err <= 1e-4
+
+
+def test_kernel_timer_counts_tc_launches(W):
+    """wgp_kernel_timer_*: CUDA-event timing of the tensor-core kernel launches only (bench.py's
+    roofline numerator); one launch per 64-column RHS chunk."""
+    rng = np.random.default_rng(3)
+    X = rng.random((5000, 6))
+    op = W.KernelOperator(W.KernelHyperparams(0.4, 1.0, 0.1, 0), X, precision=W.F32_3XTF32)
+    V = rng.standard_normal((5000, 100))
+    W.kernel_timer_enable(True)
+    op.kmatvec(V)
+    op.kmatvec(V[:, :10])
+    ms, n = W.kernel_timer_read()
+    W.kernel_timer_enable(False)
+    assert n == 3 and ms > 0.0
+    W.kernel_timer_enable(False)
+    op.kmatvec(V[:, :10])
+    assert W.kernel_timer_read() == (0.0, 0)
