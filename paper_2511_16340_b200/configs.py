@@ -55,6 +55,7 @@ class GrowthState:
     n_solved: int = 0
     round: int = 0
     history: list = field(default_factory=list)
+    op_fast: W.KernelOperator | None = None  # tensor-core twin of op for candidate evaluation
 
     @property
     def n_obs(self) -> int:
@@ -102,6 +103,8 @@ class GrowthState:
         pv = W.rff_eval(self.op, self.priors, Xn) if S else np.zeros((m, 0))
         nd = self.noise_rng.normal_fill(m * S, self.hyp.noise_scale).reshape(m, S)  # i-major
         self.op.append_rows(Xn)
+        if self.op_fast is not None:
+            self.op_fast.append_rows(Xn)
         self.y = np.concatenate([self.y, yn])
         self.prior_values = np.vstack([self.prior_values, pv])
         self.noise_draws = np.vstack([self.noise_draws, nd])
@@ -149,14 +152,18 @@ class BumpObjective:
 
 def posterior_at(state: GrowthState, Xc: np.ndarray) -> np.ndarray:
     """eval_posterior (sampling.cpp:66-75) for every sample at once on the device:
-    prior_s(X*) + K(X*, X)(w_mean - w_s)  ->  m x S."""
-    pri = W.rff_eval(state.op, state.priors, Xc)
+    prior_s(X*) + K(X*, X)(w_mean - w_s)  ->  m x S.  With a tensor-core twin operator the
+    candidates go through the tcgen05 cross mode and the fp32 RFF kernel (acquisition only
+    ranks the values; the solves stay on the fp64 operator)."""
     Wd = state.weights[:, :1] - state.weights[:, 1:]
-    return pri + state.op.cross_matvec(Xc, Wd)
+    if state.op_fast is not None:
+        return W.rff_eval(state.op_fast, state.priors, Xc, fast=True) + state.op_fast.cross_matvec(Xc, Wd)
+    return W.rff_eval(state.op, state.priors, Xc) + state.op.cross_matvec(Xc, Wd)
 
 
 def bo_loop(dim=4, n_init=5000, batch=64, rounds=50, n_samples=128, candidates=100_000,
-            warm=True, seed=0, cfg: W.SolverConfig | None = None, precision=W.F64, ctx=None) -> dict:
+            warm=True, seed=0, cfg: W.SolverConfig | None = None, precision=W.F64, ctx=None,
+            fast_candidates: bool = True) -> dict:
     """Configuration 5: BoConfig defaults (Matern-3/2 l=0.3, s_f=1, sigma_n=1e-3, F=2000;
     thompson.hpp:29-58), CG with the small budget (5 iterations, tol 1e-2)."""
     hyp = W.KernelHyperparams(0.3, 1.0, 1e-3, W.MATERN32)
@@ -166,6 +173,8 @@ def bo_loop(dim=4, n_init=5000, batch=64, rounds=50, n_samples=128, candidates=1
     X0 = uniform_rows_fast(W.derive_seed(seed, 2), n_init, dim)
     y0 = obj.observe(X0)
     st = growth_state(X0, y0, hyp, n_samples, 2000, seed, precision, ctx)
+    if fast_candidates:
+        st.op_fast = W.KernelOperator(hyp, X0, precision=W.F32_3XTF32, ctx=ctx)
     recs = []
     for r in range(rounds):
         rec = st.solve_round(cfg, warm)

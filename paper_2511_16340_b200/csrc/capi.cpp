@@ -24,6 +24,9 @@ void throw_error(wgp_status code, const char* fmt, ...) {
 }
 
 void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major);
+void launch_rff_eval32(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
+                       const double* ph, const double* amp, int F, int S, double coeff,
+                       double* out, int64_t ldo, cudaStream_t st);
 void launch_rff_eval64(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
                        const double* ph, const double* amp, int F, int S, double coeff,
                        double* out, int64_t ldo, cudaStream_t st);
@@ -458,9 +461,10 @@ wgp_status wgp_precond_info(wgp_op* op, int64_t rank, double shift, int mode, in
   });
 }
 
-wgp_status wgp_rff_eval(wgp_op* op, const double* Omega, const double* phases, const double* amps,
-                        int F, int S, double signal_scale, const double* Xs, int64_t m, int64_t ldx,
-                        double* out, int64_t ldo) {
+static wgp_status rff_eval_impl(wgp_op* op, const double* Omega, const double* phases,
+                                const double* amps, int F, int S, double signal_scale,
+                                const double* Xs, int64_t m, int64_t ldx, double* out, int64_t ldo,
+                                bool fast) {
   return guard([&] {
     WGP_REQUIRE(op && Omega && phases && amps && out, "wgp_rff_eval: null argument");
     WGP_REQUIRE(F >= 1 && S >= 0, "sample_prior: dim and num_features must be positive");
@@ -489,11 +493,26 @@ wgp_status wgp_rff_eval(wgp_op* op, const double* Omega, const double* phases, c
     WGP_CUDA(cudaMemcpyAsync(dPh.p, phases, sizeof(double) * nf, cudaMemcpyHostToDevice, st));
     WGP_CUDA(cudaMemcpyAsync(dAm.p, amps, sizeof(double) * nf, cudaMemcpyHostToDevice, st));
     const double coeff = signal_scale * std::sqrt(2.0 / (double)F);  // sampling.cpp:40-41
-    launch_rff_eval64(Xd, op->dpad, dim, m, dOm.p, dPh.p, dAm.p, F, S, coeff, dOut.p, m, st);
+    if (fast)
+      launch_rff_eval32(Xd, op->dpad, dim, m, dOm.p, dPh.p, dAm.p, F, S, coeff, dOut.p, m, st);
+    else
+      launch_rff_eval64(Xd, op->dpad, dim, m, dOm.p, dPh.p, dAm.p, F, S, coeff, dOut.p, m, st);
     WGP_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * ldo, dOut.p, sizeof(double) * m,
                                sizeof(double) * m, S, cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
   });
+}
+
+wgp_status wgp_rff_eval(wgp_op* op, const double* Omega, const double* phases, const double* amps,
+                        int F, int S, double signal_scale, const double* Xs, int64_t m, int64_t ldx,
+                        double* out, int64_t ldo) {
+  return rff_eval_impl(op, Omega, phases, amps, F, S, signal_scale, Xs, m, ldx, out, ldo, false);
+}
+
+wgp_status wgp_rff_eval_fast(wgp_op* op, const double* Omega, const double* phases,
+                             const double* amps, int F, int S, double signal_scale, const double* Xs,
+                             int64_t m, int64_t ldx, double* out, int64_t ldo) {
+  return rff_eval_impl(op, Omega, phases, amps, F, S, signal_scale, Xs, m, ldx, out, ldo, true);
 }
 
 }  // extern "C"

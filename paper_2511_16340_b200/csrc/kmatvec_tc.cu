@@ -54,7 +54,7 @@ constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
 constexpr int NSET = 3;         // epilogue sets (8 warps each) taking tiles round-robin
 constexpr int NPROD = 1;        // producer warps per ring (XB ring, V ring); 3 measured slower
 #ifndef WGP_TC_NG2
-#define WGP_TC_NG2 3
+#define WGP_TC_NG2 1
 #endif
 // GEMM2 issuer warps taking tiles round-robin (on SMSPs 3, 0, 2): the warp issuing a tile's 12
 // MMAs costs its SM sub-partition issue slots, and K(t) needs all four TMEM quadrants
@@ -103,6 +103,7 @@ struct Params {
   int gram;
   int sleep_ns;  // epilogue wait backoff (WGP_TC_SLEEP)
   int role_sleep_ns;  // MMA-issuer wait backoff (WGP_TC_RSLEEP)
+  int prod_sleep_ns;  // producer wait backoff (WGP_TC_PSLEEP)
   int dbg;  // timing experiments only (WGP_TC_DEBUG): 1 GEMM2 hi.hi only, 2 GEMM1 one K-step, 4 no map
   unsigned long long* trace;  // debug: per-tile event clocks of CTA 0 (nullptr normally)
   unsigned long long* cta_trace;  // debug: per-CTA [start, loop end, end] globaltimer + smid
@@ -220,6 +221,15 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
   }
 }
 
+// Role-warp waits: spinning warps take issue slots from the epilogue warps sharing their SM
+// sub-partition (and K(t) needs every quadrant), so waits with slack can back off.
+__device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity, int sleep_ns) {
+  if (sleep_ns > 0)
+    ptx::mbar_wait_sleep(bar, parity, (uint32_t)sleep_ns);
+  else
+    ptx::mbar_wait(bar, parity);
+}
+
 template <int SWQ>
 __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NSX, int NSV) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -311,7 +321,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     if (is_xb) {
       for (int t = pk; t < T; t += NPROD) {
         const int st = t % NSX;
-        if (t >= NSX) ptx::mbar_wait(&xb_empty[st], ((t / NSX) & 1) ^ 1);
+        if (t >= NSX) wait_role(&xb_empty[st], ((t / NSX) & 1) ^ 1, p.prod_sleep_ns);
         if (leader) {
           trace_ev(p, t, 6);
           ptx::mbar_arrive_expect_tx(&xb_full[st], XB_BYTES);
@@ -324,7 +334,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     } else {
       for (int t = pk; t < T; t += NPROD) {
         const int st = t % NSV;
-        if (t >= NSV) ptx::mbar_wait(&v_empty[st], ((t / NSV) & 1) ^ 1);
+        if (t >= NSV) wait_role(&v_empty[st], ((t / NSV) & 1) ^ 1, p.prod_sleep_ns);
         if (leader) {
           trace_ev(p, t, 8);
           ptx::mbar_arrive_expect_tx(&v_full[st], 2 * VT_BYTES);
@@ -388,12 +398,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         const int c = t / CH, ya = c & 1;
         const bool first = t == c * CH, last = t == T - 1 || t == c * CH + CH - 1;
         if (first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
-        ptx::mbar_wait(&v_full[st2], ph2);
+        wait_role(&v_full[st2], ph2, p.role_sleep_ns);
         if (lane == 0) trace_ev(p, t, 9);
-        ptx::mbar_wait(&k_full[b2], phb2);
+        wait_role(&k_full[b2], phb2, p.role_sleep_ns);
         // accumulation order: tile t's MMAs enter the tensor pipe after tile t-1's (issued by
         // the previous issuer, which arrives on g2_tok once its MMAs are dispatched)
-        if (NG2 > 1 && t > 0) ptx::mbar_wait(&g2_tok[t % NG2], (t / NG2 - (t % NG2 == 0 ? 1 : 0)) & 1);
+        if (NG2 > 1 && t > 0)
+          wait_role(&g2_tok[t % NG2], (t / NG2 - (t % NG2 == 0 ? 1 : 0)) & 1, p.role_sleep_ns);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 1);
@@ -978,6 +989,8 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     prm.sleep_ns = sleep_ns;
     static const int rsleep_ns = getenv("WGP_TC_RSLEEP") ? atoi(getenv("WGP_TC_RSLEEP")) : 0;
     prm.role_sleep_ns = rsleep_ns;
+    static const int psleep_ns = getenv("WGP_TC_PSLEEP") ? atoi(getenv("WGP_TC_PSLEEP")) : 0;
+    prm.prod_sleep_ns = psleep_ns;
     prm.trace = nullptr;
     static const char* trace_path = getenv("WGP_TC_TRACE");
     prm.cta_trace = nullptr;

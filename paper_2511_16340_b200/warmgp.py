@@ -46,7 +46,7 @@ EXPORTS = (
     "wgp_cross_matvec", "wgp_solve_many", "wgp_solve", "wgp_pivoted_cholesky", "wgp_precond_info",
     "wgp_rff_eval", "wgp_derive_seed", "wgp_rng_next_u64", "wgp_rng_uniform", "wgp_rng_normal",
     "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
-    "wgp_rng_normal_fill", "wgp_kernel_timer_enable", "wgp_kernel_timer_read",
+    "wgp_rng_normal_fill", "wgp_kernel_timer_enable", "wgp_kernel_timer_read", "wgp_rff_eval_fast",
 )
 
 
@@ -127,6 +127,7 @@ def _declare(L):
         "wgp_pivoted_cholesky": (C.c_int, [P, I64, P, I64, P]),
         "wgp_precond_info": (C.c_int, [P, I64, D, C.c_int, P, P]),
         "wgp_rff_eval": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, I64, P, I64]),
+        "wgp_rff_eval_fast": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, I64, P, I64]),
         "wgp_derive_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
         "wgp_rng_next_u64": (C.c_uint64, [P]),
         "wgp_rng_uniform": (D, [P]),
@@ -556,7 +557,7 @@ def sample_prior(hyp: KernelHyperparams, dim: int, num_features: int, seed: int)
     return RffPrior(Om, ph, am, hyp.signal_scale)
 
 
-def rff_eval(op: KernelOperator, priors: list, Xs=None) -> np.ndarray:
+def rff_eval(op: KernelOperator, priors: list, Xs=None, fast: bool = False) -> np.ndarray:
     """eval_prior (sampling.cpp:37-46) for several priors sharing F and signal scale, fused on
     the device; evaluated at the operator's rows (Xs=None) or at host points Xs (m x d)."""
     if not priors:
@@ -578,8 +579,8 @@ def rff_eval(op: KernelOperator, priors: list, Xs=None) -> np.ndarray:
     else:
         m = op.n
     out = np.zeros((m, S), order="F")
-    _check(lib().wgp_rff_eval(op._h, _ptr(Om), _ptr(ph), _ptr(am), F, S, sf, _ptr(Xs), m, max(m, 1),
-                              _ptr(out), max(m, 1)))
+    fn = lib().wgp_rff_eval_fast if fast else lib().wgp_rff_eval
+    _check(fn(op._h, _ptr(Om), _ptr(ph), _ptr(am), F, S, sf, _ptr(Xs), m, max(m, 1), _ptr(out), max(m, 1)))
     return out
 
 
@@ -604,7 +605,7 @@ def kernel_timer_read() -> tuple[float, int]:
     return ms.value, n.value
 
 
-def eval_posterior(op: KernelOperator, priors: list, weights, Xs) -> np.ndarray:
+def eval_posterior(op: KernelOperator, priors: list, weights, Xs, fast: bool = False) -> np.ndarray:
     """eval_posterior (sampling.cpp:66-75) for S pathwise samples at once: prior_s(X*) +
     K(X*, X) weights[:, s], with the operator's rows as the training inputs -> m x S."""
     weights = np.asarray(weights, dtype=np.float64)
@@ -612,7 +613,7 @@ def eval_posterior(op: KernelOperator, priors: list, weights, Xs) -> np.ndarray:
         weights = weights[:, None]
     if weights.shape != (op.n, len(priors)):
         raise ValueError("eval_posterior: weights length != training rows")
-    out = rff_eval(op, priors, Xs)
+    out = rff_eval(op, priors, Xs, fast=fast)
     if op.n > 0:
         out = out + op.cross_matvec(Xs, weights)
     return out

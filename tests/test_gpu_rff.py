@@ -43,3 +43,37 @@ def test_build_sample_rhs_vs_oracle(W, O):
     a = W.build_sample_rhs(op, pw, 0.05, 1)
     b = O.build_sample_rhs(po, X, 0.05, 1)
     np.testing.assert_allclose(a, b, rtol=0, atol=1e-12)
+
+
+def test_rff_eval_fast_close_to_fp64(W):
+    """wgp_rff_eval_fast (fp32 phases, reduced MUFU cos) tracks the fp64 kernel to ~1e-6 of the
+    prior's scale at BO-like sizes (F = 2000, phases up to |w.x| ~ 30)."""
+    import numpy as np
+    rng = np.random.default_rng(2)
+    for kind, ls, d in ((0, 0.3, 4), (1, 0.5, 6)):
+        hyp = W.KernelHyperparams(ls, 1.0, 1e-3, kind)
+        X = rng.random((500, d))
+        op = W.KernelOperator(hyp, X, precision=W.F32_3XTF32)
+        priors = [W.sample_prior(hyp, d, 2000, W.derive_seed(9, s)) for s in range(5)]
+        Xc = rng.random((20000, d))
+        ref = W.rff_eval(op, priors, Xc)
+        got = W.rff_eval(op, priors, Xc, fast=True)
+        assert np.abs(got - ref).max() <= 2e-5 * np.abs(ref).max()
+
+
+def test_bo_candidates_fast_path(W):
+    """The BO loop's candidate evaluation on the tensor-core twin + fp32 RFF agrees with the
+    fp64 evaluation (same solved weights) and picks the same argmax for nearly every sample."""
+    import numpy as np
+    from paper_2511_16340_b200 import configs as Cfg
+    X0 = Cfg.uniform_rows_fast(3, 1500, 3)
+    y0 = np.sin(5 * X0[:, 0]) + X0[:, 1]
+    hyp = W.KernelHyperparams(0.3, 1.0, 1e-3, W.MATERN32)
+    st = Cfg.growth_state(X0, y0, hyp, 16, 2000, 3, W.F64)
+    st.solve_round(W.SolverConfig(tolerance=1e-2, max_iters=5, precond_rank=100, precond_shift=1e-6), warm=True)
+    Xc = Cfg.uniform_rows_fast(4, 30000, 3)
+    ref = Cfg.posterior_at(st, Xc)
+    st.op_fast = W.KernelOperator(hyp, X0, precision=W.F32_3XTF32)
+    got = Cfg.posterior_at(st, Xc)
+    assert np.abs(got - ref).max() <= 1e-4 * np.abs(ref).max()
+    assert np.mean(np.argmax(got, 0) == np.argmax(ref, 0)) >= 0.9
