@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
                                                     int nb, const double* __restrict__ V,
                                                     const double* __restrict__ Bm, int s,
                                                     const int* __restrict__ active, KParams p,
+                                                    int64_t r0, int64_t r1,
                                                     double* __restrict__ g) {
   const int c = blockIdx.y;
   if (!active[c]) return;
@@ -44,8 +45,11 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
   const int tid = threadIdx.x;
   const int lr = tid >> 2, sub = tid & 3;
   const int bi = blockIdx.x * 64 + lr;
-  const bool valid = bi < nb;
-  const int64_t row = valid ? rows[(int64_t)c * nb + bi] : 0;
+  const int64_t row0 = bi < nb ? rows[(int64_t)c * nb + bi] : 0;
+  // sharded: this rank owns rows [r0, r1) (B holds those rows only); other batch rows get 0
+  const bool own = bi < nb && row0 >= r0 && row0 < r1;
+  const bool valid = own;
+  const int64_t row = row0;
   T xr[32];
 #pragma unroll
   for (int k = 0; k < 32; ++k) xr[k] = (valid && k < dim) ? X[row * dpad + k] : T(0);
@@ -82,9 +86,9 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
   }
   red[tid] = acc;
   __syncthreads();
-  if (valid && sub == 0) {
+  if (bi < nb && sub == 0) {
     const double tot = ((red[tid] + red[tid + 1]) + red[tid + 2]) + red[tid + 3];
-    g[(int64_t)c * nb + bi] = tot - Bm[row * s + c];
+    g[(int64_t)c * nb + bi] = own ? tot - Bm[(row - r0) * s + c] : 0.0;
   }
 }
 
@@ -272,12 +276,13 @@ __global__ void sgd_momentum_kernel(double* __restrict__ vel, int64_t n, int s,
 }
 __global__ void sgd_scatter_kernel(double* __restrict__ vel, const int* __restrict__ rows,
                                    const double* __restrict__ g, int nb, int s,
-                                   const int* __restrict__ active, double scale) {
+                                   const int* __restrict__ active, double scale, int64_t r0,
+                                   int64_t r1) {
   const int c = blockIdx.y;
   if (!active[c]) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
     const int64_t row = rows[(int64_t)c * nb + i];
-    vel[row * s + c] += scale * g[(int64_t)c * nb + i];
+    if (row >= r0 && row < r1) vel[(row - r0) * s + c] += scale * g[(int64_t)c * nb + i];
   }
 }
 __global__ void sgd_step_kernel(double* __restrict__ V, const double* __restrict__ vel, int64_t n,
@@ -304,14 +309,14 @@ inline int grid_for(int64_t total) {
 }  // namespace
 
 void launch_krows(const Op& op, const int* rows, int nb, const double* V, const double* B, int s,
-                  const int* active, double* g, cudaStream_t st) {
+                  const int* active, double* g, int64_t r0, int64_t r1, cudaStream_t st) {
   dim3 grid(ceil_div(nb, 64), s);
   if (op.f64())
     krows_kernel<double><<<grid, 256, 0, st>>>(op.X64.p, op.dpad, op.dim, op.n, rows, nb, V, B, s,
-                                               active, op.kp(), g);
+                                               active, op.kp(), r0, r1, g);
   else
     krows_kernel<float><<<grid, 256, 0, st>>>(op.X32.p, op.dpad, op.dim, op.n, rows, nb, V, B, s,
-                                              active, op.kp(), g);
+                                              active, op.kp(), r0, r1, g);
   WGP_CUDA(cudaGetLastError());
 }
 
@@ -361,9 +366,11 @@ void launch_set_cyclic(int* blk, int s, int value, cudaStream_t st) {
 
 void launch_sgd_update(double* V, double* vel, const int* rows, const double* g, int nb, int64_t n,
                        int s, const int* active, double momentum, double scale, double lr,
-                       cudaStream_t st) {
+                       int64_t r0, cudaStream_t st) {
+  // V, vel: this rank's rows [r0, r0 + n)
   sgd_momentum_kernel<<<grid_for(n * s), 256, 0, st>>>(vel, n, s, active, momentum);
-  sgd_scatter_kernel<<<dim3(ceil_div(nb, 256), s), 256, 0, st>>>(vel, rows, g, nb, s, active, scale);
+  sgd_scatter_kernel<<<dim3(ceil_div(nb, 256), s), 256, 0, st>>>(vel, rows, g, nb, s, active, scale,
+                                                                 r0, r0 + n);
   sgd_step_kernel<<<grid_for(n * s), 256, 0, st>>>(V, vel, n, s, active, lr);
   WGP_CUDA(cudaGetLastError());
 }

@@ -231,17 +231,27 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
 // ---------------------------------------------------------------------------------------
 // shared per-iteration helpers (host side)
 
+// Column sums of a*a over this rank's rows as global chunk partials, all-gathered (every
+// rank then holds every chunk; summed in chunk order below, so sharded == unsharded).
+static void sq_chunks(const Ctx& ctx, SolverWork<double>& w, const double* A, cudaStream_t st) {
+  if (w.n > 0)
+    launch_coldots<double>(A, A, nullptr, nullptr, w.n, w.s, w.part.p + (int64_t)w.c0 * w.s, st);
+  dist_allgather_chunks(ctx, w.part.p, w.N, w.s, st);
+}
+
 // |b| per column; zero right-hand sides are inactive from the start.
-static void bnorms(SolverWork<double>& w, double* bnorm, int* active, cudaStream_t st) {
-  launch_coldots<double>(w.B.p, w.B.p, nullptr, nullptr, w.n, w.s, w.part.p, st);
+static void bnorms(const Ctx& ctx, SolverWork<double>& w, double* bnorm, int* active,
+                   cudaStream_t st) {
+  sq_chunks(ctx, w, w.B.p, st);
   init_bnorm_kernel<<<sgrid(w.s), 256, 0, st>>>(w.part.p, w.nch, w.s, bnorm, active);
   WGP_CUDA(cudaGetLastError());
 }
 
 // rel = |R| / |b| per column (device), copied to the host.  Does not touch the flags.
-static void residual_norms(SolverWork<double>& w, const double* R, const double* bnorm,
-                           double* rel_dev, std::vector<double>& hrel, cudaStream_t st) {
-  launch_coldots<double>(R, R, nullptr, nullptr, w.n, w.s, w.part.p, st);
+static void residual_norms(const Ctx& ctx, SolverWork<double>& w, const double* R,
+                           const double* bnorm, double* rel_dev, std::vector<double>& hrel,
+                           cudaStream_t st) {
+  sq_chunks(ctx, w, R, st);
   resid_step_kernel<<<sgrid(w.s), 256, 0, st>>>(w.part.p, w.nch, 1, w.s, bnorm, -1.0, rel_dev,
                                                 w.act.p + w.s + 1);  // scratch flags
   WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel_dev, sizeof(double) * w.s, cudaMemcpyDeviceToHost, st));
@@ -256,18 +266,18 @@ void sgd_solve_batched(Op& op, const wgp_solver_config& cfg, const std::vector<u
                        SolverWork<double>& w, SolveOutputs& out, cudaStream_t st) {
   const int64_t n = w.n;
   const int s = w.s;
-  const int64_t batch = std::min<int64_t>(cfg.batch_size, n);
+  const int64_t batch = std::min<int64_t>(cfg.batch_size, w.N);
   WGP_REQUIRE(batch > 0, "sgd_solve: batch size must be positive");
   WGP_REQUIRE(batch <= INT32_MAX, "sgd_solve: batch too large");
   double* bnorm = w.scal.p + 3 * s;
   double* rel = w.scal.p + 4 * s;
   int* active = w.act.p;
-  bnorms(w, bnorm, active, st);
+  bnorms(*op.ctx, w, bnorm, active, st);
   launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
   std::vector<double> hrel(s);
   std::vector<int> hact(s);
   WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
-  residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+  residual_norms(*op.ctx, w, w.R.p, bnorm, rel, hrel, st);
   int n_active = 0;
   for (int c = 0; c < s; ++c) {
     out.history[c].assign(1, hact[c] ? hrel[c] : 0.0);
@@ -277,13 +287,14 @@ void sgd_solve_batched(Op& op, const wgp_solver_config& cfg, const std::vector<u
     n_active += hact[c];
   }
   if (n_active == 0) return;
-  const double scale = cfg.sgd_scaling == WGP_SGD_UNBIASED ? (double)n / (double)batch : 1.0;
+  const int64_t N = w.N;  // global rows (n = this rank's rows [w.r0, w.r0 + n))
+  const double scale = cfg.sgd_scaling == WGP_SGD_UNBIASED ? (double)N / (double)batch : 1.0;
   std::vector<Rng> rngs;
   for (int c = 0; c < s; ++c) rngs.push_back(Rng{seeds[c]});
   std::vector<std::vector<int64_t>> idx(s);
-  for (int c = 0; c < s; ++c) {
-    idx[c].resize(n);
-    for (int64_t i = 0; i < n; ++i) idx[c][i] = i;
+  for (int c = 0; c < s; ++c) {  // every rank draws the same batches (same streams)
+    idx[c].resize(N);
+    for (int64_t i = 0; i < N; ++i) idx[c][i] = i;
   }
   std::vector<int> hrows((size_t)s * batch, 0);
   DBuf<int> drows((size_t)s * batch);
@@ -295,17 +306,20 @@ void sgd_solve_batched(Op& op, const wgp_solver_config& cfg, const std::vector<u
       if (!hact[c]) continue;
       std::vector<int64_t>& ix = idx[c];
       for (int64_t i = 0; i < batch; ++i) {  // partial Fisher-Yates (:219-222)
-        const int64_t j = i + (int64_t)rngs[c].uniform_index((uint64_t)(n - i));
+        const int64_t j = i + (int64_t)rngs[c].uniform_index((uint64_t)(N - i));
         std::swap(ix[i], ix[j]);
         hrows[(size_t)c * batch + i] = (int)ix[i];
       }
     }
     WGP_CUDA(cudaMemcpyAsync(drows.p, hrows.data(), sizeof(int) * hrows.size(), cudaMemcpyHostToDevice, st));
-    launch_krows(op, drows.p, (int)batch, w.V.p, w.B.p, s, active, g.p, st);  // H[row].v - b[row]
-    launch_sgd_update(w.V.p, vel.p, drows.p, g.p, (int)batch, n, s, active, cfg.momentum, scale,
-                      cfg.learning_rate, st);
+    // H[row].v - b[row] for the batch rows this rank owns (V full, B local)
+    launch_krows(op, drows.p, (int)batch, w.V.p, w.B.p, s, active, g.p, w.r0, w.r0 + n, st);
+    if (n > 0)
+      launch_sgd_update(w.Vl(), vel.p, drows.p, g.p, (int)batch, n, s, active, cfg.momentum, scale,
+                        cfg.learning_rate, w.r0, st);
+    dist_allgather_rows(*op.ctx, w.V.p, N, s, sizeof(double), st);  // full v for the matvecs
     launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // full true residual (:231)
-    residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+    residual_norms(*op.ctx, w, w.R.p, bnorm, rel, hrel, st);
     bool changed = false;
     for (int c = 0; c < s; ++c) {
       if (!hact[c]) continue;
@@ -356,12 +370,12 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   double* bnorm = w.scal.p + 3 * s;
   double* rel = w.scal.p + 4 * s;
   int* active = w.act.p;
-  bnorms(w, bnorm, active, st);
+  bnorms(*op.ctx, w, bnorm, active, st);
   launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
   std::vector<double> hrel(s);
   std::vector<int> hact(s), confirm(s);
   WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
-  residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+  residual_norms(*op.ctx, w, w.R.p, bnorm, rel, hrel, st);
   int n_active = 0;
   for (int c = 0; c < s; ++c) {
     out.history[c].assign(1, hact[c] ? hrel[c] : 0.0);
@@ -382,7 +396,7 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
     launch_ap_block_solve(inv.p, bs, n, blk.p, active, w.R.p, s, w.V.p, delta.p, st);
     launch_kcols(op, blk.p, bs, delta.p, s, active, w.R.p, st);  // r -= H[:, B] delta
     if (k % nblk == 0) launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // drift refresh
-    residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+    residual_norms(*op.ctx, w, w.R.p, bnorm, rel, hrel, st);
     int nconf = 0;
     for (int c = 0; c < s; ++c) {
       confirm[c] = hact[c] && hrel[c] <= cfg.tolerance;
@@ -392,7 +406,7 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
       launch_residual(op, w.B.p, w.V.p, w.Z.p, s, st);
       WGP_CUDA(cudaMemcpyAsync(dconf.p, confirm.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
       launch_copy_masked_cols(w.R.p, w.Z.p, n, s, dconf.p, st);
-      residual_norms(w, w.R.p, bnorm, rel, hrel, st);
+      residual_norms(*op.ctx, w, w.R.p, bnorm, rel, hrel, st);
     }
     bool changed = false;
     for (int c = 0; c < s; ++c) {

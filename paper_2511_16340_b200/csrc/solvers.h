@@ -84,8 +84,10 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
                       SolveOutputs& out, cudaStream_t st);
 
 // sgd_ap.cu
+// g[c][i] = H[row_i] v_c - b[row_i] for batch rows this rank owns ([r0, r1); B holds those
+// rows), 0 for the others
 void launch_krows(const Op& op, const int* rows, int nb, const double* V, const double* B, int s,
-                  const int* active, double* g, cudaStream_t st);
+                  const int* active, double* g, int64_t r0, int64_t r1, cudaStream_t st);
 void launch_kcols(const Op& op, const int* blk, int bs, const double* delta, int s,
                   const int* active, double* R, cudaStream_t st);
 void launch_block_chol(const Op& op, int bs, int nblk, double* fac, double* inv, int* fail,
@@ -97,7 +99,7 @@ void launch_greedy_block(const double* R, int64_t n, int bs, int nblk, int s, co
 void launch_set_cyclic(int* blk, int s, int value, cudaStream_t st);
 void launch_sgd_update(double* V, double* vel, const int* rows, const double* g, int nb, int64_t n,
                        int s, const int* active, double momentum, double scale, double lr,
-                       cudaStream_t st);
+                       int64_t r0, cudaStream_t st);
 void launch_copy_masked_cols(double* dst, const double* src, int64_t n, int s, const int* mask,
                              cudaStream_t st);
 

@@ -89,6 +89,37 @@ def sharded_cg(H, b, rank, world, tol=1e-8, max_iters=200):
     return v, hist
 
 
+def sharded_sgd(H, b, rank, world, seed=11, batch=64, lr=0.002, momentum=0.9, iters=60):
+    """Row-sharded SGD (solvers.cu sgd_solve_batched over a sharded context): every rank
+    draws the same minibatches from the same stream (here numpy, standing in for the
+    reference Rng), computes H[row].v - b[row] for the batch rows it owns, updates its own
+    velocity/solution rows, all-gathers v, and takes residual norms from chunk partials."""
+    n = b.size
+    r0, r1 = shard_range(n, world, rank)
+    Hl, bl = H[r0:r1], b[r0:r1]
+    rng = np.random.default_rng(seed)
+    idx = np.arange(n)
+    v = np.zeros(n)
+    vel_l = np.zeros(r1 - r0)
+    bnorm = np.sqrt(gather_sum(chunk_dots(bl, bl, r0), world))
+    scale = n / batch
+    hist = []
+    for _ in range(iters):
+        for i in range(batch):  # persistent partial Fisher-Yates
+            j = i + int(rng.integers(0, n - i))
+            idx[i], idx[j] = idx[j], idx[i]
+        rows = idx[:batch].copy()
+        vel_l *= momentum
+        for row in rows:
+            if r0 <= row < r1:
+                vel_l[row - r0] += scale * (np.dot(H[row], v) - b[row])
+        vl = v[r0:r1] - lr * vel_l
+        v = gather_rows(vl, n, world)
+        r = bl - rowdot(Hl, v)
+        hist.append(np.sqrt(gather_sum(chunk_dots(r, r, r0), world)) / bnorm)
+    return v, hist
+
+
 def system(n=1300):
     rng = np.random.default_rng(0)
     X = rng.random((n, 3))
@@ -103,8 +134,9 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     H, b = system()
     v, hist = sharded_cg(H, b, rank, world)
+    vs, hs = sharded_sgd(H, b, rank, world)
     if rank == 0:
-        q.put((v, hist))
+        q.put((v, hist, vs, hs))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -118,21 +150,24 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world", [2])
-def test_sharded_cg_bitwise_equals_single_process(world):
+def test_sharded_cg_and_sgd_bitwise_equal_single_process(world):
     H, b = system()
     v1, h1 = sharded_cg(H, b, 0, 1)
+    vs1, hs1 = sharded_sgd(H, b, 0, 1)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    v2, h2 = q.get(timeout=120)
+    v2, h2, vs2, hs2 = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert h1 == h2                      # identical residual histories, bit for bit
     assert np.array_equal(v1, v2)
+    assert hs1 == hs2 and np.array_equal(vs1, vs2)  # sharded SGD likewise
+    assert hs1[-1] < hs1[0]
 
 
 def test_shard_range_matches_library(W):
