@@ -58,8 +58,6 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
   cudaStream_t st = op.ctx->stream;
   SolverWork<double> w;
   w.alloc(op, s);
-  WGP_REQUIRE(op.ctx->world == 1 || cfg.method != WGP_AP,
-              "sharded contexts support CG and SGD solves (AP: one GPU per operator)");
   upload_problem<double>(op, w, B, ldb, U1, ldu, n1, st);
   switch (cfg.method) {
     case WGP_CG: {

@@ -98,13 +98,16 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
                                                     int64_t n, const int* __restrict__ blk,
                                                     int bs, const double* __restrict__ delta,
                                                     int s, const int* __restrict__ active,
-                                                    KParams p, double* __restrict__ R) {
+                                                    KParams p, int64_t r0, int64_t nrows,
+                                                    double* __restrict__ R) {
+  // rows r0 .. r0 + nrows of the operator (this rank's), R holds those rows
   const int c = blockIdx.y;
   if (!active[c]) return;
   __shared__ T sX[64][33];
   __shared__ double sD[64];
-  const int64_t i = (int64_t)blockIdx.x * 128 + threadIdx.x;
-  const bool valid = i < n;
+  const int64_t il = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const bool valid = il < nrows;
+  const int64_t i = r0 + il;
   const int64_t start = (int64_t)blk[c] * bs;
   const int len = (int)min((int64_t)bs, n - start);
   T xr[32];
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
       }
     }
   }
-  if (valid) R[i * s + c] -= acc;
+  if (valid) R[il * s + c] -= acc;
 }
 
 // One CTA per block: A = H_BB (fp64, from X64), in-place lower Cholesky, then L^-1.
@@ -321,14 +324,15 @@ void launch_krows(const Op& op, const int* rows, int nb, const double* V, const 
 }
 
 void launch_kcols(const Op& op, const int* blk, int bs, const double* delta, int s,
-                  const int* active, double* R, cudaStream_t st) {
-  dim3 grid(ceil_div(op.n, 128), s);
+                  const int* active, double* R, int64_t r0, int64_t nrows, cudaStream_t st) {
+  if (nrows <= 0) return;
+  dim3 grid(ceil_div(nrows, 128), s);
   if (op.f64())
     kcols_kernel<double><<<grid, 128, 0, st>>>(op.X64.p, op.dpad, op.dim, op.n, blk, bs, delta, s,
-                                               active, op.kp(), R);
+                                               active, op.kp(), r0, nrows, R);
   else
     kcols_kernel<float><<<grid, 128, 0, st>>>(op.X32.p, op.dpad, op.dim, op.n, blk, bs, delta, s,
-                                              active, op.kp(), R);
+                                              active, op.kp(), r0, nrows, R);
   WGP_CUDA(cudaGetLastError());
 }
 

@@ -351,14 +351,19 @@ void sgd_solve_batched(Op& op, const wgp_solver_config& cfg, const std::vector<u
 // n_blocks); factors of every diagonal block are built once on the device.
 void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& w,
                       SolveOutputs& out, cudaStream_t st) {
-  const int64_t n = w.n;
+  // Sharded (world > 1): V is full and replicated; the residual is kept as a full N-row
+  // buffer whose rows this rank owns are updated locally and which is all-gathered before
+  // the block choice and the block solve, so every rank picks the same block, computes the
+  // same delta and applies it to its copy of V -- bit-identical to one GPU.
+  const Ctx& ctx = *op.ctx;
+  const int64_t n = w.n, N = w.N, r0 = w.r0;
   const int s = w.s;
-  const int64_t bs64 = std::min<int64_t>(cfg.block_size, n);
+  const int64_t bs64 = std::min<int64_t>(cfg.block_size, N);
   WGP_REQUIRE(bs64 > 0, "ap_solve: block size must be positive");
   WGP_REQUIRE(bs64 <= 1024, "ap_solve: block size > 1024 not supported on the device path");
   WGP_REQUIRE(op.dim <= 32, "ap_solve: dim > 32 not supported on the device path");
   const int bs = (int)bs64;
-  const int nblk = (int)((n + bs - 1) / bs);
+  const int nblk = (int)((N + bs - 1) / bs);
   DBuf<double> fac((size_t)nblk * bs * bs), inv((size_t)nblk * bs * bs);
   DBuf<int> fail(1);
   WGP_CUDA(cudaMemsetAsync(fail.p, 0, sizeof(int), st));
@@ -367,15 +372,25 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   WGP_CUDA(cudaMemcpyAsync(&hfail, fail.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   WGP_CUDA(cudaStreamSynchronize(st));
   if (hfail) throw_error(WGP_NOT_SPD, "ap_solve: diagonal block factorization failed");
+  DBuf<double> Rfull;
+  double* Rall = w.R.p;
+  if (ctx.world > 1) {
+    Rfull.alloc((size_t)N * s);
+    Rall = Rfull.p;
+  }
+  double* Rloc = Rall + r0 * s;  // this rank's rows
+  auto gather_r = [&] {
+    if (ctx.world > 1) dist_allgather_rows(ctx, Rall, N, s, sizeof(double), st);
+  };
   double* bnorm = w.scal.p + 3 * s;
   double* rel = w.scal.p + 4 * s;
   int* active = w.act.p;
-  bnorms(*op.ctx, w, bnorm, active, st);
-  launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
+  bnorms(ctx, w, bnorm, active, st);
+  launch_residual(op, w.B.p, w.V.p, Rloc, s, st);
   std::vector<double> hrel(s);
   std::vector<int> hact(s), confirm(s);
   WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
-  residual_norms(*op.ctx, w, w.R.p, bnorm, rel, hrel, st);
+  residual_norms(ctx, w, Rloc, bnorm, rel, hrel, st);
   int n_active = 0;
   for (int c = 0; c < s; ++c) {
     out.history[c].assign(1, hact[c] ? hrel[c] : 0.0);
@@ -389,14 +404,15 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   DBuf<double> delta((size_t)bs * s);
   WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
   for (int k = 1; k <= cfg.max_iters && n_active > 0; ++k) {
+    gather_r();
     if (cfg.ap_ordering == WGP_AP_GREEDY)
-      launch_greedy_block(w.R.p, n, bs, nblk, s, active, blk.p, st);
+      launch_greedy_block(Rall, N, bs, nblk, s, active, blk.p, st);
     else
       launch_set_cyclic(blk.p, s, (k - 1) % nblk, st);
-    launch_ap_block_solve(inv.p, bs, n, blk.p, active, w.R.p, s, w.V.p, delta.p, st);
-    launch_kcols(op, blk.p, bs, delta.p, s, active, w.R.p, st);  // r -= H[:, B] delta
-    if (k % nblk == 0) launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // drift refresh
-    residual_norms(*op.ctx, w, w.R.p, bnorm, rel, hrel, st);
+    launch_ap_block_solve(inv.p, bs, N, blk.p, active, Rall, s, w.V.p, delta.p, st);
+    launch_kcols(op, blk.p, bs, delta.p, s, active, Rloc, r0, n, st);  // r -= H[:, B] delta
+    if (k % nblk == 0) launch_residual(op, w.B.p, w.V.p, Rloc, s, st);  // drift refresh
+    residual_norms(ctx, w, Rloc, bnorm, rel, hrel, st);
     int nconf = 0;
     for (int c = 0; c < s; ++c) {
       confirm[c] = hact[c] && hrel[c] <= cfg.tolerance;
@@ -405,8 +421,8 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
     if (nconf) {  // confirm with the true residual (:296-300)
       launch_residual(op, w.B.p, w.V.p, w.Z.p, s, st);
       WGP_CUDA(cudaMemcpyAsync(dconf.p, confirm.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
-      launch_copy_masked_cols(w.R.p, w.Z.p, n, s, dconf.p, st);
-      residual_norms(*op.ctx, w, w.R.p, bnorm, rel, hrel, st);
+      if (n > 0) launch_copy_masked_cols(Rloc, w.Z.p, n, s, dconf.p, st);
+      residual_norms(ctx, w, Rloc, bnorm, rel, hrel, st);
     }
     bool changed = false;
     for (int c = 0; c < s; ++c) {

@@ -88,8 +88,9 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
 // rows), 0 for the others
 void launch_krows(const Op& op, const int* rows, int nb, const double* V, const double* B, int s,
                   const int* active, double* g, int64_t r0, int64_t r1, cudaStream_t st);
+// R (rows r0 .. r0 + nrows) -= H[rows, B] delta
 void launch_kcols(const Op& op, const int* blk, int bs, const double* delta, int s,
-                  const int* active, double* R, cudaStream_t st);
+                  const int* active, double* R, int64_t r0, int64_t nrows, cudaStream_t st);
 void launch_block_chol(const Op& op, int bs, int nblk, double* fac, double* inv, int* fail,
                        cudaStream_t st);
 void launch_ap_block_solve(const double* inv, int bs, int64_t n, const int* blk, const int* active,

@@ -120,6 +120,35 @@ def sharded_sgd(H, b, rank, world, seed=11, batch=64, lr=0.002, momentum=0.9, it
     return v, hist
 
 
+def sharded_ap(H, b, rank, world, bs=200, iters=40):
+    """Row-sharded greedy AP (solvers.cu ap_solve_batched over a sharded context): the
+    residual rows a rank owns are updated locally and the full residual is all-gathered
+    before each block choice and block solve, so every rank picks the same block and
+    applies the same delta to its replicated v."""
+    n = b.size
+    r0, r1 = shard_range(n, world, rank)
+    Hl, bl = H[r0:r1], b[r0:r1]
+    nblk = (n + bs - 1) // bs
+    chol = [np.linalg.cholesky(H[k * bs:(k + 1) * bs, k * bs:(k + 1) * bs]) for k in range(nblk)]
+    v = np.zeros(n)
+    bnorm = np.sqrt(gather_sum(chunk_dots(bl, bl, r0), world))
+    r_l = bl - rowdot(Hl, v)
+    hist = []
+    for k in range(1, iters + 1):
+        r = gather_rows(r_l, n, world)
+        norms = [np.linalg.norm(r[j * bs:(j + 1) * bs]) for j in range(nblk)]
+        best = int(np.argmax(norms))  # first maximum
+        L = chol[best]
+        blk = slice(best * bs, min(n, (best + 1) * bs))
+        delta = np.linalg.solve(L.T, np.linalg.solve(L, r[blk]))
+        v[blk] += delta
+        r_l = r_l - rowdot(Hl[:, blk], delta)
+        if k % nblk == 0:
+            r_l = bl - rowdot(Hl, v)
+        hist.append(np.sqrt(gather_sum(chunk_dots(r_l, r_l, r0), world)) / bnorm)
+    return v, hist
+
+
 def system(n=1300):
     rng = np.random.default_rng(0)
     X = rng.random((n, 3))
@@ -135,8 +164,9 @@ def _worker(rank, world, port, q):
     H, b = system()
     v, hist = sharded_cg(H, b, rank, world)
     vs, hs = sharded_sgd(H, b, rank, world)
+    va, ha = sharded_ap(H, b, rank, world)
     if rank == 0:
-        q.put((v, hist, vs, hs))
+        q.put((v, hist, vs, hs, va, ha))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -150,17 +180,18 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world", [2])
-def test_sharded_cg_and_sgd_bitwise_equal_single_process(world):
+def test_sharded_solvers_bitwise_equal_single_process(world):
     H, b = system()
     v1, h1 = sharded_cg(H, b, 0, 1)
     vs1, hs1 = sharded_sgd(H, b, 0, 1)
+    va1, ha1 = sharded_ap(H, b, 0, 1)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    v2, h2, vs2, hs2 = q.get(timeout=120)
+    v2, h2, vs2, hs2, va2, ha2 = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -168,6 +199,8 @@ def test_sharded_cg_and_sgd_bitwise_equal_single_process(world):
     assert np.array_equal(v1, v2)
     assert hs1 == hs2 and np.array_equal(vs1, vs2)  # sharded SGD likewise
     assert hs1[-1] < hs1[0]
+    assert ha1 == ha2 and np.array_equal(va1, va2)  # and sharded AP
+    assert ha1[-1] < ha1[0]
 
 
 def test_shard_range_matches_library(W):
