@@ -52,7 +52,21 @@ namespace tc {
 constexpr int BM = 128;        // rows per CTA (UMMA M)
 constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
 constexpr int NSET = 3;         // epilogue sets (8 warps each) taking tiles round-robin
-constexpr int NPROD = 1;        // producer warps per ring (XB ring, V ring); 3 measured slower
+#ifndef WGP_TC_NPX
+#define WGP_TC_NPX 1
+#endif
+#ifndef WGP_TC_NPV
+#define WGP_TC_NPV 1
+#endif
+// Producer warps per ring (NPX / NPV warps taking the ring's tiles round-robin).  Bulk copies
+// issued by one warp are processed one at a time (~400-900 cycles each in isolation,
+// tools/bulk_microbench2.cu), but at C3 two XB and three V producers measured no faster
+// than one of each (V arrives ~1 tile per period because the whole pipeline is paced by
+// the kernel map; the kernel time hardly depends on the V tile size: 6.8 ms at s=16 vs
+// 7.5 ms at s=64), so the default is one.
+constexpr int NPX = WGP_TC_NPX, NPV = WGP_TC_NPV;
+__host__ __device__ constexpr int xb_warp(int k) { return k == 0 ? 0 : (k == 1 ? 4 : 6); }
+__host__ __device__ constexpr int v_warp(int k) { return k == 0 ? 2 : (k == 1 ? 5 : 7); }
 #ifndef WGP_TC_NG2
 #define WGP_TC_NG2 1
 #endif
@@ -60,7 +74,7 @@ constexpr int NPROD = 1;        // producer warps per ring (XB ring, V ring); 3 
 // MMAs costs its SM sub-partition issue slots, and K(t) needs all four TMEM quadrants
 // (one per sub-partition), so a single GEMM2 warp made its quadrant the late one every tile.
 constexpr int NG2 = WGP_TC_NG2;
-constexpr int NROLE = NG2 == 1 ? 4 : 8;  // role warps: producers, GEMM1, GEMM2 issuers
+constexpr int NROLE = (NG2 == 1 && NPX == 1 && NPV == 1) ? 4 : 8;  // role warps
 constexpr int NTHREADS = 32 * NROLE + NSET * 256;  // role warps + NSET x 8 epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
 constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (fp64 drain after each)
@@ -300,18 +314,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   const uint32_t sbo1 = (p.K1 * ESZ / 16) * 128;  // 8-row group stride of XA/XB tiles
 
   const int g2k = warp == 3 ? 0 : (NG2 > 1 && warp == 4 ? 1 : (NG2 > 2 && warp == 6 ? 2 : -1));
-  if ((warp == 0 || warp == 2) || (NPROD > 1 && warp < NROLE && warp != 1 && g2k < 0)) {
+  static_assert(NG2 == 1 || (NPX == 1 && NPV == 1), "GEMM2 issuers share warps 4/6 with producers");
+  static_assert(NPX <= 3 && NPV <= 3, "role warp layout");
+  int xk = -1, vk = -1;
+  for (int k = 0; k < NPX; ++k) if (warp == xb_warp(k)) xk = k;
+  for (int k = 0; k < NPV; ++k) if (warp == v_warp(k)) vk = k;
+  if (xk >= 0 || vk >= 0) {
     // ------------------------------------------------------------ producers (TMA engine)
     // Two independent rings: XB_j is consumed by GEMM1 right away, V_j only by GEMM2 after
     // the kernel map, so V stays resident ~4x longer; separate rings let each be as deep as
-    // its own lifetime needs.  Bulk copies issued by one warp are processed one at a time
-    // (~400-900 cycles each, nearly size-independent; tools/bulk_microbench2.cu), so each
-    // ring can be fed by NPROD warps taking its tiles round-robin (NPROD = 3 measured 9%
-    // slower at C3 than 1: the copies are not the binding stage).
-    // warps 0 (, 4, 6) -> XB ring; 2 (, 5, 7) -> V ring
-    static_assert(NPROD == 1 || (NROLE == 2 + 2 * NPROD && NPROD <= 3 && NG2 == 1), "role warp layout");
-    const bool is_xb = warp == 0 || warp == 4 || warp == 6;
-    const int pk = warp == 0 || warp == 2 ? 0 : (warp == 4 || warp == 5 ? 1 : 2);
+    // its own lifetime needs, each fed by NPX / NPV warps taking its tiles round-robin.
+    const bool is_xb = xk >= 0;
+    const int pk = is_xb ? xk : vk;
     const bool leader = ptx::elect_one();
     if (warp == 0 && leader) {
       ptx::mbar_arrive_expect_tx(xa_full, XA_BYTES);
@@ -319,7 +333,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
                     xa_full);
     }
     if (is_xb) {
-      for (int t = pk; t < T; t += NPROD) {
+      for (int t = pk; t < T; t += NPX) {
         const int st = t % NSX;
         if (t >= NSX) wait_role(&xb_empty[st], ((t / NSX) & 1) ^ 1, p.prod_sleep_ns);
         if (leader) {
@@ -332,7 +346,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         __syncwarp();
       }
     } else {
-      for (int t = pk; t < T; t += NPROD) {
+      for (int t = pk; t < T; t += NPV) {
         const int st = t % NSV;
         if (t >= NSV) wait_role(&v_empty[st], ((t / NSV) & 1) ^ 1, p.prod_sleep_ns);
         if (leader) {
@@ -425,6 +439,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
             for (int ks = 0; ks < BJ / 16; ++ks)
               ptx::mma_f16_ts(ycor, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);
           }
+          trace_ev(p, t, 10);
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
           if (last) ptx::mma_commit(&y_full[ya]);
@@ -581,7 +596,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&k_full[b]);
       if (tr) trace_ev(p, t, 5);
-      if (lane == 0 && half == 0 && set == 0 && (q == 1 || q == 3)) trace_ev(p, t, q == 1 ? 10 : 11);
+      if (lane == 0 && half == 0 && set == 0 && q == 3) trace_ev(p, t, 11);
       if (drainer && dc0 < p.s_pad && drained < NCH - 1 && t >= (drained + 1) * CH + 4)
         drain_step(drained);
     }
@@ -1038,7 +1053,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
                                cudaMemcpyDeviceToHost, st));
       WGP_CUDA(cudaStreamSynchronize(st));
       if (FILE* f = fopen(trace_path, "w")) {
-        fprintf(f, "tile,g1_issue,g2_issue,epi_wait_s,epi_s_ready,epi_wait_k,epi_done,prod_issue,epi_ld_done,v_issue,g2_vready,done_q1,done_q3\n");
+        fprintf(f, "tile,g1_issue,g2_issue,epi_wait_s,epi_s_ready,epi_wait_k,epi_done,prod_issue,epi_ld_done,v_issue,g2_vready,g2_issued,done_q3\n");
         for (int t = 0; t < ntiles; ++t)
         {
           fprintf(f, "%d", t);
