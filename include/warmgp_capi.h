@@ -193,6 +193,11 @@ uint64_t wgp_rng_uniform_index(uint64_t* state, uint64_t n);
 /* n consecutive scale * normal() draws from (and advancing) the generator at *state. */
 void wgp_rng_normal_fill(uint64_t* state, int64_t n, double scale, double* out);
 
+/* exact_solve (analysis.cpp:15-26): X = H^{-1} B by a dense fp64 Cholesky of the operator's
+ * H on the device (materialised once; n <= 60000).  B, X: n x s column-major.  A
+ * non-positive pivot returns WGP_NOT_SPD (the reference's LLT failure).  Unsharded only. */
+wgp_status wgp_exact_solve(wgp_op* op, const double* B, int64_t ldb, int s, double* X, int64_t ldx);
+
 /* ---- measurement: CUDA-event timing of the tensor-core kernel-matvec launches only (the
  *      prep kernels around it excluded), for roofline reporting.  enable != 0 starts
  *      recording (and clears); read synchronizes the recorded events and returns the summed

@@ -24,6 +24,7 @@ void throw_error(wgp_status code, const char* fmt, ...) {
 }
 
 void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major);
+bool exact_solve_dev(const Op& op, double* Y, int s, cudaStream_t st);
 void launch_rff_eval32(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
                        const double* ph, const double* amp, int F, int S, double coeff,
                        double* out, int64_t ldo, cudaStream_t st);
@@ -511,6 +512,26 @@ wgp_status wgp_rff_eval_fast(wgp_op* op, const double* Omega, const double* phas
                              const double* amps, int F, int S, double signal_scale, const double* Xs,
                              int64_t m, int64_t ldx, double* out, int64_t ldo) {
   return rff_eval_impl(op, Omega, phases, amps, F, S, signal_scale, Xs, m, ldx, out, ldo, true);
+}
+
+wgp_status wgp_exact_solve(wgp_op* op, const double* B, int64_t ldb, int s, double* X, int64_t ldx) {
+  return guard([&] {
+    WGP_REQUIRE(op && B && X && s >= 1, "wgp_exact_solve: bad argument");
+    WGP_REQUIRE(op->ctx->world == 1, "exact_solve: unsharded operators only");
+    const int64_t n = op->n;
+    WGP_REQUIRE(n >= 1 && ldb >= n && ldx >= n, "exact_solve: bad shape");
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    DBuf<double> stage((size_t)n * s), Y((size_t)n * s);
+    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, B, sizeof(double) * ldb, sizeof(double) * n,
+                               s, cudaMemcpyHostToDevice, st));
+    launch_colmajor_to_rows(stage.p, n, n, s, Y.p, true, st);
+    if (!exact_solve_dev(*op, Y.p, s, st)) throw_error(WGP_NOT_SPD, "exact_solve: Cholesky failed");
+    launch_rows_to_colmajor(Y.p, n, s, stage.p, n, true, st);
+    WGP_CUDA(cudaMemcpy2DAsync(X, sizeof(double) * ldx, stage.p, sizeof(double) * n, sizeof(double) * n,
+                               s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+  });
 }
 
 }  // extern "C"

@@ -47,6 +47,7 @@ EXPORTS = (
     "wgp_rff_eval", "wgp_derive_seed", "wgp_rng_next_u64", "wgp_rng_uniform", "wgp_rng_normal",
     "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
     "wgp_rng_normal_fill", "wgp_kernel_timer_enable", "wgp_kernel_timer_read", "wgp_rff_eval_fast",
+    "wgp_exact_solve",
 )
 
 
@@ -137,6 +138,7 @@ def _declare(L):
         "wgp_normal_fill": (None, [C.c_uint64, I64, D, P]),
         "wgp_rng_normal_fill": (None, [P, I64, D, P]),
         "wgp_kernel_timer_enable": (None, [C.c_int]),
+        "wgp_exact_solve": (C.c_int, [P, P, I64, C.c_int, P, I64]),
         "wgp_kernel_timer_read": (C.c_int, [P, P]),
         "wgp_sample_prior": (C.c_int, [C.c_int, D, I64, I64, C.c_uint64, P, P, P]),
     }
@@ -617,3 +619,16 @@ def eval_posterior(op: KernelOperator, priors: list, weights, Xs, fast: bool = F
     if op.n > 0:
         out = out + op.cross_matvec(Xs, weights)
     return out
+
+
+def exact_solve(op: KernelOperator, b) -> np.ndarray:
+    """exact_solve (analysis.cpp:15-26): H^{-1} b by a dense fp64 device Cholesky of the
+    operator's H; b: n or n x s.  NotSpdError if the factorization fails."""
+    B = np.asfortranarray(np.asarray(b, dtype=np.float64))
+    vec = B.ndim == 1
+    if vec:
+        B = B.reshape(-1, 1, order="F")
+    n, s = B.shape
+    Xo = np.zeros((n, s), order="F")
+    _check(lib().wgp_exact_solve(op._h, _ptr(B), n, s, _ptr(Xo), n))
+    return Xo[:, 0] if vec else Xo

@@ -156,3 +156,18 @@ def test_f64_path_on_ill_conditioned_c2_like(W):
     op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.1, W.RBF), X, precision=W.F64)
     r = W.solve(op, b, W.Initialization.cold(), W.SolverConfig(tolerance=1e-4, max_iters=2000, precond_rank=100, precond_shift=0.01))
     assert r.converged and r.residual_history[-1] <= 1e-4
+
+
+@pytest.mark.parametrize("n,kind", [(300, 0), (1900, 1)])
+def test_exact_solve_matches_oracle(W, O, n, kind):
+    """wgp_exact_solve (device dense Cholesky, analysis.cpp:15-26) vs the oracle's exact_solve,
+    incl. the config-1 warm-start system H11 (N=1900, RBF, sigma_n^2 = 1e-2)."""
+    ls, sn = (0.5, 0.1) if kind == 1 else (0.4, 0.2)
+    X = O.uniform_inputs(O.derive_seed(0, 1), n, 8)
+    y = O.gaussian_vector(O.derive_seed(0, 8), n)
+    ref = O.exact_solve(O.gram_matrix(X, O.KernelHyperparams(ls, 1.0, sn, kind)), y)
+    op = W.KernelOperator(W.KernelHyperparams(ls, 1.0, sn, kind), X, precision=W.F64)
+    got = W.exact_solve(op, y)
+    assert np.linalg.norm(got - ref) <= 1e-8 * np.linalg.norm(ref)
+    two = W.exact_solve(op, np.column_stack([y, 2 * y]))
+    assert np.array_equal(two[:, 0], got) and np.allclose(two[:, 1], 2 * got, rtol=1e-12)

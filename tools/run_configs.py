@@ -39,14 +39,14 @@ def run_c1(quick=False) -> dict:
     op = W.KernelOperator(hyp, X, precision=W.F64)
     prior = W.sample_prior(hyp, 8, 1024, W.derive_seed(0, 7))
     y = W.build_sample_rhs(op, prior, 0.1, W.derive_seed(0, 8))
-    # u1 = exact_solve(H11, y1) (analysis.cpp:15-26): dense H11 from the device operator,
-    # host Cholesky (the exact warm start is setup, not the measured path)
+    # u1 = exact_solve(H11, y1) (analysis.cpp:15-26) on the device (dense fp64 Cholesky)
     op1 = W.KernelOperator(hyp, X[:n1], precision=W.F64)
-    H1 = op1.kmatvec(np.eye(n1))
-    L = np.linalg.cholesky(0.5 * (H1 + H1.T))
-    u1 = np.linalg.solve(L.T, np.linalg.solve(L, y[:n1]))
+    t0 = time.perf_counter()
+    u1 = W.exact_solve(op1, y[:n1])
+    t_exact = time.perf_counter() - t0
     cfg = W.SolverConfig(tolerance=1e-6, max_iters=2000, precond_rank=100, precond_shift=0.01)
-    out = {"config": "c1", "n": n, "n1": n1, "precision": "f64", "tol": 1e-6}
+    out = {"config": "c1", "n": n, "n1": n1, "precision": "f64", "tol": 1e-6,
+           "exact_solve_u1_seconds": t_exact}
     for mode, init in (("cold", W.Initialization.cold()), ("warm", W.Initialization.warm(u1))):
         W.solve(op, y, init, cfg)  # warm-up
         t0 = time.perf_counter()
