@@ -339,6 +339,34 @@ inline Matrix eval_posterior(const KernelOperator& H, const std::vector<RffPrior
   return out;
 }
 
+// ascend_peaks (thompson.cpp:209-258) for S posterior samples (priors[s], weights column s)
+// at once: starts holds S*P rows (sample-major) of dim columns; returns S best points and
+// values.  grad_posterior (sampling.cpp:77-87) is wgp_grad_posterior.
+struct AscendResult {  // thompson.hpp AscendResult
+  Matrix points;
+  Vector values;
+};
+inline AscendResult ascend_peaks(const KernelOperator& H, const std::vector<RffPrior>& priors,
+                                 const Matrix& weights, const Matrix& starts, int steps, double rate) {
+  const int S = (int)priors.size();
+  if (S == 0 || starts.rows % S != 0 || weights.rows != H.size() || weights.cols != S)
+    throw std::invalid_argument("ascend_peaks: one peak set per posterior sample required");
+  const int64_t F = priors[0].frequencies.rows, D = priors[0].frequencies.cols;
+  std::vector<double> Om((size_t)(S * F * D)), ph((size_t)(S * F)), am((size_t)(S * F));
+  for (int p = 0; p < S; ++p) {
+    std::copy(priors[p].frequencies.data.begin(), priors[p].frequencies.data.end(), Om.begin() + p * F * D);
+    std::copy(priors[p].phases.begin(), priors[p].phases.end(), ph.begin() + p * F);
+    std::copy(priors[p].amplitudes.begin(), priors[p].amplitudes.end(), am.begin() + p * F);
+  }
+  AscendResult r;
+  r.points = Matrix(S, D);
+  r.values.assign((size_t)S, 0.0);
+  check(wgp_ascend_peaks(H.get(), Om.data(), ph.data(), am.data(), (int)F, S, priors[0].signal_scale,
+                         weights.data.data(), weights.rows, starts.data.data(), (int)(starts.rows / S),
+                         steps, rate, r.points.data.data(), r.values.data()));
+  return r;
+}
+
 #ifdef WARMGP_GPU_EIGEN
 // ---------------------------------------------------------------- Eigen overloads
 // For the reference build (Eigen::MatrixXd is column-major fp64, like Matrix): the call

@@ -198,6 +198,23 @@ void wgp_rng_normal_fill(uint64_t* state, int64_t n, double scale, double* out);
  * non-positive pivot returns WGP_NOT_SPD (the reference's LLT failure).  Unsharded only. */
 wgp_status wgp_exact_solve(wgp_op* op, const double* B, int64_t ldb, int s, double* X, int64_t ldx);
 
+/* grad_posterior (sampling.cpp:77-87): gradients at m points of the posterior samples
+ * prior_s + K(., X) W[:, s] (the operator's rows as training inputs; priors as in
+ * wgp_rff_eval, W: n x S column-major).  Point i belongs to sample sidx[i]; Xs, G: m x dim
+ * column-major.  Matern-3/2 as in the reference; RBF analogue for RBF operators.  fp64. */
+wgp_status wgp_grad_posterior(wgp_op* op, const double* Omega, const double* phases,
+                              const double* amps, int F, int S, double signal_scale,
+                              const double* W, int64_t ldw, const double* Xs, int64_t ldx,
+                              const int32_t* sidx, int64_t m, double* G, int64_t ldg);
+/* ascend_peaks (thompson.cpp:209-258) for S samples at once: Adam ascent (beta 0.9/0.999,
+ * eps 1e-8, clamp to [0,1]^dim, freeze on a non-finite gradient) from P starts per sample
+ * (starts: S*P x dim column-major, row s*P + t), best point/value per sample over all its
+ * trajectories (strict >, earlier start and step win ties).  best_x: S x dim column-major. */
+wgp_status wgp_ascend_peaks(wgp_op* op, const double* Omega, const double* phases,
+                            const double* amps, int F, int S, double signal_scale, const double* W,
+                            int64_t ldw, const double* starts, int P, int steps, double rate,
+                            double* best_x, double* best_val);
+
 /* ---- measurement: CUDA-event timing of the tensor-core kernel-matvec launches only (the
  *      prep kernels around it excluded), for roofline reporting.  enable != 0 starts
  *      recording (and clears); read synchronizes the recorded events and returns the summed

@@ -157,6 +157,8 @@ def _declare(L):
         "wgo_eval_prior": (C.c_int, [P, P, P, I64, I64, D, P, I64, P]),
         "wgo_build_sample_rhs": (C.c_int, [P, P, P, I64, I64, D, P, I64, D, C.c_uint64, P]),
         "wgo_eval_posterior": (C.c_int, [P, P, P, P, I64, P, I64, I64, P, P, I64, P]),
+        "wgo_grad_posterior": (C.c_int, [P, P, P, P, I64, P, I64, I64, P, P, P]),
+        "wgo_ascend_peaks": (C.c_int, [P, P, P, P, I64, P, I64, I64, P, P, I64, C.c_int, D, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -607,3 +609,28 @@ def eval_posterior(h: KernelHyperparams, p: RffPrior, X_train, weights, Xs) -> n
                                     p.num_features, _ptr(X_train), X_train.shape[0], X_train.shape[1],
                                     _ptr(weights), _ptr(Xs), Xs.shape[0], _ptr(out)))
     return out
+
+
+def grad_posterior(h: KernelHyperparams, p: RffPrior, X_train, weights, x) -> np.ndarray:
+    """grad_posterior (sampling.cpp:77-87) at one point."""
+    X_train = _f64(X_train)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    g = np.zeros(x.size)
+    _check(lib().wgo_grad_posterior(_hyp(h), _ptr(_f64(p.frequencies)), _ptr(_f64(p.phases)),
+                                    _ptr(_f64(p.amplitudes)), p.num_features, _ptr(X_train),
+                                    X_train.shape[0], x.size, _ptr(_f64(weights)), _ptr(x), _ptr(g)))
+    return g
+
+
+def ascend_peaks(h: KernelHyperparams, p: RffPrior, X_train, weights, starts, steps: int, rate: float):
+    """ascend_peaks (thompson.cpp:209-258) for one posterior sample -> (best point, value)."""
+    X_train = _f64(X_train)
+    starts = _f64(starts)
+    dim = starts.shape[1]
+    bx = np.zeros(dim)
+    bv = C.c_double(0.0)
+    _check(lib().wgo_ascend_peaks(_hyp(h), _ptr(_f64(p.frequencies)), _ptr(_f64(p.phases)),
+                                  _ptr(_f64(p.amplitudes)), p.num_features, _ptr(X_train),
+                                  X_train.shape[0], dim, _ptr(_f64(weights)), _ptr(starts),
+                                  starts.shape[0], steps, rate, _ptr(bx), C.byref(bv)))
+    return bx, bv.value

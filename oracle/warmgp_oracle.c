@@ -980,3 +980,82 @@ int wgo_eval_posterior(const wgo_hyp* h, const double* Omega, const double* phas
   }
   return WGO_OK;
 }
+
+
+/* grad_prior (sampling.cpp:48-54) + the kernel-weighted sum of grad_posterior (:77-87). */
+int wgo_grad_posterior(const wgo_hyp* h, const double* Omega, const double* phases,
+                       const double* amps, int64_t F, const double* Xtrain, int64_t n,
+                       int64_t dim, const double* weights, const double* x, double* g) {
+  if (F < 1 || dim < 1) return WGO_INVALID_ARGUMENT;
+  const double coeff = h->signal_scale * sqrt(2.0 / (double)F);
+  for (int64_t k = 0; k < dim; ++k) g[k] = 0.0;
+  /* -coeff * Omega^T (sin(Omega x + phi) .* w) */
+  for (int64_t k = 0; k < dim; ++k) {
+    double acc = 0.0;
+    for (int64_t f = 0; f < F; ++f) {
+      double arg = 0.0;
+      for (int64_t q = 0; q < dim; ++q) arg += Omega[q * F + f] * x[q];
+      arg += phases[f];
+      acc += Omega[k * F + f] * (sin(arg) * amps[f]);
+    }
+    g[k] = -coeff * acc;
+  }
+  const double l = h->lengthscale, s2 = h->signal_scale * h->signal_scale;
+  for (int64_t j = 0; j < n; ++j) {
+    double r2 = 0.0;
+    for (int64_t k = 0; k < dim; ++k) {
+      const double df = Xtrain[k * n + j] - x[k];
+      r2 += df * df;
+    }
+    double f;
+    if (h->kind == WGO_RBF) {
+      f = weights[j] * (s2 / (l * l)) * exp(-0.5 * r2 / (l * l));
+    } else {
+      f = weights[j] * (3.0 * s2 / (l * l)) * exp(-sqrt(3.0) * sqrt(r2) / l);
+    }
+    for (int64_t k = 0; k < dim; ++k) g[k] += f * (Xtrain[k * n + j] - x[k]);
+  }
+  return WGO_OK;
+}
+
+int wgo_ascend_peaks(const wgo_hyp* h, const double* Omega, const double* phases,
+                     const double* amps, int64_t F, const double* Xtrain, int64_t n, int64_t dim,
+                     const double* weights, const double* peaks, int64_t P, int steps,
+                     double rate, double* best_x, double* best_val) {
+  if (dim < 1 || dim > 64) return WGO_INVALID_ARGUMENT;
+  double x[64], m[64], v[64], g[64], val;
+  double bv = -INFINITY;
+  for (int64_t k = 0; k < dim; ++k) best_x[k] = 0.0;
+  for (int64_t t = 0; t < P; ++t) {
+    for (int64_t k = 0; k < dim; ++k) {
+      x[k] = peaks[k * P + t];
+      m[k] = v[k] = 0.0;
+    }
+    wgo_eval_posterior(h, Omega, phases, amps, F, Xtrain, n, dim, weights, x, 1, &val);
+    if (val > bv) {
+      bv = val;
+      for (int64_t k = 0; k < dim; ++k) best_x[k] = x[k];
+    }
+    for (int k = 1; k <= steps; ++k) {
+      wgo_grad_posterior(h, Omega, phases, amps, F, Xtrain, n, dim, weights, x, g);
+      int finite = 1;
+      for (int64_t q = 0; q < dim; ++q) finite &= isfinite(g[q]) ? 1 : 0;
+      if (!finite) break;
+      const double bc1 = 1.0 - pow(0.9, k), bc2 = 1.0 - pow(0.999, k);
+      for (int64_t q = 0; q < dim; ++q) {
+        m[q] = 0.9 * m[q] + 0.1 * g[q];
+        v[q] = 0.999 * v[q] + 0.001 * (g[q] * g[q]);
+        const double step = (m[q] / bc1) / (sqrt(v[q] / bc2) + 1e-8);
+        x[q] += rate * step;
+        x[q] = x[q] < 0.0 ? 0.0 : (x[q] > 1.0 ? 1.0 : x[q]);
+      }
+      wgo_eval_posterior(h, Omega, phases, amps, F, Xtrain, n, dim, weights, x, 1, &val);
+      if (val > bv) {
+        bv = val;
+        for (int64_t q = 0; q < dim; ++q) best_x[q] = x[q];
+      }
+    }
+  }
+  *best_val = bv;
+  return WGO_OK;
+}

@@ -193,6 +193,20 @@ int wgo_eval_posterior(const wgo_hyp* h, const double* Omega, const double* phas
                        int64_t dim, const double* weights, const double* Xs, int64_t m,
                        double* out);
 
+/* grad_posterior, sampling.cpp:77-87 (with grad_prior :48-54): gradient of eval_posterior at
+ * one point x (dim).  Matern-3/2 as in the reference; RBF analogue (s^2/l^2 e^{-r^2/2l^2}) as
+ * the documented extension. */
+int wgo_grad_posterior(const wgo_hyp* h, const double* Omega, const double* phases,
+                       const double* amps, int64_t F, const double* Xtrain, int64_t n,
+                       int64_t dim, const double* weights, const double* x, double* g);
+/* ascend_peaks for one sample, thompson.cpp:209-258: Adam ascent from each of P start rows
+ * (peaks: P x dim col-major), steps/rate as given, clamped to [0,1]^dim; best point and
+ * value over all trajectories (strict >, first wins). */
+int wgo_ascend_peaks(const wgo_hyp* h, const double* Omega, const double* phases,
+                     const double* amps, int64_t F, const double* Xtrain, int64_t n, int64_t dim,
+                     const double* weights, const double* peaks, int64_t P, int steps,
+                     double rate, double* best_x, double* best_val);
+
 #ifdef __cplusplus
 }
 #endif

@@ -163,9 +163,14 @@ def posterior_at(state: GrowthState, Xc: np.ndarray) -> np.ndarray:
 
 def bo_loop(dim=4, n_init=5000, batch=64, rounds=50, n_samples=128, candidates=100_000,
             warm=True, seed=0, cfg: W.SolverConfig | None = None, precision=W.F64, ctx=None,
-            fast_candidates: bool = True) -> dict:
+            fast_candidates: bool = True, peak_groups: int = 5, ascent_steps: int = 30,
+            ascent_rate: float = 0.05) -> dict:
     """Configuration 5: BoConfig defaults (Matern-3/2 l=0.3, s_f=1, sigma_n=1e-3, F=2000;
-    thompson.hpp:29-58), CG with the small budget (5 iterations, tol 1e-2)."""
+    thompson.hpp:29-58), CG with the small budget (5 iterations, tol 1e-2).  Acquisition as
+    select_peaks + ascend_peaks (thompson.cpp:188-258): the candidates are split into
+    `peak_groups` groups, each sample's argmax in every group is a start, and the device Adam
+    ascent (ascent_steps / ascent_rate, BoConfig defaults 30 / 0.05) picks the batch point;
+    ascent_steps = 0 takes the plain argmax."""
     hyp = W.KernelHyperparams(0.3, 1.0, 1e-3, W.MATERN32)
     cfg = cfg or W.SolverConfig(method=W.CG, tolerance=1e-2, max_iters=5, precond_rank=100,
                                 precond_shift=hyp.noise_scale ** 2)
@@ -180,9 +185,14 @@ def bo_loop(dim=4, n_init=5000, batch=64, rounds=50, n_samples=128, candidates=1
         rec = st.solve_round(cfg, warm)
         t0 = time.perf_counter()
         Xc = uniform_rows_fast(W.derive_seed(seed, 0xA0000 + st.round), candidates, dim)
-        F = posterior_at(st, Xc)  # candidates x samples
-        arg = np.argmax(F[:, :batch], axis=0)  # first `batch` samples acquire (thompson.cpp:403-410)
-        Xn = Xc[arg]
+        F = posterior_at(st, Xc)[:, :batch]  # candidates x samples; the first `batch` acquire
+        if ascent_steps > 0:
+            g = np.array_split(np.arange(candidates), peak_groups)
+            starts = np.stack([Xc[gi[np.argmax(F[gi], axis=0)]] for gi in g], axis=1)  # batch x groups x D
+            wd = st.weights[:, :1] - st.weights[:, 1:1 + batch]
+            Xn, _ = W.ascend_peaks(st.op, st.priors[:batch], wd, starts, ascent_steps, ascent_rate)
+        else:
+            Xn = Xc[np.argmax(F, axis=0)]
         rec["candidate_seconds"] = time.perf_counter() - t0
         yn = obj.observe(Xn)
         st.add_points(Xn, yn)

@@ -25,6 +25,12 @@ void throw_error(wgp_status code, const char* fmt, ...) {
 
 void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major);
 bool exact_solve_dev(const Op& op, double* Y, int s, cudaStream_t st);
+void launch_grad_posterior(const Op& op, const double* Om, const double* ph, const double* am,
+                           int F, double coeff, const double* W, const double* Xs,
+                           const int* sidx, int64_t m, double* G, cudaStream_t st);
+void launch_ascend(const Op& op, const double* Om, const double* ph, const double* am, int F,
+                   double coeff, const double* W, int S, const double* starts, int P, int steps,
+                   double rate, double* best_val, double* best_x, cudaStream_t st);
 void launch_rff_eval32(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
                        const double* ph, const double* amp, int F, int S, double coeff,
                        double* out, int64_t ldo, cudaStream_t st);
@@ -531,6 +537,90 @@ wgp_status wgp_exact_solve(wgp_op* op, const double* B, int64_t ldb, int s, doub
     WGP_CUDA(cudaMemcpy2DAsync(X, sizeof(double) * ldx, stage.p, sizeof(double) * n, sizeof(double) * n,
                                s, cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+// upload S priors (prior-major, each F x dim column-major) and W (n x S column-major)
+static void upload_posterior(const Op& op, const double* Omega, const double* phases,
+                             const double* amps, int F, int S, const double* W, int64_t ldw,
+                             DBuf<double>& dOm, DBuf<double>& dPh, DBuf<double>& dAm,
+                             DBuf<double>& dW, cudaStream_t st) {
+  const size_t nom = (size_t)S * F * op.dim, nf = (size_t)S * F;
+  dOm.alloc(nom);
+  dPh.alloc(nf);
+  dAm.alloc(nf);
+  dW.alloc((size_t)std::max<int64_t>(op.n, 1) * S);
+  WGP_CUDA(cudaMemcpyAsync(dOm.p, Omega, sizeof(double) * nom, cudaMemcpyHostToDevice, st));
+  WGP_CUDA(cudaMemcpyAsync(dPh.p, phases, sizeof(double) * nf, cudaMemcpyHostToDevice, st));
+  WGP_CUDA(cudaMemcpyAsync(dAm.p, amps, sizeof(double) * nf, cudaMemcpyHostToDevice, st));
+  if (op.n > 0)
+    WGP_CUDA(cudaMemcpy2DAsync(dW.p, sizeof(double) * op.n, W, sizeof(double) * ldw,
+                               sizeof(double) * op.n, S, cudaMemcpyHostToDevice, st));
+}
+
+wgp_status wgp_grad_posterior(wgp_op* op, const double* Omega, const double* phases,
+                              const double* amps, int F, int S, double signal_scale,
+                              const double* W, int64_t ldw, const double* Xs, int64_t ldx,
+                              const int32_t* sidx, int64_t m, double* G, int64_t ldg) {
+  return guard([&] {
+    WGP_REQUIRE(op && Omega && phases && amps && W && Xs && sidx && G, "wgp_grad_posterior: null argument");
+    WGP_REQUIRE(F >= 1 && S >= 1 && m >= 0 && ldw >= op->n && ldx >= m && ldg >= m,
+                "grad_posterior: bad shape");
+    WGP_REQUIRE(op->ctx->world == 1, "grad_posterior: unsharded operators only");
+    for (int64_t i = 0; i < m; ++i)
+      WGP_REQUIRE(sidx[i] >= 0 && sidx[i] < S, "grad_posterior: sample index out of range");
+    if (m == 0) return;
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    const int dim = op->dim;
+    DBuf<double> dOm, dPh, dAm, dW, dX((size_t)m * dim), dG((size_t)m * dim);
+    DBuf<int> dS((size_t)m);
+    upload_posterior(*op, Omega, phases, amps, F, S, W, ldw, dOm, dPh, dAm, dW, st);
+    std::vector<double> hx((size_t)m * dim);
+    for (int64_t i = 0; i < m; ++i)
+      for (int k = 0; k < dim; ++k) hx[(size_t)i * dim + k] = Xs[(int64_t)k * ldx + i];
+    WGP_CUDA(cudaMemcpyAsync(dX.p, hx.data(), sizeof(double) * hx.size(), cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpyAsync(dS.p, sidx, sizeof(int) * m, cudaMemcpyHostToDevice, st));
+    const double coeff = signal_scale * std::sqrt(2.0 / (double)F);
+    launch_grad_posterior(*op, dOm.p, dPh.p, dAm.p, F, coeff, dW.p, dX.p, dS.p, m, dG.p, st);
+    WGP_CUDA(cudaMemcpyAsync(hx.data(), dG.p, sizeof(double) * hx.size(), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < m; ++i)
+      for (int k = 0; k < dim; ++k) G[(int64_t)k * ldg + i] = hx[(size_t)i * dim + k];
+  });
+}
+
+wgp_status wgp_ascend_peaks(wgp_op* op, const double* Omega, const double* phases,
+                            const double* amps, int F, int S, double signal_scale, const double* W,
+                            int64_t ldw, const double* starts, int P, int steps, double rate,
+                            double* best_x, double* best_val) {
+  return guard([&] {
+    WGP_REQUIRE(op && Omega && phases && amps && W && starts && best_x && best_val,
+                "wgp_ascend_peaks: null argument");
+    WGP_REQUIRE(F >= 1 && S >= 1 && P >= 1 && steps >= 0 && ldw >= op->n, "ascend_peaks: bad shape");
+    WGP_REQUIRE(op->ctx->world == 1, "ascend_peaks: unsharded operators only");
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    const int dim = op->dim;
+    const int64_t m = (int64_t)S * P;
+    DBuf<double> dOm, dPh, dAm, dW, dX((size_t)m * dim), dBX((size_t)m * dim), dBV((size_t)m);
+    upload_posterior(*op, Omega, phases, amps, F, S, W, ldw, dOm, dPh, dAm, dW, st);
+    std::vector<double> hx((size_t)m * dim), hv((size_t)m);
+    for (int64_t i = 0; i < m; ++i)
+      for (int k = 0; k < dim; ++k) hx[(size_t)i * dim + k] = starts[(int64_t)k * m + i];
+    WGP_CUDA(cudaMemcpyAsync(dX.p, hx.data(), sizeof(double) * hx.size(), cudaMemcpyHostToDevice, st));
+    const double coeff = signal_scale * std::sqrt(2.0 / (double)F);
+    launch_ascend(*op, dOm.p, dPh.p, dAm.p, F, coeff, dW.p, S, dX.p, P, steps, rate, dBV.p, dBX.p, st);
+    WGP_CUDA(cudaMemcpyAsync(hx.data(), dBX.p, sizeof(double) * hx.size(), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaMemcpyAsync(hv.data(), dBV.p, sizeof(double) * hv.size(), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    for (int s = 0; s < S; ++s) {  // start order, strict > (thompson.cpp:227-252)
+      int64_t best = (int64_t)s * P;
+      for (int t = 1; t < P; ++t)
+        if (hv[(size_t)s * P + t] > hv[(size_t)best]) best = (int64_t)s * P + t;
+      best_val[s] = hv[(size_t)best];
+      for (int k = 0; k < dim; ++k) best_x[(int64_t)k * S + s] = hx[(size_t)best * dim + k];
+    }
   });
 }
 

@@ -47,7 +47,7 @@ EXPORTS = (
     "wgp_rff_eval", "wgp_derive_seed", "wgp_rng_next_u64", "wgp_rng_uniform", "wgp_rng_normal",
     "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
     "wgp_rng_normal_fill", "wgp_kernel_timer_enable", "wgp_kernel_timer_read", "wgp_rff_eval_fast",
-    "wgp_exact_solve",
+    "wgp_exact_solve", "wgp_grad_posterior", "wgp_ascend_peaks",
 )
 
 
@@ -139,6 +139,8 @@ def _declare(L):
         "wgp_rng_normal_fill": (None, [P, I64, D, P]),
         "wgp_kernel_timer_enable": (None, [C.c_int]),
         "wgp_exact_solve": (C.c_int, [P, P, I64, C.c_int, P, I64]),
+        "wgp_grad_posterior": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, P, I64, P, I64, P, I64]),
+        "wgp_ascend_peaks": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, P, C.c_int, C.c_int, D, P, P]),
         "wgp_kernel_timer_read": (C.c_int, [P, P]),
         "wgp_sample_prior": (C.c_int, [C.c_int, D, I64, I64, C.c_uint64, P, P, P]),
     }
@@ -632,3 +634,45 @@ def exact_solve(op: KernelOperator, b) -> np.ndarray:
     Xo = np.zeros((n, s), order="F")
     _check(lib().wgp_exact_solve(op._h, _ptr(B), n, s, _ptr(Xo), n))
     return Xo[:, 0] if vec else Xo
+
+
+def _stack_priors(priors):
+    F = priors[0].num_features
+    sf = priors[0].signal_scale
+    for p in priors:
+        if p.num_features != F or p.signal_scale != sf:
+            raise ValueError("priors must share F and the signal scale")
+    Om = np.ascontiguousarray(np.stack([np.asfortranarray(p.frequencies).ravel(order="F") for p in priors]))
+    ph = np.ascontiguousarray(np.stack([p.phases for p in priors]))
+    am = np.ascontiguousarray(np.stack([p.amplitudes for p in priors]))
+    return Om, ph, am, F, sf
+
+
+def grad_posterior(op: KernelOperator, priors: list, weights, Xs, sample_index) -> np.ndarray:
+    """grad_posterior (sampling.cpp:77-87) at m points; point i uses sample sample_index[i]
+    (prior priors[s], weights[:, s]) with the operator's rows as training inputs -> m x dim."""
+    Om, ph, am, F, sf = _stack_priors(priors)
+    Wt = np.asfortranarray(np.asarray(weights, dtype=np.float64).reshape(op.n, len(priors)))
+    Xs = np.asfortranarray(np.asarray(Xs, dtype=np.float64))
+    m = Xs.shape[0]
+    sidx = np.ascontiguousarray(np.asarray(sample_index, dtype=np.int32))
+    G = np.zeros((m, op.dim), order="F")
+    _check(lib().wgp_grad_posterior(op._h, _ptr(Om), _ptr(ph), _ptr(am), F, len(priors), sf, _ptr(Wt),
+                                    max(op.n, 1), _ptr(Xs), max(m, 1), _ptr(sidx), m, _ptr(G), max(m, 1)))
+    return G
+
+
+def ascend_peaks(op: KernelOperator, priors: list, weights, starts, steps: int, rate: float):
+    """ascend_peaks (thompson.cpp:209-258) for all samples at once; starts: S x P x dim.
+    Returns (best points S x dim, best values S)."""
+    Om, ph, am, F, sf = _stack_priors(priors)
+    S = len(priors)
+    starts = np.asarray(starts, dtype=np.float64)
+    P = starts.shape[1]
+    Wt = np.asfortranarray(np.asarray(weights, dtype=np.float64).reshape(op.n, S))
+    st = np.asfortranarray(starts.reshape(S * P, op.dim))
+    bx = np.zeros((S, op.dim), order="F")
+    bv = np.zeros(S)
+    _check(lib().wgp_ascend_peaks(op._h, _ptr(Om), _ptr(ph), _ptr(am), F, S, sf, _ptr(Wt), max(op.n, 1),
+                                  _ptr(st), P, steps, rate, _ptr(bx), _ptr(bv)))
+    return bx, bv

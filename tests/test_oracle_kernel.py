@@ -119,3 +119,66 @@ def test_matrix_free_matches_dense(O, kind):
     np.testing.assert_allclose(O.kmatvec(X, h, V, rows=(100, 200)), (H @ V)[100:200], rtol=1e-13, atol=1e-12)
     Xs = O.uniform_inputs(78, 50, 5)
     np.testing.assert_allclose(O.cross_matvec(Xs, X, h, V), O.cross_kernel(Xs, X, h) @ V, rtol=1e-12, atol=1e-12)
+
+
+def _grad_case(O):
+    hyp = O.KernelHyperparams(0.6, 1.1, 1e-3, O.MATERN32)
+    X = O.uniform_inputs(51, 15, 3)
+    return hyp, X
+
+
+def test_oracle_grad_posterior_reference_cases(O):
+    """test_sampling.cpp:190-228: zero amplitudes + zero weights give a zero gradient; the
+    gradient matches central finite differences of eval_posterior (rel 1e-5); finite at a
+    training point."""
+    hyp, X = _grad_case(O)
+    p = O.sample_prior(hyp, 3, 32, 52)
+    p.amplitudes[:] = 0.0
+    assert np.abs(O.grad_posterior(hyp, p, X, np.zeros(15), [0.2, 0.4, 0.6])).max() == 0.0
+    p = O.sample_prior(hyp, 3, 128, 53)
+    w = O.gaussian_vector(54, 15)
+    rng = O.Rng(55)
+    h = 1e-5
+    for _ in range(10):
+        x = np.array([rng.uniform() for _ in range(3)])
+        g = O.grad_posterior(hyp, p, X, w, x)
+        fd = np.zeros(3)
+        for d in range(3):
+            xp, xm = x.copy(), x.copy()
+            xp[d] += h
+            xm[d] -= h
+            fd[d] = (O.eval_posterior(hyp, p, X, w, xp[None, :])[0] - O.eval_posterior(hyp, p, X, w, xm[None, :])[0]) / (2 * h)
+        assert np.linalg.norm(g - fd) / np.linalg.norm(g) < 1e-5
+    p = O.sample_prior(hyp, 3, 64, 56)
+    assert np.isfinite(O.grad_posterior(hyp, p, X, O.gaussian_vector(57, 15), X[4])).all()
+
+
+def test_oracle_grad_posterior_rbf_finite_differences(O):
+    """RBF extension: the same finite-difference check."""
+    hyp = O.KernelHyperparams(0.5, 0.9, 1e-3, O.RBF)
+    X = O.uniform_inputs(61, 20, 4)
+    p = O.sample_prior(hyp, 4, 64, 62)
+    w = O.gaussian_vector(63, 20)
+    x = np.array([0.3, 0.7, 0.1, 0.5])
+    g = O.grad_posterior(hyp, p, X, w, x)
+    h = 1e-5
+    fd = np.array([(O.eval_posterior(hyp, p, X, w, (x + h * e)[None, :])[0]
+                    - O.eval_posterior(hyp, p, X, w, (x - h * e)[None, :])[0]) / (2 * h) for e in np.eye(4)])
+    assert np.linalg.norm(g - fd) / np.linalg.norm(g) < 1e-5
+
+
+def test_oracle_ascend_peaks_reference_cases(O):
+    """test_thompson.cpp:189-232: a single positive representer weight is a radial bump at x0;
+    zero steps return the best start; 200 steps at rate 0.01 climb to x0."""
+    hyp = O.KernelHyperparams(0.25, 1.0, 1e-3, O.MATERN32)
+    x0 = np.array([[0.43, 0.57]])
+    silent = O.sample_prior(hyp, 2, 16, 80)
+    silent.amplitudes[:] = 0.0
+    starts = np.array([[0.35, 0.5], [0.5, 0.62], [0.41, 0.55]])
+    w = np.array([2.0])
+    vals = [O.eval_posterior(hyp, silent, x0, w, st[None, :])[0] for st in starts]
+    bx, bv = O.ascend_peaks(hyp, silent, x0, w, starts, 0, 0.02)
+    assert np.array_equal(bx, starts[int(np.argmax(vals))])
+    bx, bv = O.ascend_peaks(hyp, silent, x0, w, starts, 200, 0.01)
+    peak = O.eval_posterior(hyp, silent, x0, w, x0)[0]
+    assert np.linalg.norm(bx - x0[0]) < 1e-2 and bv >= peak - 1e-3 and bv >= max(vals)
