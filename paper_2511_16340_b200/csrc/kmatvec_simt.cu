@@ -10,6 +10,8 @@
 // Distances here use explicit differences sum_k (x_rk - x_jk)^2, which equals the
 // reference's norm form to rounding and has no cancellation; the tensor-core path
 // (kmatvec_tc.cu) uses the norm form as a contraction.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace wgp {
@@ -183,13 +185,151 @@ void launch_bs(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* 
   WGP_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------------------------------------
+// fp64 path on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64): per 64-row x 32-column
+// tile, phase 1 evaluates the kernel entries into shared memory on the CUDA cores (the
+// exp/sqrt sequences), phase 2 multiplies the tile into the accumulators with DMMA.  Warp w
+// owns rows 8w..8w+7 and all NT 8-column RHS tiles; one A fragment (K) feeds NT DMMAs, so
+// phase 2 moves ~1 byte of shared memory per FMA.  DMMA runs at the same 64 FMA/clk/SM as
+// DFMA on B200 (tools/dmma_microbench.cu) with 1/8 of the instructions, leaving issue slots
+// to phase 1.  Each output column's sum order is fixed and independent of s.
+constexpr int DM = 64, DN = 32;
+
+template <int NT>
+__global__ void __launch_bounds__(256) kmatvec_dmma_kernel(
+    const double* __restrict__ Xr, int64_t nrows, int64_t row0, const double* __restrict__ Xc,
+    int64_t ncols, int dpad, int dim, const double* __restrict__ V, int s,
+    const double* __restrict__ B, double* __restrict__ Y, KParams p, int gram) {
+  constexpr int BS = NT * 8;
+  extern __shared__ double dsm[];
+  const int ds = dim + 1;
+  double* sXr = dsm;                   // [DM][ds]
+  double* sXc = sXr + DM * ds;         // [DN][ds]
+  double* sK = sXc + DN * ds;          // [DM][DN + 1]
+  double* sV = sK + DM * (DN + 1);     // [DN][BS + 1]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t rbase = (int64_t)blockIdx.x * DM;
+  const int c0 = blockIdx.y * BS;
+  for (int e = tid; e < DM * dim; e += 256) {
+    const int r = e / dim, k = e % dim;
+    const int64_t gr = rbase + r;
+    sXr[r * ds + k] = gr < nrows ? Xr[gr * dpad + k] : 0.0;
+  }
+  double acc[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const double kdiag = p.s2 + p.noise2;
+  for (int64_t jb = 0; jb < ncols; jb += DN) {
+    __syncthreads();
+    for (int e = tid; e < DN * dim; e += 256) {
+      const int j = e / dim, k = e % dim;
+      const int64_t gj = jb + j;
+      sXc[j * ds + k] = gj < ncols ? Xc[gj * dpad + k] : 0.0;
+    }
+    for (int e = tid; e < DN * BS; e += 256) {
+      const int j = e / BS, c = e % BS;
+      const int64_t gj = jb + j;
+      sV[j * (BS + 1) + c] = (gj < ncols && c0 + c < s) ? V[gj * s + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    // phase 1: 64 x 32 kernel entries, 8 per thread; the dimension loop runs outside the 8
+    // entries so the eight distance and exp/sqrt chains interleave (ILP)
+    {
+      constexpr int NQ = DM * DN / 256;
+      const int j = tid % DN;
+      const int64_t gj = jb + j;
+      double d2[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) d2[q] = 0.0;
+      for (int k = 0; k < dim; ++k) {
+        const double xc = sXc[j * ds + k];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const double df = sXr[(tid / DN + q * (256 / DN)) * ds + k] - xc;
+          d2[q] = fma(df, df, d2[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int r = tid / DN + q * (256 / DN);
+        double kv = kmap<double>(d2[q], p);
+        if (gram && row0 + rbase + r == gj) kv = kdiag;
+        if (gj >= ncols) kv = 0.0;
+        sK[r * (DN + 1) + j] = kv;
+      }
+    }
+    __syncthreads();
+    // phase 2: Y[8w.., :] += K[8w.., 32] . V[32, BS] in 8 k-steps of 4
+#pragma unroll
+    for (int k0 = 0; k0 < DN; k0 += 4) {
+      const double a = sK[(warp * 8 + (lane >> 2)) * (DN + 1) + k0 + (lane & 3)];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const double b = sV[(k0 + (lane & 3)) * (BS + 1) + t * 8 + (lane >> 2)];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[t][0]), "+d"(acc[t][1])
+                     : "d"(a), "d"(b));
+      }
+    }
+  }
+  const int64_t gr = rbase + warp * 8 + (lane >> 2);
+  if (gr >= nrows) return;
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = c0 + t * 8 + (lane & 3) * 2 + u;
+      if (c >= s) continue;
+      const double y = acc[t][u];
+      Y[gr * s + c] = B ? B[gr * s + c] - y : y;
+    }
+}
+
+template <int NT>
+void launch_dmma(const double* Xr, int64_t nrows, int64_t row0, const double* Xc, int64_t ncols,
+                 int dpad, int dim, const double* V, int s, const double* B, double* Y, KParams kp,
+                 bool gram, cudaStream_t st) {
+  dim3 grid(ceil_div(nrows, DM), ceil_div(s, NT * 8));
+  const size_t smem = sizeof(double) * ((size_t)(DM + DN) * (dim + 1) + DM * (DN + 1) +
+                                        (size_t)DN * (NT * 8 + 1));
+  if (smem > 48 * 1024)
+    WGP_CUDA(cudaFuncSetAttribute(kmatvec_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+  kmatvec_dmma_kernel<NT><<<grid, 256, smem, st>>>(Xr, nrows, row0, Xc, ncols, dpad, dim, V, s, B, Y,
+                                                   kp, gram ? 1 : 0);
+  WGP_CUDA(cudaGetLastError());
+}
+
 }  // namespace
+
+// fp64 kernel-matvec: DMMA kernel (RHS chunks of up to 128 columns); WGP_F64_SIMT=1 selects
+// the all-CUDA-core kernel instead (validation).
+static void launch_f64(const Op& op, const double* Xr, int64_t nrows, int64_t row0,
+                       const double* Xc, int64_t ncols, const double* V, int s, const double* B,
+                       double* Y, bool gram, cudaStream_t st) {
+  WGP_REQUIRE(op.dim <= 32, "fp64 kmatvec: dim <= 32 supported, got %d", op.dim);
+  const KParams kp = op.kp();
+  const int dp = op.dpad, d = op.dim;
+  if (s <= 8) return launch_dmma<1>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
+  if (s <= 16) return launch_dmma<2>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
+  if (s <= 24) return launch_dmma<3>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
+  if (s <= 32) return launch_dmma<4>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
+  if (s <= 64) return launch_dmma<8>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
+  return launch_dmma<16>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
+}
 
 template <typename T>
 void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
                          int64_t ncols, const double* V, int s, const double* B, double* Y,
                          bool gram, cudaStream_t st) {
   if (nrows <= 0 || s <= 0) return;
+  if constexpr (sizeof(T) == 8) {
+    static const bool simt = getenv("WGP_F64_SIMT") && atoi(getenv("WGP_F64_SIMT")) != 0;
+    if (!simt) {
+      return launch_f64(op, reinterpret_cast<const double*>(Xr), nrows, row0,
+                        reinterpret_cast<const double*>(Xc), ncols, V, s, B, Y, gram, st);
+    }
+  }
   if (s <= 1) return launch_bs<T, 1>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
   if (s <= 2) return launch_bs<T, 2>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
   if (s <= 4) return launch_bs<T, 4>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
