@@ -51,7 +51,16 @@ namespace tc {
 
 constexpr int BM = 128;        // rows per CTA (UMMA M)
 constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
-constexpr int NSET = 3;         // epilogue sets (8 warps each) taking tiles round-robin
+#ifndef WGP_TC_SETW
+#define WGP_TC_SETW 8
+#endif
+constexpr int EPIW = 24;        // epilogue warps
+constexpr int SETW = WGP_TC_SETW;  // warps per epilogue set (8: 32 columns each, 4: 64)
+constexpr int NSET = EPIW / SETW;  // sets taking tiles round-robin
+constexpr int CPW = 64 / (SETW / 4);  // tile columns per epilogue warp
+// SETW = 4 (six sets, 64 columns per warp) hung in testing (the drain schedule assumes the
+// two-drainer-set layout); only the measured 8-warp sets are enabled.
+static_assert(SETW == 8, "only 8-warp epilogue sets are supported");
 #ifndef WGP_TC_NPX
 #define WGP_TC_NPX 1
 #endif
@@ -75,7 +84,7 @@ __host__ __device__ constexpr int v_warp(int k) { return k == 0 ? 2 : (k == 1 ? 
 // (one per sub-partition), so a single GEMM2 warp made its quadrant the late one every tile.
 constexpr int NG2 = WGP_TC_NG2;
 constexpr int NROLE = (NG2 == 1 && NPX == 1 && NPV == 1) ? 4 : 8;  // role warps
-constexpr int NTHREADS = 32 * NROLE + NSET * 256;  // role warps + NSET x 8 epilogue warps
+constexpr int NTHREADS = 32 * (NROLE + EPIW);  // role warps + epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
 constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (fp64 drain after each)
 // TMEM: a ring of NB 64-column tile buffers followed by the Y accumulator.  A buffer holds
@@ -295,7 +304,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     ptx::mbar_init(xa_full, 1);
     for (int i = 0; i < MAX_NB; ++i) {
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&k_full[i], 8);
+      ptx::mbar_init(&k_full[i], SETW);
       ptx::mbar_init(&b_free[i], 1);
     }
     for (int i = 0; i < NG2; ++i) ptx::mbar_init(&g2_tok[i], 1);
@@ -456,8 +465,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // NSET sets of 8 warps take tiles round-robin (set = t mod NSET); within a set, warp
     // (quadrant q, half) maps rows 32q.. and columns 32 half.. of the tile, 16 at a time.
     const int q = warp & 3;                   // TMEM lane quadrant accessible to this warp
-    const int g = (warp - NROLE) >> 2;        // 0 .. 2 NSET - 1
-    const int set = g >> 1, half = g & 1;
+    const int g = (warp - NROLE) >> 2;        // group of 4 warps (one per quadrant), 0..5
+    const int set = g / (SETW / 4), half = g % (SETW / 4);
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int r = q * 32 + lane;              // row within the CTA tile
     const int64_t gi = p.row0 + (int64_t)blockIdx.x * BM + r;
@@ -468,7 +477,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // columns, summed in fp64 into this CTA's slice of the column-major partials buffer
     // [gy][s][nrows] (lanes = consecutive rows: coalesced; L2-resident); reduce_splits scales
     // and transposes.
-    const bool drainer = set < 2;
+    const bool drainer = g < 4;
     const int dc0 = (g & 3) * 16;
     const bool row_ok = lr < p.nrows;
     const int ncol = max(0, min(16, p.s - dc0));
@@ -552,11 +561,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         ptx::mbar_wait(&s_full[b], bph);
       ptx::tc_fence_after();
       if (tr) trace_ev(p, t, 3);
-      const int64_t gj_base = (int64_t)(jt0 + t) * BJ + half * 32;
-      const bool diag = p.gram && gj_base < grow0 + BM && gj_base + 32 > grow0;
+      const int64_t gj_base = (int64_t)(jt0 + t) * BJ + half * CPW;
+      const bool diag = p.gram && gj_base < grow0 + BM && gj_base + CPW > grow0;
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const uint32_t col = tmem + lane_off + b * 64 + half * 32 + h2 * 16;
+      for (int h2 = 0; h2 < CPW / 16; ++h2) {
+        const uint32_t col = tmem + lane_off + b * 64 + half * CPW + h2 * 16;
         uint32_t v[16];
         ptx::tmem_ld16(col, v);
         ptx::tmem_wait_ld();
