@@ -104,8 +104,11 @@ constexpr int TRW = 12;  // trace slots per tile
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
 // Software-exponential share (quarters) of the kernel map: Matern spends 2 SFU ops per pair
 // (sqrt, ex2), RBF 1.
-constexpr int SWQ_MATERN = 2;
-constexpr int SWQ_RBF = 1;
+// (0 = all exponentials on MUFU: fastest at every measured share for both kernels; the
+// software path is kept as a compile-time option, -DWGP_TC_SWQ=1..4.)
+#ifndef WGP_TC_SWQ
+#define WGP_TC_SWQ 0
+#endif
 
 struct Params {
   const void* XA;       // tiled A operand rows (this launch's rows start at tile 0)
@@ -124,10 +127,6 @@ struct Params {
   double out_scale;     // s^2 * 2^-10
   double noise2;
   int gram;
-  int sleep_ns;  // epilogue wait backoff (WGP_TC_SLEEP)
-  int role_sleep_ns;  // MMA-issuer wait backoff (WGP_TC_RSLEEP)
-  int prod_sleep_ns;  // producer wait backoff (WGP_TC_PSLEEP)
-  int dbg;  // timing experiments only (WGP_TC_DEBUG): 1 GEMM2 hi.hi only, 2 GEMM1 one K-step, 4 no map
   unsigned long long* trace;  // debug: per-tile event clocks of CTA 0 (nullptr normally)
   unsigned long long* cta_trace;  // debug: per-CTA [start, loop end, end] globaltimer + smid
 };
@@ -244,15 +243,6 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
   }
 }
 
-// Role-warp waits: spinning warps take issue slots from the epilogue warps sharing their SM
-// sub-partition (and K(t) needs every quadrant), so waits with slack can back off.
-__device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity, int sleep_ns) {
-  if (sleep_ns > 0)
-    ptx::mbar_wait_sleep(bar, parity, (uint32_t)sleep_ns);
-  else
-    ptx::mbar_wait(bar, parity);
-}
-
 template <int SWQ>
 __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NSX, int NSV) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -344,7 +334,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     if (is_xb) {
       for (int t = pk; t < T; t += NPX) {
         const int st = t % NSX;
-        if (t >= NSX) wait_role(&xb_empty[st], ((t / NSX) & 1) ^ 1, p.prod_sleep_ns);
+        if (t >= NSX) ptx::mbar_wait(&xb_empty[st], ((t / NSX) & 1) ^ 1);
         if (leader) {
           trace_ev(p, t, 6);
           ptx::mbar_arrive_expect_tx(&xb_full[st], XB_BYTES);
@@ -357,7 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     } else {
       for (int t = pk; t < T; t += NPV) {
         const int st = t % NSV;
-        if (t >= NSV) wait_role(&v_empty[st], ((t / NSV) & 1) ^ 1, p.prod_sleep_ns);
+        if (t >= NSV) ptx::mbar_wait(&v_empty[st], ((t / NSV) & 1) ^ 1);
         if (leader) {
           trace_ev(p, t, 8);
           ptx::mbar_arrive_expect_tx(&v_full[st], 2 * VT_BYTES);
@@ -383,23 +373,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       int st1 = 0, b1 = 0;
       uint32_t ph1 = 0, phb1 = 0;
       for (int t = 0; t < T; ++t) {
-        if (p.role_sleep_ns > 0) {
-          ptx::mbar_wait_sleep(&xb_full[st1], ph1, p.role_sleep_ns);
-          if (t >= NB) ptx::mbar_wait_sleep(&b_free[b1], phb1 ^ 1, p.role_sleep_ns);
-        } else {
-          ptx::mbar_wait(&xb_full[st1], ph1);
-          if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
-        }
+        ptx::mbar_wait(&xb_full[st1], ph1);
+        if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 0);
           const uint64_t dB = dXB0 + xb_step * st1;
-          const int nks = (p.dbg & 2) ? 1 : KS1;
           if (p.g1f16) {
-            for (int ks = 0; ks < nks; ++ks)
+            for (int ks = 0; ks < KS1; ++ks)
               ptx::mma_f16_ss(tmem + b1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
           } else {
-            for (int ks = 0; ks < nks; ++ks)
+            for (int ks = 0; ks < KS1; ++ks)
               ptx::mma_tf32_ss(tmem + b1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
           }
           ptx::mma_commit(&s_full[b1]);
@@ -421,13 +405,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         const int c = t / CH, ya = c & 1;
         const bool first = t == c * CH, last = t == T - 1 || t == c * CH + CH - 1;
         if (first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
-        wait_role(&v_full[st2], ph2, p.role_sleep_ns);
+        ptx::mbar_wait(&v_full[st2], ph2);
         if (lane == 0) trace_ev(p, t, 9);
-        wait_role(&k_full[b2], phb2, p.role_sleep_ns);
+        ptx::mbar_wait(&k_full[b2], phb2);
         // accumulation order: tile t's MMAs enter the tensor pipe after tile t-1's (issued by
         // the previous issuer, which arrives on g2_tok once its MMAs are dispatched)
         if (NG2 > 1 && t > 0)
-          wait_role(&g2_tok[t % NG2], (t / NG2 - (t % NG2 == 0 ? 1 : 0)) & 1, p.role_sleep_ns);
+          ptx::mbar_wait(&g2_tok[t % NG2], (t / NG2 - (t % NG2 == 0 ? 1 : 0)) & 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 1);
@@ -440,14 +424,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks)
             ptx::mma_f16_ts(yacc, kb + ks * 16, dVh + 16 * ks, idesc2, (!first || ks > 0) ? 1u : 0u);
-          if (!(p.dbg & 1)) {
 #pragma unroll
-            for (int ks = 0; ks < BJ / 16; ++ks)
-              ptx::mma_f16_ts(ycor, kb + ks * 16, dVl + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(ycor, kb + ks * 16, dVl + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
 #pragma unroll
-            for (int ks = 0; ks < BJ / 16; ++ks)
-              ptx::mma_f16_ts(ycor, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);
-          }
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(ycor, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);
           trace_ev(p, t, 10);
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
@@ -501,7 +483,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
                    : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3])
                    : "r"(tmem + lane_off + TM_Y + ya * 64 + dc0 + dk));
       ptx::tmem_wait_ld();
-      if (row_ok && !(p.dbg & 8)) {
+      if (row_ok) {
         // first chunk stores, later chunks add with fire-and-forget reductions performed at
         // L2.  Each address is only ever touched by this thread, and same-address operations
         // of one thread stay in program order, so the fp64 summation order (chunk 0, 1, 2,
@@ -532,11 +514,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // after the sweep: the correction accumulator, added last (the final y_full commit
     // covers it)
     auto drain_corr = [&]() {
-      if (p.dbg & 1) return;
       uint32_t y[16];
       ptx::tmem_ld16(tmem + lane_off + TM_C + dc0, y);
       ptx::tmem_wait_ld();
-      if (row_ok && !(p.dbg & 8)) {
+      if (row_ok) {
 #pragma unroll
         for (int k = 0; k < 16; ++k)
           if (k < ncol)
@@ -555,10 +536,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         while (drained < NCH - 1 && t - NB >= (drained + 2) * CH) drain_all(drained);
       const bool tr = lane == 0 && q == 0 && half == 0 && set == 0;
       if (tr) trace_ev(p, t, 2);
-      if (p.sleep_ns > 0)
-        ptx::mbar_wait_sleep(&s_full[b], bph, p.sleep_ns);
-      else
-        ptx::mbar_wait(&s_full[b], bph);
+      ptx::mbar_wait(&s_full[b], bph);
       ptx::tc_fence_after();
       if (tr) trace_ev(p, t, 3);
       const int64_t gj_base = (int64_t)(jt0 + t) * BJ + half * CPW;
@@ -571,12 +549,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         ptx::tmem_wait_ld();
         if (tr && h2 == 0) trace_ev(p, t, 7);
         float kv[16];
-        if (p.dbg & 4) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) kv[c] = __uint_as_float(v[c]);
-        } else {
-          kernel_map<SWQ, 16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
-        }
+        kernel_map<SWQ, 16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
         if (diag) {  // tile touches the diagonal: k(x,x) = s^2 exactly
           const int64_t gj0 = gj_base + h2 * 16;
 #pragma unroll
@@ -1007,14 +980,6 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     prm.out_scale = kp.s2 * 0x1.0p-10;
     prm.noise2 = kp.noise2;
     prm.gram = gram ? 1 : 0;
-    static const int dbg = getenv("WGP_TC_DEBUG") ? atoi(getenv("WGP_TC_DEBUG")) : 0;
-    prm.dbg = dbg;
-    static const int sleep_ns = getenv("WGP_TC_SLEEP") ? atoi(getenv("WGP_TC_SLEEP")) : 0;
-    prm.sleep_ns = sleep_ns;
-    static const int rsleep_ns = getenv("WGP_TC_RSLEEP") ? atoi(getenv("WGP_TC_RSLEEP")) : 0;
-    prm.role_sleep_ns = rsleep_ns;
-    static const int psleep_ns = getenv("WGP_TC_PSLEEP") ? atoi(getenv("WGP_TC_PSLEEP")) : 0;
-    prm.prod_sleep_ns = psleep_ns;
     prm.trace = nullptr;
     static const char* trace_path = getenv("WGP_TC_TRACE");
     prm.cta_trace = nullptr;
@@ -1030,13 +995,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     const size_t smem = tc_smem_bytes(K1, esz, s_pad, &nsx, &nsv);
     WGP_REQUIRE(nsx >= 2 && nsv >= 2, "kmatvec_tc: dim %d too large for the shared-memory pipeline",
                 op.dim);
-    static const int forced_swq = getenv("WGP_TC_SWQ") ? atoi(getenv("WGP_TC_SWQ")) : -1;
-    const int swq = forced_swq >= 0 ? std::min(forced_swq, 4)
-                                    : (kp.kind == WGP_MATERN32 ? tc::SWQ_MATERN : tc::SWQ_RBF);
-    auto kern = swq == 0 ? tc::kmatvec_tc_kernel<0>
-              : swq == 1 ? tc::kmatvec_tc_kernel<1>
-              : swq == 2 ? tc::kmatvec_tc_kernel<2>
-              : swq == 3 ? tc::kmatvec_tc_kernel<3> : tc::kmatvec_tc_kernel<4>;
+    auto kern = tc::kmatvec_tc_kernel<WGP_TC_SWQ>;
     WGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     KernelTimer& kt = kernel_timer();
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
