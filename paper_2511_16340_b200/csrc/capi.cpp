@@ -173,6 +173,8 @@ wgp_status wgp_ctx_create(int device, wgp_ctx** out) {
     c->device = device;
     WGP_CUDA(cudaSetDevice(device));
     WGP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    WGP_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : c->part_ev) WGP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     *out = c.release();
   });
 }
@@ -201,6 +203,9 @@ void wgp_ctx_destroy(wgp_ctx* c) {
   cudaSetDevice(c->device);
   if (c->comm) dist_destroy(*c);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (auto& e : c->part_ev)
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -292,10 +297,28 @@ wgp_status wgp_kmatvec(wgp_op* op, const double* V, int64_t ldv, int s, double* 
     WGP_CUDA(cudaMemcpy2DAsync(stage, sizeof(double) * n, V, sizeof(double) * ldv,
                                sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
     launch_colmajor_to_rows(stage, n, n, s, dV, true, st);
-    launch_kmatvec_full(*op, dV, dY, s, st);
-    launch_rows_to_colmajor(dY, n, s, stage, n, true, st);
-    WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage, sizeof(double) * n,
-                               sizeof(double) * n, s, cudaMemcpyDeviceToHost, st));
+    // the rows are computed in two parts; the first part's rows are transposed and copied
+    // back on the copy stream while the second part computes
+    Ctx& c = *op->ctx;
+    const int parts = launch_kmatvec_parts(*op, dV, dY, s, st, 2, c.part_ev);
+    if (parts == 1) {
+      launch_rows_to_colmajor(dY, n, s, stage, n, true, st);
+      WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage, sizeof(double) * n,
+                                 sizeof(double) * n, s, cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+    const int64_t tiles128 = (n + 127) / 128;
+    for (int part = 0; part < parts; ++part) {  // same split as launch_kmatvec_tc's row parts
+      const int64_t a = std::min(n, tiles128 * part / parts * 128);
+      const int64_t b = std::min(n, tiles128 * (part + 1) / parts * 128);
+      WGP_CUDA(cudaStreamWaitEvent(c.copy_stream, c.part_ev[part], 0));
+      if (b <= a) continue;
+      launch_rows_to_colmajor(dY + a * s, b - a, s, stage + a, n, true, c.copy_stream);
+      WGP_CUDA(cudaMemcpy2DAsync(Y + a, sizeof(double) * ldy, stage + a, sizeof(double) * n,
+                                 sizeof(double) * (b - a), s, cudaMemcpyDeviceToHost, c.copy_stream));
+    }
+    WGP_CUDA(cudaStreamSynchronize(c.copy_stream));
     WGP_CUDA(cudaStreamSynchronize(st));
   });
 }

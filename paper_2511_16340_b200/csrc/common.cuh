@@ -84,6 +84,8 @@ struct Comm;  // NCCL plumbing (dist.cpp)
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host-API result copies overlapping compute
+  cudaEvent_t part_ev[2] = {nullptr, nullptr};
   int rank = 0, world = 1;
   Comm* comm = nullptr;
 };

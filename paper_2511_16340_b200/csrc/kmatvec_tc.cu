@@ -911,8 +911,14 @@ bool tc_supported(int dim, int precision) {
 void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64_t nrows,
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
-                       DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st) {
+                       DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st, int row_parts,
+                       cudaEvent_t* part_done) {
   if (nrows <= 0 || s <= 0) return;
+  // Row parts (one RHS chunk only): the V preparation is shared, each part's rows finish
+  // with their own reduce and an event, so a caller can start moving finished rows (e.g.
+  // the device-to-host copy of the host API) while the next part computes.
+  if (s > tc::MAX_SPAD || nrows < 2 * tc::BM) row_parts = 1;
+  row_parts = std::max(1, row_parts);
   const bool f16 = op.tc_f16;
   const int esz = f16 ? 2 : 4;
   const int K1 = tc_k1(op.dim, op.precision, f16);
@@ -960,12 +966,25 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     prm.ntiles = ntiles;
     static const int forced_ch = getenv("WGP_TC_CH") ? atoi(getenv("WGP_TC_CH")) : 0;
     prm.ch = forced_ch > 0 ? forced_ch : tc::CH_DEFAULT;
-    const int row_ctas = (int)((nrows + tc::BM - 1) / tc::BM);
+    for (int part = 0; part < row_parts; ++part) {
+    // rows [pa, pb) of this launch, part boundaries on 128-row CTA tiles
+    const int64_t tiles128 = (nrows + tc::BM - 1) / tc::BM;
+    const int64_t pa = std::min(nrows, tiles128 * part / row_parts * tc::BM);
+    const int64_t pb = std::min(nrows, tiles128 * (part + 1) / row_parts * tc::BM);
+    const int64_t nrows_p = pb - pa;
+    if (nrows_p <= 0) {
+      if (part_done) WGP_CUDA(cudaEventRecord(part_done[part], st));
+      continue;
+    }
+    prm.XA = static_cast<const char*>(XA_rows) + (size_t)pa * K1 * esz;
+    prm.nrows = nrows_p;
+    prm.row0 = row0 + pa;
+    const int row_ctas = (int)((nrows_p + tc::BM - 1) / tc::BM);
     static const int forced_splits = getenv("WGP_TC_SPLITS") ? atoi(getenv("WGP_TC_SPLITS")) : 0;
     const int nsplit = forced_splits > 0 ? forced_splits : tc::choose_splits(row_ctas, ntiles);
     prm.tiles_per_split = (ntiles + nsplit - 1) / nsplit;
     const int gy = (ntiles + prm.tiles_per_split - 1) / prm.tiles_per_split;
-    ysplit.ensure((size_t)gy * nrows * sc);
+    ysplit.ensure((size_t)gy * nrows_p * sc);
     prm.Ypart = ysplit.p;
     prm.s = sc;
     prm.s_pad = s_pad;
@@ -1011,8 +1030,9 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     }
     WGP_CUDA(cudaGetLastError());
     {
-      tc::reduce_splits_kernel<<<dim3((unsigned)((nrows + 31) / 32), (sc + 31) / 32), 256, 0, st>>>(
-          ysplit.p, gy, nrows, row0, sc, sc_down, prm.out_scale, Vc, Bc, kp.noise2, gram ? 1 : 0, Yc);
+      tc::reduce_splits_kernel<<<dim3((unsigned)((nrows_p + 31) / 32), (sc + 31) / 32), 256, 0, st>>>(
+          ysplit.p, gy, nrows_p, row0 + pa, sc, sc_down, prm.out_scale, Vc,
+          Bc ? Bc + pa * sc : nullptr, kp.noise2, gram ? 1 : 0, Yc + pa * sc);
       WGP_CUDA(cudaGetLastError());
     }
     if (trace_path) {
@@ -1039,6 +1059,8 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
         fclose(f);
       }
     }
+      if (part_done) WGP_CUDA(cudaEventRecord(part_done[part], st));
+    }  // row parts
     if (sc != s) {
       WGP_CUDA(cudaMemcpy2DAsync(Y64 + c0, sizeof(double) * s, Yc, sizeof(double) * sc,
                                  sizeof(double) * sc, nrows, cudaMemcpyDeviceToDevice, st));

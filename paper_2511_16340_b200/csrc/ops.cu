@@ -131,6 +131,19 @@ static void dispatch(Op& op, const double* B, const double* V, double* Y, int s,
   }
 }
 
+int launch_kmatvec_parts(Op& op, const double* V, double* Y, int s, cudaStream_t st, int parts,
+                         cudaEvent_t* part_done) {
+  if (op.ctx->world == 1 && op.tensor() && tc_supported(op.dim, op.precision) && s <= 64 &&
+      op.n >= 2 * 128 * parts) {
+    ensure_tc_operands(op, st);
+    launch_kmatvec_tc(op, op.XA.p, op.XB.p, op.n, 0, op.n, V, s, nullptr, Y, true, op.vt, op.vchunk,
+                      op.ychunk, op.ysplit, st, parts, part_done);
+    return parts;
+  }
+  dispatch(op, nullptr, V, Y, s, st);
+  return 1;
+}
+
 // Y (this rank's rows) = H V, V full n x s (fp64 row-major).
 void launch_kmatvec_full(Op& op, const double* V, double* Y, int s, cudaStream_t st) {
   dispatch(op, nullptr, V, Y, s, st);

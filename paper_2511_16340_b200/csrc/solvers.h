@@ -46,7 +46,13 @@ void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0,
 void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64_t nrows,
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
-                       DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st);
+                       DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st,
+                       int row_parts = 1, cudaEvent_t* part_done = nullptr);
+// Host-API form of the gram matvec: on tensor-core operators the rows are computed in
+// `parts` parts, part_done[p] recorded as each part's rows are final (else one part).
+// Returns the number of parts used.
+int launch_kmatvec_parts(Op& op, const double* V, double* Y, int s, cudaStream_t st, int parts,
+                         cudaEvent_t* part_done);
 void tc_build_operands(Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
                        cudaStream_t st);
 int tc_k1(int dim, int precision, bool f16);
