@@ -34,6 +34,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -663,13 +664,16 @@ __global__ void build_operands_kernel(const double* __restrict__ X, int dpad, in
   }
 }
 
-// max over rows of |x - c|_inf / l and |x - c|^2 / l^2 (one block; operand rebuilds only)
+// max over rows of |x - c|_inf / l and |x - c|^2 / l^2 (operand rebuilds only): grid-stride
+// blocks, block maxima merged with atomicMax on the IEEE bits (ordered for non-negative
+// doubles); out must be zeroed.
 __global__ void scaled_extent_kernel(const double* __restrict__ X, int dpad, int dim,
                                      const double* __restrict__ center, double inv_l, int64_t n,
-                                     double* __restrict__ out) {
-  __shared__ double red[2][1024];
+                                     unsigned long long* __restrict__ out) {
+  __shared__ double red[2][256];
   double mx = 0.0, msq = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
     double sq = 0.0;
     for (int k = 0; k < dim; ++k) {
       const double x = (X[i * dpad + k] - center[k]) * inv_l;
@@ -689,38 +693,39 @@ __global__ void scaled_extent_kernel(const double* __restrict__ X, int dpad, int
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    out[0] = red[0][0];
-    out[1] = red[1][0];
+    atomicMax(&out[0], (unsigned long long)__double_as_longlong(red[0][0]));
+    atomicMax(&out[1], (unsigned long long)__double_as_longlong(red[1][0]));
   }
 }
 
-// Per-column max |V| (one block per column) -> power-of-two scales 2^e_c, 2^-e_c with
-// |V * 2^e_c| < 2^14 for the fp16 split.
-__global__ void colscale_kernel(const double* __restrict__ V, int64_t n, int s, int s_pad,
-                                float* __restrict__ scale_up, float* __restrict__ scale_down) {
-  const int c = blockIdx.x;
+// Per-column max |V|: blocks of 64 rows x all columns (coalesced row-major reads), block
+// maxima merged with atomicMax on the IEEE bits (ordered for non-negative doubles).
+__global__ void colmax_kernel(const double* __restrict__ V, int64_t n, int s,
+                              unsigned long long* __restrict__ cmax) {
+  const int64_t r0 = (int64_t)blockIdx.x * 64;
+  const int64_t r1 = min(n, r0 + 64);
+  for (int c0 = 0; c0 < s; c0 += 256) {
+    double a = 0.0;
+    const int c = c0 + (threadIdx.x % 256);
+    if (c < s)
+      for (int64_t j = r0; j < r1; ++j) a = fmax(a, fabs(V[j * s + c]));
+    if (c < s) atomicMax(&cmax[c], (unsigned long long)__double_as_longlong(a));
+  }
+}
+
+__global__ void colscale_finish_kernel(const unsigned long long* __restrict__ cmax, int s, int s_pad,
+                                       float* __restrict__ scale_up, float* __restrict__ scale_down) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= s_pad) return;
-  double m = 0.0;
-  if (c < s)
-    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) m = fmax(m, fabs(V[j * s + c]));
-  __shared__ double red[256];
-  red[threadIdx.x] = m;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
-    __syncthreads();
+  const double mx = c < s ? __longlong_as_double((long long)cmax[c]) : 0.0;
+  int e = 0;
+  if (mx > 0.0) {
+    int ex;
+    frexp(mx, &ex);  // mx = f * 2^ex, f in [0.5, 1)
+    e = max(-100, min(100, 14 - ex));
   }
-  if (threadIdx.x == 0) {
-    int e = 0;
-    if (red[0] > 0.0) {
-      int ex;
-      frexp(red[0], &ex);  // red = f * 2^ex, f in [0.5, 1)
-      e = 14 - ex;         // |V| * 2^e < 2^14
-      e = max(-100, min(100, e));
-    }
-    scale_up[c] = ldexpf(1.0f, e);
-    scale_down[c] = ldexpf(1.0f, -e);
-  }
+  scale_up[c] = ldexpf(1.0f, e);
+  scale_down[c] = ldexpf(1.0f, -e);
 }
 
 // V [ncols][s] fp64 -> per-64-row tile [hi|lo][s_pad/8][8 chunks][8 c][8 j] fp16.
@@ -820,13 +825,16 @@ void tc_build_operands(Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* c
   bool f16 = false;
   static const int force_tf32 = getenv("WGP_TC_TF32_GEMM1") ? atoi(getenv("WGP_TC_TF32_GEMM1")) : 0;
   if (op.precision == WGP_F32_3XTF32 && !force_tf32) {
-    DBuf<double> ext(2);
-    tc::scaled_extent_kernel<<<1, 1024, 0, st>>>(op.X64.p, op.dpad, op.dim, center, inv_l, op.n,
-                                                ext.p);
+    DBuf<unsigned long long> ext(2);
+    WGP_CUDA(cudaMemsetAsync(ext.p, 0, sizeof(unsigned long long) * 2, st));
+    tc::scaled_extent_kernel<<<tc::grid_for(op.n), 256, 0, st>>>(op.X64.p, op.dpad, op.dim, center,
+                                                                inv_l, op.n, ext.p);
     WGP_CUDA(cudaGetLastError());
-    double h[2];
-    WGP_CUDA(cudaMemcpyAsync(h, ext.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    unsigned long long hb[2];
+    WGP_CUDA(cudaMemcpyAsync(hb, ext.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
+    double h[2];
+    std::memcpy(h, hb, sizeof(h));
     f16 = h[0] <= 64.0 && h[1] <= 8192.0;
   }
   op.tc_f16 = f16;
@@ -856,12 +864,16 @@ bool tc_build_cross_rows(const Op& op, const double* Xs, int64_t m, int dpad, DB
   const bool f16 = op.tc_f16;
   const double inv_l = 1.0 / op.lengthscale;
   if (f16) {
-    DBuf<double> ext(2);
-    tc::scaled_extent_kernel<<<1, 1024, 0, st>>>(Xs, dpad, op.dim, op.center.p, inv_l, m, ext.p);
+    DBuf<unsigned long long> ext(2);
+    WGP_CUDA(cudaMemsetAsync(ext.p, 0, sizeof(unsigned long long) * 2, st));
+    tc::scaled_extent_kernel<<<tc::grid_for(m), 256, 0, st>>>(Xs, dpad, op.dim, op.center.p, inv_l, m,
+                                                             ext.p);
     WGP_CUDA(cudaGetLastError());
-    double h[2];
-    WGP_CUDA(cudaMemcpyAsync(h, ext.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    unsigned long long hb[2];
+    WGP_CUDA(cudaMemcpyAsync(hb, ext.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
+    double h[2];
+    std::memcpy(h, hb, sizeof(h));
     if (!(h[0] <= 64.0 && h[1] <= 8192.0)) return false;
   }
   const int K1 = tc_k1(op.dim, op.precision, f16);
@@ -946,11 +958,17 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     const int ntiles = (int)((ncols + tc::BJ - 1) / tc::BJ);
     // scratch: fp16 tiles (2 x s_pad x 64 halves per tile) + 2 x s_pad scales (floats)
     const size_t vt_halves = (size_t)ntiles * tc::BJ * s_pad * 2;
-    vt_scratch.ensure((vt_halves + 1) / 2 + 2 * (size_t)s_pad + 64);
+    // (+ the per-column max bits, 8-byte aligned, after the scales)
+    const size_t vt_floats = ((vt_halves + 1) / 2 + 1) & ~(size_t)1;
+    vt_scratch.ensure(vt_floats + 2 * (size_t)s_pad + 64 + 2 * (size_t)tc::MAX_SPAD);
     __half* vt = reinterpret_cast<__half*>(vt_scratch.p);
-    float* sc_up = vt_scratch.p + (vt_halves + 1) / 2 + 32;
+    float* sc_up = vt_scratch.p + vt_floats + 32;
     float* sc_down = sc_up + s_pad;
-    tc::colscale_kernel<<<s_pad, 256, 0, st>>>(Vc, ncols, sc, s_pad, sc_up, sc_down);
+    unsigned long long* cmax =
+        reinterpret_cast<unsigned long long*>(vt_scratch.p + vt_floats + 64 + 2 * (size_t)s_pad);
+    WGP_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * sc, st));
+    tc::colmax_kernel<<<ceil_div(ncols, 64), 256, 0, st>>>(Vc, ncols, sc, cmax);
+    tc::colscale_finish_kernel<<<1, 128, 0, st>>>(cmax, sc, s_pad, sc_up, sc_down);
     tc::split_v_kernel<<<tc::grid_for((int64_t)ntiles * tc::BJ * s_pad), 256, 0, st>>>(
         Vc, ncols, sc, s_pad, (int64_t)ntiles * tc::BJ, sc_up, vt);
     WGP_CUDA(cudaGetLastError());
