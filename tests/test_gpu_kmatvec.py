@@ -143,3 +143,30 @@ def test_kernel_timer_counts_tc_launches(W):
     W.kernel_timer_enable(False)
     op.kmatvec(V[:, :10])
     assert W.kernel_timer_read() == (0.0, 0)
+
+
+@pytest.mark.parametrize("d", [24, 32])
+def test_tc_wide_dims_and_tf32_operand_fallback(W, d):
+    """Tensor-core path at the widest supported dims, and with coordinates far outside the fp16
+    operand range (|x|/l >> 64), which switches GEMM1 to tf32 operands: both stay within the
+    fp32 bar of the fp64 operator."""
+    rng = np.random.default_rng(d)
+    X = rng.random((3000, d))
+    V = rng.standard_normal((3000, 8))
+    for scale, ls in ((1.0, 0.9), (300.0, 0.9 * 300.0 / 5.0)):
+        Xs = X * scale
+        h = W.KernelHyperparams(ls, 1.0, 0.1, W.MATERN32)
+        ref = W.KernelOperator(h, Xs, precision=W.F64).kmatvec(V)
+        got = W.KernelOperator(h, Xs, precision=W.F32_3XTF32).kmatvec(V)
+        assert colrel(got, ref) <= 1e-4, (d, scale)
+
+
+def test_tf32_precision_mode(W):
+    """WGP_TF32: single-pass tf32 distances (not parity-grade): ~1e-3, documented."""
+    rng = np.random.default_rng(11)
+    X = rng.random((4000, 6))
+    V = rng.standard_normal((4000, 16))
+    h = W.KernelHyperparams(0.5, 1.0, 0.1, W.RBF)
+    ref = W.KernelOperator(h, X, precision=W.F64).kmatvec(V)
+    got = W.KernelOperator(h, X, precision=W.TF32).kmatvec(V)
+    assert colrel(got, ref) <= 5e-3
