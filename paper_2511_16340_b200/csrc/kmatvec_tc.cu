@@ -97,7 +97,7 @@ constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (fp64 drai
 // accumulator: -7.5e-6 for positive V at CH = 16, i.e. 192 instructions per chunk, and
 // 3.5e-4 at N = 101k in a single chain), so every CH tiles the epilogue warps drain the
 // finished accumulator into fp64 partial sums in shared memory.  Measured at N = 10k RBF
-// (tests/gpu_probe_ch.py): CH = 16 -> 3.3e-6 relative, 4 -> 1.1e-6, 1 -> 4.9e-7, at 1.0 /
+// (tools/probes/gpu_probe_ch.py): CH = 16 -> 3.3e-6 relative, 4 -> 1.1e-6, 1 -> 4.9e-7, at 1.0 /
 // 1.08 / 2.2x the C3 time (the fp64 shared-memory traffic of the drains); WGP_TC_CH overrides.
 // TMEM: NB = 6 buffers [0,384), Y0 [384,448), Y1 [448,512).
 constexpr int MAX_NB = 5;

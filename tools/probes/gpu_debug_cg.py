@@ -1,7 +1,7 @@
 """GPU debugging aid (not collected by pytest): TC-path matvec/residual vs oracle on the
 config that produced NaNs in CG, then short CG runs."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 from oracle import oracle as O

@@ -1,6 +1,6 @@
 """GPU debugging aid (not collected): RBF / fp32-path CG NaN hunt."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 from oracle import oracle as O

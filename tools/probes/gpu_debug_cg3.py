@@ -1,6 +1,6 @@
 """GPU debugging aid (not collected): reproduce the fp32-path RBF CG NaN in test order."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from oracle import oracle as O
 from paper_2511_16340_b200 import warmgp as W

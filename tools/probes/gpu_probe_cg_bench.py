@@ -1,6 +1,6 @@
 """Probe (not collected): the bench C3 CG leg, with per-solve timing and kernel totals."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import bench
 from paper_2511_16340_b200 import warmgp as W

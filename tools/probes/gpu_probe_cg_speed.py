@@ -1,6 +1,6 @@
 """Probe (not collected): where a C3-sized CG iteration spends its time."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from paper_2511_16340_b200 import warmgp as W
 n, d, s = 100000, 16, 64

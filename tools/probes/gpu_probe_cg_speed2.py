@@ -1,6 +1,6 @@
 """Probe (not collected): CG speed before/after appending rows (bench C3 leg)."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from paper_2511_16340_b200 import warmgp as W
 n0, n, d, s = 100000, 101000, 16, 64

@@ -1,6 +1,6 @@
 """Probe (not collected): accuracy/speed of the TC accumulation chunk length (WGP_TC_CH)."""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 from paper_2511_16340_b200 import warmgp as W, configs as Cfg

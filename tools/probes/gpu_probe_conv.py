@@ -1,6 +1,6 @@
 """Probe (not collected): does each precision reach tol 1e-4 on BASELINE-like systems?"""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from paper_2511_16340_b200 import warmgp as W
 

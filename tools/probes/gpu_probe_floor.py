@@ -1,7 +1,7 @@
 """Probe (not collected): attainable-accuracy floor of the fp32 operators on a C2 system.
 For v = H^{-1} b (fp64 CG to 1e-10) report ||H~ v - H v|| / ||b|| per precision."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from paper_2511_16340_b200 import warmgp as W, configs as Cfg
 

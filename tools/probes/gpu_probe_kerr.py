@@ -1,7 +1,7 @@
 """Probe (not collected): per-entry error of the TC operator (V = unit columns isolates the
 kernel map from accumulation), and error vs N for random V."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from paper_2511_16340_b200 import warmgp as W, configs as Cfg
 

@@ -1,6 +1,6 @@
 """Probe (not collected): C3-shaped kernel-matvec time vs RHS width s (V tile bytes)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 from paper_2511_16340_b200 import warmgp as W
 n, d = 101000, 16

@@ -1,6 +1,6 @@
 """Debug aid (not a test): one C3-shaped matvec with per-tile event clocks of CTA 0."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 from paper_2511_16340_b200 import warmgp as W

@@ -1,6 +1,6 @@
 """Debug aid (not a test): one C4-shaped (RBF d=8 s=32, N=100k) matvec with per-tile clocks."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 from paper_2511_16340_b200 import warmgp as W, configs as Cfg
