@@ -7,9 +7,11 @@ initialisations are the previous weights zero-extended (:349-356), per-column SG
 seeds are derive_seed(derive_seed(seed, 0xc0000 + round), col) (:372), divergence
 keeps the initial weights with a one-entry history (solve_best_effort :299-317), and
 the prior values / noise of new rows are drawn in the reference's order (:415-422,
-noise i-major then sample).  The acquisition of configuration 5 is "evaluate the
-posterior samples at 100k random candidates and take each sample's argmax", which
-replaces the reference's propose/select/ascend heuristics (out of scope).
+noise i-major then sample).  The acquisition of configuration 5 evaluates the posterior
+samples at 100k uniform candidates, takes each sample's argmax in every candidate group
+as Adam starting points and ascends them on the device (select_peaks + ascend_peaks,
+thompson.cpp:188-258); the reference's anchored candidate proposal
+(propose_candidates, thompson.cpp:160-185) is replaced by uniform candidates.
 """
 from __future__ import annotations
 

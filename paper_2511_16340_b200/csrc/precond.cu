@@ -174,11 +174,11 @@ __global__ void apply_upper_kernel(const double* __restrict__ L, const double* _
   }
 }
 
-// T[chunk][a][c] = sum_{i in chunk} M[i, a] R[i, c]
+// T[chunk][a][c] = sum_{i in chunk} M[i, a] R[i, c]  (R: s columns of a row-major [n][ld])
 template <typename T>
 __global__ void __launch_bounds__(256) mtr_partial_kernel(const T* __restrict__ M,
-                                                          const T* __restrict__ R, int64_t n,
-                                                          int k, int kpad, int s,
+                                                          const T* __restrict__ R, int64_t ld,
+                                                          int64_t n, int k, int kpad, int s,
                                                           double* __restrict__ part) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RT = 32;
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256) mtr_partial_kernel(const T* __restrict__ 
     }
     for (int e = threadIdx.x; e < RT * s; e += 256) {
       const int64_t i = rb + e / s;
-      sR[e] = i < r1 ? R[i * s + e % s] : T(0);
+      sR[e] = i < r1 ? R[i * ld + e % s] : T(0);
     }
     __syncthreads();
 #pragma unroll
@@ -223,10 +223,10 @@ __global__ void __launch_bounds__(256) mtr_partial_kernel(const T* __restrict__ 
   }
 }
 
-// Z[i, c] = (R[i, c] - sum_a M[i, a] t[a, c]) / shift
+// Z[i, c] = (R[i, c] - sum_a M[i, a] t[a, c]) / shift  (R, Z: s columns of row-major [n][ld])
 template <typename T>
 __global__ void __launch_bounds__(256) woodbury_out_kernel(const T* __restrict__ M,
-                                                           const T* __restrict__ R,
+                                                           const T* __restrict__ R, int64_t ld,
                                                            const double* __restrict__ t, int64_t n,
                                                            int k, int kpad, int s, double inv_shift,
                                                            T* __restrict__ Z) {
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256) woodbury_out_kernel(const T* __restrict__
     const T* Mi = M + i * kpad;
     T acc = T(0);
     for (int a = 0; a < k; ++a) acc = fma(Mi[a], st[a * s + c], acc);
-    Z[e] = (T)(((double)R[e] - (double)acc) * inv_shift);
+    Z[i * ld + c] = (T)(((double)R[i * ld + c] - (double)acc) * inv_shift);
   }
 }
 
@@ -387,24 +387,34 @@ void precond_apply(const Op& op, const PrecondDev& pd, const T* R, T* Z, int s, 
     if (nl > 0) WGP_CUDA(cudaMemcpyAsync(Z, R, sizeof(T) * nl * s, cudaMemcpyDeviceToDevice, st));
     return;
   }
-  WGP_REQUIRE((int64_t)k * s <= 256 * 64, "preconditioner: rank*s too large (%d*%d)", k, s);
   const T* M = (const T*)pd.M64.p;  // solver vectors are fp64 for every precision
   const int nch = ceil_div(pd.n, kChunkRows);
   const int c0 = (int)(pd.r0 / kChunkRows);
-  const size_t smem1 = sizeof(T) * 32 * (pd.kpad + s);
-  if (nl > 0)
-    mtr_partial_kernel<T><<<ceil_div(nl, kChunkRows), 256, smem1, st>>>(
-        M, R, nl, k, (int)pd.kpad, s, work_part + (int64_t)c0 * k * s);
-  dist_allgather_chunks(*op.ctx, work_part, pd.n, (int64_t)k * s, st);
-  sum_partials_kernel<<<ceil_div((int64_t)k * s, 256), 256, 0, st>>>(work_part, nch, k * s, work_t);
-  const size_t smem2 = sizeof(T) * k * s;
-  if (smem2 > 48 * 1024)
-    WGP_CUDA(cudaFuncSetAttribute(woodbury_out_kernel<T>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  if (nl > 0)
-    woodbury_out_kernel<T><<<grid_rows(nl * s), 256, smem2, st>>>(M, R, work_t, nl, k, (int)pd.kpad,
-                                                                  s, 1.0 / pd.shift, Z);
-  WGP_CUDA(cudaGetLastError());
+  // column groups of <= 256*64 / k columns (the per-thread accumulators of mtr_partial);
+  // each column's arithmetic is independent of the grouping
+  const int sg_max = std::max(1, std::min(s, 256 * 64 / k));
+  for (int g0 = 0; g0 < s; g0 += sg_max) {
+    const int sg = std::min(sg_max, s - g0);
+    const size_t smem1 = sizeof(T) * 32 * (pd.kpad + sg);
+    if (smem1 > 48 * 1024)  // rank + columns > 192 (e.g. config 5: rank 100, 129 columns)
+      WGP_CUDA(cudaFuncSetAttribute(mtr_partial_kernel<T>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+    if (nl > 0)
+      mtr_partial_kernel<T><<<ceil_div(nl, kChunkRows), 256, smem1, st>>>(
+          M, R + g0, s, nl, k, (int)pd.kpad, sg, work_part + (int64_t)c0 * k * sg);
+    WGP_CUDA(cudaGetLastError());
+    dist_allgather_chunks(*op.ctx, work_part, pd.n, (int64_t)k * sg, st);
+    sum_partials_kernel<<<ceil_div((int64_t)k * sg, 256), 256, 0, st>>>(work_part, nch, k * sg, work_t);
+    const size_t smem2 = sizeof(T) * k * sg;
+    if (smem2 > 48 * 1024)
+      WGP_CUDA(cudaFuncSetAttribute(woodbury_out_kernel<T>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    if (nl > 0)
+      woodbury_out_kernel<T><<<grid_rows(nl * sg), 256, smem2, st>>>(M, R + g0, s, work_t, nl, k,
+                                                                     (int)pd.kpad, sg, 1.0 / pd.shift,
+                                                                     Z + g0);
+    WGP_CUDA(cudaGetLastError());
+  }
 }
 
 template void precond_apply<double>(const Op&, const PrecondDev&, const double*, double*, int,

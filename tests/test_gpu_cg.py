@@ -171,3 +171,23 @@ def test_exact_solve_matches_oracle(W, O, n, kind):
     assert np.linalg.norm(got - ref) <= 1e-8 * np.linalg.norm(ref)
     two = W.exact_solve(op, np.column_stack([y, 2 * y]))
     assert np.array_equal(two[:, 0], got) and np.allclose(two[:, 1], 2 * got, rtol=1e-12)
+
+
+@pytest.mark.parametrize("s", [65, 129, 200])
+def test_cg_wide_batches_equal_single_columns(W, s):
+    """solve_many over many columns (config 5: y + 128 samples) with a rank-100 preconditioner
+    equals the per-column solves bitwise: the Woodbury apply's shared-memory staging grows with
+    rank + s and must stay correct past the 48 KB default."""
+    rng = np.random.default_rng(s)
+    n = 1500
+    X = rng.random((n, 2))
+    B = np.asfortranarray(rng.standard_normal((n, s)))
+    h = W.KernelHyperparams(0.3, 1.0, 1e-3, W.MATERN32)
+    op = W.KernelOperator(h, X, precision=W.F64)
+    cfg = W.SolverConfig(method=W.CG, tolerance=1e-2, max_iters=5, precond_rank=100, precond_shift=1e-6)
+    res = W.solve_many(op, B, [W.Initialization.cold()] * s, cfg)
+    for c in (0, s // 2, s - 1):
+        one = W.solve_many(op, np.asfortranarray(B[:, c:c + 1]), [W.Initialization.cold()], cfg)[0]
+        assert np.isfinite(res[c].v).all()
+        assert np.array_equal(res[c].v, one.v), c
+        assert res[c].residual_history == one.residual_history

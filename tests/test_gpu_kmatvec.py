@@ -170,3 +170,19 @@ def test_tf32_precision_mode(W):
     ref = W.KernelOperator(h, X, precision=W.F64).kmatvec(V)
     got = W.KernelOperator(h, X, precision=W.TF32).kmatvec(V)
     assert colrel(got, ref) <= 5e-3
+
+
+@pytest.mark.parametrize("n,s", [(130, 3), (700, 64), (9000, 17), (33001, 100)])
+def test_tc_stream_k_pieces(W, n, s):
+    """The persistent stream-K schedule cuts row blocks across CTAs (a CTA range of fewer tiles
+    than one row block's sweep gives up to four pieces per row block at n = 9000; tiny n runs
+    fewer than 148 CTAs): every piece lands in its own partial slot and the reduction adds
+    exactly the covering pieces -- checked against the fp64 operator, with the diagonal."""
+    rng = np.random.default_rng(n)
+    X = rng.random((n, 7))
+    V = rng.standard_normal((n, s))
+    for kind in (0, 1):
+        h = W.KernelHyperparams(0.4, 1.1, 0.05, kind)
+        ref = W.KernelOperator(h, X, precision=W.F64).kmatvec(V)
+        got = W.KernelOperator(h, X, precision=W.F32_3XTF32).kmatvec(V)
+        assert colrel(got, ref) <= 2e-5, (n, s, kind)
