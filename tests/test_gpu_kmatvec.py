@@ -173,11 +173,10 @@ def test_tf32_precision_mode(W):
 
 
 @pytest.mark.parametrize("n,s", [(130, 3), (700, 64), (9000, 17), (33001, 100)])
-def test_tc_stream_k_pieces(W, n, s):
-    """The persistent stream-K schedule cuts row blocks across CTAs (a CTA range of fewer tiles
-    than one row block's sweep gives up to four pieces per row block at n = 9000; tiny n runs
-    fewer than 148 CTAs): every piece lands in its own partial slot and the reduction adds
-    exactly the covering pieces -- checked against the fp64 operator, with the diagonal."""
+def test_tc_split_grids(W, n, s):
+    """Grid shapes from a single CTA (n = 130) through several j-splits per row block (n = 9000,
+    33001) and a ragged two-chunk RHS (s = 100): every split's partial slot is written and the
+    reduction adds them -- checked against the fp64 operator, diagonal included."""
     rng = np.random.default_rng(n)
     X = rng.random((n, 7))
     V = rng.standard_normal((n, s))
