@@ -352,7 +352,7 @@ def run_ours(args):
             "config": {"workload": "C3 kernel-matvec (BASELINE configs[2])", "n": n, "d": DIM, "s": S,
                        "kernel": "matern32", "lengthscale": LS, "noise_var": NOISE_VAR,
                        "rows_per_rank": r1 - r0, "l2": "flushed (256 MiB memset) before each step"},
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": 4 * args.steps,  # colscale + split_v + kmatvec_tc + reduce_splits per step
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": 5 * args.steps,  # colmax + colscale_finish + split_v + kmatvec_tc + reduce_splits per step
             "cg_warm_vs_cold": cg,
             "clocks": clk.summary(), "wall_s": t_wall,
             "step_ms_min": float(np.min(ms)), "step_ms_max": float(np.max(ms)),
@@ -366,7 +366,7 @@ def run_ours(args):
 
 # dram bytes (read + write) per launch of tc::kmatvec_tc_kernel on this workload, from the
 # committed ncu --set full capture (profiles/r01_kmatvec_tc_metrics.json)
-TRAFFIC_BYTES = 120.68e6
+TRAFFIC_BYTES = 117.28e6
 
 
 def main():
