@@ -52,6 +52,7 @@ inline void check(wgp_status st, int iterations = 0) {
     case WGP_NOT_SPD: throw NotSpdError(msg);
     case WGP_DIVERGED: throw DivergenceError(msg, iterations);
     case WGP_OOM: throw std::bad_alloc();
+    case WGP_RUNTIME_ERROR: throw std::runtime_error(msg);
     default: throw CudaError(msg);
   }
 }
@@ -367,6 +368,46 @@ inline AscendResult ascend_peaks(const KernelOperator& H, const std::vector<RffP
   return r;
 }
 
+// ---------------------------------------------------------------- analysis (analysis.hpp)
+// exact_solve (analysis.cpp:15-26): dense fp64 Cholesky of the operator's H on the device.
+inline Vector exact_solve(const KernelOperator& H, const Vector& b) {
+  if ((int64_t)b.size() != H.size()) throw std::invalid_argument("exact_solve: length mismatch");
+  Vector x(b.size());
+  check(wgp_exact_solve(H.get(), b.data(), (int64_t)b.size(), 1, x.data(), (int64_t)x.size()));
+  return x;
+}
+
+struct MllResult {  // analysis.hpp:42-45
+  double value = 0.0;
+  double grad[3] = {0.0, 0.0, 0.0};  // d/d(log l, log s_f, log sigma_n)
+};
+// mll (analysis.cpp:99-139) of y under the operator's rows at hyp (the operator's own kind).
+inline MllResult mll(const KernelOperator& H, const Vector& y, const KernelHyperparams& hyp) {
+  if ((int64_t)y.size() != H.size()) throw std::invalid_argument("mll: X rows != y length");
+  const double h3[3] = {hyp.lengthscale, hyp.signal_scale, hyp.noise_scale};
+  MllResult r;
+  check(wgp_mll(H.get(), y.data(), h3, &r.value, r.grad));
+  return r;
+}
+// optimize_mll (analysis.cpp:141-182): best hyperparameters seen by the Adam ascent.
+inline KernelHyperparams optimize_mll(const KernelOperator& H, const Vector& y,
+                                      const KernelHyperparams& init, int steps, double step_size) {
+  if ((int64_t)y.size() != H.size()) throw std::invalid_argument("mll: X rows != y length");
+  const double h3[3] = {init.lengthscale, init.signal_scale, init.noise_scale};
+  double out[3];
+  check(wgp_optimize_mll(H.get(), y.data(), h3, steps, step_size, out));
+  KernelHyperparams r = init;
+  r.lengthscale = out[0];
+  r.signal_scale = out[1];
+  r.noise_scale = out[2];
+  return r;
+}
+// median_heuristic_lengthscale (analysis.cpp:184-203)
+inline double median_heuristic_lengthscale(const Matrix& X, uint64_t seed = 0) {
+  return wgp_median_heuristic_lengthscale(X.data.data(), X.rows, X.rows > 0 ? X.rows : 1, (int)X.cols,
+                                          seed);
+}
+
 #ifdef WARMGP_GPU_EIGEN
 // ---------------------------------------------------------------- Eigen overloads
 // For the reference build (Eigen::MatrixXd is column-major fp64, like Matrix): the call
@@ -404,6 +445,24 @@ inline SolveResult solve(const KernelOperator& H, const Eigen::VectorXd& b, cons
 }
 inline Eigen::MatrixXd operator*(const KernelOperator& H, const Eigen::MatrixXd& V) {
   return to_eigen(H * to_gpu(V));
+}
+// analysis.hpp signatures: mll(X, y, hyp) / optimize_mll(X, y, init, steps, step) on a
+// temporary fp64 device operator over X
+inline MllResult mll(Context& ctx, const Eigen::MatrixXd& X, const Eigen::VectorXd& y,
+                     const KernelHyperparams& hyp) {
+  KernelOperator H(ctx, to_gpu(X), hyp, Precision::F64);
+  return mll(H, to_gpu(y), hyp);
+}
+inline KernelHyperparams optimize_mll(Context& ctx, const Eigen::MatrixXd& X, const Eigen::VectorXd& y,
+                                      const KernelHyperparams& init, int steps, double step_size) {
+  KernelOperator H(ctx, to_gpu(X), init, Precision::F64);
+  return optimize_mll(H, to_gpu(y), init, steps, step_size);
+}
+inline Eigen::VectorXd exact_solve(const KernelOperator& H, const Eigen::VectorXd& b) {
+  return to_eigen(exact_solve(H, to_gpu(b)));
+}
+inline double median_heuristic_lengthscale(const Eigen::MatrixXd& X, uint64_t seed = 0) {
+  return median_heuristic_lengthscale(to_gpu(X), seed);
 }
 #endif  // WARMGP_GPU_EIGEN
 

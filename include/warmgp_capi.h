@@ -45,6 +45,7 @@ typedef enum {
   WGP_CUDA_ERROR = 4,
   WGP_NCCL_ERROR = 5,
   WGP_OOM = 6,
+  WGP_RUNTIME_ERROR = 7,    /* std::runtime_error (optimize_mll, analysis.cpp:159,173) */
 } wgp_status;
 
 typedef enum { WGP_MATERN32 = 0, WGP_RBF = 1 } wgp_kernel;
@@ -197,6 +198,25 @@ void wgp_rng_normal_fill(uint64_t* state, int64_t n, double scale, double* out);
  * H on the device (materialised once; n <= 60000).  B, X: n x s column-major.  A
  * non-positive pivot returns WGP_NOT_SPD (the reference's LLT failure).  Unsharded only. */
 wgp_status wgp_exact_solve(wgp_op* op, const double* B, int64_t ldb, int s, double* X, int64_t ldx);
+
+/* mll (analysis.cpp:99-139): marginal log-likelihood of y (n) under the operator's rows and
+ * kernel, at hyperparameters hyp3 = {lengthscale, signal_scale, noise_scale} (nullable: the
+ * operator's own), and its gradient with respect to (log l, log s_f, log sigma_n).  Dense
+ * fp64 on the device (H factored, [alpha | H^{-1}] by blocked substitution; n <= 30000).
+ * Matern-3/2 as the reference; the RBF analogue for RBF operators.  Not SPD -> WGP_NOT_SPD.
+ * Unsharded only. */
+wgp_status wgp_mll(wgp_op* op, const double* y, const double* hyp3, double* value, double* grad3);
+/* optimize_mll (analysis.cpp:141-182): Adam (0.9 / 0.999 / 1e-8) on the log-parameters from
+ * init3 (nullable: the operator's), clamped to [1e-3, 1e3] x [1e-3, 1e3] x [1e-4, 1e2],
+ * `steps` steps of `step_size`; out3 = the best hyperparameters seen.  A non-finite MLL
+ * returns WGP_RUNTIME_ERROR.  The operator itself is not modified. */
+wgp_status wgp_optimize_mll(wgp_op* op, const double* y, const double* init3, int steps,
+                            double step_size, double* out3);
+/* median_heuristic_lengthscale (analysis.cpp:184-203): median pairwise distance of 256 rows
+ * drawn with Rng(derive_seed(seed, 0x6d656469)).uniform_index(n); X: n x dim column-major
+ * (leading dimension ldx).  Host computation (256 x 256 distances). */
+double wgp_median_heuristic_lengthscale(const double* X, int64_t n, int64_t ldx, int dim,
+                                        uint64_t seed);
 
 /* grad_posterior (sampling.cpp:77-87): gradients at m points of the posterior samples
  * prior_s + K(., X) W[:, s] (the operator's rows as training inputs; priors as in

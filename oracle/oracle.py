@@ -153,6 +153,9 @@ def _declare(L):
         "wgo_solve_many": (C.c_int, [P, P, I64, C.c_int, P, I64, P, P, P, P, P, P, P, P]),
         "wgo_exact_solve": (C.c_int, [P, I64, P, P]),
         "wgo_rkhs_distance": (D, [P, P, P]),
+        "wgo_mll": (C.c_int, [P, P, I64, I64, P, P, P]),
+        "wgo_optimize_mll": (C.c_int, [P, P, I64, I64, P, C.c_int, D, P]),
+        "wgo_median_heuristic_lengthscale": (D, [P, I64, I64, C.c_uint64]),
         "wgo_sample_prior": (C.c_int, [P, I64, I64, C.c_uint64, P, P, P]),
         "wgo_eval_prior": (C.c_int, [P, P, P, I64, I64, D, P, I64, P]),
         "wgo_build_sample_rhs": (C.c_int, [P, P, P, I64, I64, D, P, I64, D, C.c_uint64, P]),
@@ -546,6 +549,41 @@ def exact_solve(H, b) -> np.ndarray:
 def rkhs_distance(H, v_init, v_exact) -> float:
     op = _as_op(H)
     return lib().wgo_rkhs_distance(op.ref, _ptr(_f64(v_init)), _ptr(_f64(v_exact)))
+
+
+@dataclass
+class MllResult:
+    """warmgp::MllResult (analysis.hpp:42-45)."""
+    value: float
+    grad: np.ndarray  # d/d(log l, log s_f, log sigma_n)
+
+
+def mll(X, y, h: KernelHyperparams) -> MllResult:
+    """mll (analysis.cpp:99-139)."""
+    X = _f64(X)
+    y = _f64(y).ravel()
+    if X.shape[0] != y.shape[0]:
+        raise ValueError("mll: X rows != y length")
+    val = C.c_double(0.0)
+    g = np.zeros(3)
+    _check(lib().wgo_mll(_hyp(h), _ptr(X), X.shape[0], X.shape[1], _ptr(y), C.byref(val), _ptr(g)))
+    return MllResult(val.value, g)
+
+
+def optimize_mll(X, y, init: KernelHyperparams, steps: int, step_size: float) -> KernelHyperparams:
+    """optimize_mll (analysis.cpp:141-182)."""
+    X = _f64(X)
+    y = _f64(y).ravel()
+    out = Hyp()
+    _check(lib().wgo_optimize_mll(_hyp(init), _ptr(X), X.shape[0], X.shape[1], _ptr(y), steps,
+                                  step_size, C.byref(out)))
+    return KernelHyperparams(out.lengthscale, out.signal_scale, out.noise_scale, out.kind)
+
+
+def median_heuristic_lengthscale(X, seed: int = 0) -> float:
+    """median_heuristic_lengthscale (analysis.cpp:184-203)."""
+    X = _f64(X)
+    return lib().wgo_median_heuristic_lengthscale(_ptr(X), X.shape[0], X.shape[1], seed & (2**64 - 1))
 
 
 # ----------------------------------------------------------------- sampling

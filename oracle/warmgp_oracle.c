@@ -910,6 +910,168 @@ double wgo_rkhs_distance(const wgo_op* op, const double* v_init, const double* v
   return sqrt(q > 0.0 ? q : 0.0);
 }
 
+/* mll_with_dist, analysis.cpp:99-131.  D: n x n distances (pairwise_distances). */
+static int mll_with_dist(const wgo_hyp* h, const double* Dm, int64_t n, const double* y,
+                         double* value, double* grad3) {
+  const double s2 = h->signal_scale * h->signal_scale;
+  const double sn2 = h->noise_scale * h->noise_scale;
+  const double l = h->lengthscale;
+  const size_t nn = (size_t)(n * n);
+  double* K = (double*)malloc(sizeof(double) * nn);
+  double* L = (double*)malloc(sizeof(double) * nn);
+  for (size_t t = 0; t < nn; ++t) {
+    const double r = Dm[t];
+    if (h->kind == WGO_RBF) {
+      K[t] = s2 * exp(-0.5 * (r / l) * (r / l));
+    } else {
+      const double z = r * (kSqrt3 / l); /* :103 */
+      K[t] = s2 * (1.0 + z) * exp(-z);
+    }
+    L[t] = K[t];
+  }
+  for (int64_t i = 0; i < n; ++i) L[i * n + i] += sn2; /* :106 */
+  if (cholesky_lower(L, n) != WGO_OK) {
+    free(K);
+    free(L);
+    return fail(WGO_NOT_SPD, "mll: covariance not SPD at these hyperparameters");
+  }
+  double* alpha = (double*)malloc(sizeof(double) * (size_t)n);
+  memcpy(alpha, y, sizeof(double) * (size_t)n);
+  cholesky_solve(L, n, alpha); /* :112 */
+  double logdet = 0.0;
+  for (int64_t i = 0; i < n; ++i) logdet += log(L[i * n + i]);
+  logdet *= 2.0;
+  *value = -0.5 * dot(y, alpha, n) - 0.5 * logdet - 0.5 * (double)n * 1.8378770664093454836;
+  /* grad_j = 0.5 tr((alpha alpha^T - H^{-1}) dH_j), H^{-1} column by column (:121-130) */
+  double* e = (double*)malloc(sizeof(double) * (size_t)n);
+  double g0 = 0.0, g1 = 0.0, tr = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    memset(e, 0, sizeof(double) * (size_t)n);
+    e[j] = 1.0;
+    cholesky_solve(L, n, e); /* column j of H^{-1} */
+    for (int64_t i = 0; i < n; ++i) {
+      const double a = alpha[i] * alpha[j] - e[i];
+      const double r = Dm[j * n + i];
+      const double rho = r / l;
+      const double dkl = h->kind == WGO_RBF ? K[j * n + i] * rho * rho
+                                            : 3.0 * s2 * rho * rho * exp(-kSqrt3 * rho);
+      g0 += a * dkl;
+      g1 += a * 2.0 * K[j * n + i];
+    }
+    tr += alpha[j] * alpha[j] - e[j];
+  }
+  grad3[0] = 0.5 * g0;
+  grad3[1] = 0.5 * g1;
+  grad3[2] = 0.5 * tr * 2.0 * sn2;
+  free(e);
+  free(alpha);
+  free(K);
+  free(L);
+  return WGO_OK;
+}
+
+int wgo_mll(const wgo_hyp* h, const double* X, int64_t n, int64_t d, const double* y, double* value,
+            double* grad3) { /* analysis.cpp:135-139 */
+  int st = wgo_hyp_validate(h);
+  if (st) return st;
+  if (n < 1) return fail(WGO_INVALID_ARGUMENT, "mll: X rows != y length");
+  double* Dm = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  wgo_pairwise_distances(X, n, X, n, d, Dm);
+  st = mll_with_dist(h, Dm, n, y, value, grad3);
+  free(Dm);
+  return st;
+}
+
+int wgo_optimize_mll(const wgo_hyp* init, const double* X, int64_t n, int64_t d, const double* y,
+                     int steps, double step_size, wgo_hyp* out) { /* analysis.cpp:141-182 */
+  int st = wgo_hyp_validate(init);
+  if (st) return st;
+  double* Dm = (double*)malloc(sizeof(double) * (size_t)(n * n));
+  wgo_pairwise_distances(X, n, X, n, d, Dm);
+  double th[3] = {log(init->lengthscale), log(init->signal_scale), log(init->noise_scale)};
+  const double lo[3] = {log(1e-3), log(1e-3), log(1e-4)}, hi[3] = {log(1e3), log(1e3), log(1e2)};
+  wgo_hyp cur_h = {init->kind, exp(th[0]), exp(th[1]), exp(th[2])};
+  double val, g[3];
+  st = mll_with_dist(&cur_h, Dm, n, y, &val, g);
+  if (st) {
+    free(Dm);
+    return st;
+  }
+  if (!isfinite(val)) {
+    free(Dm);
+    return fail(WGO_RUNTIME_ERROR, "optimize_mll: non-finite MLL at the initial hyperparameters");
+  }
+  double best[3] = {th[0], th[1], th[2]}, best_val = val;
+  double m[3] = {0, 0, 0}, v[3] = {0, 0, 0};
+  for (int t = 1; t <= steps; ++t) {
+    const double bc1 = 1.0 - pow(0.9, t), bc2 = 1.0 - pow(0.999, t);
+    for (int k = 0; k < 3; ++k) {
+      m[k] = 0.9 * m[k] + (1.0 - 0.9) * g[k];
+      v[k] = 0.999 * v[k] + (1.0 - 0.999) * (g[k] * g[k]);
+      const double step = (m[k] / bc1) / (sqrt(v[k] / bc2) + 1e-8);
+      double x = th[k] + step_size * step;
+      th[k] = x < lo[k] ? lo[k] : (x > hi[k] ? hi[k] : x);
+    }
+    cur_h.lengthscale = exp(th[0]);
+    cur_h.signal_scale = exp(th[1]);
+    cur_h.noise_scale = exp(th[2]);
+    st = mll_with_dist(&cur_h, Dm, n, y, &val, g);
+    if (st) {
+      free(Dm);
+      return st;
+    }
+    if (!isfinite(val)) {
+      free(Dm);
+      return fail(WGO_RUNTIME_ERROR, "optimize_mll: non-finite MLL at step %d (lengthscale %g)", t,
+                  exp(th[0]));
+    }
+    if (val > best_val) {
+      best_val = val;
+      best[0] = th[0];
+      best[1] = th[1];
+      best[2] = th[2];
+    }
+  }
+  free(Dm);
+  out->kind = init->kind;
+  out->lengthscale = exp(best[0]);
+  out->signal_scale = exp(best[1]);
+  out->noise_scale = exp(best[2]);
+  return WGO_OK;
+}
+
+static int cmp_double(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+double wgo_median_heuristic_lengthscale(const double* X, int64_t n, int64_t d, uint64_t seed) {
+  const int64_t cap = n < 256 ? n : 256; /* analysis.cpp:184-203 */
+  double* sub = (double*)malloc(sizeof(double) * (size_t)(cap * d + 1));
+  wgo_rng rng = {wgo_derive_seed(seed, 0x6d656469ULL)};
+  for (int64_t i = 0; i < cap; ++i) {
+    const int64_t r = (int64_t)wgo_rng_uniform_index(&rng, (uint64_t)n);
+    for (int64_t k = 0; k < d; ++k) sub[k * cap + i] = X[k * n + r];
+  }
+  double* Dm = (double*)malloc(sizeof(double) * (size_t)(cap * cap + 1));
+  wgo_pairwise_distances(sub, cap, sub, cap, d, Dm);
+  const int64_t cnt = cap * (cap - 1) / 2;
+  double* vals = (double*)malloc(sizeof(double) * (size_t)(cnt + 1));
+  int64_t q = 0;
+  for (int64_t j = 0; j < cap; ++j)
+    for (int64_t i = j + 1; i < cap; ++i) vals[q++] = Dm[j * cap + i];
+  double med = 1.0;
+  if (cnt > 0) {
+    /* nth_element(size/2) == the (size/2)-th order statistic */
+    qsort(vals, (size_t)cnt, sizeof(double), cmp_double);
+    med = vals[cnt / 2] > 0.0 ? vals[cnt / 2] : 1.0;
+  }
+  free(vals);
+  free(Dm);
+  free(sub);
+  return med;
+}
+
 /* ======================= sampling.cpp ======================= */
 
 int wgo_sample_prior(const wgo_hyp* h, int64_t dim, int64_t F, uint64_t seed, double* Omega,

@@ -35,6 +35,7 @@ enum {
   WGO_INVALID_ARGUMENT = 1, /* std::invalid_argument */
   WGO_NOT_SPD = 2,          /* warmgp::NotSpdError   types.hpp:15-18 */
   WGO_DIVERGED = 3,         /* warmgp::DivergenceError types.hpp:21-26 */
+  WGO_RUNTIME_ERROR = 7,    /* std::runtime_error (optimize_mll, analysis.cpp:159,173) */
 };
 const char* wgo_last_error(void);
 
@@ -173,6 +174,18 @@ int wgo_solve_many(const wgo_op* op, const double* B, int64_t s, int warm, const
 int wgo_exact_solve(const double* H, int64_t n, const double* b, double* x);
 /* rkhs_distance, analysis.cpp:28-32 */
 double wgo_rkhs_distance(const wgo_op* op, const double* v_init, const double* v_exact);
+/* mll, analysis.cpp:99-139 (mll_with_dist on pairwise_distances(X, X)): value and gradient
+ * with respect to (log l, log s_f, log sigma_n).  Matern-3/2 as the reference; kind == WGO_RBF
+ * uses the RBF analogue (dK/dlog l = K r^2 / l^2).  X: n x d col-major.  Not SPD ->
+ * WGO_NOT_SPD. */
+int wgo_mll(const wgo_hyp* h, const double* X, int64_t n, int64_t d, const double* y, double* value,
+            double* grad3);
+/* optimize_mll, analysis.cpp:141-182: Adam on the log-parameters inside the soft box, best
+ * seen returned; a non-finite MLL -> WGO_RUNTIME_ERROR (std::runtime_error). */
+int wgo_optimize_mll(const wgo_hyp* init, const double* X, int64_t n, int64_t d, const double* y,
+                     int steps, double step_size, wgo_hyp* out);
+/* median_heuristic_lengthscale, analysis.cpp:184-203 */
+double wgo_median_heuristic_lengthscale(const double* X, int64_t n, int64_t d, uint64_t seed);
 
 /* ---------------- sampling.hpp / sampling.cpp ---------------- */
 /* sample_prior, sampling.cpp:14-35.  Omega: F x dim col-major, phases/amps: F.

@@ -3,9 +3,11 @@
 // Every entry point converts C++ exceptions into a wgp_status plus a thread-local
 // message; no exception crosses the ABI.  Host buffers use the reference's Eigen layout
 // (column-major fp64); they are converted to the device layout on the GPU.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <vector>
 
 #include "rng.h"
 #include "solvers.h"
@@ -25,6 +27,8 @@ void throw_error(wgp_status code, const char* fmt, ...) {
 
 void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major);
 bool exact_solve_dev(const Op& op, double* Y, int s, cudaStream_t st);
+bool mll_dev(const Op& op, double l, double sf, double sn, const double* y, double* value,
+             double* grad3, cudaStream_t st);
 void launch_grad_posterior(const Op& op, const double* Om, const double* ph, const double* am,
                            int F, double coeff, const double* W, const double* Xs,
                            const int* sidx, int64_t m, double* G, cudaStream_t st);
@@ -561,6 +565,97 @@ wgp_status wgp_exact_solve(wgp_op* op, const double* B, int64_t ldb, int s, doub
                                s, cudaMemcpyDeviceToHost, st));
     WGP_CUDA(cudaStreamSynchronize(st));
   });
+}
+
+wgp_status wgp_mll(wgp_op* op, const double* y, const double* hyp3, double* value, double* grad3) {
+  return guard([&] {
+    WGP_REQUIRE(op && y && value && grad3, "wgp_mll: null argument");
+    WGP_REQUIRE(op->ctx->world == 1, "mll: unsharded operators only");
+    WGP_REQUIRE(op->n >= 1, "mll: X rows != y length");
+    set_device(*op->ctx);
+    const double l = hyp3 ? hyp3[0] : op->lengthscale, sf = hyp3 ? hyp3[1] : op->signal_scale,
+                 sn = hyp3 ? hyp3[2] : op->noise_scale;
+    if (!mll_dev(*op, l, sf, sn, y, value, grad3, op->ctx->stream))
+      throw_error(WGP_NOT_SPD, "mll: covariance not SPD at these hyperparameters");
+  });
+}
+
+wgp_status wgp_optimize_mll(wgp_op* op, const double* y, const double* init3, int steps,
+                            double step_size, double* out3) {
+  return guard([&] {
+    WGP_REQUIRE(op && y && out3, "wgp_optimize_mll: null argument");
+    WGP_REQUIRE(op->ctx->world == 1, "optimize_mll: unsharded operators only");
+    WGP_REQUIRE(steps >= 0, "optimize_mll: negative step count");
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    const double h0[3] = {init3 ? init3[0] : op->lengthscale, init3 ? init3[1] : op->signal_scale,
+                          init3 ? init3[2] : op->noise_scale};
+    WGP_REQUIRE(h0[0] > 0.0 && h0[1] > 0.0 && h0[2] > 0.0,
+                "KernelHyperparams: all scales must be positive");
+    // analysis.cpp:141-182: Adam on theta = log(l, s_f, sigma_n) inside the soft box
+    double th[3] = {std::log(h0[0]), std::log(h0[1]), std::log(h0[2])};
+    const double lo[3] = {std::log(1e-3), std::log(1e-3), std::log(1e-4)};
+    const double hi[3] = {std::log(1e3), std::log(1e3), std::log(1e2)};
+    double val = 0.0, g[3];
+    auto eval = [&](const double* t) {
+      if (!mll_dev(*op, std::exp(t[0]), std::exp(t[1]), std::exp(t[2]), y, &val, g, st))
+        throw_error(WGP_NOT_SPD, "mll: covariance not SPD at these hyperparameters");
+    };
+    eval(th);
+    if (!std::isfinite(val))
+      throw_error(WGP_RUNTIME_ERROR, "optimize_mll: non-finite MLL at the initial hyperparameters");
+    double best[3] = {th[0], th[1], th[2]}, best_val = val;
+    double m[3] = {0.0, 0.0, 0.0}, v[3] = {0.0, 0.0, 0.0};
+    for (int t = 1; t <= steps; ++t) {
+      const double bc1 = 1.0 - std::pow(0.9, t), bc2 = 1.0 - std::pow(0.999, t);
+      for (int k = 0; k < 3; ++k) {
+        m[k] = 0.9 * m[k] + (1.0 - 0.9) * g[k];
+        v[k] = 0.999 * v[k] + (1.0 - 0.999) * (g[k] * g[k]);
+        const double step = (m[k] / bc1) / (std::sqrt(v[k] / bc2) + 1e-8);
+        th[k] = std::min(std::max(th[k] + step_size * step, lo[k]), hi[k]);
+      }
+      eval(th);
+      if (!std::isfinite(val))
+        throw_error(WGP_RUNTIME_ERROR, "optimize_mll: non-finite MLL at step %d (lengthscale %g)", t,
+                    std::exp(th[0]));
+      if (val > best_val) {
+        best_val = val;
+        for (int k = 0; k < 3; ++k) best[k] = th[k];
+      }
+    }
+    for (int k = 0; k < 3; ++k) out3[k] = std::exp(best[k]);
+  });
+}
+
+double wgp_median_heuristic_lengthscale(const double* X, int64_t n, int64_t ldx, int dim,
+                                        uint64_t seed) {
+  if (!X || n < 1 || dim < 1 || ldx < n) return 1.0;
+  const int64_t cap = std::min<int64_t>(n, 256);  // analysis.cpp:184-203
+  std::vector<double> sub((size_t)(cap * dim));
+  Rng rng{derive_seed(seed, 0x6d656469ULL)};
+  for (int64_t i = 0; i < cap; ++i) {
+    const int64_t r = (int64_t)rng.uniform_index((uint64_t)n);
+    for (int k = 0; k < dim; ++k) sub[(size_t)(k * cap + i)] = X[k * ldx + r];
+  }
+  // pairwise_distances (kernel.cpp:39-46): sqrt(max(|a|^2 + |b|^2 - 2 a.b, 0))
+  std::vector<double> sq((size_t)cap, 0.0);
+  for (int k = 0; k < dim; ++k)
+    for (int64_t i = 0; i < cap; ++i) sq[(size_t)i] += sub[(size_t)(k * cap + i)] * sub[(size_t)(k * cap + i)];
+  std::vector<double> vals;
+  vals.reserve((size_t)(cap * (cap - 1) / 2));
+  for (int64_t j = 0; j < cap; ++j)
+    for (int64_t i = j + 1; i < cap; ++i) {
+      double gsum = 0.0;
+      for (int k = 0; k < dim; ++k) gsum += sub[(size_t)(k * cap + i)] * sub[(size_t)(k * cap + j)];
+      double d2 = -2.0 * gsum;
+      d2 += sq[(size_t)i];
+      d2 += sq[(size_t)j];
+      vals.push_back(std::sqrt(d2 > 0.0 ? d2 : 0.0));
+    }
+  if (vals.empty()) return 1.0;
+  std::nth_element(vals.begin(), vals.begin() + vals.size() / 2, vals.end());
+  const double med = vals[vals.size() / 2];
+  return med > 0.0 ? med : 1.0;
 }
 
 // upload S priors (prior-major, each F x dim column-major) and W (n x S column-major)

@@ -48,6 +48,7 @@ EXPORTS = (
     "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
     "wgp_rng_normal_fill", "wgp_kernel_timer_enable", "wgp_kernel_timer_read", "wgp_rff_eval_fast",
     "wgp_exact_solve", "wgp_grad_posterior", "wgp_ascend_peaks",
+    "wgp_mll", "wgp_optimize_mll", "wgp_median_heuristic_lengthscale",
 )
 
 
@@ -139,6 +140,9 @@ def _declare(L):
         "wgp_rng_normal_fill": (None, [P, I64, D, P]),
         "wgp_kernel_timer_enable": (None, [C.c_int]),
         "wgp_exact_solve": (C.c_int, [P, P, I64, C.c_int, P, I64]),
+        "wgp_mll": (C.c_int, [P, P, P, P, P]),
+        "wgp_optimize_mll": (C.c_int, [P, P, P, C.c_int, D, P]),
+        "wgp_median_heuristic_lengthscale": (D, [P, I64, I64, C.c_int, C.c_uint64]),
         "wgp_grad_posterior": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, P, I64, P, I64, P, I64]),
         "wgp_ascend_peaks": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, P, C.c_int, C.c_int, D, P, P]),
         "wgp_kernel_timer_read": (C.c_int, [P, P]),
@@ -634,6 +638,56 @@ def exact_solve(op: KernelOperator, b) -> np.ndarray:
     Xo = np.zeros((n, s), order="F")
     _check(lib().wgp_exact_solve(op._h, _ptr(B), n, s, _ptr(Xo), n))
     return Xo[:, 0] if vec else Xo
+
+
+@dataclass
+class MllResult:
+    """warmgp::MllResult (analysis.hpp:42-45): value and d/d(log l, log s_f, log sigma_n)."""
+    value: float
+    grad: np.ndarray
+
+
+def _mll_op(X_or_op, hyp):
+    if isinstance(X_or_op, KernelOperator):
+        return X_or_op
+    if hyp is None:
+        raise ValueError("mll: hyperparameters required with raw inputs")
+    return KernelOperator(hyp, X_or_op, precision=F64)
+
+
+def mll(X_or_op, y, hyp: KernelHyperparams | None = None) -> MllResult:
+    """mll (analysis.cpp:99-139) on the device: X_or_op is the inputs (n x d; a temporary fp64
+    operator is built) or an operator (its rows); hyp defaults to the operator's.  Matern-3/2
+    as the reference (RBF analogue for RBF operators).  NotSpdError if H is not SPD."""
+    op = _mll_op(X_or_op, hyp)
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64).ravel())
+    if y.shape[0] != op.n:
+        raise ValueError("mll: X rows != y length")
+    h3 = None if hyp is None else np.array([hyp.lengthscale, hyp.signal_scale, hyp.noise_scale])
+    val = C.c_double(0.0)
+    g = np.zeros(3)
+    _check(lib().wgp_mll(op._h, _ptr(y), _ptr(h3), C.byref(val), _ptr(g)))
+    return MllResult(val.value, g)
+
+
+def optimize_mll(X_or_op, y, init_hyp: KernelHyperparams, steps: int, step_size: float) -> KernelHyperparams:
+    """optimize_mll (analysis.cpp:141-182): Adam on the log-parameters (device MLL per step);
+    returns the best hyperparameters seen.  RuntimeError on a non-finite MLL."""
+    op = _mll_op(X_or_op, init_hyp)
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64).ravel())
+    if y.shape[0] != op.n:
+        raise ValueError("optimize_mll: X rows != y length")
+    h3 = np.array([init_hyp.lengthscale, init_hyp.signal_scale, init_hyp.noise_scale])
+    out = np.zeros(3)
+    _check(lib().wgp_optimize_mll(op._h, _ptr(y), _ptr(h3), int(steps), float(step_size), _ptr(out)))
+    return KernelHyperparams(float(out[0]), float(out[1]), float(out[2]), init_hyp.kind)
+
+
+def median_heuristic_lengthscale(X, seed: int = 0) -> float:
+    """median_heuristic_lengthscale (analysis.cpp:184-203)."""
+    X = _f64(X)
+    return float(lib().wgp_median_heuristic_lengthscale(_ptr(X), X.shape[0], max(X.shape[0], 1), X.shape[1],
+                                                        seed & (2**64 - 1)))
 
 
 def _stack_priors(priors):

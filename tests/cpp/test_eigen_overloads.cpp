@@ -45,6 +45,21 @@ int main() {
   std::vector<g::Initialization> inits = {g::warm(g::to_eigen(r.v)), g::Initialization::warm(r.v)};
   const auto rs = g::solve_many(H, B, inits, cfg);
   if (rs.size() != 2 || !rs[0].converged || !rs[1].converged) { std::printf("solve_many failed\n"); return 1; }
+  // analysis.hpp overloads: exact_solve, mll / optimize_mll on Eigen values
+  g::KernelOperator H0 = g::gram_matrix(ctx, X, hyp);
+  const Eigen::VectorXd xs = g::exact_solve(H0, b);
+  Eigen::MatrixXd Xs1(n, 1);
+  for (int i = 0; i < n; ++i) Xs1(i, 0) = xs(i);
+  const Eigen::MatrixXd Hx = H0 * Xs1;
+  double e2 = 0;
+  for (int i = 0; i < n; ++i) e2 += (Hx(i, 0) - b(i)) * (Hx(i, 0) - b(i));
+  if (std::sqrt(e2 / nb) > 1e-10) { std::printf("exact_solve residual %g\n", std::sqrt(e2 / nb)); return 1; }
+  const g::MllResult m1 = g::mll(ctx, X, b, hyp);
+  const g::MllResult m2 = g::mll(H0, g::to_gpu(b), hyp);
+  if (m1.value != m2.value || !std::isfinite(m1.value)) { std::printf("mll mismatch\n"); return 1; }
+  const g::KernelHyperparams fit = g::optimize_mll(ctx, X, b, hyp, 5, 0.1);
+  if (g::mll(H0, g::to_gpu(b), fit).value < m1.value) { std::printf("optimize_mll worse\n"); return 1; }
+  if (!(g::median_heuristic_lengthscale(X) > 0.0)) { std::printf("median heuristic\n"); return 1; }
   std::printf("eigen overloads ok: %d iters, warm %d/%d\n", r.iterations, rs[0].iterations, rs[1].iterations);
   return 0;
 }

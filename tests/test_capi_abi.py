@@ -69,3 +69,15 @@ def test_cpp_headers_compile_without_gpu():
             subprocess.run(["g++", "-O1", "-std=c++17", "-I", os.path.join(root, "include"), *extra,
                             os.path.join(root, "tests", "cpp", src), "-L", libdir, "-lwarmgp_b200",
                             f"-Wl,-rpath,{libdir}", "-o", os.path.join(td, src + ".bin")], check=True)
+
+
+def test_median_heuristic_matches_oracle(W, O):
+    """median_heuristic_lengthscale (analysis.cpp:184-203) is host code in the product library:
+    same draws and the same order statistic as the oracle, scale-aware (test_analysis.cpp:208-215)."""
+    X = O.uniform_inputs(30, 200, 3)
+    base = W.median_heuristic_lengthscale(X)
+    assert base == O.median_heuristic_lengthscale(X)
+    assert 0.1 < base < 2.0
+    assert W.median_heuristic_lengthscale(10.0 * X) == pytest.approx(10.0 * base, rel=1e-12)
+    X = O.uniform_inputs(31, 1000, 2)
+    assert W.median_heuristic_lengthscale(X, 7) == O.median_heuristic_lengthscale(X, 7)
