@@ -3,31 +3,34 @@
 //   Y[i, :] = sum_j k(x_i, x_j) V[j, :] + sigma_n^2 V[i, :]      (gram, H = K + sigma_n^2 I)
 //
 // restating gram_matrix (kernel.cpp:48-72) + H*p (solvers.cpp:162) without materialising
-// K.  One CTA owns 128 rows i and streams all columns j in tiles of 64:
+// K.  One CTA owns 128 rows i and a contiguous range of 64-column j tiles (grid: row blocks
+// x j splits):
 //
-//   GEMM1  S = XA_i . XB_j^T      (M=128, N=64, K=K1)  tcgen05.mma kind::tf32, SS, S in TMEM.
+//   GEMM1  S = XA_i . XB_j^T      (M=128, N=64, K=K1)  tcgen05.mma SS, S (fp32) in TMEM.
 //          The operands are pre-formatted so the contraction yields the squared distance
-//          directly (the norm form |x|^2 + |y|^2 - 2 x.y of kernel.cpp:39-46, 65):
-//            F32_3XTF32: XA = [-2xh | -2xh | -2xl | sqh | sql | 1 | 1]
-//                        XB = [ xh  |  xl  |  xh  |  1  |  1  | sqh | sql]
-//            (round-to-nearest tf32 hi/lo splits: x.y to ~2^-22 |x||y|; a fourth xl.yl
-//            product gains nothing measurable -- the fp32 accumulation below dominates --
-//            and costs 7% at C3 through K1 = 4d+4)
-//            TF32:       XA = [-2xh | sqh | 1]   XB = [xh | 1 | sqh]   (single pass, ~2^-11)
+//          directly (the norm form |x|^2 + |y|^2 - 2 x.y of kernel.cpp:39-46, 65), as
+//          3-way hi/lo splits: kind::f16 on x/l when the scaled coordinates fit fp16
+//          comfortably (|x|/l <= 64), else kind::tf32 on x:
+//            XA = [-2xh | -2xh | -2xl | sqh | sql | 1 | 1]
+//            XB = [ xh  |  xl  |  xh  |  1  |  1  | sqh | sql]
+//          (TF32 precision: XA = [-2xh | sqh | 1], XB = [xh | 1 | sqh], single pass, ~2^-11)
 //   map    epilogue warps: tcgen05.ld S -> k(d2)/s^2 * 2^10 in registers (Matern-3/2 or RBF;
-//          MUFU sqrt/ex2) -> fp16 hi/lo split -> tcgen05.st into TMEM (K never leaves the SM).
-//   GEMM2  Y += K_hi V_hi + K_hi V_lo + K_lo V_hi   (M=128, N=s_pad, K=64)  kind::f16, A from
-//          TMEM (TS form), fp32 accumulator in TMEM for the whole j sweep.  V is pre-split
-//          into fp16 hi/lo with a per-column power-of-two scale (3xFP16 ~ 2^-22 relative).
-//   out    Y * s^2 / (2^10 * scale_c) + sigma_n^2 V_i in fp64 (or B - that: the true residual
-//          of solvers.cpp:171) written as fp64.
+//          MUFU sqrt/ex2, packed FP32) -> fp16 hi/lo split -> tcgen05.st back into the same
+//          TMEM columns (K never leaves the SM).
+//   GEMM2  Y += K_hi V_hi (chunk accumulator), C += K_hi V_lo + K_lo V_hi (correction
+//          accumulator)  (M=128, N=s_pad, K=64)  kind::f16, A from TMEM (TS form).  V is
+//          pre-split into fp16 hi/lo with a per-column power-of-two scale.
+//   drain  every CH tiles the finished chunk accumulator is added (fp32 vector reductions)
+//          into L2-resident partials; reduce_splits_kernel sums splits in fp64 and writes
+//          Y * s^2 / (2^10 * scale_c) + sigma_n^2 V_i (or B - that: the true residual of
+//          solvers.cpp:171) as fp64.
 //
-// Warp roles (20 warps): 0 = bulk-copy producer (TMA engine, UBLKCP), 1 = GEMM1 issuer,
-// 3 = GEMM2 issuer (whole warps run the schedules, one elected lane issues), 2 = TMEM
-// allocator, 4..19 = epilogue:
-// two sets of 8 warps taking alternate j tiles (2 warps per TMEM lane quadrant, 32 columns
-// each).  Pipelines: smem stages (XB_j, V_j hi/lo) x NS; a ring of 6-7 TMEM tile buffers
-// (S written by GEMM1, overwritten in place by K for GEMM2); mbarriers + tcgen05.commit.
+// Warp roles (28 warps): 0 = XB bulk-copy producer (TMA engine, UBLKCP) + XA load,
+// 1 = GEMM1 issuer, 2 = V bulk-copy producer + TMEM allocator, 3 = GEMM2 issuer (whole warps
+// run the schedules, one elected lane issues), 4..27 = epilogue: three sets of 8 warps
+// taking j tiles round-robin (2 warps per TMEM lane quadrant, 32 columns each).  Pipelines:
+// smem rings of XB_j (NSX) and V_j hi/lo (NSV); a ring of NB TMEM tile buffers (S written
+// by GEMM1, overwritten in place by K for GEMM2); mbarriers + tcgen05.commit.
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -87,19 +90,18 @@ constexpr int NG2 = WGP_TC_NG2;
 constexpr int NROLE = (NG2 == 1 && NPX == 1 && NPV == 1) ? 4 : 8;  // role warps
 constexpr int NTHREADS = 32 * (NROLE + EPIW);  // role warps + epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
-constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (fp64 drain after each)
-// TMEM: a ring of NB 64-column tile buffers followed by the Y accumulator.  A buffer holds
-// S(t) (fp32 d^2, written by GEMM1); the epilogue loads it into registers and writes K(t)
-// back in place as packed fp16 (each warp into the 32 columns it read: 16 hi + 16 lo), which
-// GEMM2 then reads as its A operand; GEMM2's commit frees the buffer for GEMM1 of tile
-// t + NB.  Two 64-column Y accumulators alternate per chunk of CH tiles: each tcgen05.mma
-// truncates its fp32 sum (a relative bias of about -2^-25 per instruction against the running
-// accumulator: -7.5e-6 for positive V at CH = 16, i.e. 192 instructions per chunk, and
-// 3.5e-4 at N = 101k in a single chain), so every CH tiles the epilogue warps drain the
-// finished accumulator into fp64 partial sums in shared memory.  Measured at N = 10k RBF
-// (tools/probes/gpu_probe_ch.py): CH = 16 -> 3.3e-6 relative, 4 -> 1.1e-6, 1 -> 4.9e-7, at 1.0 /
-// 1.08 / 2.2x the C3 time (the fp64 shared-memory traffic of the drains); WGP_TC_CH overrides.
-// TMEM: NB = 6 buffers [0,384), Y0 [384,448), Y1 [448,512).
+constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (drained after each)
+// TMEM (512 columns): a ring of NB = 5 64-column tile buffers [0, 320), two 64-column chunk
+// accumulators [320, 448) and the sweep-long correction accumulator [448, 512).  A buffer
+// holds S(t) (fp32 d^2, written by GEMM1); the epilogue loads it into registers and writes
+// K(t) back in place as packed fp16 (each warp into the 32 columns it read: 16 hi + 16 lo),
+// which GEMM2 then reads as its A operand; GEMM2's commit frees the buffer for GEMM1 of tile
+// t + NB.  The chunk accumulators alternate per chunk of CH tiles: each tcgen05.mma truncates
+// its fp32 sum (a relative bias of about -2^-25 per instruction against the running
+// accumulator), so every CH tiles the epilogue warps drain the finished accumulator into the
+// partials.  Measured at the C3 shape (tools/probes/gpu_probe_ch_c3.py, vs the fp64
+// operator): CH = 16 -> 1.4e-6 (random V) / 5.8e-6 (positive V); 32 -> 2.6e-6 / 1.2e-5;
+// 64 -> 4.9e-6 / 2.5e-5, each doubling ~1-2% faster.  WGP_TC_CH overrides.
 constexpr int MAX_NB = 5;
 constexpr int TRW = 12;  // trace slots per tile
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
@@ -121,7 +123,7 @@ struct Params {
   int ntiles;           // ceil(ncols / BJ)
   int tiles_per_split;  // j tiles per CTA along grid.y (2-D decomposition)
   int ch;               // j tiles per accumulation chunk
-  double* Ypart;        // fp64 partial sums [gridDim.y][nrows][s] (unscaled; reduce_splits)
+  float* Ypart;         // fp32 partial sums [gridDim.y][s_pad / 4][nrows][4] (unscaled)
   int s, s_pad, K1;
   int kind;
   float c1, neg_c_log2e;
@@ -158,17 +160,6 @@ __device__ __forceinline__ float tf32_rn(float x) {
   uint32_t u;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
   return __uint_as_float(u);
-}
-
-// Exact fp32 -> fp64 with integer ops on the ALU pipe (F2F.F64.F32 issues to the XU pipe,
-// which the kernel map keeps ~80% busy with MUFU work).  fp32 denormals flush to zero;
-// TMEM accumulators never hold inf/nan for finite inputs.
-__device__ __forceinline__ double f32_to_f64_alu(uint32_t u) {
-  const uint32_t mag = u & 0x7FFFFFFFu;
-  const uint32_t hi = mag < 0x00800000u ? (u & 0x80000000u)
-                                        : (u & 0x80000000u) | ((mag >> 3) + 0x38000000u);
-  const uint32_t lo = mag < 0x00800000u ? 0u : (u << 29);
-  return __hiloint2double((int)hi, (int)lo);
 }
 
 __device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
@@ -457,17 +448,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
     const float kdiag = 1024.0f;              // k(x,x)/s^2 * 2^10
     // drain share of this warp (sets 0 and 1 only): its quadrant's 32 rows x 16 accumulator
-    // columns, summed in fp64 into this CTA's slice of the column-major partials buffer
-    // [gy][s][nrows] (lanes = consecutive rows: coalesced; L2-resident); reduce_splits scales
-    // and transposes.
+    // columns, summed into this CTA's slice of the partials buffer [gy][s_pad/4][nrows][4]
+    // (4 columns of a row contiguous: one 16-byte vector reduction per lane and visit, a
+    // warp covering 512 contiguous bytes; L2-resident); reduce_splits scales and transposes.
     const bool drainer = g < 4;
     const int dc0 = (g & 3) * 16;
     const bool row_ok = lr < p.nrows;
     const int ncol = max(0, min(16, p.s - dc0));
-    double* __restrict__ ypart = p.Ypart + ((size_t)blockIdx.y * p.s + dc0) * p.nrows + lr;
+    float* __restrict__ ypart =
+        p.Ypart + (((size_t)blockIdx.y * (p.s_pad / 4) + dc0 / 4) * p.nrows + lr) * 4;
     int drained = 0;
     // Incremental drain: a finished chunk accumulator is moved out DSTEP columns per visit
-    // (one visit after each of this warp's tiles), so the fp64 store traffic trickles instead
+    // (one visit after each of this warp's tiles), so the reduction traffic trickles instead
     // of arriving as one 64-KB burst per chunk (which stalled every warp's TMEM/LSU traffic
     // for ~2000 cycles).  Chunk d may start once the epilogue is 4 tiles into chunk d+1 (its
     // GEMM2 long done) and must finish before GEMM2 starts chunk d+2.
@@ -484,21 +476,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
                    : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3])
                    : "r"(tmem + lane_off + TM_Y + ya * 64 + dc0 + dk));
       ptx::tmem_wait_ld();
-      if (row_ok) {
-        // first chunk stores, later chunks add with fire-and-forget reductions performed at
-        // L2.  Each address is only ever touched by this thread, and same-address operations
-        // of one thread stay in program order, so the fp64 summation order (chunk 0, 1, 2,
-        // ...) is deterministic.
-#pragma unroll
-        for (int k = 0; k < DSTEP; ++k) {
-          if (dk + k >= ncol) break;
-          double* dst = ypart + (size_t)(dk + k) * p.nrows;
-          if (c == 0)
-            *dst = f32_to_f64_alu(y[k]);
-          else
-            asm volatile("red.global.add.f64 [%0], %1;" ::"l"(dst), "d"(f32_to_f64_alu(y[k]))
-                         : "memory");
-        }
+      if (row_ok && dk < ncol) {
+        // first chunk stores, later chunks add with fire-and-forget vector reductions
+        // performed at L2 (fp32: ~50 chunk terms per sweep at C3, relative rounding ~1e-7).
+        // Each address is only ever touched by this thread, and same-address operations of
+        // one thread stay in program order, so the summation order (chunk 0, 1, 2, ...) is
+        // deterministic.
+        float* dst = ypart + (size_t)(dk / 4) * p.nrows * 4;
+        if (c == 0)
+          asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(y[0]), "r"(y[1]),
+                       "r"(y[2]), "r"(y[3])
+                       : "memory");
+        else
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(y[0]),
+                       "r"(y[1]), "r"(y[2]), "r"(y[3])
+                       : "memory");
       }
       dk += DSTEP;
       if (dk >= 16) {
@@ -520,10 +512,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       ptx::tmem_wait_ld();
       if (row_ok) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
+        for (int k = 0; k < 16; k += 4)
           if (k < ncol)
-            asm volatile("red.global.add.f64 [%0], %1;" ::"l"(ypart + (size_t)k * p.nrows),
-                         "d"(f32_to_f64_alu(y[k]))
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
+                             ypart + (size_t)(k / 4) * p.nrows * 4),
+                         "r"(y[k]), "r"(y[k + 1]), "r"(y[k + 2]), "r"(y[k + 3])
                          : "memory");
       }
     };
@@ -750,10 +743,11 @@ __global__ void split_v_kernel(const double* __restrict__ V, int64_t ncols, int 
 }
 
 // Y = (sum over j-splits, fixed order) * s^2 2^-10 / scale_c + sigma^2 V_i (gram), or B - that.
-// Partials are column-major [nsplit][s][nrows]; 32 x 32 (row, column) tiles are transposed
-// through shared memory so both the partial reads and the row-major writes coalesce.
-__global__ void reduce_splits_kernel(const double* __restrict__ Ypart, int nsplit, int64_t nrows,
-                                     int64_t row0, int s, const float* __restrict__ vscale,
+// Partials are [nsplit][s_pad/4][nrows][4] fp32; a 32-row x 32-column tile is read as one
+// float4 (4 columns of a row) per thread -- a warp reads 512 contiguous bytes -- summed over
+// the splits in fp64, and transposed through shared memory so the row-major writes coalesce.
+__global__ void reduce_splits_kernel(const float* __restrict__ Ypart, int nsplit, int64_t nrows,
+                                     int64_t row0, int s, int s_pad, const float* __restrict__ vscale,
                                      double out_scale, const double* __restrict__ V64,
                                      const double* __restrict__ B64, double noise2, int gram,
                                      double* __restrict__ Y64) {
@@ -761,15 +755,25 @@ __global__ void reduce_splits_kernel(const double* __restrict__ Ypart, int nspli
   const int64_t rb = (int64_t)blockIdx.x * 32;
   const int cb = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
-  for (int k = ty; k < 32; k += 8) {
-    const int c = cb + k;
+  {
+    const int c0 = cb + 4 * ty;  // this thread's 4 columns
     const int64_t r = rb + tx;
-    double acc = 0.0;
-    if (c < s && r < nrows) {
-      for (int q = 0; q < nsplit; ++q) acc += Ypart[((size_t)q * s + c) * nrows + r];
-      acc *= out_scale * (double)vscale[c];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (c0 < s && r < nrows) {
+      const size_t G = (size_t)(s_pad / 4);
+      for (int q = 0; q < nsplit; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(Ypart + (((size_t)q * G + c0 / 4) * nrows + r) * 4);
+        acc[0] += (double)v.x;
+        acc[1] += (double)v.y;
+        acc[2] += (double)v.z;
+        acc[3] += (double)v.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (c0 + k < s) acc[k] *= out_scale * (double)vscale[c0 + k];
     }
-    tile[k][tx] = acc;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tile[4 * ty + k][tx] = acc[k];
   }
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
@@ -1002,8 +1006,8 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     const int nsplit = forced_splits > 0 ? forced_splits : tc::choose_splits(row_ctas, ntiles);
     prm.tiles_per_split = (ntiles + nsplit - 1) / nsplit;
     const int gy = (ntiles + prm.tiles_per_split - 1) / prm.tiles_per_split;
-    ysplit.ensure((size_t)gy * nrows_p * sc);
-    prm.Ypart = ysplit.p;
+    ysplit.ensure(((size_t)gy * nrows_p * s_pad + 1) / 2);  // fp32 partials in fp64 storage
+    prm.Ypart = reinterpret_cast<float*>(ysplit.p);
     prm.s = sc;
     prm.s_pad = s_pad;
     prm.K1 = K1;
@@ -1049,7 +1053,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     WGP_CUDA(cudaGetLastError());
     {
       tc::reduce_splits_kernel<<<dim3((unsigned)((nrows_p + 31) / 32), (sc + 31) / 32), 256, 0, st>>>(
-          ysplit.p, gy, nrows_p, row0 + pa, sc, sc_down, prm.out_scale, Vc,
+          reinterpret_cast<const float*>(ysplit.p), gy, nrows_p, row0 + pa, sc, s_pad, sc_down, prm.out_scale, Vc,
           Bc ? Bc + pa * sc : nullptr, kp.noise2, gram ? 1 : 0, Yc + pa * sc);
       WGP_CUDA(cudaGetLastError());
     }
