@@ -366,7 +366,7 @@ def run_ours(args):
 
 # dram bytes (read + write) per launch of tc::kmatvec_tc_kernel on this workload, from the
 # committed ncu --set full capture (profiles/r01_kmatvec_tc_metrics.json)
-TRAFFIC_BYTES = 117.28e6
+TRAFFIC_BYTES = 78.55e6
 
 
 def main():
