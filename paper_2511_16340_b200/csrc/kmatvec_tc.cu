@@ -55,39 +55,17 @@ namespace tc {
 
 constexpr int BM = 128;        // rows per CTA (UMMA M)
 constexpr int BJ = 64;         // columns j per tile (GEMM1 N, GEMM2 K)
-#ifndef WGP_TC_SETW
-#define WGP_TC_SETW 8
-#endif
-constexpr int EPIW = 24;        // epilogue warps
-constexpr int SETW = WGP_TC_SETW;  // warps per epilogue set (8: 32 columns each, 4: 64)
+constexpr int EPIW = 24;       // epilogue warps
+constexpr int SETW = 8;        // warps per epilogue set (2 per TMEM lane quadrant)
 constexpr int NSET = EPIW / SETW;  // sets taking tiles round-robin
-constexpr int CPW = 64 / (SETW / 4);  // tile columns per epilogue warp
-// SETW = 4 (six sets, 64 columns per warp) hung in testing (the drain schedule assumes the
-// two-drainer-set layout); only the measured 8-warp sets are enabled.
-static_assert(SETW == 8, "only 8-warp epilogue sets are supported");
-#ifndef WGP_TC_NPX
-#define WGP_TC_NPX 1
-#endif
-#ifndef WGP_TC_NPV
-#define WGP_TC_NPV 1
-#endif
-// Producer warps per ring (NPX / NPV warps taking the ring's tiles round-robin).  Bulk copies
-// issued by one warp are processed one at a time (~400-900 cycles each in isolation,
-// tools/bulk_microbench2.cu), but at C3 two XB and three V producers measured no faster
-// than one of each (V arrives ~1 tile per period because the whole pipeline is paced by
-// the kernel map; the kernel time hardly depends on the V tile size: 6.8 ms at s=16 vs
-// 7.5 ms at s=64), so the default is one.
-constexpr int NPX = WGP_TC_NPX, NPV = WGP_TC_NPV;
-__host__ __device__ constexpr int xb_warp(int k) { return k == 0 ? 0 : (k == 1 ? 4 : 6); }
-__host__ __device__ constexpr int v_warp(int k) { return k == 0 ? 2 : (k == 1 ? 5 : 7); }
-#ifndef WGP_TC_NG2
-#define WGP_TC_NG2 1
-#endif
-// GEMM2 issuer warps taking tiles round-robin (on SMSPs 3, 0, 2): the warp issuing a tile's 12
-// MMAs costs its SM sub-partition issue slots, and K(t) needs all four TMEM quadrants
-// (one per sub-partition), so a single GEMM2 warp made its quadrant the late one every tile.
-constexpr int NG2 = WGP_TC_NG2;
-constexpr int NROLE = (NG2 == 1 && NPX == 1 && NPV == 1) ? 4 : 8;  // role warps
+constexpr int CPW = 32;        // tile columns per epilogue warp
+// One producer warp per smem ring: bulk copies issued by one warp are processed one at a
+// time (~400-900 cycles each in isolation, tools/bulk_microbench2.cu), but two XB and three
+// V producers measured no faster than one of each at C3 (the pipeline is paced by the
+// epilogue, not by V arrival).  Role warps: 0 XB producer, 1 GEMM1, 2 V producer, 3 GEMM2.
+// (Round-robin GEMM2 issue over several warps and 4-warp epilogue sets were tried and
+// measured no faster / hung.)
+constexpr int NROLE = 4;
 constexpr int NTHREADS = 32 * (NROLE + EPIW);  // role warps + epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
 constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (drained after each)
@@ -105,13 +83,6 @@ constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (drained a
 constexpr int MAX_NB = 5;
 constexpr int TRW = 12;  // trace slots per tile
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
-// Software-exponential share (quarters) of the kernel map: Matern spends 2 SFU ops per pair
-// (sqrt, ex2), RBF 1.
-// (0 = all exponentials on MUFU: fastest at every measured share for both kernels; the
-// software path is kept as a compile-time option, -DWGP_TC_SWQ=1..4.)
-#ifndef WGP_TC_SWQ
-#define WGP_TC_SWQ 0
-#endif
 
 struct Params {
   const void* XA;       // tiled A operand rows (this launch's rows start at tile 0)
@@ -167,32 +138,11 @@ __device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// 2^a for a pair on the FMA pipe (FFMA2/FADD2 + integer exponent insert): a is clamped to
-// >= -125, rounded to j = rn(a) with the 1.5*2^23 shifter, and 2^(a-j) in [2^-1/2, 2^1/2]
-// comes from a degree-5 near-minimax polynomial (max relative error 2.3e-7 evaluated in
-// fp32, vs ~1.2e-7 for MUFU.EX2).  Used for a fraction of the map's exponentials so the SFU
-// (16/clk/SM) and the FP32 pipe (128/clk/SM, two lanes per FFMA2) finish together.
-__device__ __forceinline__ float2 sw_ex2x2(float2 a) {
-  a.x = fmaxf(a.x, -125.0f);
-  a.y = fmaxf(a.y, -125.0f);
-  const float2 t = __fadd2_rn(a, make_float2(12582912.0f, 12582912.0f));
-  const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
-  const float2 f = __ffma2_rn(j, make_float2(-1.0f, -1.0f), a);
-  float2 q = __ffma2_rn(make_float2(1.32764655e-3f, 1.32764655e-3f), f,
-                        make_float2(9.67554096e-3f, 9.67554096e-3f));
-  q = __ffma2_rn(q, f, make_float2(5.55071346e-2f, 5.55071346e-2f));
-  q = __ffma2_rn(q, f, make_float2(2.40221202e-1f, 2.40221202e-1f));
-  q = __ffma2_rn(q, f, make_float2(6.93146944e-1f, 6.93146944e-1f));
-  q = __ffma2_rn(q, f, make_float2(1.00000012f, 1.00000012f));
-  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
-}
-
-// Kernel map of one 32-column row slice: v = fp32 d^2 from TMEM, kv = k/s^2 * 2^10.
-// Pairs of columns go through the packed FP32 pipe; SWQ of every 4 pairs take the software
-// exponential, the rest MUFU.EX2.  sqrt(|d2|): a tiny negative d2 from the norm-form
-// cancellation maps to ~0 like the reference's max(.,0) clamp (kernel.cpp:44).
-template <int SWQ, int NCOL>
+// Kernel map of NCOL columns of a row: v = fp32 d^2 from TMEM, kv = k/s^2 * 2^10.  Pairs of
+// columns go through the packed FP32 pipe, sqrt and exp2 through MUFU (moving a share of
+// either to an FMA-pipe polynomial measured no faster).  sqrt(|d2|): a tiny negative d2 from
+// the norm-form cancellation maps to ~0 like the reference's max(.,0) clamp (kernel.cpp:44).
+template <int NCOL>
 __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* kv, float c1,
                                            float nclog2e) {
   const float2 NC = make_float2(nclog2e, nclog2e);
@@ -206,12 +156,8 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
       r.y = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q + 1])));
       const float2 a = __ffma2_rn(r, NC, OFF);  // log2(2^10 e^{-z})
       float2 e;
-      if ((q & 3) < SWQ) {
-        e = sw_ex2x2(a);
-      } else {
-        e.x = ptx::ex2_approx(a.x);
-        e.y = ptx::ex2_approx(a.y);
-      }
+      e.x = ptx::ex2_approx(a.x);
+      e.y = ptx::ex2_approx(a.y);
       const float2 z = __fmul2_rn(r, C1);
       const float2 k = __ffma2_rn(z, e, e);  // 2^10 (1+z) e^{-z}
       kv[2 * q] = k.x;
@@ -223,19 +169,14 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
       const float2 d2 = make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
       const float2 a = __ffma2_rn(d2, NC, OFF);  // log2(2^10 e^{-d2/2l^2})
       float2 e;
-      if ((q & 3) < SWQ) {
-        e = sw_ex2x2(a);
-      } else {
-        e.x = ptx::ex2_approx(a.x);
-        e.y = ptx::ex2_approx(a.y);
-      }
+      e.x = ptx::ex2_approx(a.x);
+      e.y = ptx::ex2_approx(a.y);
       kv[2 * q] = e.x;
       kv[2 * q + 1] = e.y;
     }
   }
 }
 
-template <int SWQ>
 __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NSX, int NSV) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -257,8 +198,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* b_free = k_full + MAX_NB;     // [MAX_NB] GEMM2 -> GEMM1
   uint64_t* y_full = b_free + MAX_NB;     // [2] chunk accumulator done (GEMM2 commit)
   uint64_t* y_free = y_full + 2;          // [2] chunk accumulator drained (16 warp arrivals)
-  uint64_t* g2_tok = y_free + 2;          // [NG2] GEMM2 issue-order tokens
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(g2_tok + NG2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_free + 2);
   constexpr int NB = MAX_NB;
   // TMEM: ring of NB 64-column S/K buffers [0, 320), the two chunk accumulators of the
   // leading product Kh.Vh at TM_Y + 64 a, and one sweep-long accumulator of the correction
@@ -289,7 +229,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       ptx::mbar_init(&k_full[i], SETW);
       ptx::mbar_init(&b_free[i], 1);
     }
-    for (int i = 0; i < NG2; ++i) ptx::mbar_init(&g2_tok[i], 1);
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&y_full[i], 1);
       ptx::mbar_init(&y_free[i], 4 * (p.s_pad / 16));  // drainer warps with columns
@@ -304,27 +243,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   const int KS1 = p.K1 * ESZ / 32;          // GEMM1 K-steps (32 bytes of K per instruction)
   const uint32_t sbo1 = (p.K1 * ESZ / 16) * 128;  // 8-row group stride of XA/XB tiles
 
-  const int g2k = warp == 3 ? 0 : (NG2 > 1 && warp == 4 ? 1 : (NG2 > 2 && warp == 6 ? 2 : -1));
-  static_assert(NG2 == 1 || (NPX == 1 && NPV == 1), "GEMM2 issuers share warps 4/6 with producers");
-  static_assert(NPX <= 3 && NPV <= 3, "role warp layout");
-  int xk = -1, vk = -1;
-  for (int k = 0; k < NPX; ++k) if (warp == xb_warp(k)) xk = k;
-  for (int k = 0; k < NPV; ++k) if (warp == v_warp(k)) vk = k;
-  if (xk >= 0 || vk >= 0) {
+  if (warp == 0 || warp == 2) {
     // ------------------------------------------------------------ producers (TMA engine)
     // Two independent rings: XB_j is consumed by GEMM1 right away, V_j only by GEMM2 after
     // the kernel map, so V stays resident ~4x longer; separate rings let each be as deep as
-    // its own lifetime needs, each fed by NPX / NPV warps taking its tiles round-robin.
-    const bool is_xb = xk >= 0;
-    const int pk = is_xb ? xk : vk;
+    // its own lifetime needs.
     const bool leader = ptx::elect_one();
     if (warp == 0 && leader) {
       ptx::mbar_arrive_expect_tx(xa_full, XA_BYTES);
       ptx::bulk_g2s(sXA, static_cast<const char*>(p.XA) + (size_t)blockIdx.x * XA_BYTES, XA_BYTES,
                     xa_full);
     }
-    if (is_xb) {
-      for (int t = pk; t < T; t += NPX) {
+    if (warp == 0) {
+      for (int t = 0; t < T; ++t) {
         const int st = t % NSX;
         if (t >= NSX) ptx::mbar_wait(&xb_empty[st], ((t / NSX) & 1) ^ 1);
         if (leader) {
@@ -337,7 +268,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         __syncwarp();
       }
     } else {
-      for (int t = pk; t < T; t += NPV) {
+      for (int t = 0; t < T; ++t) {
         const int st = t % NSV;
         if (t >= NSV) ptx::mbar_wait(&v_empty[st], ((t / NSV) & 1) ^ 1);
         if (leader) {
@@ -349,7 +280,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         __syncwarp();
       }
     }
-  } else if (warp == 1 || g2k >= 0) {
+  } else if (warp == 1 || warp == 3) {
     // ------------------------------------------------------------ MMA issuers
     // tcgen05.mma issue blocks for about the instruction's execution time, so one thread
     // cannot keep two dependent streams fed.  Warp 1 issues GEMM1 (distance tiles) and warp 3
@@ -391,7 +322,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sV), 128, (BJ / 8) * 128);
       const uint64_t v_step = (uint64_t)((2 * VT_BYTES) >> 4);
       const uint64_t vlo_step = (uint64_t)(VT_BYTES >> 4);
-      for (int t = g2k; t < T; t += NG2) {
+      for (int t = 0; t < T; ++t) {
         const int st2 = t % NSV, b2 = t % NB;
         const uint32_t ph2 = (t / NSV) & 1, phb2 = (t / NB) & 1;
         const int c = t / CH, ya = c & 1;
@@ -400,10 +331,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         ptx::mbar_wait(&v_full[st2], ph2);
         if (lane == 0) trace_ev(p, t, 9);
         ptx::mbar_wait(&k_full[b2], phb2);
-        // accumulation order: tile t's MMAs enter the tensor pipe after tile t-1's (issued by
-        // the previous issuer, which arrives on g2_tok once its MMAs are dispatched)
-        if (NG2 > 1 && t > 0)
-          ptx::mbar_wait(&g2_tok[t % NG2], (t / NG2 - (t % NG2 == 0 ? 1 : 0)) & 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 1);
@@ -426,10 +353,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
           if (last) ptx::mma_commit(&y_full[ya]);
-          if (NG2 > 1) {
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&g2_tok[(t + 1) % NG2]);
-          }
         }
         __syncwarp();
       }
@@ -543,7 +466,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         ptx::tmem_wait_ld();
         if (tr && h2 == 0) trace_ev(p, t, 7);
         float kv[16];
-        kernel_map<SWQ, 16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
+        kernel_map<16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
         if (diag) {  // tile touches the diagonal: k(x,x) = s^2 exactly
           const int64_t gj0 = gj_base + h2 * 16;
 #pragma unroll
@@ -1036,7 +959,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     const size_t smem = tc_smem_bytes(K1, esz, s_pad, &nsx, &nsv);
     WGP_REQUIRE(nsx >= 2 && nsv >= 2, "kmatvec_tc: dim %d too large for the shared-memory pipeline",
                 op.dim);
-    auto kern = tc::kmatvec_tc_kernel<WGP_TC_SWQ>;
+    auto kern = tc::kmatvec_tc_kernel;
     WGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     KernelTimer& kt = kernel_timer();
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
