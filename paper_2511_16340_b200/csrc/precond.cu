@@ -131,19 +131,58 @@ __global__ void pchol_step_kernel(const double* __restrict__ X, const double* __
   }
 }
 
-// Per-chunk partial of G = A^T A (A local rows [n_local][kpad]); chunk q of the local rows
-// is global chunk c0 + q, so the fixed-order sum over chunks is world-size independent.
-__global__ void gram_chunk_kernel(const double* __restrict__ A, int64_t n_local, int k, int kpad,
-                                  double* __restrict__ part) {
+// Per-chunk partials of A^T B (A: [n][lda], B: [n][ldb] local rows, row-major):
+// part[chunk][a][c] = sum over the chunk's rows, in row order, of A[i][a] B[i][c] for a < ka,
+// c < kb.  Grid (chunk, a-block of 64, c-block of 64); the chunk's rows are staged 32 at a
+// time in shared memory and each thread owns a 4 x 4 output tile (8 shared loads per 16
+// FMAs).  Every output is one fma chain over the rows in order, so the partial does not
+// depend on the tiling, and chunk q of the local rows is global chunk c0 + q: the fixed-order
+// sum over chunks is world-size independent.
+__global__ void __launch_bounds__(256) chunk_atb_kernel(const double* __restrict__ A, int lda, int ka,
+                                                        const double* __restrict__ B, int ldb, int kb,
+                                                        int64_t n, double* __restrict__ part) {
+  constexpr int RT = 32;
+  __shared__ double sA[RT][64 + 1], sB[RT][64 + 1];
   const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
-  const int64_t r1 = min(n_local, r0 + (int64_t)kChunkRows);
-  double* out = part + (int64_t)blockIdx.x * k * k;
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    const int a = e / k, b = e % k;
-    double acc = 0.0;
-    for (int64_t i = r0; i < r1; ++i) acc += A[i * kpad + a] * A[i * kpad + b];
-    out[e] = acc;
+  const int64_t r1 = min(n, r0 + (int64_t)kChunkRows);
+  const int a0 = blockIdx.y * 64, c0 = blockIdx.z * 64;
+  const int ta = (threadIdx.x / 16) * 4, tc = (threadIdx.x % 16) * 4;
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  for (int64_t rb = r0; rb < r1; rb += RT) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < RT * 64; e += 256) {
+      const int r = e / 64, q = e % 64;
+      const int64_t i = rb + r;
+      sA[r][q] = (i < r1 && a0 + q < ka) ? A[i * lda + a0 + q] : 0.0;
+      sB[r][q] = (i < r1 && c0 + q < kb) ? B[i * ldb + c0 + q] : 0.0;
+    }
+    __syncthreads();
+    const int rows = (int)(r1 - rb < RT ? r1 - rb : RT);
+    for (int ii = 0; ii < rows; ++ii) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        av[u] = sA[ii][ta + u];
+        bv[u] = sB[ii][tc + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
   }
+  double* out = part + (int64_t)blockIdx.x * ka * kb;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int a = a0 + ta + u, c = c0 + tc + v;
+      if (a < ka && c < kb) out[(int64_t)a * kb + c] = acc[u][v];
+    }
 }
 
 __global__ void sum_partials_kernel(const double* __restrict__ part, int np, int count,
@@ -174,74 +213,55 @@ __global__ void apply_upper_kernel(const double* __restrict__ L, const double* _
   }
 }
 
-// T[chunk][a][c] = sum_{i in chunk} M[i, a] R[i, c]  (R: s columns of a row-major [n][ld])
-template <typename T>
-__global__ void __launch_bounds__(256) mtr_partial_kernel(const T* __restrict__ M,
-                                                          const T* __restrict__ R, int64_t ld,
-                                                          int64_t n, int k, int kpad, int s,
-                                                          double* __restrict__ part) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int RT = 32;
-  T* sM = reinterpret_cast<T*>(smem);  // RT x kpad
-  T* sR = sM + RT * kpad;               // RT x s
-  const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
-  const int64_t r1 = min(n, r0 + (int64_t)kChunkRows);
-  const int outs = k * s;
-  constexpr int MAXQ = 64;  // supports k*s <= 256*64
-  double acc[MAXQ];
-  const int nq = (outs + 255) / 256;
+// Z[i, c] = (R[i, c] - sum_a M[i, a] t[a, c]) / shift  (R, Z: s columns of row-major [n][ld]).
+// 64 rows x 64 columns per CTA, 4 x 4 outputs per thread; M and t are staged 32 a at a time
+// in shared memory; each output is one fma chain over a in order.
+__global__ void __launch_bounds__(256) woodbury_tile_kernel(const double* __restrict__ M, int kpad, int k,
+                                                            const double* __restrict__ R, int64_t ld,
+                                                            const double* __restrict__ t, int s, int64_t n,
+                                                            double inv_shift, double* __restrict__ Z) {
+  constexpr int AT = 32;
+  __shared__ double sM[64][AT + 1], sT[AT][64 + 1];
+  const int64_t rb = (int64_t)blockIdx.x * 64;
+  const int cb = blockIdx.y * 64;
+  const int tr = (threadIdx.x / 16) * 4, tc = (threadIdx.x % 16) * 4;
+  double acc[4][4];
 #pragma unroll
-  for (int q = 0; q < MAXQ; ++q) acc[q] = 0.0;
-  for (int64_t rb = r0; rb < r1; rb += RT) {
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  for (int a0 = 0; a0 < k; a0 += AT) {
     __syncthreads();
-    for (int e = threadIdx.x; e < RT * kpad; e += 256) {
-      const int64_t i = rb + e / kpad;
-      sM[e] = i < r1 ? M[i * kpad + e % kpad] : T(0);
-    }
-    for (int e = threadIdx.x; e < RT * s; e += 256) {
-      const int64_t i = rb + e / s;
-      sR[e] = i < r1 ? R[i * ld + e % s] : T(0);
+    for (int e = threadIdx.x; e < 64 * AT; e += 256) {
+      const int r = e / AT, a = e % AT;
+      sM[r][a] = (rb + r < n && a0 + a < k) ? M[(rb + r) * kpad + a0 + a] : 0.0;
+      const int a2 = e / 64, c = e % 64;
+      sT[a2][c] = (a0 + a2 < k && cb + c < s) ? t[(int64_t)(a0 + a2) * s + cb + c] : 0.0;
     }
     __syncthreads();
+    const int na = min(AT, k - a0);
+    for (int a = 0; a < na; ++a) {
+      double mv[4], tv[4];
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) {
-      if (q >= nq) break;
-      const int o = threadIdx.x + q * 256;
-      if (o >= outs) break;
-      const int a = o / s, c = o % s;
-      double t = acc[q];
-      for (int ii = 0; ii < RT; ++ii) t = fma((double)sM[ii * kpad + a], (double)sR[ii * s + c], t);
-      acc[q] = t;
+      for (int u = 0; u < 4; ++u) {
+        mv[u] = sM[tr + u][a];
+        tv[u] = sT[a][tc + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(mv[u], tv[v], acc[u][v]);
     }
   }
-  double* out = part + (int64_t)blockIdx.x * outs;
 #pragma unroll
-  for (int q = 0; q < MAXQ; ++q) {
-    if (q >= nq) break;
-    const int o = threadIdx.x + q * 256;
-    if (o < outs) out[o] = acc[q];
-  }
-}
-
-// Z[i, c] = (R[i, c] - sum_a M[i, a] t[a, c]) / shift  (R, Z: s columns of row-major [n][ld])
-template <typename T>
-__global__ void __launch_bounds__(256) woodbury_out_kernel(const T* __restrict__ M,
-                                                           const T* __restrict__ R, int64_t ld,
-                                                           const double* __restrict__ t, int64_t n,
-                                                           int k, int kpad, int s, double inv_shift,
-                                                           T* __restrict__ Z) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* st = reinterpret_cast<T*>(smem);  // k x s
-  for (int e = threadIdx.x; e < k * s; e += blockDim.x) st[e] = (T)t[e];
-  __syncthreads();
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * s;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / s;
-    const int c = (int)(e % s);
-    const T* Mi = M + i * kpad;
-    T acc = T(0);
-    for (int a = 0; a < k; ++a) acc = fma(Mi[a], st[a * s + c], acc);
-    Z[i * ld + c] = (T)(((double)R[i * ld + c] - (double)acc) * inv_shift);
+  for (int u = 0; u < 4; ++u) {
+    const int64_t i = rb + tr + u;
+    if (i >= n) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int c = cb + tc + v;
+      if (c < s) Z[i * ld + c] = (R[i * ld + c] - acc[u][v]) * inv_shift;
+    }
   }
 }
 
@@ -319,8 +339,8 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   const int c0 = (int)(pd.r0 / kChunkRows);
   DBuf<double> part((size_t)nch * k * k), G((size_t)k * k);
   if (pd.n_local > 0)
-    gram_chunk_kernel<<<ceil_div(pd.n_local, kChunkRows), 256, 0, st>>>(pd.L.p, pd.n_local, k, (int)pd.kpad,
-                                                                        part.p + (int64_t)c0 * k * k);
+    chunk_atb_kernel<<<dim3(ceil_div(pd.n_local, kChunkRows), ceil_div(k, 64), ceil_div(k, 64)), 256, 0, st>>>(
+        pd.L.p, (int)pd.kpad, k, pd.L.p, (int)pd.kpad, k, pd.n_local, part.p + (int64_t)c0 * k * k);
   dist_allgather_chunks(*op.ctx, part.p, n, (int64_t)k * k, st);
   sum_partials_kernel<<<ceil_div((int64_t)k * k, 256), 256, 0, st>>>(part.p, nch, k * k, G.p);
   WGP_CUDA(cudaGetLastError());
@@ -387,34 +407,22 @@ void precond_apply(const Op& op, const PrecondDev& pd, const T* R, T* Z, int s, 
     if (nl > 0) WGP_CUDA(cudaMemcpyAsync(Z, R, sizeof(T) * nl * s, cudaMemcpyDeviceToDevice, st));
     return;
   }
-  const T* M = (const T*)pd.M64.p;  // solver vectors are fp64 for every precision
+  static_assert(sizeof(T) == sizeof(double), "solver vectors are fp64 for every precision");
+  const double* M = pd.M64.p;
   const int nch = ceil_div(pd.n, kChunkRows);
   const int c0 = (int)(pd.r0 / kChunkRows);
-  // column groups of <= 256*64 / k columns (the per-thread accumulators of mtr_partial);
-  // each column's arithmetic is independent of the grouping
-  const int sg_max = std::max(1, std::min(s, 256 * 64 / k));
-  for (int g0 = 0; g0 < s; g0 += sg_max) {
-    const int sg = std::min(sg_max, s - g0);
-    const size_t smem1 = sizeof(T) * 32 * (pd.kpad + sg);
-    if (smem1 > 48 * 1024)  // rank + columns > 192 (e.g. config 5: rank 100, 129 columns)
-      WGP_CUDA(cudaFuncSetAttribute(mtr_partial_kernel<T>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-    if (nl > 0)
-      mtr_partial_kernel<T><<<ceil_div(nl, kChunkRows), 256, smem1, st>>>(
-          M, R + g0, s, nl, k, (int)pd.kpad, sg, work_part + (int64_t)c0 * k * sg);
-    WGP_CUDA(cudaGetLastError());
-    dist_allgather_chunks(*op.ctx, work_part, pd.n, (int64_t)k * sg, st);
-    sum_partials_kernel<<<ceil_div((int64_t)k * sg, 256), 256, 0, st>>>(work_part, nch, k * sg, work_t);
-    const size_t smem2 = sizeof(T) * k * sg;
-    if (smem2 > 48 * 1024)
-      WGP_CUDA(cudaFuncSetAttribute(woodbury_out_kernel<T>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    if (nl > 0)
-      woodbury_out_kernel<T><<<grid_rows(nl * sg), 256, smem2, st>>>(M, R + g0, s, work_t, nl, k,
-                                                                     (int)pd.kpad, sg, 1.0 / pd.shift,
-                                                                     Z + g0);
-    WGP_CUDA(cudaGetLastError());
-  }
+  // t = M^T r: chunk partials (fixed order, world-size independent), then summed
+  if (nl > 0)
+    chunk_atb_kernel<<<dim3(ceil_div(nl, kChunkRows), ceil_div(k, 64), ceil_div(s, 64)), 256, 0, st>>>(
+        M, (int)pd.kpad, k, R, s, s, nl, work_part + (int64_t)c0 * k * s);
+  WGP_CUDA(cudaGetLastError());
+  dist_allgather_chunks(*op.ctx, work_part, pd.n, (int64_t)k * s, st);
+  sum_partials_kernel<<<ceil_div((int64_t)k * s, 256), 256, 0, st>>>(work_part, nch, k * s, work_t);
+  // z = (r - M t) / shift
+  if (nl > 0)
+    woodbury_tile_kernel<<<dim3(ceil_div(nl, 64), ceil_div(s, 64)), 256, 0, st>>>(
+        M, (int)pd.kpad, k, R, s, work_t, s, nl, 1.0 / pd.shift, Z);
+  WGP_CUDA(cudaGetLastError());
 }
 
 template void precond_apply<double>(const Op&, const PrecondDev&, const double*, double*, int,
