@@ -104,6 +104,7 @@ struct Op {
   // translation applied before forming them, and per-call V staging.
   DBuf<float> XA, XB, vt;
   DBuf<double> center, vchunk, ychunk, ysplit;
+  mutable DBuf<double> f64split;  // fp64 kernel-matvec column-split partials
   std::vector<double> h_center;
   bool tc_dirty = true;
   // GEMM1 operand format chosen at operand build: fp16 splits of x / l (kind::f16, half the

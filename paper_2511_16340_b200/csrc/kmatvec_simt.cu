@@ -196,10 +196,11 @@ void launch_bs(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* 
 constexpr int DM = 64, DN = 32;
 
 template <int NT>
-__global__ void __launch_bounds__(256) kmatvec_dmma_kernel(
+__global__ void __launch_bounds__(256, NT <= 3 ? 4 : (NT <= 8 ? 3 : 2)) kmatvec_dmma_kernel(
     const double* __restrict__ Xr, int64_t nrows, int64_t row0, const double* __restrict__ Xc,
     int64_t ncols, int dpad, int dim, const double* __restrict__ V, int s,
-    const double* __restrict__ B, double* __restrict__ Y, KParams p, int gram) {
+    const double* __restrict__ B, double* __restrict__ Y, KParams p, int gram, int64_t jlen,
+    double* __restrict__ part) {
   constexpr int BS = NT * 8;
   extern __shared__ double dsm[];
   const int ds = dim + 1;
@@ -219,7 +220,10 @@ __global__ void __launch_bounds__(256) kmatvec_dmma_kernel(
 #pragma unroll
   for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
   const double kdiag = p.s2 + p.noise2;
-  for (int64_t jb = 0; jb < ncols; jb += DN) {
+  // this CTA's column range (grid.z splits the sweep into fixed-length ranges)
+  const int64_t j_lo = (int64_t)blockIdx.z * jlen;
+  const int64_t j_hi = min(ncols, j_lo + jlen);
+  for (int64_t jb = j_lo; jb < j_hi; jb += DN) {
     __syncthreads();
     for (int e = tid; e < DN * dim; e += 256) {
       const int j = e / dim, k = e % dim;
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(256) kmatvec_dmma_kernel(
   }
   const int64_t gr = rbase + warp * 8 + (lane >> 2);
   if (gr >= nrows) return;
+  double* out = part ? part + (size_t)blockIdx.z * nrows * s : Y;
 #pragma unroll
   for (int t = 0; t < NT; ++t)
 #pragma unroll
@@ -281,28 +286,61 @@ __global__ void __launch_bounds__(256) kmatvec_dmma_kernel(
       const int c = c0 + t * 8 + (lane & 3) * 2 + u;
       if (c >= s) continue;
       const double y = acc[t][u];
-      Y[gr * s + c] = B ? B[gr * s + c] - y : y;
+      out[gr * s + c] = (B && !part) ? B[gr * s + c] - y : y;
     }
 }
+
+// Y = sum over the column splits in order (or B - that).
+__global__ void sum_splits_kernel(const double* __restrict__ part, int nsplit, int64_t count,
+                                  const double* __restrict__ B, double* __restrict__ Y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double y = 0.0;
+    for (int q = 0; q < nsplit; ++q) y += part[(size_t)q * count + e];
+    Y[e] = B ? B[e] - y : y;
+  }
+}
+
+// Column splits: the j sweep is cut into fixed 4096-column ranges (at most 16) summed in
+// order by sum_splits_kernel, so small row counts still fill the GPU (C2: 313 row blocks ->
+// 1565 CTAs).  The split depends on ncols only, so every rank of a row-sharded operator
+// sums each output identically and the result is world-size independent.
+constexpr int64_t kSplitCols = 4096;
+inline int f64_splits(int64_t ncols) { return (int)std::min<int64_t>(16, (ncols + kSplitCols - 1) / kSplitCols); }
 
 template <int NT>
 void launch_dmma(const double* Xr, int64_t nrows, int64_t row0, const double* Xc, int64_t ncols,
                  int dpad, int dim, const double* V, int s, const double* B, double* Y, KParams kp,
-                 bool gram, cudaStream_t st) {
-  dim3 grid(ceil_div(nrows, DM), ceil_div(s, NT * 8));
+                 bool gram, DBuf<double>& split_buf, cudaStream_t st) {
+  const int nsplit = std::max(1, f64_splits(ncols));
+  const int64_t jlen = nsplit == 1 ? ncols : (((ncols + nsplit - 1) / nsplit + DN - 1) / DN) * DN;
+  double* part = nullptr;
+  if (nsplit > 1) {
+    split_buf.ensure((size_t)nsplit * nrows * s);
+    part = split_buf.p;
+  }
+  dim3 grid(ceil_div(nrows, DM), ceil_div(s, NT * 8), nsplit);
   const size_t smem = sizeof(double) * ((size_t)(DM + DN) * (dim + 1) + DM * (DN + 1) +
                                         (size_t)DN * (NT * 8 + 1));
   if (smem > 48 * 1024)
     WGP_CUDA(cudaFuncSetAttribute(kmatvec_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   kmatvec_dmma_kernel<NT><<<grid, 256, smem, st>>>(Xr, nrows, row0, Xc, ncols, dpad, dim, V, s, B, Y,
-                                                   kp, gram ? 1 : 0);
+                                                   kp, gram ? 1 : 0, jlen, part);
   WGP_CUDA(cudaGetLastError());
+  if (part) {
+    const int64_t count = nrows * s;
+    sum_splits_kernel<<<(int)std::min<int64_t>(148 * 8, (count + 255) / 256), 256, 0, st>>>(part, nsplit, count,
+                                                                                           B, Y);
+    WGP_CUDA(cudaGetLastError());
+  }
 }
 
 }  // namespace
 
-// fp64 kernel-matvec: DMMA kernel (RHS chunks of up to 128 columns); WGP_F64_SIMT=1 selects
+// fp64 kernel-matvec: DMMA kernel (one RHS group up to 136 columns -- the kernel entries are
+// evaluated once per group, so config 5's 129 columns run as one group -- else groups of
+// 128); WGP_F64_SIMT=1 selects
 // the all-CUDA-core kernel instead (validation).
 static void launch_f64(const Op& op, const double* Xr, int64_t nrows, int64_t row0,
                        const double* Xc, int64_t ncols, const double* V, int s, const double* B,
@@ -310,12 +348,13 @@ static void launch_f64(const Op& op, const double* Xr, int64_t nrows, int64_t ro
   WGP_REQUIRE(op.dim <= 32, "fp64 kmatvec: dim <= 32 supported, got %d", op.dim);
   const KParams kp = op.kp();
   const int dp = op.dpad, d = op.dim;
-  if (s <= 8) return launch_dmma<1>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
-  if (s <= 16) return launch_dmma<2>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
-  if (s <= 24) return launch_dmma<3>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
-  if (s <= 32) return launch_dmma<4>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
-  if (s <= 64) return launch_dmma<8>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
-  return launch_dmma<16>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, st);
+  if (s <= 8) return launch_dmma<1>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
+  if (s <= 16) return launch_dmma<2>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
+  if (s <= 24) return launch_dmma<3>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
+  if (s <= 32) return launch_dmma<4>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
+  if (s <= 64) return launch_dmma<8>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
+  if (s <= 136) return launch_dmma<17>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
+  return launch_dmma<16>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
 }
 
 template <typename T>
