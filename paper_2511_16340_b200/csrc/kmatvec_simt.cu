@@ -22,35 +22,6 @@ constexpr int BM = 64, BN = 64, NT = 256;
 template <typename T>
 __device__ __forceinline__ T kmap(T d2, const KParams& p);
 
-// e^x for x <= 0 in fp64 DFMA/integer ops: n = rn(x log2 e) via the 1.5*2^52 shifter,
-// r = x - n ln2 (Cody-Waite hi/lo, |r| <= ln2/2), e^r by its degree-11 Taylor polynomial
-// (max relative error 9e-15 over [-708, 0], measured against libm), 2^n inserted into the
-// exponent field.  x is clamped at -708 (e^-708 ~ 3e-308: below that a kernel entry
-// contributes nothing at fp64 resolution).  ~16 DP ops against ~25+ for the libdevice exp
-// with its special-case handling, on the pipe that bounds this kernel.
-__device__ __forceinline__ double exp_neg(double x) {
-  x = fmax(x, -708.0);
-  const double shifter = 6755399441055744.0;  // 1.5 * 2^52
-  const double t = fma(x, 1.4426950408889634, shifter);
-  const double n = t - shifter;
-  double r = fma(-n, 6.93147180369123816490e-01, x);
-  r = fma(-n, 1.90821492927058770002e-10, r);
-  double q = 2.505210838544171877505e-08;  // 1/11!
-  q = fma(q, r, 2.755731922398589065256e-07);
-  q = fma(q, r, 2.755731922398589065256e-06);
-  q = fma(q, r, 2.480158730158730158730e-05);
-  q = fma(q, r, 1.984126984126984126984e-04);
-  q = fma(q, r, 1.388888888888888888889e-03);
-  q = fma(q, r, 8.333333333333333333333e-03);
-  q = fma(q, r, 4.166666666666666666667e-02);
-  q = fma(q, r, 1.666666666666666666667e-01);
-  q = fma(q, r, 0.5);
-  q = fma(q, r, 1.0);
-  q = fma(q, r, 1.0);
-  const long long ni = __double_as_longlong(t) - __double_as_longlong(shifter);
-  return __longlong_as_double(__double_as_longlong(q) + (ni << 52));
-}
-
 template <>
 __device__ __forceinline__ double kmap<double>(double d2, const KParams& p) {
   d2 = d2 > 0.0 ? d2 : 0.0;

@@ -10,6 +10,8 @@
 // kernel-matvec (explicit differences; H(i,i) = s^2 + sigma_n^2 exactly), in the operator's
 // compute type (fp64, or fp32 for the fp32 precisions).  Per-column work of different
 // columns is independent, so batching columns never changes a column's result.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace wgp {
@@ -28,57 +30,63 @@ __device__ __forceinline__ T kentry(const T* __restrict__ xi, const T* __restric
   return T(p.s2) * (T(1) + z) * exp(-z);
 }
 
-// One block = 64 gathered rows of one column.  4 threads per row split the j range.
-template <typename T>
+__device__ __forceinline__ double kexp(double x) { return exp_neg(x); }  // x <= 0
+__device__ __forceinline__ float kexp(float x) { return expf(x); }
+
+// One block = 64 gathered rows of one column over one fixed-length j range (grid.z); 4
+// threads per row take every 4th j of each 64-column tile.  Partial sums go to
+// part[z][c][i] and krows_sum_kernel adds the ranges in order: the j ranges depend on n only,
+// so a row's value is the same whichever rank owns it.
+template <typename T, int DMAX>
 __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int dpad, int dim,
-                                                    int64_t n, const int* __restrict__ rows,
-                                                    int nb, const double* __restrict__ V,
-                                                    const double* __restrict__ Bm, int s,
+                                                    int64_t n, int64_t jlen,
+                                                    const int* __restrict__ rows, int nb,
+                                                    const double* __restrict__ V, int s,
                                                     const int* __restrict__ active, KParams p,
                                                     int64_t r0, int64_t r1,
-                                                    double* __restrict__ g) {
+                                                    double* __restrict__ part) {
   const int c = blockIdx.y;
   if (!active[c]) return;
-  __shared__ T sX[64][33];
+  __shared__ T sX[64][DMAX + 1];
   __shared__ double sV[64];
   __shared__ double red[256];
   const int tid = threadIdx.x;
   const int lr = tid >> 2, sub = tid & 3;
   const int bi = blockIdx.x * 64 + lr;
-  const int64_t row0 = bi < nb ? rows[(int64_t)c * nb + bi] : 0;
+  const int64_t row = bi < nb ? rows[(int64_t)c * nb + bi] : 0;
   // sharded: this rank owns rows [r0, r1) (B holds those rows only); other batch rows get 0
-  const bool own = bi < nb && row0 >= r0 && row0 < r1;
-  const bool valid = own;
-  const int64_t row = row0;
-  T xr[32];
+  const bool valid = bi < nb && row >= r0 && row < r1;
+  T xr[DMAX];
 #pragma unroll
-  for (int k = 0; k < 32; ++k) xr[k] = (valid && k < dim) ? X[row * dpad + k] : T(0);
+  for (int k = 0; k < DMAX; ++k) xr[k] = (valid && k < dim) ? X[row * dpad + k] : T(0);
+  const T s2 = T(p.s2), c1 = T(p.c1), kdiag = T(p.s2 + p.noise2);
+  const int64_t j_lo = (int64_t)blockIdx.z * jlen, j_hi = min(n, j_lo + jlen);
   double acc = 0.0;
-  for (int64_t j0 = 0; j0 < n; j0 += 64) {
+  for (int64_t j0 = j_lo; j0 < j_hi; j0 += 64) {
     __syncthreads();
-    for (int e = tid; e < 64 * dim; e += 256) {
-      const int j = e / dim, k = e % dim;
-      sX[j][k] = j0 + j < n ? X[(j0 + j) * dpad + k] : T(0);
+    for (int e = tid; e < 64 * DMAX; e += 256) {  // coordinates >= dim are zero
+      const int j = e / DMAX, k = e % DMAX;
+      sX[j][k] = (j0 + j < j_hi && k < dim) ? X[(j0 + j) * dpad + k] : T(0);
     }
-    if (tid < 64) sV[tid] = j0 + tid < n ? V[(j0 + tid) * s + c] : 0.0;
+    if (tid < 64) sV[tid] = j0 + tid < j_hi ? V[(j0 + tid) * s + c] : 0.0;
     __syncthreads();
     if (valid) {
-      for (int jj = sub; jj < 64 && j0 + jj < n; jj += 4) {
+      const int jn = (int)(j_hi - j0 < 64 ? j_hi - j0 : 64);
+      for (int jj = sub; jj < jn; jj += 4) {
         T d2 = T(0);
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < dim) {
-            const T df = xr[k] - sX[jj][k];
-            d2 = fma(df, df, d2);
-          }
+        for (int k = 0; k < DMAX; ++k) {
+          const T df = xr[k] - sX[jj][k];
+          d2 = fma(df, df, d2);
+        }
         T kv;
         if (j0 + jj == row) {
-          kv = T(p.s2 + p.noise2);
+          kv = kdiag;
         } else if (p.kind == WGP_RBF) {
-          kv = T(p.s2) * exp(-T(p.c1) * d2);
+          kv = s2 * kexp(-c1 * d2);
         } else {
-          const T z = T(p.c1) * sqrt(d2);
-          kv = T(p.s2) * (T(1) + z) * exp(-z);
+          const T z = c1 * sqrt(d2);
+          kv = s2 * (T(1) + z) * kexp(-z);
         }
         acc = fma((double)kv, sV[jj], acc);
       }
@@ -86,14 +94,27 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
   }
   red[tid] = acc;
   __syncthreads();
-  if (bi < nb && sub == 0) {
-    const double tot = ((red[tid] + red[tid + 1]) + red[tid + 2]) + red[tid + 3];
-    g[(int64_t)c * nb + bi] = own ? tot - Bm[(row - r0) * s + c] : 0.0;
-  }
+  if (bi < nb && sub == 0)
+    part[((int64_t)blockIdx.z * s + c) * nb + bi] = ((red[tid] + red[tid + 1]) + red[tid + 2]) + red[tid + 3];
+}
+
+// g[c][i] = sum over the j ranges in order - b_c[row] (owned rows; 0 elsewhere).
+__global__ void krows_sum_kernel(const double* __restrict__ part, int nsplit, const int* __restrict__ rows,
+                                 int nb, const double* __restrict__ Bm, int s,
+                                 const int* __restrict__ active, int64_t r0, int64_t r1,
+                                 double* __restrict__ g) {
+  const int c = blockIdx.y;
+  const int bi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bi >= nb || !active[c]) return;
+  const int64_t row = rows[(int64_t)c * nb + bi];
+  const bool own = row >= r0 && row < r1;
+  double tot = 0.0;
+  for (int q = 0; q < nsplit; ++q) tot += part[((int64_t)q * s + c) * nb + bi];
+  g[(int64_t)c * nb + bi] = own ? tot - Bm[(row - r0) * s + c] : 0.0;
 }
 
 // r[i, c] -= sum_{j in block_c} H[i, j] delta[j - start_c, c]    (thread per row i)
-template <typename T>
+template <typename T, int DMAX>
 __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int dpad, int dim,
                                                     int64_t n, const int* __restrict__ blk,
                                                     int bs, const double* __restrict__ delta,
@@ -103,22 +124,23 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
   // rows r0 .. r0 + nrows of the operator (this rank's), R holds those rows
   const int c = blockIdx.y;
   if (!active[c]) return;
-  __shared__ T sX[64][33];
+  __shared__ T sX[64][DMAX + 1];
   __shared__ double sD[64];
   const int64_t il = (int64_t)blockIdx.x * 128 + threadIdx.x;
   const bool valid = il < nrows;
   const int64_t i = r0 + il;
   const int64_t start = (int64_t)blk[c] * bs;
   const int len = (int)min((int64_t)bs, n - start);
-  T xr[32];
+  T xr[DMAX];
 #pragma unroll
-  for (int k = 0; k < 32; ++k) xr[k] = (valid && k < dim) ? X[i * dpad + k] : T(0);
+  for (int k = 0; k < DMAX; ++k) xr[k] = (valid && k < dim) ? X[i * dpad + k] : T(0);
+  const T s2 = T(p.s2), c1 = T(p.c1), kdiag = T(p.s2 + p.noise2);
   double acc = 0.0;
   for (int j0 = 0; j0 < len; j0 += 64) {
     __syncthreads();
-    for (int e = threadIdx.x; e < 64 * dim; e += 128) {
-      const int j = e / dim, k = e % dim;
-      sX[j][k] = j0 + j < len ? X[(start + j0 + j) * dpad + k] : T(0);
+    for (int e = threadIdx.x; e < 64 * DMAX; e += 128) {  // coordinates >= dim are zero
+      const int j = e / DMAX, k = e % DMAX;
+      sX[j][k] = (j0 + j < len && k < dim) ? X[(start + j0 + j) * dpad + k] : T(0);
     }
     if (threadIdx.x < 64) sD[threadIdx.x] = j0 + threadIdx.x < len ? delta[(int64_t)(j0 + threadIdx.x) * s + c] : 0.0;
     __syncthreads();
@@ -127,19 +149,18 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
       for (int jj = 0; jj < m; ++jj) {
         T d2 = T(0);
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < dim) {
-            const T df = xr[k] - sX[jj][k];
-            d2 = fma(df, df, d2);
-          }
+        for (int k = 0; k < DMAX; ++k) {
+          const T df = xr[k] - sX[jj][k];
+          d2 = fma(df, df, d2);
+        }
         T kv;
         if (start + j0 + jj == i) {
-          kv = T(p.s2 + p.noise2);
+          kv = kdiag;
         } else if (p.kind == WGP_RBF) {
-          kv = T(p.s2) * exp(-T(p.c1) * d2);
+          kv = s2 * kexp(-c1 * d2);
         } else {
-          const T z = T(p.c1) * sqrt(d2);
-          kv = T(p.s2) * (T(1) + z) * exp(-z);
+          const T z = c1 * sqrt(d2);
+          kv = s2 * (T(1) + z) * kexp(-z);
         }
         acc = fma((double)kv, sD[jj], acc);
       }
@@ -311,28 +332,59 @@ inline int grid_for(int64_t total) {
 
 }  // namespace
 
+template <typename T, int DM>
+static void krows_launch(const Op& op, const T* X, dim3 grid, int64_t jlen, const int* rows, int nb,
+                         const double* V, int s, const int* active, int64_t r0, int64_t r1,
+                         cudaStream_t st) {
+  krows_kernel<T, DM><<<grid, 256, 0, st>>>(X, op.dpad, op.dim, op.n, jlen, rows, nb, V, s, active, op.kp(),
+                                            r0, r1, op.krows_part.p);
+}
+
 void launch_krows(const Op& op, const int* rows, int nb, const double* V, const double* B, int s,
                   const int* active, double* g, int64_t r0, int64_t r1, cudaStream_t st) {
-  dim3 grid(ceil_div(nb, 64), s);
-  if (op.f64())
-    krows_kernel<double><<<grid, 256, 0, st>>>(op.X64.p, op.dpad, op.dim, op.n, rows, nb, V, B, s,
-                                               active, op.kp(), r0, r1, g);
-  else
-    krows_kernel<float><<<grid, 256, 0, st>>>(op.X32.p, op.dpad, op.dim, op.n, rows, nb, V, B, s,
-                                              active, op.kp(), r0, r1, g);
+  // fixed j ranges of >= 1024 columns (at most 64), a function of n only
+  const int64_t n = op.n;
+  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / 1024));
+  const int64_t jlen = (((n + nsplit - 1) / nsplit + 63) / 64) * 64;
+  op.krows_part.ensure((size_t)nsplit * s * nb);
+  const dim3 grid(ceil_div(nb, 64), s, nsplit);
+  const int d = op.dim;
+  if (op.f64()) {
+    if (d <= 8) krows_launch<double, 8>(op, op.X64.p, grid, jlen, rows, nb, V, s, active, r0, r1, st);
+    else if (d <= 16) krows_launch<double, 16>(op, op.X64.p, grid, jlen, rows, nb, V, s, active, r0, r1, st);
+    else krows_launch<double, 32>(op, op.X64.p, grid, jlen, rows, nb, V, s, active, r0, r1, st);
+  } else {
+    if (d <= 8) krows_launch<float, 8>(op, op.X32.p, grid, jlen, rows, nb, V, s, active, r0, r1, st);
+    else if (d <= 16) krows_launch<float, 16>(op, op.X32.p, grid, jlen, rows, nb, V, s, active, r0, r1, st);
+    else krows_launch<float, 32>(op, op.X32.p, grid, jlen, rows, nb, V, s, active, r0, r1, st);
+  }
   WGP_CUDA(cudaGetLastError());
+  krows_sum_kernel<<<dim3(ceil_div(nb, 128), s), 128, 0, st>>>(op.krows_part.p, nsplit, rows, nb, B, s,
+                                                               active, r0, r1, g);
+  WGP_CUDA(cudaGetLastError());
+}
+
+template <typename T, int DM>
+static void kcols_launch(const Op& op, const T* X, dim3 grid, const int* blk, int bs, const double* delta,
+                         int s, const int* active, int64_t r0, int64_t nrows, double* R, cudaStream_t st) {
+  kcols_kernel<T, DM><<<grid, 128, 0, st>>>(X, op.dpad, op.dim, op.n, blk, bs, delta, s, active, op.kp(),
+                                            r0, nrows, R);
 }
 
 void launch_kcols(const Op& op, const int* blk, int bs, const double* delta, int s,
                   const int* active, double* R, int64_t r0, int64_t nrows, cudaStream_t st) {
   if (nrows <= 0) return;
-  dim3 grid(ceil_div(nrows, 128), s);
-  if (op.f64())
-    kcols_kernel<double><<<grid, 128, 0, st>>>(op.X64.p, op.dpad, op.dim, op.n, blk, bs, delta, s,
-                                               active, op.kp(), r0, nrows, R);
-  else
-    kcols_kernel<float><<<grid, 128, 0, st>>>(op.X32.p, op.dpad, op.dim, op.n, blk, bs, delta, s,
-                                              active, op.kp(), r0, nrows, R);
+  const dim3 grid(ceil_div(nrows, 128), s);
+  const int d = op.dim;
+  if (op.f64()) {
+    if (d <= 8) kcols_launch<double, 8>(op, op.X64.p, grid, blk, bs, delta, s, active, r0, nrows, R, st);
+    else if (d <= 16) kcols_launch<double, 16>(op, op.X64.p, grid, blk, bs, delta, s, active, r0, nrows, R, st);
+    else kcols_launch<double, 32>(op, op.X64.p, grid, blk, bs, delta, s, active, r0, nrows, R, st);
+  } else {
+    if (d <= 8) kcols_launch<float, 8>(op, op.X32.p, grid, blk, bs, delta, s, active, r0, nrows, R, st);
+    else if (d <= 16) kcols_launch<float, 16>(op, op.X32.p, grid, blk, bs, delta, s, active, r0, nrows, R, st);
+    else kcols_launch<float, 32>(op, op.X32.p, grid, blk, bs, delta, s, active, r0, nrows, R, st);
+  }
   WGP_CUDA(cudaGetLastError());
 }
 

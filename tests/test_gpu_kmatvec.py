@@ -185,3 +185,20 @@ def test_tc_split_grids(W, n, s):
         ref = W.KernelOperator(h, X, precision=W.F64).kmatvec(V)
         got = W.KernelOperator(h, X, precision=W.F32_3XTF32).kmatvec(V)
         assert colrel(got, ref) <= 2e-5, (n, s, kind)
+
+
+@pytest.mark.parametrize("s", [17, 129])
+def test_f64_column_splits_batch_independent(W, O, s):
+    """fp64 kernel-matvec past one 4096-column split (n = 9000: three splits summed in order):
+    each column equals its single-column product bitwise (the batched-vs-sequential contract of
+    solve_many, test_solvers.cpp:397-413) and matches the oracle at the fp64 bar."""
+    n = 9000
+    X = O.uniform_inputs(77, n, 3)
+    V = np.random.default_rng(s).standard_normal((n, s))
+    h = O.KernelHyperparams(0.3, 1.0, 0.1, O.MATERN32)
+    op = W.KernelOperator(W.KernelHyperparams(0.3, 1.0, 0.1, W.MATERN32), X, precision=W.F64)
+    Y = op.kmatvec(V)
+    for c in (0, s // 2, s - 1):
+        assert np.array_equal(Y[:, c], op.kmatvec(V[:, c:c + 1])[:, 0]), c
+    ref = O.kmatvec(X, h, V[:, :3])
+    assert colrel(Y[:, :3], ref) <= 1e-10
