@@ -212,6 +212,53 @@ def cg_time_to_tolerance(W, ctx, X, prec, hyp, tol=1e-4, seed=0):
             "warm_over_cold_iters": warm["iters_mean"] / max(cold["iters_mean"], 1e-9)}
 
 
+def vector_kernels_gbs(W, ctx, n, stream, flush, peaks, reps=20):
+    """North-star item (2): the fused solver vector kernels of one CG iteration
+    (solvers.cpp:163-180) on [n][S] fp64 arrays at the C3 shape, through the C-ABI device
+    entry points, timed with CUDA events on the launching stream, L2 flushed before each
+    launch by READING a 256 MiB buffer (a memset flush leaves 126 MB of dirty lines that the
+    timed kernel would then have to write back).  Algorithmic bytes: axpy/xpby read two arrays and write one (24 B per element),
+    a dot reads two (16 B per element)."""
+    import torch
+
+    dt = torch.float64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(n, S, device="cuda", dtype=dt, generator=g)
+    B = torch.randn(n, S, device="cuda", dtype=dt, generator=g)
+    coef = torch.rand(S, device="cuda", dtype=dt, generator=g) + 0.5
+    act = torch.ones(S, device="cuda", dtype=torch.int32)
+    out = torch.empty(S, device="cuda", dtype=dt)
+    work = torch.empty(((n + 511) // 512) * S, device="cuda", dtype=dt)
+    sp = stream.cuda_stream
+    rd = flush.view(torch.float64)
+    sink = torch.empty((), device="cuda", dtype=dt)
+    ops = {
+        "axpy_cols (v += alpha p)": (lambda: ctx.axpy_cols_dev(A.data_ptr(), B.data_ptr(), coef.data_ptr(), n, S, sp), 24),
+        "xpby_cols (p = z + beta p)": (lambda: ctx.xpby_cols_dev(A.data_ptr(), B.data_ptr(), coef.data_ptr(),
+                                                                  act.data_ptr(), n, S, sp), 24),
+        "coldots (p.Hp, r.z, |r|^2)": (lambda: ctx.coldots_dev(A.data_ptr(), B.data_ptr(), n, S, out.data_ptr(),
+                                                               work.data_ptr(), sp), 16),
+    }
+    res = {}
+    for name, (fn, bpe) in ops.items():
+        for _ in range(3):
+            fn()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a, b in ev:
+            torch.sum(rd, dim=0, out=sink)  # read-only L2 flush
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in ev]))
+        gbs = n * S * bpe / (ms * 1e-3) / 1e9
+        res[name] = {"us": ms * 1e3, "GB/s": gbs, "frac_hbm": gbs / peaks["hbm_gbs"],
+                     "bytes": n * S * bpe}
+    res["shape"] = f"[{n}][{S}] fp64, L2 flushed (256 MiB read) per launch, median of {reps}"
+    res["peak_hbm_gbs"] = peaks["hbm_gbs"]
+    return res
+
+
 # --------------------------------------------------------------------------- GPU arm
 def run_ours(args):
     import torch
@@ -330,6 +377,10 @@ def run_ours(args):
                           "note": "SFU roofline at sm_max_mhz (16 MUFU ops/clk/SM, measured by "
                                   "tools/mufu_microbench.cu): the Matern map's sqrt+exp2 per pair"}}
 
+    vec = None
+    if world == 1:
+        vec = vector_kernels_gbs(W, ctx, n, stream, flush, peaks)
+
     cg = None
     if world == 1 and not args.no_cg:
         cg = cg_time_to_tolerance(W, ctx, X, prec, hyp)
@@ -354,6 +405,7 @@ def run_ours(args):
                        "rows_per_rank": r1 - r0, "l2": "flushed (256 MiB memset) before each step"},
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": 5 * args.steps,  # colmax + colscale_finish + split_v + kmatvec_tc + reduce_splits per step
             "cg_warm_vs_cold": cg,
+            "vector_kernels": vec,
             "clocks": clk.summary(), "wall_s": t_wall,
             "step_ms_min": float(np.min(ms)), "step_ms_max": float(np.max(ms)),
         }

@@ -131,6 +131,21 @@ wgp_status wgp_kmatvec_dev(wgp_op* op, const void* dV, void* dY, int s, void* st
 /* dY = dB - H dV (true residual b - H v, solvers.cpp:150,171,203,231,268,293,298). */
 wgp_status wgp_residual_dev(wgp_op* op, const void* dB, const void* dV, void* dY, int s,
                             void* stream);
+/* ---- fused solver vector kernels on device [n][s] row-major fp64 arrays (the
+ *      per-iteration vector work of cg_solve_with, solvers.cpp:163-180), asynchronous on
+ *      `stream` (NULL: the context stream).  dAlpha/dBeta: s fp64; dActive: s int32. ---- */
+/* dY[:, c] += alpha_c dX[:, c] for alpha_c != 0   (res.v += alpha * p, solvers.cpp:168) */
+wgp_status wgp_axpy_cols_dev(wgp_ctx* ctx, void* dY, const void* dX, const void* dAlpha,
+                             int64_t n, int s, void* stream);
+/* dP[:, c] = dZ[:, c] + beta_c dP[:, c] where dActive[c] != 0   (p = z + beta p, :180) */
+wgp_status wgp_xpby_cols_dev(wgp_ctx* ctx, void* dP, const void* dZ, const void* dBeta,
+                             const void* dActive, int64_t n, int s, void* stream);
+/* dOut[c] = sum_i dA[i, c] dB[i, c] (p.dot(Hp) :163, r.norm() :172, r.dot(z) :179) in the
+ * solvers' fixed order: 512-row chunks, each as 32 sequential 16-row slabs added in slab
+ * order, chunks added in index order -- independent of s and of sharding.  dWork: at least
+ * ceil(n / 512) * s fp64. */
+wgp_status wgp_coldots_dev(wgp_ctx* ctx, const void* dA, const void* dB, int64_t n, int s,
+                           void* dOut, void* dWork, void* stream);
 /* Cross mode Y = K(X*, X) W, no noise term (cross_kernel kernel.cpp:74-89 times
  * weights, as in eval_posterior sampling.cpp:66-75).  Host column-major fp64. */
 wgp_status wgp_cross_matvec(wgp_op* op, const double* Xstar, int64_t m, int64_t ldx,

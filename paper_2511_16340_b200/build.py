@@ -50,6 +50,25 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def _nccl_link() -> list:
+    """Link NCCL from the torch-bundled wheel when present (the same libnccl.so.2 soname
+    torch loads: whichever of torch and this library loads first, the process then holds
+    one NCCL that both can use -- the system 2.27 lacks symbols torch 2.11 needs), else the
+    system library."""
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+        dirs = [os.path.join(p, "lib") for p in (spec.submodule_search_locations or [])] if spec else []
+    except Exception:  # noqa: BLE001
+        dirs = []
+    for d in dirs:
+        if os.path.exists(os.path.join(d, "libnccl.so.2")):
+            return ["-L" + d, "-l:libnccl.so.2", "-Xlinker", "-rpath," + d,
+                    "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+    return ["-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
@@ -57,7 +76,7 @@ def build(verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, *_nccl_link()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

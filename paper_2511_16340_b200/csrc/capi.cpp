@@ -4,7 +4,10 @@
 // message; no exception crosses the ABI.  Host buffers use the reference's Eigen layout
 // (column-major fp64); they are converted to the device layout on the GPU.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -63,20 +66,46 @@ static wgp_status guard(F&& f) {
 
 static void set_device(const Ctx& ctx) { WGP_CUDA(cudaSetDevice(ctx.device)); }
 
+// Opt-in phase timing of a solve (WGP_PHASE_TIMING=1): synchronises the stream at each
+// phase boundary and prints wall times to stderr.  Off by default (no extra syncs).
+struct PhaseTimer {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(cudaStream_t s) : st(s) {
+    const char* e = getenv("WGP_PHASE_TIMING");
+    on = e && atoi(e) != 0;
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    WGP_CUDA(cudaStreamSynchronize(st));
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[wgp phase] %-14s %9.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int64_t ldb, int s,
                       const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
                       SolveOutputs& out, bool derive_seeds) {
   cudaStream_t st = op.ctx->stream;
+  PhaseTimer pt(st);
   SolverWork<double> w;
   w.alloc(op, s);
+  pt.mark("alloc");
   upload_problem<double>(op, w, B, ldb, U1, ldu, n1, st);
+  pt.mark("upload");
   switch (cfg.method) {
     case WGP_CG: {
       PrecondDev pd;
       const int64_t rank = std::min<int64_t>(cfg.precond_rank, op.n);  // from_matrix :125-126
       if (rank > 0) {
         build_pivoted_cholesky(op, rank, pd, st);
+        pt.mark("pivchol");
         finish_preconditioner(op, cfg.precond_shift, cfg.precond_shift_mode, pd, st);
+        pt.mark("precond");
       } else {
         int64_t a, b;
         op.local_rows(&a, &b);
@@ -85,6 +114,7 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
         pd.n_local = b - a;
       }
       cg_solve_batched<double>(op, cfg, pd, w, out, st);
+      pt.mark("cg_loop");
       break;
     }
     case WGP_SGD: {
@@ -102,6 +132,7 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
       throw_error(WGP_INVALID_ARGUMENT, "solve: unknown method");
   }
   download_solution<double>(w, V, ldv, st);
+  pt.mark("download");
 }
 
 }  // namespace wgp
@@ -279,6 +310,39 @@ wgp_status wgp_residual_dev(wgp_op* op, const void* dB, const void* dV, void* dY
     WGP_REQUIRE(op->n >= 1, "wgp_residual_dev: empty operator");
     cudaStream_t st = stream ? (cudaStream_t)stream : op->ctx->stream;
     launch_residual(*op, (const double*)dB, (const double*)dV, (double*)dY, s, st);
+  });
+}
+
+wgp_status wgp_axpy_cols_dev(wgp_ctx* ctx, void* dY, const void* dX, const void* dAlpha,
+                             int64_t n, int s, void* stream) {
+  return guard([&] {
+    WGP_REQUIRE(ctx && dY && dX && dAlpha && n >= 0 && s >= 1, "wgp_axpy_cols_dev: bad argument");
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    launch_axpy_cols<double>((double*)dY, (const double*)dX, (const double*)dAlpha, n, s, st);
+  });
+}
+
+wgp_status wgp_xpby_cols_dev(wgp_ctx* ctx, void* dP, const void* dZ, const void* dBeta,
+                             const void* dActive, int64_t n, int s, void* stream) {
+  return guard([&] {
+    WGP_REQUIRE(ctx && dP && dZ && dBeta && dActive && n >= 0 && s >= 1,
+                "wgp_xpby_cols_dev: bad argument");
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    launch_xpby_cols<double>((double*)dP, (const double*)dZ, (const double*)dBeta,
+                             (const int*)dActive, n, s, st);
+  });
+}
+
+wgp_status wgp_coldots_dev(wgp_ctx* ctx, const void* dA, const void* dB, int64_t n, int s,
+                           void* dOut, void* dWork, void* stream) {
+  return guard([&] {
+    WGP_REQUIRE(ctx && dA && dB && dOut && dWork && n >= 1 && s >= 1,
+                "wgp_coldots_dev: bad argument");
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    const int nch = (int)((n + kChunkRows - 1) / kChunkRows);
+    launch_coldots<double>((const double*)dA, (const double*)dB, nullptr, nullptr, n, s,
+                           (double*)dWork, st);
+    launch_chunk_sum((const double*)dWork, nch, s, (double*)dOut, st);
   });
 }
 

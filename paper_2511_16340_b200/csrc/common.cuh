@@ -158,6 +158,24 @@ struct Op {
   }
 };
 
+// Sum of chunk partials part[q * stride] for q = 0..nch-1 in index order (the fixed order
+// that keeps sums independent of s and of the world size).  The loads are independent of the
+// running sum, so they are issued 8 ahead instead of one dependent L2 round trip per chunk.
+__device__ __forceinline__ double chunk_sum_ordered(const double* __restrict__ part, int nch,
+                                                    int64_t stride) {
+  double acc = 0.0;
+  int q = 0;
+  for (; q + 8 <= nch; q += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = part[(int64_t)(q + k) * stride];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += v[k];
+  }
+  for (; q < nch; ++q) acc += part[(int64_t)q * stride];
+  return acc;
+}
+
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // ------------------------------------------------------------------ collectives (dist.cpp)
@@ -179,6 +197,7 @@ void launch_rows_to_colmajor(const void* src, int64_t n, int s, double* dst, int
 template <typename T>
 void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t n, int s,
                     double* part, cudaStream_t st);  // part: [nchunks][nq][s]
+void launch_chunk_sum(const double* part, int nch, int s, double* out, cudaStream_t st);
 template <typename T>
 void launch_axpy_cols(T* Y, const T* X, const double* alpha, int64_t n, int s, cudaStream_t st);
 template <typename T>

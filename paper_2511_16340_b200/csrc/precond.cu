@@ -188,9 +188,7 @@ __global__ void __launch_bounds__(256) chunk_atb_kernel(const double* __restrict
 __global__ void sum_partials_kernel(const double* __restrict__ part, int np, int count,
                                     double* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int q = 0; q < np; ++q) acc += part[(int64_t)q * count + e];
-    out[e] = acc;
+    out[e] = chunk_sum_ordered(part + e, np, count);
   }
 }
 

@@ -21,8 +21,7 @@ namespace {
 __global__ void init_bnorm_kernel(const double* __restrict__ part, int nch, int s,
                                   double* __restrict__ bnorm, int* __restrict__ active) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int q = 0; q < nch; ++q) acc += part[(int64_t)q * s + c];
+    const double acc = chunk_sum_ordered(part + c, nch, s);
     bnorm[c] = sqrt(acc);
     active[c] = acc != 0.0;  // zero RHS: zero_rhs_result (solvers.cpp:51-58, :145)
   }
@@ -33,8 +32,7 @@ __global__ void resid_step_kernel(const double* __restrict__ part, int nch, int 
                                   const double* __restrict__ bnorm, double tol,
                                   double* __restrict__ rel, int* __restrict__ active) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int q = 0; q < nch; ++q) acc += part[((int64_t)q * nq) * s + c];
+    const double acc = chunk_sum_ordered(part + c, nch, (int64_t)nq * s);
     const double r = bnorm[c] > 0.0 ? sqrt(acc) / bnorm[c] : 0.0;
     rel[c] = r;
     if (active[c] && r <= tol) active[c] = 0;
@@ -45,8 +43,7 @@ __global__ void cg_alpha_kernel(const double* __restrict__ part, int nch, int s,
                                 const double* __restrict__ rz, const int* __restrict__ active,
                                 double* __restrict__ alpha, int* __restrict__ fail_col) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
-    double pHp = 0.0;
-    for (int q = 0; q < nch; ++q) pHp += part[(int64_t)q * s + c];
+    const double pHp = chunk_sum_ordered(part + c, nch, s);
     if (!active[c]) {
       alpha[c] = 0.0;
       continue;
@@ -61,8 +58,7 @@ __global__ void cg_beta_kernel(const double* __restrict__ part, int nch, int s,
                                double* __restrict__ rz, const int* __restrict__ active,
                                double* __restrict__ beta, int init) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
-    double rzn = 0.0;
-    for (int q = 0; q < nch; ++q) rzn += part[(int64_t)q * s + c];
+    const double rzn = chunk_sum_ordered(part + c, nch, s);
     if (init) {
       rz[c] = rzn;
       beta[c] = 0.0;

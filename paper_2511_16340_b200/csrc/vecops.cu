@@ -5,6 +5,8 @@
 // Reductions are deterministic and world-size independent: each block reduces one
 // kChunkRows-row chunk in a fixed order to fp64 partials part[chunk][q][c]; the
 // scalar-step kernels (solver_kernels.cu) then add the chunks in index order.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace wgp {
@@ -49,39 +51,66 @@ __global__ void rows_to_colmajor_kernel(const T* __restrict__ src, int64_t n, in
   }
 }
 
-// One block per chunk.  Per column the chunk is cut into 32 fixed 16-row slabs summed
+// One block per (chunk, group of up to 32 columns).  Per column the chunk is cut into 32 fixed 16-row slabs summed
 // sequentially, then the 32 slab sums are added in slab order: the order of every column's
 // sum depends only on the row index, never on s or on the other columns (solve_many must
 // equal single-RHS solves bitwise, test_solvers.cpp:397-413).
 constexpr int kSlabRows = kChunkRows / 32;
+constexpr int kColsPerBlock = 32;  // coldots: columns per block (x 8 slabs = 256 threads)
 
 template <typename T, int NQ>
 __global__ void __launch_bounds__(256) coldots_kernel(const T* __restrict__ A0,
                                                       const T* __restrict__ B0,
                                                       const T* __restrict__ A1,
                                                       const T* __restrict__ B1, int64_t n, int s,
-                                                      double* __restrict__ part) {
-  extern __shared__ double red[];  // [NQ][32][s]
+                                                      int cb, int spp, double* __restrict__ part) {
+  // block (chunk, group of cb <= 32 columns): threads = cb columns x spp slabs, the 32 slabs
+  // in passes of spp; a warp reads whole row segments of up to 256 contiguous bytes
+  __shared__ double red[NQ][32][kColsPerBlock];
   const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
-  for (int f = threadIdx.x; f < 32 * s; f += blockDim.x) {
-    const int q = f / s, c = f % s;
+  const int cl = threadIdx.x % cb;
+  const int c = blockIdx.y * cb + cl;
+  for (int q = threadIdx.x / cb; q < 32; q += spp) {
+    if (c >= s) break;
     const int64_t i0 = r0 + (int64_t)q * kSlabRows;
     const int64_t i1 = min(n, i0 + kSlabRows);
     double a0 = 0.0, a1 = 0.0;
-    for (int64_t i = i0; i < i1; ++i) {
-      const int64_t e = i * s + c;
-      a0 = fma((double)A0[e], (double)B0[e], a0);
-      if (NQ > 1) a1 = fma((double)A1[e], (double)B1[e], a1);
+    const T* pa0 = A0 + i0 * s + c;
+    const T* pb0 = B0 + i0 * s + c;
+    const T* pa1 = A1 + i0 * s + c;
+    const T* pb1 = B1 + i0 * s + c;
+    if (i1 - i0 == kSlabRows) {
+      // full slab: all its loads issued before the (ordered) FMA chain
+      T xa[kSlabRows], xb[kSlabRows], ya[NQ > 1 ? kSlabRows : 1], yb[NQ > 1 ? kSlabRows : 1];
+#pragma unroll
+      for (int k = 0; k < kSlabRows; ++k) {
+        xa[k] = pa0[(int64_t)k * s];
+        xb[k] = pb0[(int64_t)k * s];
+        if (NQ > 1) {
+          ya[k] = pa1[(int64_t)k * s];
+          yb[k] = pb1[(int64_t)k * s];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kSlabRows; ++k) {
+        a0 = fma((double)xa[k], (double)xb[k], a0);
+        if (NQ > 1) a1 = fma((double)ya[k], (double)yb[k], a1);
+      }
+    } else {
+      for (int64_t k = 0; k < i1 - i0; ++k) {
+        a0 = fma((double)pa0[k * s], (double)pb0[k * s], a0);
+        if (NQ > 1) a1 = fma((double)pa1[k * s], (double)pb1[k * s], a1);
+      }
     }
-    red[q * s + c] = a0;
-    if (NQ > 1) red[(32 + q) * s + c] = a1;
+    red[0][q][cl] = a0;
+    if (NQ > 1) red[NQ - 1][q][cl] = a1;
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < s; c += blockDim.x) {
+  if (threadIdx.x < cb && c < s) {
     double t0 = 0.0, t1 = 0.0;
-    for (int q = 0; q < 32; ++q) {
-      t0 += red[q * s + c];
-      if (NQ > 1) t1 += red[(32 + q) * s + c];
+    for (int k = 0; k < 32; ++k) {
+      t0 += red[0][k][cl];
+      if (NQ > 1) t1 += red[NQ - 1][k][cl];
     }
     double* out = part + (int64_t)blockIdx.x * NQ * s;
     out[c] = t0;
@@ -89,24 +118,83 @@ __global__ void __launch_bounds__(256) coldots_kernel(const T* __restrict__ A0,
   }
 }
 
+// Column sums of chunk partials part[chunk][s] in chunk order (the scalar-step kernels'
+// order), for the standalone device dot product of the C-ABI.
+__global__ void chunk_sum_kernel(const double* __restrict__ part, int nch, int s,
+                                 double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= s) return;
+  out[c] = chunk_sum_ordered(part + c, nch, s);
+}
+
+// Element-wise column updates of [n][s] arrays.  The grid covers `rows_step` whole rows per
+// step (rows_step * s threads), so every thread keeps one column -- its coefficient and
+// activity flag stay in registers, with no index division in the loop -- and a warp still
+// touches consecutive addresses.
 template <typename T>
-__global__ void axpy_cols_kernel(T* __restrict__ Y, const T* __restrict__ X,
-                                 const double* __restrict__ alpha, int64_t total, int s) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const double a = alpha[e % s];
-    if (a != 0.0) Y[e] = (T)((double)Y[e] + a * (double)X[e]);
-  }
+__global__ void __launch_bounds__(256) axpy_cols_kernel(T* __restrict__ Y, const T* __restrict__ X,
+                                                        const double* __restrict__ alpha,
+                                                        int64_t total, int s, int64_t stride) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= stride) return;
+  const double a = alpha[t % s];
+  if (a == 0.0) return;
+#pragma unroll 4
+  for (int64_t e = t; e < total; e += stride) Y[e] = (T)((double)Y[e] + a * (double)X[e]);
 }
 
 template <typename T>
-__global__ void xpby_cols_kernel(T* __restrict__ P, const T* __restrict__ Z,
-                                 const double* __restrict__ beta, const int* __restrict__ active,
-                                 int64_t total, int s) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % s);
-    if (active[c]) P[e] = (T)((double)Z[e] + beta[c] * (double)P[e]);
+__global__ void __launch_bounds__(256) xpby_cols_kernel(T* __restrict__ P, const T* __restrict__ Z,
+                                                        const double* __restrict__ beta,
+                                                        const int* __restrict__ active,
+                                                        int64_t total, int s, int64_t stride) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= stride) return;
+  const int c = (int)(t % s);
+  if (!active[c]) return;
+  const double b = beta[c];
+#pragma unroll 4
+  for (int64_t e = t; e < total; e += stride) P[e] = (T)((double)Z[e] + b * (double)P[e]);
+}
+
+// fp64 pairs (s even): 16-byte accesses, one column pair per thread
+__global__ void __launch_bounds__(256) axpy_cols2_kernel(double2* __restrict__ Y,
+                                                         const double2* __restrict__ X,
+                                                         const double* __restrict__ alpha,
+                                                         int64_t total2, int s2, int64_t stride2) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= stride2) return;
+  const int c = 2 * (int)(t % s2);
+  const double a0 = alpha[c], a1 = alpha[c + 1];
+  if (a0 == 0.0 && a1 == 0.0) return;
+#pragma unroll 4
+  for (int64_t e = t; e < total2; e += stride2) {
+    double2 y = Y[e];
+    const double2 x = X[e];
+    if (a0 != 0.0) y.x = y.x + a0 * x.x;
+    if (a1 != 0.0) y.y = y.y + a1 * x.y;
+    Y[e] = y;
+  }
+}
+
+__global__ void __launch_bounds__(256) xpby_cols2_kernel(double2* __restrict__ P,
+                                                         const double2* __restrict__ Z,
+                                                         const double* __restrict__ beta,
+                                                         const int* __restrict__ active,
+                                                         int64_t total2, int s2, int64_t stride2) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= stride2) return;
+  const int c = 2 * (int)(t % s2);
+  const bool on0 = active[c] != 0, on1 = active[c + 1] != 0;
+  if (!on0 && !on1) return;
+  const double b0 = beta[c], b1 = beta[c + 1];
+#pragma unroll 4
+  for (int64_t e = t; e < total2; e += stride2) {
+    double2 pv = P[e];
+    const double2 z = Z[e];
+    if (on0) pv.x = z.x + b0 * pv.x;
+    if (on1) pv.y = z.y + b1 * pv.y;
+    P[e] = pv;
   }
 }
 
@@ -153,26 +241,42 @@ void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t 
   if (s <= 0) return;
   const int nch = ceil_div(n, kChunkRows);
   if (nch <= 0) return;
-  const size_t smem = sizeof(double) * 32 * s * (A1 ? 2 : 1);
-  if (A1) {
-    if (smem > 48 * 1024)
-      WGP_CUDA(cudaFuncSetAttribute(coldots_kernel<T, 2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    coldots_kernel<T, 2><<<nch, 256, smem, st>>>(A0, B0, A1, B1, n, s, part);
-  } else {
-    if (smem > 48 * 1024)
-      WGP_CUDA(cudaFuncSetAttribute(coldots_kernel<T, 1>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    coldots_kernel<T, 1><<<nch, 256, smem, st>>>(A0, B0, A0, B0, n, s, part);
-  }
+  const int cb = s < kColsPerBlock ? s : kColsPerBlock;
+  const int spp = std::min(32, 256 / cb);  // slabs per pass
+  const dim3 grid(nch, ceil_div(s, cb));
+  if (A1)
+    coldots_kernel<T, 2><<<grid, cb * spp, 0, st>>>(A0, B0, A1, B1, n, s, cb, spp, part);
+  else
+    coldots_kernel<T, 1><<<grid, cb * spp, 0, st>>>(A0, B0, A0, B0, n, s, cb, spp, part);
   WGP_CUDA(cudaGetLastError());
+}
+
+void launch_chunk_sum(const double* part, int nch, int s, double* out, cudaStream_t st) {
+  if (s <= 0) return;
+  chunk_sum_kernel<<<(s + 127) / 128, 128, 0, st>>>(part, nch, s, out);
+  WGP_CUDA(cudaGetLastError());
+}
+
+// rows per grid step: about 2048 resident threads per SM, whole rows
+static int64_t col_stride(int64_t n, int s) {
+  const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)148 * 2048 / s));
+  return rows * s;
 }
 
 template <typename T>
 void launch_axpy_cols(T* Y, const T* X, const double* alpha, int64_t n, int s, cudaStream_t st) {
   const int64_t total = n * s;
   if (total <= 0) return;
-  axpy_cols_kernel<T><<<grid_for(total), 256, 0, st>>>(Y, X, alpha, total, s);
+  if (std::is_same<T, double>::value && s % 2 == 0 && ((uintptr_t)Y % 16 == 0) &&
+      ((uintptr_t)X % 16 == 0)) {
+    const int64_t stride2 = col_stride(n, s / 2);
+    axpy_cols2_kernel<<<(unsigned)((stride2 + 255) / 256), 256, 0, st>>>(
+        (double2*)Y, (const double2*)X, alpha, total / 2, s / 2, stride2);
+    WGP_CUDA(cudaGetLastError());
+    return;
+  }
+  const int64_t stride = col_stride(n, s);
+  axpy_cols_kernel<T><<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(Y, X, alpha, total, s, stride);
   WGP_CUDA(cudaGetLastError());
 }
 
@@ -181,7 +285,17 @@ void launch_xpby_cols(T* P, const T* Z, const double* beta, const int* active, i
                       cudaStream_t st) {
   const int64_t total = n * s;
   if (total <= 0) return;
-  xpby_cols_kernel<T><<<grid_for(total), 256, 0, st>>>(P, Z, beta, active, total, s);
+  if (std::is_same<T, double>::value && s % 2 == 0 && ((uintptr_t)P % 16 == 0) &&
+      ((uintptr_t)Z % 16 == 0)) {
+    const int64_t stride2 = col_stride(n, s / 2);
+    xpby_cols2_kernel<<<(unsigned)((stride2 + 255) / 256), 256, 0, st>>>(
+        (double2*)P, (const double2*)Z, beta, active, total / 2, s / 2, stride2);
+    WGP_CUDA(cudaGetLastError());
+    return;
+  }
+  const int64_t stride = col_stride(n, s);
+  xpby_cols_kernel<T><<<(unsigned)((stride + 255) / 256), 256, 0, st>>>(P, Z, beta, active, total,
+                                                                         s, stride);
   WGP_CUDA(cudaGetLastError());
 }
 

@@ -49,6 +49,7 @@ EXPORTS = (
     "wgp_rng_normal_fill", "wgp_kernel_timer_enable", "wgp_kernel_timer_read", "wgp_rff_eval_fast",
     "wgp_exact_solve", "wgp_grad_posterior", "wgp_ascend_peaks",
     "wgp_mll", "wgp_optimize_mll", "wgp_median_heuristic_lengthscale",
+    "wgp_axpy_cols_dev", "wgp_xpby_cols_dev", "wgp_coldots_dev",
 )
 
 
@@ -122,6 +123,9 @@ def _declare(L):
         "wgp_kmatvec": (C.c_int, [P, P, I64, C.c_int, P, I64]),
         "wgp_kmatvec_dev": (C.c_int, [P, P, P, C.c_int, P]),
         "wgp_residual_dev": (C.c_int, [P, P, P, P, C.c_int, P]),
+        "wgp_axpy_cols_dev": (C.c_int, [P, P, P, P, I64, C.c_int, P]),
+        "wgp_xpby_cols_dev": (C.c_int, [P, P, P, P, P, I64, C.c_int, P]),
+        "wgp_coldots_dev": (C.c_int, [P, P, P, I64, C.c_int, P, P, P]),
         "wgp_cross_matvec": (C.c_int, [P, P, I64, I64, P, I64, C.c_int, P, I64]),
         "wgp_solve_many": (C.c_int, [P, P, P, I64, C.c_int, P, I64, I64, P, I64, P, P, I64, P, P,
                                      P, P]),
@@ -228,6 +232,20 @@ class DeviceContext:
         """In-place all-gather of this group's row slices of a full n x s fp64 buffer."""
         _check(lib().wgp_allgather_rows_dev(self._h, C.c_void_p(dV_ptr), n, s,
                                             C.c_void_p(stream) if stream else None))
+
+    # fused solver vector kernels on device [n][s] row-major fp64 buffers (solvers.cpp:163-180)
+    def axpy_cols_dev(self, dY: int, dX: int, dAlpha: int, n: int, s: int, stream: int = 0):
+        _check(lib().wgp_axpy_cols_dev(self._h, C.c_void_p(dY), C.c_void_p(dX), C.c_void_p(dAlpha),
+                                       n, s, C.c_void_p(stream)))
+
+    def xpby_cols_dev(self, dP: int, dZ: int, dBeta: int, dActive: int, n: int, s: int, stream: int = 0):
+        _check(lib().wgp_xpby_cols_dev(self._h, C.c_void_p(dP), C.c_void_p(dZ), C.c_void_p(dBeta),
+                                       C.c_void_p(dActive), n, s, C.c_void_p(stream)))
+
+    def coldots_dev(self, dA: int, dB: int, n: int, s: int, dOut: int, dWork: int, stream: int = 0):
+        """dWork: at least ceil(n / 512) * s fp64."""
+        _check(lib().wgp_coldots_dev(self._h, C.c_void_p(dA), C.c_void_p(dB), n, s, C.c_void_p(dOut),
+                                     C.c_void_p(dWork), C.c_void_p(stream)))
 
     @property
     def stream(self) -> int:
@@ -419,7 +437,7 @@ def solve_many(op: KernelOperator, rhs, inits: list, cfg: SolverConfig, return_s
         for c, i in enumerate(inits):
             if i.warm_start:
                 U1[:, c] = i.u1
-    V = np.zeros((n, s), order="F")
+    V = np.empty((n, s), order="F")  # every entry is written by the solve
     hs = cfg.max_iters + 1
     hist = np.zeros((s, hs))
     its = np.zeros(s, dtype=np.int32)
@@ -429,7 +447,8 @@ def solve_many(op: KernelOperator, rhs, inits: list, cfg: SolverConfig, return_s
     dv = np.zeros(s, dtype=np.int32)
     st = lib().wgp_solve_many(op._h, C.byref(cfg), _ptr(B), n, s, _ptr(U1), max(n1, 1), n1, _ptr(V), n,
                               _ptr(its), _ptr(hist), hs, _ptr(hl), _ptr(cv), _ptr(cst), _ptr(dv))
-    results = [SolveResult(V[:, c].copy(), int(its[c]), hist[c, : hl[c]].tolist(), bool(cv[c]))
+    # each result's v is its own (contiguous) column of the Fortran-order V: no copy
+    results = [SolveResult(V[:, c], int(its[c]), hist[c, : hl[c]].tolist(), bool(cv[c]))
                for c in range(s)]
     if return_status:
         if st not in (OK, NOT_SPD, DIVERGED):
