@@ -627,16 +627,31 @@ __global__ void scaled_extent_kernel(const double* __restrict__ X, int dpad, int
 
 // Per-column max |V|: blocks of 64 rows x all columns (coalesced row-major reads), block
 // maxima merged with atomicMax on the IEEE bits (ordered for non-negative doubles).
-__global__ void colmax_kernel(const double* __restrict__ V, int64_t n, int s,
-                              unsigned long long* __restrict__ cmax) {
+// max_j |V[j, c]| per column (fp64 bits: non-negative doubles order like their bit
+// patterns).  Block = 64 rows; threads = R row lanes x cp columns (cp = min(s, 256)), each
+// lane striding the block's rows, lanes combined in shared memory, one atomic per column.
+__global__ void __launch_bounds__(256) colmax_kernel(const double* __restrict__ V, int64_t n, int s,
+                                                     unsigned long long* __restrict__ cmax) {
+  __shared__ double red[256];
   const int64_t r0 = (int64_t)blockIdx.x * 64;
   const int64_t r1 = min(n, r0 + 64);
-  for (int c0 = 0; c0 < s; c0 += 256) {
+  const int cp = min(s, 256);
+  const int R = 256 / cp;
+  const int lane_r = threadIdx.x / cp, cl = threadIdx.x % cp;
+  for (int c0 = 0; c0 < s; c0 += cp) {
+    const int c = c0 + cl;
     double a = 0.0;
-    const int c = c0 + (threadIdx.x % 256);
-    if (c < s)
-      for (int64_t j = r0; j < r1; ++j) a = fmax(a, fabs(V[j * s + c]));
-    if (c < s) atomicMax(&cmax[c], (unsigned long long)__double_as_longlong(a));
+    if (lane_r < R && c < s) {
+#pragma unroll 4
+      for (int64_t j = r0 + lane_r; j < r1; j += R) a = fmax(a, fabs(V[j * s + c]));
+    }
+    red[threadIdx.x] = a;
+    __syncthreads();
+    if (threadIdx.x < cp && c < s) {
+      for (int k = 1; k < R; ++k) a = fmax(a, red[k * cp + cl]);
+      atomicMax(&cmax[c], (unsigned long long)__double_as_longlong(a));
+    }
+    __syncthreads();
   }
 }
 
@@ -655,24 +670,34 @@ __global__ void colscale_finish_kernel(const unsigned long long* __restrict__ cm
   scale_down[c] = ldexpf(1.0f, -e);
 }
 
-// V [ncols][s] fp64 -> per-64-row tile [hi|lo][s_pad/8][8 chunks][8 c][8 j] fp16.
+// V [ncols][s] fp64 -> per-64-row tile [hi|lo][s_pad/8][8 chunks][8 c][8 j] fp16.  One
+// thread per (column c, 8-row group): a warp reads consecutive columns of each row
+// (coalesced) and every thread writes its 8 hi and 8 lo halves as two 16-byte stores.
 __global__ void split_v_kernel(const double* __restrict__ V, int64_t ncols, int s, int s_pad,
                                int64_t total_rows, const float* __restrict__ scale_up,
                                __half* __restrict__ Vt) {
-  const int64_t total = total_rows * s_pad;
+  const int64_t total = (total_rows / 8) * s_pad;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = e / s_pad;
-    const int c = (int)(e % s_pad);
-    const double v = (j < ncols && c < s) ? V[j * s + c] * (double)scale_up[c] : 0.0;
-    const __half vh = __double2half(v);
-    const __half vl = __double2half(v - (double)__half2float(vh));
-    const int64_t t = j / BJ;
-    const int jj = (int)(j % BJ);
-    const int64_t idx = ((int64_t)((c >> 3) * (BJ / 8) + (jj >> 3)) * 8 + (c & 7)) * 8 + (jj & 7);
+    const int64_t jg = e / s_pad;
+    const int c = (int)(e - jg * s_pad);
+    const int64_t j0 = jg * 8;
+    const double su = (double)scale_up[c];
+    __align__(16) __half hv[8];
+    __align__(16) __half lv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t j = j0 + k;
+      const double v = (j < ncols && c < s) ? V[j * s + c] * su : 0.0;
+      hv[k] = __double2half(v);
+      lv[k] = __double2half(v - (double)__half2float(hv[k]));
+    }
+    const int64_t t = j0 / BJ;
+    const int jj0 = (int)(j0 % BJ);
+    const int64_t idx = ((int64_t)((c >> 3) * (BJ / 8) + (jj0 >> 3)) * 8 + (c & 7)) * 8;
     __half* base = Vt + t * 2 * (int64_t)s_pad * BJ;
-    base[idx] = vh;
-    base[(int64_t)s_pad * BJ + idx] = vl;
+    *reinterpret_cast<uint4*>(base + idx) = *reinterpret_cast<const uint4*>(hv);
+    *reinterpret_cast<uint4*>(base + (int64_t)s_pad * BJ + idx) = *reinterpret_cast<const uint4*>(lv);
   }
 }
 
@@ -907,7 +932,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     WGP_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * sc, st));
     tc::colmax_kernel<<<ceil_div(ncols, 64), 256, 0, st>>>(Vc, ncols, sc, cmax);
     tc::colscale_finish_kernel<<<1, 128, 0, st>>>(cmax, sc, s_pad, sc_up, sc_down);
-    tc::split_v_kernel<<<tc::grid_for((int64_t)ntiles * tc::BJ * s_pad), 256, 0, st>>>(
+    tc::split_v_kernel<<<tc::grid_for((int64_t)ntiles * (tc::BJ / 8) * s_pad), 256, 0, st>>>(
         Vc, ncols, sc, s_pad, (int64_t)ntiles * tc::BJ, sc_up, vt);
     WGP_CUDA(cudaGetLastError());
     tc::Params prm;
