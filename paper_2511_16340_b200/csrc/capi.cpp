@@ -92,14 +92,16 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
                       SolveOutputs& out, bool derive_seeds) {
   cudaStream_t st = op.ctx->stream;
   PhaseTimer pt(st);
-  SolverWork<double> w;
+  if (!op.solve_cache) op.solve_cache = std::make_shared<SolverWork<double>>();
+  SolverWork<double>& w = *static_cast<SolverWork<double>*>(op.solve_cache.get());
   w.alloc(op, s);
   pt.mark("alloc");
   upload_problem<double>(op, w, B, ldb, U1, ldu, n1, st);
   pt.mark("upload");
   switch (cfg.method) {
     case WGP_CG: {
-      PrecondDev pd;
+      if (!op.precond_cache) op.precond_cache = std::make_shared<PrecondDev>();
+      PrecondDev& pd = *static_cast<PrecondDev*>(op.precond_cache.get());
       const int64_t rank = std::min<int64_t>(cfg.precond_rank, op.n);  // from_matrix :125-126
       if (rank > 0) {
         build_pivoted_cholesky(op, rank, pd, st);
@@ -112,6 +114,8 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
         pd.n = op.n;
         pd.r0 = a;
         pd.n_local = b - a;
+        pd.k = 0;  // identity (the cached factors of an earlier solve are not used)
+        pd.kpad = 0;
       }
       cg_solve_batched<double>(op, cfg, pd, w, out, st);
       pt.mark("cg_loop");

@@ -15,6 +15,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -138,6 +139,11 @@ struct Op {
   mutable DBuf<double> f64split;  // fp64 kernel-matvec column-split partials
   mutable DBuf<double> krows_part;  // SGD minibatch-row partials per j range
   std::vector<double> h_center;
+  // solver work buffers (SolverWork<double>) and preconditioner factors (PrecondDev), kept
+  // across solve calls on this operator: reallocated only when they must grow, so a solve
+  // pays no cudaMalloc / synchronous cudaFree for its [n][s] vectors (calls on one handle
+  // are never concurrent)
+  std::shared_ptr<void> solve_cache, precond_cache;
   bool tc_dirty = true;
   // GEMM1 operand format chosen at operand build: fp16 splits of x / l (kind::f16, half the
   // bytes and MMA time of tf32) when the scaled coordinates fit fp16, else tf32 splits of x.

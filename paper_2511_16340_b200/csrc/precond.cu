@@ -284,7 +284,7 @@ void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStre
   pd.k = 0;
   pd.kpad = rank > 0 ? ((rank + 3) / 4) * 4 : 0;
   if (rank == 0) return;
-  pd.L.alloc((size_t)std::max<int64_t>(nl, 1) * pd.kpad);
+  pd.L.ensure((size_t)std::max<int64_t>(nl, 1) * pd.kpad);
   WGP_CUDA(cudaMemsetAsync(pd.L.p, 0, sizeof(double) * std::max<int64_t>(nl, 1) * pd.kpad, st));
   const KParams p = op.kp();
   const double dval = p.s2 + p.noise2;  // stationary kernels: every diagonal entry is equal
@@ -385,7 +385,7 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   DBuf<double> dW((size_t)k * k);
   WGP_CUDA(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
   const int64_t nl = std::max<int64_t>(pd.n_local, 1);
-  pd.M64.alloc((size_t)nl * pd.kpad);
+  pd.M64.ensure((size_t)nl * pd.kpad);
   const size_t smem = sizeof(double) * k * k;
   if (smem > 48 * 1024)
     WGP_CUDA(cudaFuncSetAttribute(apply_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -86,15 +86,15 @@ void SolverWork<T>::alloc(const Op& op, int s_) {
   nch = ceil_div(N, kChunkRows);
   c0 = (int)(r0 / kChunkRows);
   const size_t ns = (size_t)std::max<int64_t>(n, 1) * s, Ns = (size_t)N * s;
-  V.alloc(Ns);
-  P.alloc(Ns);
-  R.alloc(ns);
-  Z.alloc(ns);
-  HP.alloc(ns);
-  B.alloc(ns);
-  part.alloc((size_t)(nch > 0 ? nch : 1) * 2 * s);
-  scal.alloc((size_t)6 * s);
-  act.alloc((size_t)2 * s + 2);
+  V.ensure(Ns);
+  P.ensure(Ns);
+  R.ensure(ns);
+  Z.ensure(ns);
+  HP.ensure(ns);
+  B.ensure(ns);
+  part.ensure((size_t)(nch > 0 ? nch : 1) * 2 * s);
+  scal.ensure((size_t)6 * s);
+  act.ensure((size_t)2 * s + 2);
 }
 
 template <typename T>
@@ -103,7 +103,8 @@ void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb
   const int64_t n = w.n;
   const int s = w.s;
   // B: this rank's rows of the host column-major matrix -> row-major on the device
-  DBuf<double> stage((size_t)std::max<int64_t>(std::max(n, n1), 1) * s);
+  w.stage.ensure((size_t)std::max<int64_t>(std::max(n, n1), 1) * s);
+  DBuf<double>& stage = w.stage;
   if (n > 0) {
     WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, B + w.r0, sizeof(double) * ldb,
                                sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
@@ -122,7 +123,8 @@ template <typename T>
 void download_solution(SolverWork<T>& w, double* V, int64_t ldv, cudaStream_t st) {
   const int64_t N = w.N;
   const int s = w.s;
-  DBuf<double> stage((size_t)std::max<int64_t>(N, 1) * s);
+  w.stage.ensure((size_t)std::max<int64_t>(N, 1) * s);
+  DBuf<double>& stage = w.stage;
   launch_rows_to_colmajor(w.V.p, N, s, stage.p, N, true, st);
   WGP_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * ldv, stage.p, sizeof(double) * N,
                              sizeof(double) * N, s, cudaMemcpyDeviceToHost, st));

@@ -24,6 +24,7 @@ struct SolverWork {
   DBuf<int> act;       // active[s] + failure column
   DBuf<double> pwork;  // preconditioner chunk partials
   DBuf<double> tvec;   // M^T r  (k x s)
+  DBuf<double> stage;  // host-boundary staging (column-major) for upload / download
   void alloc(const Op& op, int s);
 };
 

@@ -191,3 +191,32 @@ def test_cg_wide_batches_equal_single_columns(W, s):
         assert np.isfinite(res[c].v).all()
         assert np.array_equal(res[c].v, one.v), c
         assert res[c].residual_history == one.residual_history
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_cached_work_buffers_reuse(W, O, precision):
+    """Solver vectors and preconditioner factors are cached on the operator across calls:
+    a sequence of solves with different RHS counts, preconditioner ranks (including 0),
+    methods and an append in between gives bitwise the results of fresh operators."""
+    X = O.uniform_inputs(99, 900, 5)
+    hyp = W.KernelHyperparams(0.6, 1.0, 0.1, W.RBF)
+    rng = np.random.default_rng(4)
+    seq = [(7, 40, W.CG, 900), (3, 0, W.CG, 900), (9, 25, W.CG, 900), (2, 10, W.AP, 900),
+           (5, 30, W.CG, 1000), (1, 0, W.CG, 1000)]
+    cached = W.KernelOperator(hyp, X[:900], precision=precision)
+    Xg = np.vstack([X, O.uniform_inputs(100, 100, 5)])
+    for s, rank, method, n in seq:
+        if n > cached.n:
+            cached.append_rows(Xg[cached.n:n])
+        B = np.asfortranarray(rng.standard_normal((n, s)))
+        cfg = W.SolverConfig(method=method, tolerance=1e-5, max_iters=60, precond_rank=rank,
+                             precond_shift=0.01, block_size=100)
+        got = W.solve_many(cached, B, [W.Initialization.cold()] * s, cfg)
+        fresh = W.KernelOperator(hyp, Xg[:900], precision=precision)  # same build + append
+        if n > 900:
+            fresh.append_rows(Xg[900:n])
+        ref = W.solve_many(fresh, B, [W.Initialization.cold()] * s, cfg)
+        for a, b in zip(got, ref):
+            assert a.iterations == b.iterations
+            assert a.residual_history == b.residual_history
+            assert np.array_equal(a.v, b.v)
