@@ -89,6 +89,40 @@ __global__ void argmax_final_kernel(const double* __restrict__ pv, const int64_t
   }
 }
 
+// Single GPU: the global argmax, the pivot index (dpiv, -1 when none is left above the
+// floor) and the pivot row lpiv in one block, with no host round trip; kcount = steps done.
+__global__ void pivot_select_kernel(const double* __restrict__ pv, const int64_t* __restrict__ pi,
+                                    int nb, const double* __restrict__ L,
+                                    const double* __restrict__ d, int64_t r0, int k, int kpad,
+                                    double* __restrict__ lpiv, int64_t* __restrict__ dpiv,
+                                    int* __restrict__ kcount) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  ArgBest b{0.0, -1};
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) b = better(b, ArgBest{pv[t], pi[t]});
+  sv[threadIdx.x] = b.v;
+  si[threadIdx.x] = b.i;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      ArgBest r = better(ArgBest{sv[threadIdx.x], si[threadIdx.x]},
+                         ArgBest{sv[threadIdx.x + o], si[threadIdx.x + o]});
+      sv[threadIdx.x] = r.v;
+      si[threadIdx.x] = r.i;
+    }
+    __syncthreads();
+  }
+  const int64_t piv = si[0];
+  if (threadIdx.x == 0) {
+    *dpiv = piv;
+    if (piv >= 0) *kcount = k + 1;
+  }
+  if (piv < 0) return;
+  const int64_t li = piv - r0;
+  for (int t = threadIdx.x; t < k; t += blockDim.x) lpiv[t] = L[li * kpad + t];
+  if (threadIdx.x == 0) lpiv[k] = sqrt(d[li]);
+}
+
 // Owner of the pivot row: lpiv[0..k) = L[piv, :k], lpiv[k] = sqrt(d[piv]).
 __global__ void fill_pivot_kernel(const double* __restrict__ L, const double* __restrict__ d,
                                   int64_t li, int k, int kpad, double* __restrict__ lpiv) {
@@ -100,9 +134,11 @@ __global__ void fill_pivot_kernel(const double* __restrict__ L, const double* __
 // and root = sqrt(d[piv]) arrive in lpiv (broadcast from the owning rank).
 __global__ void pchol_step_kernel(const double* __restrict__ X, const double* __restrict__ sq,
                                   int64_t n_local, int64_t r0, int dpad, int dim, KParams p, int k,
-                                  int kpad, int64_t piv, const double* __restrict__ lpiv,
-                                  double* __restrict__ L, double* __restrict__ d,
-                                  int* __restrict__ used) {
+                                  int kpad, const int64_t* __restrict__ dpiv,
+                                  const double* __restrict__ lpiv, double* __restrict__ L,
+                                  double* __restrict__ d, int* __restrict__ used) {
+  const int64_t piv = *dpiv;
+  if (piv < 0) return;  // no pivot at this step (the factorisation stopped early)
   const double root = lpiv[k];
   const double* xp = X + piv * dpad;
   for (int64_t li = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; li < n_local;
@@ -296,6 +332,27 @@ void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStre
   const int nb = 148 * 2;
   DBuf<double> pv(nb), best2(2), all2((size_t)2 * ctx.world), lpiv(pd.kpad + 1);
   DBuf<int64_t> pi(nb);
+  DBuf<int64_t> dpiv(1);
+  if (ctx.world == 1) {
+    // no host synchronisation per pivot: selection, pivot row and the early stop all stay
+    // on the device; one read of the achieved rank at the end
+    DBuf<int> kcount(1);
+    WGP_CUDA(cudaMemsetAsync(kcount.p, 0, sizeof(int), st));
+    for (int64_t k = 0; k < rank; ++k) {
+      argmax_partial_kernel<<<nb, 256, 0, st>>>(d.p, used.p, nl, r0, floor_, pv.p, pi.p);
+      pivot_select_kernel<<<1, 256, 0, st>>>(pv.p, pi.p, nb, pd.L.p, d.p, r0, (int)k, (int)pd.kpad,
+                                             lpiv.p, dpiv.p, kcount.p);
+      pchol_step_kernel<<<grid_rows(std::max<int64_t>(nl, 1)), 256, 0, st>>>(
+          op.X64.p, op.sq64.p, nl, r0, op.dpad, op.dim, p, (int)k, (int)pd.kpad, dpiv.p, lpiv.p,
+          pd.L.p, d.p, used.p);
+    }
+    WGP_CUDA(cudaGetLastError());
+    int kc = 0;
+    WGP_CUDA(cudaMemcpyAsync(&kc, kcount.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    pd.k = kc;
+    return;
+  }
   std::vector<double> h_all((size_t)2 * ctx.world);
   for (int64_t k = 0; k < rank; ++k) {
     argmax_partial_kernel<<<nb, 256, 0, st>>>(d.p, used.p, nl, r0, floor_, pv.p, pi.p);
@@ -320,10 +377,11 @@ void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStre
     const int owner = owner_rank(ctx, n, piv);
     if (owner == ctx.rank) fill_pivot_kernel<<<1, 128, 0, st>>>(pd.L.p, d.p, piv - r0, (int)k, (int)pd.kpad, lpiv.p);
     dist_broadcast(ctx, lpiv.p, sizeof(double) * (pd.kpad + 1), owner, st);
+    WGP_CUDA(cudaMemcpyAsync(dpiv.p, &piv, sizeof(int64_t), cudaMemcpyHostToDevice, st));
     pchol_step_kernel<<<grid_rows(std::max<int64_t>(nl, 1)), 256, 0, st>>>(
-        op.X64.p, op.sq64.p, nl, r0, op.dpad, op.dim, p, (int)k, (int)pd.kpad, piv, lpiv.p, pd.L.p,
-        d.p, used.p);
-    WGP_CUDA(cudaGetLastError());
+        op.X64.p, op.sq64.p, nl, r0, op.dpad, op.dim, p, (int)k, (int)pd.kpad, dpiv.p, lpiv.p,
+        pd.L.p, d.p, used.p);
+    WGP_CUDA(cudaGetLastError());  // (a pageable-source copy has read piv on return)
     pd.k = k + 1;
   }
 }
