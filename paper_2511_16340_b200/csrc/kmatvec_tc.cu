@@ -177,7 +177,6 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
   }
 }
 
-template <bool ST16>
 __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NSX, int NSV) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -487,18 +486,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
           lo[c] = pack_h2(rem.x, rem.y);
         }
         // K back into the 16 columns just read: [hi 8 | lo 8]
-        if (ST16) {
-          uint32_t hl[16];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            hl[c] = hi[c];
-            hl[8 + c] = lo[c];
-          }
-          ptx::tmem_st16(col, hl);
-        } else {
-          ptx::tmem_st8(col, hi);
-          ptx::tmem_st8(col + 8, lo);
-        }
+        ptx::tmem_st8(col, hi);
+        ptx::tmem_st8(col + 8, lo);
       }
       if (tr) trace_ev(p, t, 4);
       ptx::tmem_wait_st();
@@ -995,8 +984,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     const size_t smem = tc_smem_bytes(K1, esz, s_pad, &nsx, &nsv);
     WGP_REQUIRE(nsx >= 2 && nsv >= 2, "kmatvec_tc: dim %d too large for the shared-memory pipeline",
                 op.dim);
-    static const int st16 = getenv("WGP_TC_ST16") ? atoi(getenv("WGP_TC_ST16")) : 0;  // EXPERIMENT
-    auto kern = st16 ? tc::kmatvec_tc_kernel<true> : tc::kmatvec_tc_kernel<false>;
+    auto kern = tc::kmatvec_tc_kernel;
     WGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     KernelTimer& kt = kernel_timer();
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
