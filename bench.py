@@ -459,7 +459,7 @@ def run_ours(args):
 
 # dram bytes (read + write) per launch of tc::kmatvec_tc_kernel on this workload, from the
 # committed ncu --set full capture (profiles/r01_kmatvec_tc_metrics.json)
-TRAFFIC_BYTES = 79.31e6
+TRAFFIC_BYTES = 81.88e6
 
 
 def main():
