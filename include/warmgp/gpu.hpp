@@ -144,6 +144,10 @@ class Context {
   Context(int device, int rank, int world, const void* nccl_uid128) {
     check(wgp_ctx_create_sharded(device, rank, world, nccl_uid128, &h_));
   }
+  // rank of a loopback group (ranks = threads of one process on one device; testing)
+  Context(int device, int rank, void* loopback_group) {
+    check(wgp_ctx_create_loopback(device, rank, loopback_group, &h_));
+  }
   ~Context() { wgp_ctx_destroy(h_); }
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
@@ -171,6 +175,9 @@ class KernelOperator {
     check(wgp_op_append_rows(h_, X2.data.data(), X2.rows, X2.rows > 0 ? X2.rows : 1, 1));
   }
   int64_t size() const { return wgp_op_size(h_); }
+  int64_t rows() const { return size(); }  // Eigen-style, as H.rows() in the reference
+  // CG true-residual mode (wgp_residual_mode): ANCHORED removes the fp32 residual floor
+  void set_residual_mode(wgp_residual_mode m) { check(wgp_op_set_residual_mode(h_, (int)m)); }
   Matrix operator*(const Matrix& V) const {  // H * V  (solvers.cpp:162)
     Matrix Y(V.rows, V.cols);
     check(wgp_kmatvec(h_, V.data.data(), V.rows, (int)V.cols, Y.data.data(), Y.rows));
@@ -274,6 +281,126 @@ inline SolveResult ap_solve(const KernelOperator& H, const Vector& b, const Init
   return solve(H, b, i, cfg);
 }
 
+// init_weights (solvers.cpp:27-38): cold -> 0, warm -> [u1; 0]
+inline Vector init_weights(const Initialization& init, int64_t n1, int64_t n2) {
+  if (init.warm_start && (int64_t)init.u1.size() != n1)
+    throw std::invalid_argument("init_weights: warm-start vector length does not match n1");
+  Vector v((size_t)std::max<int64_t>(n1 + n2, 0));
+  check(wgp_init_weights(init.warm_start ? init.u1.data() : nullptr, n1, n2, v.data()));
+  return v;
+}
+
+// relative_residual (solvers.cpp:62-66): |H v - b| / |b|; zero b -> std::invalid_argument
+inline double relative_residual(const KernelOperator& H, const Vector& v, const Vector& b) {
+  if ((int64_t)v.size() != H.size() || (int64_t)b.size() != H.size())
+    throw std::invalid_argument("relative_residual: length mismatch");
+  double out = 0.0;
+  check(wgp_relative_residual(H.get(), v.data(), (int64_t)v.size(), b.data(), (int64_t)b.size(), 1, &out));
+  return out;
+}
+
+// quadratic_objective (solvers.cpp:68-70): 0.5 v.Hv - v.b
+inline double quadratic_objective(const KernelOperator& H, const Vector& v, const Vector& b) {
+  if ((int64_t)v.size() != H.size() || (int64_t)b.size() != H.size())
+    throw std::invalid_argument("quadratic_objective: length mismatch");
+  double out = 0.0;
+  check(wgp_quadratic_objective(H.get(), v.data(), (int64_t)v.size(), b.data(), (int64_t)b.size(), 1, &out));
+  return out;
+}
+
+// pivoted_cholesky (solvers.cpp:72-107): n x r factor (r <= rank), computed on the device
+inline Matrix pivoted_cholesky(const KernelOperator& H, int64_t rank) {
+  const int64_t n = H.size();
+  Matrix L(n, std::max<int64_t>(rank, 0));
+  int64_t achieved = 0;
+  check(wgp_pivoted_cholesky(H.get(), rank, rank > 0 ? L.data.data() : nullptr, n > 0 ? n : 1, &achieved));
+  L.cols = achieved;
+  L.data.resize((size_t)(n * achieved));
+  return L;
+}
+
+// CgPreconditioner (solvers.hpp:82-100) as a device handle over the operator it was built for.
+class CgPreconditioner {
+ public:
+  CgPreconditioner() = default;  // identity (no handle): cg_solve_with builds a rank-0 one
+  static CgPreconditioner from_matrix(const KernelOperator& H, int64_t rank, double shift,
+                                      SolverConfig::PrecondShiftMode mode =
+                                          SolverConfig::PrecondShiftMode::Calibrated) {
+    CgPreconditioner p;
+    check(wgp_precond_create(H.get(), rank, shift, (int)mode, &p.h_));
+    return p;
+  }
+  // CgPreconditioner(L, shift) (solvers.cpp:109-121) with L a host factor of the operator's rows
+  CgPreconditioner(const KernelOperator& H, const Matrix& L, double shift) {
+    check(wgp_precond_create_from_factor(H.get(), L.data.data(), L.rows > 0 ? L.rows : 1, L.cols,
+                                         shift, &h_));
+  }
+  CgPreconditioner(CgPreconditioner&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  CgPreconditioner& operator=(CgPreconditioner&& o) noexcept {
+    if (this != &o) {
+      wgp_precond_destroy(h_);
+      h_ = o.h_;
+      o.h_ = nullptr;
+    }
+    return *this;
+  }
+  CgPreconditioner(const CgPreconditioner&) = delete;
+  CgPreconditioner& operator=(const CgPreconditioner&) = delete;
+  ~CgPreconditioner() { wgp_precond_destroy(h_); }
+
+  bool is_identity() const { return rank() == 0; }
+  int64_t rank() const {
+    if (!h_) return 0;
+    int64_t k = 0;
+    double sh = 0.0;
+    check(wgp_precond_get(h_, &k, &sh));
+    return k;
+  }
+  double shift() const {
+    int64_t k = 0;
+    double sh = 1.0;
+    if (h_) check(wgp_precond_get(h_, &k, &sh));
+    return sh;
+  }
+  Vector apply(const Vector& r) const {  // solvers.cpp:135-140
+    if (!h_) return r;
+    Vector z(r.size());
+    check(wgp_precond_apply(h_, r.data(), (int64_t)r.size(), 1, z.data(), (int64_t)z.size()));
+    return z;
+  }
+  wgp_precond* get() const { return h_; }
+
+ private:
+  wgp_precond* h_ = nullptr;
+};
+
+// cg_solve_with (solvers.hpp:118-119): CG with an externally built preconditioner (no
+// factorization inside); the bo_round pattern calls it per column with one handle.
+inline SolveResult cg_solve_with(const KernelOperator& H, const Vector& b, const Initialization& init,
+                                 const SolverConfig& cfg, const CgPreconditioner& precond) {
+  const int64_t n = (int64_t)b.size();
+  if (n != H.size()) throw std::invalid_argument("cg_solve_with: rhs length != operator size");
+  CgPreconditioner identity;
+  const wgp_precond* pc = precond.get();
+  if (!pc) {  // default-constructed identity preconditioner
+    identity = CgPreconditioner::from_matrix(H, 0, 1.0);
+    pc = identity.get();
+  }
+  wgp_solver_config c = cfg.c();
+  const int64_t hs = (int64_t)cfg.max_iters + 1;
+  SolveResult r;
+  r.v.assign((size_t)n, 0.0);
+  std::vector<double> hist((size_t)hs);
+  int32_t its = 0, hl = 0, cv = 0;
+  const int64_t n1 = init.warm_start ? (int64_t)init.u1.size() : 0;
+  check(wgp_cg_solve_with(H.get(), pc, &c, b.data(), n, 1, init.warm_start ? init.u1.data() : nullptr,
+                          n1 > 0 ? n1 : 1, n1, r.v.data(), n, &its, hist.data(), hs, &hl, &cv));
+  r.iterations = its;
+  r.residual_history.assign(hist.begin(), hist.begin() + hl);
+  r.converged = cv != 0;
+  return r;
+}
+
 // ---------------------------------------------------------------- sampling (sampling.hpp)
 struct RffPrior {
   Matrix frequencies;  // F x D
@@ -309,6 +436,34 @@ inline Matrix eval_priors(const KernelOperator& H, const std::vector<RffPrior>& 
   check(wgp_rff_eval(H.get(), Om.data(), ph.data(), am.data(), (int)F, S, priors[0].signal_scale,
                      nullptr, m, m, out.data.data(), m));
   return out;
+}
+
+// eval_prior (sampling.cpp:37-46) of one prior at the rows of X* (m x D)
+inline Vector eval_prior(const KernelOperator& H, const RffPrior& prior, const Matrix& Xstar) {
+  const int64_t m = Xstar.rows, F = prior.frequencies.rows;
+  Vector out((size_t)m);
+  if (!m) return out;
+  check(wgp_rff_eval(H.get(), prior.frequencies.data.data(), prior.phases.data(), prior.amplitudes.data(),
+                     (int)F, 1, prior.signal_scale, Xstar.data.data(), m, m, out.data(), m));
+  return out;
+}
+
+// build_sample_rhs (sampling.cpp:56-64) at the operator's rows
+inline Vector build_sample_rhs(const KernelOperator& H, const RffPrior& prior, double noise_scale,
+                               std::uint64_t seed) {
+  Vector out((size_t)H.size());
+  check(wgp_build_sample_rhs(H.get(), prior.frequencies.data.data(), prior.phases.data(),
+                             prior.amplitudes.data(), (int)prior.frequencies.rows, prior.signal_scale,
+                             noise_scale, seed, out.data()));
+  return out;
+}
+
+// cross_kernel (kernel.cpp:74-89): dense K(X*, X_op), no noise term
+inline Matrix cross_kernel(const KernelOperator& H, const Matrix& Xstar) {
+  Matrix K(Xstar.rows, H.size());
+  check(wgp_cross_kernel(H.get(), Xstar.data.data(), Xstar.rows, Xstar.rows > 0 ? Xstar.rows : 1,
+                         K.data.data(), Xstar.rows > 0 ? Xstar.rows : 1));
+  return K;
 }
 
 // eval_posterior (sampling.cpp:66-75) for S samples at m points at once:

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define WGP_ABI_VERSION 1
+#define WGP_ABI_VERSION 2
 
 typedef enum {
   WGP_OK = 0,
@@ -55,6 +55,15 @@ typedef enum { WGP_MATERN32 = 0, WGP_RBF = 1 } wgp_kernel;
  * split (<=1e-4).  TF32: single-pass tensor-core contractions (fastest, not
  * parity-grade).  F32_SIMT: fp32 CUDA-core path (validation of the others). */
 typedef enum { WGP_F64 = 0, WGP_F32_3XTF32 = 1, WGP_TF32 = 2, WGP_F32_SIMT = 3 } wgp_precision;
+
+/* True residual b - H v of the CG iteration (solvers.cpp:150,171) on fp32 operators.
+ * DIRECT: the operator itself (default).  ANCHORED: r_a - H (v - v_a), where v_a is an
+ * anchor iterate and r_a = b - H v_a is evaluated by the fp64 kernel; the solver re-anchors
+ * when the predicted error of the fp32 part, |v - v_a| times its measured error rate,
+ * exceeds 5% of |r|.  ANCHORED removes the attainable-residual floor eps |H||v| / |b| of
+ * fp32 operators on ill-conditioned systems for a few fp64 matvecs per solve.  F64
+ * operators ignore the mode. */
+typedef enum { WGP_RESIDUAL_DIRECT = 0, WGP_RESIDUAL_ANCHORED = 1 } wgp_residual_mode;
 
 typedef enum { WGP_CG = 0, WGP_SGD = 1, WGP_AP = 2 } wgp_method;              /* solvers.hpp:10 */
 typedef enum { WGP_SGD_UNBIASED = 0, WGP_SGD_BLOCK = 1 } wgp_sgd_scaling;     /* solvers.hpp:16-19 */
@@ -87,9 +96,14 @@ const char* wgp_last_error(void);
 void wgp_solver_config_default(wgp_solver_config* cfg);
 
 /* Row partition used by sharded contexts: rows [*row0, *row1) of an n-row
- * operator belong to `rank` of `world`.  Boundaries are multiples of the
- * reduction chunk so per-column sums are bit-identical for every world size. */
+ * operator belong to `rank` of `world`.  Every rank owns an equal slot of
+ * ceil(ceil(n / 512) / world) 512-row chunks (the last slots stop at n), so
+ * boundaries are multiples of the reduction chunk (per-column sums are
+ * bit-identical for every world size) and a full buffer padded to
+ * wgp_shard_padded_rows(n, world) rows is exchanged by one in-place all-gather
+ * of equal slices. */
 void wgp_shard_range(int64_t n, int world, int rank, int64_t* row0, int64_t* row1);
+int64_t wgp_shard_padded_rows(int64_t n, int world);
 
 /* ---- device context: one per GPU (one process per GPU) ---- */
 wgp_status wgp_ctx_create(int device, wgp_ctx** out);
@@ -99,10 +113,19 @@ wgp_status wgp_ctx_create(int device, wgp_ctx** out);
 wgp_status wgp_nccl_unique_id(void* out128);
 wgp_status wgp_ctx_create_sharded(int device, int rank, int world, const void* unique_id128,
                                   wgp_ctx** out);
+/* Loopback group: `world` ranks emulated by host threads of ONE process on one device
+ * (one context per thread, wgp_ctx_create_loopback).  Collectives are host barriers plus
+ * device-to-device copies between the ranks' buffers -- no kernel ever waits on another
+ * rank -- so the sharded solver code runs unchanged where fewer GPUs than ranks exist
+ * (correctness testing; not a performance configuration). */
+wgp_status wgp_loopback_group_create(int world, void** group);
+void wgp_loopback_group_destroy(void* group);
+wgp_status wgp_ctx_create_loopback(int device, int rank, void* group, wgp_ctx** out);
 void wgp_ctx_destroy(wgp_ctx* ctx);
-/* In-place all-gather of row slices: dV is a full n x s row-major fp64 buffer on every
- * rank, rank r holding valid rows wgp_shard_range(n, world, r); afterwards all rows are
- * valid everywhere (NCCL over NVLink; the exchange step of a sharded matvec). */
+/* In-place all-gather of row slices: dV is a full row-major fp64 buffer of
+ * wgp_shard_padded_rows(n, world) x s on every rank, rank r holding valid rows
+ * wgp_shard_range(n, world, r); afterwards rows [0, n) are valid everywhere (one
+ * ncclAllGather of equal slices over NVLink; the exchange step of a sharded matvec). */
 wgp_status wgp_allgather_rows_dev(wgp_ctx* ctx, void* dV, int64_t n, int s, void* stream);
 /* cudaStream_t the context launches on (for device-pointer callers). */
 void* wgp_ctx_stream(wgp_ctx* ctx);
@@ -118,6 +141,12 @@ void wgp_op_destroy(wgp_op* op);
 wgp_status wgp_op_append_rows(wgp_op* op, const double* X_rows, int64_t n_new, int64_t ld,
                               int col_major);
 int64_t wgp_op_size(const wgp_op* op);
+/* Select the CG true-residual mode (wgp_residual_mode) of this operator's solves. */
+wgp_status wgp_op_set_residual_mode(wgp_op* op, int mode);
+int wgp_op_residual_mode(const wgp_op* op);
+/* Number of fp64 anchor evaluations made by the last CG solve on this operator (ANCHORED
+ * mode; 0 otherwise). */
+int wgp_op_last_anchor_count(const wgp_op* op);
 int wgp_op_dim(const wgp_op* op);
 int wgp_op_precision(const wgp_op* op);
 
@@ -181,6 +210,55 @@ wgp_status wgp_pivoted_cholesky(wgp_op* op, int64_t rank, double* L, int64_t ldl
                                 int64_t* achieved);
 wgp_status wgp_precond_info(wgp_op* op, int64_t rank, double shift, int mode, int64_t* achieved,
                             double* shift_out);
+
+/* ---- reusable preconditioner (CgPreconditioner, solvers.hpp:82-100) and cg_solve_with
+ *      (solvers.hpp:118-119, solvers.cpp:142-183): one factorization shared by many solves,
+ *      as bo_round does for its per-column solves (thompson.cpp:359-384).  The handle
+ *      lives on the operator's device and is valid while the operator keeps the row count
+ *      it was built at (after wgp_op_append_rows, using it returns WGP_INVALID_ARGUMENT). */
+typedef struct wgp_precond wgp_precond;
+/* CgPreconditioner::from_matrix (solvers.cpp:123-133): pivoted Cholesky of rank
+ * min(rank, n) and the Woodbury factors; rank 0 = identity.  mode: wgp_shift_mode. */
+wgp_status wgp_precond_create(wgp_op* op, int64_t rank, double shift, int mode, wgp_precond** out);
+/* CgPreconditioner(L, shift) (solvers.cpp:109-121): from a host factor L (n x k column-major,
+ * ldl), shift used as given (must be > 0 for k > 0; capacitance failure -> WGP_NOT_SPD). */
+wgp_status wgp_precond_create_from_factor(wgp_op* op, const double* L, int64_t ldl, int64_t k,
+                                          double shift, wgp_precond** out);
+void wgp_precond_destroy(wgp_precond* pc);
+/* achieved rank and (calibrated) shift of the handle */
+wgp_status wgp_precond_get(const wgp_precond* pc, int64_t* rank, double* shift);
+/* CgPreconditioner::apply (solvers.cpp:135-140) on host columns: Z = (L L^T + shift I)^{-1} R,
+ * R and Z n x s column-major.  Unsharded. */
+wgp_status wgp_precond_apply(wgp_precond* pc, const double* R, int64_t ldr, int s, double* Z,
+                             int64_t ldz);
+/* cg_solve_with: wgp_solve_many's CG (cfg->method is ignored, cfg->precond_* too) with the
+ * caller's preconditioner -- no factorization inside.  Same arguments and outputs as
+ * wgp_solve_many; a column solved alone gives bitwise the result it gets in a batch. */
+wgp_status wgp_cg_solve_with(wgp_op* op, const wgp_precond* pc, const wgp_solver_config* cfg,
+                             const double* B, int64_t ldb, int s, const double* U1, int64_t ldu,
+                             int64_t n1, double* V, int64_t ldv, int32_t* iterations,
+                             double* history, int64_t hist_stride, int32_t* history_len,
+                             int32_t* converged);
+
+/* ---- remaining free functions of the reference API ---- */
+/* cross_kernel (kernel.cpp:74-89): K (m x n column-major, ldk) = k(X*, X_op), no noise
+ * term, fp64 on the device (n <= 65535). */
+wgp_status wgp_cross_kernel(wgp_op* op, const double* Xstar, int64_t m, int64_t ldx, double* K,
+                            int64_t ldk);
+/* relative_residual (solvers.cpp:62-66) per column: out[c] = |H v_c - b_c| / |b_c|; a zero
+ * b_c returns WGP_INVALID_ARGUMENT.  V, B n x s column-major; the operator's precision. */
+wgp_status wgp_relative_residual(wgp_op* op, const double* V, int64_t ldv, const double* B,
+                                 int64_t ldb, int s, double* out);
+/* quadratic_objective (solvers.cpp:68-70) per column: 0.5 v.Hv - v.b */
+wgp_status wgp_quadratic_objective(wgp_op* op, const double* V, int64_t ldv, const double* B,
+                                   int64_t ldb, int s, double* out);
+/* init_weights (solvers.cpp:27-38): out (n1 + n2) = u1 == NULL ? 0 : [u1; 0]. */
+wgp_status wgp_init_weights(const double* u1, int64_t n1, int64_t n2, double* out);
+/* build_sample_rhs (sampling.cpp:56-64): out (n) = prior at the operator's rows (one prior:
+ * Omega F x dim column-major, phases F, amps F) + noise_scale Rng(seed).normal() per row. */
+wgp_status wgp_build_sample_rhs(wgp_op* op, const double* Omega, const double* phases,
+                                const double* amps, int F, double signal_scale,
+                                double noise_scale, uint64_t seed, double* out);
 
 /* ---- random Fourier features (eval_prior sampling.cpp:37-46, batched over S
  *      priors; build_sample_rhs :56-64 adds host-drawn noise afterwards) ----
@@ -256,6 +334,9 @@ wgp_status wgp_ascend_peaks(wgp_op* op, const double* Omega, const double* phase
  *      kernel time and launch count since the last enable. ---- */
 void wgp_kernel_timer_enable(int enable);
 wgp_status wgp_kernel_timer_read(double* total_ms, int64_t* launches);
+/* Same for one tagged kernel family: "kmatvec_tc", "kmatvec_f64", "kmatvec_f32", "krows"
+ * (SGD minibatch rows), "kcols" (AP block columns), "rff_eval" (fp64), "rff_eval32". */
+wgp_status wgp_kernel_timer_read_tag(const char* tag, double* total_ms, int64_t* launches);
 /* out[i] = scale * Rng(seed).normal(), i = 0..n-1 (build_sample_rhs noise, sampling.cpp:58-62) */
 void wgp_normal_fill(uint64_t seed, int64_t n, double scale, double* out);
 /* sample_prior (sampling.cpp:14-35): Omega F x dim column-major, phases F, amps F.

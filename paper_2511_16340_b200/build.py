@@ -34,12 +34,12 @@ def _headers_mtime():
     return max(os.path.getmtime(h) for h in hs)
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, src + ".o")
+def _compile(src: str, verbose: bool, build_dir: str = BUILD, extra=()) -> str:
+    obj = os.path.join(build_dir, src + ".o")
     path = os.path.join(CSRC, src)
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path), _headers_mtime()):
         return obj
-    cmd = [NVCC, *ARCH, *COMMON, "-c", path, "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", path, "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose else []
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -69,19 +69,32 @@ def _nccl_link() -> list:
     return ["-lnccl", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, extra=(), lib: str = LIB, build_dir: str = BUILD) -> str:
+    """Compile every source and link ``lib``.  ``extra`` nvcc flags (e.g. -D switches of A/B
+    probe variants) go with a separate ``build_dir`` and ``lib``."""
+    os.makedirs(build_dir, exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
-        return LIB
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, *_nccl_link()]
+        objs = list(ex.map(lambda s: _compile(s, verbose, build_dir, tuple(extra)), srcs))
+    if os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(o) for o in objs):
+        return lib
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, *_nccl_link()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    # python -m paper_2511_16340_b200.build [-v] [--variant NAME -DFLAG ...]: a variant
+    # library tools/probes/_variants/libwarmgp_NAME.so for A/B probes (WGP_LIB_PATH)
+    args = sys.argv[1:]
+    if "--variant" in args:
+        i = args.index("--variant")
+        name, flags = args[i + 1], [a for a in args[i + 2:] if a.startswith("-D")]
+        vdir = os.path.join(ROOT, "tools", "probes", "_variants")
+        os.makedirs(vdir, exist_ok=True)
+        print(build(verbose="-v" in args, extra=flags, lib=os.path.join(vdir, f"libwarmgp_{name}.so"),
+                    build_dir=os.path.join(ROOT, "build", f"variant_{name}")))
+    else:
+        print(build(verbose="-v" in args))

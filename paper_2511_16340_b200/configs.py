@@ -92,7 +92,7 @@ class GrowthState:
                "max_sample_iterations": max(r.iterations for r in res[1:]) if s > 1 else 0,
                "avg_sample_residual": float(np.mean([r.final_residual() for r in res[1:]])) if s > 1 else 0.0,
                "iterations": [r.iterations for r in res], "converged": int(sum(r.converged for r in res)),
-               "diverged": int(sum(status == W.DIVERGED))}
+               "diverged": int(sum(status == W.DIVERGED)), "anchors": self.op.last_anchor_count}
         self.history.append(rec)
         return rec
 
@@ -112,10 +112,11 @@ class GrowthState:
         self.noise_draws = np.vstack([self.noise_draws, nd])
 
 
-def growth_state(X0, y0, hyp, n_samples, num_features, seed, precision=W.F64, ctx=None) -> GrowthState:
+def growth_state(X0, y0, hyp, n_samples, num_features, seed, precision=W.F64, ctx=None,
+                 residual=W.RESIDUAL_DIRECT) -> GrowthState:
     """bo_init's sampling half (thompson.cpp:260-293): priors derive_seed(seed, 100 + s),
     prior values at the initial design, noise from Rng(derive_seed(seed, 3)) i-major."""
-    op = W.KernelOperator(hyp, X0, precision=precision, ctx=ctx)
+    op = W.KernelOperator(hyp, X0, precision=precision, ctx=ctx, residual=residual)
     d = X0.shape[1]
     priors = [W.sample_prior(hyp, d, num_features, W.derive_seed(seed, 100 + s)) for s in range(n_samples)]
     pv = W.rff_eval(op, priors) if n_samples else np.zeros((X0.shape[0], 0))
@@ -224,7 +225,8 @@ def grid_search_sgd_lr(op, b, cfg: W.SolverConfig, grid=(0.03, 0.1, 0.3, 1.0)) -
 
 
 def growth_sweep(method=W.CG, steps=range(21), n0=10_000, step=500, pool=20_000, d=8, n_samples=16,
-                 precision=W.F64, tol=1e-4, max_iters=2000, seed=0, lr=None, ctx=None) -> dict:
+                 precision=W.F64, tol=1e-4, max_iters=2000, seed=0, lr=None, ctx=None,
+                 residual=W.RESIDUAL_DIRECT) -> dict:
     """Configuration 2: RBF (l=0.5, s_f=1, sigma_n^2=1e-2), systems N = n0 + step*t drawn from
     a fixed pool, s = 17 (y + 16 pathwise samples, F=1024), warm (previous step's solution
     zero-extended) vs cold, per solver (AP block 500 greedy, SGD batch 512)."""
@@ -237,10 +239,10 @@ def growth_sweep(method=W.CG, steps=range(21), n0=10_000, step=500, pool=20_000,
     cfg = W.SolverConfig(method=method, tolerance=tol, max_iters=max_iters, precond_rank=100,
                          precond_shift=hyp.noise_scale ** 2, block_size=500, batch_size=512,
                          learning_rate=lr if lr is not None else 0.3, seed=seed)
-    out = {"method": method, "precision": precision, "steps": []}
+    out = {"method": method, "precision": precision, "residual": residual, "steps": []}
     states = {}
     for mode in ("warm", "cold"):
-        st = growth_state(Xp[:n0], yp[:n0], hyp, n_samples, 1024, seed, precision, ctx)
+        st = growth_state(Xp[:n0], yp[:n0], hyp, n_samples, 1024, seed, precision, ctx, residual)
         states[mode] = st
     ts = list(steps)
     for t in range(max(ts) + 1):

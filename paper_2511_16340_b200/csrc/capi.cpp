@@ -19,6 +19,8 @@ namespace wgp {
 
 static thread_local std::string g_last_error;
 
+void set_last_error(const char* msg) { g_last_error = msg; }
+
 void throw_error(wgp_status code, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
@@ -45,7 +47,10 @@ void launch_rff_eval64(const double* X, int ldx_row, int dim, int64_t m, const d
                        const double* ph, const double* amp, int F, int S, double coeff,
                        double* out, int64_t ldo, cudaStream_t st);
 void dist_init(Ctx& ctx, const void* uid);
+struct LoopGroup;
+void dist_init_loopback(Ctx& ctx, LoopGroup* g);
 void dist_destroy(Ctx& ctx);
+int loop_group_world(const LoopGroup* g);
 
 template <typename F>
 static wgp_status guard(F&& f) {
@@ -89,7 +94,7 @@ struct PhaseTimer {
 
 static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int64_t ldb, int s,
                       const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
-                      SolveOutputs& out, bool derive_seeds) {
+                      SolveOutputs& out, bool derive_seeds, const PrecondDev* given = nullptr) {
   cudaStream_t st = op.ctx->stream;
   PhaseTimer pt(st);
   if (!op.solve_cache) op.solve_cache = std::make_shared<SolverWork<double>>();
@@ -100,6 +105,11 @@ static void run_solve(Op& op, const wgp_solver_config& cfg, const double* B, int
   pt.mark("upload");
   switch (cfg.method) {
     case WGP_CG: {
+      if (given) {  // cg_solve_with (solvers.cpp:142): the caller's preconditioner, no rebuild
+        cg_solve_batched<double>(op, cfg, *given, w, out, st);
+        pt.mark("cg_loop");
+        break;
+      }
       if (!op.precond_cache) op.precond_cache = std::make_shared<PrecondDev>();
       PrecondDev& pd = *static_cast<PrecondDev*>(op.precond_cache.get());
       const int64_t rank = std::min<int64_t>(cfg.precond_rank, op.n);  // from_matrix :125-126
@@ -156,20 +166,27 @@ void wgp_kernel_timer_enable(int enable) {
   kt.on = enable != 0;
 }
 
-wgp_status wgp_kernel_timer_read(double* total_ms, int64_t* launches) {
+wgp_status wgp_kernel_timer_read_tag(const char* tag, double* total_ms, int64_t* launches) {
   return guard([&] {
-    WGP_REQUIRE(total_ms && launches, "wgp_kernel_timer_read: null argument");
+    WGP_REQUIRE(tag && total_ms && launches, "wgp_kernel_timer_read: null argument");
     wgp::KernelTimer& kt = wgp::kernel_timer();
     double tot = 0.0;
+    int64_t cnt = 0;
     for (auto& e : kt.ev) {
-      WGP_CUDA(cudaEventSynchronize(e.second));
+      if (std::strcmp(e.tag, tag) != 0) continue;
+      WGP_CUDA(cudaEventSynchronize(e.b));
       float ms = 0.f;
-      WGP_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+      WGP_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
       tot += ms;
+      ++cnt;
     }
     *total_ms = tot;
-    *launches = (int64_t)kt.ev.size();
+    *launches = cnt;
   });
+}
+
+wgp_status wgp_kernel_timer_read(double* total_ms, int64_t* launches) {
+  return wgp_kernel_timer_read_tag("kmatvec_tc", total_ms, launches);
 }
 
 const char* wgp_last_error(void) { return g_last_error.c_str(); }
@@ -191,16 +208,18 @@ void wgp_solver_config_default(wgp_solver_config* c) {  // solvers.hpp:27-48
 }
 
 void wgp_shard_range(int64_t n, int world, int rank, int64_t* row0, int64_t* row1) {
-  // contiguous chunk-aligned blocks; every rank gets floor/ceil of the chunk count
+  // equal chunk-aligned slots of shard_chunks(n, world) chunks (common.cuh); the rows of
+  // the last slot(s) stop at n
   if (world < 1) world = 1;
-  const int64_t nch = (n + kChunkRows - 1) / kChunkRows;
-  const int64_t c0 = nch * rank / world, c1 = nch * (rank + 1) / world;
-  int64_t a = c0 * kChunkRows, b = c1 * kChunkRows;
+  const int64_t c = shard_chunks(n, world);
+  int64_t a = (int64_t)rank * c * kChunkRows, b = (int64_t)(rank + 1) * c * kChunkRows;
   if (a > n) a = n;
   if (b > n) b = n;
   *row0 = a;
   *row1 = b;
 }
+
+int64_t wgp_shard_padded_rows(int64_t n, int world) { return padded_rows(n, world); }
 
 wgp_status wgp_ctx_create(int device, wgp_ctx** out) {
   return guard([&] {
@@ -233,6 +252,22 @@ wgp_status wgp_ctx_create_sharded(int device, int rank, int world, const void* u
       wgp_ctx_destroy(c);
       throw;
     }
+    *out = c;
+  });
+}
+
+wgp_status wgp_ctx_create_loopback(int device, int rank, void* group, wgp_ctx** out) {
+  return guard([&] {
+    WGP_REQUIRE(group && out, "wgp_ctx_create_loopback: null argument");
+    LoopGroup* g = static_cast<LoopGroup*>(group);
+    const int world = loop_group_world(g);
+    WGP_REQUIRE(rank >= 0 && rank < world, "wgp_ctx_create_loopback: bad rank");
+    wgp_ctx* c = nullptr;
+    wgp_status stc = wgp_ctx_create(device, &c);
+    if (stc != WGP_OK) throw Error(stc, g_last_error);
+    c->rank = rank;
+    c->world = world;
+    if (world > 1) dist_init_loopback(*c, g);
     *out = c;
   });
 }
@@ -295,6 +330,18 @@ wgp_status wgp_op_append_rows(wgp_op* op, const double* X, int64_t n_new, int64_
 }
 
 int64_t wgp_op_size(const wgp_op* op) { return op ? op->n : 0; }
+
+wgp_status wgp_op_set_residual_mode(wgp_op* op, int mode) {
+  return guard([&] {
+    WGP_REQUIRE(op, "wgp_op_set_residual_mode: null op");
+    WGP_REQUIRE(mode == WGP_RESIDUAL_DIRECT || mode == WGP_RESIDUAL_ANCHORED,
+                "unknown residual mode %d", mode);
+    op->resid_mode = mode;
+  });
+}
+
+int wgp_op_residual_mode(const wgp_op* op) { return op ? op->resid_mode : -1; }
+int wgp_op_last_anchor_count(const wgp_op* op) { return op ? op->last_anchors : 0; }
 int wgp_op_dim(const wgp_op* op) { return op ? op->dim : 0; }
 int wgp_op_precision(const wgp_op* op) { return op ? op->precision : -1; }
 
@@ -446,7 +493,8 @@ static wgp_status solve_impl(wgp_op* op, const wgp_solver_config* cfg, const dou
                              int s, const double* U1, int64_t ldu, int64_t n1, double* V, int64_t ldv,
                              int32_t* iterations, double* history, int64_t hist_stride,
                              int32_t* history_len, int32_t* converged, int32_t* col_status,
-                             int32_t* diverged_at, bool derive_seeds) {
+                             int32_t* diverged_at, bool derive_seeds,
+                             const PrecondDev* given = nullptr) {
   int fail_col = -1;
   int fail_iters = 0;
   wgp_status st = guard([&] {
@@ -466,7 +514,7 @@ static wgp_status solve_impl(wgp_op* op, const wgp_solver_config* cfg, const dou
     set_device(*op->ctx);
     SolveOutputs out(s);
     try {
-      run_solve(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out, derive_seeds);
+      run_solve(*op, *cfg, B, ldb, s, U1, ldu, n1, V, ldv, out, derive_seeds, given);
     } catch (Error& e) {
       fail_col = e.col;
       fail_iters = e.iterations;
@@ -527,6 +575,7 @@ wgp_status wgp_pivoted_cholesky(wgp_op* op, int64_t rank, double* L, int64_t ldl
     WGP_REQUIRE(op && achieved, "wgp_pivoted_cholesky: null argument");
     WGP_REQUIRE(rank >= 0 && rank <= op->n, "pivoted_cholesky: rank out of range");
     WGP_REQUIRE(!L || ldl >= op->n, "wgp_pivoted_cholesky: ldl < n");
+    WGP_REQUIRE(!L || op->ctx->world == 1, "pivoted_cholesky: L download needs an unsharded context");
     set_device(*op->ctx);
     cudaStream_t st = op->ctx->stream;
     PrecondDev pd;
@@ -808,6 +857,144 @@ wgp_status wgp_ascend_peaks(wgp_op* op, const double* Omega, const double* phase
       for (int k = 0; k < dim; ++k) best_x[(int64_t)k * S + s] = hx[(size_t)best * dim + k];
     }
   });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------
+// Reusable preconditioner (CgPreconditioner, solvers.hpp:82-100) and cg_solve_with
+// (solvers.hpp:118-119): bo_round builds ONE preconditioner per round and reuses it for every
+// per-column solve (thompson.cpp:359-384).
+struct wgp_precond {
+  wgp_op* op = nullptr;
+  int64_t n_at_build = 0;
+  PrecondDev pd;
+};
+
+static void check_precond(const wgp_precond* pc, const wgp_op* op) {
+  WGP_REQUIRE(pc, "null preconditioner");
+  WGP_REQUIRE(!op || pc->op == op, "preconditioner built for another operator");
+  WGP_REQUIRE(pc->op->n == pc->n_at_build,
+              "preconditioner built for %lld rows, operator now has %lld (rows appended)",
+              (long long)pc->n_at_build, (long long)pc->op->n);
+}
+
+extern "C" {
+
+wgp_status wgp_precond_create(wgp_op* op, int64_t rank, double shift, int mode, wgp_precond** out) {
+  return guard([&] {
+    WGP_REQUIRE(op && out, "wgp_precond_create: null argument");
+    WGP_REQUIRE(rank >= 0, "CgPreconditioner: negative rank");
+    WGP_REQUIRE(mode == WGP_SHIFT_CALIBRATED || mode == WGP_SHIFT_NOISE_ONLY, "unknown shift mode");
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    std::unique_ptr<wgp_precond> pc(new wgp_precond());
+    pc->op = op;
+    pc->n_at_build = op->n;
+    rank = std::min<int64_t>(rank, op->n);  // from_matrix (solvers.cpp:123-133)
+    if (rank > 0) {
+      build_pivoted_cholesky(*op, rank, pc->pd, st);
+      finish_preconditioner(*op, shift, mode, pc->pd, st);
+    } else {
+      int64_t a, b;
+      op->local_rows(&a, &b);
+      pc->pd.n = op->n;
+      pc->pd.r0 = a;
+      pc->pd.n_local = b - a;
+      pc->pd.shift = shift;
+    }
+    *out = pc.release();
+  });
+}
+
+wgp_status wgp_precond_create_from_factor(wgp_op* op, const double* L, int64_t ldl, int64_t k,
+                                          double shift, wgp_precond** out) {
+  return guard([&] {
+    WGP_REQUIRE(op && out && (k == 0 || L), "wgp_precond_create_from_factor: null argument");
+    WGP_REQUIRE(k >= 0 && (k == 0 || ldl >= op->n), "CgPreconditioner: bad factor shape");
+    set_device(*op->ctx);
+    cudaStream_t st = op->ctx->stream;
+    std::unique_ptr<wgp_precond> pc(new wgp_precond());
+    pc->op = op;
+    pc->n_at_build = op->n;
+    int64_t a, b;
+    op->local_rows(&a, &b);
+    PrecondDev& pd = pc->pd;
+    pd.n = op->n;
+    pd.r0 = a;
+    pd.n_local = b - a;
+    pd.k = k;
+    pd.shift = shift;
+    pd.kpad = k > 0 ? ((k + 3) / 4) * 4 : 0;
+    if (k > 0) {
+      // CgPreconditioner(L, shift) (solvers.cpp:109-121): this rank's rows of L, row-major
+      const int64_t nl = std::max<int64_t>(pd.n_local, 1);
+      std::vector<double> h((size_t)nl * pd.kpad, 0.0);
+      for (int64_t i = 0; i < pd.n_local; ++i)
+        for (int64_t t = 0; t < k; ++t) h[(size_t)i * pd.kpad + t] = L[t * ldl + a + i];
+      pd.L.ensure(h.size());
+      WGP_CUDA(cudaMemcpyAsync(pd.L.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
+      finish_preconditioner(*op, shift, WGP_SHIFT_NOISE_ONLY, pd, st);  // shift used as given
+    }
+    *out = pc.release();
+  });
+}
+
+void wgp_precond_destroy(wgp_precond* pc) {
+  if (!pc) return;
+  cudaSetDevice(pc->op->ctx->device);
+  delete pc;
+}
+
+wgp_status wgp_precond_get(const wgp_precond* pc, int64_t* rank, double* shift) {
+  return guard([&] {
+    WGP_REQUIRE(pc && rank && shift, "wgp_precond_get: null argument");
+    *rank = pc->pd.k;
+    *shift = pc->pd.shift;
+  });
+}
+
+wgp_status wgp_precond_apply(wgp_precond* pc, const double* R, int64_t ldr, int s, double* Z,
+                             int64_t ldz) {
+  return guard([&] {
+    check_precond(pc, nullptr);
+    Op& op = *pc->op;
+    WGP_REQUIRE(R && Z && s >= 1, "wgp_precond_apply: bad argument");
+    WGP_REQUIRE(op.ctx->world == 1, "wgp_precond_apply: host form needs an unsharded context");
+    const int64_t n = op.n;
+    WGP_REQUIRE(ldr >= n && ldz >= n, "CgPreconditioner::apply: length mismatch");
+    set_device(*op.ctx);
+    cudaStream_t st = op.ctx->stream;
+    DBuf<double> stage((size_t)n * s), dR((size_t)n * s), dZ((size_t)n * s);
+    const int64_t k = pc->pd.k;
+    DBuf<double> wt((size_t)(k + 1) * s), wp((size_t)padded_chunks(n, 1) * (k + 1) * s);
+    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, R, sizeof(double) * ldr,
+                               sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+    launch_colmajor_to_rows(stage.p, n, n, s, dR.p, true, st);
+    precond_apply<double>(op, pc->pd, dR.p, dZ.p, s, wt.p, wp.p, st);
+    launch_rows_to_colmajor(dZ.p, n, s, stage.p, n, true, st);
+    WGP_CUDA(cudaMemcpy2DAsync(Z, sizeof(double) * ldz, stage.p, sizeof(double) * n,
+                               sizeof(double) * n, s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+wgp_status wgp_cg_solve_with(wgp_op* op, const wgp_precond* pc, const wgp_solver_config* cfg,
+                             const double* B, int64_t ldb, int s, const double* U1, int64_t ldu,
+                             int64_t n1, double* V, int64_t ldv, int32_t* iterations,
+                             double* history, int64_t hist_stride, int32_t* history_len,
+                             int32_t* converged) {
+  try {
+    check_precond(pc, op);
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  }
+  if (!cfg) return WGP_INVALID_ARGUMENT;
+  wgp_solver_config c = *cfg;
+  c.method = WGP_CG;
+  return solve_impl(op, &c, B, ldb, s, U1, ldu, n1, V, ldv, iterations, history, hist_stride,
+                    history_len, converged, nullptr, nullptr, true, &pc->pd);
 }
 
 }  // extern "C"

@@ -34,6 +34,7 @@ struct Error : std::runtime_error {
 };
 
 [[noreturn]] void throw_error(wgp_status code, const char* fmt, ...);
+void set_last_error(const char* msg);  // the thread-local message of wgp_last_error()
 
 #define WGP_CUDA(call)                                                                   \
   do {                                                                                   \
@@ -111,7 +112,7 @@ __device__ __forceinline__ double exp_neg(double x) {
 }
 #endif
 
-struct Comm;  // NCCL plumbing (dist.cpp)
+struct Comm;  // NCCL / loopback plumbing (dist.cpp)
 
 struct Ctx {
   int device = 0;
@@ -144,6 +145,13 @@ struct Op {
   // pays no cudaMalloc / synchronous cudaFree for its [n][s] vectors (calls on one handle
   // are never concurrent)
   std::shared_ptr<void> solve_cache, precond_cache;
+  // true-residual mode of the CG solver on fp32 operators (wgp_op_set_residual_mode):
+  // WGP_RESIDUAL_DIRECT recomputes b - H v with the operator itself; WGP_RESIDUAL_ANCHORED
+  // evaluates it as r_a - H (v - v_a) with r_a = b - H v_a from the fp64 kernel at anchor
+  // iterates v_a, re-anchoring when the predicted error of the fast part reaches a fraction
+  // of the residual (solvers.cu).
+  int resid_mode = WGP_RESIDUAL_DIRECT;
+  int last_anchors = 0;  // fp64 anchor evaluations of the last CG solve
   bool tc_dirty = true;
   // GEMM1 operand format chosen at operand build: fp16 splits of x / l (kind::f16, half the
   // bytes and MMA time of tf32) when the scaled coordinates fit fp16, else tf32 splits of x.
@@ -183,6 +191,22 @@ __device__ __forceinline__ double chunk_sum_ordered(const double* __restrict__ p
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// Row partition (wgp_shard_range): every rank owns an equal, chunk-aligned slot of
+// shard_chunks(n, world) chunks (the last ranks' rows stop at n), so a full buffer padded
+// to padded_chunks(n, world) chunks is exchanged by ONE in-place all-gather of equal
+// slices.  Full [rows][s] buffers and [chunk][...] partial arrays that are all-gathered
+// are allocated with padded_chunks(...) chunks.
+inline int64_t shard_chunks(int64_t n, int world) {
+  const int64_t nch = (n + kChunkRows - 1) / kChunkRows;
+  if (world < 1) world = 1;
+  const int64_t c = (nch + world - 1) / world;
+  return c > 0 ? c : 1;
+}
+inline int64_t padded_chunks(int64_t n, int world) {
+  return shard_chunks(n, world) * (world < 1 ? 1 : world);
+}
+inline int64_t padded_rows(int64_t n, int world) { return padded_chunks(n, world) * kChunkRows; }
 
 // ------------------------------------------------------------------ collectives (dist.cpp)
 // All are no-ops (or local copies) when ctx.world == 1.

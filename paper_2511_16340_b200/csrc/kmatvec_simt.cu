@@ -12,7 +12,7 @@
 // (kmatvec_tc.cu) uses the norm form as a contraction.
 #include <cstdlib>
 
-#include "common.cuh"
+#include "solvers.h"
 
 namespace wgp {
 namespace {
@@ -333,6 +333,7 @@ void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0,
                          int64_t ncols, const double* V, int s, const double* B, double* Y,
                          bool gram, cudaStream_t st) {
   if (nrows <= 0 || s <= 0) return;
+  TimedScope ts_(sizeof(T) == 8 ? "kmatvec_f64" : "kmatvec_f32", st);
   if constexpr (sizeof(T) == 8) {
     static const bool simt = getenv("WGP_F64_SIMT") && atoi(getenv("WGP_F64_SIMT")) != 0;
     if (!simt) {

@@ -146,7 +146,17 @@ template <int NCOL>
 __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* kv, float c1,
                                            float nclog2e) {
   const float2 NC = make_float2(nclog2e, nclog2e);
+#ifdef WGP_KSCALE_IN_EXP
+  // (earlier form, kept for A/B probes) the 2^10 scale folded into the exponent argument:
+  // one FFMA2 fewer, but the argument then carries |a| ~ 10 and its fp32 rounding puts
+  // ~4e-7 relative error on the largest entries (d ~ 0)
   const float2 OFF = make_float2(KSCALE_LOG2, KSCALE_LOG2);
+#else
+  // the 2^10 scale is applied after ex2 (an exact power-of-two FMUL2): the exponent
+  // argument -z log2 e / -d2 log2 e / 2l^2 is ~0 for the largest entries, so its rounding
+  // error (|a| 2^-24, x ln 2 on k) vanishes where k matters most
+  const float2 SC = make_float2(0x1.0p10f, 0x1.0p10f);
+#endif
   if (kind == WGP_MATERN32) {
     const float2 C1 = make_float2(c1, c1);
 #pragma unroll
@@ -154,10 +164,17 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
       float2 r;
       r.x = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q])));
       r.y = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q + 1])));
+#ifdef WGP_KSCALE_IN_EXP
       const float2 a = __ffma2_rn(r, NC, OFF);  // log2(2^10 e^{-z})
+#else
+      const float2 a = __fmul2_rn(r, NC);  // log2(e^{-z})
+#endif
       float2 e;
       e.x = ptx::ex2_approx(a.x);
       e.y = ptx::ex2_approx(a.y);
+#ifndef WGP_KSCALE_IN_EXP
+      e = __fmul2_rn(e, SC);  // 2^10 e^{-z}, exact
+#endif
       const float2 z = __fmul2_rn(r, C1);
       const float2 k = __ffma2_rn(z, e, e);  // 2^10 (1+z) e^{-z}
       kv[2 * q] = k.x;
@@ -167,10 +184,17 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
 #pragma unroll
     for (int q = 0; q < NCOL / 2; ++q) {
       const float2 d2 = make_float2(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+#ifdef WGP_KSCALE_IN_EXP
       const float2 a = __ffma2_rn(d2, NC, OFF);  // log2(2^10 e^{-d2/2l^2})
+#else
+      const float2 a = __fmul2_rn(d2, NC);  // log2(e^{-d2/2l^2})
+#endif
       float2 e;
       e.x = ptx::ex2_approx(a.x);
       e.y = ptx::ex2_approx(a.y);
+#ifndef WGP_KSCALE_IN_EXP
+      e = __fmul2_rn(e, SC);
+#endif
       kv[2 * q] = e.x;
       kv[2 * q + 1] = e.y;
     }
@@ -986,17 +1010,9 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
                 op.dim);
     auto kern = tc::kmatvec_tc_kernel;
     WGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    KernelTimer& kt = kernel_timer();
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    if (kt.on) {
-      WGP_CUDA(cudaEventCreate(&ev0));
-      WGP_CUDA(cudaEventCreate(&ev1));
-      WGP_CUDA(cudaEventRecord(ev0, st));
-    }
-    kern<<<dim3(row_ctas, gy), tc::NTHREADS, smem, st>>>(prm, nsx, nsv);
-    if (kt.on) {
-      WGP_CUDA(cudaEventRecord(ev1, st));
-      kt.ev.emplace_back(ev0, ev1);
+    {
+      TimedScope ts("kmatvec_tc", st);
+      kern<<<dim3(row_ctas, gy), tc::NTHREADS, smem, st>>>(prm, nsx, nsv);
     }
     WGP_CUDA(cudaGetLastError());
     {

@@ -149,6 +149,14 @@ void launch_kmatvec_full(Op& op, const double* V, double* Y, int s, cudaStream_t
   dispatch(op, nullptr, V, Y, s, st);
 }
 
+void launch_residual_f64(Op& op, const double* B, const double* V, double* Y, int s,
+                         cudaStream_t st) {
+  int64_t r0, r1;
+  op.local_rows(&r0, &r1);
+  launch_kmatvec_simt<double>(op, op.X64.p + r0 * op.dpad, r1 - r0, r0, op.X64.p, op.n, V, s, B, Y,
+                              true, st);
+}
+
 // Y = B - H V  (B and Y: this rank's rows; V full)
 void launch_residual(Op& op, const double* B, const double* V, double* Y, int s, cudaStream_t st) {
   dispatch(op, B, V, Y, s, st);

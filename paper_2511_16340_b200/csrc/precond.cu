@@ -393,7 +393,7 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   const KParams p = op.kp();
   const int nch = ceil_div(n, kChunkRows);
   const int c0 = (int)(pd.r0 / kChunkRows);
-  DBuf<double> part((size_t)nch * k * k), G((size_t)k * k);
+  DBuf<double> part((size_t)padded_chunks(n, op.ctx->world) * k * k), G((size_t)k * k);
   if (pd.n_local > 0)
     chunk_atb_kernel<<<dim3(ceil_div(pd.n_local, kChunkRows), ceil_div(k, 64), ceil_div(k, 64)), 256, 0, st>>>(
         pd.L.p, (int)pd.kpad, k, pd.L.p, (int)pd.kpad, k, pd.n_local, part.p + (int64_t)c0 * k * k);

@@ -4,7 +4,7 @@
 // dense X Omega^T GEMM followed by cos and a GEMV.  Here the phase contraction (K = d),
 // the cos and the amplitude reduction are fused per (row tile, prior): the m x F phase
 // matrix never exists.  fp64 throughout (RHS generation is not precision-relaxed).
-#include "common.cuh"
+#include "solvers.h"
 
 namespace wgp {
 namespace {
@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(RT) rff_eval32_kernel(const double* __restrict
 void launch_rff_eval32(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
                        const double* ph, const double* amp, int F, int S, double coeff,
                        double* out, int64_t ldo, cudaStream_t st) {
+  TimedScope ts_("rff_eval32", st);
   WGP_REQUIRE(dim <= 32, "rff_eval: dim <= 32 supported, got %d", dim);
   if (m <= 0 || S <= 0) return;
   const size_t smem = sizeof(float) * (FT * dim + 2 * FT);
@@ -127,6 +128,7 @@ void launch_rff_eval32(const double* X, int ldx_row, int dim, int64_t m, const d
 void launch_rff_eval64(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
                        const double* ph, const double* amp, int F, int S, double coeff,
                        double* out, int64_t ldo, cudaStream_t st) {
+  TimedScope ts_("rff_eval", st);
   WGP_REQUIRE(dim <= 32, "rff_eval: dim <= 32 supported, got %d", dim);
   if (m <= 0 || S <= 0) return;
   const size_t smem = sizeof(double) * (FT * dim + 2 * FT);

@@ -12,7 +12,7 @@
 // columns is independent, so batching columns never changes a column's result.
 #include <algorithm>
 
-#include "common.cuh"
+#include "solvers.h"
 
 namespace wgp {
 namespace {
@@ -342,6 +342,7 @@ static void krows_launch(const Op& op, const T* X, dim3 grid, int64_t jlen, cons
 
 void launch_krows(const Op& op, const int* rows, int nb, const double* V, const double* B, int s,
                   const int* active, double* g, int64_t r0, int64_t r1, cudaStream_t st) {
+  TimedScope ts_("krows", st);
   // fixed j ranges of >= 1024 columns (at most 64), a function of n only
   const int64_t n = op.n;
   const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / 1024));
@@ -374,6 +375,7 @@ static void kcols_launch(const Op& op, const T* X, dim3 grid, const int* blk, in
 void launch_kcols(const Op& op, const int* blk, int bs, const double* delta, int s,
                   const int* active, double* R, int64_t r0, int64_t nrows, cudaStream_t st) {
   if (nrows <= 0) return;
+  TimedScope ts_("kcols", st);
   const dim3 grid(ceil_div(nrows, 128), s);
   const int d = op.dim;
   if (op.f64()) {

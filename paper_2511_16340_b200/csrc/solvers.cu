@@ -11,6 +11,7 @@
 // (alpha, beta, freeze) runs in single-block "step" kernels on the device.
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "rng.h"
 #include "solvers.h"
@@ -71,6 +72,27 @@ __global__ void cg_beta_kernel(const double* __restrict__ part, int nch, int s,
   }
 }
 
+// Anchored residual (Op::resid_mode): from the two-slot chunk partials of (|r|^2, |d|^2)
+// per column, rel = |r| / |b| and dn = |d| (no freezing: the host decides after a possible
+// re-anchor).
+__global__ void anchor_norms_kernel(const double* __restrict__ part, int nch, int s,
+                                    const double* __restrict__ bnorm, double* __restrict__ rel,
+                                    double* __restrict__ dn) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
+    const double rr = chunk_sum_ordered(part + c, nch, 2 * (int64_t)s);
+    const double dd = chunk_sum_ordered(part + s + c, nch, 2 * (int64_t)s);
+    rel[c] = bnorm[c] > 0.0 ? sqrt(rr) / bnorm[c] : 0.0;
+    dn[c] = sqrt(dd);
+  }
+}
+
+__global__ void fill2_kernel(double* __restrict__ a, int s) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
+    a[c] = 1.0;
+    a[s + c] = -1.0;
+  }
+}
+
 inline int sgrid(int s) { return (s + 255) / 256; }
 
 }  // namespace
@@ -85,14 +107,22 @@ void SolverWork<T>::alloc(const Op& op, int s_) {
   s = s_;
   nch = ceil_div(N, kChunkRows);
   c0 = (int)(r0 / kChunkRows);
-  const size_t ns = (size_t)std::max<int64_t>(n, 1) * s, Ns = (size_t)N * s;
+  // full-row buffers and all-gathered chunk partials are padded to world equal slots
+  const int world = op.ctx->world;
+  const size_t ns = (size_t)std::max<int64_t>(n, 1) * s, Ns = (size_t)padded_rows(N, world) * s;
+  const size_t pch = (size_t)padded_chunks(N, world);
   V.ensure(Ns);
   P.ensure(Ns);
   R.ensure(ns);
   Z.ensure(ns);
   HP.ensure(ns);
   B.ensure(ns);
-  part.ensure((size_t)(nch > 0 ? nch : 1) * 2 * s);
+  if (op.resid_mode == WGP_RESIDUAL_ANCHORED && !op.f64()) {
+    VA.ensure(Ns);
+    RA.ensure(ns);
+    anc.ensure((size_t)4 * s);
+  }
+  part.ensure(pch * 2 * s);
   scal.ensure((size_t)6 * s);
   act.ensure((size_t)2 * s + 2);
 }
@@ -111,6 +141,7 @@ void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb
     launch_colmajor_to_rows(stage.p, n, n, s, w.B.p, true, st);
   }
   WGP_CUDA(cudaMemsetAsync(w.V.p, 0, sizeof(T) * w.N * s, st));
+  w.warm = U1 && n1 > 0;
   if (U1 && n1 > 0) {  // expand_init: [u1; 0] (solvers.cpp:43-48), full rows on every rank
     WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n1, U1, sizeof(double) * ldu,
                                sizeof(double) * n1, s, cudaMemcpyHostToDevice, st));
@@ -139,6 +170,69 @@ static void dots(const Op& op, SolverWork<T>& w, const T* A, const T* Bv, cudaSt
   dist_allgather_chunks(*op.ctx, w.part.p, w.N, w.s, st);
 }
 
+// Two column dot products in one pass (slots q = 0, 1 of [nch][2][s] partials).
+template <typename T>
+static void dots2(const Op& op, SolverWork<T>& w, const T* A0, const T* B0, const T* A1,
+                  const T* B1, cudaStream_t st) {
+  if (w.n > 0)
+    launch_coldots<T>(A0, B0, A1, B1, w.n, w.s, w.part.p + (int64_t)w.c0 * 2 * w.s, st);
+  dist_allgather_chunks(*op.ctx, w.part.p, w.N, 2 * (int64_t)w.s, st);
+}
+
+// Anchored true residual (WGP_RESIDUAL_ANCHORED, fp32 operators).  The iterate is kept as
+// v = v_a + d (VA full rows, V = d full rows); r_a = b - H v_a comes from the fp64 kernel,
+// the fast operator only sees d:  r = r_a - H_fast d.  Its error is about eps_c |d_c|, with
+// eps_c the error per unit |d| of column c measured at the previous anchors (x2), so the
+// floor eps |H||v| / |b| of the direct form shrinks by |d| / |v|.  When eps_c |d_c| exceeds
+// kAnchorFrac |r_c| for an active column the solver re-anchors: v_a += d, d = 0,
+// r = r_a = b - H v_a in fp64 (and eps_c is re-measured from r_fast - r_a).
+constexpr double kAnchorFracDefault = 0.05;
+static double anchor_frac() {  // WGP_ANCHOR_FRAC overrides (probes; 0 = anchor every iteration)
+  const char* e = getenv("WGP_ANCHOR_FRAC");
+  return e ? atof(e) : kAnchorFracDefault;
+}
+constexpr double kAnchorSafety = 2.0;
+
+template <typename T>
+struct Anchor {
+  Op& op;
+  SolverWork<T>& w;
+  cudaStream_t st;
+  std::vector<double> eps, dn, hrel_fast;
+  int count = 0;
+  Anchor(Op& o, SolverWork<T>& wk, cudaStream_t s_)
+      : op(o), w(wk), st(s_), eps(wk.s, INFINITY), dn(wk.s, 0.0), hrel_fast(wk.s, 0.0) {}
+  double* ones() { return w.anc.p; }
+  double* minus_ones() { return w.anc.p + w.s; }
+  double* dnorm() { return w.anc.p + 2 * w.s; }
+
+  // Move the anchor to the current iterate and set R = r_a exactly (fp64 kernel).  With
+  // calibrate, R holds the fast residual of the same iterate on entry: eps is re-measured.
+  void reanchor(bool calibrate) {
+    const int64_t n = w.n, N = w.N;
+    const int s = w.s;
+    if (calibrate && n > 0)
+      WGP_CUDA(cudaMemcpyAsync(w.Z.p, w.R.p, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
+    launch_axpy_cols<T>(w.VA.p, w.V.p, ones(), N, s, st);  // v_a += d (full rows, replicated)
+    WGP_CUDA(cudaMemsetAsync(w.V.p, 0, sizeof(T) * N * s, st));
+    launch_residual_f64(op, w.B.p, w.VA.p, w.RA.p, s, st);
+    if (n > 0) WGP_CUDA(cudaMemcpyAsync(w.R.p, w.RA.p, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
+    ++count;
+    if (!calibrate) return;
+    if (n > 0) launch_axpy_cols<T>(w.Z.p, w.R.p, minus_ones(), n, s, st);  // r_fast - r_a
+    dots(op, w, w.Z.p, w.Z.p, st);
+    launch_chunk_sum(w.part.p, w.nch, s, dnorm(), st);
+    std::vector<double> e2(s);
+    WGP_CUDA(cudaMemcpyAsync(e2.data(), dnorm(), sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    for (int c = 0; c < s; ++c)
+      if (dn[c] > 0.0) {
+        const double e = kAnchorSafety * std::sqrt(e2[c]) / dn[c];
+        eps[c] = std::isinf(eps[c]) ? e : std::max(eps[c], e);
+      }
+  }
+};
+
 template <typename T>
 void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd,
                       SolverWork<T>& w, SolveOutputs& out, cudaStream_t st) {
@@ -153,20 +247,39 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
   int* fail = w.act.p + s;
   const int nch = w.nch;
   const Ctx& ctx = *op.ctx;
-  w.pwork.ensure((size_t)(nch > 0 ? nch : 1) * (pd.k + 1) * s);
+  const bool anchored = op.resid_mode == WGP_RESIDUAL_ANCHORED && !op.f64();
+  w.pwork.ensure((size_t)padded_chunks(N, ctx.world) * (pd.k + 1) * s);
   w.tvec.ensure((size_t)(pd.k + 1) * s);
+  Anchor<T> anc(op, w, st);
+  const double frac = anchor_frac();
+  op.last_anchors = 0;
 
   // |b| per column
   dots(op, w, w.B.p, w.B.p, st);
   init_bnorm_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, bnorm, active);
   // r0 = b - H v0 (solvers.cpp:150); V is full on every rank
-  launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
+  if (anchored) {
+    fill2_kernel<<<sgrid(s), 256, 0, st>>>(w.anc.p, s);
+    // v = v_a + d with v_a = v0, d = 0: r0 = r_a in fp64 (exactly b for a cold start)
+    std::swap(w.V, w.VA);
+    WGP_CUDA(cudaMemsetAsync(w.V.p, 0, sizeof(T) * N * s, st));
+    if (w.warm) {
+      launch_residual_f64(op, w.B.p, w.VA.p, w.RA.p, s, st);
+      anc.count = 1;
+    } else if (n > 0) {
+      WGP_CUDA(cudaMemcpyAsync(w.RA.p, w.B.p, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
+    }
+    if (n > 0) WGP_CUDA(cudaMemcpyAsync(w.R.p, w.RA.p, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
+  } else {
+    launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);
+  }
   dots(op, w, w.R.p, w.R.p, st);
   resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance, rel,
                                               active);
-  std::vector<double> hrel(s);
+  std::vector<double> hrel(s), hbnorm(s);
   std::vector<int> hact(s + 1), prev_act(s);
   WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+  WGP_CUDA(cudaMemcpyAsync(hbnorm.data(), bnorm, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
   WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
   WGP_CUDA(cudaStreamSynchronize(st));
   int n_active = 0;
@@ -177,7 +290,16 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
     n_active += hact[c];
     prev_act[c] = hact[c];
   }
-  if (n_active == 0) return;
+  auto finish = [&] {
+    if (anchored) {  // v = v_a + d
+      launch_axpy_cols<T>(w.V.p, w.VA.p, anc.ones(), N, s, st);
+      op.last_anchors = anc.count;
+    }
+  };
+  if (n_active == 0) {
+    finish();
+    return;
+  }
 
   // z = P r; p = z; rz = r.z (solvers.cpp:157-159)
   precond_apply<T>(op, pd, w.R.p, w.Z.p, s, w.tvec.p, w.pwork.p, st);
@@ -194,14 +316,48 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
     cg_alpha_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, alpha, fail);
     if (n > 0) launch_axpy_cols<T>(w.Vl(), w.Pl(), alpha, n, s, st);  // v += alpha p (:168)
     dist_allgather_rows(ctx, w.V.p, N, s, sizeof(T), st);
-    launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);         // r = b - H v (:171)
-    dots(op, w, w.R.p, w.R.p, st);
-    resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance, rel,
-                                                active);
-    WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
-    WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * (s + 1), cudaMemcpyDeviceToHost,
-                             st));
-    WGP_CUDA(cudaStreamSynchronize(st));
+    if (!anchored) {
+      launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // r = b - H v (:171)
+      dots(op, w, w.R.p, w.R.p, st);
+      resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance,
+                                                  rel, active);
+      WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * (s + 1), cudaMemcpyDeviceToHost,
+                               st));
+      WGP_CUDA(cudaStreamSynchronize(st));
+    } else {
+      // r = r_a - H_fast d (:171 on v = v_a + d); |r| and |d| per column in one pass
+      launch_residual(op, w.RA.p, w.V.p, w.R.p, s, st);
+      dots2(op, w, w.R.p, w.R.p, w.Vl(), w.Vl(), st);
+      anchor_norms_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, bnorm, rel, anc.dnorm());
+      WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaMemcpyAsync(anc.dn.data(), anc.dnorm(), sizeof(double) * s,
+                               cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * (s + 1), cudaMemcpyDeviceToHost,
+                               st));
+      WGP_CUDA(cudaStreamSynchronize(st));
+      bool need = false;
+      for (int c = 0; c < s; ++c)
+        if (hact[c] && anc.eps[c] * anc.dn[c] >= frac * hrel[c] * hbnorm[c]) need = true;
+      if (need) {  // re-anchor at this iterate; the history gets the fp64 residual
+        anc.reanchor(true);
+        dots(op, w, w.R.p, w.R.p, st);
+        resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance,
+                                                    rel, active);
+        WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+        WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * s, cudaMemcpyDeviceToHost, st));
+        WGP_CUDA(cudaStreamSynchronize(st));
+      } else {  // freeze converged columns (resid_step's rule, decided on the host)
+        bool changed = false;
+        for (int c = 0; c < s; ++c)
+          if (hact[c] && hrel[c] <= cfg.tolerance) {
+            hact[c] = 0;
+            changed = true;
+          }
+        if (changed)
+          WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
+      }
+    }
     if (hact[s] != INT_MAX) {
       Error e(WGP_NOT_SPD, "cg_solve: non-positive curvature encountered");
       e.col = hact[s];
@@ -223,6 +379,7 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
     cg_beta_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta, 0);
     if (n > 0) launch_xpby_cols<T>(w.Pl(), w.Z.p, beta, active, n, s, st);  // p = z + beta p (:180)
   }
+  finish();
   WGP_CUDA(cudaGetLastError());
 }
 
@@ -373,7 +530,7 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   DBuf<double> Rfull;
   double* Rall = w.R.p;
   if (ctx.world > 1) {
-    Rfull.alloc((size_t)N * s);
+    Rfull.alloc((size_t)padded_rows(N, ctx.world) * s);
     Rall = Rfull.p;
   }
   double* Rloc = Rall + r0 * s;  // this rank's rows

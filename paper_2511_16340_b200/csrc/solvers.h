@@ -17,6 +17,11 @@ struct SolverWork {
   int nch = 0;          // global chunk count
   int c0 = 0;
   DBuf<T> V, R, Z, P, HP, B;
+  // anchored true residual (Op::resid_mode): V then holds d = v - v_a, VA the anchor v_a
+  // (full rows), RA = b - H v_a (local rows, fp64 kernel); warm = nonzero initial v
+  DBuf<T> VA, RA;
+  DBuf<double> anc;  // [4][s]: ones, minus ones, |d| per column, spare
+  bool warm = false;
   T* Vl() const { return V.p + r0 * s; }
   T* Pl() const { return P.p + r0 * s; }
   DBuf<double> part;   // [nch][2][s] chunk partials
@@ -40,6 +45,10 @@ struct SolveOutputs {
 // tcgen05 3xTF32), which converts on the fly.
 void launch_kmatvec_full(Op& op, const double* V, double* Y, int s, cudaStream_t st);
 void launch_residual(Op& op, const double* B, const double* V, double* Y, int s, cudaStream_t st);
+// Y = B - H V on this rank's rows with the fp64 kernel whatever the operator's precision
+// (the anchor residuals of WGP_RESIDUAL_ANCHORED)
+void launch_residual_f64(Op& op, const double* B, const double* V, double* Y, int s,
+                         cudaStream_t st);
 template <typename T>
 void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
                          int64_t ncols, const double* V, int s, const double* B, double* Y,
@@ -61,19 +70,43 @@ bool op_cross_tc(Op& op, const double* Xs, int64_t m, int dpad, const double* W,
                  cudaStream_t st);
 bool tc_build_cross_rows(const Op& op, const double* Xs, int64_t m, int dpad, DBuf<float>& XAc,
                          cudaStream_t st);
-// launch timing of the main TC kernel (wgp_kernel_timer_*): event pairs on the launch stream
+// launch timing of the hot kernels (wgp_kernel_timer_*): event pairs on the launch stream,
+// tagged by kernel ("kmatvec_tc", "kmatvec_f64", "krows", "kcols", "rff_eval", "rff_eval32")
 struct KernelTimer {
   bool on = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  struct Entry {
+    const char* tag;
+    cudaEvent_t a, b;
+  };
+  std::vector<Entry> ev;
   void clear() {
     for (auto& e : ev) {
-      cudaEventDestroy(e.first);
-      cudaEventDestroy(e.second);
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
     }
     ev.clear();
   }
 };
 KernelTimer& kernel_timer();
+// RAII: CUDA events around the launches in its scope when the timer is on
+struct TimedScope {
+  cudaEvent_t a = nullptr;
+  cudaStream_t st;
+  const char* tag;
+  TimedScope(const char* t, cudaStream_t s) : st(s), tag(t) {
+    if (kernel_timer().on) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~TimedScope() {
+    if (!a) return;
+    cudaEvent_t b = nullptr;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, st);
+    kernel_timer().ev.push_back({tag, a, b});
+  }
+};
 bool tc_supported(int dim, int precision);  // false -> the fp32 CUDA-core kernel serves this dim
 
 template <typename T>

@@ -51,27 +51,27 @@ __global__ void rows_to_colmajor_kernel(const T* __restrict__ src, int64_t n, in
   }
 }
 
-// One block per (chunk, group of up to 32 columns).  Per column the chunk is cut into 32 fixed 16-row slabs summed
-// sequentially, then the 32 slab sums are added in slab order: the order of every column's
-// sum depends only on the row index, never on s or on the other columns (solve_many must
-// equal single-RHS solves bitwise, test_solvers.cpp:397-413).
+// One block per (chunk, group of up to 16 columns), one thread per (column, 16-row slab):
+// all 32 slabs of the chunk load at once (16 rows x 2 NQ arrays in flight per thread, one
+// pass), then one thread per column adds the 32 slab sums in slab order.  Per column the
+// chunk is 32 fixed 16-row slabs, each summed sequentially, slab sums added in slab order:
+// the order of every column's sum depends only on the row index, never on s or on the other
+// columns (solve_many must equal single-RHS solves bitwise, test_solvers.cpp:397-413).
 constexpr int kSlabRows = kChunkRows / 32;
-constexpr int kColsPerBlock = 32;  // coldots: columns per block (x 8 slabs = 256 threads)
+constexpr int kColsPerBlock = 16;  // coldots: columns per block (x 32 slabs = 512 threads)
 
 template <typename T, int NQ>
-__global__ void __launch_bounds__(256) coldots_kernel(const T* __restrict__ A0,
+__global__ void __launch_bounds__(512) coldots_kernel(const T* __restrict__ A0,
                                                       const T* __restrict__ B0,
                                                       const T* __restrict__ A1,
                                                       const T* __restrict__ B1, int64_t n, int s,
-                                                      int cb, int spp, double* __restrict__ part) {
-  // block (chunk, group of cb <= 32 columns): threads = cb columns x spp slabs, the 32 slabs
-  // in passes of spp; a warp reads whole row segments of up to 256 contiguous bytes
+                                                      int cb, double* __restrict__ part) {
   __shared__ double red[NQ][32][kColsPerBlock];
   const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
   const int cl = threadIdx.x % cb;
+  const int q = threadIdx.x / cb;  // slab
   const int c = blockIdx.y * cb + cl;
-  for (int q = threadIdx.x / cb; q < 32; q += spp) {
-    if (c >= s) break;
+  if (c < s) {
     const int64_t i0 = r0 + (int64_t)q * kSlabRows;
     const int64_t i1 = min(n, i0 + kSlabRows);
     double a0 = 0.0, a1 = 0.0;
@@ -106,25 +106,37 @@ __global__ void __launch_bounds__(256) coldots_kernel(const T* __restrict__ A0,
     if (NQ > 1) red[NQ - 1][q][cl] = a1;
   }
   __syncthreads();
-  if (threadIdx.x < cb && c < s) {
-    double t0 = 0.0, t1 = 0.0;
-    for (int k = 0; k < 32; ++k) {
-      t0 += red[0][k][cl];
-      if (NQ > 1) t1 += red[NQ - 1][k][cl];
+  if (threadIdx.x < cb * NQ) {
+    const int col = threadIdx.x % cb, qq = threadIdx.x / cb;
+    const int cc = blockIdx.y * cb + col;
+    if (cc < s) {
+      double t = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) t += red[qq][k][col];
+      part[(int64_t)blockIdx.x * NQ * s + (int64_t)qq * s + cc] = t;
     }
-    double* out = part + (int64_t)blockIdx.x * NQ * s;
-    out[c] = t0;
-    if (NQ > 1) out[s + c] = t1;
   }
 }
 
 // Column sums of chunk partials part[chunk][s] in chunk order (the scalar-step kernels'
 // order), for the standalone device dot product of the C-ABI.
-__global__ void chunk_sum_kernel(const double* __restrict__ part, int nch, int s,
-                                 double* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= s) return;
-  out[c] = chunk_sum_ordered(part + c, nch, s);
+// One block per column: the block stages the column's nch partials in shared memory with
+// parallel loads, then one thread adds them in chunk order (the same order as
+// chunk_sum_ordered) -- a chain of dependent fp64 adds instead of dependent L2 round trips.
+__global__ void __launch_bounds__(256) chunk_sum_kernel(const double* __restrict__ part, int nch,
+                                                        int s, double* __restrict__ out) {
+  __shared__ double buf[2048];
+  const int c = blockIdx.x;
+  double acc = 0.0;
+  for (int base = 0; base < nch; base += 2048) {
+    const int m = min(2048, nch - base);
+    for (int q = threadIdx.x; q < m; q += blockDim.x) buf[q] = part[(int64_t)(base + q) * s + c];
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int q = 0; q < m; ++q) acc += buf[q];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[c] = acc;
 }
 
 // Element-wise column updates of [n][s] arrays.  The grid covers `rows_step` whole rows per
@@ -242,18 +254,17 @@ void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t 
   const int nch = ceil_div(n, kChunkRows);
   if (nch <= 0) return;
   const int cb = s < kColsPerBlock ? s : kColsPerBlock;
-  const int spp = std::min(32, 256 / cb);  // slabs per pass
   const dim3 grid(nch, ceil_div(s, cb));
   if (A1)
-    coldots_kernel<T, 2><<<grid, cb * spp, 0, st>>>(A0, B0, A1, B1, n, s, cb, spp, part);
+    coldots_kernel<T, 2><<<grid, cb * 32, 0, st>>>(A0, B0, A1, B1, n, s, cb, part);
   else
-    coldots_kernel<T, 1><<<grid, cb * spp, 0, st>>>(A0, B0, A0, B0, n, s, cb, spp, part);
+    coldots_kernel<T, 1><<<grid, cb * 32, 0, st>>>(A0, B0, A0, B0, n, s, cb, part);
   WGP_CUDA(cudaGetLastError());
 }
 
 void launch_chunk_sum(const double* part, int nch, int s, double* out, cudaStream_t st) {
   if (s <= 0) return;
-  chunk_sum_kernel<<<(s + 127) / 128, 128, 0, st>>>(part, nch, s, out);
+  chunk_sum_kernel<<<s, 256, 0, st>>>(part, nch, s, out);
   WGP_CUDA(cudaGetLastError());
 }
 

@@ -26,7 +26,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwarmgp_b200.so")
+# WGP_LIB_PATH: an alternative build of the same library (A/B probes only)
+LIB_PATH = os.environ.get("WGP_LIB_PATH") or os.path.join(_HERE, "libwarmgp_b200.so")
 
 MATERN32, RBF = 0, 1
 F64, F32_3XTF32, TF32, F32_SIMT = 0, 1, 2, 3
@@ -34,6 +35,7 @@ CG, SGD, AP = 0, 1, 2
 SGD_UNBIASED, SGD_BLOCK = 0, 1
 AP_GREEDY, AP_CYCLIC = 0, 1
 SHIFT_CALIBRATED, SHIFT_NOISE_ONLY = 0, 1
+RESIDUAL_DIRECT, RESIDUAL_ANCHORED = 0, 1
 OK, INVALID_ARGUMENT, NOT_SPD, DIVERGED, CUDA_ERROR, NCCL_ERROR, OOM = range(7)
 
 # Every symbol include/warmgp_capi.h declares (checked by tests/test_capi_abi.py).
@@ -50,6 +52,12 @@ EXPORTS = (
     "wgp_exact_solve", "wgp_grad_posterior", "wgp_ascend_peaks",
     "wgp_mll", "wgp_optimize_mll", "wgp_median_heuristic_lengthscale",
     "wgp_axpy_cols_dev", "wgp_xpby_cols_dev", "wgp_coldots_dev",
+    "wgp_op_set_residual_mode", "wgp_op_residual_mode", "wgp_op_last_anchor_count",
+    "wgp_loopback_group_create", "wgp_loopback_group_destroy", "wgp_ctx_create_loopback",
+    "wgp_shard_padded_rows",
+    "wgp_precond_create", "wgp_precond_create_from_factor", "wgp_precond_destroy", "wgp_precond_get",
+    "wgp_precond_apply", "wgp_cg_solve_with", "wgp_cross_kernel", "wgp_relative_residual",
+    "wgp_quadratic_objective", "wgp_init_weights", "wgp_build_sample_rhs", "wgp_kernel_timer_read_tag",
 )
 
 
@@ -111,6 +119,21 @@ def _declare(L):
         "wgp_ctx_create": (C.c_int, [C.c_int, P]),
         "wgp_nccl_unique_id": (C.c_int, [P]),
         "wgp_ctx_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, P, P]),
+        "wgp_loopback_group_create": (C.c_int, [C.c_int, P]),
+        "wgp_loopback_group_destroy": (None, [P]),
+        "wgp_ctx_create_loopback": (C.c_int, [C.c_int, C.c_int, P, P]),
+        "wgp_shard_padded_rows": (I64, [I64, C.c_int]),
+        "wgp_precond_create": (C.c_int, [P, I64, D, C.c_int, P]),
+        "wgp_precond_create_from_factor": (C.c_int, [P, P, I64, I64, D, P]),
+        "wgp_precond_destroy": (None, [P]),
+        "wgp_precond_get": (C.c_int, [P, P, P]),
+        "wgp_precond_apply": (C.c_int, [P, P, I64, C.c_int, P, I64]),
+        "wgp_cg_solve_with": (C.c_int, [P, P, P, P, I64, C.c_int, P, I64, I64, P, I64, P, P, I64, P, P]),
+        "wgp_cross_kernel": (C.c_int, [P, P, I64, I64, P, I64]),
+        "wgp_relative_residual": (C.c_int, [P, P, I64, P, I64, C.c_int, P]),
+        "wgp_quadratic_objective": (C.c_int, [P, P, I64, P, I64, C.c_int, P]),
+        "wgp_init_weights": (C.c_int, [P, I64, I64, P]),
+        "wgp_build_sample_rhs": (C.c_int, [P, P, P, P, C.c_int, D, D, C.c_uint64, P]),
         "wgp_ctx_destroy": (None, [P]),
         "wgp_allgather_rows_dev": (C.c_int, [P, P, I64, C.c_int, P]),
         "wgp_ctx_stream": (P, [P]),
@@ -120,6 +143,9 @@ def _declare(L):
         "wgp_op_size": (I64, [P]),
         "wgp_op_dim": (C.c_int, [P]),
         "wgp_op_precision": (C.c_int, [P]),
+        "wgp_op_set_residual_mode": (C.c_int, [P, C.c_int]),
+        "wgp_op_residual_mode": (C.c_int, [P]),
+        "wgp_op_last_anchor_count": (C.c_int, [P]),
         "wgp_kmatvec": (C.c_int, [P, P, I64, C.c_int, P, I64]),
         "wgp_kmatvec_dev": (C.c_int, [P, P, P, C.c_int, P]),
         "wgp_residual_dev": (C.c_int, [P, P, P, P, C.c_int, P]),
@@ -150,6 +176,7 @@ def _declare(L):
         "wgp_grad_posterior": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, P, I64, P, I64, P, I64]),
         "wgp_ascend_peaks": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, P, C.c_int, C.c_int, D, P, P]),
         "wgp_kernel_timer_read": (C.c_int, [P, P]),
+        "wgp_kernel_timer_read_tag": (C.c_int, [C.c_char_p, P, P]),
         "wgp_sample_prior": (C.c_int, [C.c_int, D, I64, I64, C.c_uint64, P, P, P]),
     }
     for name, (res, args) in sig.items():
@@ -201,6 +228,11 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
     return a.value, b.value
 
 
+def shard_padded_rows(n: int, world: int) -> int:
+    """Rows of a full buffer exchanged by allgather_rows_dev (world equal slots)."""
+    return int(lib().wgp_shard_padded_rows(n, world))
+
+
 @dataclass
 class KernelHyperparams:
     """warmgp::KernelHyperparams (kernel.hpp:8-14) + ``kind`` (RBF extension)."""
@@ -210,12 +242,39 @@ class KernelHyperparams:
     kind: int = MATERN32
 
 
+class LoopbackGroup:
+    """`world` ranks emulated by threads of this process on one device
+    (wgp_loopback_group_create): each thread creates DeviceContext(device, rank,
+    loopback=group) and runs the sharded calls; collectives are host barriers plus
+    device-to-device copies (correctness testing of the sharded path, not a performance
+    configuration).  The library calls release the GIL, so the rank threads run
+    concurrently."""
+
+    def __init__(self, world: int):
+        self._h = C.c_void_p()
+        _check(lib().wgp_loopback_group_create(int(world), C.byref(self._h)))
+        self.world = int(world)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().wgp_loopback_group_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
+
+
 class DeviceContext:
     """One CUDA device (one process per GPU); optionally a NCCL row-sharded group."""
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None,
+                 loopback: "LoopbackGroup | None" = None):
         self._h = C.c_void_p()
-        if world == 1:
+        self._group = loopback  # keeps the group alive while this context exists
+        if loopback is not None:
+            world = loopback.world
+            _check(lib().wgp_ctx_create_loopback(device, rank, loopback._h, C.byref(self._h)))
+        elif world == 1:
             _check(lib().wgp_ctx_create(device, C.byref(self._h)))
         else:
             buf = C.create_string_buffer(bytes(unique_id), 128)
@@ -229,7 +288,8 @@ class DeviceContext:
         return buf.raw
 
     def allgather_rows_dev(self, dV_ptr: int, n: int, s: int, stream: int = 0):
-        """In-place all-gather of this group's row slices of a full n x s fp64 buffer."""
+        """In-place all-gather of this group's row slices of a full fp64 buffer with
+        shard_padded_rows(n, world) x s rows."""
         _check(lib().wgp_allgather_rows_dev(self._h, C.c_void_p(dV_ptr), n, s,
                                             C.c_void_p(stream) if stream else None))
 
@@ -281,7 +341,8 @@ class KernelOperator:
     """
 
     def __init__(self, hyp: KernelHyperparams, X=None, dim: int | None = None,
-                 precision: int = F64, ctx: DeviceContext | None = None):
+                 precision: int = F64, ctx: DeviceContext | None = None,
+                 residual: int = RESIDUAL_DIRECT):
         self.ctx = ctx or default_context()
         self.hyp = hyp
         if X is not None:
@@ -294,6 +355,8 @@ class KernelOperator:
                                    hyp.noise_scale, precision, int(dim), C.byref(self._h)))
         self.dim = int(dim)
         self.precision = precision
+        if residual != RESIDUAL_DIRECT:
+            self.residual_mode = residual
         if X is not None and X.shape[0] > 0:
             self.append_rows(X)
 
@@ -306,6 +369,20 @@ class KernelOperator:
     @property
     def n(self) -> int:
         return int(lib().wgp_op_size(self._h))
+
+    @property
+    def residual_mode(self) -> int:
+        """CG true-residual mode (RESIDUAL_DIRECT / RESIDUAL_ANCHORED, warmgp_capi.h)."""
+        return int(lib().wgp_op_residual_mode(self._h))
+
+    @residual_mode.setter
+    def residual_mode(self, mode: int):
+        _check(lib().wgp_op_set_residual_mode(self._h, int(mode)))
+
+    @property
+    def last_anchor_count(self) -> int:
+        """fp64 anchor evaluations made by the last CG solve (RESIDUAL_ANCHORED)."""
+        return int(lib().wgp_op_last_anchor_count(self._h))
 
     def size(self) -> int:
         return self.n
@@ -400,23 +477,103 @@ class SolveResult:
 
 
 def init_weights(init: Initialization, n1: int, n2: int) -> np.ndarray:
-    """init_weights (solvers.cpp:27-38): cold -> zeros(n1+n2); warm -> [u1; 0]."""
+    """init_weights (solvers.cpp:27-38) through wgp_init_weights: cold -> zeros(n1+n2);
+    warm -> [u1; 0]."""
     if n1 < 0 or n2 < 0:
         raise ValueError("init_weights: negative block size")
+    if init.warm_start and init.u1.size != n1:
+        raise ValueError("init_weights: warm-start vector length does not match n1")
     v = np.zeros(n1 + n2)
-    if init.warm_start:
-        if init.u1.size != n1:
-            raise ValueError("init_weights: warm-start vector length does not match n1")
-        v[:n1] = init.u1
+    u1 = np.ascontiguousarray(init.u1, dtype=np.float64) if init.warm_start else None
+    _check(lib().wgp_init_weights(_ptr(u1), n1, n2, _ptr(v)))
     return v
+
+
+def relative_residual(op: "KernelOperator", v, b) -> float | np.ndarray:
+    """relative_residual (solvers.cpp:62-66): |H v - b| / |b| per column (zero b -> ValueError)."""
+    V, B = _f64(v), _f64(b)
+    one = V.ndim == 1
+    V = V.reshape(op.n, -1, order="F")
+    B = B.reshape(op.n, -1, order="F")
+    out = np.zeros(V.shape[1])
+    _check(lib().wgp_relative_residual(op._h, _ptr(V), op.n, _ptr(B), op.n, V.shape[1], _ptr(out)))
+    return float(out[0]) if one else out
+
+
+def quadratic_objective(op: "KernelOperator", v, b) -> float | np.ndarray:
+    """quadratic_objective (solvers.cpp:68-70): 0.5 v.Hv - v.b per column."""
+    V, B = _f64(v), _f64(b)
+    one = V.ndim == 1
+    V = V.reshape(op.n, -1, order="F")
+    B = B.reshape(op.n, -1, order="F")
+    out = np.zeros(V.shape[1])
+    _check(lib().wgp_quadratic_objective(op._h, _ptr(V), op.n, _ptr(B), op.n, V.shape[1], _ptr(out)))
+    return float(out[0]) if one else out
+
+
+def cross_kernel(op: "KernelOperator", Xs) -> np.ndarray:
+    """cross_kernel (kernel.cpp:74-89): dense K(X*, X_op), m x n fp64, no noise term."""
+    Xs = _f64(Xs)
+    m = Xs.shape[0]
+    K = np.zeros((m, op.n), order="F")
+    _check(lib().wgp_cross_kernel(op._h, _ptr(Xs), m, max(m, 1), _ptr(K), max(m, 1)))
+    return K
+
+
+class CgPreconditioner:
+    """CgPreconditioner (solvers.hpp:82-100) as a device handle: built once, shared by many
+    cg_solve_with calls (bo_round, thompson.cpp:359-384)."""
+
+    def __init__(self, op: "KernelOperator", handle):
+        self.op = op
+        self._h = handle
+
+    @staticmethod
+    def from_matrix(op: "KernelOperator", rank: int, shift: float, mode: int = SHIFT_CALIBRATED):
+        h = C.c_void_p()
+        _check(lib().wgp_precond_create(op._h, int(rank), float(shift), int(mode), C.byref(h)))
+        return CgPreconditioner(op, h)
+
+    @staticmethod
+    def from_factor(op: "KernelOperator", L, shift: float):
+        L = _f64(L).reshape(op.n, -1, order="F")
+        h = C.c_void_p()
+        _check(lib().wgp_precond_create_from_factor(op._h, _ptr(L), max(op.n, 1), L.shape[1],
+                                                    float(shift), C.byref(h)))
+        return CgPreconditioner(op, h)
+
+    def info(self):
+        k, sh = C.c_int64(), C.c_double()
+        _check(lib().wgp_precond_get(self._h, C.byref(k), C.byref(sh)))
+        return k.value, sh.value
+
+    def is_identity(self) -> bool:
+        return self.info()[0] == 0
+
+    def apply(self, r) -> np.ndarray:
+        R = _f64(r)
+        one = R.ndim == 1
+        R = R.reshape(self.op.n, -1, order="F")
+        Z = np.zeros_like(R, order="F")
+        _check(lib().wgp_precond_apply(self._h, _ptr(R), self.op.n, R.shape[1], _ptr(Z), self.op.n))
+        return Z[:, 0] if one else Z
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().wgp_precond_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
 
 
 def solve_many(op: KernelOperator, rhs, inits: list, cfg: SolverConfig, return_status: bool = False):
     """solve_many (solvers.cpp:321-354) on the device: all columns in one batched solve.
 
     Raises at the lowest failing column like the reference.  With
-    ``return_status=True`` no exception is raised; returns (results, status, diverged_at)
-    so callers can implement solve_best_effort (thompson.cpp:299-317)."""
+    ``return_status=True`` a DivergenceError is not raised; returns (results, status,
+    diverged_at) so callers can implement solve_best_effort (thompson.cpp:299-317).  Every
+    other error (NotSpdError, invalid arguments) still raises."""
     B = _f64(rhs)
     if B.ndim == 1:
         B = B.reshape(-1, 1, order="F")
@@ -451,7 +608,10 @@ def solve_many(op: KernelOperator, rhs, inits: list, cfg: SolverConfig, return_s
     results = [SolveResult(V[:, c], int(its[c]), hist[c, : hl[c]].tolist(), bool(cv[c]))
                for c in range(s)]
     if return_status:
-        if st not in (OK, NOT_SPD, DIVERGED):
+        # only DivergenceError is a per-column outcome (solve_best_effort catches nothing
+        # else, thompson.cpp:299-317); NOT_SPD aborts the whole solve before any output is
+        # written, so it raises like every other error
+        if st not in (OK, DIVERGED):
             _check(st)
         return results, cst, dv
     if st != OK:
@@ -475,6 +635,38 @@ def solve(op: KernelOperator, b, init: Initialization, cfg: SolverConfig) -> Sol
                          C.byref(hl), C.byref(cv), C.byref(dv))
     _check(st, dv.value)
     return SolveResult(v, its.value, hist[: hl.value].tolist(), bool(cv.value))
+
+
+def cg_solve_many_with(op: KernelOperator, rhs, inits: list, cfg: SolverConfig,
+                       precond: CgPreconditioner) -> list:
+    """cg_solve_with (solvers.cpp:142-183) for several columns with one external preconditioner."""
+    B = _f64(rhs)
+    if B.ndim == 1:
+        B = B.reshape(-1, 1, order="F")
+    n, s = B.shape
+    if len(inits) != s or n != op.n:
+        raise ValueError("cg_solve_with: one initialization per column, rows == operator size")
+    n1 = 0
+    U1 = None
+    if any(i.warm_start for i in inits):
+        n1 = {i.u1.size for i in inits if i.warm_start}.pop()
+        U1 = np.zeros((n1, s), order="F")
+        for c, i in enumerate(inits):
+            if i.warm_start:
+                U1[:, c] = i.u1
+    V = np.empty((n, s), order="F")
+    hs = cfg.max_iters + 1
+    hist = np.zeros((s, hs))
+    its, hl, cv = (np.zeros(s, dtype=np.int32) for _ in range(3))
+    _check(lib().wgp_cg_solve_with(op._h, precond._h, C.byref(cfg), _ptr(B), n, s, _ptr(U1), max(n1, 1), n1,
+                                   _ptr(V), n, _ptr(its), _ptr(hist), hs, _ptr(hl), _ptr(cv)))
+    return [SolveResult(V[:, c], int(its[c]), hist[c, : hl[c]].tolist(), bool(cv[c])) for c in range(s)]
+
+
+def cg_solve_with(op: KernelOperator, b, init: Initialization, cfg: SolverConfig,
+                  precond: CgPreconditioner) -> SolveResult:
+    """cg_solve_with (solvers.hpp:118-119): CG reusing an externally built preconditioner."""
+    return cg_solve_many_with(op, np.asarray(b, dtype=np.float64).reshape(-1, 1), [init], cfg, precond)[0]
 
 
 def cg_solve(op, b, init, cfg) -> SolveResult:
@@ -612,11 +804,15 @@ def rff_eval(op: KernelOperator, priors: list, Xs=None, fast: bool = False) -> n
 
 
 def build_sample_rhs(op: KernelOperator, prior: RffPrior, noise_scale: float, seed: int) -> np.ndarray:
-    """build_sample_rhs (sampling.cpp:56-64): prior at the operator's rows + host-drawn noise."""
-    rhs = rff_eval(op, [prior])[:, 0].copy()
-    if noise_scale > 0.0:
-        rhs += normal_fill(seed, rhs.size, noise_scale)
-    return rhs
+    """build_sample_rhs (sampling.cpp:56-64) through wgp_build_sample_rhs: the prior at the
+    operator's rows + noise_scale Rng(seed).normal() per row."""
+    Om = np.asfortranarray(prior.frequencies, dtype=np.float64)
+    ph = np.ascontiguousarray(prior.phases, dtype=np.float64)
+    am = np.ascontiguousarray(prior.amplitudes, dtype=np.float64)
+    out = np.zeros(op.n)
+    _check(lib().wgp_build_sample_rhs(op._h, _ptr(Om), _ptr(ph), _ptr(am), Om.shape[0],
+                                      float(prior.signal_scale), float(noise_scale), seed & _M64, _ptr(out)))
+    return out
 
 
 def kernel_timer_enable(on: bool = True) -> None:
@@ -624,11 +820,13 @@ def kernel_timer_enable(on: bool = True) -> None:
     lib().wgp_kernel_timer_enable(1 if on else 0)
 
 
-def kernel_timer_read() -> tuple[float, int]:
-    """(summed kernel milliseconds, launches) since the last kernel_timer_enable(True)."""
+def kernel_timer_read(tag: str = "kmatvec_tc") -> tuple[float, int]:
+    """(summed kernel milliseconds, launches) of one kernel family ("kmatvec_tc",
+    "kmatvec_f64", "kmatvec_f32", "krows", "kcols", "rff_eval", "rff_eval32") since the
+    last kernel_timer_enable(True)."""
     ms = C.c_double(0.0)
     n = C.c_int64(0)
-    _check(lib().wgp_kernel_timer_read(C.byref(ms), C.byref(n)))
+    _check(lib().wgp_kernel_timer_read_tag(tag.encode(), C.byref(ms), C.byref(n)))
     return ms.value, n.value
 
 

@@ -26,7 +26,7 @@ def test_header_symbols_all_exported(W):
 
 
 def test_abi_version_and_defaults(W):
-    assert W.lib().wgp_abi_version() == 1
+    assert W.lib().wgp_abi_version() == 2
     c = W.SolverConfig()  # solvers.hpp:27-48
     assert (c.method, c.tolerance, c.max_iters, c.learning_rate, c.momentum) == (W.CG, 1e-2, 1000, 0.3, 0.9)
     assert (c.batch_size, c.block_size, c.precond_rank, c.precond_shift, c.seed) == (100, 100, 100, 1e-6, 0)
@@ -40,10 +40,12 @@ def test_shard_range_partition(W, n, world):
     assert ranges[0][0] == 0 and ranges[-1][1] == n
     for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
         assert a1 == b0
-    for a, b in ranges:
-        assert a <= b and a % 512 == 0  # chunk-aligned: reductions independent of world size
-    sizes = [b - a for a, b in ranges]
-    assert max(sizes) - min(sizes) <= 512 + (n % 512)
+    slot = -(-(-(-n // 512)) // world) * 512 if n else 512  # equal slots of whole chunks
+    slot = max(slot, 512)
+    for r, (a, b) in enumerate(ranges):
+        assert a <= b and (a % 512 == 0 or a == n)  # chunk-aligned: sums independent of world
+        assert a == min(r * slot, n) and b - a <= slot  # rank r's slot of the padded buffer
+    assert W.shard_padded_rows(n, world) == world * slot >= n
 
 
 def test_sample_prior_matches_oracle(W, O):

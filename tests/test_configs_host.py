@@ -25,3 +25,28 @@ def test_bump_objective_deterministic():
     assert np.array_equal(a.value(X), b.value(X))
     assert a.centers.shape == (20, 3) and (a.widths >= 0.05).all() and (a.amps >= 0.5).all()
     assert np.array_equal(a.observe(X), b.observe(X))
+
+
+def test_solve_many_return_status_raises_not_spd(W, monkeypatch):
+    """with return_status=True only DIVERGED is a per-column outcome; a NOT_SPD
+    solve wrote no outputs and must raise (solve_best_effort catches DivergenceError only,
+    thompson.cpp:299-317).  The library call is stubbed: no GPU needed."""
+    import pytest
+
+    class FakeLib:
+        def wgp_solve_many(self, *a):
+            return W.NOT_SPD
+
+        def wgp_last_error(self):
+            return b"cg_solve: non-positive curvature encountered"
+
+    class FakeOp:
+        n = 4
+        _h = None
+
+    cfg = W.SolverConfig.__new__(W.SolverConfig)  # a ctypes struct: no library call
+    cfg.max_iters = 10
+    monkeypatch.setattr(W, "lib", lambda: FakeLib())
+    B = np.ones((4, 2), order="F")
+    with pytest.raises(W.NotSpdError):
+        W.solve_many(FakeOp(), B, [W.Initialization.cold()] * 2, cfg, return_status=True)

@@ -17,9 +17,11 @@ CHUNK = 512
 
 
 def shard_range(n, world, rank):
+    """Equal slots of ceil(nch / world) chunks (wgp_shard_range; the exchange is one
+    in-place all-gather of equal slices of a buffer padded to world slots)."""
     nch = (n + CHUNK - 1) // CHUNK
-    c0, c1 = nch * rank // world, nch * (rank + 1) // world
-    return min(c0 * CHUNK, n), min(c1 * CHUNK, n)
+    c = max(1, -(-nch // world))
+    return min(rank * c * CHUNK, n), min((rank + 1) * c * CHUNK, n)
 
 
 def chunk_dots(a, b, row0):

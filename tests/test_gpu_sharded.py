@@ -1,0 +1,113 @@
+"""Row-sharded solvers through libwarmgp_b200.so at world 2, 3 and 4 on ONE GPU: the ranks are
+threads of this process (wgp_loopback_group_create / wgp_ctx_create_loopback), each with its
+own context, operator and stream; the collectives are host barriers plus device-to-device
+copies, so no kernel ever waits on another rank.  Everything else -- the equal-slot
+partition, the padded full-row buffers, the chunk-partial exchanges, the sharded pivoted
+Cholesky (per-pivot all-gather + broadcast), CG/SGD/AP's local updates -- is the code an
+NCCL world runs.
+
+The fp64 path is bit-identical to world 1 for every world size (fixed 512-row reduction
+chunks summed in chunk order; fixed 4096-column matvec splits).  The tensor-core path's
+column splits follow each rank's row count, so it is compared within tolerance."""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def run_world(W, world, fn):
+    """fn(ctx, rank) in `world` threads on device 0; returns the per-rank results."""
+    grp = W.LoopbackGroup(world)
+    out, err = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            ctx = W.DeviceContext(0, r, loopback=grp)
+            out[r] = fn(ctx, r)
+            ctx.close()
+        except Exception as e:  # noqa: BLE001
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in ts), "a rank hung"
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+def problem(n, d, s, seed=3):
+    rng = np.random.default_rng(seed)
+    X = rng.random((n, d))
+    B = np.asfortranarray(rng.standard_normal((n, s)))
+    U1 = rng.standard_normal((n - 200, s)) * 0.1
+    return X, B, U1
+
+
+def solve(W, ctx, hyp, X, B, inits, cfg, prec):
+    op = W.KernelOperator(hyp, X, precision=prec, ctx=ctx)
+    res = W.solve_many(op, B, inits, cfg)
+    return np.column_stack([r.v for r in res]), [r.iterations for r in res], [r.residual_history for r in res]
+
+
+CASES = [
+    ("cg", dict(method=0, tolerance=1e-8, max_iters=300, precond_rank=40, precond_shift=0.01)),
+    ("sgd", dict(method=1, tolerance=1e-3, max_iters=60, batch_size=256, learning_rate=0.3, seed=11)),
+    ("ap", dict(method=2, tolerance=1e-6, max_iters=80, block_size=300)),
+]
+
+
+@pytest.mark.parametrize("world,n", [(2, 3000), (3, 3000), (4, 1100)])
+@pytest.mark.parametrize("name,kw", CASES, ids=[c[0] for c in CASES])
+def test_sharded_f64_bitwise_equals_single(W, world, n, name, kw):
+    """(4, 1100): 3 chunks over 4 ranks -- rank 3 owns no rows."""
+    hyp = W.KernelHyperparams(0.6, 1.0, 0.3, W.MATERN32)
+    X, B, U1 = problem(n, 5, 3)
+    inits = [W.Initialization.warm(U1[:, c]) for c in range(3)]
+    cfg = W.SolverConfig(**kw)
+    ref = solve(W, W.default_context(), hyp, X, B, inits, cfg, W.F64)
+    got = run_world(W, world, lambda ctx, r: solve(W, ctx, hyp, X, B, inits, cfg, W.F64))
+    for r in range(world):
+        V, its, hist = got[r]
+        assert its == ref[1], (r, its, ref[1])
+        assert np.array_equal(V, ref[0]), (r, np.abs(V - ref[0]).max())
+        for h, hr in zip(hist, ref[2]):
+            assert h == hr
+
+
+def test_sharded_tensor_core_cg_close(W):
+    hyp = W.KernelHyperparams(1.0, 1.0, 0.5, W.MATERN32)
+    X, B, U1 = problem(6000, 8, 4, seed=5)
+    inits = [W.Initialization.cold()] * 4
+    cfg = W.SolverConfig(tolerance=1e-6, max_iters=300, precond_rank=50, precond_shift=0.25)
+    ref = solve(W, W.default_context(), hyp, X, B, inits, cfg, W.F32_3XTF32)
+    got = run_world(W, 2, lambda ctx, r: solve(W, ctx, hyp, X, B, inits, cfg, W.F32_3XTF32))
+    for V, its, _ in got:
+        assert all(abs(a - b) <= 1 for a, b in zip(its, ref[1])), (its, ref[1])
+        assert np.linalg.norm(V - ref[0]) <= 1e-5 * np.linalg.norm(ref[0])
+
+
+def test_loopback_allgather_rows(W):
+    import torch
+    n, s, world = 2100, 3, 3
+    pad = W.shard_padded_rows(n, world)
+
+    def fn(ctx, r):
+        a, b = W.shard_range(n, world, r)
+        buf = torch.full((pad, s), -1.0, dtype=torch.float64, device="cuda")
+        buf[a:b] = torch.arange(a, b, dtype=torch.float64, device="cuda")[:, None] * 10 + torch.arange(s, device="cuda")
+        torch.cuda.synchronize()
+        ctx.allgather_rows_dev(buf.data_ptr(), n, s, 0)
+        torch.cuda.synchronize()
+        return buf[:n].cpu().numpy()
+
+    got = run_world(W, world, fn)
+    want = np.arange(n)[:, None] * 10.0 + np.arange(s)
+    for g in got:
+        assert np.array_equal(g, want)

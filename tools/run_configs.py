@@ -58,8 +58,12 @@ def run_c1(quick=False) -> dict:
 
 def run_c2(quick=False) -> dict:
     steps = range(0, 21, 10) if quick else range(21)
-    out = {"config": "c2", "precision": "f64", "note": "fp32 paths stall above tol 1e-4 on this "
-           "kappa~1e5 system (see DESIGN.md); runs in fp64", "solvers": {}}
+    out = {"config": "c2", "precision": "f32 (3xF16 tensor-core operator)",
+           "note": "BASELINE configs[1] runs fp32: CG with the fp64-anchored true residual (the "
+                   "direct fp32 residual floors near 3e-4 above tol 1e-4 on this kappa~1e5 system, "
+                   "DESIGN.md §6); AP and SGD on the fp32 operator (their 2000-iteration residuals, "
+                   "~1e-2, are far above that floor); the fp64 CG sweep alongside for reference",
+           "solvers": {}}
     # SGD learning rate: grid_search_sgd_lr on the N=10k probe system (acceptance grid)
     hyp = W.KernelHyperparams(0.5, 1.0, 0.1, W.RBF)
     Xp = Cfg.uniform_rows_fast(W.derive_seed(0, 1), 10_000, 8)
@@ -73,16 +77,18 @@ def run_c2(quick=False) -> dict:
     out["sgd_lr"] = lr
     out["sgd_grid_seconds"] = time.perf_counter() - t0
     del probe
-    for name, method in (("cg", W.CG), ("ap", W.AP), ("sgd", W.SGD)):
+    runs = (("cg", W.CG, W.F32_3XTF32, W.RESIDUAL_ANCHORED), ("ap", W.AP, W.F32_3XTF32, W.RESIDUAL_DIRECT),
+            ("sgd", W.SGD, W.F32_3XTF32, W.RESIDUAL_DIRECT), ("cg_f64", W.CG, W.F64, W.RESIDUAL_DIRECT))
+    for name, method, prec, resid in runs:
         t0 = time.perf_counter()
-        res = Cfg.growth_sweep(method=method, steps=steps, lr=lr, precision=W.F64)
+        res = Cfg.growth_sweep(method=method, steps=steps, lr=lr, precision=prec, residual=resid)
         res["wall_seconds"] = time.perf_counter() - t0
         out["solvers"][name] = res
         _summ(name, res)
-    # the spec's fp32 arithmetic, for the record: 3xTF32 CG on the same sweep (subset of steps)
-    res = Cfg.growth_sweep(method=W.CG, steps=(0, 10, 20), precision=W.F32_3XTF32)
-    out["solvers"]["cg_f32_3xtf32"] = res
-    _summ("cg_f32_3xtf32", res)
+    # the direct fp32 residual, for the record (stalls at its floor; subset of steps)
+    res = Cfg.growth_sweep(method=W.CG, steps=(0, 20), precision=W.F32_3XTF32, max_iters=1000)
+    out["solvers"]["cg_f32_direct"] = res
+    _summ("cg_f32_direct", res)
     return out
 
 
