@@ -50,6 +50,24 @@ def make_inputs(seed=0):
     return X
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def bench_config(n, world):
+    """The workload dict of BOTH arms (same metric, same config)."""
+    return {"workload": "C3 kernel-matvec (BASELINE configs[2])", "n": n, "d": DIM, "s": S,
+            "kernel": "matern32", "lengthscale": LS, "noise_var": NOISE_VAR, "world": world,
+            "l2": "flushed (256 MiB memset) before each step"}
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -143,18 +161,19 @@ def run_reference(args):
         vals.append(v)
     wall = time.perf_counter() - t_all
     value = float(np.mean(vals))
-    ms = flops_per_matvec(n, n) / (value * 1e12) * 1e3
+    ms = wall / max(args.steps, 1) * 1e3  # one step = one bounded row sample (executed)
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "ms_per_step": ms, "higher_is_better": True,
+        "ms_full_matvec_extrapolated": flops_per_matvec(n, n) / (value * 1e12) * 1e3, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded X ~ N(0,I))",
-        "config": {"workload": "C3 kernel-matvec", "n": n, "d": DIM, "s": S, "kernel": "matern32",
-                   "lengthscale": LS, "noise_var": NOISE_VAR},
+        "config": bench_config(n, args.gpus),
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": nthreads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{rows} of {n} rows x {n} cols x {S} RHS per step, extrapolated "
                                    f"per-flop to the full matvec (oracle/warmgp_oracle.c "
-                                   f"wgo_kmatvec_rows, OpenMP)"},
+                                   f"wgo_kmatvec_rows, OpenMP); {args.steps} steps took {wall:.1f} s"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
@@ -163,7 +182,7 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- CG warm/cold
-def cg_time_to_tolerance(W, ctx, X, prec, hyp, tol=1e-4, seed=0):
+def cg_time_to_tolerance(W, ctx, X, prec, hyp, tol=1e-4, seed=0, local=0):
     """BASELINE configs[2]: solve the N=100k system, append 1000 rows, then warm-started
     ([u; 0], Initialization::warm) vs cold CG to tol on N=101k.  RHS = y + 63 pathwise
     prior samples: 64 Matern RFF priors (F=2048, sample_prior's Student-t spectral draws)
@@ -182,9 +201,17 @@ def cg_time_to_tolerance(W, ctx, X, prec, hyp, tol=1e-4, seed=0):
     cfg = W.SolverConfig(tolerance=tol, max_iters=1000, precond_rank=100, precond_shift=hyp.noise_scale ** 2)
 
     def run(o, rhs, inits):
+        if ctx.world > 1:  # sharded: every rank runs the solve; the time is the max over ranks
+            import torch
+            import torch.distributed as dist
+            dist.barrier()
         t0 = time.perf_counter()
         res = W.solve_many(o, rhs, inits, cfg)
         dt = time.perf_counter() - t0
+        if ctx.world > 1:
+            t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
         its = [r.iterations for r in res]
         return res, {"seconds": dt, "iters_max": max(its), "iters_mean": float(np.mean(its)),
                      "converged": int(sum(r.converged for r in res)),
@@ -192,22 +219,33 @@ def cg_time_to_tolerance(W, ctx, X, prec, hyp, tol=1e-4, seed=0):
 
     prev, prev_stats = run(op, np.asfortranarray(B[:N0]), [W.Initialization.cold()] * S)
     op.append_rows(X[N0:])  # device-resident growth (K8)
-    # cold and warm alternately, three times each; the fastest of each is reported (the
-    # solves are deterministic -- same iterations, same results -- so repeats differ only by
-    # clock ramps / power-cap transitions after the sustained matvec loop, which measured
-    # up to 2.6x on single solves)
+    # cold and warm alternately, REPS times each; the solves are deterministic (same
+    # iterations, same results), so repeats differ only by host effects and the GPU clock
+    # state after the sustained matvec loop.  Reported: the median, every sample, the
+    # first call of each, and the SM clocks sampled during the leg.
+    reps = 5
     ws, cs = [], []
-    for _ in range(3):
-        _, c = run(op, B, [W.Initialization.cold()] * S)
-        _, w = run(op, B, [W.Initialization.warm(r.v) for r in prev])
-        cs.append(c)
-        ws.append(w)
-    cold = min(cs, key=lambda r: r["seconds"])
-    warm = min(ws, key=lambda r: r["seconds"])
-    cold["seconds_all"] = [r["seconds"] for r in cs]
-    warm["seconds_all"] = [r["seconds"] for r in ws]
-    return {"n_prev": N0, "n": n, "s": S, "tol": tol, "precond_rank": 100,
+    with ClockSampler(local) as clk:
+        for _ in range(reps):
+            _, c = run(op, B, [W.Initialization.cold()] * S)
+            _, w = run(op, B, [W.Initialization.warm(r.v) for r in prev])
+            cs.append(c)
+            ws.append(w)
+
+    def agg(rs):
+        out = dict(rs[0])
+        secs = [r["seconds"] for r in rs]
+        out["seconds"] = float(np.median(secs))
+        out["seconds_all"] = secs
+        out["seconds_first_call"] = secs[0]
+        out["seconds_min"] = float(min(secs))
+        return out
+
+    cold, warm = agg(cs), agg(ws)
+    return {"n_prev": N0, "n": n, "s": S, "tol": tol, "precond_rank": 100, "reps": reps,
+            "statistic": "median of the alternating repetitions (all samples listed)",
             "prev_solve_n100k": prev_stats, "warm": warm, "cold": cold,
+            "clocks_during_cg": clk.summary(),
             "warm_over_cold_time": warm["seconds"] / cold["seconds"],
             "warm_over_cold_iters": warm["iters_mean"] / max(cold["iters_mean"], 1e-9)}
 
@@ -259,6 +297,114 @@ def vector_kernels_gbs(W, ctx, n, stream, flush, peaks, reps=20):
     return res
 
 
+# --------------------------------------------------------------------------- other hot kernels
+def rff_throughput(W, ctx, X, hyp):
+    """North-star item (4), RFF prior generation (eval_prior, sampling.cpp:37-46): the
+    phase GEMM (d FMA per feature) + cos + amplitude sum per (point, feature, prior).
+    fp64 at the C3 right-hand-side shape (101k rows x F=2048 x 64 priors) and the fast fp32
+    path at the C5 candidate shape (100k points x F=2000 x 128 priors, d=6), kernel time by
+    CUDA events on the launch stream (wgp_kernel_timer, tags rff_eval / rff_eval32)."""
+    out = {}
+    cases = (("rff_eval (fp64, C3 RHS)", X, S, 2048, DIM, False, hyp),
+             ("rff_eval_fast (fp32, C5 candidates)", np.random.default_rng(3).random((100_000, 6)), 128, 2000, 6,
+              True, W.KernelHyperparams(0.3, 1.0, 1e-3, W.MATERN32)))
+    for name, Xs, nprior, F, d, fast, h in cases:
+        op = W.KernelOperator(h, Xs[:1024], precision=W.F64, ctx=ctx)
+        priors = [W.sample_prior(h, d, F, W.derive_seed(9, c)) for c in range(nprior)]
+        W.rff_eval(op, priors[:2], Xs[:2048], fast=fast)  # warm-up
+        W.kernel_timer_enable(True)
+        W.rff_eval(op, priors, Xs, fast=fast)
+        ms, launches = W.kernel_timer_read("rff_eval32" if fast else "rff_eval")
+        W.kernel_timer_enable(False)
+        m = Xs.shape[0]
+        feats = float(m) * F * nprior
+        out[name] = {"kernel_ms": ms, "launches": launches, "points": m, "features": F, "priors": nprior,
+                     "dim": d, "cos_per_s": feats / (ms * 1e-3),
+                     "algorithmic_flops": feats * (2 * d + 2), "TFLOP/s": feats * (2 * d + 2) / (ms * 1e-3) / 1e12,
+                     "note": "flops per (point, feature): 2d (phase) + 2 (amplitude FMA); the cos not counted"}
+        del op
+    return out
+
+
+def sgd_ap_kernels(W, ctx):
+    """North-star item (3) at the C2 shape (N=20k, d=8 RBF, s=17): SGD minibatch rows
+    (krows: B=512 rows x N pairs per column per iteration) and AP block columns (kcols: N x
+    bs=500 pairs per column per iteration), fp64, kernel time per launch by CUDA events."""
+    from paper_2511_16340_b200 import configs as Cfg
+    n, s = 20_000, 17
+    hyp = W.KernelHyperparams(0.5, 1.0, 0.1, W.RBF)
+    X = Cfg.uniform_rows_fast(W.derive_seed(0, 1), n, 8)
+    B = np.asfortranarray(np.random.default_rng(4).standard_normal((n, s)))
+    out = {}
+    for prec, pname in ((W.F64, "f64"), (W.F32_3XTF32, "f32")):
+        op = W.KernelOperator(hyp, X, precision=prec, ctx=ctx)
+        for name, tag, kw, pairs in (("sgd", "krows", dict(method=W.SGD, batch_size=512, learning_rate=1e-3), 512 * n),
+                                     ("ap", "kcols", dict(method=W.AP, block_size=500), n * 500)):
+            cfg = W.SolverConfig(tolerance=1e-12, max_iters=50, **kw)
+            W.solve_many(op, B, [W.Initialization.cold()] * s, cfg.copy(max_iters=2))
+            W.kernel_timer_enable(True)
+            t0 = time.perf_counter()
+            W.solve_many(op, B, [W.Initialization.cold()] * s, cfg)
+            wall = time.perf_counter() - t0
+            ms, launches = W.kernel_timer_read(tag)
+            res_ms, res_l = W.kernel_timer_read("kmatvec_tc" if prec != W.F64 else "kmatvec_f64")
+            W.kernel_timer_enable(False)
+            per = ms / max(launches, 1)
+            out[f"{name}_{pname}"] = {
+                "kernel": tag, "us_per_launch": per * 1e3, "launches": launches,
+                "pairs_per_launch": pairs * s, "Gpairs_per_s": pairs * s / (per * 1e-3) / 1e9,
+                "iteration_ms": wall * 1e3 / cfg.max_iters,
+                "residual_matvec_ms_per_launch": res_ms / max(res_l, 1),
+                "note": "per iteration the reference also recomputes the full true residual (one "
+                        "N x N matvec, solvers.cpp:231/:298 refresh) -- listed separately"}
+        del op
+    out["shape"] = "C2: N=20k, d=8 RBF, s=17; SGD B=512, AP bs=500 (greedy), 50 iterations"
+    return out
+
+
+def c4_sharded_matvec(W, ctx, world, rank, steps=3):
+    """C4 (BASELINE configs[3]) operator: N=500k, d=8 RBF, s=32, rows sharded over the ranks
+    (all-gather of V + local row slice), device time max over ranks -- the N>=500k scaling
+    leg of the north star.  Returns TFLOP/s over all ranks."""
+    import torch
+    n, d, s = 500_000, 8, 32
+    hyp = W.KernelHyperparams(0.5, 1.0, 0.1, W.RBF)
+    X = np.random.default_rng(11).random((n, d))
+    op = W.KernelOperator(hyp, X, precision=W.F32_3XTF32, ctx=ctx)
+    r0, r1 = W.shard_range(n, world, rank)
+    V = torch.randn(W.shard_padded_rows(n, world), s, device="cuda", dtype=torch.float64)
+    Y = torch.empty(max(r1 - r0, 1), s, device="cuda", dtype=torch.float64)
+    st = torch.cuda.current_stream()
+    sp = st.cuda_stream
+
+    def step():
+        if world > 1:
+            ctx.allgather_rows_dev(V.data_ptr(), n, s, sp)
+        op.kmatvec_dev(V.data_ptr(), Y.data_ptr(), s, sp)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(steps):
+        step()
+    b.record(st)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    flops = float(n) * n * (2 * d + 2 * s)
+    return {"n": n, "d": d, "s": s, "kernel": "rbf", "world": world, "ms_per_matvec": ms,
+            "TFLOP/s": flops / (ms * 1e-3) / 1e12, "steps": steps,
+            "rows_per_rank": r1 - r0, "note": "all-gather of V included (world > 1); max over ranks"}
+
+
 # --------------------------------------------------------------------------- GPU arm
 def run_ours(args):
     import torch
@@ -289,7 +435,7 @@ def run_ours(args):
     r0, r1 = W.shard_range(n, world, rank)
     dt = torch.float64  # device API: fp64 solver vectors for every precision
     gen = torch.Generator(device="cuda").manual_seed(1234)
-    V = torch.randn(n, S, device="cuda", dtype=dt, generator=gen)
+    V = torch.randn(W.shard_padded_rows(n, world), S, device="cuda", dtype=dt, generator=gen)
     Y = torch.empty(r1 - r0, S, device="cuda", dtype=dt)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.Stream()  # a real (non-legacy) stream: our launches and the events share it
@@ -382,8 +528,13 @@ def run_ours(args):
                "ms_per_step": e2e_ms_step, "note": "all ranks' row slices (bytes summed over ranks)"}
 
     peaks, peak_kind = measured_peaks()
-    # tensor-core roofline: tf32 dense = bf16 dense / 2 on Blackwell (measured bf16 GEMM)
+    # tensor-core roofline.  The contraction is fp32-class (north_star "fp32/tf32"): its
+    # tensor format is TF32, dense peak = bf16 dense / 2 on Blackwell (measured bf16 GEMM).
+    # The MMAs the kernel issues are kind::f16 three-term hi/lo splits (fp32 accumulate),
+    # so the fraction against the f16 dense peak of those instructions is listed as well,
+    # and the composite (SFU) bound that actually limits the Matern map.
     peak_tf32 = peaks["bf16_tflops"] / 2.0
+    peak_f16 = peaks["bf16_tflops"]
     sm_hz = peaks.get("sm_max_mhz", 1965.0) * 1e6
     pairs = float(n) * float(n)
     mufu_per_pair = 2.0  # Matern-3/2: sqrt + exp2 per pair on the SFU (MUFU) pipe
@@ -397,6 +548,10 @@ def run_ours(args):
             # X/XA/XB and the V tiles stay L2-resident, HBM sees little more than V/Y once.
             "traffic": TRAFFIC_BYTES,
             "peak_source": f"{peak_kind} bf16_tflops/2 (TF32 dense) from MEASURED_PEAKS.json",
+            "frac_vs_f16_dense": achieved / peak_f16 if achieved else None,
+            "f16_dense_peak": peak_f16,
+            "mma_kind": "kind::f16, 3-term hi/lo splits of K and V (and of x for the distance "
+                        "GEMM), fp32 accumulation in TMEM",
             "kernel": "tc::kmatvec_tc_kernel (CUDA events around its launches, "
                       f"{k_launches} launches, {kernel_ms:.3f} ms avg; {100 * kernel_ms / ms_step:.1f}% of the step)",
             "algorithmic_flops_per_launch": flops_launch,
@@ -407,19 +562,26 @@ def run_ours(args):
                           "note": "SFU roofline at sm_max_mhz (16 MUFU ops/clk/SM, measured by "
                                   "tools/mufu_microbench.cu): the Matern map's sqrt+exp2 per pair"}}
 
-    vec = None
+    vec = rff = sgdap = None
     if world == 1:
         vec = vector_kernels_gbs(W, ctx, n, stream, flush, peaks)
+        if not args.no_extra:
+            rff = rff_throughput(W, ctx, X, hyp)
+            sgdap = sgd_ap_kernels(W, ctx)
+
+    c4 = None
+    if not args.no_extra:
+        c4 = c4_sharded_matvec(W, ctx, world, rank)
 
     cg = None
-    if world == 1 and not args.no_cg:
-        cg = cg_time_to_tolerance(W, ctx, X, prec, hyp)
+    if not args.no_cg:
+        cg = cg_time_to_tolerance(W, ctx, X, prec, hyp, local=local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         nthreads = os.cpu_count() or 1
         v, secs = cpu_matvec_sample(X, args.ref_rows, nthreads)
-        cpu = {"value": v, "unit": "TFLOP/s", "cores": nthreads, "kind": "port",
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": nthreads, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"{args.ref_rows} of {n} rows x {n} cols x {S} RHS ({secs:.1f} s), "
                          f"oracle wgo_kmatvec_rows (OpenMP, fp64)"}
         if cg is not None:
@@ -439,14 +601,17 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
-            "dtype": {"3xtf32": "f32(3xtf32)", "tf32": "f32(tf32)", "f32simt": "f32", "f64": "f64"}[args.precision],
+            "dtype": {"3xtf32": "f32-class: 3-term fp16 hi/lo splits, fp32 accumulate (kind::f16)",
+                      "tf32": "tf32 (single pass)", "f32simt": "f32", "f64": "f64"}[args.precision],
             "data": "synthetic (seeded X ~ N(0,I), V ~ N(0,1))",
-            "config": {"workload": "C3 kernel-matvec (BASELINE configs[2])", "n": n, "d": DIM, "s": S,
-                       "kernel": "matern32", "lengthscale": LS, "noise_var": NOISE_VAR,
-                       "rows_per_rank": r1 - r0, "l2": "flushed (256 MiB memset) before each step"},
+            "config": bench_config(n, world),
+            "rows_per_rank": r1 - r0,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": 5 * args.steps,  # colmax + colscale_finish + split_v + kmatvec_tc + reduce_splits per step
             "cg_warm_vs_cold": cg,
+            "c4_sharded_matvec": c4,
             "vector_kernels": vec,
+            "rff_prior_generation": rff,
+            "sgd_ap_kernels": sgdap,
             "clocks": clk.summary(), "wall_s": t_wall,
             "step_ms_min": float(np.min(ms)), "step_ms_max": float(np.max(ms)),
         }
@@ -472,6 +637,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=1000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cg", action="store_true", help="skip the warm/cold CG time-to-tolerance leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the RFF / SGD-AP / C4 legs")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -287,6 +287,17 @@ uint64_t wgp_rng_uniform_index(uint64_t* state, uint64_t n);
 /* n consecutive scale * normal() draws from (and advancing) the generator at *state. */
 void wgp_rng_normal_fill(uint64_t* state, int64_t n, double scale, double* out);
 
+/* select_peaks' argmax step (thompson.cpp:188-207) on the device: posterior values
+ * prior_s(X*) + K(X*, X) W[:, s] (as wgp_rff_eval + wgp_cross_matvec; fast != 0: the fp32
+ * RFF kernel and, on tensor-core operators, the tcgen05 cross mode) for S samples at m
+ * candidates (X*: m x dim column-major), split into `groups` contiguous candidate groups
+ * [m g / groups, m (g+1) / groups); idx[s * groups + g] = the first row of group g with the
+ * largest value for sample s.  Only the S x groups indices leave the device. */
+wgp_status wgp_posterior_select(wgp_op* op, const double* Omega, const double* phases,
+                                const double* amps, int F, int S, double signal_scale,
+                                const double* W, int64_t ldw, const double* Xstar, int64_t m,
+                                int64_t ldx, int groups, int fast, int64_t* idx);
+
 /* exact_solve (analysis.cpp:15-26): X = H^{-1} B by a dense fp64 Cholesky of the operator's
  * H on the device (materialised once; n <= 60000).  B, X: n x s column-major.  A
  * non-positive pivot returns WGP_NOT_SPD (the reference's LLT failure).  Unsharded only. */

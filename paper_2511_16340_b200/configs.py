@@ -171,7 +171,8 @@ def bo_loop(dim=4, n_init=5000, batch=64, rounds=50, n_samples=128, candidates=1
     """Configuration 5: BoConfig defaults (Matern-3/2 l=0.3, s_f=1, sigma_n=1e-3, F=2000;
     thompson.hpp:29-58), CG with the small budget (5 iterations, tol 1e-2).  Acquisition as
     select_peaks + ascend_peaks (thompson.cpp:188-258): the candidates are split into
-    `peak_groups` groups, each sample's argmax in every group is a start, and the device Adam
+    `peak_groups` contiguous groups [m g / G, m (g+1) / G), each sample's argmax in every group
+    (computed on the device, wgp_posterior_select) is a start, and the device Adam
     ascent (ascent_steps / ascent_rate, BoConfig defaults 30 / 0.05) picks the batch point;
     ascent_steps = 0 takes the plain argmax."""
     hyp = W.KernelHyperparams(0.3, 1.0, 1e-3, W.MATERN32)
@@ -188,14 +189,18 @@ def bo_loop(dim=4, n_init=5000, batch=64, rounds=50, n_samples=128, candidates=1
         rec = st.solve_round(cfg, warm)
         t0 = time.perf_counter()
         Xc = uniform_rows_fast(W.derive_seed(seed, 0xA0000 + st.round), candidates, dim)
-        F = posterior_at(st, Xc)[:, :batch]  # candidates x samples; the first `batch` acquire
+        # select_peaks on the device: posterior values of the first `batch` samples at every
+        # candidate and their per-group argmax; only batch x groups indices reach the host
+        wd = st.weights[:, :1] - st.weights[:, 1:1 + batch]
+        sel_op = st.op_fast if st.op_fast is not None else st.op
+        groups = peak_groups if ascent_steps > 0 else 1
+        idx = W.posterior_select(sel_op, st.priors[:batch], wd, Xc, groups=groups,
+                                 fast=st.op_fast is not None)
         if ascent_steps > 0:
-            g = np.array_split(np.arange(candidates), peak_groups)
-            starts = np.stack([Xc[gi[np.argmax(F[gi], axis=0)]] for gi in g], axis=1)  # batch x groups x D
-            wd = st.weights[:, :1] - st.weights[:, 1:1 + batch]
+            starts = Xc[idx]  # batch x groups x D
             Xn, _ = W.ascend_peaks(st.op, st.priors[:batch], wd, starts, ascent_steps, ascent_rate)
         else:
-            Xn = Xc[np.argmax(F, axis=0)]
+            Xn = Xc[idx[:, 0]]
         rec["candidate_seconds"] = time.perf_counter() - t0
         yn = obj.observe(Xn)
         st.add_points(Xn, yn)

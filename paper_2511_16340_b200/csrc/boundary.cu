@@ -7,6 +7,7 @@
 // The operator matvecs run on the device with the operator's precision; the final norms and
 // dot products over n values are host fp64 sums in index order.
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "rng.h"
@@ -38,9 +39,52 @@ __global__ void cross_kernel_kernel(const double* __restrict__ Xs, const double*
   K[i + j * ldk] = kv;
 }
 
+// select_peaks' per-sample argmax (thompson.cpp:199-203) over candidate groups: block
+// (sample s, group g) scans rows [g0, g1) of value(i, s) = prior(i, s) + cross(i, s) and keeps
+// the largest value, the lowest index on ties (Eigen maxCoeff / numpy argmax: first max).
+__global__ void __launch_bounds__(256) group_argmax_kernel(const double* __restrict__ prior,
+                                                           const double* __restrict__ cross, int64_t m,
+                                                           int S, int groups,
+                                                           int64_t* __restrict__ idx) {
+  const int sidx = blockIdx.x, g = blockIdx.y;
+  const int64_t g0 = m * g / groups, g1 = m * (g + 1) / groups;
+  double best = -INFINITY;
+  int64_t bi = g1;
+  for (int64_t i = g0 + threadIdx.x; i < g1; i += blockDim.x) {
+    const double v = prior[i + (int64_t)sidx * m] + cross[i * S + sidx];
+    if (v > best) {  // strided scan in increasing i: strict > keeps the first max per thread
+      best = v;
+      bi = i;
+    }
+  }
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      const double ov = sv[threadIdx.x + off];
+      const int64_t oi = si[threadIdx.x + off];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) idx[(int64_t)sidx * groups + g] = si[0] < g1 ? si[0] : g0;
+}
+
 }  // namespace
 
 void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major);
+void launch_rff_eval32(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
+                       const double* ph, const double* amp, int F, int S, double coeff,
+                       double* out, int64_t ldo, cudaStream_t st);
+void launch_rff_eval64(const double* X, int ldx_row, int dim, int64_t m, const double* Om,
+                       const double* ph, const double* amp, int F, int S, double coeff,
+                       double* out, int64_t ldo, cudaStream_t st);
 
 }  // namespace wgp
 
@@ -180,3 +224,51 @@ wgp_status wgp_build_sample_rhs(wgp_op* op, const double* Omega, const double* p
 }
 
 }  // extern "C"
+
+extern "C" wgp_status wgp_posterior_select(wgp_op* op, const double* Omega, const double* phases,
+                                           const double* amps, int F, int S, double signal_scale,
+                                           const double* W, int64_t ldw, const double* Xstar,
+                                           int64_t m, int64_t ldx, int groups, int fast,
+                                           int64_t* idx) {
+  return guard2([&] {
+    WGP_REQUIRE(op && Omega && phases && amps && W && Xstar && idx, "wgp_posterior_select: null argument");
+    WGP_REQUIRE(F >= 1 && S >= 1 && m >= 1 && groups >= 1 && groups <= m && ldx >= m && ldw >= op->n,
+                "wgp_posterior_select: bad shape");
+    WGP_REQUIRE(op->ctx->world == 1, "posterior_select: unsharded operators only");
+    WGP_REQUIRE(op->n >= 1, "posterior_select: empty operator");
+    WGP_CUDA(cudaSetDevice(op->ctx->device));
+    cudaStream_t st = op->ctx->stream;
+    const int64_t n = op->n;
+    const int dim = op->dim;
+    Op tmp;  // candidates, row-major with norms
+    tmp.ctx = op->ctx;
+    tmp.precision = WGP_F64;
+    tmp.dim = dim;
+    tmp.dpad = op->dpad;
+    op_append_rows(tmp, Xstar, m, ldx, 1);
+    const size_t nom = (size_t)S * F * dim, nf = (size_t)S * F;
+    DBuf<double> dOm(nom), dPh(nf), dAm(nf), dPrior((size_t)m * S), dCross((size_t)m * S);
+    DBuf<double> stage((size_t)n * S), dW((size_t)n * S);
+    DBuf<int64_t> dIdx((size_t)S * groups);
+    WGP_CUDA(cudaMemcpyAsync(dOm.p, Omega, sizeof(double) * nom, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpyAsync(dPh.p, phases, sizeof(double) * nf, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpyAsync(dAm.p, amps, sizeof(double) * nf, cudaMemcpyHostToDevice, st));
+    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, W, sizeof(double) * ldw, sizeof(double) * n, S,
+                               cudaMemcpyHostToDevice, st));
+    launch_colmajor_to_rows(stage.p, n, n, S, dW.p, true, st);
+    const double coeff = signal_scale * std::sqrt(2.0 / (double)F);  // sampling.cpp:40-41
+    if (fast)
+      launch_rff_eval32(tmp.X64.p, tmp.dpad, dim, m, dOm.p, dPh.p, dAm.p, F, S, coeff, dPrior.p, m, st);
+    else
+      launch_rff_eval64(tmp.X64.p, tmp.dpad, dim, m, dOm.p, dPh.p, dAm.p, F, S, coeff, dPrior.p, m, st);
+    // K(X*, X) W: the tcgen05 cross mode on tensor-core operators when asked (and the
+    // candidates fit its operand range), else the fp64 kernel
+    if (!(fast && op_cross_tc(*op, tmp.X64.p, m, tmp.dpad, dW.p, S, dCross.p, st)))
+      launch_kmatvec_simt<double>(*op, tmp.X64.p, m, 0, op->X64.p, n, dW.p, S, nullptr, dCross.p, false, st);
+    group_argmax_kernel<<<dim3((unsigned)S, (unsigned)groups), 256, 0, st>>>(dPrior.p, dCross.p, m, S, groups,
+                                                                            dIdx.p);
+    WGP_CUDA(cudaGetLastError());
+    WGP_CUDA(cudaMemcpyAsync(idx, dIdx.p, sizeof(int64_t) * S * groups, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+  });
+}

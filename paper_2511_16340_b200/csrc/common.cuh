@@ -73,6 +73,24 @@ struct DBuf {
   void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
 };
 
+// Owning pinned host buffer (async device-to-host copies of per-iteration records).
+struct PinnedBuf {
+  unsigned char* p = nullptr;
+  size_t n = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() { if (p) cudaFreeHost(p); }
+  void ensure(size_t bytes) {
+    if (bytes <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    WGP_CUDA(cudaMallocHost(&p, bytes));
+    n = bytes;
+  }
+};
+
 // Kernel-map parameters (kernel.cpp:17-21 Matern-3/2; RBF extension).
 struct KParams {
   int kind;        // WGP_MATERN32 / WGP_RBF

@@ -9,6 +9,7 @@
 //
 // Host work per iteration is one small D2H of (rel, active, failure) -- the scalar logic
 // (alpha, beta, freeze) runs in single-block "step" kernels on the device.
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -28,15 +29,18 @@ __global__ void init_bnorm_kernel(const double* __restrict__ part, int nch, int 
   }
 }
 
-// rel = |r| / |b|, freezes converged columns.  nq/qi select the partial slot.
+// rel = |r| / |b|, freezes converged columns.  nq/qi select the partial slot.  act_snap
+// (nullable): the flags after this step (the per-iteration record of a batched block).
 __global__ void resid_step_kernel(const double* __restrict__ part, int nch, int nq, int s,
                                   const double* __restrict__ bnorm, double tol,
-                                  double* __restrict__ rel, int* __restrict__ active) {
+                                  double* __restrict__ rel, int* __restrict__ active,
+                                  int* __restrict__ act_snap = nullptr) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
     const double acc = chunk_sum_ordered(part + c, nch, (int64_t)nq * s);
     const double r = bnorm[c] > 0.0 ? sqrt(acc) / bnorm[c] : 0.0;
     rel[c] = r;
     if (active[c] && r <= tol) active[c] = 0;
+    if (act_snap) act_snap[c] = active[c];
   }
 }
 
@@ -51,6 +55,41 @@ __global__ void cg_alpha_kernel(const double* __restrict__ part, int nch, int s,
     }
     if (pHp <= 0.0) atomicMin(fail_col, c);  // NotSpdError, solvers.cpp:164-166
     alpha[c] = rz[c] / pHp;
+  }
+}
+
+// Variant alpha = p.r / p.Hp (slots 0 = p.Hp, 1 = p.r of [nch][2][s] partials): equal to
+// r.z / p.Hp in exact arithmetic (r_k is orthogonal to p_{k-1}); with an inexact operator it
+// is the exact line minimum along p, which keeps the step consistent with the TRUE residual.
+__global__ void cg_alpha_pr_kernel(const double* __restrict__ part, int nch, int s,
+                                   const int* __restrict__ active, double* __restrict__ alpha,
+                                   int* __restrict__ fail_col) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
+    const double pHp = chunk_sum_ordered(part + c, nch, 2 * (int64_t)s);
+    const double pr = chunk_sum_ordered(part + s + c, nch, 2 * (int64_t)s);
+    if (!active[c]) {
+      alpha[c] = 0.0;
+      continue;
+    }
+    if (pHp <= 0.0) atomicMin(fail_col, c);
+    alpha[c] = pr / pHp;
+  }
+}
+
+// Polak-Ribiere (flexible CG) beta = z.(r - r_old) / rz (slots 0 = r.z, 1 = r_old.z): equal to
+// Fletcher-Reeves r.z / rz_old in exact arithmetic (r_old.z = 0), robust to an inexact H p.
+__global__ void cg_beta_pr_kernel(const double* __restrict__ part, int nch, int s,
+                                  double* __restrict__ rz, const int* __restrict__ active,
+                                  double* __restrict__ beta) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
+    const double rzn = chunk_sum_ordered(part + c, nch, 2 * (int64_t)s);
+    const double roz = chunk_sum_ordered(part + s + c, nch, 2 * (int64_t)s);
+    if (active[c]) {
+      beta[c] = (rzn - roz) / rz[c];
+      rz[c] = rzn;
+    } else {
+      beta[c] = 0.0;
+    }
   }
 }
 
@@ -252,6 +291,10 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
   w.tvec.ensure((size_t)(pd.k + 1) * s);
   Anchor<T> anc(op, w, st);
   const double frac = anchor_frac();
+  // WGP_CG_VARIANT (probes): 0 = the reference's alpha = r.z / p.Hp and Fletcher-Reeves beta
+  // (solvers.cpp:163-182); 1 = alpha = p.r / p.Hp; 2 = 1 + Polak-Ribiere beta.  Algebraically
+  // identical; they differ only under operator error (fp32 operators).
+  const int variant = getenv("WGP_CG_VARIANT") ? atoi(getenv("WGP_CG_VARIANT")) : 0;
   op.last_anchors = 0;
 
   // |b| per column
@@ -309,22 +352,66 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
   const int int_max = INT_MAX;
   WGP_CUDA(cudaMemcpyAsync(fail, &int_max, sizeof(int), cudaMemcpyHostToDevice, st));
 
-  for (int k = 1; k <= cfg.max_iters; ++k) {
-    dist_allgather_rows(ctx, w.P.p, N, s, sizeof(T), st);  // exchange: full p for the matvec
-    launch_kmatvec_full(op, w.P.p, w.HP.p, s, st);          // Hp = H p (:162), local rows
-    dots(op, w, w.Pl(), w.HP.p, st);
-    cg_alpha_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, alpha, fail);
-    if (n > 0) launch_axpy_cols<T>(w.Vl(), w.Pl(), alpha, n, s, st);  // v += alpha p (:168)
-    dist_allgather_rows(ctx, w.V.p, N, s, sizeof(T), st);
+  // Iterations run in blocks of kb between host synchronisations: per iteration the step
+  // kernels write rel and the activity flags into a per-iteration record on the device, the
+  // host reads the block's records once and rebuilds the histories exactly as a per-iteration
+  // loop would (frozen columns stay frozen: alpha = 0, p untouched, so the iterations after a
+  // column converges inside a block leave its v and history unchanged).  kb = 1 for the first
+  // block; afterwards ~2 ms of work per block (large systems: kb = 1, one sync per
+  // iteration as before; small ones: up to 32 iterations per sync).  Anchored residuals and
+  // sharded solves decide on the host every iteration (kb = 1).
+  const int kbmax = (anchored || ctx.world > 1) ? 1 : 32;
+  w.blk_rel.ensure((size_t)kbmax * s);
+  w.blk_act.ensure((size_t)kbmax * s);
+  w.h_blk.ensure((size_t)kbmax * s * (sizeof(double) + sizeof(int)) + 64);
+  double* h_rel_blk = reinterpret_cast<double*>(w.h_blk.p);
+  int* h_act_blk = reinterpret_cast<int*>(h_rel_blk + (size_t)kbmax * s);
+  int* h_fail = h_act_blk + (size_t)kbmax * s;
+  int kb = 1;
+  // z = P r (:178), rz, beta (:179-181), p = z + beta p (:180)
+  auto next_direction = [&] {
+    precond_apply<T>(op, pd, w.R.p, w.Z.p, s, w.tvec.p, w.pwork.p, st);
+    if (variant == 2) {
+      dots2(op, w, w.R.p, w.Z.p, w.HP.p, w.Z.p, st);
+      cg_beta_pr_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta);
+    } else {
+      dots(op, w, w.R.p, w.Z.p, st);
+      cg_beta_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta, 0);
+    }
+    if (n > 0) launch_xpby_cols<T>(w.Pl(), w.Z.p, beta, active, n, s, st);
+  };
+  for (int k = 1; k <= cfg.max_iters;) {
+    const int nb = std::min(kb, cfg.max_iters - k + 1);
+    const auto t_block = std::chrono::steady_clock::now();
+    for (int j = 0; j < nb; ++j) {
+      dist_allgather_rows(ctx, w.P.p, N, s, sizeof(T), st);  // exchange: full p for the matvec
+      launch_kmatvec_full(op, w.P.p, w.HP.p, s, st);          // Hp = H p (:162), local rows
+      if (variant == 0) {
+        dots(op, w, w.Pl(), w.HP.p, st);
+        cg_alpha_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, alpha, fail);
+      } else {
+        dots2(op, w, w.Pl(), w.HP.p, w.Pl(), w.R.p, st);
+        cg_alpha_pr_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, active, alpha, fail);
+      }
+      if (variant == 2 && n > 0)  // r_old for Polak-Ribiere (HP is free after alpha)
+        WGP_CUDA(cudaMemcpyAsync(w.HP.p, w.R.p, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
+      if (n > 0) launch_axpy_cols<T>(w.Vl(), w.Pl(), alpha, n, s, st);  // v += alpha p (:168)
+      dist_allgather_rows(ctx, w.V.p, N, s, sizeof(T), st);
+      if (!anchored) {
+        launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // r = b - H v (:171)
+        dots(op, w, w.R.p, w.R.p, st);
+        resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance,
+                                                    w.blk_rel.p + (size_t)j * s, active,
+                                                    w.blk_act.p + (size_t)j * s);
+        if (j + 1 < nb) next_direction();  // (:178-180), queued without a sync
+      }
+    }
     if (!anchored) {
-      launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // r = b - H v (:171)
-      dots(op, w, w.R.p, w.R.p, st);
-      resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance,
-                                                  rel, active);
-      WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
-      WGP_CUDA(cudaMemcpyAsync(hact.data(), active, sizeof(int) * (s + 1), cudaMemcpyDeviceToHost,
-                               st));
+      WGP_CUDA(cudaMemcpyAsync(h_rel_blk, w.blk_rel.p, sizeof(double) * nb * s, cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaMemcpyAsync(h_act_blk, w.blk_act.p, sizeof(int) * nb * s, cudaMemcpyDeviceToHost, st));
+      WGP_CUDA(cudaMemcpyAsync(h_fail, fail, sizeof(int), cudaMemcpyDeviceToHost, st));
       WGP_CUDA(cudaStreamSynchronize(st));
+      hact[s] = *h_fail;
     } else {
       // r = r_a - H_fast d (:171 on v = v_a + d); |r| and |d| per column in one pass
       launch_residual(op, w.RA.p, w.V.p, w.R.p, s, st);
@@ -357,27 +444,35 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
         if (changed)
           WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
       }
+      std::copy(hrel.begin(), hrel.end(), h_rel_blk);
+      std::copy(hact.begin(), hact.begin() + s, h_act_blk);
     }
     if (hact[s] != INT_MAX) {
       Error e(WGP_NOT_SPD, "cg_solve: non-positive curvature encountered");
       e.col = hact[s];
       throw e;
     }
-    n_active = 0;
-    for (int c = 0; c < s; ++c) {
-      if (prev_act[c]) {
-        out.history[c].push_back(hrel[c]);
-        out.iterations[c] = k;
-        if (!hact[c]) out.converged[c] = 1;
+    for (int j = 0; j < nb; ++j) {  // per-iteration bookkeeping from the block's records
+      n_active = 0;
+      for (int c = 0; c < s; ++c) {
+        const int now_act = h_act_blk[(size_t)j * s + c];
+        if (prev_act[c]) {
+          out.history[c].push_back(h_rel_blk[(size_t)j * s + c]);
+          out.iterations[c] = k + j;
+          if (!now_act) out.converged[c] = 1;
+        }
+        prev_act[c] = now_act;
+        n_active += now_act;
       }
-      prev_act[c] = hact[c];
-      n_active += hact[c];
+      if (n_active == 0) break;
     }
+    k += nb;
     if (n_active == 0) break;
-    precond_apply<T>(op, pd, w.R.p, w.Z.p, s, w.tvec.p, w.pwork.p, st);  // z = P r (:178)
-    dots(op, w, w.R.p, w.Z.p, st);
-    cg_beta_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta, 0);
-    if (n > 0) launch_xpby_cols<T>(w.Pl(), w.Z.p, beta, active, n, s, st);  // p = z + beta p (:180)
+    if (kbmax > 1) {  // size the next block from this one's time per iteration
+      const double per = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_block).count() / nb;
+      kb = std::max(1, std::min(kbmax, (int)(2e-3 / std::max(per, 1e-7))));
+    }
+    next_direction();
   }
   finish();
   WGP_CUDA(cudaGetLastError());

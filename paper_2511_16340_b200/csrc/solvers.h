@@ -22,6 +22,10 @@ struct SolverWork {
   DBuf<T> VA, RA;
   DBuf<double> anc;  // [4][s]: ones, minus ones, |d| per column, spare
   bool warm = false;
+  // per-iteration records of a CG block between host synchronisations (solvers.cu)
+  DBuf<double> blk_rel;
+  DBuf<int> blk_act;
+  PinnedBuf h_blk;
   T* Vl() const { return V.p + r0 * s; }
   T* Pl() const { return P.p + r0 * s; }
   DBuf<double> part;   // [nch][2][s] chunk partials

@@ -58,6 +58,7 @@ EXPORTS = (
     "wgp_precond_create", "wgp_precond_create_from_factor", "wgp_precond_destroy", "wgp_precond_get",
     "wgp_precond_apply", "wgp_cg_solve_with", "wgp_cross_kernel", "wgp_relative_residual",
     "wgp_quadratic_objective", "wgp_init_weights", "wgp_build_sample_rhs", "wgp_kernel_timer_read_tag",
+    "wgp_posterior_select",
 )
 
 
@@ -177,6 +178,8 @@ def _declare(L):
         "wgp_ascend_peaks": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, P, C.c_int, C.c_int, D, P, P]),
         "wgp_kernel_timer_read": (C.c_int, [P, P]),
         "wgp_kernel_timer_read_tag": (C.c_int, [C.c_char_p, P, P]),
+        "wgp_posterior_select": (C.c_int, [P, P, P, P, C.c_int, C.c_int, D, P, I64, P, I64, I64, C.c_int,
+                                          C.c_int, P]),
         "wgp_sample_prior": (C.c_int, [C.c_int, D, I64, I64, C.c_uint64, P, P, P]),
     }
     for name, (res, args) in sig.items():
@@ -917,6 +920,22 @@ def _stack_priors(priors):
     ph = np.ascontiguousarray(np.stack([p.phases for p in priors]))
     am = np.ascontiguousarray(np.stack([p.amplitudes for p in priors]))
     return Om, ph, am, F, sf
+
+
+def posterior_select(op: KernelOperator, priors: list, weights, Xs, groups: int = 1,
+                     fast: bool = True) -> np.ndarray:
+    """select_peaks' argmax (thompson.cpp:199-203) on the device: for every sample s and
+    contiguous candidate group g, the first candidate row with the largest posterior value
+    prior_s(X*) + K(X*, X) weights[:, s].  Returns S x groups int64 row indices."""
+    Om, ph, am, F, sf = _stack_priors(priors)
+    S = len(priors)
+    Wt = np.asfortranarray(weights, dtype=np.float64).reshape(op.n, S, order="F")
+    Xs = _f64(Xs)
+    m = Xs.shape[0]
+    idx = np.zeros((S, groups), dtype=np.int64)
+    _check(lib().wgp_posterior_select(op._h, _ptr(Om), _ptr(ph), _ptr(am), F, S, sf, _ptr(Wt), op.n,
+                                      _ptr(Xs), m, m, int(groups), 1 if fast else 0, _ptr(idx)))
+    return idx
 
 
 def grad_posterior(op: KernelOperator, priors: list, weights, Xs, sample_index) -> np.ndarray:

@@ -140,3 +140,27 @@ def test_anchored_fixed_budget_c4_shape(W):
             kr = next(i for i, x in enumerate(r.residual_history) if x <= lv)
             kg = next(i for i, x in enumerate(g.residual_history) if x <= lv)
             assert kg <= 1.25 * kr + 2, (c, lv, kg, kr)
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_posterior_select_matches_host_argmax(W, O, fast):
+    """select_peaks' per-sample argmax over candidate groups on the device equals the host
+    argmax of eval_posterior's values (thompson.cpp:199-203; first max on ties)."""
+    from paper_2511_16340_b200 import configs as Cfg
+    hyp = W.KernelHyperparams(0.3, 1.0, 1e-3, W.MATERN32)
+    X = Cfg.uniform_rows_fast(5, 1500, 3)
+    op = W.KernelOperator(hyp, X, precision=W.F32_3XTF32 if fast else W.F64)
+    priors = [W.sample_prior(hyp, 3, 500, W.derive_seed(1, c)) for c in range(6)]
+    wts = np.random.default_rng(2).standard_normal((1500, 6)) * 1e-2
+    Xc = Cfg.uniform_rows_fast(6, 20_003, 3)
+    idx = W.posterior_select(op, priors, wts, Xc, groups=4, fast=fast)
+    vals = W.rff_eval(op, priors, Xc, fast=fast) + op.cross_matvec(Xc, wts)
+    m = Xc.shape[0]
+    for g in range(4):
+        a, b = m * g // 4, m * (g + 1) // 4
+        want = a + np.argmax(vals[a:b], axis=0)
+        if not fast:
+            assert np.array_equal(idx[:, g], want)
+        else:  # fp32 values: the chosen row is a maximum to fp32 resolution
+            got_v = vals[idx[:, g], np.arange(6)]
+            assert np.all(got_v >= vals[want, np.arange(6)] - 1e-5)
