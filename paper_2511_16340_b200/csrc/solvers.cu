@@ -58,41 +58,6 @@ __global__ void cg_alpha_kernel(const double* __restrict__ part, int nch, int s,
   }
 }
 
-// Variant alpha = p.r / p.Hp (slots 0 = p.Hp, 1 = p.r of [nch][2][s] partials): equal to
-// r.z / p.Hp in exact arithmetic (r_k is orthogonal to p_{k-1}); with an inexact operator it
-// is the exact line minimum along p, which keeps the step consistent with the TRUE residual.
-__global__ void cg_alpha_pr_kernel(const double* __restrict__ part, int nch, int s,
-                                   const int* __restrict__ active, double* __restrict__ alpha,
-                                   int* __restrict__ fail_col) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
-    const double pHp = chunk_sum_ordered(part + c, nch, 2 * (int64_t)s);
-    const double pr = chunk_sum_ordered(part + s + c, nch, 2 * (int64_t)s);
-    if (!active[c]) {
-      alpha[c] = 0.0;
-      continue;
-    }
-    if (pHp <= 0.0) atomicMin(fail_col, c);
-    alpha[c] = pr / pHp;
-  }
-}
-
-// Polak-Ribiere (flexible CG) beta = z.(r - r_old) / rz (slots 0 = r.z, 1 = r_old.z): equal to
-// Fletcher-Reeves r.z / rz_old in exact arithmetic (r_old.z = 0), robust to an inexact H p.
-__global__ void cg_beta_pr_kernel(const double* __restrict__ part, int nch, int s,
-                                  double* __restrict__ rz, const int* __restrict__ active,
-                                  double* __restrict__ beta) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
-    const double rzn = chunk_sum_ordered(part + c, nch, 2 * (int64_t)s);
-    const double roz = chunk_sum_ordered(part + s + c, nch, 2 * (int64_t)s);
-    if (active[c]) {
-      beta[c] = (rzn - roz) / rz[c];
-      rz[c] = rzn;
-    } else {
-      beta[c] = 0.0;
-    }
-  }
-}
-
 // rz_next = r.z ; beta = rz_next / rz (active columns only), solvers.cpp:179-182.
 __global__ void cg_beta_kernel(const double* __restrict__ part, int nch, int s,
                                double* __restrict__ rz, const int* __restrict__ active,
@@ -291,10 +256,6 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
   w.tvec.ensure((size_t)(pd.k + 1) * s);
   Anchor<T> anc(op, w, st);
   const double frac = anchor_frac();
-  // WGP_CG_VARIANT (probes): 0 = the reference's alpha = r.z / p.Hp and Fletcher-Reeves beta
-  // (solvers.cpp:163-182); 1 = alpha = p.r / p.Hp; 2 = 1 + Polak-Ribiere beta.  Algebraically
-  // identical; they differ only under operator error (fp32 operators).
-  const int variant = getenv("WGP_CG_VARIANT") ? atoi(getenv("WGP_CG_VARIANT")) : 0;
   op.last_anchors = 0;
 
   // |b| per column
@@ -371,13 +332,8 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
   // z = P r (:178), rz, beta (:179-181), p = z + beta p (:180)
   auto next_direction = [&] {
     precond_apply<T>(op, pd, w.R.p, w.Z.p, s, w.tvec.p, w.pwork.p, st);
-    if (variant == 2) {
-      dots2(op, w, w.R.p, w.Z.p, w.HP.p, w.Z.p, st);
-      cg_beta_pr_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta);
-    } else {
-      dots(op, w, w.R.p, w.Z.p, st);
-      cg_beta_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta, 0);
-    }
+    dots(op, w, w.R.p, w.Z.p, st);
+    cg_beta_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, beta, 0);
     if (n > 0) launch_xpby_cols<T>(w.Pl(), w.Z.p, beta, active, n, s, st);
   };
   for (int k = 1; k <= cfg.max_iters;) {
@@ -386,15 +342,8 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
     for (int j = 0; j < nb; ++j) {
       dist_allgather_rows(ctx, w.P.p, N, s, sizeof(T), st);  // exchange: full p for the matvec
       launch_kmatvec_full(op, w.P.p, w.HP.p, s, st);          // Hp = H p (:162), local rows
-      if (variant == 0) {
-        dots(op, w, w.Pl(), w.HP.p, st);
-        cg_alpha_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, alpha, fail);
-      } else {
-        dots2(op, w, w.Pl(), w.HP.p, w.Pl(), w.R.p, st);
-        cg_alpha_pr_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, active, alpha, fail);
-      }
-      if (variant == 2 && n > 0)  // r_old for Polak-Ribiere (HP is free after alpha)
-        WGP_CUDA(cudaMemcpyAsync(w.HP.p, w.R.p, sizeof(T) * n * s, cudaMemcpyDeviceToDevice, st));
+      dots(op, w, w.Pl(), w.HP.p, st);
+      cg_alpha_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, alpha, fail);
       if (n > 0) launch_axpy_cols<T>(w.Vl(), w.Pl(), alpha, n, s, st);  // v += alpha p (:168)
       dist_allgather_rows(ctx, w.V.p, N, s, sizeof(T), st);
       if (!anchored) {

@@ -58,7 +58,7 @@ def solve(W, ctx, hyp, X, B, inits, cfg, prec):
 
 CASES = [
     ("cg", dict(method=0, tolerance=1e-8, max_iters=300, precond_rank=40, precond_shift=0.01)),
-    ("sgd", dict(method=1, tolerance=1e-3, max_iters=60, batch_size=256, learning_rate=0.3, seed=11)),
+    ("sgd", dict(method=1, tolerance=1e-3, max_iters=60, batch_size=256, learning_rate=2e-4, seed=11)),
     ("ap", dict(method=2, tolerance=1e-6, max_iters=80, block_size=300)),
 ]
 

@@ -1,5 +1,8 @@
 """Probe: fp32 (3xF16 tensor-core) CG with the direct vs the fp64-anchored true residual,
 against the fp64 operator, at C2 / reduced-C4 / C3 shapes.  Prints one JSON object per case.
+(Measured r2 in profiles/r02_anchor_probe.log; two algebraically equivalent CG variants --
+alpha = p.r / p.Hp and Polak-Ribiere beta -- were also run and changed nothing, so they
+were removed from the solver.)
 
   python tools/probes/gpu_probe_anchor.py [c2] [c4] [c3]
 """
@@ -20,11 +23,7 @@ from paper_2511_16340_b200 import warmgp as W  # noqa: E402
 
 MODES = (("f64", W.F64, W.RESIDUAL_DIRECT), ("tc_direct", W.F32_3XTF32, W.RESIDUAL_DIRECT),
          ("tc_anchored", W.F32_3XTF32, W.RESIDUAL_ANCHORED),
-         ("tc_anchor_every_iter", W.F32_3XTF32, W.RESIDUAL_ANCHORED),
-         ("tc_anchored_v1", W.F32_3XTF32, W.RESIDUAL_ANCHORED),
-         ("tc_anchored_v2", W.F32_3XTF32, W.RESIDUAL_ANCHORED),
-         ("f64_v2", W.F64, W.RESIDUAL_DIRECT),
-         ("tc_direct_v2", W.F32_3XTF32, W.RESIDUAL_DIRECT))
+         ("tc_anchor_every_iter", W.F32_3XTF32, W.RESIDUAL_ANCHORED))
 
 
 def crossings(h, levels=(1e-1, 1e-2, 1e-3, 1e-4, 1e-5, 1e-6)):
@@ -51,10 +50,6 @@ def solve_all(hyp, X, B, inits_fn, cfg, label, modes=MODES):
             os.environ["WGP_ANCHOR_FRAC"] = "0"
         else:
             os.environ.pop("WGP_ANCHOR_FRAC", None)
-        if name.endswith("_v1") or name.endswith("_v2"):
-            os.environ["WGP_CG_VARIANT"] = name[-1]
-        else:
-            os.environ.pop("WGP_CG_VARIANT", None)
         op = W.KernelOperator(hyp, X, precision=prec, residual=rm)
         W.solve_many(op, B[:, :1], [W.Initialization.cold()], cfg.copy(max_iters=2))  # warm-up
         t0 = time.perf_counter()
@@ -116,7 +111,7 @@ def c3():
     op = W.KernelOperator(hyp, X[:n0], precision=W.F64)
     prev = W.solve_many(op, np.asfortranarray(B[:n0]), [W.Initialization.cold()] * s, cfg)
     del op
-    modes = (MODES[0], MODES[1], MODES[3], MODES[4], MODES[5], MODES[7])
+    modes = (MODES[0], MODES[1], MODES[3])
     solve_all(hyp, X, B, lambda: [W.Initialization.warm(r.v) for r in prev], cfg, "c3_warm", modes)
     solve_all(hyp, X, B, lambda: [W.Initialization.cold()] * s, cfg, "c3_cold", modes)
 
