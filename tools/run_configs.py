@@ -7,7 +7,8 @@ tests/test_gpu_configs.py).
 c1  N=2000 RBF fp64, exact u1 on 1900 rows, CG warm vs cold to 1e-6 (bench_regression.cpp:139-197)
 c2  sequential growth 10k->20k (+500), CG / AP(500, greedy) / SGD(512), warm vs cold, s=17
 c3  covered by bench.py (kernel-matvec TFLOP/s and warm/cold CG time-to-tolerance)
-c4  N=500k RBF d=8, s=32, 1000-iteration budget CG and SGD, warm from N=495k, 3xTF32
+c4  N=500k RBF d=8, s=32, 1000-iteration budget CG (fp64-anchored residual) and SGD, warm from
+    N=495k, fp32 tensor-core operator
 c5  BO loop D=2..6, N0=5000, +64/round, 50 rounds, s=128 samples, 100k candidates
 """
 from __future__ import annotations
@@ -107,7 +108,8 @@ def run_c4(quick=False) -> dict:
     X = Cfg.uniform_rows_fast(W.derive_seed(0, 1), n, d)
     op = W.KernelOperator(hyp, X[:n_prev], precision=W.F32_3XTF32)
     priors = [W.sample_prior(hyp, d, 1024, W.derive_seed(0, 7 + 100 * c)) for c in range(s)]
-    out = {"config": "c4", "n": n, "n_prev": n_prev, "s": s, "budget": budget, "precision": "f32_3xtf32",
+    out = {"config": "c4", "n": n, "n_prev": n_prev, "s": s, "budget": budget,
+           "precision": "f32 (3xF16 tensor-core operator); CG with the fp64-anchored true residual",
            "solvers": {}}
     B_prev = W.rff_eval(op, priors) + W.normal_fill(W.derive_seed(0, 8), n_prev * s, 0.1).reshape(n_prev, s)
     op.append_rows(X[n_prev:])
@@ -123,12 +125,17 @@ def run_c4(quick=False) -> dict:
     del probe
     out["sgd_lr"] = lr
     out["sgd_grid_seconds"] = time.perf_counter() - t0
+    f64 = W.KernelOperator(hyp, X, precision=W.F64)  # true residuals of the final iterates
     for name, method, extra in (("cg", W.CG, {}), ("sgd", W.SGD, {"learning_rate": lr, "batch_size": 512})):
         cfg = W.SolverConfig(method=method, tolerance=1e-12, max_iters=budget, precond_rank=100,
                              precond_shift=0.01, **extra)
+        # CG with the fp64-anchored true residual (the direct fp32 residual floors and then
+        # diverges on this system); SGD on the plain fp32 operator
+        resid = W.RESIDUAL_ANCHORED if method == W.CG else W.RESIDUAL_DIRECT
+        op.residual_mode = resid
         # warm source: the n_prev system's budgeted solution (device operator restricted by
         # building it on the first n_prev rows)
-        prev = W.KernelOperator(hyp, X[:n_prev], precision=W.F32_3XTF32)
+        prev = W.KernelOperator(hyp, X[:n_prev], precision=W.F32_3XTF32, residual=resid)
         t0 = time.perf_counter()
         rp = W.solve_many(prev, np.asfortranarray(B_prev), [W.Initialization.cold()] * s, cfg)
         t_prev = time.perf_counter() - t0
@@ -140,6 +147,8 @@ def run_c4(quick=False) -> dict:
             t0 = time.perf_counter()
             rs = W.solve_many(op, B, inits, cfg)
             t = time.perf_counter() - t0
+            anchors = op.last_anchor_count
+            true = W.relative_residual(f64, np.column_stack([r.v for r in rs]), B)
             fr = [r.final_residual() for r in rs]
             mn = [min(r.residual_history) for r in rs]  # fixed budget on an fp32 operator:
             # the final residual of an unconverged CG fluctuates; the minimum is the stable figure
@@ -147,7 +156,9 @@ def run_c4(quick=False) -> dict:
                          "max_final_residual": float(np.max(fr)), "mean_min_residual": float(np.mean(mn)),
                          "residual_at": {str(k): float(np.mean([r.residual_history[min(k, len(r.residual_history) - 1)]
                                                                  for r in rs])) for k in (10, 50, 100, 250, 500)},
-                         "iterations": int(rs[0].iterations)}
+                         "iterations": int(rs[0].iterations), "anchors": anchors,
+                         "mean_true_final_residual_fp64": float(np.mean(true)),
+                         "max_true_final_residual_fp64": float(np.max(true))}
             print(f"  c4 {name} {mode}: {t:.1f}s mean final residual {np.mean(fr):.3e}", flush=True)
         out["solvers"][name] = rec
     return out
