@@ -233,6 +233,11 @@ void dist_allgather_rows(const Ctx& ctx, void* full, int64_t n, int64_t row_elem
 void dist_allgather_chunks(const Ctx& ctx, double* part, int64_t n, int64_t per_chunk,
                            cudaStream_t st);
 void dist_broadcast(const Ctx& ctx, void* buf, size_t bytes, int root, cudaStream_t st);
+// In-place sum over ranks of `count` doubles (NCCL all-reduce; loopback: rank order).  Used
+// where every entry has a single non-zero contributor, so the sum is exact and the result
+// bitwise the one-GPU value.
+void dist_allreduce_sum(const Ctx& ctx, double* buf, size_t count, cudaStream_t st);
+void launch_sum_slots(const double* slots, int world, size_t count, double* out, cudaStream_t st);
 void dist_allgather(const Ctx& ctx, const double* in, double* out, size_t count, cudaStream_t st);
 int owner_rank(const Ctx& ctx, int64_t n, int64_t row);
 

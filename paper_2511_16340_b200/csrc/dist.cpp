@@ -164,6 +164,23 @@ void dist_broadcast(const Ctx& ctx, void* buf, size_t bytes, int root, cudaStrea
   WGP_NCCL(ncclBroadcast(buf, buf, bytes, ncclChar, root, ctx.comm->nccl, st));
 }
 
+void dist_allreduce_sum(const Ctx& ctx, double* buf, size_t count, cudaStream_t st) {
+  if (ctx.world == 1 || count == 0) return;
+  if (ctx.comm->loop) {
+    DBuf<double> slots((size_t)ctx.world * count);
+    WGP_CUDA(cudaMemcpyAsync(slots.p + (size_t)ctx.rank * count, buf, sizeof(double) * count,
+                             cudaMemcpyDeviceToDevice, st));
+    loop_exchange(
+        ctx, buf, [&](int, const void* pq) { return pq; },
+        [&](int q) { return (void*)(slots.p + (size_t)q * count); },
+        [&](int) { return sizeof(double) * count; }, st);
+    launch_sum_slots(slots.p, ctx.world, count, buf, st);
+    WGP_CUDA(cudaStreamSynchronize(st));  // slots is freed on return
+    return;
+  }
+  WGP_NCCL(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx.comm->nccl, st));
+}
+
 // Every rank contributes `count` doubles; out holds world x count in rank order.
 void dist_allgather(const Ctx& ctx, const double* in, double* out, size_t count, cudaStream_t st) {
   if (in != out + (size_t)ctx.rank * count)

@@ -25,9 +25,9 @@
 //          Y * s^2 / (2^10 * scale_c) + sigma_n^2 V_i (or B - that: the true residual of
 //          solvers.cpp:171) as fp64.
 //
-// Warp roles (28 warps): 0 = XB bulk-copy producer (TMA engine, UBLKCP) + XA load,
-// 1 = GEMM1 issuer, 2 = V bulk-copy producer + TMEM allocator, 3 = GEMM2 issuer (whole warps
-// run the schedules, one elected lane issues), 4..27 = epilogue: three sets of 8 warps
+// Warp roles (28 warps): 24 = XB bulk-copy producer (TMA engine, UBLKCP) + XA load,
+// 25 = GEMM1 issuer, 26 = V bulk-copy producer + TMEM allocator, 27 = GEMM2 issuer (whole
+// warps run the schedules, one elected lane issues), 0..23 = epilogue: three sets of 8 warps
 // taking j tiles round-robin (2 warps per TMEM lane quadrant, 32 columns each).  Pipelines:
 // smem rings of XB_j (NSX) and V_j hi/lo (NSV); a ring of NB TMEM tile buffers (S written
 // by GEMM1, overwritten in place by K for GEMM2); mbarriers + tcgen05.commit.
@@ -62,7 +62,8 @@ constexpr int CPW = 32;        // tile columns per epilogue warp
 // One producer warp per smem ring: bulk copies issued by one warp are processed one at a
 // time (~400-900 cycles each in isolation, tools/bulk_microbench2.cu), but two XB and three
 // V producers measured no faster than one of each at C3 (the pipeline is paced by the
-// epilogue, not by V arrival).  Role warps: 0 XB producer, 1 GEMM1, 2 V producer, 3 GEMM2.
+// epilogue, not by V arrival).  Role r (warp EPIW + r): 0 XB producer, 1 GEMM1, 2 V producer,
+// 3 GEMM2.
 // (Round-robin GEMM2 issue over several warps and 4-warp epilogue sets were tried and
 // measured no faster / hung.)
 constexpr int NROLE = 4;
@@ -81,7 +82,7 @@ constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (drained a
 // operator): CH = 16 -> 1.4e-6 (random V) / 5.8e-6 (positive V); 32 -> 2.6e-6 / 1.2e-5;
 // 64 -> 4.9e-6 / 2.5e-5, each doubling ~1-2% faster.  WGP_TC_CH overrides.
 constexpr int MAX_NB = 5;
-constexpr int TRW = 12;  // trace slots per tile
+constexpr int TRW = 14;  // trace slots per tile
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
 
 struct Params {
@@ -142,9 +143,43 @@ __device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
 // columns go through the packed FP32 pipe, sqrt and exp2 through MUFU (moving a share of
 // either to an FMA-pipe polynomial measured no faster).  sqrt(|d2|): a tiny negative d2 from
 // the norm-form cancellation maps to ~0 like the reference's max(.,0) clamp (kernel.cpp:44).
-template <int NCOL>
+// sqrt of two non-negative floats on the FMA/ALU pipes (no MUFU): integer-magic rsqrt seed
+// (|rel err| <= 3.5%), one third-order step (~2e-4), then a Newton step folded into r = u y.
+__device__ __forceinline__ float2 soft_sqrt2(float2 u) {
+  float2 y = make_float2(__uint_as_float(0x5f375a86u - (__float_as_uint(u.x) >> 1)),
+                         __uint_as_float(0x5f375a86u - (__float_as_uint(u.y) >> 1)));
+  const float2 ONE = make_float2(1.0f, 1.0f);
+  float2 t = __fmul2_rn(u, y);
+  float2 e = __ffma2_rn(make_float2(-t.x, -t.y), y, ONE);          // 1 - u y^2
+  const float2 pp = __ffma2_rn(e, make_float2(0.375f, 0.375f), make_float2(0.5f, 0.5f));
+  y = __ffma2_rn(__fmul2_rn(y, e), pp, y);                          // y (1 + e/2 + 3e^2/8)
+  t = __fmul2_rn(u, y);
+  e = __ffma2_rn(make_float2(-t.x, -t.y), y, ONE);
+  return __ffma2_rn(t, __fmul2_rn(e, make_float2(0.5f, 0.5f)), t);  // u y (1 + e/2)
+}
+
+#ifndef WGP_SOFT_Q0
+#define WGP_SOFT_Q0 0
+#endif
+#ifndef WGP_SOFT_Q1
+#define WGP_SOFT_Q1 0
+#endif
+#ifndef WGP_SOFT_Q2
+#define WGP_SOFT_Q2 0
+#endif
+#ifndef WGP_SOFT_Q3
+#define WGP_SOFT_Q3 0
+#endif
+
+template <int NCOL, int SOFT = 0>
 __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* kv, float c1,
                                            float nclog2e) {
+#ifdef WGP_SKIP_MAP
+  // timing-only probe build: no map (invalid results)
+#pragma unroll
+  for (int q = 0; q < NCOL; ++q) kv[q] = __uint_as_float(v[q]) * 0.5f;
+  return;
+#endif
   const float2 NC = make_float2(nclog2e, nclog2e);
 #ifdef WGP_KSCALE_IN_EXP
   // (earlier form, kept for A/B probes) the 2^10 scale folded into the exponent argument:
@@ -162,8 +197,12 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
 #pragma unroll
     for (int q = 0; q < NCOL / 2; ++q) {
       float2 r;
-      r.x = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q])));
-      r.y = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q + 1])));
+      if (q < SOFT) {
+        r = soft_sqrt2(make_float2(fabsf(__uint_as_float(v[2 * q])), fabsf(__uint_as_float(v[2 * q + 1]))));
+      } else {
+        r.x = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q])));
+        r.y = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q + 1])));
+      }
 #ifdef WGP_KSCALE_IN_EXP
       const float2 a = __ffma2_rn(r, NC, OFF);  // log2(2^10 e^{-z})
 #else
@@ -204,6 +243,11 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
 __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NSX, int NSV) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Epilogue warps 0..EPIW-1, role warps EPIW..EPIW+3 (role r on SM sub-partition r): the
+  // issue arbiter favours the highest warp id, so the producers and MMA issuers -- a few
+  // instructions per tile on the critical path -- win the issue slot over the map warps
+  // they share a sub-partition with.
+  const int role = warp - EPIW;  // < 0 for epilogue warps
   const uint32_t ESZ = p.g1f16 ? 2 : 4;     // GEMM1 operand element bytes
   const uint32_t XA_BYTES = BM * p.K1 * ESZ;
   const uint32_t XB_BYTES = BJ * p.K1 * ESZ;
@@ -259,7 +303,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  if (role == 2) ptx::tmem_alloc(tmem_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -267,21 +311,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   const int KS1 = p.K1 * ESZ / 32;          // GEMM1 K-steps (32 bytes of K per instruction)
   const uint32_t sbo1 = (p.K1 * ESZ / 16) * 128;  // 8-row group stride of XA/XB tiles
 
-  if (warp == 0 || warp == 2) {
+  if (role == 0 || role == 2) {
     // ------------------------------------------------------------ producers (TMA engine)
     // Two independent rings: XB_j is consumed by GEMM1 right away, V_j only by GEMM2 after
     // the kernel map, so V stays resident ~4x longer; separate rings let each be as deep as
     // its own lifetime needs.
     const bool leader = ptx::elect_one();
-    if (warp == 0 && leader) {
+    if (role == 0 && leader) {
       ptx::mbar_arrive_expect_tx(xa_full, XA_BYTES);
       ptx::bulk_g2s(sXA, static_cast<const char*>(p.XA) + (size_t)blockIdx.x * XA_BYTES, XA_BYTES,
                     xa_full);
     }
-    if (warp == 0) {
-      for (int t = 0; t < T; ++t) {
-        const int st = t % NSX;
-        if (t >= NSX) ptx::mbar_wait(&xb_empty[st], ((t / NSX) & 1) ^ 1);
+    // (ring positions by counters: an integer division by a runtime ring size compiles to
+    // MUFU.RCP, which queues behind the epilogue's SFU work on a loaded SM sub-partition)
+    if (role == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < T; ++t, st = (st + 1 == NSX) ? 0 : st + 1, ph ^= (st == 0)) {
+        if (t >= NSX) ptx::mbar_wait(&xb_empty[st], ph ^ 1);
         if (leader) {
           trace_ev(p, t, 6);
           ptx::mbar_arrive_expect_tx(&xb_full[st], XB_BYTES);
@@ -292,30 +339,63 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         __syncwarp();
       }
     } else {
-      for (int t = 0; t < T; ++t) {
-        const int st = t % NSV;
-        if (t >= NSV) ptx::mbar_wait(&v_empty[st], ((t / NSV) & 1) ^ 1);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < T; ++t, st = (st + 1 == NSV) ? 0 : st + 1, ph ^= (st == 0)) {
+        if (t >= NSV) ptx::mbar_wait(&v_empty[st], ph ^ 1);
         if (leader) {
           trace_ev(p, t, 8);
+#if defined(WGP_HALF_V) || defined(WGP_V_SPLIT)  // (probe builds: half the V bytes here)
+#ifdef WGP_V_SPLIT
+          ptx::mbar_arrive_expect_tx(&v_full[st], 2 * VT_BYTES);  // lo half: copied by warp 1
+          if (NSV - NB < 1)
+            ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES + VT_BYTES,
+                          p.Vt + (size_t)(jt0 + t) * 2 * p.s_pad * BJ + (size_t)p.s_pad * BJ, VT_BYTES,
+                          &v_full[st]);
+#else
+          ptx::mbar_arrive_expect_tx(&v_full[st], VT_BYTES);
+#endif
+          ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES, p.Vt + (size_t)(jt0 + t) * 2 * p.s_pad * BJ,
+                        VT_BYTES, &v_full[st]);
+#else
           ptx::mbar_arrive_expect_tx(&v_full[st], 2 * VT_BYTES);
           ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES, p.Vt + (size_t)(jt0 + t) * 2 * p.s_pad * BJ,
                         2 * VT_BYTES, &v_full[st]);
+#endif
         }
         __syncwarp();
       }
     }
-  } else if (warp == 1 || warp == 3) {
+  } else if (role == 1 || role == 3) {
     // ------------------------------------------------------------ MMA issuers
     // tcgen05.mma issue blocks for about the instruction's execution time, so one thread
-    // cannot keep two dependent streams fed.  Warp 1 issues GEMM1 (distance tiles) and warp 3
+    // cannot keep two dependent streams fed.  Role 1 issues GEMM1 (distance tiles) and role 3
     // issues GEMM2 (K.V); each waits only on its own inputs and each tcgen05.commit tracks
-    // its own thread's MMAs.  Whole warps run the schedule (uniform control flow,
-    // descriptors in uniform registers); one elected lane issues.
-    if (warp == 1) {
+    // its own thread's MMAs.  Whole warps run the schedules (uniform control flow, descriptors
+    // in uniform registers: a single-lane loop measured 3x slower MMA issue); one elected lane
+    // issues.
+    if (role == 1) {
       const uint32_t idesc1 = p.g1f16 ? ptx::idesc_f16(BM, BJ) : ptx::idesc_tf32(BM, BJ);
       const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
       const uint64_t dXB0 = ptx::umma_desc(ptx::smem_u32(sXB), 128, sbo1);
       const uint64_t xb_step = (uint64_t)(XB_BYTES >> 4);  // descriptor start-address units
+#ifdef WGP_V_SPLIT
+      // probe: the lo half of V tile u is copied by this warp, VD tiles ahead of GEMM1: the
+      // stage of tile t + VD was released by GEMM2(t + VD - NSV), implied by b_free(t - NB)
+      // when VD <= NSV - NB.
+      const int VD = min(3, NSV - NB);
+      auto copy_vlo = [&](int u) {
+        if (VD >= 1 && u < T) {
+          const int st = u % NSV;
+          ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES + VT_BYTES,
+                        p.Vt + (size_t)(jt0 + u) * 2 * p.s_pad * BJ + (size_t)p.s_pad * BJ, VT_BYTES,
+                        &v_full[st]);
+        }
+      };
+      if (ptx::elect_one())
+        for (int u = 0; u < VD; ++u) copy_vlo(u);
+      __syncwarp();
+#endif
       ptx::mbar_wait(xa_full, 0);
       int st1 = 0, b1 = 0;
       uint32_t ph1 = 0, phb1 = 0;
@@ -324,6 +404,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
+#ifdef WGP_V_SPLIT
+          copy_vlo(t + VD);
+#endif
           trace_ev(p, t, 0);
           const uint64_t dB = dXB0 + xb_step * st1;
           if (p.g1f16) {
@@ -346,12 +429,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sV), 128, (BJ / 8) * 128);
       const uint64_t v_step = (uint64_t)((2 * VT_BYTES) >> 4);
       const uint64_t vlo_step = (uint64_t)(VT_BYTES >> 4);
+      int st2 = 0, b2 = 0, c = 0, pos = 0;  // V stage, TMEM buffer, chunk, tile within chunk
+      uint32_t ph2 = 0, phb2 = 0;
       for (int t = 0; t < T; ++t) {
-        const int st2 = t % NSV, b2 = t % NB;
-        const uint32_t ph2 = (t / NSV) & 1, phb2 = (t / NB) & 1;
-        const int c = t / CH, ya = c & 1;
-        const bool first = t == c * CH, last = t == T - 1 || t == c * CH + CH - 1;
+        const int ya = c & 1;
+        const bool first = pos == 0, last = t == T - 1 || pos == CH - 1;
         if (first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
+        if (lane == 0) trace_ev(p, t, 13);
         ptx::mbar_wait(&v_full[st2], ph2);
         if (lane == 0) trace_ev(p, t, 9);
         ptx::mbar_wait(&k_full[b2], phb2);
@@ -367,26 +451,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks)
             ptx::mma_f16_ts(yacc, kb + ks * 16, dVh + 16 * ks, idesc2, (!first || ks > 0) ? 1u : 0u);
+#ifndef WGP_NO_CORR  // (probe builds: timing without the correction products)
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks)
             ptx::mma_f16_ts(ycor, kb + ks * 16, dVl + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks)
             ptx::mma_f16_ts(ycor, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);
+#endif
           trace_ev(p, t, 10);
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
           if (last) ptx::mma_commit(&y_full[ya]);
+          trace_ev(p, t, 12);
         }
         __syncwarp();
+        if (++st2 == NSV) { st2 = 0; ph2 ^= 1; }
+        if (++b2 == NB) { b2 = 0; phb2 ^= 1; }
+        if (++pos == CH) { pos = 0; ++c; }
       }
     }
-  } else if (warp >= NROLE) {
+  } else if (warp < EPIW) {
     // ------------------------------------------------------------ kernel-map epilogue
     // NSET sets of 8 warps take tiles round-robin (set = t mod NSET); within a set, warp
     // (quadrant q, half) maps rows 32q.. and columns 32 half.. of the tile, 16 at a time.
     const int q = warp & 3;                   // TMEM lane quadrant accessible to this warp
-    const int g = (warp - NROLE) >> 2;        // group of 4 warps (one per quadrant), 0..5
+    const int g = warp >> 2;                  // group of 4 warps (one per quadrant), 0..5
     const int set = g / (SETW / 4), half = g % (SETW / 4);
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int r = q * 32 + lane;              // row within the CTA tile
@@ -412,18 +502,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // GEMM2 long done) and must finish before GEMM2 starts chunk d+2.
     constexpr int DSTEP = 4;
     int dk = 0;  // columns of chunk `drained` already moved
-    auto drain_step = [&](int c) {
+    // A drain visit in two halves: issue the accumulator load (after the chunk's y_full), and
+    // -- once a tcgen05.wait::ld has covered it -- the reduction into the partials.  Inside
+    // the tile loop the load goes out with the tile's first S load and shares its wait.
+    auto drain_issue = [&](int c, uint32_t* y) {
       const int ya = c & 1;
       if (dk == 0) {
         ptx::mbar_wait(&y_full[ya], (c >> 1) & 1);
         ptx::tc_fence_after();
       }
-      uint32_t y[DSTEP];
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                    : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3])
                    : "r"(tmem + lane_off + TM_Y + ya * 64 + dc0 + dk));
-      ptx::tmem_wait_ld();
+    };
+    auto drain_finish = [&](int c, const uint32_t* y) {
+      const int ya = c & 1;
+#ifdef WGP_NO_DRAIN  // (probe builds: timing without the partial-sum reductions)
+      if (false) {
+#else
       if (row_ok && dk < ncol) {
+#endif
         // first chunk stores, later chunks add with fire-and-forget vector reductions
         // performed at L2 (fp32: ~50 chunk terms per sweep at C3, relative rounding ~1e-7).
         // Each address is only ever touched by this thread, and same-address operations of
@@ -447,6 +545,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         dk = 0;
         ++drained;
       }
+    };
+    auto drain_step = [&](int c) {
+      uint32_t y[DSTEP];
+      drain_issue(c, y);
+      ptx::tmem_wait_ld();
+      drain_finish(c, y);
     };
     auto drain_all = [&](int c) {  // the last chunk, after the sweep
       while (drained == c) drain_step(c);
@@ -482,15 +586,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       if (tr) trace_ev(p, t, 3);
       const int64_t gj_base = (int64_t)(jt0 + t) * BJ + half * CPW;
       const bool diag = p.gram && gj_base < grow0 + BM && gj_base + CPW > grow0;
+      // this tile's drain visit (a finished chunk, 4 tiles after its last GEMM2 was issued)
+      const bool dvisit = drainer && dc0 < p.s_pad && drained < NCH - 1 && t >= (drained + 1) * CH + 4;
+      const int dchunk = drained;
+      uint32_t ydr[DSTEP];
+      if (dvisit) drain_issue(dchunk, ydr);
 #pragma unroll
       for (int h2 = 0; h2 < CPW / 16; ++h2) {
         const uint32_t col = tmem + lane_off + b * 64 + half * CPW + h2 * 16;
         uint32_t v[16];
         ptx::tmem_ld16(col, v);
         ptx::tmem_wait_ld();
+        if (h2 == 0 && dvisit) drain_finish(dchunk, ydr);
         if (tr && h2 == 0) trace_ev(p, t, 7);
         float kv[16];
-        kernel_map<16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
+        if (WGP_SOFT_Q0 + WGP_SOFT_Q1 + WGP_SOFT_Q2 + WGP_SOFT_Q3 == 0) {
+          kernel_map<16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
+        } else {  // probe builds: per-quadrant share of FMA-pipe square roots
+          switch (q) {
+            case 0: kernel_map<16, WGP_SOFT_Q0>(p.kind, v, kv, p.c1, p.neg_c_log2e); break;
+            case 1: kernel_map<16, WGP_SOFT_Q1>(p.kind, v, kv, p.c1, p.neg_c_log2e); break;
+            case 2: kernel_map<16, WGP_SOFT_Q2>(p.kind, v, kv, p.c1, p.neg_c_log2e); break;
+            default: kernel_map<16, WGP_SOFT_Q3>(p.kind, v, kv, p.c1, p.neg_c_log2e); break;
+          }
+        }
         if (diag) {  // tile touches the diagonal: k(x,x) = s^2 exactly
           const int64_t gj0 = gj_base + h2 * 16;
 #pragma unroll
@@ -520,10 +639,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       if (lane == 0) ptx::mbar_arrive(&k_full[b]);
       if (tr) trace_ev(p, t, 5);
       if (lane == 0 && half == 0 && set == 0 && q == 3) trace_ev(p, t, 11);
-      if (drainer && dc0 < p.s_pad && drained < NCH - 1 && t >= (drained + 1) * CH + 4)
-        drain_step(drained);
     }
-    if (warp == NROLE && lane == 0) cta_ev(p, 1);
+    if (warp == 0 && lane == 0) cta_ev(p, 1);
     if (drainer && dc0 < p.s_pad) {
       while (drained < NCH) drain_all(drained);
       drain_corr();
@@ -532,7 +649,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) cta_ev(p, 2);
-  if (warp == 2) {
+  if (role == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }
@@ -1027,7 +1144,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
                                cudaMemcpyDeviceToHost, st));
       WGP_CUDA(cudaStreamSynchronize(st));
       if (FILE* f = fopen(trace_path, "w")) {
-        fprintf(f, "tile,g1_issue,g2_issue,epi_wait_s,epi_s_ready,epi_wait_k,epi_done,prod_issue,epi_ld_done,v_issue,g2_vready,g2_issued,done_q3\n");
+        fprintf(f, "tile,g1_issue,g2_issue,epi_wait_s,epi_s_ready,epi_wait_k,epi_done,prod_issue,epi_ld_done,v_issue,g2_vready,g2_issued,done_q3,g2_committed,g2_yfree_ok\n");
         for (int t = 0; t < ntiles; ++t)
         {
           fprintf(f, "%d", t);

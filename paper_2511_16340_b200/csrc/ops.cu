@@ -36,6 +36,24 @@ __global__ void append_rows_kernel(const double* __restrict__ src, int64_t ld, i
 
 }  // namespace
 
+// out[e] = sum over q of slots[q][e], in rank order (loopback all-reduce).
+__global__ void sum_slots_kernel(const double* __restrict__ slots, int world, size_t count,
+                                 double* __restrict__ out) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count;
+       e += (size_t)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int q = 0; q < world; ++q) a += slots[(size_t)q * count + e];
+    out[e] = a;
+  }
+}
+
+void launch_sum_slots(const double* slots, int world, size_t count, double* out, cudaStream_t st) {
+  if (!count) return;
+  const unsigned g = (unsigned)std::min<size_t>((count + 255) / 256, 148 * 8);
+  sum_slots_kernel<<<g, 256, 0, st>>>(slots, world, count, out);
+  WGP_CUDA(cudaGetLastError());
+}
+
 void op_append_rows(Op& op, const double* host_rows, int64_t n_new, int64_t ld, int col_major) {
   if (n_new <= 0) return;
   cudaStream_t st = op.ctx->stream;

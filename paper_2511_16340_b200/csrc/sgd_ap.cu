@@ -230,11 +230,13 @@ __global__ void __launch_bounds__(512) block_chol_kernel(const double* __restric
   }
 }
 
-// delta_c = L^-T (L^-1 r_c[B]) for the column's chosen block; v_c[B] += delta_c.
+// delta_c = L^-T (L^-1 r_c[B]) for the column's chosen block; v_c[B] += delta_c.  The block's
+// residual rows come from the full residual R (rows [start, start + len)) or, when Rblk is
+// given, from the gathered block rows Rblk[i][c] (sharded solves).
 __global__ void __launch_bounds__(1024) ap_block_solve_kernel(
     const double* __restrict__ inv, int bs, int64_t n, const int* __restrict__ blk,
-    const int* __restrict__ active, const double* __restrict__ R, int s, double* __restrict__ V,
-    double* __restrict__ delta) {
+    const int* __restrict__ active, const double* __restrict__ R, const double* __restrict__ Rblk,
+    int s, double* __restrict__ V, double* __restrict__ delta) {
   const int c = blockIdx.x;
   if (!active[c]) return;
   extern __shared__ double sh[];
@@ -243,7 +245,8 @@ __global__ void __launch_bounds__(1024) ap_block_solve_kernel(
   const int64_t start = (int64_t)blk[c] * bs;
   const int len = (int)min((int64_t)bs, n - start);
   const double* Li = inv + (int64_t)blk[c] * bs * bs;
-  for (int i = threadIdx.x; i < len; i += blockDim.x) rb[i] = R[(start + i) * s + c];
+  for (int i = threadIdx.x; i < len; i += blockDim.x)
+    rb[i] = Rblk ? Rblk[(int64_t)i * s + c] : R[(start + i) * s + c];
   __syncthreads();
   for (int i = threadIdx.x; i < len; i += blockDim.x) {  // y = L^-1 r  (lower)
     double a = 0.0;
@@ -259,32 +262,69 @@ __global__ void __launch_bounds__(1024) ap_block_solve_kernel(
   }
 }
 
-// Per column: squared norms of each block of r, then greedy argmax (strict >, first wins)
-// -- one block per column, n_blocks small (<= a few hundred).
-__global__ void greedy_block_kernel(const double* __restrict__ R, int64_t n, int bs, int nblk,
-                                    int s, const int* __restrict__ active, int* __restrict__ blk) {
+// Greedy block choice (solvers.cpp:277-286), in two steps so that a row-sharded residual
+// gives bitwise the one-GPU choice: the rows are cut into segments at every block boundary
+// and every kChunkRows boundary (a segment lies in one block and one chunk, so one rank owns
+// it); seg_norms writes the squared norm of each segment this rank owns (32-lane
+// interleaved sums + xor-shuffle, a fixed order) and 0 for the others -- summed over ranks
+// exactly, since one rank contributes each value -- and greedy_from_segments adds a block's
+// segments in order, takes the square root and the argmax (strict >, first wins).
+__global__ void seg_norms_kernel(const double* __restrict__ Rloc, int64_t r0, int64_t nloc,
+                                 const int64_t* __restrict__ seg_start, int nseg, int s,
+                                 const int* __restrict__ active, double* __restrict__ segn) {
   const int c = blockIdx.x;
-  if (!active[c]) return;
-  extern __shared__ double nrm[];
-  for (int b = threadIdx.y; b < nblk; b += blockDim.y) {
-    const int64_t s0 = (int64_t)b * bs;
-    const int64_t s1 = min(n, s0 + bs);
+  for (int g = threadIdx.y; g < nseg; g += blockDim.y) {
+    const int64_t a0 = seg_start[g], a1 = seg_start[g + 1];
     double a = 0.0;
-    for (int64_t i = s0 + threadIdx.x; i < s1; i += 32) a = fma(R[i * s + c], R[i * s + c], a);
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (threadIdx.x == 0) nrm[b] = sqrt(a);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && threadIdx.y == 0) {
-    double best = -1.0;
-    int arg = 0;
-    for (int b = 0; b < nblk; ++b)
-      if (nrm[b] > best) {
-        best = nrm[b];
-        arg = b;
+    if (active[c] && a0 >= r0 && a0 < r0 + nloc) {
+      for (int64_t i = a0 + threadIdx.x; i < a1; i += 32) {
+        const double r = Rloc[(i - r0) * s + c];
+        a = fma(r, r, a);
       }
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    }
+    if (threadIdx.x == 0) segn[(int64_t)g * s + c] = a;
+  }
+}
+
+__global__ void greedy_from_segments_kernel(const double* __restrict__ segn,
+                                            const int* __restrict__ seg_block, int nseg, int nblk,
+                                            int s, const int* __restrict__ active,
+                                            int* __restrict__ blk) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
+    if (!active[c]) continue;
+    double best = -1.0, cur = 0.0;
+    int arg = 0;
+    for (int g = 0; g < nseg; ++g) {
+      cur += segn[(int64_t)g * s + c];
+      if (g + 1 == nseg || seg_block[g + 1] != seg_block[g]) {
+        const double nrm = sqrt(cur);
+        if (nrm > best) {
+          best = nrm;
+          arg = seg_block[g];
+        }
+        cur = 0.0;
+      }
+    }
     blk[c] = arg;
   }
+}
+
+// Rows of each active column's chosen block that this rank owns -> Rblk[i][c] (0 for rows of
+// other ranks): the exact all-reduce of these gives every rank the block's residual.
+__global__ void gather_block_rows_kernel(const double* __restrict__ Rloc, int64_t r0, int64_t nloc,
+                                         int64_t n, int bs, const int* __restrict__ blk,
+                                         const int* __restrict__ active, int s,
+                                         double* __restrict__ Rblk) {
+  const int c = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= bs) return;
+  double v = 0.0;
+  if (active[c]) {
+    const int64_t row = (int64_t)blk[c] * bs + i;
+    if (row < n && row >= r0 && row < r0 + nloc) v = Rloc[(row - r0) * s + c];
+  }
+  Rblk[(int64_t)i * s + c] = v;
 }
 
 __global__ void set_cyclic_kernel(int* blk, int s, int value) {
@@ -398,22 +438,32 @@ void launch_block_chol(const Op& op, int bs, int nblk, double* fac, double* inv,
 }
 
 void launch_ap_block_solve(const double* inv, int bs, int64_t n, const int* blk, const int* active,
-                           const double* R, int s, double* V, double* delta, cudaStream_t st) {
+                           const double* R, const double* Rblk, int s, double* V, double* delta,
+                           cudaStream_t st) {
   const size_t smem = sizeof(double) * 2 * bs;
   if (smem > 48 * 1024)
     WGP_CUDA(cudaFuncSetAttribute(ap_block_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-  ap_block_solve_kernel<<<s, 1024, smem, st>>>(inv, bs, n, blk, active, R, s, V, delta);
+  ap_block_solve_kernel<<<s, 1024, smem, st>>>(inv, bs, n, blk, active, R, Rblk, s, V, delta);
   WGP_CUDA(cudaGetLastError());
 }
 
-void launch_greedy_block(const double* R, int64_t n, int bs, int nblk, int s, const int* active,
-                         int* blk, cudaStream_t st) {
-  const size_t smem = sizeof(double) * nblk;
-  if (smem > 48 * 1024)
-    WGP_CUDA(cudaFuncSetAttribute(greedy_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-  greedy_block_kernel<<<s, dim3(32, 16), smem, st>>>(R, n, bs, nblk, s, active, blk);
+void launch_seg_norms(const double* Rloc, int64_t r0, int64_t nloc, const int64_t* seg_start, int nseg,
+                      int s, const int* active, double* segn, cudaStream_t st) {
+  seg_norms_kernel<<<s, dim3(32, 16), 0, st>>>(Rloc, r0, nloc, seg_start, nseg, s, active, segn);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_greedy_from_segments(const double* segn, const int* seg_block, int nseg, int nblk, int s,
+                                 const int* active, int* blk, cudaStream_t st) {
+  greedy_from_segments_kernel<<<(s + 63) / 64, 64, 0, st>>>(segn, seg_block, nseg, nblk, s, active, blk);
+  WGP_CUDA(cudaGetLastError());
+}
+
+void launch_gather_block_rows(const double* Rloc, int64_t r0, int64_t nloc, int64_t n, int bs,
+                              const int* blk, const int* active, int s, double* Rblk, cudaStream_t st) {
+  gather_block_rows_kernel<<<dim3((bs + 127) / 128, s), 128, 0, st>>>(Rloc, r0, nloc, n, bs, blk, active, s,
+                                                                     Rblk);
   WGP_CUDA(cudaGetLastError());
 }
 

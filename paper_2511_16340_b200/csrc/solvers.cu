@@ -550,10 +550,12 @@ void sgd_solve_batched(Op& op, const wgp_solver_config& cfg, const std::vector<u
 // n_blocks); factors of every diagonal block are built once on the device.
 void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& w,
                       SolveOutputs& out, cudaStream_t st) {
-  // Sharded (world > 1): V is full and replicated; the residual is kept as a full N-row
-  // buffer whose rows this rank owns are updated locally and which is all-gathered before
-  // the block choice and the block solve, so every rank picks the same block, computes the
-  // same delta and applies it to its copy of V -- bit-identical to one GPU.
+  // Sharded (world > 1): V is replicated, the residual is row-sharded (R holds
+  // this rank's rows only).  Per iteration the ranks exchange only the greedy block norms
+  // (per-segment squared norms, one owner per segment) and the chosen block's residual rows
+  // (bs x s, one owner per row), both by an exact all-reduce; every rank then computes the
+  // same delta, applies it to its copy of V and updates its own residual rows with K1-col --
+  // bit-identical to one GPU.
   const Ctx& ctx = *op.ctx;
   const int64_t n = w.n, N = w.N, r0 = w.r0;
   const int s = w.s;
@@ -571,16 +573,28 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   WGP_CUDA(cudaMemcpyAsync(&hfail, fail.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   WGP_CUDA(cudaStreamSynchronize(st));
   if (hfail) throw_error(WGP_NOT_SPD, "ap_solve: diagonal block factorization failed");
-  DBuf<double> Rfull;
-  double* Rall = w.R.p;
-  if (ctx.world > 1) {
-    Rfull.alloc((size_t)padded_rows(N, ctx.world) * s);
-    Rall = Rfull.p;
+  double* Rloc = w.R.p;  // this rank's rows
+  // segments: rows cut at every block and every chunk boundary (each in one block, one chunk)
+  std::vector<int64_t> seg_start;
+  std::vector<int> seg_block;
+  for (int b = 0; b < nblk; ++b) {
+    const int64_t a0 = (int64_t)b * bs, a1 = std::min<int64_t>(N, a0 + bs);
+    for (int64_t a = a0; a < a1;) {
+      seg_start.push_back(a);
+      seg_block.push_back(b);
+      a = std::min<int64_t>(a1, (a / kChunkRows + 1) * kChunkRows);
+    }
   }
-  double* Rloc = Rall + r0 * s;  // this rank's rows
-  auto gather_r = [&] {
-    if (ctx.world > 1) dist_allgather_rows(ctx, Rall, N, s, sizeof(double), st);
-  };
+  const int nseg = (int)seg_start.size();
+  seg_start.push_back(N);
+  DBuf<int64_t> dseg_start(seg_start.size());
+  DBuf<int> dseg_block(seg_block.size());
+  DBuf<double> segn((size_t)nseg * s), Rblk;
+  WGP_CUDA(cudaMemcpyAsync(dseg_start.p, seg_start.data(), sizeof(int64_t) * seg_start.size(),
+                           cudaMemcpyHostToDevice, st));
+  WGP_CUDA(cudaMemcpyAsync(dseg_block.p, seg_block.data(), sizeof(int) * seg_block.size(),
+                           cudaMemcpyHostToDevice, st));
+  if (ctx.world > 1) Rblk.alloc((size_t)bs * s);
   double* bnorm = w.scal.p + 3 * s;
   double* rel = w.scal.p + 4 * s;
   int* active = w.act.p;
@@ -603,12 +617,19 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   DBuf<double> delta((size_t)bs * s);
   WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
   for (int k = 1; k <= cfg.max_iters && n_active > 0; ++k) {
-    gather_r();
-    if (cfg.ap_ordering == WGP_AP_GREEDY)
-      launch_greedy_block(Rall, N, bs, nblk, s, active, blk.p, st);
-    else
+    if (cfg.ap_ordering == WGP_AP_GREEDY) {
+      launch_seg_norms(Rloc, r0, n, dseg_start.p, nseg, s, active, segn.p, st);
+      dist_allreduce_sum(ctx, segn.p, (size_t)nseg * s, st);
+      launch_greedy_from_segments(segn.p, dseg_block.p, nseg, nblk, s, active, blk.p, st);
+    } else {
       launch_set_cyclic(blk.p, s, (k - 1) % nblk, st);
-    launch_ap_block_solve(inv.p, bs, N, blk.p, active, Rall, s, w.V.p, delta.p, st);
+    }
+    if (ctx.world > 1) {  // the chosen blocks' residual rows, from their owners
+      launch_gather_block_rows(Rloc, r0, n, N, bs, blk.p, active, s, Rblk.p, st);
+      dist_allreduce_sum(ctx, Rblk.p, (size_t)bs * s, st);
+    }
+    launch_ap_block_solve(inv.p, bs, N, blk.p, active, Rloc, ctx.world > 1 ? Rblk.p : nullptr, s,
+                          w.V.p, delta.p, st);
     launch_kcols(op, blk.p, bs, delta.p, s, active, Rloc, r0, n, st);  // r -= H[:, B] delta
     if (k % nblk == 0) launch_residual(op, w.B.p, w.V.p, Rloc, s, st);  // drift refresh
     residual_norms(ctx, w, Rloc, bnorm, rel, hrel, st);

@@ -138,9 +138,14 @@ void launch_kcols(const Op& op, const int* blk, int bs, const double* delta, int
 void launch_block_chol(const Op& op, int bs, int nblk, double* fac, double* inv, int* fail,
                        cudaStream_t st);
 void launch_ap_block_solve(const double* inv, int bs, int64_t n, const int* blk, const int* active,
-                           const double* R, int s, double* V, double* delta, cudaStream_t st);
-void launch_greedy_block(const double* R, int64_t n, int bs, int nblk, int s, const int* active,
-                         int* blk, cudaStream_t st);
+                           const double* R, const double* Rblk, int s, double* V, double* delta,
+                           cudaStream_t st);
+void launch_seg_norms(const double* Rloc, int64_t r0, int64_t nloc, const int64_t* seg_start, int nseg,
+                      int s, const int* active, double* segn, cudaStream_t st);
+void launch_greedy_from_segments(const double* segn, const int* seg_block, int nseg, int nblk, int s,
+                                 const int* active, int* blk, cudaStream_t st);
+void launch_gather_block_rows(const double* Rloc, int64_t r0, int64_t nloc, int64_t n, int bs,
+                              const int* blk, const int* active, int s, double* Rblk, cudaStream_t st);
 void launch_set_cyclic(int* blk, int s, int value, cudaStream_t st);
 void launch_sgd_update(double* V, double* vel, const int* rows, const double* g, int nb, int64_t n,
                        int s, const int* active, double momentum, double scale, double lr,

@@ -51,70 +51,80 @@ __global__ void rows_to_colmajor_kernel(const T* __restrict__ src, int64_t n, in
   }
 }
 
-// One block per (chunk, group of up to 16 columns), one thread per (column, 16-row slab):
-// all 32 slabs of the chunk load at once (16 rows x 2 NQ arrays in flight per thread, one
-// pass), then one thread per column adds the 32 slab sums in slab order.  Per column the
-// chunk is 32 fixed 16-row slabs, each summed sequentially, slab sums added in slab order:
-// the order of every column's sum depends only on the row index, never on s or on the other
-// columns (solve_many must equal single-RHS solves bitwise, test_solvers.cpp:397-413).
+// Per column the chunk is 32 fixed 16-row slabs, each summed sequentially, slab sums added
+// in slab order: the order of every column's sum depends only on the row index, never on s
+// or on the other columns (solve_many must equal single-RHS solves bitwise,
+// test_solvers.cpp:397-413).  Work item = (chunk, group of up to kColsPerBlock columns), one
+// thread per (column, slab); a grid of a few resident blocks per SM walks the items, so the
+// load phase of one block overlaps the slab reduction of another and the last wave is thin.
+// Each slab is loaded in two 8-row halves (all loads of a half issued before its FMA chain):
+// 80 registers, 3 blocks of 256 threads per SM, ~200 KB of loads in flight per SM.
 constexpr int kSlabRows = kChunkRows / 32;
-constexpr int kColsPerBlock = 16;  // coldots: columns per block (x 32 slabs = 512 threads)
+constexpr int kColsPerBlock = 8;  // coldots: columns per work item (x 32 slabs = 256 threads)
+constexpr int kColdotsBlocksPerSM = 3;
 
 template <typename T, int NQ>
-__global__ void __launch_bounds__(512) coldots_kernel(const T* __restrict__ A0,
-                                                      const T* __restrict__ B0,
-                                                      const T* __restrict__ A1,
-                                                      const T* __restrict__ B1, int64_t n, int s,
-                                                      int cb, double* __restrict__ part) {
+__global__ void __launch_bounds__(256, kColdotsBlocksPerSM)
+    coldots_kernel(const T* __restrict__ A0, const T* __restrict__ B0, const T* __restrict__ A1,
+                   const T* __restrict__ B1, int64_t n, int s, int cb, int ngroups, int64_t items,
+                   double* __restrict__ part) {
   __shared__ double red[NQ][32][kColsPerBlock];
-  const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
   const int cl = threadIdx.x % cb;
   const int q = threadIdx.x / cb;  // slab
-  const int c = blockIdx.y * cb + cl;
-  if (c < s) {
-    const int64_t i0 = r0 + (int64_t)q * kSlabRows;
-    const int64_t i1 = min(n, i0 + kSlabRows);
-    double a0 = 0.0, a1 = 0.0;
-    const T* pa0 = A0 + i0 * s + c;
-    const T* pb0 = B0 + i0 * s + c;
-    const T* pa1 = A1 + i0 * s + c;
-    const T* pb1 = B1 + i0 * s + c;
-    if (i1 - i0 == kSlabRows) {
-      // full slab: all its loads issued before the (ordered) FMA chain
-      T xa[kSlabRows], xb[kSlabRows], ya[NQ > 1 ? kSlabRows : 1], yb[NQ > 1 ? kSlabRows : 1];
+  constexpr int H = kSlabRows / 2;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t chunk = item / ngroups;
+    const int grp = (int)(item - chunk * ngroups);
+    const int c = grp * cb + cl;
+    if (q < 32 && c < s) {
+      const int64_t i0 = chunk * kChunkRows + (int64_t)q * kSlabRows;
+      const int64_t i1 = min(n, i0 + kSlabRows);
+      double a0 = 0.0, a1 = 0.0;
+      const T* pa0 = A0 + i0 * s + c;
+      const T* pb0 = B0 + i0 * s + c;
+      const T* pa1 = A1 + i0 * s + c;
+      const T* pb1 = B1 + i0 * s + c;
+      if (i1 - i0 == kSlabRows) {
 #pragma unroll
-      for (int k = 0; k < kSlabRows; ++k) {
-        xa[k] = pa0[(int64_t)k * s];
-        xb[k] = pb0[(int64_t)k * s];
-        if (NQ > 1) {
-          ya[k] = pa1[(int64_t)k * s];
-          yb[k] = pb1[(int64_t)k * s];
+        for (int h = 0; h < 2; ++h) {
+          T xa[H], xb[H], ya[NQ > 1 ? H : 1], yb[NQ > 1 ? H : 1];
+#pragma unroll
+          for (int k = 0; k < H; ++k) {
+            const int64_t o = (int64_t)(h * H + k) * s;
+            xa[k] = pa0[o];
+            xb[k] = pb0[o];
+            if (NQ > 1) {
+              ya[k] = pa1[o];
+              yb[k] = pb1[o];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < H; ++k) {
+            a0 = fma((double)xa[k], (double)xb[k], a0);
+            if (NQ > 1) a1 = fma((double)ya[k], (double)yb[k], a1);
+          }
+        }
+      } else {
+        for (int64_t k = 0; k < i1 - i0; ++k) {
+          a0 = fma((double)pa0[k * s], (double)pb0[k * s], a0);
+          if (NQ > 1) a1 = fma((double)pa1[k * s], (double)pb1[k * s], a1);
         }
       }
-#pragma unroll
-      for (int k = 0; k < kSlabRows; ++k) {
-        a0 = fma((double)xa[k], (double)xb[k], a0);
-        if (NQ > 1) a1 = fma((double)ya[k], (double)yb[k], a1);
-      }
-    } else {
-      for (int64_t k = 0; k < i1 - i0; ++k) {
-        a0 = fma((double)pa0[k * s], (double)pb0[k * s], a0);
-        if (NQ > 1) a1 = fma((double)pa1[k * s], (double)pb1[k * s], a1);
-      }
+      red[0][q][cl] = a0;
+      if (NQ > 1) red[NQ - 1][q][cl] = a1;
     }
-    red[0][q][cl] = a0;
-    if (NQ > 1) red[NQ - 1][q][cl] = a1;
-  }
-  __syncthreads();
-  if (threadIdx.x < cb * NQ) {
-    const int col = threadIdx.x % cb, qq = threadIdx.x / cb;
-    const int cc = blockIdx.y * cb + col;
-    if (cc < s) {
-      double t = 0.0;
+    __syncthreads();
+    if (threadIdx.x < cb * NQ) {
+      const int col = threadIdx.x % cb, qq = threadIdx.x / cb;
+      const int cc = grp * cb + col;
+      if (cc < s) {
+        double t = 0.0;
 #pragma unroll 8
-      for (int k = 0; k < 32; ++k) t += red[qq][k][col];
-      part[(int64_t)blockIdx.x * NQ * s + (int64_t)qq * s + cc] = t;
+        for (int k = 0; k < 32; ++k) t += red[qq][k][col];
+        part[chunk * NQ * s + (int64_t)qq * s + cc] = t;
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -254,11 +264,13 @@ void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t 
   const int nch = ceil_div(n, kChunkRows);
   if (nch <= 0) return;
   const int cb = s < kColsPerBlock ? s : kColsPerBlock;
-  const dim3 grid(nch, ceil_div(s, cb));
+  const int ngroups = ceil_div(s, cb);
+  const int64_t items = (int64_t)nch * ngroups;
+  const int grid = (int)std::min<int64_t>(items, (int64_t)148 * kColdotsBlocksPerSM);
   if (A1)
-    coldots_kernel<T, 2><<<grid, cb * 32, 0, st>>>(A0, B0, A1, B1, n, s, cb, part);
+    coldots_kernel<T, 2><<<grid, cb * 32, 0, st>>>(A0, B0, A1, B1, n, s, cb, ngroups, items, part);
   else
-    coldots_kernel<T, 1><<<grid, cb * 32, 0, st>>>(A0, B0, A0, B0, n, s, cb, part);
+    coldots_kernel<T, 1><<<grid, cb * 32, 0, st>>>(A0, B0, A0, B0, n, s, cb, ngroups, items, part);
   WGP_CUDA(cudaGetLastError());
 }
 
