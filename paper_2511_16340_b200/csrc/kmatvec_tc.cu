@@ -502,9 +502,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // GEMM2 long done) and must finish before GEMM2 starts chunk d+2.
     constexpr int DSTEP = 4;
     int dk = 0;  // columns of chunk `drained` already moved
-    // A drain visit in two halves: issue the accumulator load (after the chunk's y_full), and
-    // -- once a tcgen05.wait::ld has covered it -- the reduction into the partials.  Inside
-    // the tile loop the load goes out with the tile's first S load and shares its wait.
+    // A drain visit: the accumulator load (after the chunk's y_full), its wait, and the
+    // reduction into the partials.
     auto drain_issue = [&](int c, uint32_t* y) {
       const int ya = c & 1;
       if (dk == 0) {
@@ -586,18 +585,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       if (tr) trace_ev(p, t, 3);
       const int64_t gj_base = (int64_t)(jt0 + t) * BJ + half * CPW;
       const bool diag = p.gram && gj_base < grow0 + BM && gj_base + CPW > grow0;
-      // this tile's drain visit (a finished chunk, 4 tiles after its last GEMM2 was issued)
-      const bool dvisit = drainer && dc0 < p.s_pad && drained < NCH - 1 && t >= (drained + 1) * CH + 4;
-      const int dchunk = drained;
-      uint32_t ydr[DSTEP];
-      if (dvisit) drain_issue(dchunk, ydr);
 #pragma unroll
       for (int h2 = 0; h2 < CPW / 16; ++h2) {
         const uint32_t col = tmem + lane_off + b * 64 + half * CPW + h2 * 16;
         uint32_t v[16];
         ptx::tmem_ld16(col, v);
         ptx::tmem_wait_ld();
-        if (h2 == 0 && dvisit) drain_finish(dchunk, ydr);
         if (tr && h2 == 0) trace_ev(p, t, 7);
         float kv[16];
         if (WGP_SOFT_Q0 + WGP_SOFT_Q1 + WGP_SOFT_Q2 + WGP_SOFT_Q3 == 0) {
@@ -639,6 +632,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       if (lane == 0) ptx::mbar_arrive(&k_full[b]);
       if (tr) trace_ev(p, t, 5);
       if (lane == 0 && half == 0 && set == 0 && q == 3) trace_ev(p, t, 11);
+      // (issuing this visit's accumulator load together with the next tile's first S load,
+      // sharing one tcgen05.wait::ld, measured 2-4% slower at every shape)
+      if (drainer && dc0 < p.s_pad && drained < NCH - 1 && t >= (drained + 1) * CH + 4)
+        drain_step(drained);
     }
     if (warp == 0 && lane == 0) cta_ev(p, 1);
     if (drainer && dc0 < p.s_pad) {
