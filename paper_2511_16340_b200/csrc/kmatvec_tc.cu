@@ -143,35 +143,7 @@ __device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
 // columns go through the packed FP32 pipe, sqrt and exp2 through MUFU (moving a share of
 // either to an FMA-pipe polynomial measured no faster).  sqrt(|d2|): a tiny negative d2 from
 // the norm-form cancellation maps to ~0 like the reference's max(.,0) clamp (kernel.cpp:44).
-// sqrt of two non-negative floats on the FMA/ALU pipes (no MUFU): integer-magic rsqrt seed
-// (|rel err| <= 3.5%), one third-order step (~2e-4), then a Newton step folded into r = u y.
-__device__ __forceinline__ float2 soft_sqrt2(float2 u) {
-  float2 y = make_float2(__uint_as_float(0x5f375a86u - (__float_as_uint(u.x) >> 1)),
-                         __uint_as_float(0x5f375a86u - (__float_as_uint(u.y) >> 1)));
-  const float2 ONE = make_float2(1.0f, 1.0f);
-  float2 t = __fmul2_rn(u, y);
-  float2 e = __ffma2_rn(make_float2(-t.x, -t.y), y, ONE);          // 1 - u y^2
-  const float2 pp = __ffma2_rn(e, make_float2(0.375f, 0.375f), make_float2(0.5f, 0.5f));
-  y = __ffma2_rn(__fmul2_rn(y, e), pp, y);                          // y (1 + e/2 + 3e^2/8)
-  t = __fmul2_rn(u, y);
-  e = __ffma2_rn(make_float2(-t.x, -t.y), y, ONE);
-  return __ffma2_rn(t, __fmul2_rn(e, make_float2(0.5f, 0.5f)), t);  // u y (1 + e/2)
-}
-
-#ifndef WGP_SOFT_Q0
-#define WGP_SOFT_Q0 0
-#endif
-#ifndef WGP_SOFT_Q1
-#define WGP_SOFT_Q1 0
-#endif
-#ifndef WGP_SOFT_Q2
-#define WGP_SOFT_Q2 0
-#endif
-#ifndef WGP_SOFT_Q3
-#define WGP_SOFT_Q3 0
-#endif
-
-template <int NCOL, int SOFT = 0>
+template <int NCOL>
 __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* kv, float c1,
                                            float nclog2e) {
 #ifdef WGP_SKIP_MAP
@@ -197,12 +169,8 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
 #pragma unroll
     for (int q = 0; q < NCOL / 2; ++q) {
       float2 r;
-      if (q < SOFT) {
-        r = soft_sqrt2(make_float2(fabsf(__uint_as_float(v[2 * q])), fabsf(__uint_as_float(v[2 * q + 1]))));
-      } else {
-        r.x = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q])));
-        r.y = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q + 1])));
-      }
+      r.x = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q])));
+      r.y = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q + 1])));
 #ifdef WGP_KSCALE_IN_EXP
       const float2 a = __ffma2_rn(r, NC, OFF);  // log2(2^10 e^{-z})
 #else
@@ -345,23 +313,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         if (t >= NSV) ptx::mbar_wait(&v_empty[st], ph ^ 1);
         if (leader) {
           trace_ev(p, t, 8);
-#if defined(WGP_HALF_V) || defined(WGP_V_SPLIT)  // (probe builds: half the V bytes here)
-#ifdef WGP_V_SPLIT
-          ptx::mbar_arrive_expect_tx(&v_full[st], 2 * VT_BYTES);  // lo half: copied by warp 1
-          if (NSV - NB < 1)
-            ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES + VT_BYTES,
-                          p.Vt + (size_t)(jt0 + t) * 2 * p.s_pad * BJ + (size_t)p.s_pad * BJ, VT_BYTES,
-                          &v_full[st]);
-#else
-          ptx::mbar_arrive_expect_tx(&v_full[st], VT_BYTES);
-#endif
-          ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES, p.Vt + (size_t)(jt0 + t) * 2 * p.s_pad * BJ,
-                        VT_BYTES, &v_full[st]);
-#else
           ptx::mbar_arrive_expect_tx(&v_full[st], 2 * VT_BYTES);
           ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES, p.Vt + (size_t)(jt0 + t) * 2 * p.s_pad * BJ,
                         2 * VT_BYTES, &v_full[st]);
-#endif
         }
         __syncwarp();
       }
@@ -379,23 +333,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
       const uint64_t dXB0 = ptx::umma_desc(ptx::smem_u32(sXB), 128, sbo1);
       const uint64_t xb_step = (uint64_t)(XB_BYTES >> 4);  // descriptor start-address units
-#ifdef WGP_V_SPLIT
-      // probe: the lo half of V tile u is copied by this warp, VD tiles ahead of GEMM1: the
-      // stage of tile t + VD was released by GEMM2(t + VD - NSV), implied by b_free(t - NB)
-      // when VD <= NSV - NB.
-      const int VD = min(3, NSV - NB);
-      auto copy_vlo = [&](int u) {
-        if (VD >= 1 && u < T) {
-          const int st = u % NSV;
-          ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES + VT_BYTES,
-                        p.Vt + (size_t)(jt0 + u) * 2 * p.s_pad * BJ + (size_t)p.s_pad * BJ, VT_BYTES,
-                        &v_full[st]);
-        }
-      };
-      if (ptx::elect_one())
-        for (int u = 0; u < VD; ++u) copy_vlo(u);
-      __syncwarp();
-#endif
       ptx::mbar_wait(xa_full, 0);
       int st1 = 0, b1 = 0;
       uint32_t ph1 = 0, phb1 = 0;
@@ -404,9 +341,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
-#ifdef WGP_V_SPLIT
-          copy_vlo(t + VD);
-#endif
           trace_ev(p, t, 0);
           const uint64_t dB = dXB0 + xb_step * st1;
           if (p.g1f16) {
@@ -593,16 +527,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         ptx::tmem_wait_ld();
         if (tr && h2 == 0) trace_ev(p, t, 7);
         float kv[16];
-        if (WGP_SOFT_Q0 + WGP_SOFT_Q1 + WGP_SOFT_Q2 + WGP_SOFT_Q3 == 0) {
-          kernel_map<16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
-        } else {  // probe builds: per-quadrant share of FMA-pipe square roots
-          switch (q) {
-            case 0: kernel_map<16, WGP_SOFT_Q0>(p.kind, v, kv, p.c1, p.neg_c_log2e); break;
-            case 1: kernel_map<16, WGP_SOFT_Q1>(p.kind, v, kv, p.c1, p.neg_c_log2e); break;
-            case 2: kernel_map<16, WGP_SOFT_Q2>(p.kind, v, kv, p.c1, p.neg_c_log2e); break;
-            default: kernel_map<16, WGP_SOFT_Q3>(p.kind, v, kv, p.c1, p.neg_c_log2e); break;
-          }
-        }
+        kernel_map<16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
         if (diag) {  // tile touches the diagonal: k(x,x) = s^2 exactly
           const int64_t gj0 = gj_base + h2 * 16;
 #pragma unroll
