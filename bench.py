@@ -377,10 +377,8 @@ def c4_sharded_matvec(W, ctx, world, rank, steps=3):
     st = torch.cuda.current_stream()
     sp = st.cuda_stream
 
-    def step():
-        if world > 1:
-            ctx.allgather_rows_dev(V.data_ptr(), n, s, sp)
-        op.kmatvec_dev(V.data_ptr(), Y.data_ptr(), s, sp)
+    def step():  # all-gather of the V slots overlapped with the local diagonal block
+        op.kmatvec_sharded_dev(V.data_ptr(), Y.data_ptr(), s, sp)
 
     step()
     torch.cuda.synchronize()
@@ -402,7 +400,9 @@ def c4_sharded_matvec(W, ctx, world, rank, steps=3):
     flops = float(n) * n * (2 * d + 2 * s)
     return {"n": n, "d": d, "s": s, "kernel": "rbf", "world": world, "ms_per_matvec": ms,
             "TFLOP/s": flops / (ms * 1e-3) / 1e12, "steps": steps,
-            "rows_per_rank": r1 - r0, "note": "all-gather of V included (world > 1); max over ranks"}
+            "rows_per_rank": r1 - r0,
+            "note": "wgp_kmatvec_sharded_dev: all-gather of the V slots (world > 1) overlapped with "
+                    "the local diagonal block; device time, max over ranks"}
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -443,9 +443,10 @@ def run_ours(args):
     sp = stream.cuda_stream
 
     def step():
-        if world > 1:  # the exchange step of a sharded matvec: all-gather the V row slices
-            ctx.allgather_rows_dev(V.data_ptr(), n, S, sp)
-        op.kmatvec_dev(V.data_ptr(), Y.data_ptr(), S, sp)
+        if world > 1:  # sharded: all-gather of the V row slots overlapped with the local block
+            op.kmatvec_sharded_dev(V.data_ptr(), Y.data_ptr(), S, sp)
+        else:
+            op.kmatvec_dev(V.data_ptr(), Y.data_ptr(), S, sp)
 
     for _ in range(args.warmup):
         step()
@@ -469,7 +470,9 @@ def run_ours(args):
     ms_step = float(np.mean(ms))
     k_ms, k_launches = W.kernel_timer_read()
     W.kernel_timer_enable(False)
-    kernel_ms = k_ms / max(1, k_launches)
+    # the tensor-core kernel's time per step (one launch at world 1; the diagonal block and the
+    # remote column ranges at world > 1)
+    kernel_ms = k_ms / max(1, args.steps)
     t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -553,7 +556,8 @@ def run_ours(args):
             "mma_kind": "kind::f16, 3-term hi/lo splits of K and V (and of x for the distance "
                         "GEMM), fp32 accumulation in TMEM",
             "kernel": "tc::kmatvec_tc_kernel (CUDA events around its launches, "
-                      f"{k_launches} launches, {kernel_ms:.3f} ms avg; {100 * kernel_ms / ms_step:.1f}% of the step)",
+                      f"{k_launches} launches over {args.steps} steps, {kernel_ms:.3f} ms per step; "
+                      f"{100 * kernel_ms / ms_step:.1f}% of the step)",
             "algorithmic_flops_per_launch": flops_launch,
             "algorithmic_flops_per_pair": 2 * DIM + 2 * S,
             "composite": {"bound": "mufu", "mufu_ops_per_pair": mufu_per_pair,
@@ -606,7 +610,7 @@ def run_ours(args):
             "data": "synthetic (seeded X ~ N(0,I), V ~ N(0,1))",
             "config": bench_config(n, world),
             "rows_per_rank": r1 - r0,
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": 5 * args.steps,  # colmax + colscale_finish + split_v + kmatvec_tc + reduce_splits per step
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": (5 if world == 1 else 15) * args.steps,  # colmax + colscale_finish + split_v + kmatvec_tc + reduce_splits per launch (world > 1: diagonal block + two remote column ranges)
             "cg_warm_vs_cold": cg,
             "c4_sharded_matvec": c4,
             "vector_kernels": vec,

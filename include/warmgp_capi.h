@@ -157,6 +157,12 @@ wgp_status wgp_kmatvec(wgp_op* op, const double* V, int64_t ldv, int s, double* 
  * unsharded) row-major, both in the op's compute type, on the context stream
  * (stream == NULL) or on `stream`.  Asynchronous. */
 wgp_status wgp_kmatvec_dev(wgp_op* op, const void* dV, void* dY, int s, void* stream);
+/* Sharded form of wgp_kmatvec_dev (one matvec of solvers.cpp:162 on row-sharded
+ * solver vectors): dV is the padded full-row buffer (wgp_shard_padded_rows rows) with this
+ * rank's slot up to date; the row slots are all-gathered (NCCL over NVLink, on the context's
+ * communication stream) while the local diagonal block K(X_g, X_g) V_g runs, then the other
+ * columns.  dY: this rank's rows.  World 1: same as wgp_kmatvec_dev. */
+wgp_status wgp_kmatvec_sharded_dev(wgp_op* op, void* dV, void* dY, int s, void* stream);
 /* dY = dB - H dV (true residual b - H v, solvers.cpp:150,171,203,231,268,293,298). */
 wgp_status wgp_residual_dev(wgp_op* op, const void* dB, const void* dV, void* dY, int s,
                             void* stream);

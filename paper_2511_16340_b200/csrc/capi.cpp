@@ -233,6 +233,8 @@ wgp_status wgp_ctx_create(int device, wgp_ctx** out) {
     WGP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     WGP_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (auto& e : c->part_ev) WGP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    WGP_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    for (auto& e : c->comm_ev) WGP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     *out = c.release();
   });
 }
@@ -279,6 +281,9 @@ void wgp_ctx_destroy(wgp_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto& e : c->part_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  for (auto& e : c->comm_ev)
     if (e) cudaEventDestroy(e);
   delete c;
 }
@@ -351,6 +356,16 @@ wgp_status wgp_kmatvec_dev(wgp_op* op, const void* dV, void* dY, int s, void* st
     WGP_REQUIRE(op->n >= 1, "wgp_kmatvec_dev: empty operator");
     cudaStream_t st = stream ? (cudaStream_t)stream : op->ctx->stream;
     launch_kmatvec_full(*op, (const double*)dV, (double*)dY, s, st);
+  });
+}
+
+wgp_status wgp_kmatvec_sharded_dev(wgp_op* op, void* dV, void* dY, int s, void* stream) {
+  return guard([&] {
+    WGP_REQUIRE(op && dV && dY && s >= 1, "wgp_kmatvec_sharded_dev: bad argument");
+    WGP_REQUIRE(op->n >= 1, "wgp_kmatvec_sharded_dev: empty operator");
+    cudaStream_t st = stream ? (cudaStream_t)stream : op->ctx->stream;
+    cudaEvent_t ev = dist_allgather_rows_begin(*op->ctx, dV, op->n, s, sizeof(double), st);
+    launch_kmatvec_overlap(*op, nullptr, (const double*)dV, (double*)dY, s, ev, st);
   });
 }
 

@@ -137,6 +137,10 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // host-API result copies overlapping compute
   cudaEvent_t part_ev[2] = {nullptr, nullptr};
+  // sharded operators: the row all-gather runs on comm_stream while the compute stream works
+  // on the local diagonal block (comm_ev[0]: slot ready, comm_ev[1]: gather complete)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t comm_ev[2] = {nullptr, nullptr};
   int rank = 0, world = 1;
   Comm* comm = nullptr;
 };
@@ -230,6 +234,12 @@ inline int64_t padded_rows(int64_t n, int world) { return padded_chunks(n, world
 // All are no-ops (or local copies) when ctx.world == 1.
 void dist_allgather_rows(const Ctx& ctx, void* full, int64_t n, int64_t row_elems, size_t esize,
                          cudaStream_t st);
+// Start the all-gather of the row slots of `full` (this rank's slot final on `st`); work
+// queued on `st` afterwards overlaps it.  Returns the event that completes the gather
+// (world 1: nullptr, nothing to wait for; loopback: the exchange is done before returning
+// and the event is already recorded).
+cudaEvent_t dist_allgather_rows_begin(const Ctx& ctx, void* full, int64_t n, int64_t row_elems,
+                                      size_t esize, cudaStream_t st);
 void dist_allgather_chunks(const Ctx& ctx, double* part, int64_t n, int64_t per_chunk,
                            cudaStream_t st);
 void dist_broadcast(const Ctx& ctx, void* buf, size_t bytes, int root, cudaStream_t st);

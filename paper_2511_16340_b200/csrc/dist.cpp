@@ -144,6 +144,22 @@ void dist_allgather_rows(const Ctx& ctx, void* full, int64_t n, int64_t row_elem
   allgather_slots(ctx, full, (size_t)shard_chunks(n, ctx.world) * kChunkRows * row_elems * esize, st);
 }
 
+cudaEvent_t dist_allgather_rows_begin(const Ctx& ctx, void* full, int64_t n, int64_t row_elems,
+                                      size_t esize, cudaStream_t st) {
+  if (ctx.world == 1) return nullptr;
+  const size_t slot = (size_t)shard_chunks(n, ctx.world) * kChunkRows * row_elems * esize;
+  if (ctx.comm->loop) {
+    allgather_slots(ctx, full, slot, st);
+    WGP_CUDA(cudaEventRecord(ctx.comm_ev[1], st));
+    return ctx.comm_ev[1];
+  }
+  WGP_CUDA(cudaEventRecord(ctx.comm_ev[0], st));
+  WGP_CUDA(cudaStreamWaitEvent(ctx.comm_stream, ctx.comm_ev[0], 0));
+  allgather_slots(ctx, full, slot, ctx.comm_stream);
+  WGP_CUDA(cudaEventRecord(ctx.comm_ev[1], ctx.comm_stream));
+  return ctx.comm_ev[1];
+}
+
 // Per-chunk partial arrays [padded_chunks][per_chunk] fp64 (chunk c of rows [512c, 512c+512)).
 void dist_allgather_chunks(const Ctx& ctx, double* part, int64_t n, int64_t per_chunk,
                            cudaStream_t st) {

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256, NT <= 3 ? 4 : (NT <= 8 ? 3 : 2)) kmatvec_
     const double* __restrict__ Xr, int64_t nrows, int64_t row0, const double* __restrict__ Xc,
     int64_t ncols, int dpad, int dim, const double* __restrict__ V, int s,
     const double* __restrict__ B, double* __restrict__ Y, KParams p, int gram, int64_t jlen,
-    double* __restrict__ part) {
+    double* __restrict__ part, int z0) {
   constexpr int BS = NT * 8;
   extern __shared__ double dsm[];
   const int ds = dim + 1;
@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(256, NT <= 3 ? 4 : (NT <= 8 ? 3 : 2)) kmatvec_
   for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
   const double kdiag = p.s2 + p.noise2;
   // this CTA's column range (grid.z splits the sweep into fixed-length ranges)
-  const int64_t j_lo = (int64_t)blockIdx.z * jlen;
+  const int zs = z0 + (int)blockIdx.z;  // column split of this CTA
+  const int64_t j_lo = (int64_t)zs * jlen;
   const int64_t j_hi = min(ncols, j_lo + jlen);
   for (int64_t jb = j_lo; jb < j_hi; jb += DN) {
     __syncthreads();
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(256, NT <= 3 ? 4 : (NT <= 8 ? 3 : 2)) kmatvec_
   }
   const int64_t gr = rbase + warp * 8 + (lane >> 2);
   if (gr >= nrows) return;
-  double* out = part ? part + (size_t)blockIdx.z * nrows * s : Y;
+  double* out = part ? part + (size_t)zs * nrows * s : Y;
 #pragma unroll
   for (int t = 0; t < NT; ++t)
 #pragma unroll
@@ -272,17 +273,21 @@ __global__ void sum_splits_kernel(const double* __restrict__ part, int nsplit, i
   }
 }
 
-// Column splits: the j sweep is cut into fixed 4096-column ranges (at most 16) summed in
-// order by sum_splits_kernel, so small row counts still fill the GPU (C2: 313 row blocks ->
-// 1565 CTAs).  The split depends on ncols only, so every rank of a row-sharded operator
-// sums each output identically and the result is world-size independent.
-constexpr int64_t kSplitCols = 4096;
+// Column splits: the j sweep is cut into up to 16 equal ranges of at least 128 columns,
+// summed in order by sum_splits_kernel, so small row counts still fill the GPU (config 1,
+// N=2000: 32 row blocks x 16 splits instead of 32 CTAs each sweeping 2000 columns, 185 ->
+// ~15 us per matvec).  The split depends on ncols only, so every rank of a row-sharded
+// operator sums each output identically and the result is world-size independent.
+constexpr int64_t kSplitCols = 128;
 inline int f64_splits(int64_t ncols) { return (int)std::min<int64_t>(16, (ncols + kSplitCols - 1) / kSplitCols); }
 
+// With a ColPhase (sharded matvec overlapping the V all-gather): the splits whose columns
+// lie inside [c0, c1) run first, the others after ph->ready; every split is computed and
+// summed exactly as in the single launch, so the result is bitwise the same.
 template <int NT>
 void launch_dmma(const double* Xr, int64_t nrows, int64_t row0, const double* Xc, int64_t ncols,
                  int dpad, int dim, const double* V, int s, const double* B, double* Y, KParams kp,
-                 bool gram, DBuf<double>& split_buf, cudaStream_t st) {
+                 bool gram, DBuf<double>& split_buf, cudaStream_t st, const ColPhase* ph) {
   const int nsplit = std::max(1, f64_splits(ncols));
   const int64_t jlen = nsplit == 1 ? ncols : (((ncols + nsplit - 1) / nsplit + DN - 1) / DN) * DN;
   double* part = nullptr;
@@ -290,15 +295,32 @@ void launch_dmma(const double* Xr, int64_t nrows, int64_t row0, const double* Xc
     split_buf.ensure((size_t)nsplit * nrows * s);
     part = split_buf.p;
   }
-  dim3 grid(ceil_div(nrows, DM), ceil_div(s, NT * 8), nsplit);
   const size_t smem = sizeof(double) * ((size_t)(DM + DN) * (dim + 1) + DM * (DN + 1) +
                                         (size_t)DN * (NT * 8 + 1));
   if (smem > 48 * 1024)
     WGP_CUDA(cudaFuncSetAttribute(kmatvec_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-  kmatvec_dmma_kernel<NT><<<grid, 256, smem, st>>>(Xr, nrows, row0, Xc, ncols, dpad, dim, V, s, B, Y,
-                                                   kp, gram ? 1 : 0, jlen, part);
-  WGP_CUDA(cudaGetLastError());
+  auto run = [&](int za, int zb) {
+    if (zb <= za) return;
+    dim3 grid(ceil_div(nrows, DM), ceil_div(s, NT * 8), zb - za);
+    kmatvec_dmma_kernel<NT><<<grid, 256, smem, st>>>(Xr, nrows, row0, Xc, ncols, dpad, dim, V, s, B, Y,
+                                                     kp, gram ? 1 : 0, jlen, part, za);
+    WGP_CUDA(cudaGetLastError());
+  };
+  if (!ph || !ph->ready) {
+    run(0, nsplit);
+  } else {
+    int za = nsplit, zb = nsplit;  // splits inside [c0, c1)
+    if (nsplit > 1) {
+      za = (int)std::min<int64_t>(nsplit, (ph->c0 + jlen - 1) / jlen);
+      zb = za;
+      while (zb < nsplit && std::min<int64_t>(ncols, (int64_t)(zb + 1) * jlen) <= ph->c1) ++zb;
+    }
+    run(za, zb);
+    WGP_CUDA(cudaStreamWaitEvent(st, ph->ready, 0));
+    run(0, za);
+    run(zb, nsplit);
+  }
   if (part) {
     const int64_t count = nrows * s;
     sum_splits_kernel<<<(int)std::min<int64_t>(148 * 8, (count + 255) / 256), 256, 0, st>>>(part, nsplit, count,
@@ -315,32 +337,36 @@ void launch_dmma(const double* Xr, int64_t nrows, int64_t row0, const double* Xc
 // the all-CUDA-core kernel instead (validation).
 static void launch_f64(const Op& op, const double* Xr, int64_t nrows, int64_t row0,
                        const double* Xc, int64_t ncols, const double* V, int s, const double* B,
-                       double* Y, bool gram, cudaStream_t st) {
+                       double* Y, bool gram, cudaStream_t st, const ColPhase* ph) {
   WGP_REQUIRE(op.dim <= 32, "fp64 kmatvec: dim <= 32 supported, got %d", op.dim);
   const KParams kp = op.kp();
   const int dp = op.dpad, d = op.dim;
-  if (s <= 8) return launch_dmma<1>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
-  if (s <= 16) return launch_dmma<2>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
-  if (s <= 24) return launch_dmma<3>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
-  if (s <= 32) return launch_dmma<4>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
-  if (s <= 64) return launch_dmma<8>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
-  if (s <= 136) return launch_dmma<17>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
-  return launch_dmma<16>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st);
+  if (s <= 8) return launch_dmma<1>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st, ph);
+  if (s <= 16) return launch_dmma<2>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st, ph);
+  if (s <= 24) return launch_dmma<3>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st, ph);
+  if (s <= 32) return launch_dmma<4>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st, ph);
+  if (s <= 64) return launch_dmma<8>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st, ph);
+  if (s <= 136) return launch_dmma<17>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st, ph);
+  return launch_dmma<16>(Xr, nrows, row0, Xc, ncols, dp, d, V, s, B, Y, kp, gram, op.f64split, st, ph);
 }
 
 template <typename T>
 void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
                          int64_t ncols, const double* V, int s, const double* B, double* Y,
-                         bool gram, cudaStream_t st) {
-  if (nrows <= 0 || s <= 0) return;
+                         bool gram, cudaStream_t st, const ColPhase* ph) {
+  if (nrows <= 0 || s <= 0) {
+    if (ph && ph->ready) WGP_CUDA(cudaStreamWaitEvent(st, ph->ready, 0));
+    return;
+  }
   TimedScope ts_(sizeof(T) == 8 ? "kmatvec_f64" : "kmatvec_f32", st);
   if constexpr (sizeof(T) == 8) {
     static const bool simt = getenv("WGP_F64_SIMT") && atoi(getenv("WGP_F64_SIMT")) != 0;
     if (!simt) {
       return launch_f64(op, reinterpret_cast<const double*>(Xr), nrows, row0,
-                        reinterpret_cast<const double*>(Xc), ncols, V, s, B, Y, gram, st);
+                        reinterpret_cast<const double*>(Xc), ncols, V, s, B, Y, gram, st, ph);
     }
   }
+  if (ph && ph->ready) WGP_CUDA(cudaStreamWaitEvent(st, ph->ready, 0));  // no overlap here
   if (s <= 1) return launch_bs<T, 1>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
   if (s <= 2) return launch_bs<T, 2>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
   if (s <= 4) return launch_bs<T, 4>(op, Xr, nrows, row0, Xc, ncols, V, s, B, Y, gram, st);
@@ -352,9 +378,10 @@ void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0,
 
 template void launch_kmatvec_simt<double>(const Op&, const double*, int64_t, int64_t,
                                           const double*, int64_t, const double*, int,
-                                          const double*, double*, bool, cudaStream_t);
+                                          const double*, double*, bool, cudaStream_t,
+                                          const ColPhase*);
 template void launch_kmatvec_simt<float>(const Op&, const float*, int64_t, int64_t, const float*,
                                          int64_t, const double*, int, const double*, double*, bool,
-                                         cudaStream_t);
+                                         cudaStream_t, const ColPhase*);
 
 }  // namespace wgp

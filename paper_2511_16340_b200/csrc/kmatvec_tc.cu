@@ -92,6 +92,7 @@ struct Params {
   const __half* Vt;     // tiled V hi/lo per j tile (fp16, per-column scaled)
   const float* vscale;  // [s_pad] 2^-e_c: undo the per-column V scale
   int64_t nrows, row0, ncols;
+  int64_t col0;         // global index of column 0 of this launch (diagonal detection)
   int ntiles;           // ceil(ncols / BJ)
   int tiles_per_split;  // j tiles per CTA along grid.y (2-D decomposition)
   int ch;               // j tiles per accumulation chunk
@@ -267,7 +268,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&y_full[i], 1);
+#ifdef WGP_DRAIN_SETS01
       ptx::mbar_init(&y_free[i], 4 * (p.s_pad / 16));  // drainer warps with columns
+#else
+      ptx::mbar_init(&y_free[i], 4 * min(EPIW / 4, p.s_pad / 4));  // drainer warps with quads
+#endif
     }
     ptx::fence_mbar_init();
   }
@@ -418,24 +423,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     const int64_t grow0 = p.row0 + (int64_t)blockIdx.x * BM;
     const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
     const float kdiag = 1024.0f;              // k(x,x)/s^2 * 2^10
-    // drain share of this warp (sets 0 and 1 only): its quadrant's 32 rows x 16 accumulator
-    // columns, summed into this CTA's slice of the partials buffer [gy][s_pad/4][nrows][4]
-    // (4 columns of a row contiguous: one 16-byte vector reduction per lane and visit, a
-    // warp covering 512 contiguous bytes; L2-resident); reduce_splits scales and transposes.
-    const bool drainer = g < 4;
-    const int dc0 = (g & 3) * 16;
+    // Drain share of this warp: a list of 4-column quads of its TMEM lane quadrant's 32 rows
+    // (quad qd -> accumulator columns 4qd..4qd+3), summed into this CTA's slice of the
+    // partials buffer [gy][s_pad/4][nrows][4] (4 columns of a row contiguous: one 16-byte
+    // vector reduction per lane and visit, a warp covering 512 contiguous bytes;
+    // L2-resident); reduce_splits scales and transposes.  The quads are dealt round-robin
+    // over all six warp groups (quad = g + 6k), so every epilogue set carries a third of
+    // the drain work (WGP_DRAIN_SETS01: the earlier layout, 16 consecutive columns per group
+    // of sets 0 and 1 only).
+    const int nquads = p.s_pad / 4;
+#ifdef WGP_DRAIN_SETS01
+    const int q_base = (g & 3) * 4, q_stride = 1;
+    const int my_nq = (g < 4 && q_base < nquads) ? 4 : 0;
+#else
+    const int q_base = g, q_stride = EPIW / 4;
+    const int my_nq = g < nquads ? (nquads - 1 - g) / q_stride + 1 : 0;
+#endif
+    const bool drainer = my_nq > 0;
     const bool row_ok = lr < p.nrows;
-    const int ncol = max(0, min(16, p.s - dc0));
-    float* __restrict__ ypart =
-        p.Ypart + (((size_t)blockIdx.y * (p.s_pad / 4) + dc0 / 4) * p.nrows + lr) * 4;
+    float* __restrict__ ypart = p.Ypart + ((size_t)blockIdx.y * nquads * p.nrows + lr) * 4;
     int drained = 0;
-    // Incremental drain: a finished chunk accumulator is moved out DSTEP columns per visit
-    // (one visit after each of this warp's tiles), so the reduction traffic trickles instead
-    // of arriving as one 64-KB burst per chunk (which stalled every warp's TMEM/LSU traffic
-    // for ~2000 cycles).  Chunk d may start once the epilogue is 4 tiles into chunk d+1 (its
+    // Incremental drain: a finished chunk accumulator is moved out one quad per visit (one
+    // visit after each of this warp's tiles), so the reduction traffic trickles instead of
+    // arriving as one 64-KB burst per chunk (which stalled every warp's TMEM/LSU traffic for
+    // ~2000 cycles).  Chunk d may start once the epilogue is 4 tiles into chunk d+1 (its
     // GEMM2 long done) and must finish before GEMM2 starts chunk d+2.
-    constexpr int DSTEP = 4;
-    int dk = 0;  // columns of chunk `drained` already moved
+    int dk = 0;  // quads of chunk `drained` already moved
     // A drain visit: the accumulator load (after the chunk's y_full), its wait, and the
     // reduction into the partials.
     auto drain_issue = [&](int c, uint32_t* y) {
@@ -446,21 +459,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       }
       asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                    : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3])
-                   : "r"(tmem + lane_off + TM_Y + ya * 64 + dc0 + dk));
+                   : "r"(tmem + lane_off + TM_Y + ya * 64 + 4 * (q_base + q_stride * dk)));
     };
     auto drain_finish = [&](int c, const uint32_t* y) {
       const int ya = c & 1;
+      const int qd = q_base + q_stride * dk;
 #ifdef WGP_NO_DRAIN  // (probe builds: timing without the partial-sum reductions)
       if (false) {
 #else
-      if (row_ok && dk < ncol) {
+      if (row_ok && 4 * qd < p.s) {
 #endif
         // first chunk stores, later chunks add with fire-and-forget vector reductions
         // performed at L2 (fp32: ~50 chunk terms per sweep at C3, relative rounding ~1e-7).
         // Each address is only ever touched by this thread, and same-address operations of
         // one thread stay in program order, so the summation order (chunk 0, 1, 2, ...) is
         // deterministic.
-        float* dst = ypart + (size_t)(dk / 4) * p.nrows * 4;
+        float* dst = ypart + (size_t)qd * p.nrows * 4;
         if (c == 0)
           asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(y[0]), "r"(y[1]),
                        "r"(y[2]), "r"(y[3])
@@ -470,8 +484,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
                        "r"(y[1]), "r"(y[2]), "r"(y[3])
                        : "memory");
       }
-      dk += DSTEP;
-      if (dk >= 16) {
+      if (++dk >= my_nq) {
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&y_free[ya]);
@@ -480,7 +493,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       }
     };
     auto drain_step = [&](int c) {
-      uint32_t y[DSTEP];
+      uint32_t y[4];
       drain_issue(c, y);
       ptx::tmem_wait_ld();
       drain_finish(c, y);
@@ -488,20 +501,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     auto drain_all = [&](int c) {  // the last chunk, after the sweep
       while (drained == c) drain_step(c);
     };
-    // after the sweep: the correction accumulator, added last (the final y_full commit
-    // covers it)
+    // after the sweep: the correction accumulator's quads, added last (the final y_full
+    // commit covers it)
     auto drain_corr = [&]() {
-      uint32_t y[16];
-      ptx::tmem_ld16(tmem + lane_off + TM_C + dc0, y);
-      ptx::tmem_wait_ld();
-      if (row_ok) {
-#pragma unroll
-        for (int k = 0; k < 16; k += 4)
-          if (k < ncol)
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
-                             ypart + (size_t)(k / 4) * p.nrows * 4),
-                         "r"(y[k]), "r"(y[k + 1]), "r"(y[k + 2]), "r"(y[k + 3])
-                         : "memory");
+      for (int k = 0; k < my_nq; ++k) {
+        const int qd = q_base + q_stride * k;
+        uint32_t y[4];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3])
+                     : "r"(tmem + lane_off + TM_C + 4 * qd));
+        ptx::tmem_wait_ld();
+        if (row_ok && 4 * qd < p.s)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
+                           ypart + (size_t)qd * p.nrows * 4),
+                       "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3])
+                       : "memory");
       }
     };
     for (int t = set; t < T; t += NSET) {
@@ -510,14 +524,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       // S(t) needs GEMM1(t) <- GEMM2(t - NB) <- (if that tile opens chunk >= drained + 2) this
       // warp's share of chunk `drained`: finish it before blocking, so the pipeline can never
       // wait on a drain that is itself waiting (deadlock-free for any CH).
-      if (drainer && dc0 < p.s_pad)
+      if (drainer)
         while (drained < NCH - 1 && t - NB >= (drained + 2) * CH) drain_all(drained);
       const bool tr = lane == 0 && q == 0 && half == 0 && set == 0;
       if (tr) trace_ev(p, t, 2);
       ptx::mbar_wait(&s_full[b], bph);
       ptx::tc_fence_after();
       if (tr) trace_ev(p, t, 3);
-      const int64_t gj_base = (int64_t)(jt0 + t) * BJ + half * CPW;
+      const int64_t gj_base = p.col0 + (int64_t)(jt0 + t) * BJ + half * CPW;
       const bool diag = p.gram && gj_base < grow0 + BM && gj_base + CPW > grow0;
 #pragma unroll
       for (int h2 = 0; h2 < CPW / 16; ++h2) {
@@ -559,11 +573,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       if (lane == 0 && half == 0 && set == 0 && q == 3) trace_ev(p, t, 11);
       // (issuing this visit's accumulator load together with the next tile's first S load,
       // sharing one tcgen05.wait::ld, measured 2-4% slower at every shape)
-      if (drainer && dc0 < p.s_pad && drained < NCH - 1 && t >= (drained + 1) * CH + 4)
+      if (drainer && drained < NCH - 1 && t >= (drained + 1) * CH + 4)
         drain_step(drained);
     }
     if (warp == 0 && lane == 0) cta_ev(p, 1);
-    if (drainer && dc0 < p.s_pad) {
+    if (drainer) {
       while (drained < NCH) drain_all(drained);
       drain_corr();
     }
@@ -753,15 +767,16 @@ __global__ void split_v_kernel(const double* __restrict__ V, int64_t ncols, int 
   }
 }
 
-// Y = (sum over j-splits, fixed order) * s^2 2^-10 / scale_c + sigma^2 V_i (gram), or B - that.
+// Y = C + sgn ((sum over j-splits, fixed order) * s^2 2^-10 / scale_c + sigma^2 V_i (gram)),
+// C optional (B - H V: C = B, sgn = -1).
 // Partials are [nsplit][s_pad/4][nrows][4] fp32; a 32-row x 32-column tile is read as one
 // float4 (4 columns of a row) per thread -- a warp reads 512 contiguous bytes -- summed over
 // the splits in fp64, and transposed through shared memory so the row-major writes coalesce.
 __global__ void reduce_splits_kernel(const float* __restrict__ Ypart, int nsplit, int64_t nrows,
                                      int64_t row0, int s, int s_pad, const float* __restrict__ vscale,
                                      double out_scale, const double* __restrict__ V64,
-                                     const double* __restrict__ B64, double noise2, int gram,
-                                     double* __restrict__ Y64) {
+                                     int64_t vrow0, const double* __restrict__ C64, double sgn,
+                                     double noise2, int gram, double* __restrict__ Y64) {
   __shared__ double tile[32][33];
   const int64_t rb = (int64_t)blockIdx.x * 32;
   const int cb = blockIdx.y * 32;
@@ -793,8 +808,8 @@ __global__ void reduce_splits_kernel(const float* __restrict__ Ypart, int nsplit
     if (c < s && r < nrows) {
       const int64_t e = r * s + c;
       double acc = tile[tx][k];
-      if (gram) acc += noise2 * V64[row0 * s + e];
-      Y64[e] = B64 ? B64[e] - acc : acc;
+      if (gram) acc += noise2 * V64[vrow0 * s + e];
+      Y64[e] = C64 ? C64[e] + sgn * acc : sgn * acc;
     }
   }
 }
@@ -939,8 +954,10 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
                        DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st, int row_parts,
-                       cudaEvent_t* part_done) {
-  if (nrows <= 0 || s <= 0) return;
+                       cudaEvent_t* part_done, int64_t col0, const double* C64, double sgn) {
+  if (nrows <= 0 || s <= 0 || ncols <= 0) return;
+  const double* Cin = B64 ? B64 : C64;
+  const double csgn = B64 ? -1.0 : sgn;
   // Row parts (one RHS chunk only): the V preparation is shared, each part's rows finish
   // with their own reduce and an event, so a caller can start moving finished rows (e.g.
   // the device-to-host copy of the host API) while the next part computes.
@@ -954,19 +971,19 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
   for (int c0 = 0; c0 < s; c0 += tc::MAX_SPAD) {
     const int sc = std::min(tc::MAX_SPAD, s - c0);
     const double* Vc = V64;
-    const double* Bc = B64;
+    const double* Bc = Cin;
     double* Yc = Y64;
     if (sc != s) {  // gather this column chunk (s > 128)
       vchunk.ensure((size_t)ncols * sc);
-      ychunk.ensure((size_t)nrows * sc * (B64 ? 2 : 1));
+      ychunk.ensure((size_t)nrows * sc * (Cin ? 2 : 1));
       WGP_CUDA(cudaMemcpy2DAsync(vchunk.p, sizeof(double) * sc, V64 + c0, sizeof(double) * s,
                                  sizeof(double) * sc, ncols, cudaMemcpyDeviceToDevice, st));
-      if (B64)
-        WGP_CUDA(cudaMemcpy2DAsync(ychunk.p + (size_t)nrows * sc, sizeof(double) * sc, B64 + c0,
+      if (Cin)
+        WGP_CUDA(cudaMemcpy2DAsync(ychunk.p + (size_t)nrows * sc, sizeof(double) * sc, Cin + c0,
                                    sizeof(double) * s, sizeof(double) * sc, nrows,
                                    cudaMemcpyDeviceToDevice, st));
       Vc = vchunk.p;
-      Bc = B64 ? ychunk.p + (size_t)nrows * sc : nullptr;
+      Bc = Cin ? ychunk.p + (size_t)nrows * sc : nullptr;
       Yc = ychunk.p;
     }
     const int s_pad = ((sc + 15) / 16) * 16;
@@ -996,6 +1013,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     prm.nrows = nrows;
     prm.row0 = row0;
     prm.ncols = ncols;
+    prm.col0 = col0;
     prm.ntiles = ntiles;
     static const int forced_ch = getenv("WGP_TC_CH") ? atoi(getenv("WGP_TC_CH")) : 0;
     prm.ch = forced_ch > 0 ? forced_ch : tc::CH_DEFAULT;
@@ -1057,7 +1075,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     {
       tc::reduce_splits_kernel<<<dim3((unsigned)((nrows_p + 31) / 32), (sc + 31) / 32), 256, 0, st>>>(
           reinterpret_cast<const float*>(ysplit.p), gy, nrows_p, row0 + pa, sc, s_pad, sc_down, prm.out_scale, Vc,
-          Bc ? Bc + pa * sc : nullptr, kp.noise2, gram ? 1 : 0, Yc + pa * sc);
+          row0 + pa - col0, Bc ? Bc + pa * sc : nullptr, csgn, kp.noise2, gram ? 1 : 0, Yc + pa * sc);
       WGP_CUDA(cudaGetLastError());
     }
     if (trace_path) {

@@ -162,6 +162,39 @@ int launch_kmatvec_parts(Op& op, const double* V, double* Y, int s, cudaStream_t
   return 1;
 }
 
+void launch_kmatvec_overlap(Op& op, const double* B, const double* V, double* Y, int s,
+                            cudaEvent_t gathered, cudaStream_t st) {
+  if (!gathered) return dispatch(op, B, V, Y, s, st);
+  int64_t r0, r1;
+  op.local_rows(&r0, &r1);
+  if (op.tensor() && tc_supported(op.dim, op.precision)) {
+    // local diagonal block (gram: sigma^2 V and the exact diagonal), then, once V is
+    // complete, the columns before and after the slot accumulated into Y
+    ensure_tc_operands(op, st);
+    const size_t rb = (size_t)tc_k1(op.dim, op.precision, op.tc_f16) * (op.tc_f16 ? 2 : 4);
+    const char* XB = reinterpret_cast<const char*>(op.XB.p);
+    launch_kmatvec_tc(op, op.XA.p, reinterpret_cast<const float*>(XB + r0 * rb), r1 - r0, r0, r1 - r0,
+                      V + r0 * s, s, B, Y, true, op.vt, op.vchunk, op.ychunk, op.ysplit, st, 1, nullptr, r0);
+    WGP_CUDA(cudaStreamWaitEvent(st, gathered, 0));
+    const double sg = B ? -1.0 : 1.0;
+    launch_kmatvec_tc(op, op.XA.p, op.XB.p, r1 - r0, r0, r0, V, s, nullptr, Y, false, op.vt, op.vchunk,
+                      op.ychunk, op.ysplit, st, 1, nullptr, 0, Y, sg);
+    launch_kmatvec_tc(op, op.XA.p, reinterpret_cast<const float*>(XB + r1 * rb), r1 - r0, r0, op.n - r1,
+                      V + r1 * s, s, nullptr, Y, false, op.vt, op.vchunk, op.ychunk, op.ysplit, st, 1,
+                      nullptr, r1, Y, sg);
+  } else if (op.f64()) {
+    ColPhase ph;
+    ph.c0 = r0;
+    ph.c1 = r1;
+    ph.ready = gathered;
+    launch_kmatvec_simt<double>(op, op.X64.p + r0 * op.dpad, r1 - r0, r0, op.X64.p, op.n, V, s, B, Y,
+                                true, st, &ph);
+  } else {
+    WGP_CUDA(cudaStreamWaitEvent(st, gathered, 0));
+    dispatch(op, B, V, Y, s, st);
+  }
+}
+
 // Y (this rank's rows) = H V, V full n x s (fp64 row-major).
 void launch_kmatvec_full(Op& op, const double* V, double* Y, int s, cudaStream_t st) {
   dispatch(op, nullptr, V, Y, s, st);

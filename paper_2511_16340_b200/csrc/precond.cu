@@ -221,6 +221,73 @@ __global__ void __launch_bounds__(256) chunk_atb_kernel(const double* __restrict
     }
 }
 
+// Narrow right-hand sides (s <= 8): the same partials as chunk_atb_kernel -- one fma chain per
+// output over the chunk's rows in order, so the bits do not depend on which kernel ran -- with
+// one thread per (a, column) instead of 4 x 4 register tiles that would leave all but s of
+// every 64 output columns idle.  Block = 128 a values (k <= 128 per block), grid.y = s.
+__global__ void __launch_bounds__(128) chunk_atb_narrow_kernel(const double* __restrict__ A, int lda,
+                                                               int ka, const double* __restrict__ B,
+                                                               int ldb, int kb, int64_t n,
+                                                               double* __restrict__ part) {
+  const int64_t r0 = (int64_t)blockIdx.x * kChunkRows;
+  const int64_t r1 = min(n, r0 + (int64_t)kChunkRows);
+  const int a = blockIdx.z * 128 + threadIdx.x, c = blockIdx.y;
+  if (a >= ka) return;
+  double acc = 0.0;
+  int64_t i = r0;
+  for (; i + 8 <= r1; i += 8) {
+    double av[8], bv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      av[u] = A[(i + u) * lda + a];
+      bv[u] = B[(i + u) * ldb + c];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = fma(av[u], bv[u], acc);
+  }
+  for (; i < r1; ++i) acc = fma(A[i * lda + a], B[i * ldb + c], acc);
+  part[(int64_t)blockIdx.x * ka * kb + (int64_t)a * kb + c] = acc;
+}
+
+// Narrow right-hand sides: z = (r - M t) / shift with one thread per row computing all s
+// (<= 8) columns -- each output one fma chain over a in order, as woodbury_tile_kernel.
+template <int SC>
+__global__ void __launch_bounds__(128) woodbury_narrow_kernel(const double* __restrict__ M, int kpad,
+                                                              int k, const double* __restrict__ R,
+                                                              int64_t ld, const double* __restrict__ t,
+                                                              int s, int64_t n, double inv_shift,
+                                                              double* __restrict__ Z) {
+  constexpr int AT = 32;
+  __shared__ double sM[128][AT + 1], sT[AT][SC];
+  const int64_t rb = (int64_t)blockIdx.x * 128;
+  const int64_t i = rb + threadIdx.x;
+  double acc[SC];
+#pragma unroll
+  for (int v = 0; v < SC; ++v) acc[v] = 0.0;
+  for (int a0 = 0; a0 < k; a0 += AT) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 128 * AT; e += 128) {
+      const int r = e / AT, a = e % AT;
+      sM[r][a] = (rb + r < n && a0 + a < k) ? M[(rb + r) * kpad + a0 + a] : 0.0;
+    }
+    for (int e = threadIdx.x; e < AT * SC; e += 128) {
+      const int a = e / SC, c = e % SC;
+      sT[a][c] = (a0 + a < k && c < s) ? t[(int64_t)(a0 + a) * s + c] : 0.0;
+    }
+    __syncthreads();
+    const int na = min(AT, k - a0);
+    for (int a = 0; a < na; ++a) {
+      const double m = sM[threadIdx.x][a];
+#pragma unroll
+      for (int v = 0; v < SC; ++v) acc[v] = fma(m, sT[a][v], acc[v]);
+    }
+  }
+  if (i >= n) return;
+#pragma unroll
+  for (int v = 0; v < SC; ++v)
+    if (v < s) Z[i * ld + v] = (R[i * ld + v] - acc[v]) * inv_shift;
+}
+
 __global__ void sum_partials_kernel(const double* __restrict__ part, int np, int count,
                                     double* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
@@ -468,16 +535,27 @@ void precond_apply(const Op& op, const PrecondDev& pd, const T* R, T* Z, int s, 
   const int nch = ceil_div(pd.n, kChunkRows);
   const int c0 = (int)(pd.r0 / kChunkRows);
   // t = M^T r: chunk partials (fixed order, world-size independent), then summed
-  if (nl > 0)
+  if (nl > 0 && s <= 8)
+    chunk_atb_narrow_kernel<<<dim3(ceil_div(nl, kChunkRows), s, ceil_div(k, 128)), 128, 0, st>>>(
+        M, (int)pd.kpad, k, R, s, s, nl, work_part + (int64_t)c0 * k * s);
+  else if (nl > 0)
     chunk_atb_kernel<<<dim3(ceil_div(nl, kChunkRows), ceil_div(k, 64), ceil_div(s, 64)), 256, 0, st>>>(
         M, (int)pd.kpad, k, R, s, s, nl, work_part + (int64_t)c0 * k * s);
   WGP_CUDA(cudaGetLastError());
   dist_allgather_chunks(*op.ctx, work_part, pd.n, (int64_t)k * s, st);
   sum_partials_kernel<<<ceil_div((int64_t)k * s, 256), 256, 0, st>>>(work_part, nch, k * s, work_t);
   // z = (r - M t) / shift
-  if (nl > 0)
+  if (nl > 0 && s <= 8) {
+    const dim3 g(ceil_div(nl, 128));
+    const double is = 1.0 / pd.shift;
+    if (s <= 1) woodbury_narrow_kernel<1><<<g, 128, 0, st>>>(M, (int)pd.kpad, k, R, s, work_t, s, nl, is, Z);
+    else if (s <= 2) woodbury_narrow_kernel<2><<<g, 128, 0, st>>>(M, (int)pd.kpad, k, R, s, work_t, s, nl, is, Z);
+    else if (s <= 4) woodbury_narrow_kernel<4><<<g, 128, 0, st>>>(M, (int)pd.kpad, k, R, s, work_t, s, nl, is, Z);
+    else woodbury_narrow_kernel<8><<<g, 128, 0, st>>>(M, (int)pd.kpad, k, R, s, work_t, s, nl, is, Z);
+  } else if (nl > 0) {
     woodbury_tile_kernel<<<dim3(ceil_div(nl, 64), ceil_div(s, 64)), 256, 0, st>>>(
         M, (int)pd.kpad, k, R, s, work_t, s, nl, 1.0 / pd.shift, Z);
+  }
   WGP_CUDA(cudaGetLastError());
 }
 

@@ -339,15 +339,18 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
   for (int k = 1; k <= cfg.max_iters;) {
     const int nb = std::min(kb, cfg.max_iters - k + 1);
     const auto t_block = std::chrono::steady_clock::now();
+    cudaEvent_t vg = nullptr;  // all-gather of the updated v (sharded)
     for (int j = 0; j < nb; ++j) {
-      dist_allgather_rows(ctx, w.P.p, N, s, sizeof(T), st);  // exchange: full p for the matvec
-      launch_kmatvec_full(op, w.P.p, w.HP.p, s, st);          // Hp = H p (:162), local rows
+      // exchange: full p for the matvec, overlapped with the local diagonal block of Hp = H p
+      // (:162, local rows)
+      cudaEvent_t pg = dist_allgather_rows_begin(ctx, w.P.p, N, s, sizeof(T), st);
+      launch_kmatvec_overlap(op, nullptr, w.P.p, w.HP.p, s, pg, st);
       dots(op, w, w.Pl(), w.HP.p, st);
       cg_alpha_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, rz, active, alpha, fail);
       if (n > 0) launch_axpy_cols<T>(w.Vl(), w.Pl(), alpha, n, s, st);  // v += alpha p (:168)
-      dist_allgather_rows(ctx, w.V.p, N, s, sizeof(T), st);
+      vg = dist_allgather_rows_begin(ctx, w.V.p, N, s, sizeof(T), st);
       if (!anchored) {
-        launch_residual(op, w.B.p, w.V.p, w.R.p, s, st);  // r = b - H v (:171)
+        launch_kmatvec_overlap(op, w.B.p, w.V.p, w.R.p, s, vg, st);  // r = b - H v (:171)
         dots(op, w, w.R.p, w.R.p, st);
         resid_step_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, 1, s, bnorm, cfg.tolerance,
                                                     w.blk_rel.p + (size_t)j * s, active,
@@ -363,7 +366,7 @@ void cg_solve_batched(Op& op, const wgp_solver_config& cfg, const PrecondDev& pd
       hact[s] = *h_fail;
     } else {
       // r = r_a - H_fast d (:171 on v = v_a + d); |r| and |d| per column in one pass
-      launch_residual(op, w.RA.p, w.V.p, w.R.p, s, st);
+      launch_kmatvec_overlap(op, w.RA.p, w.V.p, w.R.p, s, vg, st);
       dots2(op, w, w.R.p, w.R.p, w.Vl(), w.Vl(), st);
       anchor_norms_kernel<<<sgrid(s), 256, 0, st>>>(w.part.p, nch, s, bnorm, rel, anc.dnorm());
       WGP_CUDA(cudaMemcpyAsync(hrel.data(), rel, sizeof(double) * s, cudaMemcpyDeviceToHost, st));

@@ -53,15 +53,29 @@ void launch_residual(Op& op, const double* B, const double* V, double* Y, int s,
 // (the anchor residuals of WGP_RESIDUAL_ANCHORED)
 void launch_residual_f64(Op& op, const double* B, const double* V, double* Y, int s,
                          cudaStream_t st);
+// Sharded matvec overlapped with the row all-gather of V: columns [c0, c1) (this rank's
+// slot) are valid on the stream at launch, the others only once `ready` has fired.
+struct ColPhase {
+  int64_t c0 = 0, c1 = 0;
+  cudaEvent_t ready = nullptr;
+};
+// Y (this rank's rows) = H V, or B - H V, with V's rows outside this rank's slot arriving
+// through `gathered` (dist_allgather_rows_begin; nullptr = V already complete): the local
+// diagonal block runs first, the rest after the event.
+void launch_kmatvec_overlap(Op& op, const double* B, const double* V, double* Y, int s,
+                            cudaEvent_t gathered, cudaStream_t st);
 template <typename T>
 void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0, const T* Xc,
                          int64_t ncols, const double* V, int s, const double* B, double* Y,
-                         bool gram, cudaStream_t st);
+                         bool gram, cudaStream_t st, const ColPhase* ph = nullptr);
+// C: Y = C + sgn (K V [+ sigma^2 V_i when gram]) on rows [row0, row0 + nrows) and columns
+// [col0, col0 + ncols) (XB, V64 already offset to col0); B64 given: C = B64, sgn = -1.
 void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64_t nrows,
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
                        DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st,
-                       int row_parts = 1, cudaEvent_t* part_done = nullptr);
+                       int row_parts = 1, cudaEvent_t* part_done = nullptr, int64_t col0 = 0,
+                       const double* C64 = nullptr, double sgn = 1.0);
 // Host-API form of the gram matvec: on tensor-core operators the rows are computed in
 // `parts` parts, part_done[p] recorded as each part's rows are final (else one part).
 // Returns the number of parts used.

@@ -54,24 +54,24 @@ __global__ void rows_to_colmajor_kernel(const T* __restrict__ src, int64_t n, in
 // Per column the chunk is 32 fixed 16-row slabs, each summed sequentially, slab sums added
 // in slab order: the order of every column's sum depends only on the row index, never on s
 // or on the other columns (solve_many must equal single-RHS solves bitwise,
-// test_solvers.cpp:397-413).  Work item = (chunk, group of up to kColsPerBlock columns), one
-// thread per (column, slab); a grid of a few resident blocks per SM walks the items, so the
-// load phase of one block overlaps the slab reduction of another and the last wave is thin.
-// Each slab is loaded in two 8-row halves (all loads of a half issued before its FMA chain):
-// 80 registers, 3 blocks of 256 threads per SM, ~200 KB of loads in flight per SM.
+// test_solvers.cpp:397-413).  Work item = (chunk, group of up to 32 columns), one thread per
+// (column, slab): a warp reads 32 consecutive columns of a row (256 contiguous bytes per fp64
+// load); one 1024-thread block per SM walks the items.  Each slab is loaded in 8-row halves
+// (4-row quarters for two dot products), all loads of a part issued before its FMA chain:
+// 16 loads in flight per thread, 128 KB per SM.
 constexpr int kSlabRows = kChunkRows / 32;
-constexpr int kColsPerBlock = 8;  // coldots: columns per work item (x 32 slabs = 256 threads)
-constexpr int kColdotsBlocksPerSM = 3;
+constexpr int kColsPerBlock = 32;  // coldots: columns per work item (x 32 slabs = 1024 threads)
 
 template <typename T, int NQ>
-__global__ void __launch_bounds__(256, kColdotsBlocksPerSM)
+__global__ void __launch_bounds__(1024, 1)
     coldots_kernel(const T* __restrict__ A0, const T* __restrict__ B0, const T* __restrict__ A1,
                    const T* __restrict__ B1, int64_t n, int s, int cb, int ngroups, int64_t items,
                    double* __restrict__ part) {
   __shared__ double red[NQ][32][kColsPerBlock];
   const int cl = threadIdx.x % cb;
   const int q = threadIdx.x / cb;  // slab
-  constexpr int H = kSlabRows / 2;
+  constexpr int NH = NQ == 1 ? 2 : 4;  // loads in flight per thread: 16 (64 registers at 1024 threads)
+  constexpr int H = kSlabRows / NH;
   for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const int64_t chunk = item / ngroups;
     const int grp = (int)(item - chunk * ngroups);
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256, kColdotsBlocksPerSM)
       const T* pb1 = B1 + i0 * s + c;
       if (i1 - i0 == kSlabRows) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NH; ++h) {
           T xa[H], xb[H], ya[NQ > 1 ? H : 1], yb[NQ > 1 ? H : 1];
 #pragma unroll
           for (int k = 0; k < H; ++k) {
@@ -266,7 +266,7 @@ void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t 
   const int cb = s < kColsPerBlock ? s : kColsPerBlock;
   const int ngroups = ceil_div(s, cb);
   const int64_t items = (int64_t)nch * ngroups;
-  const int grid = (int)std::min<int64_t>(items, (int64_t)148 * kColdotsBlocksPerSM);
+  const int grid = (int)std::min<int64_t>(items, 148);
   if (A1)
     coldots_kernel<T, 2><<<grid, cb * 32, 0, st>>>(A0, B0, A1, B1, n, s, cb, ngroups, items, part);
   else

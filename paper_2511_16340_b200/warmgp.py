@@ -44,7 +44,8 @@ EXPORTS = (
     "wgp_ctx_create", "wgp_nccl_unique_id", "wgp_ctx_create_sharded", "wgp_ctx_destroy",
     "wgp_allgather_rows_dev",
     "wgp_ctx_stream", "wgp_op_create", "wgp_op_destroy", "wgp_op_append_rows", "wgp_op_size",
-    "wgp_op_dim", "wgp_op_precision", "wgp_kmatvec", "wgp_kmatvec_dev", "wgp_residual_dev",
+    "wgp_op_dim", "wgp_op_precision", "wgp_kmatvec", "wgp_kmatvec_dev", "wgp_kmatvec_sharded_dev",
+    "wgp_residual_dev",
     "wgp_cross_matvec", "wgp_solve_many", "wgp_solve", "wgp_pivoted_cholesky", "wgp_precond_info",
     "wgp_rff_eval", "wgp_derive_seed", "wgp_rng_next_u64", "wgp_rng_uniform", "wgp_rng_normal",
     "wgp_rng_chi_square3", "wgp_rng_uniform_index", "wgp_normal_fill", "wgp_sample_prior",
@@ -149,6 +150,7 @@ def _declare(L):
         "wgp_op_last_anchor_count": (C.c_int, [P]),
         "wgp_kmatvec": (C.c_int, [P, P, I64, C.c_int, P, I64]),
         "wgp_kmatvec_dev": (C.c_int, [P, P, P, C.c_int, P]),
+        "wgp_kmatvec_sharded_dev": (C.c_int, [P, P, P, C.c_int, P]),
         "wgp_residual_dev": (C.c_int, [P, P, P, P, C.c_int, P]),
         "wgp_axpy_cols_dev": (C.c_int, [P, P, P, P, I64, C.c_int, P]),
         "wgp_xpby_cols_dev": (C.c_int, [P, P, P, P, P, I64, C.c_int, P]),
@@ -412,6 +414,12 @@ class KernelOperator:
     def kmatvec_dev(self, dV_ptr: int, dY_ptr: int, s: int, stream: int = 0):
         _check(lib().wgp_kmatvec_dev(self._h, C.c_void_p(dV_ptr), C.c_void_p(dY_ptr), s,
                                      C.c_void_p(stream) if stream else None))
+
+    def kmatvec_sharded_dev(self, dV_ptr: int, dY_ptr: int, s: int, stream: int = 0):
+        """Row-sharded H V: dV the padded full-row buffer with this rank's slot current; the
+        slots are all-gathered while the local diagonal block computes; dY this rank's rows."""
+        _check(lib().wgp_kmatvec_sharded_dev(self._h, C.c_void_p(dV_ptr), C.c_void_p(dY_ptr), s,
+                                             C.c_void_p(stream) if stream else None))
 
     def residual_dev(self, dB_ptr: int, dV_ptr: int, dY_ptr: int, s: int, stream: int = 0):
         _check(lib().wgp_residual_dev(self._h, C.c_void_p(dB_ptr), C.c_void_p(dV_ptr),

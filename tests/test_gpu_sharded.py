@@ -7,8 +7,11 @@ Cholesky (per-pivot all-gather + broadcast), CG/SGD/AP's local updates -- is the
 NCCL world runs.
 
 The fp64 path is bit-identical to world 1 for every world size (fixed 512-row reduction
-chunks summed in chunk order; fixed 4096-column matvec splits).  The tensor-core path's
-column splits follow each rank's row count, so it is compared within tolerance."""
+chunks summed in chunk order; matvec column splits that depend on the column count only).
+The sharded CG's matvecs overlap the row all-gather with the local diagonal block: on the
+fp64 path the splits inside the local slot run first and all splits are summed as in one
+launch (still bit-identical); the tensor-core path runs the diagonal block and the remote
+column ranges as separate launches, so it is compared within tolerance."""
 import threading
 
 import numpy as np
@@ -81,16 +84,30 @@ def test_sharded_f64_bitwise_equals_single(W, world, n, name, kw):
             assert h == hr
 
 
-def test_sharded_tensor_core_cg_close(W):
+@pytest.mark.parametrize("world,resid", [(2, "direct"), (3, "direct"), (2, "anchored")])
+def test_sharded_tensor_core_cg_close(W, world, resid):
     hyp = W.KernelHyperparams(1.0, 1.0, 0.5, W.MATERN32)
     X, B, U1 = problem(6000, 8, 4, seed=5)
     inits = [W.Initialization.cold()] * 4
-    cfg = W.SolverConfig(tolerance=1e-6, max_iters=300, precond_rank=50, precond_shift=0.25)
-    ref = solve(W, W.default_context(), hyp, X, B, inits, cfg, W.F32_3XTF32)
-    got = run_world(W, 2, lambda ctx, r: solve(W, ctx, hyp, X, B, inits, cfg, W.F32_3XTF32))
+    # the direct fp32 residual floors near 1e-6 on this system, so the direct
+    # form is run to 1e-4 and the anchored form (fp64 true residual) to 1e-7
+    mode = W.RESIDUAL_DIRECT if resid == "direct" else W.RESIDUAL_ANCHORED
+    tol = 1e-4 if resid == "direct" else 1e-7
+    cfg = W.SolverConfig(tolerance=tol, max_iters=300, precond_rank=50, precond_shift=0.25)
+
+    def run(ctx):
+        op = W.KernelOperator(hyp, X, precision=W.F32_3XTF32, ctx=ctx, residual=mode)
+        res = W.solve_many(op, B, inits, cfg)
+        assert all(r.converged for r in res)
+        return np.column_stack([r.v for r in res]), [r.iterations for r in res], None
+
+    ref = run(W.default_context())
+    got = run_world(W, world, lambda ctx, r: run(ctx))
     for V, its, _ in got:
-        assert all(abs(a - b) <= 1 for a, b in zip(its, ref[1])), (its, ref[1])
-        assert np.linalg.norm(V - ref[0]) <= 1e-5 * np.linalg.norm(ref[0])
+        # the phases (diagonal block, remote column ranges) change the fp32 summation order,
+        # which moves CG's counts to tolerance by a couple of iterations either way
+        assert all(abs(a - b) <= 2 for a, b in zip(its, ref[1])), (its, ref[1])
+        assert np.linalg.norm(V - ref[0]) <= 10 * tol * np.linalg.norm(ref[0])
 
 
 def test_loopback_allgather_rows(W):
