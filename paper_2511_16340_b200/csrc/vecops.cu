@@ -7,7 +7,7 @@
 // scalar-step kernels (solver_kernels.cu) then add the chunks in index order.
 #include <type_traits>
 
-#include "common.cuh"
+#include "solvers.h"
 
 namespace wgp {
 namespace {
@@ -142,8 +142,17 @@ __global__ void __launch_bounds__(256) chunk_sum_kernel(const double* __restrict
     const int m = min(2048, nch - base);
     for (int q = threadIdx.x; q < m; q += blockDim.x) buf[q] = part[(int64_t)(base + q) * s + c];
     __syncthreads();
-    if (threadIdx.x == 0)
-      for (int q = 0; q < m; ++q) acc += buf[q];
+    if (threadIdx.x == 0) {
+      int q = 0;
+      for (; q + 8 <= m; q += 8) {  // shared loads 8 ahead of the ordered adds
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = buf[q + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += v[u];
+      }
+      for (; q < m; ++q) acc += buf[q];
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0) out[c] = acc;
@@ -267,6 +276,7 @@ void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t 
   const int ngroups = ceil_div(s, cb);
   const int64_t items = (int64_t)nch * ngroups;
   const int grid = (int)std::min<int64_t>(items, 148);
+  TimedScope ts_("coldots", st);
   if (A1)
     coldots_kernel<T, 2><<<grid, cb * 32, 0, st>>>(A0, B0, A1, B1, n, s, cb, ngroups, items, part);
   else

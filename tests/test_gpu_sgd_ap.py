@@ -89,11 +89,15 @@ def test_warm_not_worse_than_cold_plus_one(W, O):
             assert warm.iterations <= cold.iterations + 1
 
 
+@pytest.mark.parametrize("seed", [44, 45])
 @pytest.mark.parametrize("method", [1, 2])
-def test_f32_path_sgd_ap(W, O, method):
-    h, X, H, b = system(O, 44, 1500, dim=4, ls=0.5, noise=0.5)
+def test_f32_path_sgd_ap(W, O, method, seed):
+    """North-star bar: iteration counts to tolerance within +-2% of the oracle on the fp32
+    tensor-core operator (measured spread over seeds 44-47: <= 0.6%,
+    tools/probes/gpu_sgd_ap_f32_counts.py)."""
+    h, X, H, b = system(O, seed, 1500, dim=4, ls=0.5, noise=0.5)
     kw = dict(method=method, tolerance=1e-4, max_iters=5000, learning_rate=0.005, batch_size=100, block_size=100)
     ref = O.solve(H, b, O.Initialization.cold(), O.SolverConfig(**kw))
     got = W.solve(wop(W, X, h, precision=W.F32_3XTF32), b, W.Initialization.cold(), W.SolverConfig(**kw))
-    assert got.converged
-    assert abs(got.iterations - ref.iterations) <= max(2, round(0.05 * ref.iterations)), (got.iterations, ref.iterations)
+    assert ref.converged and got.converged
+    assert abs(got.iterations - ref.iterations) <= max(2, round(0.02 * ref.iterations)), (got.iterations, ref.iterations)
