@@ -1,0 +1,136 @@
+"""The product (libwarmgp_b200.so, through the C-ABI) against outputs of the REFERENCE's own
+solver code (tests/golden/ref_golden.json; see tests/golden/make_ref_golden.py and
+tests/test_oracle_vs_reference.py for the same goldens against the CPU oracle).  Inputs are
+regenerated from the recorded seeds with the reference-pinned RNG helpers (the product's own
+host RNG reproduces the same streams).  fp64 device path; tolerances as the oracle's, with the
+device's reduction orders."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ref_golden.json")))["cases"]
+
+
+def whyp(W, h):
+    return W.KernelHyperparams(h[0], h[1], h[2], W.MATERN32)
+
+
+def test_kmatvec_and_cross_kernel_vs_reference(W, O):
+    c = GOLD["gram"]
+    X = O.uniform_inputs(c["seed"], c["n"], c["d"])
+    H = np.asarray(c["H"]).reshape(c["n"], c["n"], order="F")
+    op = W.KernelOperator(whyp(W, c["hyp"]), X, precision=W.F64)
+    V = np.asfortranarray(np.random.default_rng(0).standard_normal((c["n"], 5)))
+    np.testing.assert_allclose(op.kmatvec(V), H @ V, rtol=1e-12, atol=1e-12)
+    k = GOLD["cross_kernel"]
+    Xs = O.uniform_inputs(k["seed_star"], k["m"], c["d"])
+    np.testing.assert_allclose(W.cross_kernel(op, Xs), np.asarray(k["K"]).reshape(k["m"], c["n"], order="F"),
+                               rtol=1e-12, atol=1e-14)
+
+
+def test_append_rows_vs_reference_extend_system(W, O):
+    c = GOLD["extend_system"]
+    X1, X2 = O.uniform_inputs(c["seeds"][0], c["n1"], 3), O.uniform_inputs(c["seeds"][1], c["n2"], 3)
+    op = W.KernelOperator(whyp(W, c["hyp"]), X1, precision=W.F64)
+    op.append_rows(X2)
+    n = c["n1"] + c["n2"]
+    H = np.asarray(c["H"]).reshape(n, n, order="F")
+    np.testing.assert_allclose(op.kmatvec(np.eye(n, order="F")), H, rtol=1e-12, atol=1e-14)
+
+
+def test_pivoted_cholesky_and_preconditioner_vs_reference(W, O):
+    c = GOLD["pivoted_cholesky"]
+    X = O.uniform_inputs(c["seed"], c["n"], 3)
+    op = W.KernelOperator(whyp(W, c["hyp"]), X, precision=W.F64)
+    L = W.pivoted_cholesky(op, c["rank"])
+    assert L.shape[1] == c["achieved"]
+    np.testing.assert_allclose(L, np.asarray(c["L"]).reshape(c["n"], c["achieved"], order="F"), rtol=1e-10, atol=1e-12)
+    p = GOLD["precond_apply"]
+    r = O.gaussian_vector(p["seed_r"], c["n"])
+    for mode, z in p["z_by_mode"].items():
+        pre = W.CgPreconditioner.from_matrix(op, p["rank"], p["shift"], int(mode))
+        np.testing.assert_allclose(pre.apply(r), z, rtol=1e-9, atol=1e-12)
+
+
+def _system(W, O):
+    s = GOLD["solvers"]
+    X = O.uniform_inputs(s["seed_X"], s["n"], s["d"])
+    op = W.KernelOperator(whyp(W, s["hyp"]), X, precision=W.F64)
+    b = O.gaussian_vector(s["seed_b"], s["n"])
+    u1 = np.linalg.solve(O.gram_matrix(X[: s["warm_rows"]], O.KernelHyperparams(*s["hyp"], O.MATERN32)),
+                         b[: s["warm_rows"]])
+    return op, b, u1
+
+
+def _check(got, ref, name, count_tol):
+    assert abs(got.iterations - ref["iterations"]) <= count_tol, (name, got.iterations, ref["iterations"])
+    assert got.converged == ref["converged"], name
+    k = min(10, len(ref["history"]), len(got.residual_history))
+    np.testing.assert_allclose(got.residual_history[:k], ref["history"][:k], rtol=1e-5, err_msg=name)
+    v, vr = np.asarray(got.v), np.asarray(ref["v"])
+    assert np.linalg.norm(v - vr) <= 1e-4 * np.linalg.norm(vr) + 1e-12, name
+
+
+@pytest.mark.parametrize("name", ["cg", "cg_noise_only", "cg_rank0", "sgd", "sgd_block", "ap_greedy", "ap_cyclic"])
+@pytest.mark.parametrize("start", ["cold", "warm"])
+def test_solvers_vs_reference(W, O, name, start):
+    op, b, u1 = _system(W, O)
+    run = GOLD["solvers"]["runs"][name]
+    got = W.solve(op, b, W.Initialization.cold() if start == "cold" else W.Initialization.warm(u1),
+                  W.SolverConfig(**run["cfg"]))
+    _check(got, run[start], f"{name}/{start}", 1 if name.startswith("cg") else 0)
+    if name.startswith(("sgd", "ap")):  # one RNG stream / deterministic block order
+        np.testing.assert_allclose(got.residual_history, run[start]["history"], rtol=1e-7)
+
+
+@pytest.mark.parametrize("name", ["cg", "sgd", "ap"])
+def test_solve_many_vs_reference(W, O, name):
+    op, _, _ = _system(W, O)
+    c = GOLD["solve_many"]
+    B = np.asfortranarray(np.column_stack([O.gaussian_vector(s, op.n) for s in c["seeds_b"]]))
+    run = c["runs"][name]
+    res = W.solve_many(op, B, [W.Initialization.cold()] * 3, W.SolverConfig(**run["cfg"]))
+    V = np.asarray(run["V"]).reshape(op.n, 3, order="F")
+    for i, r in enumerate(res):
+        _check(r, {"iterations": run["iterations"][i], "converged": run["converged"][i],
+                   "history": run["history"][i], "v": V[:, i]}, f"{name}[{i}]", 1 if name == "cg" else 0)
+
+
+def test_error_semantics_vs_reference(W, O):
+    op, b, _ = _system(W, O)
+    z = GOLD["zero_rhs"]
+    got = W.solve(op, np.zeros(op.n), W.Initialization.cold(), W.SolverConfig(method=0, tolerance=1e-6, max_iters=50))
+    assert got.iterations == z["iterations"] == 0 and got.residual_history == z["history"] == [0.0]
+    assert got.converged
+    d = GOLD["sgd_divergence"]
+    with pytest.raises(W.DivergenceError) as e:
+        W.solve(op, b, W.Initialization.cold(), W.SolverConfig(**d["cfg"]))
+    assert e.value.iterations == d["iterations"]
+    rr = GOLD["relative_residual"]
+    v = np.asarray(GOLD["solvers"]["runs"]["cg"]["cold"]["v"])
+    assert W.relative_residual(op, v, b) == pytest.approx(rr["value"], rel=1e-9)
+
+
+def test_sampling_vs_reference(W, O):
+    s = GOLD["sampling"]
+    h = whyp(W, s["hyp"])
+    F, d = s["F"], s["dim"]
+    p = W.sample_prior(h, d, F, s["seed"])
+    np.testing.assert_array_equal(p.frequencies, np.asarray(s["frequencies"]).reshape(F, d, order="F"))
+    np.testing.assert_array_equal(p.phases, s["phases"])
+    np.testing.assert_array_equal(p.amplitudes, s["amplitudes"])
+    Xt = O.uniform_inputs(s["seed_Xt"], 20, d)
+    Xq = O.uniform_inputs(s["seed_Xq"], 10, d)
+    op = W.KernelOperator(h, Xt, precision=W.F64)
+    np.testing.assert_allclose(W.rff_eval(op, [p], Xq)[:, 0], s["eval_prior"], rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(W.build_sample_rhs(op, p, s["rhs_noise"], s["rhs_seed"]), s["build_sample_rhs"],
+                               rtol=1e-12, atol=1e-13)
+    w = O.gaussian_vector(s["seed_w"], 20)
+    np.testing.assert_allclose(W.eval_posterior(op, [p], w, Xq)[:, 0], s["eval_posterior"], rtol=1e-12, atol=1e-13)
+    row = s["grad_posterior_at_row"]
+    g = W.grad_posterior(op, [p], w, Xq[row:row + 1], [0])[0]
+    np.testing.assert_allclose(g, s["grad_posterior"], rtol=1e-11, atol=1e-13)
