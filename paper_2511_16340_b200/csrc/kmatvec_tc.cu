@@ -66,17 +66,10 @@ constexpr int CPW = 32;        // tile columns per epilogue warp
 // 3 GEMM2.
 // (Round-robin GEMM2 issue over several warps and 4-warp epilogue sets were tried and
 // measured no faster / hung.)
-// Role 4 (warp 28, sub-partition 0) issues GEMM2's correction products K_h V_l + K_l V_h into
-// the sweep-long correction accumulator while role 3 issues the leading K_h V_h into the
-// chunk accumulators: the two write different accumulators, so they need no ordering
-// between them, and the 12 MMAs of a tile no longer queue behind one issuing thread on one
-// sub-partition (WGP_G2_SINGLE: the earlier single GEMM2 issuer).
-#ifdef WGP_G2_SINGLE
+// (Splitting GEMM2 over two issuing warps -- the leading product on role 3, the correction
+// products on a fifth role warp, each with its own accumulators -- measured 2-7% slower: the
+// MMAs of both issuers share one tensor pipe and GEMM1 then waits on two commits.)
 constexpr int NROLE = 4;
-#else
-constexpr int NROLE = 5;
-#endif
-constexpr int NG2 = NROLE - 3;  // GEMM2 issuing threads (commits per tile on b_free / v_empty)
 constexpr int NTHREADS = 32 * (NROLE + EPIW);  // role warps + epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
 constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (drained after each)
@@ -269,14 +262,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     }
     for (int i = 0; i < NSV; ++i) {
       ptx::mbar_init(&v_full[i], 1);
-      ptx::mbar_init(&v_empty[i], NG2);
+      ptx::mbar_init(&v_empty[i], 1);
     }
     ptx::mbar_init(xa_full, 1);
     ptx::mbar_init(c_full, 1);
     for (int i = 0; i < MAX_NB; ++i) {
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&k_full[i], SETW);
-      ptx::mbar_init(&b_free[i], NG2);
+      ptx::mbar_init(&b_free[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&y_full[i], 1);
@@ -337,7 +330,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         __syncwarp();
       }
     }
-  } else if (role == 1 || role == 3 || role == 4) {
+  } else if (role == 1 || role == 3) {
     // ------------------------------------------------------------ MMA issuers
     // tcgen05.mma issue blocks for about the instruction's execution time, so one thread
     // cannot keep two dependent streams fed.  Role 1 issues GEMM1 (distance tiles) and role 3
@@ -375,8 +368,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         if (++b1 == NB) { b1 = 0; phb1 ^= 1; }
       }
     } else {
-      const bool corr = NG2 == 1 || role == 4;  // issues the correction products
-      const bool lead = NG2 == 1 || role == 3;  // issues the leading product (chunk accumulators)
       const uint32_t idesc2 = ptx::idesc_f16(BM, p.s_pad);
       // fp16 V tile: rows c (N) in 8-row groups, K = 64 j in 8-element (16 B) chunks
       const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sV), 128, (BJ / 8) * 128);
@@ -387,41 +378,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       for (int t = 0; t < T; ++t) {
         const int ya = c & 1;
         const bool first = pos == 0, last = t == T - 1 || pos == CH - 1;
-        if (lead && first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
-        if (lane == 0 && lead) trace_ev(p, t, 13);
+        if (first && c >= 2) ptx::mbar_wait(&y_free[ya], ((c >> 1) - 1) & 1);
+        if (lane == 0) trace_ev(p, t, 13);
         ptx::mbar_wait(&v_full[st2], ph2);
-        if (lane == 0 && lead) trace_ev(p, t, 9);
+        if (lane == 0) trace_ev(p, t, 9);
         ptx::mbar_wait(&k_full[b2], phb2);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
-          if (lead) trace_ev(p, t, 1);
+          trace_ev(p, t, 1);
           const uint64_t dVh = dV0 + v_step * st2;
           const uint64_t dVl = dVh + vlo_step;
           const uint32_t yacc = tmem + TM_Y + ya * 64;
           const uint32_t ycor = tmem + TM_C;
           // K layout in the buffer: per 16 j, [hi (8 packed cols) | lo (8 packed cols)]
           const uint32_t kb = tmem + b2 * 64;
-          if (lead) {
 #pragma unroll
-            for (int ks = 0; ks < BJ / 16; ++ks)
-              ptx::mma_f16_ts(yacc, kb + ks * 16, dVh + 16 * ks, idesc2, (!first || ks > 0) ? 1u : 0u);
-          }
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(yacc, kb + ks * 16, dVh + 16 * ks, idesc2, (!first || ks > 0) ? 1u : 0u);
 #ifndef WGP_NO_CORR  // (probe builds: timing without the correction products)
-          if (corr) {
 #pragma unroll
-            for (int ks = 0; ks < BJ / 16; ++ks)
-              ptx::mma_f16_ts(ycor, kb + ks * 16, dVl + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(ycor, kb + ks * 16, dVl + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
 #pragma unroll
-            for (int ks = 0; ks < BJ / 16; ++ks)
-              ptx::mma_f16_ts(ycor, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);
-          }
+          for (int ks = 0; ks < BJ / 16; ++ks)
+            ptx::mma_f16_ts(ycor, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);
 #endif
-          if (lead) trace_ev(p, t, 10);
+          trace_ev(p, t, 10);
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
-          if (lead && last) ptx::mma_commit(&y_full[ya]);
-          if (corr && t == T - 1) ptx::mma_commit(c_full);
-          if (lead) trace_ev(p, t, 12);
+          if (last) ptx::mma_commit(&y_full[ya]);
+          if (t == T - 1) ptx::mma_commit(c_full);  // the correction accumulator is final
+          trace_ev(p, t, 12);
         }
         __syncwarp();
         if (++st2 == NSV) { st2 = 0; ph2 ^= 1; }
