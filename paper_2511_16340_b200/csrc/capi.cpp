@@ -431,10 +431,11 @@ wgp_status wgp_kmatvec(wgp_op* op, const double* V, int64_t ldv, int s, double* 
     WGP_CUDA(cudaMemcpy2DAsync(stage, sizeof(double) * n, V, sizeof(double) * ldv,
                                sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
     launch_colmajor_to_rows(stage, n, n, s, dV, true, st);
-    // the rows are computed in two parts; the first part's rows are transposed and copied
-    // back on the copy stream while the second part computes
+    // the rows are computed in Ctx::kHostParts parts; each finished part's rows are
+    // transposed and copied back on the copy stream while the next parts compute, so only the
+    // last part's copy is exposed
     Ctx& c = *op->ctx;
-    const int parts = launch_kmatvec_parts(*op, dV, dY, s, st, 2, c.part_ev);
+    const int parts = launch_kmatvec_parts(*op, dV, dY, s, st, Ctx::kHostParts, c.part_ev);
     if (parts == 1) {
       launch_rows_to_colmajor(dY, n, s, stage, n, true, st);
       WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage, sizeof(double) * n,

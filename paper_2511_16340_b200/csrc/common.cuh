@@ -136,7 +136,8 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // host-API result copies overlapping compute
-  cudaEvent_t part_ev[2] = {nullptr, nullptr};
+  static constexpr int kHostParts = 4;  // row parts of the host-buffer matvec (copy overlap)
+  cudaEvent_t part_ev[kHostParts] = {};
   // sharded operators: the row all-gather runs on comm_stream while the compute stream works
   // on the local diagonal block (comm_ev[0]: slot ready, comm_ev[1]: gather complete)
   cudaStream_t comm_stream = nullptr;

@@ -25,10 +25,11 @@
 //          Y * s^2 / (2^10 * scale_c) + sigma_n^2 V_i (or B - that: the true residual of
 //          solvers.cpp:171) as fp64.
 //
-// Warp roles (28 warps): 24 = XB bulk-copy producer (TMA engine, UBLKCP) + XA load,
-// 25 = GEMM1 issuer, 26 = V bulk-copy producer + TMEM allocator, 27 = GEMM2 issuer (whole
-// warps run the schedules, one elected lane issues), 0..23 = epilogue: three sets of 8 warps
-// taking j tiles round-robin (2 warps per TMEM lane quadrant, 32 columns each).  Pipelines:
+// Warp roles (32 warps): 28 = XB bulk-copy producer (TMA engine, UBLKCP) + XA load,
+// 29 = GEMM1 issuer, 30 = V bulk-copy producer + TMEM allocator, 31 = GEMM2 issuer (whole
+// warps run the schedules, one elected lane issues), 24..27 = drain warps (one per TMEM lane
+// quadrant), 0..23 = epilogue: three sets of 8 warps taking j tiles round-robin (2 warps per
+// TMEM lane quadrant, 32 columns each).  Pipelines:
 // smem rings of XB_j (NSX) and V_j hi/lo (NSV); a ring of NB TMEM tile buffers (S written
 // by GEMM1, overwritten in place by K for GEMM2); mbarriers + tcgen05.commit.
 #include <cuda_fp16.h>
@@ -70,7 +71,11 @@ constexpr int CPW = 32;        // tile columns per epilogue warp
 // products on a fifth role warp, each with its own accumulators -- measured 2-7% slower: the
 // MMAs of both issuers share one tensor pipe and GEMM1 then waits on two commits.)
 constexpr int NROLE = 4;
-constexpr int NTHREADS = 32 * (NROLE + EPIW);  // role warps + epilogue warps
+// Four drain warps (one per TMEM lane quadrant, warps EPIW..EPIW+3) move each finished chunk
+// accumulator into the partials, so the epilogue sets never drain (with the drain visits
+// spread over the epilogue sets instead: 2.6% (C3) to 4.2% (C4-shape) slower).
+constexpr int NDRAIN = 4;
+constexpr int NTHREADS = 32 * (NROLE + NDRAIN + EPIW);  // role + drain + epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
 constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (drained after each)
 // TMEM (512 columns): a ring of NB = 5 64-column tile buffers [0, 320), two 64-column chunk
@@ -84,7 +89,11 @@ constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (drained a
 // partials.  Measured at the C3 shape (tools/probes/gpu_probe_ch_c3.py, vs the fp64
 // operator): CH = 16 -> 1.4e-6 (random V) / 5.8e-6 (positive V); 32 -> 2.6e-6 / 1.2e-5;
 // 64 -> 4.9e-6 / 2.5e-5, each doubling ~1-2% faster.  WGP_TC_CH overrides.
+#ifdef WGP_NB4  // (probe builds: four TMEM tile buffers)
+constexpr int MAX_NB = 4;
+#else
 constexpr int MAX_NB = 5;
+#endif
 constexpr int TRW = 14;  // trace slots per tile
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
 
@@ -215,11 +224,11 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
 __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NSX, int NSV) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Epilogue warps 0..EPIW-1, role warps EPIW..EPIW+3 (role r on SM sub-partition r): the
-  // issue arbiter favours the highest warp id, so the producers and MMA issuers -- a few
-  // instructions per tile on the critical path -- win the issue slot over the map warps
-  // they share a sub-partition with.
-  const int role = warp - EPIW;  // < 0 for epilogue warps
+  // Epilogue warps 0..EPIW-1, drain warps EPIW..EPIW+3, role warps EPIW+4..EPIW+7 (role r on
+  // SM sub-partition r): the issue arbiter favours the highest warp id, so the producers and
+  // MMA issuers -- a few instructions per tile on the critical path -- win the issue slot over
+  // the map warps they share a sub-partition with.
+  const int role = warp - EPIW - NDRAIN;  // < 0 for epilogue (and drain) warps
   const uint32_t ESZ = p.g1f16 ? 2 : 4;     // GEMM1 operand element bytes
   const uint32_t XA_BYTES = BM * p.K1 * ESZ;
   const uint32_t XB_BYTES = BJ * p.K1 * ESZ;
@@ -237,7 +246,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* k_full = s_full + MAX_NB;     // [MAX_NB] epilogue -> GEMM2 (8 arrivals)
   uint64_t* b_free = k_full + MAX_NB;     // [MAX_NB] GEMM2 -> GEMM1
   uint64_t* y_full = b_free + MAX_NB;     // [2] chunk accumulator done (GEMM2 commit)
-  uint64_t* y_free = y_full + 2;          // [2] chunk accumulator drained (16 warp arrivals)
+  uint64_t* y_free = y_full + 2;          // [2] chunk accumulator drained (drain warps)
   uint64_t* c_full = y_free + 2;          // correction accumulator final (last commit)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_full + 1);
   constexpr int NB = MAX_NB;
@@ -273,11 +282,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&y_full[i], 1);
-#ifdef WGP_DRAIN_SETS01
-      ptx::mbar_init(&y_free[i], 4 * (p.s_pad / 16));  // drainer warps with columns
-#else
-      ptx::mbar_init(&y_free[i], 4 * min(EPIW / 4, p.s_pad / 4));  // drainer warps with quads
-#endif
+      ptx::mbar_init(&y_free[i], NDRAIN);  // chunk accumulator drained (the drain warps)
     }
     ptx::fence_mbar_init();
   }
@@ -429,111 +434,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     const int64_t grow0 = p.row0 + (int64_t)blockIdx.x * BM;
     const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
     const float kdiag = 1024.0f;              // k(x,x)/s^2 * 2^10
-    // Drain share of this warp: a list of 4-column quads of its TMEM lane quadrant's 32 rows
-    // (quad qd -> accumulator columns 4qd..4qd+3), summed into this CTA's slice of the
-    // partials buffer [gy][s_pad/4][nrows][4] (4 columns of a row contiguous: one 16-byte
-    // vector reduction per lane and visit, a warp covering 512 contiguous bytes;
-    // L2-resident); reduce_splits scales and transposes.  The quads are dealt round-robin
-    // over all six warp groups (quad = g + 6k), so every epilogue set carries a third of
-    // the drain work (WGP_DRAIN_SETS01: the earlier layout, 16 consecutive columns per group
-    // of sets 0 and 1 only).
-    const int nquads = p.s_pad / 4;
-#ifdef WGP_DRAIN_SETS01
-    const int q_base = (g & 3) * 4, q_stride = 1;
-    const int my_nq = (g < 4 && q_base < nquads) ? 4 : 0;
-#else
-    const int q_base = g, q_stride = EPIW / 4;
-    const int my_nq = g < nquads ? (nquads - 1 - g) / q_stride + 1 : 0;
-#endif
-    const bool drainer = my_nq > 0;
-    const bool row_ok = lr < p.nrows;
-    float* __restrict__ ypart = p.Ypart + ((size_t)blockIdx.y * nquads * p.nrows + lr) * 4;
-    int drained = 0;
-    // Incremental drain: a finished chunk accumulator is moved out one quad per visit (one
-    // visit after each of this warp's tiles), so the reduction traffic trickles instead of
-    // arriving as one 64-KB burst per chunk (which stalled every warp's TMEM/LSU traffic for
-    // ~2000 cycles).  Chunk d may start once the epilogue is 4 tiles into chunk d+1 (its
-    // GEMM2 long done) and must finish before GEMM2 starts chunk d+2.
-    int dk = 0;  // quads of chunk `drained` already moved
-    // A drain visit: the accumulator load (after the chunk's y_full), its wait, and the
-    // reduction into the partials.
-    auto drain_issue = [&](int c, uint32_t* y) {
-      const int ya = c & 1;
-      if (dk == 0) {
-        ptx::mbar_wait(&y_full[ya], (c >> 1) & 1);
-        ptx::tc_fence_after();
-      }
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3])
-                   : "r"(tmem + lane_off + TM_Y + ya * 64 + 4 * (q_base + q_stride * dk)));
-    };
-    auto drain_finish = [&](int c, const uint32_t* y) {
-      const int ya = c & 1;
-      const int qd = q_base + q_stride * dk;
-#ifdef WGP_NO_DRAIN  // (probe builds: timing without the partial-sum reductions)
-      if (false) {
-#else
-      if (row_ok && 4 * qd < p.s) {
-#endif
-        // first chunk stores, later chunks add with fire-and-forget vector reductions
-        // performed at L2 (fp32: ~50 chunk terms per sweep at C3, relative rounding ~1e-7).
-        // Each address is only ever touched by this thread, and same-address operations of
-        // one thread stay in program order, so the summation order (chunk 0, 1, 2, ...) is
-        // deterministic.
-        float* dst = ypart + (size_t)qd * p.nrows * 4;
-        if (c == 0)
-          asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(y[0]), "r"(y[1]),
-                       "r"(y[2]), "r"(y[3])
-                       : "memory");
-        else
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(y[0]),
-                       "r"(y[1]), "r"(y[2]), "r"(y[3])
-                       : "memory");
-      }
-      if (++dk >= my_nq) {
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&y_free[ya]);
-        dk = 0;
-        ++drained;
-      }
-    };
-    auto drain_step = [&](int c) {
-      uint32_t y[4];
-      drain_issue(c, y);
-      ptx::tmem_wait_ld();
-      drain_finish(c, y);
-    };
-    auto drain_all = [&](int c) {  // the last chunk, after the sweep
-      while (drained == c) drain_step(c);
-    };
-    // after the sweep: the correction accumulator's quads, added last (after the
-    // correction issuer's final commit)
-    auto drain_corr = [&]() {
-      ptx::mbar_wait(c_full, 0);
-      ptx::tc_fence_after();
-      for (int k = 0; k < my_nq; ++k) {
-        const int qd = q_base + q_stride * k;
-        uint32_t y[4];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3])
-                     : "r"(tmem + lane_off + TM_C + 4 * qd));
-        ptx::tmem_wait_ld();
-        if (row_ok && 4 * qd < p.s)
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
-                           ypart + (size_t)qd * p.nrows * 4),
-                       "r"(y[0]), "r"(y[1]), "r"(y[2]), "r"(y[3])
-                       : "memory");
-      }
-    };
     for (int t = set; t < T; t += NSET) {
       const int b = t % NB;                   // buffer and phase of tile t
       const uint32_t bph = (t / NB) & 1;
-      // S(t) needs GEMM1(t) <- GEMM2(t - NB) <- (if that tile opens chunk >= drained + 2) this
-      // warp's share of chunk `drained`: finish it before blocking, so the pipeline can never
-      // wait on a drain that is itself waiting (deadlock-free for any CH).
-      if (drainer)
-        while (drained < NCH - 1 && t - NB >= (drained + 2) * CH) drain_all(drained);
       const bool tr = lane == 0 && q == 0 && half == 0 && set == 0;
       if (tr) trace_ev(p, t, 2);
       ptx::mbar_wait(&s_full[b], bph);
@@ -579,15 +482,59 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       if (lane == 0) ptx::mbar_arrive(&k_full[b]);
       if (tr) trace_ev(p, t, 5);
       if (lane == 0 && half == 0 && set == 0 && q == 3) trace_ev(p, t, 11);
-      // (issuing this visit's accumulator load together with the next tile's first S load,
-      // sharing one tcgen05.wait::ld, measured 2-4% slower at every shape)
-      if (drainer && drained < NCH - 1 && t >= (drained + 1) * CH + 4)
-        drain_step(drained);
     }
     if (warp == 0 && lane == 0) cta_ev(p, 1);
-    if (drainer) {
-      while (drained < NCH) drain_all(drained);
-      drain_corr();
+  }
+  if (warp >= EPIW && warp < EPIW + NDRAIN) {
+    // ------------------------------------------------------------ drain warps
+    // Chunk c's accumulator (after its y_full) 16 columns at a time into this CTA's slice of
+    // the partials [gy][s_pad/4][nrows][4] (4 columns of a row contiguous: one 16-byte vector
+    // reduction per lane, a warp covering 512 contiguous bytes; L2-resident): the first chunk
+    // stores, later chunks add with fire-and-forget reductions performed at L2 (fp32: ~50
+    // chunk terms per sweep at C3, relative rounding ~1e-7).  Each address is only ever
+    // touched by one thread, and same-address operations of one thread stay in program order,
+    // so the summation order (chunk 0, 1, 2, ...) is deterministic.  A drain waits only on
+    // GEMM2's commits, never on the pipeline, so it cannot deadlock; it must finish before
+    // GEMM2 starts chunk c + 2 (y_free).  After the sweep: the correction accumulator.
+    const int q = warp & 3;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const int64_t lr = (int64_t)blockIdx.x * BM + q * 32 + lane;
+    const bool row_ok = lr < p.nrows;
+    const int nquads = p.s_pad / 4;
+    float* __restrict__ ypart = p.Ypart + ((size_t)blockIdx.y * nquads * p.nrows + lr) * 4;
+    auto put4 = [&](int qd, const uint32_t* y, bool store) {
+      if (!row_ok || 4 * qd >= p.s) return;
+      float* dst = ypart + (size_t)qd * p.nrows * 4;
+      if (store)
+        asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(y[0]), "r"(y[1]),
+                     "r"(y[2]), "r"(y[3]) : "memory");
+      else
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(y[0]), "r"(y[1]),
+                     "r"(y[2]), "r"(y[3]) : "memory");
+    };
+    for (int c = 0; c < NCH; ++c) {
+      const int ya = c & 1;
+      ptx::mbar_wait(&y_full[ya], (c >> 1) & 1);
+      ptx::tc_fence_after();
+      for (int c16 = 0; c16 < p.s_pad; c16 += 16) {
+        uint32_t y[16];
+        ptx::tmem_ld16(tmem + lane_off + TM_Y + ya * 64 + c16, y);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) put4(c16 / 4 + k, y + 4 * k, c == 0);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&y_free[ya]);
+    }
+    ptx::mbar_wait(c_full, 0);
+    ptx::tc_fence_after();
+    for (int c16 = 0; c16 < p.s_pad; c16 += 16) {
+      uint32_t y[16];
+      ptx::tmem_ld16(tmem + lane_off + TM_C + c16, y);
+      ptx::tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) put4(c16 / 4 + k, y + 4 * k, false);
     }
   }
   ptx::tc_fence_before();
