@@ -78,22 +78,24 @@ constexpr int NDRAIN = 4;
 constexpr int NTHREADS = 32 * (NROLE + NDRAIN + EPIW);  // role + drain + epilogue warps
 constexpr int MAX_SPAD = 64;   // RHS columns per launch (wider RHS: column chunks)
 constexpr int CH_DEFAULT = 16; // j tiles per TMEM accumulation chunk (drained after each)
-// TMEM (512 columns): a ring of NB = 5 64-column tile buffers [0, 320), two 64-column chunk
-// accumulators [320, 448) and the sweep-long correction accumulator [448, 512).  A buffer
-// holds S(t) (fp32 d^2, written by GEMM1); the epilogue loads it into registers and writes
-// K(t) back in place as packed fp16 (each warp into the 32 columns it read: 16 hi + 16 lo),
-// which GEMM2 then reads as its A operand; GEMM2's commit frees the buffer for GEMM1 of tile
-// t + NB.  The chunk accumulators alternate per chunk of CH tiles: each tcgen05.mma truncates
-// its fp32 sum (a relative bias of about -2^-25 per instruction against the running
-// accumulator), so every CH tiles the epilogue warps drain the finished accumulator into the
-// partials.  Measured at the C3 shape (tools/probes/gpu_probe_ch_c3.py, vs the fp64
-// operator): CH = 16 -> 1.4e-6 (random V) / 5.8e-6 (positive V); 32 -> 2.6e-6 / 1.2e-5;
-// 64 -> 4.9e-6 / 2.5e-5, each doubling ~1-2% faster.  WGP_TC_CH overrides.
-#ifdef WGP_NB4  // (probe builds: four TMEM tile buffers)
-constexpr int MAX_NB = 4;
-#else
-constexpr int MAX_NB = 5;
-#endif
+// TMEM (512 columns): a ring of NB = 4 64-column tile buffers [0, 256) and the accumulators
+// [256, 256 + 4 s_pad).  A buffer holds S(t) (fp32 d^2, written by GEMM1); the epilogue loads
+// it into registers and writes K(t) back in place as packed fp16 (each warp into the 32
+// columns it read: 16 hi + 16 lo), which GEMM2 then reads as its A operand; GEMM2's commit
+// frees the buffer for GEMM1 of tile t + NB.  Accumulators per chunk parity a:
+// [Y_a | C_a] adjacent, so one N = 2 s_pad MMA computes K_h [V_h | V_l] (the leading product
+// into the chunk accumulator Y_a, the first correction product into C_a; V_h and V_l tiles
+// are adjacent in shared memory) and one N = s_pad MMA adds K_l V_h into C_a: 8 MMAs per
+// tile (12 with separate products measured 1-3% slower).  Every MMA accumulates; the drain
+// warps zero the accumulators at the start and Y_a after draining it.  Each tcgen05.mma
+// truncates its fp32 sum (a relative bias of about -2^-25 per instruction against the
+// running accumulator), so Y_a covers only CH tiles before it is drained (alternating
+// parities: GEMM2 fills one while the other drains); the correction products (2^-11 of the
+// leading term) stay in C_a for the whole sweep.  Measured at the C3 shape
+// (tools/probes/gpu_probe_ch_c3.py, vs the fp64 operator): CH = 16 -> 1.4e-6 (random V) /
+// 5.8e-6 (positive V); 32 -> 2.6e-6 / 1.2e-5; 64 -> 4.9e-6 / 2.5e-5, each doubling ~1-2%
+// faster.  WGP_TC_CH overrides.
+constexpr int MAX_NB = 4;  // TMEM tile buffers (5 measured no faster)
 constexpr int TRW = 14;  // trace slots per tile
 constexpr float KSCALE_LOG2 = 10.0f;  // K stored as k/s^2 * 2^10 (fp16 normal range)
 
@@ -248,15 +250,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* y_full = b_free + MAX_NB;     // [2] chunk accumulator done (GEMM2 commit)
   uint64_t* y_free = y_full + 2;          // [2] chunk accumulator drained (drain warps)
   uint64_t* c_full = y_free + 2;          // correction accumulator final (last commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(c_full + 1);
+  uint64_t* acc_zero = c_full + 1;        // accumulators zeroed (drain warps, merged GEMM2)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_zero + 1);
   constexpr int NB = MAX_NB;
-  // TMEM: ring of NB 64-column S/K buffers [0, 320), the two chunk accumulators of the
-  // leading product Kh.Vh at TM_Y + 64 a, and one sweep-long accumulator of the correction
-  // products Kh.Vl + Kl.Vh at TM_C (2^-11 of the leading term, so its own truncation bias is
-  // negligible; keeping it out of the chunk accumulators divides their per-instruction
-  // truncation bias by three).
-  constexpr uint32_t TM_Y = 320;
-  constexpr uint32_t TM_C = 448;
+  // TMEM columns of the accumulators: [Y_0 | C_0 | Y_1 | C_1], s_pad each (see MAX_NB)
+  const uint32_t TM_ACC = 256;
+  const uint32_t AW = (uint32_t)p.s_pad;
   // this CTA's j range: tiles [jt0, jt0 + T) of the column sweep
   const int jt0 = blockIdx.y * p.tiles_per_split;
   const int T = min(p.ntiles - jt0, p.tiles_per_split);
@@ -275,6 +274,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     }
     ptx::mbar_init(xa_full, 1);
     ptx::mbar_init(c_full, 1);
+    ptx::mbar_init(acc_zero, NDRAIN);
     for (int i = 0; i < MAX_NB; ++i) {
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&k_full[i], SETW);
@@ -374,10 +374,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       }
     } else {
       const uint32_t idesc2 = ptx::idesc_f16(BM, p.s_pad);
+      const uint32_t idesc2w = ptx::idesc_f16(BM, 2 * p.s_pad);
       // fp16 V tile: rows c (N) in 8-row groups, K = 64 j in 8-element (16 B) chunks
       const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sV), 128, (BJ / 8) * 128);
       const uint64_t v_step = (uint64_t)((2 * VT_BYTES) >> 4);
-      const uint64_t vlo_step = (uint64_t)(VT_BYTES >> 4);
       int st2 = 0, b2 = 0, c = 0, pos = 0;  // V stage, TMEM buffer, chunk, tile within chunk
       uint32_t ph2 = 0, phb2 = 0;
       for (int t = 0; t < T; ++t) {
@@ -388,31 +388,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         ptx::mbar_wait(&v_full[st2], ph2);
         if (lane == 0) trace_ev(p, t, 9);
         ptx::mbar_wait(&k_full[b2], phb2);
+        if (t == 0) ptx::mbar_wait(acc_zero, 0);  // drain warps zeroed the accumulators
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           trace_ev(p, t, 1);
           const uint64_t dVh = dV0 + v_step * st2;
-          const uint64_t dVl = dVh + vlo_step;
-          const uint32_t yacc = tmem + TM_Y + ya * 64;
-          const uint32_t ycor = tmem + TM_C;
-          // K layout in the buffer: per 16 j, [hi (8 packed cols) | lo (8 packed cols)]
+          const uint32_t yacc = tmem + TM_ACC + 2 * AW * ya;
           const uint32_t kb = tmem + b2 * 64;
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks)
-            ptx::mma_f16_ts(yacc, kb + ks * 16, dVh + 16 * ks, idesc2, (!first || ks > 0) ? 1u : 0u);
-#ifndef WGP_NO_CORR  // (probe builds: timing without the correction products)
+            ptx::mma_f16_ts(yacc, kb + ks * 16, dVh + 16 * ks, idesc2w, 1u);  // [Y|C] += Kh [Vh|Vl]
 #pragma unroll
           for (int ks = 0; ks < BJ / 16; ++ks)
-            ptx::mma_f16_ts(ycor, kb + ks * 16, dVl + 16 * ks, idesc2, (t > 0 || ks > 0) ? 1u : 0u);
-#pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks)
-            ptx::mma_f16_ts(ycor, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);
-#endif
+            ptx::mma_f16_ts(yacc + AW, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);  // C += Kl Vh
           trace_ev(p, t, 10);
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
           if (last) ptx::mma_commit(&y_full[ya]);
-          if (t == T - 1) ptx::mma_commit(c_full);  // the correction accumulator is final
+          if (t == T - 1) ptx::mma_commit(c_full);  // the correction accumulators are final
           trace_ev(p, t, 12);
         }
         __syncwarp();
@@ -512,30 +505,41 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(y[0]), "r"(y[1]),
                      "r"(y[2]), "r"(y[3]) : "memory");
     };
+    const uint32_t zero16[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    for (uint32_t c16 = 0; c16 < 4 * AW; c16 += 16)  // [Y_0 | C_0 | Y_1 | C_1]
+      ptx::tmem_st16(tmem + lane_off + TM_ACC + c16, zero16);
+    ptx::tmem_wait_st();
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(acc_zero);
     for (int c = 0; c < NCH; ++c) {
       const int ya = c & 1;
+      const uint32_t ya_col = TM_ACC + 2 * AW * ya;
       ptx::mbar_wait(&y_full[ya], (c >> 1) & 1);
       ptx::tc_fence_after();
       for (int c16 = 0; c16 < p.s_pad; c16 += 16) {
         uint32_t y[16];
-        ptx::tmem_ld16(tmem + lane_off + TM_Y + ya * 64 + c16, y);
+        ptx::tmem_ld16(tmem + lane_off + ya_col + c16, y);
         ptx::tmem_wait_ld();
+        ptx::tmem_st16(tmem + lane_off + ya_col + c16, zero16);  // ready for chunk c + 2
 #pragma unroll
         for (int k = 0; k < 4; ++k) put4(c16 / 4 + k, y + 4 * k, c == 0);
       }
+      ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&y_free[ya]);
     }
     ptx::mbar_wait(c_full, 0);
     ptx::tc_fence_after();
-    for (int c16 = 0; c16 < p.s_pad; c16 += 16) {
-      uint32_t y[16];
-      ptx::tmem_ld16(tmem + lane_off + TM_C + c16, y);
-      ptx::tmem_wait_ld();
+    for (int a = 0; a < 2 && a < NCH; ++a)
+      for (int c16 = 0; c16 < p.s_pad; c16 += 16) {
+        uint32_t y[16];
+        ptx::tmem_ld16(tmem + lane_off + TM_ACC + 2 * AW * a + AW + c16, y);
+        ptx::tmem_wait_ld();
 #pragma unroll
-      for (int k = 0; k < 4; ++k) put4(c16 / 4 + k, y + 4 * k, false);
-    }
+        for (int k = 0; k < 4; ++k) put4(c16 / 4 + k, y + 4 * k, false);
+      }
   }
   ptx::tc_fence_before();
   __syncthreads();
