@@ -233,6 +233,7 @@ wgp_status wgp_ctx_create(int device, wgp_ctx** out) {
     WGP_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     WGP_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (auto& e : c->part_ev) WGP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : c->col_ev) WGP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     WGP_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
     for (auto& e : c->comm_ev) WGP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     *out = c.release();
@@ -281,6 +282,8 @@ void wgp_ctx_destroy(wgp_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto& e : c->part_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->col_ev)
     if (e) cudaEventDestroy(e);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   for (auto& e : c->comm_ev)
@@ -428,14 +431,34 @@ wgp_status wgp_kmatvec(wgp_op* op, const double* V, int64_t ldv, int s, double* 
     double* stage = (double*)op->scratch[0].p;
     double* dV = (double*)op->scratch[1].p;
     double* dY = (double*)op->scratch[2].p;
-    WGP_CUDA(cudaMemcpy2DAsync(stage, sizeof(double) * n, V, sizeof(double) * ldv,
-                               sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
-    launch_colmajor_to_rows(stage, n, n, s, dV, true, st);
-    // the rows are computed in Ctx::kHostParts parts; each finished part's rows are
-    // transposed and copied back on the copy stream while the next parts compute, so only the
-    // last part's copy is exposed
     Ctx& c = *op->ctx;
-    const int parts = launch_kmatvec_parts(*op, dV, dY, s, st, Ctx::kHostParts, c.part_ev);
+    // Tensor-core operators: V crosses in column parts (rows of V; host_col_parts: 1/8,
+    // 3/8, 1/2) on the copy stream and the columns of each part are computed as soon as it
+    // lands, so only the first part of the upload is exposed.  The rows of the result are
+    // computed in Ctx::kHostParts parts (row_part_begin: 1/2, 1/4, 3/16, 1/16); each
+    // finished part's rows are transposed and copied back on the copy stream while the next
+    // parts compute, so only the last part's copy is exposed.
+    int parts = 0;
+    if (kmatvec_colphased_ok(*op, s, Ctx::kHostParts)) {
+      int64_t cb[Ctx::kColParts + 1];
+      const int ncp = host_col_parts(n, cb);
+      WGP_CUDA(cudaEventRecord(c.col_ev[0], st));  // the stage / dV buffers are free
+      WGP_CUDA(cudaStreamWaitEvent(c.copy_stream, c.col_ev[0], 0));
+      for (int k = 0; k < ncp; ++k) {
+        const int64_t a = cb[k], rows = cb[k + 1] - a;
+        WGP_CUDA(cudaMemcpy2DAsync(stage + a, sizeof(double) * n, V + a, sizeof(double) * ldv,
+                                   sizeof(double) * rows, s, cudaMemcpyHostToDevice, c.copy_stream));
+        launch_colmajor_to_rows(stage + a, n, rows, s, dV + a * s, true, c.copy_stream);
+        WGP_CUDA(cudaEventRecord(c.col_ev[k], c.copy_stream));
+      }
+      parts = launch_kmatvec_colphased(*op, dV, dY, s, st, cb, ncp, c.col_ev, Ctx::kHostParts,
+                                       c.part_ev);
+    } else {
+      WGP_CUDA(cudaMemcpy2DAsync(stage, sizeof(double) * n, V, sizeof(double) * ldv,
+                                 sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+      launch_colmajor_to_rows(stage, n, n, s, dV, true, st);
+      parts = launch_kmatvec_parts(*op, dV, dY, s, st, Ctx::kHostParts, c.part_ev);
+    }
     if (parts == 1) {
       launch_rows_to_colmajor(dY, n, s, stage, n, true, st);
       WGP_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldy, stage, sizeof(double) * n,
@@ -443,10 +466,9 @@ wgp_status wgp_kmatvec(wgp_op* op, const double* V, int64_t ldv, int s, double* 
       WGP_CUDA(cudaStreamSynchronize(st));
       return;
     }
-    const int64_t tiles128 = (n + 127) / 128;
     for (int part = 0; part < parts; ++part) {  // same split as launch_kmatvec_tc's row parts
-      const int64_t a = std::min(n, tiles128 * part / parts * 128);
-      const int64_t b = std::min(n, tiles128 * (part + 1) / parts * 128);
+      const int64_t a = row_part_begin(n, part, parts);
+      const int64_t b = row_part_begin(n, part + 1, parts);
       WGP_CUDA(cudaStreamWaitEvent(c.copy_stream, c.part_ev[part], 0));
       if (b <= a) continue;
       launch_rows_to_colmajor(dY + a * s, b - a, s, stage + a, n, true, c.copy_stream);

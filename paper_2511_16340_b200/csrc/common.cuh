@@ -138,6 +138,8 @@ struct Ctx {
   cudaStream_t copy_stream = nullptr;  // host-API result copies overlapping compute
   static constexpr int kHostParts = 4;  // row parts of the host-buffer matvec (copy overlap)
   cudaEvent_t part_ev[kHostParts] = {};
+  static constexpr int kColParts = 4;  // max column parts of its input copy (copy overlap)
+  cudaEvent_t col_ev[kColParts] = {};
   // sharded operators: the row all-gather runs on comm_stream while the compute stream works
   // on the local diagonal block (comm_ev[0]: slot ready, comm_ev[1]: gather complete)
   cudaStream_t comm_stream = nullptr;

@@ -913,8 +913,10 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
                        DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st, int row_parts,
-                       cudaEvent_t* part_done, int64_t col0, const double* C64, double sgn) {
+                       cudaEvent_t* part_done, int64_t col0, const double* C64, double sgn,
+                       int noise_mode, const double* noiseV) {
   if (nrows <= 0 || s <= 0 || ncols <= 0) return;
+  WGP_REQUIRE(noise_mode != 1 || (noiseV && s <= tc::MAX_SPAD), "kmatvec_tc: bad noise operand");
   const double* Cin = B64 ? B64 : C64;
   const double csgn = B64 ? -1.0 : sgn;
   // Row parts (one RHS chunk only): the V preparation is shared, each part's rows finish
@@ -978,9 +980,8 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     prm.ch = forced_ch > 0 ? forced_ch : tc::CH_DEFAULT;
     for (int part = 0; part < row_parts; ++part) {
     // rows [pa, pb) of this launch, part boundaries on 128-row CTA tiles
-    const int64_t tiles128 = (nrows + tc::BM - 1) / tc::BM;
-    const int64_t pa = std::min(nrows, tiles128 * part / row_parts * tc::BM);
-    const int64_t pb = std::min(nrows, tiles128 * (part + 1) / row_parts * tc::BM);
+    const int64_t pa = row_part_begin(nrows, part, row_parts);
+    const int64_t pb = row_part_begin(nrows, part + 1, row_parts);
     const int64_t nrows_p = pb - pa;
     if (nrows_p <= 0) {
       if (part_done) WGP_CUDA(cudaEventRecord(part_done[part], st));
@@ -1032,9 +1033,14 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     }
     WGP_CUDA(cudaGetLastError());
     {
+      // sigma^2 V_i: from this launch's V rows (default), from the full V (noise_mode 1: a
+      // column-range launch whose rows' V lies outside its columns), or not at all (0)
+      const double* nv = noise_mode == 1 ? noiseV : Vc;
+      const int64_t nrow0 = noise_mode == 1 ? row0 + pa : row0 + pa - col0;
+      const int add_noise = gram && noise_mode != 0 ? 1 : 0;
       tc::reduce_splits_kernel<<<dim3((unsigned)((nrows_p + 31) / 32), (sc + 31) / 32), 256, 0, st>>>(
-          reinterpret_cast<const float*>(ysplit.p), gy, nrows_p, row0 + pa, sc, s_pad, sc_down, prm.out_scale, Vc,
-          row0 + pa - col0, Bc ? Bc + pa * sc : nullptr, csgn, kp.noise2, gram ? 1 : 0, Yc + pa * sc);
+          reinterpret_cast<const float*>(ysplit.p), gy, nrows_p, row0 + pa, sc, s_pad, sc_down, prm.out_scale, nv,
+          nrow0, Bc ? Bc + pa * sc : nullptr, csgn, kp.noise2, add_noise, Yc + pa * sc);
       WGP_CUDA(cudaGetLastError());
     }
     if (trace_path) {

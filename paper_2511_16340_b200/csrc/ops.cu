@@ -4,6 +4,8 @@
 // bo_round (thompson.cpp:403-422) for a matrix-free operator: new rows of X are
 // appended to the device copy (capacity doubling, old rows never re-uploaded) with their
 // squared norms, so the next system is ready without recomputing or storing H11.
+#include <cstdlib>
+#include <vector>
 #include "solvers.h"
 
 namespace wgp {
@@ -160,6 +162,73 @@ int launch_kmatvec_parts(Op& op, const double* V, double* Y, int s, cudaStream_t
   }
   dispatch(op, nullptr, V, Y, s, st);
   return 1;
+}
+
+namespace {
+// comma-separated cumulative sixteenths from the environment (probe overrides), else def
+std::vector<int> sixteenths(const char* env, std::vector<int> def) {
+  const char* e = getenv(env);
+  if (!e || !*e) return def;
+  std::vector<int> v;
+  for (const char* p = e; *p;) {
+    char* end = nullptr;
+    const long x = strtol(p, &end, 10);
+    if (end == p) break;
+    if (x > 0 && x < 16 && (v.empty() || x > v.back())) v.push_back((int)x);
+    p = *end == ',' ? end + 1 : end;
+  }
+  return v;
+}
+}  // namespace
+
+int64_t row_part_begin(int64_t nrows, int part, int parts) {
+  const int64_t tiles = (nrows + 127) / 128;
+  int64_t t = tiles * part / parts;
+  if (parts == Ctx::kHostParts && part > 0 && part < parts) {
+    static const std::vector<int> cuts = sixteenths("WGP_HOST_ROWCUTS", {8, 12, 15});
+    if ((int)cuts.size() == parts - 1) t = tiles * cuts[part - 1] / 16;
+  }
+  return std::min(nrows, t * 128);
+}
+
+int host_col_parts(int64_t n, int64_t* cb) {
+  static const std::vector<int> cuts = sixteenths("WGP_HOST_COLCUTS", {2, 8});
+  int ncp = 0;
+  cb[0] = 0;
+  for (int c : cuts) {
+    if (ncp + 1 >= Ctx::kColParts) break;
+    const int64_t b = n * c / 16 / 128 * 128;
+    if (b > cb[ncp]) cb[++ncp] = b;
+  }
+  cb[++ncp] = n;
+  return ncp;
+}
+
+bool kmatvec_colphased_ok(const Op& op, int s, int parts) {
+  return op.ctx->world == 1 && op.tensor() && tc_supported(op.dim, op.precision) && s <= 64 &&
+         op.n >= 2 * 128 * parts && op.n >= 16384;
+}
+
+int launch_kmatvec_colphased(Op& op, const double* V, double* Y, int s, cudaStream_t st,
+                             const int64_t* cb, int ncp, const cudaEvent_t* vready, int parts,
+                             cudaEvent_t* part_done) {
+  if (!kmatvec_colphased_ok(op, s, parts)) return 0;
+  ensure_tc_operands(op, st);
+  const size_t rb = (size_t)tc_k1(op.dim, op.precision, op.tc_f16) * (op.tc_f16 ? 2 : 4);
+  const char* XB = reinterpret_cast<const char*>(op.XB.p);
+  for (int k = 0; k < ncp; ++k) {
+    const int64_t a = cb[k], b = cb[k + 1];
+    WGP_REQUIRE(a % 128 == 0 && b > a && b <= op.n, "kmatvec_colphased: bad column parts");
+    WGP_CUDA(cudaStreamWaitEvent(st, vready[k], 0));
+    const bool last = k == ncp - 1;
+    // gram for every part (the exact diagonal wherever it falls); the noise term once, in the
+    // last part, from the complete V
+    launch_kmatvec_tc(op, op.XA.p, reinterpret_cast<const float*>(XB + a * rb), op.n, 0, b - a,
+                      V + a * s, s, nullptr, Y, true, op.vt, op.vchunk, op.ychunk, op.ysplit, st,
+                      last ? parts : 1, last ? part_done : nullptr, a, k > 0 ? Y : nullptr, 1.0,
+                      last ? 1 : 0, V);
+  }
+  return parts;
 }
 
 void launch_kmatvec_overlap(Op& op, const double* B, const double* V, double* Y, int s,

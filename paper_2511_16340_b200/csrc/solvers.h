@@ -70,17 +70,40 @@ void launch_kmatvec_simt(const Op& op, const T* Xr, int64_t nrows, int64_t row0,
                          bool gram, cudaStream_t st, const ColPhase* ph = nullptr);
 // C: Y = C + sgn (K V [+ sigma^2 V_i when gram]) on rows [row0, row0 + nrows) and columns
 // [col0, col0 + ncols) (XB, V64 already offset to col0); B64 given: C = B64, sgn = -1.
+// gram: the exact diagonal k(x, x) where global row == global column, and the noise term,
+// taken from V64's row i - col0 (noise_mode -1), from noiseV's row i (1: the full V, for a
+// column-range launch), or left out (0: another launch of the same product adds it).
 void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64_t nrows,
                        int64_t row0, int64_t ncols, const double* V64, int s, const double* B64,
                        double* Y64, bool gram, DBuf<float>& vt_scratch, DBuf<double>& vchunk,
                        DBuf<double>& ychunk, DBuf<double>& ysplit, cudaStream_t st,
                        int row_parts = 1, cudaEvent_t* part_done = nullptr, int64_t col0 = 0,
-                       const double* C64 = nullptr, double sgn = 1.0);
+                       const double* C64 = nullptr, double sgn = 1.0, int noise_mode = -1,
+                       const double* noiseV = nullptr);
 // Host-API form of the gram matvec: on tensor-core operators the rows are computed in
 // `parts` parts, part_done[p] recorded as each part's rows are final (else one part).
 // Returns the number of parts used.
 int launch_kmatvec_parts(Op& op, const double* V, double* Y, int s, cudaStream_t st, int parts,
                          cudaEvent_t* part_done);
+// First row of row part `part` of `parts` (CTA-tile aligned; part == parts gives nrows).
+// Equal parts, except the host API's four: 1/2, 1/4, 3/16, 1/16 of the rows, so each part's
+// copy-back hides under the next part's compute and the exposed last one is small
+// (WGP_HOST_ROWCUTS="a,b,c" overrides the cumulative sixteenths 8,12,15 -- probes).
+int64_t row_part_begin(int64_t nrows, int part, int parts);
+// Column parts of the host API's upload: boundaries cb[0..ncp] (multiples of 128) of the
+// cumulative shares 1/8, 1/2 (WGP_HOST_COLCUTS="a,b,..." overrides the sixteenths 2,8);
+// returns ncp (<= Ctx::kColParts).
+int host_col_parts(int64_t n, int64_t* cb);
+// The same with V arriving in column parts (host API: the host-to-device copy of part p + 1
+// overlaps the columns of part p): V rows [cb[k], cb[k + 1]) are valid after vready[k]
+// (ncp parts).  Column part k < ncp - 1 is one launch accumulating into Y; the last runs in
+// `parts` row parts recorded on part_done.  Returns the number of row parts, or 0 when the
+// operator does not take this form (then nothing is launched).
+int launch_kmatvec_colphased(Op& op, const double* V, double* Y, int s, cudaStream_t st,
+                             const int64_t* cb, int ncp, const cudaEvent_t* vready, int parts,
+                             cudaEvent_t* part_done);
+// Whether launch_kmatvec_colphased applies (world 1, tensor-core operator, s <= 64, n large)
+bool kmatvec_colphased_ok(const Op& op, int s, int parts);
 void tc_build_operands(Op& op, DBuf<float>& XA, DBuf<float>& XB, const double* center,
                        cudaStream_t st);
 int tc_k1(int dim, int precision, bool f16);

@@ -219,3 +219,31 @@ def test_tc_kernel_repeat_launches_bitwise(W, kind, n, d, s):
     ref = op.kmatvec(V)
     for _ in range(12):
         assert np.array_equal(op.kmatvec(V), ref)
+
+
+@pytest.mark.parametrize("kind,n,d,s", [(0, 40_003, 16, 64), (1, 20_000, 8, 5)])
+def test_host_form_column_parts(W, kind, n, d, s):
+    """The host-buffer matvec on a tensor-core operator uploads V in three column parts and
+    computes each part's columns as it lands (the diagonal and sigma^2 V_i once, in the right
+    parts), the last part in four row parts: it agrees with the device form (one launch over
+    all columns) to fp32-accumulation rounding, with the fp64 operator at the fp32 bar, and is
+    deterministic.  Kernel launches: one per leading column part, four for the last."""
+    import torch
+    rng = np.random.default_rng(n + s)
+    X = rng.standard_normal((n, d)) if kind == 0 else rng.random((n, d))
+    V = np.asfortranarray(rng.standard_normal((n, s)))
+    h = W.KernelHyperparams(0.8, 1.0, 0.05, kind)
+    op = W.KernelOperator(h, X, precision=W.F32_3XTF32)
+    W.kernel_timer_enable(True)
+    Y = op.kmatvec(V)
+    _, launches = W.kernel_timer_read()
+    W.kernel_timer_enable(False)
+    assert launches == 2 + 4
+    Vd = torch.from_numpy(np.ascontiguousarray(V)).cuda()
+    Yd = torch.empty_like(Vd)
+    op.kmatvec_dev(Vd.data_ptr(), Yd.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert colrel(Y, Yd.cpu().numpy()) <= 5e-6
+    ref = W.KernelOperator(h, X, precision=W.F64).kmatvec(V)
+    assert colrel(Y, ref) <= 1e-4
+    assert np.array_equal(op.kmatvec(V), Y)
