@@ -154,11 +154,48 @@ __device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
+// 2^10 * 2^a for a <= 0 on the FMA pipe (two values per packed instruction), for the share
+// of the Matern map's exponentials moved off MUFU: a = j + f with j = round(a) (the 1.5 2^23
+// magic add leaves j in the low mantissa bits of t), 2^f on [-1/2, 1/2] by a degree-5
+// relative-minimax polynomial with its coefficients scaled by 2^10 (max relative error
+// 2.3e-7 in fp32 Horner, like ex2.approx's ~2 ulp), 2^j added into the exponent field with
+// an integer shift-add.  a is clamped at -100 so the exponent stays normal (2^-90 flushes to
+// zero in the fp16 split anyway, as the MUFU path's value does).
+// pairs of each 16-column group whose ex2 runs on the FMA pipe (first / second group of a
+// warp's 32 columns)
+#ifndef WGP_EXP_POLY_A
+#define WGP_EXP_POLY_A 2
+#endif
+#ifndef WGP_EXP_POLY_B
+#define WGP_EXP_POLY_B 2
+#endif
+#if defined(WGP_KSCALE_IN_EXP) && (WGP_EXP_POLY_A || WGP_EXP_POLY_B)
+#error "WGP_EXP_POLY assumes the 2^10 scale outside the exponent argument"
+#endif
+__device__ __forceinline__ float2 ex2_poly_k(float2 a) {
+  a.x = fmaxf(a.x, -100.0f);
+  a.y = fmaxf(a.y, -100.0f);
+  const float2 M = make_float2(0x1.8p23f, 0x1.8p23f);
+  const float2 t = __fadd2_rn(a, M);
+  const float2 j = __fadd2_rn(t, make_float2(-0x1.8p23f, -0x1.8p23f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.0f, -1.0f), a);
+  float2 p = __ffma2_rn(make_float2(0x1.5c08e4p0f, 0x1.5c08e4p0f), f,
+                        make_float2(0x1.3d0c52p3f, 0x1.3d0c52p3f));
+  p = __ffma2_rn(p, f, make_float2(0x1.c6b6e4p5f, 0x1.c6b6e4p5f));
+  p = __ffma2_rn(p, f, make_float2(0x1.ebf918p7f, 0x1.ebf918p7f));
+  p = __ffma2_rn(p, f, make_float2(0x1.62e428p9f, 0x1.62e428p9f));
+  p = __ffma2_rn(p, f, make_float2(0x1.000002p10f, 0x1.000002p10f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
 // Kernel map of NCOL columns of a row: v = fp32 d^2 from TMEM, kv = k/s^2 * 2^10.  Pairs of
-// columns go through the packed FP32 pipe, sqrt and exp2 through MUFU (moving a share of
-// either to an FMA-pipe polynomial measured no faster).  sqrt(|d2|): a tiny negative d2 from
-// the norm-form cancellation maps to ~0 like the reference's max(.,0) clamp (kernel.cpp:44).
-template <int NCOL>
+// columns go through the packed FP32 pipe, sqrt and exp2 through MUFU, except the first NPOLY
+// pairs of the Matern map, whose exp2 runs on the FMA pipe (ex2_poly_k): the map is bound by
+// the SFU (two MUFU ops per pair), the FMA pipe is mostly idle.  sqrt(|d2|): a tiny negative
+// d2 from the norm-form cancellation maps to ~0 like the reference's max(.,0) clamp
+// (kernel.cpp:44).
+template <int NCOL, int NPOLY>
 __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* kv, float c1,
                                            float nclog2e) {
 #ifdef WGP_SKIP_MAP
@@ -174,13 +211,16 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
   // ~4e-7 relative error on the largest entries (d ~ 0)
   const float2 OFF = make_float2(KSCALE_LOG2, KSCALE_LOG2);
 #else
-  // the 2^10 scale is applied after ex2 (an exact power-of-two FMUL2): the exponent
+  // the 2^10 scale is applied outside ex2 (exact power-of-two factors): the exponent
   // argument -z log2 e / -d2 log2 e / 2l^2 is ~0 for the largest entries, so its rounding
   // error (|a| 2^-24, x ln 2 on k) vanishes where k matters most
   const float2 SC = make_float2(0x1.0p10f, 0x1.0p10f);
 #endif
   if (kind == WGP_MATERN32) {
     const float2 C1 = make_float2(c1, c1);
+    // 2^10 (1 + z) with z = c1 r in one FFMA2 (2^10 c1 is exact): k = u e^{-z}, three
+    // packed FP32 instructions per pair of columns besides the MUFU ops
+    const float2 C1K = make_float2(c1 * 0x1.0p10f, c1 * 0x1.0p10f);
 #pragma unroll
     for (int q = 0; q < NCOL / 2; ++q) {
       float2 r;
@@ -188,17 +228,23 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
       r.y = ptx::sqrt_approx(fabsf(__uint_as_float(v[2 * q + 1])));
 #ifdef WGP_KSCALE_IN_EXP
       const float2 a = __ffma2_rn(r, NC, OFF);  // log2(2^10 e^{-z})
-#else
-      const float2 a = __fmul2_rn(r, NC);  // log2(e^{-z})
-#endif
       float2 e;
       e.x = ptx::ex2_approx(a.x);
       e.y = ptx::ex2_approx(a.y);
-#ifndef WGP_KSCALE_IN_EXP
-      e = __fmul2_rn(e, SC);  // 2^10 e^{-z}, exact
+      const float2 k = __ffma2_rn(__fmul2_rn(r, C1), e, e);
+#else
+      const float2 a = __fmul2_rn(r, NC);  // log2(e^{-z})
+      float2 k;
+      if (q < NPOLY) {
+        const float2 e = ex2_poly_k(a);  // 2^10 e^{-z} on the FMA pipe
+        k = __ffma2_rn(__fmul2_rn(r, C1), e, e);
+      } else {
+        float2 e;
+        e.x = ptx::ex2_approx(a.x);
+        e.y = ptx::ex2_approx(a.y);
+        k = __fmul2_rn(__ffma2_rn(r, C1K, SC), e);  // 2^10 (1 + z) e^{-z}
+      }
 #endif
-      const float2 z = __fmul2_rn(r, C1);
-      const float2 k = __ffma2_rn(z, e, e);  // 2^10 (1+z) e^{-z}
       kv[2 * q] = k.x;
       kv[2 * q + 1] = k.y;
     }
@@ -223,22 +269,38 @@ __device__ __forceinline__ void kernel_map(int kind, const uint32_t* v, float* k
   }
 }
 
+// BJ_ = j columns per tile: 64 (NB = 4 TMEM tile buffers, any s_pad <= 64) or 128 (NB = 3,
+// s_pad <= 32: [0, 384) tile buffers + 4 s_pad accumulator columns).  A 128-column tile is two
+// 64-column V sub-tiles (the global V layout is per 64 columns) and half as many pipeline
+// rounds per pair: the GEMM2 issue loop (~900 cycles per round) then
+// covers 16384 pairs instead of 8192, which is what bounds the one-MUFU RBF map.
+// At BJ_ = 128 the three TMEM buffers leave no spare beyond the three epilogue sets: GEMM1 of
+// a set's next tile waits for the GEMM2 of its current one (epilogue S wait ~1200 cycles per
+// tile in the trace).  Two sets (16 epilogue warps, a spare buffer) measured slower still --
+// the map then lacks warps -- with 32-column TMEM load batches slower again.
+template <int BJ_>
 __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p, int NSX, int NSV) {
+  constexpr int NB = BJ_ == 64 ? MAX_NB : 3;
+  constexpr int EPIW_ = EPIW;
+  constexpr int NSET_ = NSET;
+  constexpr int CPW_ = BJ_ / 2;           // tile columns per epilogue warp
+  constexpr int NSUB = BJ_ / BJ;          // 64-column V sub-tiles per tile
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Epilogue warps 0..EPIW-1, drain warps EPIW..EPIW+3, role warps EPIW+4..EPIW+7 (role r on
   // SM sub-partition r): the issue arbiter favours the highest warp id, so the producers and
   // MMA issuers -- a few instructions per tile on the critical path -- win the issue slot over
   // the map warps they share a sub-partition with.
-  const int role = warp - EPIW - NDRAIN;  // < 0 for epilogue (and drain) warps
+  const int role = warp - EPIW_ - NDRAIN;  // < 0 for epilogue (and drain) warps
   const uint32_t ESZ = p.g1f16 ? 2 : 4;     // GEMM1 operand element bytes
   const uint32_t XA_BYTES = BM * p.K1 * ESZ;
-  const uint32_t XB_BYTES = BJ * p.K1 * ESZ;
-  const uint32_t VT_BYTES = p.s_pad * BJ * 2;  // one of hi / lo (fp16)
+  const uint32_t XB_BYTES = BJ_ * p.K1 * ESZ;
+  const uint32_t VT_BYTES = p.s_pad * BJ * 2;  // one of hi / lo (fp16) of a 64-column sub-tile
+  const uint32_t VS_BYTES = NSUB * 2 * VT_BYTES;  // one V stage: NSUB x [hi | lo]
   unsigned char* sXA = smem;
   unsigned char* sXB = smem + XA_BYTES;                        // NSX stages of XB_j
   unsigned char* sV = sXB + (size_t)NSX * XB_BYTES;            // NSV stages of V_j hi | lo
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + (size_t)NSV * 2 * VT_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + (size_t)NSV * VS_BYTES);
   uint64_t* xb_full = bars;               // [NSX] bulk copy -> GEMM1
   uint64_t* xb_empty = xb_full + NSX;     // [NSX] GEMM1 -> XB producer
   uint64_t* v_full = xb_empty + NSX;      // [NSV] bulk copy -> GEMM2
@@ -247,14 +309,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* s_full = xa_full + 1;         // [MAX_NB] GEMM1 -> epilogue
   uint64_t* k_full = s_full + MAX_NB;     // [MAX_NB] epilogue -> GEMM2 (8 arrivals)
   uint64_t* b_free = k_full + MAX_NB;     // [MAX_NB] GEMM2 -> GEMM1
-  uint64_t* y_full = b_free + MAX_NB;     // [2] chunk accumulator done (GEMM2 commit)
+  uint64_t* k_half = b_free + MAX_NB;     // [MAX_NB] first half of each warp's K columns (BJ_ 128)
+  uint64_t* y_full = k_half + MAX_NB;     // [2] chunk accumulator done (GEMM2 commit)
   uint64_t* y_free = y_full + 2;          // [2] chunk accumulator drained (drain warps)
   uint64_t* c_full = y_free + 2;          // correction accumulator final (last commit)
   uint64_t* acc_zero = c_full + 1;        // accumulators zeroed (drain warps, merged GEMM2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_zero + 1);
-  constexpr int NB = MAX_NB;
   // TMEM columns of the accumulators: [Y_0 | C_0 | Y_1 | C_1], s_pad each (see MAX_NB)
-  const uint32_t TM_ACC = 256;
+  const uint32_t TM_ACC = NB * BJ_;
   const uint32_t AW = (uint32_t)p.s_pad;
   // this CTA's j range: tiles [jt0, jt0 + T) of the column sweep
   const int jt0 = blockIdx.y * p.tiles_per_split;
@@ -278,6 +340,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     for (int i = 0; i < MAX_NB; ++i) {
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&k_full[i], SETW);
+      ptx::mbar_init(&k_half[i], SETW);
       ptx::mbar_init(&b_free[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -328,9 +391,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         if (t >= NSV) ptx::mbar_wait(&v_empty[st], ph ^ 1);
         if (leader) {
           trace_ev(p, t, 8);
-          ptx::mbar_arrive_expect_tx(&v_full[st], 2 * VT_BYTES);
-          ptx::bulk_g2s(sV + (size_t)st * 2 * VT_BYTES, p.Vt + (size_t)(jt0 + t) * 2 * p.s_pad * BJ,
-                        2 * VT_BYTES, &v_full[st]);
+          ptx::mbar_arrive_expect_tx(&v_full[st], VS_BYTES);
+          ptx::bulk_g2s(sV + (size_t)st * VS_BYTES, p.Vt + (size_t)(jt0 + t) * NSUB * 2 * p.s_pad * BJ,
+                        VS_BYTES, &v_full[st]);
         }
         __syncwarp();
       }
@@ -344,7 +407,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // in uniform registers: a single-lane loop measured 3x slower MMA issue); one elected lane
     // issues.
     if (role == 1) {
-      const uint32_t idesc1 = p.g1f16 ? ptx::idesc_f16(BM, BJ) : ptx::idesc_tf32(BM, BJ);
+      const uint32_t idesc1 = p.g1f16 ? ptx::idesc_f16(BM, BJ_) : ptx::idesc_tf32(BM, BJ_);
       const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
       const uint64_t dXB0 = ptx::umma_desc(ptx::smem_u32(sXB), 128, sbo1);
       const uint64_t xb_step = (uint64_t)(XB_BYTES >> 4);  // descriptor start-address units
@@ -360,10 +423,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
           const uint64_t dB = dXB0 + xb_step * st1;
           if (p.g1f16) {
             for (int ks = 0; ks < KS1; ++ks)
-              ptx::mma_f16_ss(tmem + b1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+              ptx::mma_f16_ss(tmem + b1 * BJ_, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
           } else {
             for (int ks = 0; ks < KS1; ++ks)
-              ptx::mma_tf32_ss(tmem + b1 * 64, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+              ptx::mma_tf32_ss(tmem + b1 * BJ_, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
           }
           ptx::mma_commit(&s_full[b1]);
           ptx::mma_commit(&xb_empty[st1]);
@@ -377,7 +440,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       const uint32_t idesc2w = ptx::idesc_f16(BM, 2 * p.s_pad);
       // fp16 V tile: rows c (N) in 8-row groups, K = 64 j in 8-element (16 B) chunks
       const uint64_t dV0 = ptx::umma_desc(ptx::smem_u32(sV), 128, (BJ / 8) * 128);
-      const uint64_t v_step = (uint64_t)((2 * VT_BYTES) >> 4);
+      const uint64_t v_step = (uint64_t)(VS_BYTES >> 4);
+      const uint64_t sub_step = (uint64_t)((2 * VT_BYTES) >> 4);  // next 64-column sub-tile
       int st2 = 0, b2 = 0, c = 0, pos = 0;  // V stage, TMEM buffer, chunk, tile within chunk
       uint32_t ph2 = 0, phb2 = 0;
       for (int t = 0; t < T; ++t) {
@@ -387,20 +451,42 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         if (lane == 0) trace_ev(p, t, 13);
         ptx::mbar_wait(&v_full[st2], ph2);
         if (lane == 0) trace_ev(p, t, 9);
-        ptx::mbar_wait(&k_full[b2], phb2);
         if (t == 0) ptx::mbar_wait(acc_zero, 0);  // drain warps zeroed the accumulators
-        ptx::tc_fence_after();
+        const uint64_t dVh = dV0 + v_step * st2;
+        const uint32_t yacc = tmem + TM_ACC + 2 * AW * ya;
+        const uint32_t kb = tmem + b2 * BJ_;
+        // K-step ks: 16 j's of sub-tile ks / 4 (8 TMEM columns [hi] + 8 [lo] per step)
+        auto issue = [&](int ks) {
+          const uint64_t dv = dVh + sub_step * (ks / 4) + 16 * (ks % 4);
+          ptx::mma_f16_ts(yacc, kb + ks * 16, dv, idesc2w, 1u);      // [Y|C] += Kh [Vh|Vl]
+          ptx::mma_f16_ts(yacc + AW, kb + ks * 16 + 8, dv, idesc2, 1u);  // C += Kl Vh
+        };
+        if (BJ_ == 128) {
+          // K arrives in two halves (each epilogue warp signals after the first half of its
+          // 64 columns): the K-steps of those columns (0, 1 of each warp half: ks 0, 1, 4, 5)
+          // are issued while the epilogue maps the rest, so the buffer frees (and GEMM1 of the
+          // set's next tile starts) earlier
+          ptx::mbar_wait(&k_half[b2], phb2);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            trace_ev(p, t, 1);
+            issue(0); issue(1); issue(4); issue(5);
+          }
+          __syncwarp();
+          ptx::mbar_wait(&k_full[b2], phb2);
+          ptx::tc_fence_after();
+        } else {
+          ptx::mbar_wait(&k_full[b2], phb2);
+          ptx::tc_fence_after();
+        }
         if (ptx::elect_one()) {
-          trace_ev(p, t, 1);
-          const uint64_t dVh = dV0 + v_step * st2;
-          const uint32_t yacc = tmem + TM_ACC + 2 * AW * ya;
-          const uint32_t kb = tmem + b2 * 64;
+          if (BJ_ == 128) {
+            issue(2); issue(3); issue(6); issue(7);
+          } else {
+            trace_ev(p, t, 1);
 #pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks)
-            ptx::mma_f16_ts(yacc, kb + ks * 16, dVh + 16 * ks, idesc2w, 1u);  // [Y|C] += Kh [Vh|Vl]
-#pragma unroll
-          for (int ks = 0; ks < BJ / 16; ++ks)
-            ptx::mma_f16_ts(yacc + AW, kb + ks * 16 + 8, dVh + 16 * ks, idesc2, 1u);  // C += Kl Vh
+            for (int ks = 0; ks < BJ_ / 16; ++ks) issue(ks);
+          }
           trace_ev(p, t, 10);
           ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
@@ -414,7 +500,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         if (++pos == CH) { pos = 0; ++c; }
       }
     }
-  } else if (warp < EPIW) {
+  } else if (warp < EPIW_) {
     // ------------------------------------------------------------ kernel-map epilogue
     // NSET sets of 8 warps take tiles round-robin (set = t mod NSET); within a set, warp
     // (quadrant q, half) maps rows 32q.. and columns 32 half.. of the tile, 16 at a time.
@@ -427,7 +513,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     const int64_t grow0 = p.row0 + (int64_t)blockIdx.x * BM;
     const int64_t lr = (int64_t)blockIdx.x * BM + r;  // local output row
     const float kdiag = 1024.0f;              // k(x,x)/s^2 * 2^10
-    for (int t = set; t < T; t += NSET) {
+    for (int t = set; t < T; t += NSET_) {
       const int b = t % NB;                   // buffer and phase of tile t
       const uint32_t bph = (t / NB) & 1;
       const bool tr = lane == 0 && q == 0 && half == 0 && set == 0;
@@ -435,38 +521,60 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       ptx::mbar_wait(&s_full[b], bph);
       ptx::tc_fence_after();
       if (tr) trace_ev(p, t, 3);
-      const int64_t gj_base = p.col0 + (int64_t)(jt0 + t) * BJ + half * CPW;
-      const bool diag = p.gram && gj_base < grow0 + BM && gj_base + CPW > grow0;
+      const int64_t gj_base = p.col0 + (int64_t)(jt0 + t) * BJ_ + half * CPW_;
+      const bool diag = p.gram && gj_base < grow0 + BM && gj_base + CPW_ > grow0;
+      // The warp's CPW_ columns in 16-column groups (GW) under the 64-register budget of 32
+      // warps (issuing the next group's load before the current group's split measured no
+      // faster).
+      constexpr int GW = 16;
+      const uint32_t col0 = tmem + lane_off + b * BJ_ + half * CPW_;
 #pragma unroll
-      for (int h2 = 0; h2 < CPW / 16; ++h2) {
-        const uint32_t col = tmem + lane_off + b * 64 + half * CPW + h2 * 16;
-        uint32_t v[16];
-        ptx::tmem_ld16(col, v);
+      for (int g0 = 0; g0 < CPW_; g0 += GW) {
+        uint32_t v[GW];
+#pragma unroll
+        for (int u = 0; u < GW / 16; ++u)
+          ptx::tmem_ld16(col0 + g0 + 16 * u, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * u));
         ptx::tmem_wait_ld();
-        if (tr && h2 == 0) trace_ev(p, t, 7);
-        float kv[16];
-        kernel_map<16>(p.kind, v, kv, p.c1, p.neg_c_log2e);
-        if (diag) {  // tile touches the diagonal: k(x,x) = s^2 exactly
-          const int64_t gj0 = gj_base + h2 * 16;
+        if (tr && g0 == 0) trace_ev(p, t, 7);
+        float kv[GW];
 #pragma unroll
-          for (int c = 0; c < 16; ++c)
+        for (int u = 0; u < GW / 16; ++u) {
+          if (((g0 / 16) + u) % 2 == 0)
+            kernel_map<16, WGP_EXP_POLY_A>(p.kind, v + 16 * u, kv + 16 * u, p.c1, p.neg_c_log2e);
+          else
+            kernel_map<16, WGP_EXP_POLY_B>(p.kind, v + 16 * u, kv + 16 * u, p.c1, p.neg_c_log2e);
+        }
+        if (diag) {  // tile touches the diagonal: k(x,x) = s^2 exactly
+          const int64_t gj0 = gj_base + g0;
+#pragma unroll
+          for (int c = 0; c < GW; ++c)
             if (gj0 + c == gi) kv[c] = kdiag;
         }
-        uint32_t hi[8], lo[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          // hi = kv cut to fp16's 10 mantissa bits (exact in fp16 over its normal range; an
-          // integer LOP on the ALU pipe), lo = kv - hi (FADD2, exact) rounded to fp16
-          const float2 hf = make_float2(__uint_as_float(__float_as_uint(kv[2 * c]) & 0xFFFFE000u),
-                                        __uint_as_float(__float_as_uint(kv[2 * c + 1]) & 0xFFFFE000u));
-          const float2 rem =
-              __fadd2_rn(make_float2(kv[2 * c], kv[2 * c + 1]), make_float2(-hf.x, -hf.y));
-          hi[c] = pack_h2(hf.x, hf.y);
-          lo[c] = pack_h2(rem.x, rem.y);
+        for (int u = 0; u < GW / 16; ++u) {
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            // hi = kv cut to fp16's 10 mantissa bits (exact in fp16 over its normal range; an
+            // integer LOP on the ALU pipe), lo = kv - hi (FADD2, exact) rounded to fp16
+            const float* k2 = kv + 16 * u + 2 * c;
+            const float2 hf = make_float2(__uint_as_float(__float_as_uint(k2[0]) & 0xFFFFE000u),
+                                          __uint_as_float(__float_as_uint(k2[1]) & 0xFFFFE000u));
+            const float2 rem = __fadd2_rn(make_float2(k2[0], k2[1]), make_float2(-hf.x, -hf.y));
+            hi[c] = pack_h2(hf.x, hf.y);
+            lo[c] = pack_h2(rem.x, rem.y);
+          }
+          // K back into the 16 columns just read: [hi 8 | lo 8]
+          const uint32_t col = col0 + g0 + 16 * u;
+          ptx::tmem_st8(col, hi);
+          ptx::tmem_st8(col + 8, lo);
         }
-        // K back into the 16 columns just read: [hi 8 | lo 8]
-        ptx::tmem_st8(col, hi);
-        ptx::tmem_st8(col + 8, lo);
+        if (BJ_ == 128 && g0 + GW == CPW_ / 2) {  // first half of this warp's columns in TMEM
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&k_half[b]);
+        }
       }
       if (tr) trace_ev(p, t, 4);
       ptx::tmem_wait_st();
@@ -478,7 +586,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     }
     if (warp == 0 && lane == 0) cta_ev(p, 1);
   }
-  if (warp >= EPIW && warp < EPIW + NDRAIN) {
+  if (warp >= EPIW_ && warp < EPIW_ + NDRAIN) {
     // ------------------------------------------------------------ drain warps
     // Chunk c's accumulator (after its y_full) 16 columns at a time into this CTA's slice of
     // the partials [gy][s_pad/4][nrows][4] (4 columns of a row contiguous: one 16-byte vector
@@ -884,10 +992,10 @@ bool tc_build_cross_rows(const Op& op, const double* Xs, int64_t m, int dpad, DB
 // Shared memory: XA rows + NSX XB stages + NSV V stages + 1 KB of barriers.  XB lives from
 // its copy to GEMM1 (~1 tile period), V until GEMM2 after the map (~4 periods), so the V
 // ring gets the space first: NSX = 3 (2 if tight), NSV up to 8.
-size_t tc_smem_bytes(int K1, int esz, int s_pad, int* nsx_out, int* nsv_out) {
+size_t tc_smem_bytes(int K1, int esz, int s_pad, int* nsx_out, int* nsv_out, int bj = tc::BJ) {
   const size_t xa = (size_t)tc::BM * K1 * esz;
-  const size_t xb = (size_t)tc::BJ * K1 * esz;
-  const size_t vb = 2 * (size_t)s_pad * tc::BJ * 2;
+  const size_t xb = (size_t)bj * K1 * esz;
+  const size_t vb = 2 * (size_t)s_pad * bj * 2;
   const size_t avail = 227 * 1024 - 1024 - xa;
   static const int want_x = getenv("WGP_TC_NSX") ? atoi(getenv("WGP_TC_NSX")) : 5;
   int nsx = want_x, nsv = 0;
@@ -948,9 +1056,21 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
       Yc = ychunk.p;
     }
     const int s_pad = ((sc + 15) / 16) * 16;
-    const int ntiles = (int)((ncols + tc::BJ - 1) / tc::BJ);
-    // scratch: fp16 tiles (2 x s_pad x 64 halves per tile) + 2 x s_pad scales (floats)
-    const size_t vt_halves = (size_t)ntiles * tc::BJ * s_pad * 2;
+    // 128-column tiles where the accumulators leave TMEM room for three 128-column buffers
+    // (s_pad <= 32; every column range starts on a 128-row boundary of XB, and XB holds
+    // round_up(n, 128) rows, so the last tile stays in bounds)
+    static const int forced_bj = getenv("WGP_TC_BJ") ? atoi(getenv("WGP_TC_BJ")) : 0;
+    int bj = forced_bj == 64 || forced_bj == 128 ? (s_pad <= 32 ? forced_bj : 64)
+                                                  : (s_pad <= 32 ? 128 : 64);
+    if (bj == 128) {  // (large dim: the 64-column pipeline when 128-column stages do not fit)
+      int nx = 0, nv = 0;
+      tc_smem_bytes(K1, esz, s_pad, &nx, &nv, 128);
+      if (nx < 2 || nv < 3) bj = 64;
+    }
+    const int ntiles = (int)((ncols + bj - 1) / bj);
+    const int64_t nsub = (int64_t)ntiles * (bj / tc::BJ);  // 64-column V sub-tiles
+    // scratch: fp16 tiles (2 x s_pad x 64 halves per sub-tile) + 2 x s_pad scales (floats)
+    const size_t vt_halves = (size_t)nsub * tc::BJ * s_pad * 2;
     // (+ the per-column max bits, 8-byte aligned, after the scales)
     const size_t vt_floats = ((vt_halves + 1) / 2 + 1) & ~(size_t)1;
     vt_scratch.ensure(vt_floats + 2 * (size_t)s_pad + 64 + 2 * (size_t)tc::MAX_SPAD);
@@ -962,8 +1082,8 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     WGP_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * sc, st));
     tc::colmax_kernel<<<ceil_div(ncols, 64), 256, 0, st>>>(Vc, ncols, sc, cmax);
     tc::colscale_finish_kernel<<<1, 128, 0, st>>>(cmax, sc, s_pad, sc_up, sc_down);
-    tc::split_v_kernel<<<tc::grid_for((int64_t)ntiles * (tc::BJ / 8) * s_pad), 256, 0, st>>>(
-        Vc, ncols, sc, s_pad, (int64_t)ntiles * tc::BJ, sc_up, vt);
+    tc::split_v_kernel<<<tc::grid_for(nsub * (tc::BJ / 8) * s_pad), 256, 0, st>>>(
+        Vc, ncols, sc, s_pad, nsub * tc::BJ, sc_up, vt);
     WGP_CUDA(cudaGetLastError());
     tc::Params prm;
     prm.XA = XA_rows;
@@ -977,7 +1097,8 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     prm.col0 = col0;
     prm.ntiles = ntiles;
     static const int forced_ch = getenv("WGP_TC_CH") ? atoi(getenv("WGP_TC_CH")) : 0;
-    prm.ch = forced_ch > 0 ? forced_ch : tc::CH_DEFAULT;
+    // (the same number of MMA instructions per chunk accumulator for either tile width)
+    prm.ch = forced_ch > 0 ? forced_ch : tc::CH_DEFAULT * tc::BJ / bj;
     for (int part = 0; part < row_parts; ++part) {
     // rows [pa, pb) of this launch, part boundaries on 128-row CTA tiles
     const int64_t pa = row_part_begin(nrows, part, row_parts);
@@ -1022,14 +1143,15 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
       prm.cta_trace = trace_buf.p + (size_t)ntiles * tc::TRW;
     }
     int nsx = 0, nsv = 0;
-    const size_t smem = tc_smem_bytes(K1, esz, s_pad, &nsx, &nsv);
+    const size_t smem = tc_smem_bytes(K1, esz, s_pad, &nsx, &nsv, bj);
     WGP_REQUIRE(nsx >= 2 && nsv >= 2, "kmatvec_tc: dim %d too large for the shared-memory pipeline",
                 op.dim);
-    auto kern = tc::kmatvec_tc_kernel;
+    auto kern = bj == 64 ? tc::kmatvec_tc_kernel<64> : tc::kmatvec_tc_kernel<128>;
+    const int nthreads = tc::NTHREADS;
     WGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
       TimedScope ts("kmatvec_tc", st);
-      kern<<<dim3(row_ctas, gy), tc::NTHREADS, smem, st>>>(prm, nsx, nsv);
+      kern<<<dim3(row_ctas, gy), nthreads, smem, st>>>(prm, nsx, nsv);
     }
     WGP_CUDA(cudaGetLastError());
     {
