@@ -56,18 +56,21 @@ __global__ void rows_to_colmajor_kernel(const T* __restrict__ src, int64_t n, in
 // or on the other columns (solve_many must equal single-RHS solves bitwise,
 // test_solvers.cpp:397-413).  Work item = (chunk, group of up to 32 columns), one thread per
 // (column, slab): a warp reads 32 consecutive columns of a row (256 contiguous bytes per fp64
-// load); one 1024-thread block per SM walks the items.  Each slab is loaded in 8-row halves
-// (4-row quarters for two dot products), all loads of a part issued before its FMA chain:
-// 16 loads in flight per thread, 128 KB per SM.
+// load); blocks of CB columns x 32 slabs walk the items, 1024 / (32 CB) of them per SM.  Each
+// slab is loaded in 8-row halves (4-row quarters for two dot products), all loads of a part
+// issued before its FMA chain: 16 loads in flight per thread, 128 KB per SM.  Two 512-thread
+// blocks per SM (CB = 16) measured 20.2 us per launch at [101000][64] (ncu, cold L2; 79% of
+// the measured HBM copy bandwidth) against 21.8 us for one 1024-thread block (its reduction
+// and item change leave the SM without loads in flight; the other block covers them); a
+// rolling load ring across slab rows and items (no drain at all) measured slower (21.3 /
+// 22.8 us: per-load index arithmetic and predication).
 constexpr int kSlabRows = kChunkRows / 32;
-constexpr int kColsPerBlock = 32;  // coldots: columns per work item (x 32 slabs = 1024 threads)
-
-template <typename T, int NQ>
-__global__ void __launch_bounds__(1024, 1)
+template <typename T, int NQ, int CB>
+__global__ void __launch_bounds__(CB * 32, 32 / CB)
     coldots_kernel(const T* __restrict__ A0, const T* __restrict__ B0, const T* __restrict__ A1,
                    const T* __restrict__ B1, int64_t n, int s, int cb, int ngroups, int64_t items,
                    double* __restrict__ part) {
-  __shared__ double red[NQ][32][kColsPerBlock];
+  __shared__ double red[NQ][32][CB];
   const int cl = threadIdx.x % cb;
   const int q = threadIdx.x / cb;  // slab
   constexpr int NH = NQ == 1 ? 2 : 4;  // loads in flight per thread: 16 (64 registers at 1024 threads)
@@ -272,15 +275,25 @@ void launch_coldots(const T* A0, const T* B0, const T* A1, const T* B1, int64_t 
   if (s <= 0) return;
   const int nch = ceil_div(n, kChunkRows);
   if (nch <= 0) return;
-  const int cb = s < kColsPerBlock ? s : kColsPerBlock;
+  static const int forced_cb = getenv("WGP_COLDOTS_CB") ? atoi(getenv("WGP_COLDOTS_CB")) : 0;
+  const int CBmax = forced_cb == 8 || forced_cb == 16 || forced_cb == 32 ? forced_cb : 16;
+  const int cb = s < CBmax ? s : CBmax;
   const int ngroups = ceil_div(s, cb);
   const int64_t items = (int64_t)nch * ngroups;
-  const int grid = (int)std::min<int64_t>(items, 148);
+  const int grid = (int)std::min<int64_t>(items, (int64_t)148 * (32 / CBmax));
   TimedScope ts_("coldots", st);
-  if (A1)
-    coldots_kernel<T, 2><<<grid, cb * 32, 0, st>>>(A0, B0, A1, B1, n, s, cb, ngroups, items, part);
+  auto go = [&](auto kern2, auto kern1) {
+    if (A1)
+      kern2<<<grid, cb * 32, 0, st>>>(A0, B0, A1, B1, n, s, cb, ngroups, items, part);
+    else
+      kern1<<<grid, cb * 32, 0, st>>>(A0, B0, A0, B0, n, s, cb, ngroups, items, part);
+  };
+  if (CBmax == 8)
+    go(coldots_kernel<T, 2, 8>, coldots_kernel<T, 1, 8>);
+  else if (CBmax == 16)
+    go(coldots_kernel<T, 2, 16>, coldots_kernel<T, 1, 16>);
   else
-    coldots_kernel<T, 1><<<grid, cb * 32, 0, st>>>(A0, B0, A0, B0, n, s, cb, ngroups, items, part);
+    go(coldots_kernel<T, 2, 32>, coldots_kernel<T, 1, 32>);
   WGP_CUDA(cudaGetLastError());
 }
 
