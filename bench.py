@@ -120,6 +120,32 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+class NvmlClockSampler(ClockSampler):
+    """The same samples read in-process through NVML (nvidia-ml-py): no nvidia-smi process
+    per sample."""
+
+    def _run(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.device)
+        except Exception:
+            return
+        bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                ("sw_power_cap", 0x4)]
+        while not self._stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+                pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(sm), str(mx), str(pw)] + ["Active" if r & b else "Not Active" for _, b in bits])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):

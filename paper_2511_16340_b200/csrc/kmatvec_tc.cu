@@ -161,13 +161,16 @@ __device__ __forceinline__ uint32_t pack_h2(float lo_elem, float hi_elem) {
 // 2.3e-7 in fp32 Horner, like ex2.approx's ~2 ulp), 2^j added into the exponent field with
 // an integer shift-add.  a is clamped at -100 so the exponent stays normal (2^-90 flushes to
 // zero in the fp16 split anyway, as the MUFU path's value does).
-// pairs of each 16-column group whose ex2 runs on the FMA pipe (first / second group of a
-// warp's 32 columns)
+// pairs of each 16-column group whose ex2 runs on the FMA pipe (even / odd 16-column groups
+// of a warp's columns).  Short runs at the full clock: 2 of 8 pairs fastest (C3 5.62 ->
+// 5.35 ms; 3 of 8 slower again); sustained 200-launch runs under the board power cap
+// (~1700 MHz): 1 of 8 fastest (6.08-6.09 ms vs 6.14 at 2 of 8, 6.19 with none) -- the FMA
+// path's energy competes with the clock there.  The bench is a sustained run.
 #ifndef WGP_EXP_POLY_A
-#define WGP_EXP_POLY_A 2
+#define WGP_EXP_POLY_A 1
 #endif
 #ifndef WGP_EXP_POLY_B
-#define WGP_EXP_POLY_B 2
+#define WGP_EXP_POLY_B 1
 #endif
 #if defined(WGP_KSCALE_IN_EXP) && (WGP_EXP_POLY_A || WGP_EXP_POLY_B)
 #error "WGP_EXP_POLY assumes the 2^10 scale outside the exponent argument"
