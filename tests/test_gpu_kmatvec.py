@@ -247,3 +247,59 @@ def test_host_form_column_parts(W, kind, n, d, s):
     ref = W.KernelOperator(h, X, precision=W.F64).kmatvec(V)
     assert colrel(Y, ref) <= 1e-4
     assert np.array_equal(op.kmatvec(V), Y)
+
+
+_TILE_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from paper_2511_16340_b200 import warmgp as W
+rng = np.random.default_rng(11)
+out = []
+for kind, n, d, s in ((1, 3000, 8, 32), (0, 2500, 16, 17), (1, 1700, 5, 4)):
+    X = rng.random((n, d)) * 2.0
+    V = rng.standard_normal((n, s))
+    op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.1, kind), X, precision=W.F32_3XTF32)
+    out.append(op.kmatvec(V))
+np.savez({path!r}, *out)
+"""
+
+
+@pytest.mark.parametrize("bj", ["64", "128"])
+def test_tc_tile_widths_agree(W, O, bj, tmp_path):
+    """Both tile widths of the tensor-core kernel (WGP_TC_BJ, read once per process: each in
+    its own child process) give the oracle's product within the fp32 bar at s <= 32, where
+    the default is the 128-column tile with three TMEM buffers."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(HERE)
+    path = str(tmp_path / f"y{bj}.npz")
+    env = dict(os.environ, WGP_TC_BJ=bj)
+    subprocess.run([sys.executable, "-c", _TILE_CHILD.format(root=root, path=path)], env=env, check=True,
+                   timeout=300)
+    got = np.load(path)
+    rng = np.random.default_rng(11)
+    for k, (kind, n, d, s) in enumerate(((1, 3000, 8, 32), (0, 2500, 16, 17), (1, 1700, 5, 4))):
+        X = rng.random((n, d)) * 2.0
+        V = rng.standard_normal((n, s))
+        ref = O.kmatvec(X, O.KernelHyperparams(0.5, 1.0, 0.1, kind), np.asfortranarray(V))
+        assert colrel(got[f"arr_{k}"], ref) <= 1e-5, (bj, kind, n, d, s)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_tc_far_pairs_underflow_cleanly(W, O, kind):
+    """Pairs far beyond the kernel's range (exponent arguments below the FMA-pipe exp2's
+    -100 clamp and below fp16's range after the 2^10 scale) contribute zeros: a few points
+    ~40 lengthscales from the rest (z ~ 140 for Matern, d^2/2l^2 ~ 3000 for RBF) give no
+    NaN/Inf and the oracle's product within the fp32 bar."""
+    rng = np.random.default_rng(3)
+    n, d, s = 1500, 4, 8
+    X = rng.random((n, d))
+    X[-10:] += 10.0  # 20 units per coordinate = 40 lengthscales away (|x - c| / l < 64 still)
+    V = rng.standard_normal((n, s))
+    h = O.KernelHyperparams(0.5, 1.0, 0.1, kind)
+    op = W.KernelOperator(W.KernelHyperparams(0.5, 1.0, 0.1, kind), X, precision=W.F32_3XTF32)
+    Y = op.kmatvec(V)
+    assert np.all(np.isfinite(Y))
+    ref = O.kmatvec(X, h, np.asfortranarray(V))
+    assert colrel(Y, ref) <= 1e-4
