@@ -3,10 +3,11 @@
 //   Y[i, :] = sum_j k(x_i, x_j) V[j, :] + sigma_n^2 V[i, :]      (gram, H = K + sigma_n^2 I)
 //
 // restating gram_matrix (kernel.cpp:48-72) + H*p (solvers.cpp:162) without materialising
-// K.  One CTA owns 128 rows i and a contiguous range of 64-column j tiles (grid: row blocks
-// x j splits):
+// K.  One CTA owns 128 rows i and a contiguous range of j tiles (grid: row blocks x j
+// splits); a tile is BJ_ = 64 columns (four TMEM tile buffers) or, when the RHS needs at
+// most 32 accumulator columns, 128 (three buffers: half the pipeline rounds per pair):
 //
-//   GEMM1  S = XA_i . XB_j^T      (M=128, N=64, K=K1)  tcgen05.mma SS, S (fp32) in TMEM.
+//   GEMM1  S = XA_i . XB_j^T      (M=128, N=BJ_, K=K1)  tcgen05.mma SS, S (fp32) in TMEM.
 //          The operands are pre-formatted so the contraction yields the squared distance
 //          directly (the norm form |x|^2 + |y|^2 - 2 x.y of kernel.cpp:39-46, 65), as
 //          3-way hi/lo splits: kind::f16 on x/l when the scaled coordinates fit fp16
@@ -15,11 +16,13 @@
 //            XB = [ xh  |  xl  |  xh  |  1  |  1  | sqh | sql]
 //          (TF32 precision: XA = [-2xh | sqh | 1], XB = [xh | 1 | sqh], single pass, ~2^-11)
 //   map    epilogue warps: tcgen05.ld S -> k(d2)/s^2 * 2^10 in registers (Matern-3/2 or RBF;
-//          MUFU sqrt/ex2, packed FP32) -> fp16 hi/lo split -> tcgen05.st back into the same
-//          TMEM columns (K never leaves the SM).
+//          MUFU sqrt/ex2, packed FP32, one Matern exponential in eight as an FMA-pipe
+//          polynomial) -> fp16 hi/lo split -> tcgen05.st back into the same TMEM columns (K
+//          never leaves the SM).
 //   GEMM2  Y += K_hi V_hi (chunk accumulator), C += K_hi V_lo + K_lo V_hi (correction
-//          accumulator)  (M=128, N=s_pad, K=64)  kind::f16, A from TMEM (TS form).  V is
-//          pre-split into fp16 hi/lo with a per-column power-of-two scale.
+//          accumulator)  (M=128, N=s_pad, K=BJ_)  kind::f16, A from TMEM (TS form).  V is
+//          pre-split into fp16 hi/lo with a per-column power-of-two scale, in 64-column
+//          sub-tiles.
 //   drain  every CH tiles the finished chunk accumulator is added (fp32 vector reductions)
 //          into L2-resident partials; reduce_splits_kernel sums splits in fp64 and writes
 //          Y * s^2 / (2^10 * scale_c) + sigma_n^2 V_i (or B - that: the true residual of
@@ -29,7 +32,7 @@
 // 29 = GEMM1 issuer, 30 = V bulk-copy producer + TMEM allocator, 31 = GEMM2 issuer (whole
 // warps run the schedules, one elected lane issues), 24..27 = drain warps (one per TMEM lane
 // quadrant), 0..23 = epilogue: three sets of 8 warps taking j tiles round-robin (2 warps per
-// TMEM lane quadrant, 32 columns each).  Pipelines:
+// TMEM lane quadrant, BJ_ / 2 columns each).  Pipelines:
 // smem rings of XB_j (NSX) and V_j hi/lo (NSV); a ring of NB TMEM tile buffers (S written
 // by GEMM1, overwritten in place by K for GEMM2); mbarriers + tcgen05.commit.
 #include <cuda_fp16.h>
