@@ -526,6 +526,8 @@ def run_ours(args):
             step()
             ends[k].record(stream)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t_wall = time.perf_counter() - t_wall
     ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_step = float(np.mean(ms))
