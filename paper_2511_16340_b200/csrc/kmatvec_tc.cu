@@ -475,7 +475,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
         auto issue = [&](int ks) {
           const uint64_t dv = dVh + sub_step * (ks / 4) + 16 * (ks % 4);
           ptx::mma_f16_ts(yacc, kb + ks * 16, dv, idesc2w, 1u);      // [Y|C] += Kh [Vh|Vl]
+#ifndef WGP_PROBE_SKIP_CORR  // (timing-only probe: without the K_l V_h products)
           ptx::mma_f16_ts(yacc + AW, kb + ks * 16 + 8, dv, idesc2, 1u);  // C += Kl Vh
+#endif
         };
         if (BJ_ == 128) {
           // K arrives in two halves (each epilogue warp signals after the first half of its
