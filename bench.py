@@ -613,7 +613,7 @@ def run_ours(args):
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
             "frac": achieved / peak_tf32 if achieved else None,
             # dram_bytes_read + dram_bytes_write per launch of the TC kernel, from the committed
-            # ncu --set full capture of this workload (profiles/r01_kmatvec_tc_metrics.json):
+            # ncu --set full capture of this workload (profiles/r02h_kmatvec_tc_metrics.json):
             # X/XA/XB and the V tiles stay L2-resident, HBM sees little more than V/Y once.
             "traffic": TRAFFIC_BYTES,
             "peak_source": f"{peak_kind} bf16_tflops/2 (TF32 dense) from MEASURED_PEAKS.json",
@@ -705,8 +705,8 @@ def run_ours(args):
 
 
 # dram bytes (read + write) per launch of tc::kmatvec_tc_kernel on this workload, from the
-# committed ncu --set full capture (profiles/r01_kmatvec_tc_metrics.json)
-TRAFFIC_BYTES = 81.88e6
+# committed ncu --set full capture (profiles/r02h_kmatvec_tc_metrics.json: 56.46 MB read + 23.36 MB written)
+TRAFFIC_BYTES = 79.82e6
 
 
 def main():
