@@ -9,10 +9,14 @@
 //
 // Host work per iteration is one small D2H of (rel, active, failure) -- the scalar logic
 // (alpha, beta, freeze) runs in single-block "step" kernels on the device.
+#include <algorithm>
 #include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <thread>
+#include <vector>
 
 #include "rng.h"
 #include "solvers.h"
@@ -131,6 +135,38 @@ void SolverWork<T>::alloc(const Op& op, int s_) {
   act.ensure((size_t)2 * s + 2);
 }
 
+// Host column-major block copy (rows x cols, leading dimensions lds / ldd) on several host
+// threads: the large host<->device transfers of a solve go through a pinned staging buffer
+// instead of the driver's pageable path (a fresh numpy output array page-faults on first
+// touch; spread over threads that costs a fraction of the single-threaded pageable copy:
+// C3 download 51.7 MB 11-14 ms -> a few ms).
+static void host_copy_2d(double* dst, int64_t ldd, const double* src, int64_t lds, int64_t rows,
+                         int64_t cols) {
+  const int64_t total = rows * cols;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::min<int64_t>(std::min<unsigned>(hw, 16u), std::max<int64_t>(1, total / (1 << 17)));
+  auto work = [&](int t) {  // element range [a, b) in column-major order
+    const int64_t a = total * t / nt, b = total * (t + 1) / nt;
+    for (int64_t e = a; e < b;) {
+      const int64_t c = e / rows, r = e - c * rows;
+      const int64_t len = std::min(rows - r, b - e);
+      std::memcpy(dst + c * ldd + r, src + c * lds + r, sizeof(double) * len);
+      e += len;
+    }
+  };
+  if (nt <= 1) {
+    work(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(nt - 1);
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+
+constexpr size_t kPinnedMin = (size_t)8 << 20;  // smaller transfers: the direct pageable copy
+
 template <typename T>
 void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb, const double* U1,
                     int64_t ldu, int64_t n1, cudaStream_t st) {
@@ -139,16 +175,40 @@ void upload_problem(const Op& op, SolverWork<T>& w, const double* B, int64_t ldb
   // B: this rank's rows of the host column-major matrix -> row-major on the device
   w.stage.ensure((size_t)std::max<int64_t>(std::max(n, n1), 1) * s);
   DBuf<double>& stage = w.stage;
+  const bool warm = U1 && n1 > 0;
+  const size_t nb = sizeof(double) * (size_t)n * s, nu = warm ? sizeof(double) * (size_t)n1 * s : 0;
+  const bool pinned = nb + nu >= kPinnedMin;
+  double* hB = nullptr;
+  double* hU = nullptr;
+  if (pinned) {  // both arrays into the pinned staging first (the second copy overlaps the first H2D)
+    // room for a full-length warm start too, so a cold solve followed by warm ones (the bench
+    // and bo_round pattern) pins its host staging once
+    // (and 25% headroom, so the growth steps of a sweep do not re-pin it every time)
+    const size_t need = nb + std::max(nu, sizeof(double) * (size_t)w.N * s);
+    if (need > w.h_stage.n) w.h_stage.ensure(need + need / 4);
+    hB = reinterpret_cast<double*>(w.h_stage.p);
+    hU = hB + (size_t)n * s;
+  }
   if (n > 0) {
-    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, B + w.r0, sizeof(double) * ldb,
-                               sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+    if (pinned) {
+      host_copy_2d(hB, n, B + w.r0, ldb, n, s);
+      WGP_CUDA(cudaMemcpyAsync(stage.p, hB, nb, cudaMemcpyHostToDevice, st));
+    } else {
+      WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n, B + w.r0, sizeof(double) * ldb,
+                                 sizeof(double) * n, s, cudaMemcpyHostToDevice, st));
+    }
     launch_colmajor_to_rows(stage.p, n, n, s, w.B.p, true, st);
   }
   WGP_CUDA(cudaMemsetAsync(w.V.p, 0, sizeof(T) * w.N * s, st));
-  w.warm = U1 && n1 > 0;
-  if (U1 && n1 > 0) {  // expand_init: [u1; 0] (solvers.cpp:43-48), full rows on every rank
-    WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n1, U1, sizeof(double) * ldu,
-                               sizeof(double) * n1, s, cudaMemcpyHostToDevice, st));
+  w.warm = warm;
+  if (warm) {  // expand_init: [u1; 0] (solvers.cpp:43-48), full rows on every rank
+    if (pinned) {
+      host_copy_2d(hU, n1, U1, ldu, n1, s);
+      WGP_CUDA(cudaMemcpyAsync(stage.p, hU, nu, cudaMemcpyHostToDevice, st));
+    } else {
+      WGP_CUDA(cudaMemcpy2DAsync(stage.p, sizeof(double) * n1, U1, sizeof(double) * ldu,
+                                 sizeof(double) * n1, s, cudaMemcpyHostToDevice, st));
+    }
     launch_colmajor_to_rows(stage.p, n1, n1, s, w.V.p, true, st);
   }
   WGP_CUDA(cudaStreamSynchronize(st));
@@ -161,6 +221,15 @@ void download_solution(SolverWork<T>& w, double* V, int64_t ldv, cudaStream_t st
   w.stage.ensure((size_t)std::max<int64_t>(N, 1) * s);
   DBuf<double>& stage = w.stage;
   launch_rows_to_colmajor(w.V.p, N, s, stage.p, N, true, st);
+  const size_t bytes = sizeof(double) * (size_t)N * s;
+  if (bytes >= kPinnedMin) {
+    w.h_stage.ensure(bytes);
+    double* h = reinterpret_cast<double*>(w.h_stage.p);
+    WGP_CUDA(cudaMemcpyAsync(h, stage.p, bytes, cudaMemcpyDeviceToHost, st));
+    WGP_CUDA(cudaStreamSynchronize(st));
+    host_copy_2d(V, ldv, h, N, N, s);
+    return;
+  }
   WGP_CUDA(cudaMemcpy2DAsync(V, sizeof(double) * ldv, stage.p, sizeof(double) * N,
                              sizeof(double) * N, s, cudaMemcpyDeviceToHost, st));
   WGP_CUDA(cudaStreamSynchronize(st));

@@ -34,6 +34,7 @@ struct SolverWork {
   DBuf<double> pwork;  // preconditioner chunk partials
   DBuf<double> tvec;   // M^T r  (k x s)
   DBuf<double> stage;  // host-boundary staging (column-major) for upload / download
+  PinnedBuf h_stage;   // pinned host staging of large uploads / downloads (upload_problem)
   void alloc(const Op& op, int s);
 };
 
