@@ -279,6 +279,11 @@ struct PrecondDev {
   double shift = 1.0;
   DBuf<double> L;    // [n][kpad] row-major (pivoted Cholesky factor)
   DBuf<double> M64;  // [n][kpad]  M = L C^{-T}, C = chol(shift I + L^T L): M M^T = L cap^{-1} L^T
+  // factorisation workspaces, kept (grown only) across builds: per-call cudaMalloc /
+  // synchronous cudaFree of them showed as sporadic 0.1-0.25 s stalls of a C3 solve
+  DBuf<double> w_d, w_pv, w_best2, w_all2, w_lpiv, w_part, w_G, w_W;
+  DBuf<int> w_used, w_kcount;
+  DBuf<int64_t> w_pi, w_dpiv;
 };
 void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStream_t st);
 void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd, cudaStream_t st);

@@ -391,19 +391,31 @@ void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStre
   WGP_CUDA(cudaMemsetAsync(pd.L.p, 0, sizeof(double) * std::max<int64_t>(nl, 1) * pd.kpad, st));
   const KParams p = op.kp();
   const double dval = p.s2 + p.noise2;  // stationary kernels: every diagonal entry is equal
-  DBuf<double> d(std::max<int64_t>(nl, 1));
-  DBuf<int> used(std::max<int64_t>(nl, 1));
+  DBuf<double>& d = pd.w_d;
+  DBuf<int>& used = pd.w_used;
+  d.ensure(std::max<int64_t>(nl, 1));
+  used.ensure(std::max<int64_t>(nl, 1));
   launch_fill<double>(d.p, dval, nl, st);
   WGP_CUDA(cudaMemsetAsync(used.p, 0, sizeof(int) * std::max<int64_t>(nl, 1), st));
   const double floor_ = 1e-12 * (dval > 0.0 ? dval : 0.0);  // solvers.cpp:77
   const int nb = 148 * 2;
-  DBuf<double> pv(nb), best2(2), all2((size_t)2 * ctx.world), lpiv(pd.kpad + 1);
-  DBuf<int64_t> pi(nb);
-  DBuf<int64_t> dpiv(1);
+  DBuf<double>& pv = pd.w_pv;
+  DBuf<double>& best2 = pd.w_best2;
+  DBuf<double>& all2 = pd.w_all2;
+  DBuf<double>& lpiv = pd.w_lpiv;
+  DBuf<int64_t>& pi = pd.w_pi;
+  DBuf<int64_t>& dpiv = pd.w_dpiv;
+  pv.ensure(nb);
+  best2.ensure(2);
+  all2.ensure((size_t)2 * ctx.world);
+  lpiv.ensure(pd.kpad + 1);
+  pi.ensure(nb);
+  dpiv.ensure(1);
   if (ctx.world == 1) {
     // no host synchronisation per pivot: selection, pivot row and the early stop all stay
     // on the device; one read of the achieved rank at the end
-    DBuf<int> kcount(1);
+    DBuf<int>& kcount = pd.w_kcount;
+    kcount.ensure(1);
     WGP_CUDA(cudaMemsetAsync(kcount.p, 0, sizeof(int), st));
     for (int64_t k = 0; k < rank; ++k) {
       argmax_partial_kernel<<<nb, 256, 0, st>>>(d.p, used.p, nl, r0, floor_, pv.p, pi.p);
@@ -460,7 +472,10 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   const KParams p = op.kp();
   const int nch = ceil_div(n, kChunkRows);
   const int c0 = (int)(pd.r0 / kChunkRows);
-  DBuf<double> part((size_t)padded_chunks(n, op.ctx->world) * k * k), G((size_t)k * k);
+  DBuf<double>& part = pd.w_part;
+  DBuf<double>& G = pd.w_G;
+  part.ensure((size_t)padded_chunks(n, op.ctx->world) * k * k);
+  G.ensure((size_t)k * k);
   if (pd.n_local > 0)
     chunk_atb_kernel<<<dim3(ceil_div(pd.n_local, kChunkRows), ceil_div(k, 64), ceil_div(k, 64)), 256, 0, st>>>(
         pd.L.p, (int)pd.kpad, k, pd.L.p, (int)pd.kpad, k, pd.n_local, part.p + (int64_t)c0 * k * k);
@@ -507,7 +522,8 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
     }
     for (int i = 0; i < k; ++i) W[(size_t)i * k + j] = x[i];
   }
-  DBuf<double> dW((size_t)k * k);
+  DBuf<double>& dW = pd.w_W;
+  dW.ensure((size_t)k * k);
   WGP_CUDA(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
   const int64_t nl = std::max<int64_t>(pd.n_local, 1);
   pd.M64.ensure((size_t)nl * pd.kpad);
@@ -518,7 +534,7 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   apply_upper_kernel<<<grid_rows(nl * pd.kpad), 256, smem, st>>>(
       pd.L.p, dW.p, pd.n_local, k, (int)pd.kpad, pd.M64.p, nullptr);
   WGP_CUDA(cudaGetLastError());
-  WGP_CUDA(cudaStreamSynchronize(st));  // dW / part / G are freed on return
+  WGP_CUDA(cudaStreamSynchronize(st));  // (dW is rewritten by the next build's host copy)
 }
 
 template <typename T>

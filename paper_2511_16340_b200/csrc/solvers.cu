@@ -568,8 +568,12 @@ void sgd_solve_batched(Op& op, const wgp_solver_config& cfg, const std::vector<u
     for (int64_t i = 0; i < N; ++i) idx[c][i] = i;
   }
   std::vector<int> hrows((size_t)s * batch, 0);
-  DBuf<int> drows((size_t)s * batch);
-  DBuf<double> g((size_t)s * batch), vel((size_t)n * s);
+  DBuf<int>& drows = w.sgd_rows;
+  DBuf<double>& g = w.sgd_g;
+  DBuf<double>& vel = w.sgd_vel;
+  drows.ensure((size_t)s * batch);
+  g.ensure((size_t)s * batch);
+  vel.ensure((size_t)std::max<int64_t>(n, 1) * s);
   WGP_CUDA(cudaMemsetAsync(vel.p, 0, sizeof(double) * n * s, st));
   WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
   for (int k = 1; k <= cfg.max_iters && n_active > 0; ++k) {
@@ -637,8 +641,12 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   WGP_REQUIRE(op.dim <= 32, "ap_solve: dim > 32 not supported on the device path");
   const int bs = (int)bs64;
   const int nblk = (int)((N + bs - 1) / bs);
-  DBuf<double> fac((size_t)nblk * bs * bs), inv((size_t)nblk * bs * bs);
-  DBuf<int> fail(1);
+  DBuf<double>& fac = w.ap_fac;
+  DBuf<double>& inv = w.ap_inv;
+  DBuf<int>& fail = w.ap_fail;
+  fac.ensure((size_t)nblk * bs * bs);
+  inv.ensure((size_t)nblk * bs * bs);
+  fail.ensure(1);
   WGP_CUDA(cudaMemsetAsync(fail.p, 0, sizeof(int), st));
   launch_block_chol(op, bs, nblk, fac.p, inv.p, fail.p, st);
   int hfail = 0;
@@ -659,14 +667,18 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   }
   const int nseg = (int)seg_start.size();
   seg_start.push_back(N);
-  DBuf<int64_t> dseg_start(seg_start.size());
-  DBuf<int> dseg_block(seg_block.size());
-  DBuf<double> segn((size_t)nseg * s), Rblk;
+  DBuf<int64_t>& dseg_start = w.ap_seg_start;
+  DBuf<int>& dseg_block = w.ap_seg_block;
+  DBuf<double>& segn = w.ap_segn;
+  DBuf<double>& Rblk = w.ap_rblk;
+  dseg_start.ensure(seg_start.size());
+  dseg_block.ensure(seg_block.size());
+  segn.ensure((size_t)nseg * s);
   WGP_CUDA(cudaMemcpyAsync(dseg_start.p, seg_start.data(), sizeof(int64_t) * seg_start.size(),
                            cudaMemcpyHostToDevice, st));
   WGP_CUDA(cudaMemcpyAsync(dseg_block.p, seg_block.data(), sizeof(int) * seg_block.size(),
                            cudaMemcpyHostToDevice, st));
-  if (ctx.world > 1) Rblk.alloc((size_t)bs * s);
+  if (ctx.world > 1) Rblk.ensure((size_t)bs * s);
   double* bnorm = w.scal.p + 3 * s;
   double* rel = w.scal.p + 4 * s;
   int* active = w.act.p;
@@ -685,8 +697,12 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
     n_active += hact[c];
   }
   if (n_active == 0) return;
-  DBuf<int> blk(s), dconf(s);
-  DBuf<double> delta((size_t)bs * s);
+  DBuf<int>& blk = w.ap_blk;
+  DBuf<int>& dconf = w.ap_conf;
+  DBuf<double>& delta = w.ap_delta;
+  blk.ensure(s);
+  dconf.ensure(s);
+  delta.ensure((size_t)bs * s);
   WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
   for (int k = 1; k <= cfg.max_iters && n_active > 0; ++k) {
     if (cfg.ap_ordering == WGP_AP_GREEDY) {

@@ -35,6 +35,10 @@ struct SolverWork {
   DBuf<double> tvec;   // M^T r  (k x s)
   DBuf<double> stage;  // host-boundary staging (column-major) for upload / download
   PinnedBuf h_stage;   // pinned host staging of large uploads / downloads (upload_problem)
+  // SGD / AP workspaces (grown only: no per-solve cudaMalloc / synchronous cudaFree)
+  DBuf<int> sgd_rows, ap_fail, ap_seg_block, ap_blk, ap_conf;
+  DBuf<double> sgd_g, sgd_vel, ap_fac, ap_inv, ap_segn, ap_rblk, ap_delta;
+  DBuf<int64_t> ap_seg_start;
   void alloc(const Op& op, int s);
 };
 
