@@ -49,6 +49,13 @@ void set_last_error(const char* msg);  // the thread-local message of wgp_last_e
     if (!(cond)) ::wgp::throw_error(WGP_INVALID_ARGUMENT, __VA_ARGS__); \
   } while (0)
 
+// Device block cache (mem.cpp): freed blocks are kept per (device, size bucket) and handed
+// out again instead of a new cudaMalloc; a free synchronises the device first, as cudaFree
+// did, so a cached block is never still in use by queued work.  Per-call cudaMalloc /
+// cudaFree pairs showed as sporadic 0.1-0.25 s stalls of the solves.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
+
 // Owning device buffer.
 template <typename T>
 struct DBuf {
@@ -66,11 +73,11 @@ struct DBuf {
   ~DBuf() { release(); }
   void alloc(size_t count) {
     release();
-    if (count) WGP_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
     n = count;
   }
   void ensure(size_t count) { if (count > n) alloc(count); }
-  void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+  void release() { if (p) dev_free(p, n * sizeof(T)); p = nullptr; n = 0; }
 };
 
 // Owning pinned host buffer (async device-to-host copies of per-iteration records).
