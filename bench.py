@@ -599,8 +599,14 @@ def run_ours(args):
     # The MMAs the kernel issues are kind::f16 three-term hi/lo splits (fp32 accumulate),
     # so the fraction against the f16 dense peak of those instructions is listed as well,
     # and the composite (SFU) bound that actually limits the Matern map.
-    peak_tf32 = peaks["bf16_tflops"] / 2.0
-    peak_f16 = peaks["bf16_tflops"]
+    # The timed region is 100 back-to-back steps that hold the board at its power cap, i.e. a
+    # kernel timed inside a long sustained run: the roofline denominator is the SUSTAINED
+    # measured figure (MEASURED_PEAKS.json bf16_tflops_sustained, matmuls back to back for
+    # 4 s), the burst one listed alongside.
+    peak_tf32_burst = peaks["bf16_tflops"] / 2.0
+    sustained = peaks.get("bf16_tflops_sustained")
+    peak_tf32 = sustained / 2.0 if sustained else peak_tf32_burst
+    peak_f16 = sustained if sustained else peaks["bf16_tflops"]
     sm_hz = peaks.get("sm_max_mhz", 1965.0) * 1e6
     pairs = float(n) * float(n)
     # Matern-3/2: sqrt + exp2 per pair, one exp2 in eight on the FMA pipe (kmatvec_tc.cu
@@ -616,13 +622,13 @@ def run_ours(args):
             # ncu --set full capture of this workload (profiles/r02h_kmatvec_tc_metrics.json):
             # X/XA/XB and the V tiles stay L2-resident, HBM sees little more than V/Y once.
             "traffic": TRAFFIC_BYTES,
-            "peak_source": f"{peak_kind} bf16_tflops/2 (TF32 dense) from MEASURED_PEAKS.json",
+            "peak_source": (f"{peak_kind} bf16_tflops_sustained/2 (TF32 dense, sustained: the timed loop "
+                            "runs at the board power cap) from MEASURED_PEAKS.json" if sustained else
+                            f"{peak_kind} bf16_tflops/2 (TF32 dense) from MEASURED_PEAKS.json"),
+            "frac_vs_burst_tf32": achieved / peak_tf32_burst if achieved else None,
+            "burst_tf32_peak": peak_tf32_burst,
             "frac_vs_f16_dense": achieved / peak_f16 if achieved else None,
             "f16_dense_peak": peak_f16,
-            # the 100-step loop runs at the board power cap: against the sustained bf16/2
-            # figure of MEASURED_PEAKS.json (back-to-back matmuls for 4 s) as well
-            "frac_vs_sustained_tf32": (achieved / (peaks["bf16_tflops_sustained"] / 2.0)
-                                       if achieved and peaks.get("bf16_tflops_sustained") else None),
             "mma_kind": "kind::f16, 3-term hi/lo splits of K and V (and of x for the distance "
                         "GEMM), fp32 accumulation in TMEM",
             "kernel": "tc::kmatvec_tc_kernel (CUDA events around its launches, "
