@@ -322,11 +322,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
   uint64_t* v_full = xb_empty + NSX;      // [NSV] bulk copy -> GEMM2
   uint64_t* v_empty = v_full + NSV;       // [NSV] GEMM2 -> V producer
   uint64_t* xa_full = v_empty + NSV;
-  uint64_t* s_full = xa_full + 1;         // [MAX_NB] GEMM1 -> epilogue
-  uint64_t* k_full = s_full + MAX_NB;     // [MAX_NB] epilogue -> GEMM2 (8 arrivals)
-  uint64_t* b_free = k_full + MAX_NB;     // [MAX_NB] GEMM2 -> GEMM1
-  uint64_t* k_half = b_free + MAX_NB;     // [MAX_NB] first half of each warp's K columns (BJ_ 128)
-  uint64_t* y_full = k_half + MAX_NB;     // [2] chunk accumulator done (GEMM2 commit)
+  // Per (TMEM buffer, column half) at BJ_ = 128 -- index 2 b + h -- so each half of a tile
+  // flows on its own: the epilogue warps of column half h (their own warps) wait only for
+  // S(t, h), GEMM2 issues the K-steps of half h as soon as K(t, h) is complete, and GEMM1 of
+  // tile t + NB writes half h once GEMM2 has read K(t, h).  With three buffers for three
+  // epilogue sets the set mapping tile t waits for the buffer of tile t itself: the halves
+  // shorten that round trip.  At BJ_ = 64 only index 2 b is used (the whole tile).
+  constexpr bool HALVES = BJ_ == 128;
+  uint64_t* s_full = xa_full + 1;         // [2 MAX_NB] GEMM1 -> epilogue
+  uint64_t* k_full = s_full + 2 * MAX_NB; // [2 MAX_NB] epilogue -> GEMM2
+  uint64_t* b_free = k_full + 2 * MAX_NB; // [2 MAX_NB] GEMM2 -> GEMM1
+  uint64_t* y_full = b_free + 2 * MAX_NB; // [2] chunk accumulator done (GEMM2 commit)
   uint64_t* y_free = y_full + 2;          // [2] chunk accumulator drained (drain warps)
   uint64_t* c_full = y_free + 2;          // correction accumulator final (last commit)
   uint64_t* acc_zero = c_full + 1;        // accumulators zeroed (drain warps, merged GEMM2)
@@ -354,10 +360,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     ptx::mbar_init(c_full, 1);
     ptx::mbar_init(acc_zero, NDRAIN);
     for (int i = 0; i < MAX_NB; ++i) {
-      ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&k_full[i], SETW);
-      ptx::mbar_init(&k_half[i], SETW);
-      ptx::mbar_init(&b_free[i], 1);
+      for (int h = 0; h < 2; ++h) {
+        ptx::mbar_init(&s_full[2 * i + h], 1);
+        ptx::mbar_init(&k_full[2 * i + h], HALVES ? SETW / 2 : SETW);
+        ptx::mbar_init(&b_free[2 * i + h], 1);
+      }
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&y_full[i], 1);
@@ -423,7 +430,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
     // in uniform registers: a single-lane loop measured 3x slower MMA issue); one elected lane
     // issues.
     if (role == 1) {
-      const uint32_t idesc1 = p.g1f16 ? ptx::idesc_f16(BM, BJ_) : ptx::idesc_tf32(BM, BJ_);
+      constexpr int G1N = HALVES ? BJ_ / 2 : BJ_;  // GEMM1 N per instruction group
+      const uint32_t idesc1 = p.g1f16 ? ptx::idesc_f16(BM, G1N) : ptx::idesc_tf32(BM, G1N);
       const uint64_t dXA = ptx::umma_desc(ptx::smem_u32(sXA), 128, sbo1);
       const uint64_t dXB0 = ptx::umma_desc(ptx::smem_u32(sXB), 128, sbo1);
       const uint64_t xb_step = (uint64_t)(XB_BYTES >> 4);  // descriptor start-address units
@@ -432,22 +440,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       uint32_t ph1 = 0, phb1 = 0;
       for (int t = 0; t < T; ++t) {
         ptx::mbar_wait(&xb_full[st1], ph1);
-        if (t >= NB) ptx::mbar_wait(&b_free[b1], phb1 ^ 1);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          trace_ev(p, t, 0);
-          const uint64_t dB = dXB0 + xb_step * st1;
-          if (p.g1f16) {
-            for (int ks = 0; ks < KS1; ++ks)
-              ptx::mma_f16_ss(tmem + b1 * BJ_, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
-          } else {
-            for (int ks = 0; ks < KS1; ++ks)
-              ptx::mma_tf32_ss(tmem + b1 * BJ_, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+#pragma unroll
+        for (int h = 0; h < (HALVES ? 2 : 1); ++h) {
+          if (t >= NB) ptx::mbar_wait(&b_free[2 * b1 + h], phb1 ^ 1);
+          ptx::tc_fence_after();
+          if (ptx::elect_one()) {
+            if (h == 0) trace_ev(p, t, 0);
+            // half h: XB rows 64 h.. (eight 8-row groups of sbo1 bytes further), S columns 64 h..
+            const uint64_t dB = dXB0 + xb_step * st1 + (uint64_t)h * ((8 * sbo1) >> 4);
+            const uint32_t dS = tmem + b1 * BJ_ + h * G1N;
+            if (p.g1f16) {
+              for (int ks = 0; ks < KS1; ++ks)
+                ptx::mma_f16_ss(dS, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+            } else {
+              for (int ks = 0; ks < KS1; ++ks)
+                ptx::mma_tf32_ss(dS, dXA + 16 * ks, dB + 16 * ks, idesc1, ks > 0 ? 1u : 0u);
+            }
+            ptx::mma_commit(&s_full[2 * b1 + h]);
+            if (h == (HALVES ? 1 : 0)) ptx::mma_commit(&xb_empty[st1]);
           }
-          ptx::mma_commit(&s_full[b1]);
-          ptx::mma_commit(&xb_empty[st1]);
+          __syncwarp();
         }
-        __syncwarp();
         if (++st1 == NSX) { st1 = 0; ph1 ^= 1; }
         if (++b1 == NB) { b1 = 0; phb1 ^= 1; }
       }
@@ -479,34 +492,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
           ptx::mma_f16_ts(yacc + AW, kb + ks * 16 + 8, dv, idesc2, 1u);  // C += Kl Vh
 #endif
         };
-        if (BJ_ == 128) {
-          // K arrives in two halves (each epilogue warp signals after the first half of its
-          // 64 columns): the K-steps of those columns (0, 1 of each warp half: ks 0, 1, 4, 5)
-          // are issued while the epilogue maps the rest, so the buffer frees (and GEMM1 of the
-          // set's next tile starts) earlier
-          ptx::mbar_wait(&k_half[b2], phb2);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-            trace_ev(p, t, 1);
-            issue(0); issue(1); issue(4); issue(5);
+        if (HALVES) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            ptx::mbar_wait(&k_full[2 * b2 + h], phb2);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+              if (h == 0) trace_ev(p, t, 1);
+#pragma unroll
+              for (int ks = 4 * h; ks < 4 * h + 4; ++ks) issue(ks);
+              ptx::mma_commit(&b_free[2 * b2 + h]);  // K(t, h) read: GEMM1 may rewrite half h
+            }
+            __syncwarp();
           }
-          __syncwarp();
-          ptx::mbar_wait(&k_full[b2], phb2);
-          ptx::tc_fence_after();
         } else {
-          ptx::mbar_wait(&k_full[b2], phb2);
+          ptx::mbar_wait(&k_full[2 * b2], phb2);
           ptx::tc_fence_after();
         }
         if (ptx::elect_one()) {
-          if (BJ_ == 128) {
-            issue(2); issue(3); issue(6); issue(7);
-          } else {
+          if (!HALVES) {
             trace_ev(p, t, 1);
 #pragma unroll
             for (int ks = 0; ks < BJ_ / 16; ++ks) issue(ks);
+            ptx::mma_commit(&b_free[2 * b2]);
           }
           trace_ev(p, t, 10);
-          ptx::mma_commit(&b_free[b2]);
           ptx::mma_commit(&v_empty[st2]);
           if (last) ptx::mma_commit(&y_full[ya]);
           if (t == T - 1) ptx::mma_commit(c_full);  // the correction accumulators are final
@@ -536,7 +546,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
       const uint32_t bph = (t / NB) & 1;
       const bool tr = lane == 0 && q == 0 && half == 0 && set == 0;
       if (tr) trace_ev(p, t, 2);
-      ptx::mbar_wait(&s_full[b], bph);
+      ptx::mbar_wait(&s_full[2 * b + (HALVES ? half : 0)], bph);
       ptx::tc_fence_after();
       if (tr) trace_ev(p, t, 3);
       const int64_t gj_base = p.col0 + (int64_t)(jt0 + t) * BJ_ + half * CPW_;
@@ -587,18 +597,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmatvec_tc_kernel(const Params p,
           ptx::tmem_st8(col, hi);
           ptx::tmem_st8(col + 8, lo);
         }
-        if (BJ_ == 128 && g0 + GW == CPW_ / 2) {  // first half of this warp's columns in TMEM
-          ptx::tmem_wait_st();
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&k_half[b]);
-        }
       }
       if (tr) trace_ev(p, t, 4);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&k_full[b]);
+      if (lane == 0) ptx::mbar_arrive(&k_full[2 * b + (HALVES ? half : 0)]);
       if (tr) trace_ev(p, t, 5);
       if (lane == 0 && half == 0 && set == 0 && q == 3) trace_ev(p, t, 11);
     }
