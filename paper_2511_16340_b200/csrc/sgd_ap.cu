@@ -233,32 +233,67 @@ __global__ void __launch_bounds__(512) block_chol_kernel(const double* __restric
 // delta_c = L^-T (L^-1 r_c[B]) for the column's chosen block; v_c[B] += delta_c.  The block's
 // residual rows come from the full residual R (rows [start, start + len)) or, when Rblk is
 // given, from the gathered block rows Rblk[i][c] (sharded solves).
-__global__ void __launch_bounds__(1024) ap_block_solve_kernel(
+// delta = (L L^T)^{-1} r_B for each active column's chosen block, with Li = L^{-1} (lower,
+// block_chol): y = Li r in ap_block_y_kernel, delta = Li^T y (and v_B += delta) in
+// ap_block_delta_kernel.  Grids of (column, row slice) CTAs -- one CTA per column left 131 of
+// 148 SMs idle (138 us per iteration at C2) -- and y's rows by warps with lanes along k, so
+// the reads of Li are coalesced (one thread per row of Li read it 4 KB apart).  Fixed orders:
+// y[i] = 32-lane partial sums over k combined by xor-shuffle; delta[j] = 8 warp partials (rows
+// i = w mod 8, ascending) added in warp order.
+constexpr int kApRowsPerCta = 32;
+__global__ void __launch_bounds__(256) ap_block_y_kernel(
     const double* __restrict__ inv, int bs, int64_t n, const int* __restrict__ blk,
     const int* __restrict__ active, const double* __restrict__ R, const double* __restrict__ Rblk,
-    int s, double* __restrict__ V, double* __restrict__ delta) {
-  const int c = blockIdx.x;
+    int s, double* __restrict__ ybuf) {
+  const int c = blockIdx.y;
   if (!active[c]) return;
-  extern __shared__ double sh[];
-  double* rb = sh;        // bs
-  double* y = sh + bs;    // bs
+  extern __shared__ double rb[];  // bs
   const int64_t start = (int64_t)blk[c] * bs;
   const int len = (int)min((int64_t)bs, n - start);
   const double* Li = inv + (int64_t)blk[c] * bs * bs;
   for (int i = threadIdx.x; i < len; i += blockDim.x)
     rb[i] = Rblk ? Rblk[(int64_t)i * s + c] : R[(start + i) * s + c];
   __syncthreads();
-  for (int i = threadIdx.x; i < len; i += blockDim.x) {  // y = L^-1 r  (lower)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = blockIdx.x * kApRowsPerCta;
+  for (int i = i0 + warp; i < min(len, i0 + kApRowsPerCta); i += blockDim.x / 32) {
     double a = 0.0;
-    for (int k = 0; k <= i; ++k) a = fma(Li[i * bs + k], rb[k], a);
-    y[i] = a;
+    for (int k = lane; k <= i; k += 32) a = fma(Li[(int64_t)i * bs + k], rb[k], a);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) ybuf[(int64_t)i * s + c] = a;
   }
+}
+
+__global__ void __launch_bounds__(256) ap_block_delta_kernel(
+    const double* __restrict__ inv, int bs, int64_t n, const int* __restrict__ blk,
+    const int* __restrict__ active, const double* __restrict__ ybuf, int s, double* __restrict__ V,
+    double* __restrict__ delta) {
+  // CTA = (32 consecutive j, column c); warp w adds rows i = j0 + w, j0 + w + 8, ... (lanes
+  // along j: coalesced rows of Li), the 8 warp partials are then added in warp order
+  const int c = blockIdx.y;
+  if (!active[c]) return;
+  __shared__ double part[8][32];
+  extern __shared__ double ys[];  // y[j0 .. len)
+  const int64_t start = (int64_t)blk[c] * bs;
+  const int len = (int)min((int64_t)bs, n - start);
+  const double* Li = inv + (int64_t)blk[c] * bs * bs;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = blockIdx.x * 32, j = j0 + lane;
+  for (int i = j0 + threadIdx.x; i < len; i += blockDim.x) ys[i - j0] = ybuf[(int64_t)i * s + c];
   __syncthreads();
-  for (int j = threadIdx.x; j < len; j += blockDim.x) {  // delta = L^-T y
-    double a = 0.0;
-    for (int i = j; i < len; ++i) a = fma(Li[i * bs + j], y[i], a);
-    delta[(int64_t)j * s + c] = a;
-    V[(start + j) * s + c] += a;
+  double a = 0.0;
+  if (j < len)
+    for (int i = j0 + warp; i < len; i += 8)
+      if (i >= j) a = fma(Li[(int64_t)i * bs + j], ys[i - j0], a);
+  part[warp][lane] = a;
+  __syncthreads();
+  if (warp == 0 && j < len) {
+    double d = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) d += part[w][lane];
+    delta[(int64_t)j * s + c] = d;
+    V[(start + j) * s + c] += d;
   }
 }
 
@@ -287,27 +322,32 @@ __global__ void seg_norms_kernel(const double* __restrict__ Rloc, int64_t r0, in
   }
 }
 
-__global__ void greedy_from_segments_kernel(const double* __restrict__ segn,
-                                            const int* __restrict__ seg_block, int nseg, int nblk,
-                                            int s, const int* __restrict__ active,
-                                            int* __restrict__ blk) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < s; c += gridDim.x * blockDim.x) {
-    if (!active[c]) continue;
-    double best = -1.0, cur = 0.0;
-    int arg = 0;
-    for (int g = 0; g < nseg; ++g) {
-      cur += segn[(int64_t)g * s + c];
-      if (g + 1 == nseg || seg_block[g + 1] != seg_block[g]) {
-        const double nrm = sqrt(cur);
-        if (nrm > best) {
-          best = nrm;
-          arg = seg_block[g];
-        }
-        cur = 0.0;
+__global__ void __launch_bounds__(128) greedy_from_segments_kernel(
+    const double* __restrict__ segn, const int* __restrict__ seg_block, int nseg, int nblk, int s,
+    const int* __restrict__ active, int* __restrict__ blk) {
+  // one block per column: the segment norms load in parallel (the single-thread scan of
+  // round 1 was a chain of dependent L2 loads, 48 us at C2), then one thread adds each
+  // block's segments in order and takes the argmax
+  extern __shared__ double sn[];  // nseg
+  const int c = blockIdx.x;
+  if (!active[c]) return;
+  for (int g = threadIdx.x; g < nseg; g += blockDim.x) sn[g] = segn[(int64_t)g * s + c];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double best = -1.0, cur = 0.0;
+  int arg = 0;
+  for (int g = 0; g < nseg; ++g) {
+    cur += sn[g];
+    if (g + 1 == nseg || seg_block[g + 1] != seg_block[g]) {
+      const double nrm = sqrt(cur);
+      if (nrm > best) {
+        best = nrm;
+        arg = seg_block[g];
       }
+      cur = 0.0;
     }
-    blk[c] = arg;
   }
+  blk[c] = arg;
 }
 
 // Rows of each active column's chosen block that this rank owns -> Rblk[i][c] (0 for rows of
@@ -439,12 +479,12 @@ void launch_block_chol(const Op& op, int bs, int nblk, double* fac, double* inv,
 
 void launch_ap_block_solve(const double* inv, int bs, int64_t n, const int* blk, const int* active,
                            const double* R, const double* Rblk, int s, double* V, double* delta,
-                           cudaStream_t st) {
-  const size_t smem = sizeof(double) * 2 * bs;
-  if (smem > 48 * 1024)
-    WGP_CUDA(cudaFuncSetAttribute(ap_block_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-  ap_block_solve_kernel<<<s, 1024, smem, st>>>(inv, bs, n, blk, active, R, Rblk, s, V, delta);
+                           double* ybuf, cudaStream_t st) {
+  const size_t smem = sizeof(double) * bs;  // <= 8 KB (bs <= 1024)
+  ap_block_y_kernel<<<dim3((unsigned)ceil_div(bs, kApRowsPerCta), (unsigned)s), 256, smem, st>>>(
+      inv, bs, n, blk, active, R, Rblk, s, ybuf);
+  ap_block_delta_kernel<<<dim3((unsigned)ceil_div(bs, 32), (unsigned)s), 256, smem, st>>>(
+      inv, bs, n, blk, active, ybuf, s, V, delta);
   WGP_CUDA(cudaGetLastError());
 }
 
@@ -456,7 +496,12 @@ void launch_seg_norms(const double* Rloc, int64_t r0, int64_t nloc, const int64_
 
 void launch_greedy_from_segments(const double* segn, const int* seg_block, int nseg, int nblk, int s,
                                  const int* active, int* blk, cudaStream_t st) {
-  greedy_from_segments_kernel<<<(s + 63) / 64, 64, 0, st>>>(segn, seg_block, nseg, nblk, s, active, blk);
+  const size_t smem = sizeof(double) * (size_t)std::max(nseg, 1);
+  if (smem > 48 * 1024)
+    WGP_CUDA(cudaFuncSetAttribute(greedy_from_segments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::min<size_t>(smem, 227 * 1024)));
+  WGP_REQUIRE(smem <= 227 * 1024, "ap_solve: too many row segments for the greedy choice");
+  greedy_from_segments_kernel<<<s, 128, smem, st>>>(segn, seg_block, nseg, nblk, s, active, blk);
   WGP_CUDA(cudaGetLastError());
 }
 

@@ -703,6 +703,7 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
   blk.ensure(s);
   dconf.ensure(s);
   delta.ensure((size_t)bs * s);
+  w.ap_y.ensure((size_t)bs * s);
   WGP_CUDA(cudaMemcpyAsync(active, hact.data(), sizeof(int) * s, cudaMemcpyHostToDevice, st));
   for (int k = 1; k <= cfg.max_iters && n_active > 0; ++k) {
     if (cfg.ap_ordering == WGP_AP_GREEDY) {
@@ -717,7 +718,7 @@ void ap_solve_batched(Op& op, const wgp_solver_config& cfg, SolverWork<double>& 
       dist_allreduce_sum(ctx, Rblk.p, (size_t)bs * s, st);
     }
     launch_ap_block_solve(inv.p, bs, N, blk.p, active, Rloc, ctx.world > 1 ? Rblk.p : nullptr, s,
-                          w.V.p, delta.p, st);
+                          w.V.p, delta.p, w.ap_y.p, st);
     launch_kcols(op, blk.p, bs, delta.p, s, active, Rloc, r0, n, st);  // r -= H[:, B] delta
     if (k % nblk == 0) launch_residual(op, w.B.p, w.V.p, Rloc, s, st);  // drift refresh
     residual_norms(ctx, w, Rloc, bnorm, rel, hrel, st);

@@ -37,7 +37,7 @@ struct SolverWork {
   PinnedBuf h_stage;   // pinned host staging of large uploads / downloads (upload_problem)
   // SGD / AP workspaces (grown only: no per-solve cudaMalloc / synchronous cudaFree)
   DBuf<int> sgd_rows, ap_fail, ap_seg_block, ap_blk, ap_conf;
-  DBuf<double> sgd_g, sgd_vel, ap_fac, ap_inv, ap_segn, ap_rblk, ap_delta;
+  DBuf<double> sgd_g, sgd_vel, ap_fac, ap_inv, ap_segn, ap_rblk, ap_delta, ap_y;
   DBuf<int64_t> ap_seg_start;
   void alloc(const Op& op, int s);
 };
@@ -181,7 +181,7 @@ void launch_block_chol(const Op& op, int bs, int nblk, double* fac, double* inv,
                        cudaStream_t st);
 void launch_ap_block_solve(const double* inv, int bs, int64_t n, const int* blk, const int* active,
                            const double* R, const double* Rblk, int s, double* V, double* delta,
-                           cudaStream_t st);
+                           double* ybuf, cudaStream_t st);
 void launch_seg_norms(const double* Rloc, int64_t r0, int64_t nloc, const int64_t* seg_start, int nseg,
                       int s, const int* active, double* segn, cudaStream_t st);
 void launch_greedy_from_segments(const double* segn, const int* seg_block, int nseg, int nblk, int s,
