@@ -146,6 +146,10 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
     __syncthreads();
     if (valid) {
       const int m = min(64, len - j0);
+      // the diagonal entry of this tile, if row i lies in it (a 32-bit compare per pair
+      // instead of a 64-bit index sum and compare)
+      const int64_t dl = i - (start + j0);
+      const int jd = (dl >= 0 && dl < m) ? (int)dl : -1;
       for (int jj = 0; jj < m; ++jj) {
         T d2 = T(0);
 #pragma unroll
@@ -154,7 +158,7 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
           d2 = fma(df, df, d2);
         }
         T kv;
-        if (start + j0 + jj == i) {
+        if (jj == jd) {
           kv = kdiag;
         } else if (p.kind == WGP_RBF) {
           kv = s2 * kexp(-c1 * d2);
