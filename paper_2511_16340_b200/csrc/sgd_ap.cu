@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
     __syncthreads();
     if (valid) {
       const int jn = (int)(j_hi - j0 < 64 ? j_hi - j0 : 64);
+      const int64_t dl = row - j0;  // the diagonal entry's position in this tile, if any
+      const int jd = (dl >= 0 && dl < jn) ? (int)dl : -1;
       for (int jj = sub; jj < jn; jj += 4) {
         T d2 = T(0);
 #pragma unroll
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
           d2 = fma(df, df, d2);
         }
         T kv;
-        if (j0 + jj == row) {
+        if (jj == jd) {
           kv = kdiag;
         } else if (p.kind == WGP_RBF) {
           kv = s2 * kexp(-c1 * d2);
