@@ -77,6 +77,8 @@ struct DBuf {
     n = count;
   }
   void ensure(size_t count) { if (count > n) alloc(count); }
+  // for buffers sized by a growing system (append_rows sweeps): 25% headroom per reallocation
+  void ensure_grow(size_t count) { if (count > n) alloc(count + count / 4); }
   void release() { if (p) dev_free(p, n * sizeof(T)); p = nullptr; n = 0; }
 };
 

@@ -1095,7 +1095,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     const size_t vt_halves = (size_t)nsub * tc::BJ * s_pad * 2;
     // (+ the per-column max bits, 8-byte aligned, after the scales)
     const size_t vt_floats = ((vt_halves + 1) / 2 + 1) & ~(size_t)1;
-    vt_scratch.ensure(vt_floats + 2 * (size_t)s_pad + 64 + 2 * (size_t)tc::MAX_SPAD);
+    vt_scratch.ensure_grow(vt_floats + 2 * (size_t)s_pad + 64 + 2 * (size_t)tc::MAX_SPAD);
     __half* vt = reinterpret_cast<__half*>(vt_scratch.p);
     float* sc_up = vt_scratch.p + vt_floats + 32;
     float* sc_down = sc_up + s_pad;
@@ -1138,7 +1138,7 @@ void launch_kmatvec_tc(const Op& op, const float* XA_all, const float* XB, int64
     const int nsplit = forced_splits > 0 ? forced_splits : tc::choose_splits(row_ctas, ntiles);
     prm.tiles_per_split = (ntiles + nsplit - 1) / nsplit;
     const int gy = (ntiles + prm.tiles_per_split - 1) / prm.tiles_per_split;
-    ysplit.ensure(((size_t)gy * nrows_p * s_pad + 1) / 2);  // fp32 partials in fp64 storage
+    ysplit.ensure_grow(((size_t)gy * nrows_p * s_pad + 1) / 2);  // fp32 partials in fp64 storage
     prm.Ypart = reinterpret_cast<float*>(ysplit.p);
     prm.s = sc;
     prm.s_pad = s_pad;

@@ -387,14 +387,14 @@ void build_pivoted_cholesky(const Op& op, int64_t rank, PrecondDev& pd, cudaStre
   pd.k = 0;
   pd.kpad = rank > 0 ? ((rank + 3) / 4) * 4 : 0;
   if (rank == 0) return;
-  pd.L.ensure((size_t)std::max<int64_t>(nl, 1) * pd.kpad);
+  pd.L.ensure_grow((size_t)std::max<int64_t>(nl, 1) * pd.kpad);
   WGP_CUDA(cudaMemsetAsync(pd.L.p, 0, sizeof(double) * std::max<int64_t>(nl, 1) * pd.kpad, st));
   const KParams p = op.kp();
   const double dval = p.s2 + p.noise2;  // stationary kernels: every diagonal entry is equal
   DBuf<double>& d = pd.w_d;
   DBuf<int>& used = pd.w_used;
-  d.ensure(std::max<int64_t>(nl, 1));
-  used.ensure(std::max<int64_t>(nl, 1));
+  d.ensure_grow(std::max<int64_t>(nl, 1));
+  used.ensure_grow(std::max<int64_t>(nl, 1));
   launch_fill<double>(d.p, dval, nl, st);
   WGP_CUDA(cudaMemsetAsync(used.p, 0, sizeof(int) * std::max<int64_t>(nl, 1), st));
   const double floor_ = 1e-12 * (dval > 0.0 ? dval : 0.0);  // solvers.cpp:77
@@ -474,7 +474,7 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   const int c0 = (int)(pd.r0 / kChunkRows);
   DBuf<double>& part = pd.w_part;
   DBuf<double>& G = pd.w_G;
-  part.ensure((size_t)padded_chunks(n, op.ctx->world) * k * k);
+  part.ensure_grow((size_t)padded_chunks(n, op.ctx->world) * k * k);
   G.ensure((size_t)k * k);
   if (pd.n_local > 0)
     chunk_atb_kernel<<<dim3(ceil_div(pd.n_local, kChunkRows), ceil_div(k, 64), ceil_div(k, 64)), 256, 0, st>>>(
@@ -526,7 +526,7 @@ void finish_preconditioner(const Op& op, double shift, int mode, PrecondDev& pd,
   dW.ensure((size_t)k * k);
   WGP_CUDA(cudaMemcpyAsync(dW.p, W.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
   const int64_t nl = std::max<int64_t>(pd.n_local, 1);
-  pd.M64.ensure((size_t)nl * pd.kpad);
+  pd.M64.ensure_grow((size_t)nl * pd.kpad);
   const size_t smem = sizeof(double) * k * k;
   if (smem > 48 * 1024)
     WGP_CUDA(cudaFuncSetAttribute(apply_upper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

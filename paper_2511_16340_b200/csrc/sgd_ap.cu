@@ -37,6 +37,18 @@ __device__ __forceinline__ float kexp(float x) { return expf(x); }
 // threads per row take every 4th j of each 64-column tile.  Partial sums go to
 // part[z][c][i] and krows_sum_kernel adds the ranges in order: the j ranges depend on n only,
 // so a row's value is the same whichever rank owns it.
+// One 64-row tile row of coordinates into registers as 16-byte vector loads: the per-pair
+// coordinate reads of krows / kcols were one 4- or 8-byte shared load per dimension (8 per pair
+// at d = 8: the kernels were shared-load bound); all lanes read the same row (broadcast).
+template <typename T, int DMAX>
+__device__ __forceinline__ void load_row(const T (&row)[DMAX], T (&out)[DMAX]) {
+  static_assert((DMAX * sizeof(T)) % 16 == 0, "rows of whole 16-byte vectors");
+  const uint4* src = reinterpret_cast<const uint4*>(row);
+  uint4* dst = reinterpret_cast<uint4*>(out);
+#pragma unroll
+  for (int q = 0; q < (int)(DMAX * sizeof(T) / 16); ++q) dst[q] = src[q];
+}
+
 template <typename T, int DMAX>
 __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int dpad, int dim,
                                                     int64_t n, int64_t jlen,
@@ -47,7 +59,7 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
                                                     double* __restrict__ part) {
   const int c = blockIdx.y;
   if (!active[c]) return;
-  __shared__ T sX[64][DMAX + 1];
+  __shared__ __align__(16) T sX[64][DMAX];  // rows read whole: 16-byte vector loads (broadcast)
   __shared__ double sV[64];
   __shared__ double red[256];
   const int tid = threadIdx.x;
@@ -76,9 +88,11 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
       const int jd = (dl >= 0 && dl < jn) ? (int)dl : -1;
       for (int jj = sub; jj < jn; jj += 4) {
         T d2 = T(0);
+        T xj[DMAX];
+        load_row<T, DMAX>(sX[jj], xj);
 #pragma unroll
         for (int k = 0; k < DMAX; ++k) {
-          const T df = xr[k] - sX[jj][k];
+          const T df = xr[k] - xj[k];
           d2 = fma(df, df, d2);
         }
         T kv;
@@ -126,7 +140,7 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
   // rows r0 .. r0 + nrows of the operator (this rank's), R holds those rows
   const int c = blockIdx.y;
   if (!active[c]) return;
-  __shared__ T sX[64][DMAX + 1];
+  __shared__ __align__(16) T sX[64][DMAX];  // rows read whole: 16-byte vector loads (broadcast)
   __shared__ double sD[64];
   const int64_t il = (int64_t)blockIdx.x * 128 + threadIdx.x;
   const bool valid = il < nrows;
@@ -154,9 +168,11 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
       const int jd = (dl >= 0 && dl < m) ? (int)dl : -1;
       for (int jj = 0; jj < m; ++jj) {
         T d2 = T(0);
+        T xj[DMAX];
+        load_row<T, DMAX>(sX[jj], xj);
 #pragma unroll
         for (int k = 0; k < DMAX; ++k) {
-          const T df = xr[k] - sX[jj][k];
+          const T df = xr[k] - xj[k];
           d2 = fma(df, df, d2);
         }
         T kv;

@@ -119,18 +119,18 @@ void SolverWork<T>::alloc(const Op& op, int s_) {
   const int world = op.ctx->world;
   const size_t ns = (size_t)std::max<int64_t>(n, 1) * s, Ns = (size_t)padded_rows(N, world) * s;
   const size_t pch = (size_t)padded_chunks(N, world);
-  V.ensure(Ns);
-  P.ensure(Ns);
-  R.ensure(ns);
-  Z.ensure(ns);
-  HP.ensure(ns);
-  B.ensure(ns);
+  V.ensure_grow(Ns);
+  P.ensure_grow(Ns);
+  R.ensure_grow(ns);
+  Z.ensure_grow(ns);
+  HP.ensure_grow(ns);
+  B.ensure_grow(ns);
   if (op.resid_mode == WGP_RESIDUAL_ANCHORED && !op.f64()) {
-    VA.ensure(Ns);
-    RA.ensure(ns);
-    anc.ensure((size_t)4 * s);
+    VA.ensure_grow(Ns);
+    RA.ensure_grow(ns);
+    anc.ensure_grow((size_t)4 * s);
   }
-  part.ensure(pch * 2 * s);
+  part.ensure_grow(pch * 2 * s);
   scal.ensure((size_t)6 * s);
   act.ensure((size_t)2 * s + 2);
 }
