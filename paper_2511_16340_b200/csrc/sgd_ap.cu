@@ -59,7 +59,10 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
                                                     double* __restrict__ part) {
   const int c = blockIdx.y;
   if (!active[c]) return;
-  __shared__ __align__(16) T sX[64][DMAX];  // rows read whole: 16-byte vector loads (broadcast)
+  // fp32 rows read whole with 16-byte vector loads (broadcast): krows 323 -> 304 us at C2;
+  // fp64 rows keep per-element loads (the vector form measured 596 -> 726 us there)
+  constexpr int PADX = sizeof(T) == 4 ? 0 : 1;
+  __shared__ __align__(16) T sX[64][DMAX + PADX];
   __shared__ double sV[64];
   __shared__ double red[256];
   const int tid = threadIdx.x;
@@ -88,12 +91,20 @@ __global__ void __launch_bounds__(256) krows_kernel(const T* __restrict__ X, int
       const int jd = (dl >= 0 && dl < jn) ? (int)dl : -1;
       for (int jj = sub; jj < jn; jj += 4) {
         T d2 = T(0);
-        T xj[DMAX];
-        load_row<T, DMAX>(sX[jj], xj);
+        if constexpr (sizeof(T) == 4) {
+          T xj[DMAX];
+          load_row<T, DMAX>(sX[jj], xj);
 #pragma unroll
-        for (int k = 0; k < DMAX; ++k) {
-          const T df = xr[k] - xj[k];
-          d2 = fma(df, df, d2);
+          for (int k = 0; k < DMAX; ++k) {
+            const T df = xr[k] - xj[k];
+            d2 = fma(df, df, d2);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < DMAX; ++k) {
+            const T df = xr[k] - sX[jj][k];
+            d2 = fma(df, df, d2);
+          }
         }
         T kv;
         if (jj == jd) {
@@ -140,7 +151,10 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
   // rows r0 .. r0 + nrows of the operator (this rank's), R holds those rows
   const int c = blockIdx.y;
   if (!active[c]) return;
-  __shared__ __align__(16) T sX[64][DMAX];  // rows read whole: 16-byte vector loads (broadcast)
+  // fp32 rows read whole with 16-byte vector loads (broadcast): krows 323 -> 304 us at C2;
+  // fp64 rows keep per-element loads (the vector form measured 596 -> 726 us there)
+  constexpr int PADX = sizeof(T) == 4 ? 0 : 1;
+  __shared__ __align__(16) T sX[64][DMAX + PADX];
   __shared__ double sD[64];
   const int64_t il = (int64_t)blockIdx.x * 128 + threadIdx.x;
   const bool valid = il < nrows;
@@ -168,12 +182,20 @@ __global__ void __launch_bounds__(128) kcols_kernel(const T* __restrict__ X, int
       const int jd = (dl >= 0 && dl < m) ? (int)dl : -1;
       for (int jj = 0; jj < m; ++jj) {
         T d2 = T(0);
-        T xj[DMAX];
-        load_row<T, DMAX>(sX[jj], xj);
+        if constexpr (sizeof(T) == 4) {
+          T xj[DMAX];
+          load_row<T, DMAX>(sX[jj], xj);
 #pragma unroll
-        for (int k = 0; k < DMAX; ++k) {
-          const T df = xr[k] - xj[k];
-          d2 = fma(df, df, d2);
+          for (int k = 0; k < DMAX; ++k) {
+            const T df = xr[k] - xj[k];
+            d2 = fma(df, df, d2);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < DMAX; ++k) {
+            const T df = xr[k] - sX[jj][k];
+            d2 = fma(df, df, d2);
+          }
         }
         T kv;
         if (jj == jd) {
