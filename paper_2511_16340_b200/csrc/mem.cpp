@@ -112,14 +112,20 @@ void dev_free(void* p, size_t bytes) {
   if (!p) return;
   // (called from destructors: never throws; after a device error the block is dropped --
   // blocks live inside chunks and are not the driver's to free individually)
-  {
-    SlowTimer tm{"free-sync", bytes};
-    if (cudaDeviceSynchronize() != cudaSuccess) return;
-  }
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
     cudaGetLastError();
     return;
+  }
+  {
+    // synchronise the block's own device (a process may drive several)
+    SlowTimer tm{"free-sync", bytes};
+    int cur = a.device;
+    cudaGetDevice(&cur);
+    if (cur != a.device) cudaSetDevice(a.device);
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (cur != a.device) cudaSetDevice(cur);
+    if (e != cudaSuccess) return;
   }
   std::lock_guard<std::mutex> lk(g_mu);
   cache()[{a.device, bucket(bytes)}].push_back(p);  // the block's own device
